@@ -1,0 +1,186 @@
+"""Pins for oracle O4 (eigenvalues / d rule) and the thresholding operators of PAPER.md §2.2.
+
+Thresholds are pinned by SPEC's printed values, by a brute-force numeric prox (each operator must
+be the exact minimiser of 0.5 d b^2 - u b + P(b), P from Table 1), and by the textbook d = 1
+forms (Zhang's firm threshold, Fan & Li's SCAD rule)."""
+import math
+
+import numpy as np
+import pytest
+from scipy.optimize import minimize, minimize_scalar
+
+import oracle as orc
+
+
+# ------------------------------------------------------------------ d
+def test_eigen_examples(golden):
+    for ex in golden["largest_eigenvalue"]:
+        A = np.array(ex["A"])
+        assert abs(orc.eig_jacobi(A)[-1] - ex["lambda1"]) < 1e-15
+        d, rq, gs = orc.power_rule(A)
+        assert ex["lambda1"] <= d <= ex["lambda1"] * 1.01
+
+
+def test_jacobi_matches_library_and_closed_forms():
+    rng = np.random.default_rng(7)
+    for p in (3, 10, 31):
+        B = rng.standard_normal((3 * p, p))
+        A = B.T @ B / (3 * p)
+        ev = orc.eig_jacobi(A)
+        assert np.max(np.abs(ev - np.linalg.eigvalsh(A))) < 1e-13 * ev[-1]
+    # block equicorrelation population matrix: eigenvalues 1 + (m-1) r (x groups), 1 - r
+    m, r, ng = 10, 0.4, 5
+    A = np.kron(np.eye(ng), np.full((m, m), r)) + (1 - r) * np.eye(m * ng)
+    ev = orc.eig_jacobi(A)
+    assert abs(ev[-1] - (1 + (m - 1) * r)) < 1e-13 and abs(ev[0] - (1 - r)) < 1e-13
+    # AR(1) Toeplitz: extremes approach (1+rho)/(1-rho), (1-rho)/(1+rho) as p grows
+    rho, p = 0.5, 200
+    T = rho ** np.abs(np.subtract.outer(np.arange(p), np.arange(p)))
+    ev = orc.eig_jacobi(T)
+    assert abs(ev[-1] - 3.0) < 3e-3 and abs(ev[0] - 1 / 3) < 3e-3
+    assert np.max(np.abs(ev - np.linalg.eigvalsh(T))) < 1e-12
+
+
+@pytest.mark.parametrize("kind", ["ar1_0.5", "ar1_0.3", "block_0.4", "iid"])
+def test_power_rule_brackets_lambda1(kind):
+    """R#5: d = min(Gershgorin, 1.005 RQ_200) satisfies lambda_1 <= d <= 1.01 lambda_1 on the
+    configs' population Grams and on sample Grams of those designs."""
+    rng = np.random.default_rng(8)
+    p = 100
+    if kind.startswith("ar1"):
+        rho = float(kind.split("_")[1])
+        S = rho ** np.abs(np.subtract.outer(np.arange(p), np.arange(p)))
+    elif kind.startswith("block"):
+        S = np.kron(np.eye(10), np.full((10, 10), 0.4)) + 0.6 * np.eye(p)
+    else:
+        S = np.eye(p)
+    L = np.linalg.cholesky(S)
+    for A in (S, (lambda Z: Z.T @ Z / Z.shape[0])(rng.standard_normal((4000, p)) @ L.T)):
+        lam1 = np.linalg.eigvalsh(A)[-1]
+        d, rq, gs = orc.power_rule(A)
+        assert rq <= lam1 * (1 + 1e-12)          # Rayleigh quotient never exceeds lambda_1
+        assert gs >= lam1 * (1 - 1e-12)          # Gershgorin bound
+        assert lam1 * (1 - 1e-12) <= d <= 1.01 * lam1
+
+
+# ------------------------------------------------------------------ thresholds: printed values
+def test_spec_printed_values(golden):
+    for ex in golden["soft"]:
+        assert orc.soft(ex["u"], ex["lam"], ex["d"]) == ex["out"]
+    for ex in golden["enet"]:
+        assert abs(orc.enet(ex["u"], ex["lam"], ex["alpha"], ex["d"]) - ex["out"]) < 1e-15
+    for ex in golden["mcp"]:
+        assert orc.mcp(ex["u"], ex["lam"], ex["gamma"], ex["d"]) == ex["out"]
+    for ex in golden["scad"]:
+        out = ex.get("out", ex.get("out_num", 0) / ex.get("out_den", 1))
+        assert abs(orc.scad(ex["u"], ex["lam"], ex["gamma"], ex["d"]) - out) < 1e-15
+    for ex in golden["grp_lasso"]:
+        assert np.allclose(orc.grp_lasso(ex["u"], ex["lam"], ex["d"]), ex["out"], atol=1e-15)
+    for ex in golden["grp_mcp"]:
+        assert np.allclose(orc.grp_mcp(ex["u"], ex["lam"], ex["gamma"], ex["d"]), ex["out"], atol=1e-15)
+
+
+# ------------------------------------------------------------------ penalty forms (Table 1)
+def p_mcp(b, lam, g):
+    a = abs(b)
+    return lam * a - a * a / (2 * g) if a <= g * lam else g * lam * lam / 2
+
+
+def p_scad(b, lam, g):
+    a = abs(b)
+    if a <= lam:
+        return lam * a
+    if a <= g * lam:
+        return -(a * a - 2 * g * lam * a + lam * lam) / (2 * (g - 1))
+    return (g + 1) * lam * lam / 2
+
+
+def numeric_prox(u, d, pen):
+    """argmin_b 0.5 d b^2 - u b + pen(b): dense grid then bounded Brent refinement."""
+    hi = abs(u) / d + 1.0
+    grid = np.linspace(-hi, hi, 20001)
+    vals = 0.5 * d * grid ** 2 - u * grid + np.array([pen(b) for b in grid])
+    b0 = grid[np.argmin(vals)]
+    step = grid[1] - grid[0]
+    res = minimize_scalar(lambda b: 0.5 * d * b * b - u * b + pen(b), bounds=(b0 - 2 * step, b0 + 2 * step),
+                          method="bounded", options={"xatol": 1e-12})
+    return res.x
+
+
+def test_prox_fidelity_scalar():
+    """every scalar operator is the exact prox of its Table 1 penalty with divisor d."""
+    rng = np.random.default_rng(9)
+    for _ in range(250):
+        d = rng.uniform(1.0, 4.0)
+        u = rng.uniform(-6, 6)
+        lam = rng.uniform(0.05, 2.0)
+        alpha = rng.uniform(0.05, 1.0)
+        g_m = rng.uniform(1.0 / d + 0.6, 6.0)        # gamma*d > 1 (R#8)
+        g_s = rng.uniform(max(2.0, 1.0 / d + 1.0) + 0.3, 7.0)  # gamma > 2, (gamma-1)d > 1
+        assert abs(orc.soft(u, lam, d) - numeric_prox(u, d, lambda b: lam * abs(b))) < 1e-6
+        assert abs(orc.enet(u, lam, alpha, d) - numeric_prox(
+            u, d, lambda b: alpha * lam * abs(b) + 0.5 * (1 - alpha) * lam * b * b)) < 1e-6
+        assert abs(orc.mcp(u, lam, g_m, d) - numeric_prox(u, d, lambda b: p_mcp(b, lam, g_m))) < 1e-6
+        assert abs(orc.scad(u, lam, g_s, d) - numeric_prox(u, d, lambda b: p_scad(b, lam, g_s))) < 1e-6
+
+
+def test_textbook_forms_at_d1():
+    """At d = 1: MCP = Zhang's firm threshold, SCAD = Fan & Li (2001) three-piece rule."""
+    rng = np.random.default_rng(10)
+    for _ in range(500):
+        u, lam = rng.uniform(-8, 8), rng.uniform(0.1, 2)
+        g = rng.uniform(1.5, 5)
+        firm = (np.sign(u) * g * max(abs(u) - lam, 0) / (g - 1)) if abs(u) <= g * lam else u
+        assert abs(orc.mcp(u, lam, g, 1.0) - firm) < 1e-14
+        a = rng.uniform(2.2, 5)
+        if abs(u) <= 2 * lam:
+            fl = np.sign(u) * max(abs(u) - lam, 0)
+        elif abs(u) <= a * lam:
+            fl = ((a - 1) * u - np.sign(u) * a * lam) / (a - 2)
+        else:
+            fl = u
+        assert abs(orc.scad(u, lam, a, 1.0) - fl) < 1e-13
+
+
+def test_continuity_and_limits():
+    for d in (1.0, 2.5):
+        lam, g = 0.7, 3.7
+        for edge in (lam, (d + 1) * lam, g * lam * d):
+            for f in (lambda u: orc.scad(u, lam, g, d), lambda u: orc.mcp(u, lam, g, d),
+                      lambda u: orc.soft(u, lam, d)):
+                assert abs(f(edge + 1e-9) - f(edge - 1e-9)) < 1e-6
+        # gamma -> infinity: MCP and SCAD -> soft threshold
+        for u in np.linspace(-5, 5, 41):
+            assert abs(orc.mcp(u, lam, 1e7, d) - orc.soft(u, lam, d)) < 1e-6
+            assert abs(orc.scad(u, lam, 1e7, d) - orc.soft(u, lam, d)) < 1e-6
+
+
+def test_group_prox_fidelity():
+    """Group operators are the exact prox of c*lam*P(||b||) with divisor d."""
+    rng = np.random.default_rng(11)
+    for _ in range(30):
+        d = rng.uniform(1.0, 3.0)
+        u = rng.uniform(-3, 3, 3)
+        lam = rng.uniform(0.1, 2.0)
+        g = rng.uniform(1.0 / d + 1.0, 5.0)
+        gs = rng.uniform(max(2.0, 1.0 / d + 1.0) + 0.5, 6.0)
+        for op, pen in ((lambda: orc.grp_lasso(u, lam, d), lambda nb: lam * nb),
+                        (lambda: orc.grp_mcp(u, lam, g, d), lambda nb: p_mcp(nb, lam, g)),
+                        (lambda: orc.grp_scad(u, lam, gs, d), lambda nb: p_scad(nb, lam, gs))):
+            f = lambda b: 0.5 * d * b @ b - u @ b + pen(np.linalg.norm(b))
+            best = None
+            for start in (np.zeros(3), u / d, 0.5 * u / d):
+                r = minimize(f, start, method="Nelder-Mead",
+                             options={"xatol": 1e-11, "fatol": 1e-15, "maxiter": 20000})
+                if best is None or r.fun < best.fun:
+                    best = r
+            out = op()
+            assert f(out) <= best.fun + 1e-10
+            assert np.max(np.abs(out - best.x)) < 1e-4
+
+
+def test_group_zero_norm():
+    z = np.zeros(4)
+    assert not orc.grp_lasso(z, 1.0, 2.0).any()
+    assert not orc.grp_mcp(z, 1.0, 3.0, 2.0).any()
+    assert not orc.grp_scad(z, 1.0, 3.7, 2.0).any()
