@@ -1,0 +1,143 @@
+/* oem.h — C ABI of liboem.so: the data-parallel hot path of the orthogonalizing EM (OEM)
+ * algorithm for penalized least squares on tall data (Huling & Chien, arXiv 1801.09661),
+ * B200-native (sm_100a).
+ *
+ * Citations: "P:Lnnn" = PAPER.md line nnn; "R#k" = reading k in DESIGN.md §3 (the paper's
+ * silent/garbled points and the reading taken).
+ *
+ * Conventions (all entry points)
+ *  - Pointers are DEVICE pointers unless marked (host). The caller owns every buffer it passes;
+ *    the library never frees them. The oem_ctx owns its workspace (split-n partials, packed
+ *    reduction buffers, the NCCL communicator) and releases it in oem_ctx_destroy.
+ *  - Every call is enqueued on `stream` (a cudaStream_t passed as void*; NULL = legacy default
+ *    stream). Calls that must read device results on the host (counts, maxit flags) synchronise
+ *    that stream before returning, and say so.
+ *  - X is row-major: element (i, j) at X[i*ldx + j], 0 <= i < n_local, 0 <= j < p, ldx >= p.
+ *    TMA needs X and y 16-byte aligned and ldx even (row pitch a multiple of 16 B); otherwise
+ *    OEM_ERR_ALIGN.
+ *  - All arithmetic is IEEE fp64. Reductions use no atomics and a fixed order: for a fixed
+ *    world size and inputs, outputs are bitwise reproducible.
+ *  - Errors: the boundary never throws or aborts. Each call returns an oem_status;
+ *    oem_last_error() returns a thread-local detail string for the last failing call.
+ *  - Multi-GPU: one process per GPU. X is row-sharded; each rank passes its own rows. When the
+ *    context was created with nranks > 1, the Gram entry points sum their raw outputs over all
+ *    ranks with one ncclAllReduce (sum, fp64) on `stream` before returning, so every rank holds
+ *    identical reduced statistics ("computed independently ... in parallel";
+ *    P:L72-76 Gram quantities computed on a cluster).
+ */
+#ifndef OEM_H
+#define OEM_H
+#include <stdint.h>
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct oem_ctx oem_ctx;
+
+typedef enum {
+  OEM_OK = 0,
+  OEM_ERR_INVALID_ARG = 1,  /* bad gamma/alpha/weights/groups/sizes, y not in {0,1} for logistic */
+  OEM_ERR_DIM = 2,          /* dimension mismatch (SPEC DimensionMismatch) */
+  OEM_ERR_ALIGN = 3,        /* X / y not 16-byte aligned or ldx odd (TMA constraints) */
+  OEM_ERR_EMPTY_FOLD = 4,   /* a fold has no rows (SPEC EmptyFold) */
+  OEM_ERR_NONFINITE = 5,    /* NaN/Inf in a Gram or in the path iterates (SPEC NonFinite) */
+  OEM_ERR_CUDA = 6,
+  OEM_ERR_NCCL = 7,
+  OEM_ERR_NOMEM = 8,
+  OEM_ERR_UNSUPPORTED = 9   /* a size this build does not handle (stated in the detail text) */
+} oem_status;
+
+const char* oem_status_string(oem_status s);
+const char* oem_last_error(void);
+const char* oem_version(void);
+
+/* NCCL bootstrap: rank 0 calls oem_nccl_unique_id and broadcasts the 128 bytes to the other
+ * ranks (e.g. through torch.distributed); every rank then calls oem_ctx_create with it. */
+oem_status oem_nccl_unique_id(void* uid128 /*host, 128 bytes*/);
+/* One context per (process, device). nranks == 1: uid may be NULL and no NCCL is used. */
+oem_status oem_ctx_create(int device, int nranks, int rank, const void* uid128 /*host*/, oem_ctx** out);
+oem_status oem_ctx_destroy(oem_ctx* ctx);
+
+/* ---- a2 Gram pass (P:L171-172 A = dI - X^T X, u = X^T y + A beta; "the key
+ * computational step in OEM is in forming the matrix A"; P:L328-333 O(np^2 + np)).
+ * One pass over [X | y]: G = X^T X (full symmetric p*p written, row-major), xty = X^T y (p),
+ * yty = y^T y (1). Raw sums over this rank's rows, allreduced when nranks > 1; normalisation
+ * (/n, R#1) happens in oem_fit_path. n_total (host, may be NULL) receives the global row count.
+ * n_local = 0 is allowed (zero outputs). Errors: OEM_ERR_DIM (p < 1, ldx < p, n_local < 0),
+ * OEM_ERR_ALIGN, OEM_ERR_UNSUPPORTED (p > 16383), OEM_ERR_CUDA, OEM_ERR_NCCL. */
+oem_status oem_gram(oem_ctx* ctx, const double* X, const double* y, int64_t n_local, int32_t p,
+                    int64_t ldx, double* G, double* xty, double* yty, int64_t* n_total, void* stream);
+
+/* ---- a3 fold-segmented Gram (§3: A_(k) = d_(k) I - sum_{c != k} X_c^T X_c and
+ * X_{-k}^T y_{-k} = sum_{c != k} X_c^T y_c; P:L336-339 folds computed independently).
+ * One pass over X producing K raw per-fold sums: G_folds[k*p*p + j*p + l] (full symmetric),
+ * xty_folds[k*p + j], yty_folds[k]; counts[k] (host) = global rows in fold k.
+ * fold(i) = (row_offset + i) mod K for local row i (R#19); row_offset = this rank's first
+ * global row. Errors: as oem_gram, plus OEM_ERR_INVALID_ARG (K < 1),
+ * OEM_ERR_EMPTY_FOLD (a fold with no rows globally). Synchronises `stream` only if nranks > 1
+ * (the counts allreduce is host-side arithmetic, no device sync needed). */
+oem_status oem_gram_folds(oem_ctx* ctx, const double* X, const double* y, int64_t n_local, int32_t p,
+                          int64_t ldx, int64_t row_offset, int32_t K, double* G_folds,
+                          double* xty_folds, double* yty_folds, int64_t* counts /*host K*/, void* stream);
+
+/* ---- a4 weighted Gram for the proximal-Newton logistic step (§4; working
+ * responses z_i and weights w_i at P:L376-380; R#23-25). Per row: eta = x_i^T beta,
+ * mu = 1/(1+exp(-eta)) clamped to [eps, 1-eps], w = mu(1-mu), z = eta + (y - mu)/w.
+ * Outputs raw sums: Gw = sum w x x^T (full symmetric p*p), xtwz = sum w z x (p),
+ * scalars[0] = sum w, scalars[1] = sum [y eta - log(1 + e^eta)] (log-likelihood).
+ * beta (p, device) must be identical on every rank. y01 must hold 0.0/1.0 (not checked on the
+ * device; the binding checks once per fit). Errors: as oem_gram, plus OEM_ERR_UNSUPPORTED when
+ * p > 247 (this build fuses eta into the single-panel kernel only). */
+oem_status oem_gram_weighted(oem_ctx* ctx, const double* X, const double* y01, const double* beta,
+                             int64_t n_local, int32_t p, int64_t ldx, double eps, double* Gw,
+                             double* xtwz, double* scalars, void* stream);
+
+/* ---- a6-a10 normalise, d, lambda grid, OEM path (P:L147-158 Steps 1-2; P:L171-195;
+ * P:L239-289 thresholding M-steps; §5.2 several penalties share A and X^T y).
+ * Penalty families of Table 1, update equations at P:L243-289. */
+typedef enum { OEM_LASSO = 0, OEM_ENET = 1, OEM_MCP = 2, OEM_SCAD = 3,
+               OEM_GRP_LASSO = 4, OEM_GRP_MCP = 5, OEM_GRP_SCAD = 6 } oem_family;
+typedef struct { int32_t family; double gamma; double alpha; } oem_penalty;
+typedef struct {
+  int32_t nlambda;          /* L >= 1 */
+  double lambda_min_ratio;  /* 0 < r < 1 (R#15); default 1e-3 */
+  const double* lambda;     /* host, optional explicit grid of L values shared by all units */
+  double tol;               /* stop when max_j |beta'_j - beta_j| <= tol (R#17); default 1e-11 */
+  int64_t maxit;            /* per-lambda update cap (not an error, R#17); default 1e5 */
+  const double* var_w;      /* device, p or NULL (= 1, R#13) */
+  const int32_t* group;     /* host, p group ids in [0, ngroups), or NULL */
+  int32_t ngroups;
+  const double* grp_w;      /* host, ngroups or NULL (= sqrt(group size), R#12) */
+  int32_t power_iters;      /* d rule (R#5): default 200 */
+  double d_inflate;         /* d rule (R#5): default 5e-3 */
+  int32_t fold_mode;        /* 1: inputs are K fold sums -> fit full data + K complements (R#20-22) */
+  const double* lambda_max_override; /* host, optional: use this lambda_max for every unit */
+} oem_path_cfg;
+
+/* Fit paths from raw sufficient statistics. Inputs G (nG*p*p, full symmetric), xty (nG*p),
+ * counts (host, nG): raw sums and their row counts. Gram g is normalised by counts[g] (R#1).
+ * fold_mode = 0: nG' = nG units of Gram; fold_mode = 1: the nG = K inputs are fold sums; unit 0
+ * is the full data (sum over folds, normalised by sum counts) and unit k (1..K) the complement
+ * of fold k-1 (total minus fold, normalised by n - n_k, R#20), nG' = K + 1. d per unit by the
+ * power rule (R#5, R#21) unless d_in (host, nG') is given. lambda grid per (unit, penalty) from
+ * that unit's lambda_max (R#14, R#16) — in fold mode every unit shares unit 0's grid (R#22).
+ * beta_init (device, nG'*nP*p) or NULL (= 0). Outputs (device): beta_out[nG'][nP][L][p],
+ * lambda_out[nG'][nP][L], iters_out[nG'][nP][L] (int64), converged_out[nG'][nP][L] (uint8),
+ * d_out[nG'] (double). Units run independently; a unit's lambda advances only when that unit
+ * converges or hits maxit. Synchronises `stream` (reads the non-finite flag).
+ * Errors: OEM_ERR_INVALID_ARG (MCP gamma*d <= 1, SCAD (gamma-1)*d <= 1, alpha outside [0,1],
+ * groups missing for group families, L < 1, bad ratio), OEM_ERR_EMPTY_FOLD (count 0),
+ * OEM_ERR_NONFINITE, OEM_ERR_UNSUPPORTED (p > 16383), OEM_ERR_CUDA. */
+oem_status oem_fit_path(oem_ctx* ctx, const double* G, const double* xty, const int64_t* counts /*host*/,
+                        int32_t nG, int32_t p, const oem_penalty* pens /*host nP*/, int32_t nP,
+                        const oem_path_cfg* cfg /*host*/, const double* d_in /*host or NULL*/,
+                        const double* beta_init, double* beta_out, double* lambda_out,
+                        int64_t* iters_out, uint8_t* converged_out, double* d_out, void* stream);
+
+/* Default-initialise a path config (values listed above). */
+void oem_path_cfg_default(oem_path_cfg* cfg);
+
+#ifdef __cplusplus
+}
+#endif
+#endif

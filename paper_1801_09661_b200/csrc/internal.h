@@ -1,0 +1,69 @@
+// internal.h — liboem.so internals shared by the translation units (not part of the ABI).
+#pragma once
+#include <cuda.h>
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <map>
+#include <memory>
+#include <string>
+#include <tuple>
+#include <vector>
+
+#include "../../include/oem.h"
+
+namespace oem {
+
+void set_error(const std::string& msg);
+
+// Grown-on-demand device scratch owned by the context (freed in oem_ctx_destroy).
+struct DevBuf {
+  void* ptr = nullptr;
+  size_t bytes = 0;
+  cudaError_t ensure(size_t need) {
+    if (need <= bytes) return cudaSuccess;
+    if (ptr) cudaFree(ptr);
+    ptr = nullptr;
+    bytes = 0;
+    cudaError_t e = cudaMalloc(&ptr, need);
+    if (e == cudaSuccess) bytes = need;
+    return e;
+  }
+  template <typename T> T* as() const { return static_cast<T*>(ptr); }
+  void release() {
+    if (ptr) cudaFree(ptr);
+    ptr = nullptr;
+    bytes = 0;
+  }
+};
+
+struct GramPlan;  // gram.cu
+
+}  // namespace oem
+
+struct oem_ctx {
+  int device = 0;
+  int nranks = 1, rank = 0;
+  int num_sms = 148;
+  void* nccl_comm = nullptr;  // ncclComm_t
+  oem::DevBuf partial, partial_scal, packed, tail, plan_tables, path_ws, path_small;
+  std::map<std::tuple<int, int, int64_t, int>, std::shared_ptr<oem::GramPlan>> plans;
+};
+
+namespace oem {
+
+enum GramMode { MODE_PLAIN = 0, MODE_FOLD = 1, MODE_WEIGHTED = 2 };
+
+// One pass over [X | y] producing the packed upper triangle of the augmented
+// (p+1)x(p+1) Gram per fold (nfold = K for MODE_FOLD else 1), raw sums, this rank only.
+// packed: nfold * psize (+2 scalars for MODE_WEIGHTED), psize = (p+1)(p+2)/2.
+oem_status gram_pass(oem_ctx* ctx, int mode, const double* X, const double* y, const double* beta, double eps,
+                     int64_t n_local, int p, int64_t ldx, int64_t row_offset, int K, double* packed,
+                     cudaStream_t st);
+// packed (nfold blocks) -> full symmetric G (nfold*p*p), xty (nfold*p), yty (nfold)
+oem_status gram_unpack(const double* packed, int nfold, int p, double* G, double* xty, double* yty, cudaStream_t st);
+inline int64_t packed_size(int p) { return (int64_t)(p + 1) * (p + 2) / 2; }
+
+oem_status allreduce_sum(oem_ctx* ctx, double* buf, size_t count, cudaStream_t st);
+
+}  // namespace oem

@@ -1,0 +1,863 @@
+// path.cu — a6-a10 of the hot path on sm_100a: normalise the unit Grams, d by power iteration,
+// the lambda grid, and the OEM path iterations for every (Gram, penalty) unit.
+//
+// The method: OEM's EM step in closed form, u = X^T y + (dI - X^T X) beta
+// (P:L171-172), followed by the penalty's thresholding M-step (eqs lasso / net /
+// mcp / scad / glasso / gmcp / gscad), iterated to convergence along a warm-started lambda path
+// (R#17-18), for several penalties sharing one Gram (§5.2) and for the K fold
+// complements of fast CV (§3). d >= lambda_1 by the power rule R#5.
+//
+// B200 design: one persistent cooperative launch. Each unit Gram g is owned by a group of C_g
+// CTAs; CTA c keeps its slice of rows of G resident in shared memory for the whole path (the
+// p x p matrix never leaves the SMs), and all penalties on that Gram are advanced together so
+// each G element loaded from smem feeds nP FMAs (the "small GEMM across penalties"). A row is
+// reduced by T_r lanes with xor-shuffles; coordinate-wise thresholds run on the row leader,
+// group thresholds after a CTA-level exchange (groups never straddle CTAs). Per iteration the
+// group exchanges the new beta through L2 (double-buffered) and meets at one barrier; the
+// convergence test max |dbeta| uses a uint64 atomicMax (order independent, so deterministic).
+// No host round-trip per iteration or per lambda.
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+#include <numeric>
+#include <vector>
+
+#include <cooperative_groups.h>
+
+#include "common.cuh"
+#include "internal.h"
+
+namespace oem {
+
+constexpr int PT = 512;          // threads per solver CTA
+constexpr int MAXG = 4096;       // max groups (group penalties)
+
+struct PathParams {
+  int p, nP, L, nU;              // nU = number of unit Grams (nG')
+  int ps;                        // smem row pitch (doubles)
+  int T;                         // lanes per row
+  int64_t maxit;
+  double tol;
+  const double* Gn;              // [nU][p][p] normalised (permuted) unit Grams
+  const double* cn;              // [nU][p]
+  const int* cta_unit;           // [ncta] unit of each CTA
+  const int* cta_rank;           // [ncta] rank of the CTA within its unit group
+  const int* unit_ncta;          // [nU]
+  const int* cta_j0;             // [ncta] first row
+  const int* cta_j1;             // [ncta] end row
+  int smem_rows;                 // rows cached in smem (>= max rows per CTA, else G read from global)
+  // penalties
+  const int* fam;                // [nP]
+  const double* gam;             // [nP]
+  const double* alp;             // [nP]
+  const double* var_w;           // [p] (permuted) or null
+  int ngroups;
+  const int* g_start;            // [ngroups] (permuted, contiguous)
+  const int* g_end;
+  const double* g_w;             // [ngroups]
+  const int* g_of;               // [p] group id (permuted order) or null
+  const int* perm;               // [p] original index of permuted coordinate j
+  // lambda
+  const double* lam_explicit;    // [L] or null
+  double lmin_ratio;
+  int shared_grid;               // fold mode: every unit uses unit 0's lambda_max
+  const double* lmax_override;   // device scalar or null
+  // state / outputs
+  const double* d;               // [nU]
+  const double* beta_init;       // [nU][nP][p] original order or null
+  double* bbuf;                  // [2][nU][nP][p] exchange buffers
+  unsigned long long* dslot;     // [3][nU][nP]
+  unsigned int* bar;             // [nU][2] barrier counter / generation
+  double* beta_out;              // [nU][nP][L][p] original order
+  double* lam_out;               // [nU][nP][L]
+  int64_t* it_out;
+  uint8_t* cv_out;
+  int* flags;                    // [0] non-finite, [1] invalid parameter
+  unsigned long long* bad_iter;  // [nU] first iteration with a non-finite u (all ones = none)
+};
+
+// ---------------------------------------------------------------- group barrier (global memory)
+__device__ __forceinline__ unsigned ld_acquire(const unsigned* p) {
+  unsigned v;
+  asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void group_barrier(unsigned* bar, int C) {
+  __syncthreads();
+  if (C > 1 && threadIdx.x == 0) {
+    unsigned* cnt = bar;
+    unsigned* gen = bar + 1;
+    const unsigned g = ld_acquire(gen);
+    __threadfence();
+    if (atomicAdd(cnt, 1u) == (unsigned)C - 1u) {
+      atomicExch(cnt, 0u);
+      __threadfence();
+      atomicAdd(gen, 1u);
+    } else {
+      while (ld_acquire(gen) == g) { __nanosleep(20); }
+    }
+    __threadfence();
+  }
+  __syncthreads();
+}
+
+// ---------------------------------------------------------------- thresholding operators (K6)
+// exact transcriptions of PAPER.md §2.2; lam is the weighted level (w_j lambda or c_k lambda)
+__device__ __forceinline__ double sgn(double u) { return u > 0.0 ? 1.0 : (u < 0.0 ? -1.0 : 0.0); }
+__device__ __forceinline__ double pos(double a) { return a > 0.0 ? a : 0.0; }
+__device__ __forceinline__ double th_soft(double u, double lam, double d) {     // eq (lasso)
+  return sgn(u) * pos((fabs(u) - lam) / d);
+}
+__device__ __forceinline__ double th_enet(double u, double lam, double a, double d) {  // eq (net)
+  return sgn(u) * pos((fabs(u) - lam * a) / (d + lam * (1.0 - a)));
+}
+__device__ __forceinline__ double th_mcp(double u, double lam, double g, double d) {   // eq (mcp)
+  if (fabs(u) <= lam * g * d) return sgn(u) * g * pos(fabs(u) - lam) / (g * d - 1.0);
+  return u / d;
+}
+__device__ __forceinline__ double th_scad(double u, double lam, double g, double d) {  // eq (scad)
+  const double a = fabs(u);
+  if (a <= (d + 1.0) * lam) return sgn(u) * pos(a - lam) / d;
+  if (a <= lam * g * d) return sgn(u) * ((g - 1.0) * a - lam * g) / ((g - 1.0) * d - 1.0);
+  return u / d;
+}
+__device__ __forceinline__ double th_coord(int fam, double u, double lam, double g, double a, double d) {
+  switch (fam) {
+    case OEM_LASSO: return th_soft(u, lam, d);
+    case OEM_ENET: return th_enet(u, lam, a, d);
+    case OEM_MCP: return th_mcp(u, lam, g, d);
+    default: return th_scad(u, lam, g, d);
+  }
+}
+
+__device__ __forceinline__ void atomic_max_pos(unsigned long long* slot, double v) {
+  // v >= 0: IEEE order equals unsigned-integer order of the bit patterns
+  atomicMax(slot, (unsigned long long)__double_as_longlong(v));
+}
+
+// ---------------------------------------------------------------- prep: normalise unit Grams
+// fold_mode = 0: unit g = G[g]/n_g. fold_mode = 1: unit 0 = (sum_k G_k)/n, unit k = (sum - G_{k-1})/(n - n_{k-1}).
+// Coordinates are permuted so every group is contiguous: Gn[u][j][l] = Graw[perm[j]][perm[l]].
+__global__ void prep_units_kernel(const double* __restrict__ G, const double* __restrict__ xty, int nG, int p,
+                                  int fold_mode, const double* __restrict__ inv_n, const int* __restrict__ perm,
+                                  double* __restrict__ Gn, double* __restrict__ cn, int* flags) {
+  const int nU = fold_mode ? nG + 1 : nG;
+  const int64_t per = (int64_t)p * p + p;
+  const int64_t total = (int64_t)nU * per;
+  const size_t pp = (size_t)p * p;
+  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < total; t += (int64_t)gridDim.x * blockDim.x) {
+    const int u = (int)(t / per);
+    const int64_t q = t % per;
+    size_t off;
+    int64_t stride;
+    double* dst;
+    if (q < (int64_t)p * p) {
+      const int j = (int)(q / p), l = (int)(q % p);
+      off = (size_t)perm[j] * p + perm[l];
+      stride = (int64_t)pp;
+      dst = Gn + (size_t)u * pp + q;
+    } else {
+      const int j = (int)(q - (int64_t)p * p);
+      off = perm[j];
+      stride = p;
+      dst = cn + (size_t)u * p + j;
+    }
+    const double* src = q < (int64_t)p * p ? G : xty;
+    double v;
+    if (!fold_mode) {
+      v = src[(size_t)u * stride + off];
+    } else {
+      double s = 0.0;
+      for (int k = 0; k < nG; ++k) s += src[(size_t)k * stride + off];  // fixed order
+      v = (u == 0) ? s : s - src[(size_t)(u - 1) * stride + off];    // total minus fold (R#20)
+    }
+    v = v * inv_n[u];
+    if (!isfinite(v)) flags[0] = 1;
+    *dst = v;
+  }
+}
+
+// ---------------------------------------------------------------- shared pieces of the persistent kernels
+struct CtaView {
+  int unit, rank, C, j0, j1, nr;
+  const double* Gu;   // global rows of this unit
+};
+
+__device__ __forceinline__ CtaView cta_view(const PathParams& P) {
+  CtaView v;
+  v.unit = P.cta_unit[blockIdx.x];
+  v.rank = P.cta_rank[blockIdx.x];
+  v.C = P.unit_ncta[v.unit];
+  v.j0 = P.cta_j0[blockIdx.x];
+  v.j1 = P.cta_j1[blockIdx.x];
+  v.nr = v.j1 - v.j0;
+  v.Gu = P.Gn + (size_t)v.unit * P.p * P.p;
+  return v;
+}
+
+// This CTA's rows of the unit Gram -> shared memory (resident for the whole launch).
+__device__ __forceinline__ void load_rows(const PathParams& P, const CtaView& v, double* Gs) {
+  for (int e = threadIdx.x; e < v.nr * P.p; e += blockDim.x) {
+    const int r = e / P.p, k = e % P.p;
+    Gs[r * P.ps + k] = v.Gu[(size_t)(v.j0 + r) * P.p + k];
+  }
+}
+
+// deterministic block sum (fixed tree order); red needs 33 doubles
+__device__ double block_sum(double x, double* red) {
+  for (int o = 16; o > 0; o >>= 1) x += __shfl_xor_sync(0xffffffffu, x, o);
+  const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
+  __syncthreads();
+  if (l == 0) red[w] = x;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double s = 0.0;
+    for (int i = 0; i < (int)(blockDim.x >> 5); ++i) s += red[i];
+    red[32] = s;
+  }
+  __syncthreads();
+  const double r = red[32];
+  __syncthreads();
+  return r;
+}
+__device__ double block_max(double x, double* red) {
+  for (int o = 16; o > 0; o >>= 1) x = fmax(x, __shfl_xor_sync(0xffffffffu, x, o));
+  const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
+  __syncthreads();
+  if (l == 0) red[w] = x;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double s = 0.0;
+    for (int i = 0; i < (int)(blockDim.x >> 5); ++i) s = fmax(s, red[i]);
+    red[32] = s;
+  }
+  __syncthreads();
+  const double r = red[32];
+  __syncthreads();
+  return r;
+}
+
+// w[r] = sum_k G[j0+r][k] * vec[k] for the local rows (T lanes per row, all lanes of every warp
+// take part in each round so the width-T shuffles are convergent). Result in uv[r].
+__device__ __forceinline__ void row_matvec(const PathParams& P, const CtaView& v, const double* Gs, const double* vec,
+                                           double* uv, bool absval) {
+  const int T = P.T, groups = blockDim.x / T;
+  const int rg = threadIdx.x / T, tl = threadIdx.x % T;
+  for (int rb = 0; rb < v.nr; rb += groups) {
+    const int r = rb + rg;
+    double a = 0.0;
+    if (r < v.nr) {
+      const double* grow = Gs + (size_t)r * P.ps;
+      if (absval) for (int k = tl; k < P.p; k += T) a += fabs(grow[k]);
+      else for (int k = tl; k < P.p; k += T) a = fma(grow[k], vec[k], a);
+    }
+    for (int o = T >> 1; o > 0; o >>= 1) a += __shfl_xor_sync(0xffffffffu, a, o, T);
+    if (r < v.nr && tl == 0) uv[r] = a;
+  }
+}
+
+// ---------------------------------------------------------------- K4: power iteration for d (R#5)
+// v0 = 1/sqrt(p); v <- Gv/||Gv|| for `iters` steps; RQ = v^T G v; d = min(Gershgorin, (1+inflate) RQ).
+// Cross-CTA sums go through per-CTA slots summed in rank order (deterministic); the new vector
+// is exchanged through L2 (double-buffered by step parity).
+__global__ void __launch_bounds__(PT, 1)
+power_kernel(const PathParams P, int iters, double inflate, double* wbuf /*[2][nU][p]*/,
+             double* pslot /*[3][nU][Cmax]*/, int Cmax, double* d_out) {
+  extern __shared__ __align__(16) double sm[];
+  const CtaView v = cta_view(P);
+  double* Gs = sm;
+  double* vec = Gs + (size_t)P.smem_rows * P.ps;
+  double* uv = vec + P.ps;
+  double* red = uv + P.smem_rows;
+  unsigned* bar = P.bar + 2 * v.unit;
+  load_rows(P, v, Gs);
+  const double v0 = 1.0 / sqrt((double)P.p);
+  for (int k = threadIdx.x; k < P.p; k += blockDim.x) vec[k] = v0;
+  __syncthreads();
+  // Gershgorin bound: local max row sum -> slot 2
+  row_matvec(P, v, Gs, vec, uv, true);
+  __syncthreads();
+  double gm = 0.0;
+  for (int r = threadIdx.x; r < v.nr; r += blockDim.x) gm = fmax(gm, uv[r]);
+  gm = block_max(gm, red);
+  double* gslot = pslot + ((size_t)2 * P.nU + v.unit) * Cmax;
+  if (threadIdx.x == 0) gslot[v.rank] = gm;
+  for (int it = 0; it <= iters; ++it) {
+    row_matvec(P, v, Gs, vec, uv, false);
+    __syncthreads();
+    const int par = it & 1;
+    double* wb = wbuf + ((size_t)par * P.nU + v.unit) * P.p;
+    double* ps = pslot + ((size_t)par * P.nU + v.unit) * Cmax;
+    double x = 0.0;
+    if (it < iters) {
+      for (int r = threadIdx.x; r < v.nr; r += blockDim.x) {
+        const double w = uv[r];
+        x += w * w;
+        if (v.C > 1) wb[v.j0 + r] = w;
+        else wb[r] = w;
+      }
+    } else {
+      for (int r = threadIdx.x; r < v.nr; r += blockDim.x) x += vec[v.j0 + r] * uv[r];  // RQ partial
+    }
+    const double s = block_sum(x, red);
+    if (threadIdx.x == 0) ps[v.rank] = s;
+    __threadfence();
+    group_barrier(bar, v.C);
+    double tot = 0.0;
+    for (int c = 0; c < v.C; ++c) tot += __ldcg(ps + c);
+    if (it < iters) {
+      const double nrm = sqrt(tot);
+      if (nrm > 0.0)
+        for (int k = threadIdx.x; k < P.p; k += blockDim.x) vec[k] = __ldcg(wb + k) / nrm;
+      __syncthreads();
+    } else if (v.rank == 0 && threadIdx.x == 0) {
+      double g = 0.0;
+      for (int c = 0; c < v.C; ++c) g = fmax(g, __ldcg(gslot + c));
+      const double dd = (1.0 + inflate) * tot;
+      d_out[v.unit] = g < dd ? g : dd;
+    }
+  }
+}
+
+// ---------------------------------------------------------------- K5: the persistent OEM path solver
+template <int NPT>
+__global__ void __launch_bounds__(PT, 1) path_kernel(const PathParams P) {
+  extern __shared__ __align__(16) double sm[];
+  const CtaView v = cta_view(P);
+  const int p = P.p, nP = P.nP, L = P.L;
+  double* Gs = sm;
+  double* vec = Gs + (size_t)P.smem_rows * P.ps;         // current beta [NPT][ps] (all p coordinates)
+  double* uv = vec + (size_t)NPT * P.ps;                  // u, then beta', local rows [NPT][smem_rows]
+  __shared__ int s_lidx[NPT];
+  __shared__ int64_t s_it[NPT];
+  __shared__ double s_lam[NPT];
+  __shared__ double s_lmax[NPT];
+  __shared__ double s_delta[NPT];
+  __shared__ int s_bad, s_stop;
+  unsigned* bar = P.bar + 2 * v.unit;
+  const double d = P.d[v.unit];
+  const double* c = P.cn + (size_t)v.unit * p;
+
+  load_rows(P, v, Gs);
+  // warm start / cold start beta (full vector on every CTA), permuted order
+  for (int q = 0; q < nP; ++q)
+    for (int k = threadIdx.x; k < p; k += blockDim.x)
+      vec[q * P.ps + k] = P.beta_init ? P.beta_init[((size_t)v.unit * nP + q) * p + P.perm[k]] : 0.0;
+  // lambda_max per penalty (R#14), from this unit's c, or unit 0's in fold mode (R#22)
+  if (threadIdx.x < nP) {
+    const int q = threadIdx.x;
+    const int fam = P.fam[q];
+    const double* cc = P.shared_grid ? P.cn : c;
+    double lm = 0.0;
+    if (P.lmax_override) {
+      lm = *P.lmax_override;
+    } else if (fam >= OEM_GRP_LASSO) {
+      for (int g = 0; g < P.ngroups; ++g) {
+        const double cg = P.g_w[g];
+        if (!(cg > 0.0)) continue;
+        double s = 0.0;
+        for (int j = P.g_start[g]; j < P.g_end[g]; ++j) s += cc[j] * cc[j];
+        lm = fmax(lm, sqrt(s) / cg);
+      }
+    } else {
+      const double sc = fam == OEM_ENET ? P.alp[q] : 1.0;
+      for (int j = 0; j < p; ++j) {
+        const double wj = P.var_w ? P.var_w[j] : 1.0;
+        if (!(wj > 0.0)) continue;
+        lm = fmax(lm, fabs(cc[j]) / (sc * wj));
+      }
+    }
+    s_lmax[q] = lm;
+    s_lidx[q] = 0;
+    s_it[q] = 0;
+    // parameter validity against the d in use (R#8): the paper's denominators must be > 0
+    const double g = P.gam[q];
+    bool bad = false;
+    if (fam == OEM_MCP || fam == OEM_GRP_MCP) bad = !(g > 1.0) || !(g * d > 1.0);
+    if (fam == OEM_SCAD || fam == OEM_GRP_SCAD) bad = !(g > 2.0) || !((g - 1.0) * d > 1.0);
+    if (fam == OEM_ENET) bad = !(P.alp[q] >= 0.0 && P.alp[q] <= 1.0);
+    if (bad) { atomicExch(&P.flags[1], 1); s_lidx[q] = L; }
+  }
+  if (threadIdx.x == 0) { s_bad = 0; s_stop = 0; }
+  __syncthreads();
+  auto lambda_at = [&](int q, int l) -> double {
+    if (P.lam_explicit) return P.lam_explicit[l];
+    if (L == 1) return s_lmax[q];
+    return s_lmax[q] * exp(((double)l / (double)(L - 1)) * log(P.lmin_ratio));  // R#15
+  };
+  if (threadIdx.x < nP) {
+    const int q = threadIdx.x;
+    if (s_lidx[q] < L) s_lam[q] = lambda_at(q, 0);
+    if (v.rank == 0)
+      for (int l = 0; l < L; ++l) P.lam_out[((size_t)v.unit * nP + q) * L + l] = lambda_at(q, l);
+  }
+  __syncthreads();
+
+  const int T = P.T, groups_rows = blockDim.x / T;
+  const int rg = threadIdx.x / T, tl = threadIdx.x % T;
+  const bool grp = P.g_of != nullptr;
+
+  for (int64_t t = 0;; ++t) {
+    uint32_t qmask = 0;  // units (penalties) still on their path; identical on every CTA of the group
+    for (int q = 0; q < nP; ++q)
+      if (s_lidx[q] < L) qmask |= 1u << q;
+    if (!qmask) break;
+    const int slot = (int)(t % 3);
+    unsigned long long* ds = P.dslot + ((size_t)slot * P.nU + v.unit) * nP;
+    // ---- E-step + M-step in closed form: u = c + d beta - G beta, local rows
+    for (int rb = 0; rb < v.nr; rb += groups_rows) {
+      const int r = rb + rg;
+      double acc[NPT];
+#pragma unroll
+      for (int q = 0; q < NPT; ++q) acc[q] = 0.0;
+      if (r < v.nr) {
+        const double* grow = Gs + (size_t)r * P.ps;
+        for (int k = tl; k < p; k += T) {
+          const double g = grow[k];
+#pragma unroll
+          for (int q = 0; q < NPT; ++q)
+            if ((qmask >> q) & 1u) acc[q] = fma(g, vec[q * P.ps + k], acc[q]);
+        }
+      }
+#pragma unroll
+      for (int q = 0; q < NPT; ++q) {
+        if (!((qmask >> q) & 1u)) continue;
+        double a = acc[q];
+        for (int o = T >> 1; o > 0; o >>= 1) a += __shfl_xor_sync(0xffffffffu, a, o, T);
+        if (tl == 0 && r < v.nr) {
+          const int j = v.j0 + r;
+          const double u = c[j] + d * vec[q * P.ps + j] - a;
+          if (!isfinite(u)) s_bad = 1;
+          if (!grp) {
+            const double wj = P.var_w ? P.var_w[j] : 1.0;
+            uv[q * P.smem_rows + r] = th_coord(P.fam[q], u, wj * s_lam[q], P.gam[q], P.alp[q], d);
+          } else {
+            uv[q * P.smem_rows + r] = u;
+          }
+        }
+      }
+    }
+    __syncthreads();
+    if (grp && v.nr > 0) {
+      // group M-step (eqs glasso / gmcp / gscad): groups are contiguous, inside [j0, j1)
+      const int g0 = P.g_of[v.j0], g1 = P.g_of[v.j1 - 1] + 1;
+      for (int e = threadIdx.x; e < (g1 - g0) * nP; e += blockDim.x) {
+        const int q = e % nP, gid = g0 + e / nP;
+        if (!((qmask >> q) & 1u)) continue;
+        const int a = P.g_start[gid] - v.j0, b = P.g_end[gid] - v.j0;
+        double* ug = uv + q * P.smem_rows;
+        double s = 0.0;
+        for (int r = a; r < b; ++r) s += ug[r] * ug[r];
+        const double nu = sqrt(s);
+        const double lam = P.g_w[gid] * s_lam[q];
+        const int fam = P.fam[q];
+        if (fam == OEM_GRP_LASSO) {
+          const double f = nu > 0.0 ? pos(1.0 - lam / nu) : 0.0;     // (u/d)(1 - c lam/||u||)_+
+          for (int r = a; r < b; ++r) ug[r] = ug[r] / d * f;
+        } else {
+          const double sc = nu > 0.0 ? (fam == OEM_GRP_MCP ? th_mcp(nu, lam, P.gam[q], d)
+                                                          : th_scad(nu, lam, P.gam[q], d)) / nu
+                                     : 0.0;
+          for (int r = a; r < b; ++r) ug[r] = sc * ug[r];
+        }
+      }
+      __syncthreads();
+    }
+    // ---- delta = max |beta' - beta| over local rows; publish beta'
+    double* nb = P.bbuf + ((size_t)(t & 1) * P.nU + v.unit) * nP * p;
+    for (int q = 0; q < nP; ++q) {
+      if (!((qmask >> q) & 1u)) continue;
+      double m = 0.0;
+      for (int r = threadIdx.x; r < v.nr; r += blockDim.x) {
+        const double b = uv[q * P.smem_rows + r];
+        m = fmax(m, fabs(b - vec[q * P.ps + v.j0 + r]));
+        if (v.C > 1) nb[(size_t)q * p + v.j0 + r] = b;
+      }
+      for (int o = 16; o > 0; o >>= 1) m = fmax(m, __shfl_xor_sync(0xffffffffu, m, o));
+      if ((threadIdx.x & 31) == 0 && m > 0.0) atomic_max_pos(&ds[q], m);
+    }
+    // reset the slot used next iteration (3 rotating slots: no reader or writer is on it now)
+    if (v.rank == 0 && threadIdx.x < nP) P.dslot[((size_t)((t + 1) % 3) * P.nU + v.unit) * nP + threadIdx.x] = 0ull;
+    __syncthreads();
+    if (threadIdx.x == 0 && s_bad) atomicMin(&P.bad_iter[v.unit], (unsigned long long)t);
+    __threadfence();
+    group_barrier(bar, v.C);
+    // ---- every CTA of the group reads the same delta and the new beta
+    if (threadIdx.x < nP) {
+      const unsigned long long bits = __ldcg(&ds[threadIdx.x]);
+      s_delta[threadIdx.x] = __longlong_as_double((long long)bits);
+    }
+    if (threadIdx.x == 0) s_stop = __ldcg(&P.bad_iter[v.unit]) <= (unsigned long long)t;
+    if (v.C > 1) {
+      for (int q = 0; q < nP; ++q) {
+        if (!((qmask >> q) & 1u)) continue;
+        for (int k = threadIdx.x; k < p; k += blockDim.x) vec[q * P.ps + k] = __ldcg(nb + (size_t)q * p + k);
+      }
+    } else {
+      for (int q = 0; q < nP; ++q) {
+        if (!((qmask >> q) & 1u)) continue;
+        for (int r = threadIdx.x; r < v.nr; r += blockDim.x) vec[q * P.ps + v.j0 + r] = uv[q * P.smem_rows + r];
+      }
+    }
+    __syncthreads();
+    if (s_stop) {
+      if (threadIdx.x == 0) atomicExch(&P.flags[0], 1);
+      break;
+    }
+    // ---- per-unit convergence bookkeeping (identical decisions on every CTA of the group)
+    for (int q = 0; q < nP; ++q) {
+      if (!((qmask >> q) & 1u)) continue;
+      const int64_t it = s_it[q] + 1;
+      const bool conv = s_delta[q] <= P.tol;   // R#17: max_j |dbeta_j| <= tol
+      if (conv || it >= P.maxit) {
+        const int l = s_lidx[q];
+        double* out = P.beta_out + (((size_t)v.unit * nP + q) * L + l) * p;
+        for (int r = threadIdx.x; r < v.nr; r += blockDim.x) out[P.perm[v.j0 + r]] = vec[q * P.ps + v.j0 + r];
+        __syncthreads();
+        if (threadIdx.x == 0) {
+          if (v.rank == 0) {
+            P.it_out[((size_t)v.unit * nP + q) * L + l] = it;
+            P.cv_out[((size_t)v.unit * nP + q) * L + l] = conv ? 1 : 0;
+          }
+          s_lidx[q] = l + 1;
+          s_it[q] = 0;
+          if (l + 1 < L) s_lam[q] = lambda_at(q, l + 1);
+        }
+      } else if (threadIdx.x == 0) {
+        s_it[q] = it;
+      }
+      __syncthreads();
+    }
+  }
+}
+
+// ---------------------------------------------------------------- host side
+struct Layout {
+  std::vector<int> unit, rank, ncta, j0, j1;
+  int smem_rows = 0, ps = 0, T = 1, ncta_total = 0, Cmax = 1;
+  size_t smem = 0;
+};
+
+// Split each unit's rows over C CTAs (cut at group boundaries) so the rows fit shared memory,
+// and all nU*C CTAs are co-resident (cooperative launch, one CTA per SM).
+static bool make_layout(int nU, int p, int NPT, const std::vector<int>& gstart, int num_sms, size_t smem_cap,
+                        Layout& lo, std::string& why) {
+  lo.ps = p + 2 - (p & 1);        // even pitch...
+  if ((lo.ps % 16) == 0 || (lo.ps % 16) == 8) lo.ps += 2;  // ...not a multiple of 8 doubles
+  auto bytes_for = [&](int rows) { return ((size_t)rows * lo.ps + (size_t)NPT * lo.ps + (size_t)NPT * rows) * 8; };
+  int fit = 0;
+  while (fit < p && bytes_for(fit + 1) <= smem_cap) ++fit;
+  if (fit < 1) { why = "one row does not fit shared memory"; return false; }
+  int C = (p + fit - 1) / fit;
+  for (;;) {
+    std::vector<int> cuts{0};
+    for (int c = 1; c < C; ++c) {
+      const int target = (int)((int64_t)p * c / C);
+      int best = target;
+      if (!gstart.empty()) {
+        best = -1;
+        for (int b : gstart)
+          if (b > cuts.back() && b < p && (best < 0 || std::abs(b - target) < std::abs(best - target))) best = b;
+        if (best < 0) break;
+      }
+      if (best > cuts.back() && best < p) cuts.push_back(best);
+    }
+    cuts.push_back(p);
+    int maxrows = 0;
+    for (size_t c = 0; c + 1 < cuts.size(); ++c) maxrows = std::max(maxrows, cuts[c + 1] - cuts[c]);
+    if (bytes_for(maxrows) > smem_cap) {
+      if (C >= p) { why = "rows do not fit shared memory"; return false; }
+      ++C;
+      continue;
+    }
+    C = (int)cuts.size() - 1;
+    if ((int64_t)C * nU > num_sms) {
+      why = "needs " + std::to_string((int64_t)C * nU) + " co-resident CTAs (> SM count)";
+      return false;
+    }
+    lo.smem_rows = maxrows;
+    lo.smem = bytes_for(maxrows) + 64 * 8;
+    lo.Cmax = C;
+    for (int u = 0; u < nU; ++u)
+      for (int c = 0; c < C; ++c) {
+        lo.unit.push_back(u);
+        lo.rank.push_back(c);
+        lo.j0.push_back(cuts[c]);
+        lo.j1.push_back(cuts[c + 1]);
+      }
+    lo.ncta.assign(nU, C);
+    lo.ncta_total = nU * C;
+    int T = 1;
+    while (T < 32 && PT / (T * 2) >= maxrows) T *= 2;
+    lo.T = T;
+    return true;
+  }
+}
+
+}  // namespace oem
+
+using namespace oem;
+
+extern "C" void oem_path_cfg_default(oem_path_cfg* cfg) {
+  if (!cfg) return;
+  cfg->nlambda = 100;
+  cfg->lambda_min_ratio = 1e-3;
+  cfg->lambda = nullptr;
+  cfg->tol = 1e-11;
+  cfg->maxit = 100000;
+  cfg->var_w = nullptr;
+  cfg->group = nullptr;
+  cfg->ngroups = 0;
+  cfg->grp_w = nullptr;
+  cfg->power_iters = 200;
+  cfg->d_inflate = 5e-3;
+  cfg->fold_mode = 0;
+  cfg->lambda_max_override = nullptr;
+}
+
+template <typename K>
+static oem_status coop_launch(K kern, int grid, size_t smem, cudaStream_t st, void** args) {
+  OEM_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  OEM_CUDA_TRY(cudaLaunchCooperativeKernel((const void*)kern, dim3(grid), dim3(PT), args, smem, st));
+  return OEM_OK;
+}
+
+extern "C" oem_status oem_fit_path(oem_ctx* ctx, const double* G, const double* xty, const int64_t* counts,
+                                   int32_t nG, int32_t p, const oem_penalty* pens, int32_t nP,
+                                   const oem_path_cfg* cfg_in, const double* d_in, const double* beta_init,
+                                   double* beta_out, double* lambda_out, int64_t* iters_out, uint8_t* converged_out,
+                                   double* d_out, void* stream) {
+  if (!ctx) OEM_FAIL(OEM_ERR_INVALID_ARG, "null oem_ctx");
+  OEM_CUDA_TRY(cudaSetDevice(ctx->device));
+  oem_path_cfg cfg;
+  if (cfg_in) cfg = *cfg_in;
+  else oem_path_cfg_default(&cfg);
+  cudaStream_t st = (cudaStream_t)stream;
+  if (!G || !xty || !counts || !pens || !beta_out || !lambda_out || !iters_out || !converged_out || !d_out)
+    OEM_FAIL(OEM_ERR_INVALID_ARG, "oem_fit_path: null pointer");
+  if (p < 1 || nG < 1) OEM_FAIL(OEM_ERR_DIM, "oem_fit_path: need p >= 1, nG >= 1");
+  if (p > 16383) OEM_FAIL(OEM_ERR_UNSUPPORTED, "oem_fit_path: p > 16383");
+  if (nP < 1 || nP > 8) OEM_FAIL(OEM_ERR_INVALID_ARG, "oem_fit_path: 1 <= nP <= 8 penalties per call");
+  if (cfg.nlambda < 1) OEM_FAIL(OEM_ERR_INVALID_ARG, "oem_fit_path: nlambda < 1");
+  if (!cfg.lambda && !(cfg.lambda_min_ratio > 0.0 && cfg.lambda_min_ratio < 1.0) && cfg.nlambda > 1)
+    OEM_FAIL(OEM_ERR_INVALID_ARG, "oem_fit_path: need 0 < lambda_min_ratio < 1");
+  if (!(cfg.tol > 0.0) || cfg.maxit < 1) OEM_FAIL(OEM_ERR_INVALID_ARG, "oem_fit_path: need tol > 0, maxit >= 1");
+  const int fold = cfg.fold_mode ? 1 : 0;
+  const int nU = fold ? nG + 1 : nG;
+  const int L = cfg.nlambda;
+  bool any_grp = false;
+  for (int q = 0; q < nP; ++q) {
+    const int f = pens[q].family;
+    if (f < OEM_LASSO || f > OEM_GRP_SCAD) OEM_FAIL(OEM_ERR_INVALID_ARG, "oem_fit_path: unknown penalty family");
+    if (f >= OEM_GRP_LASSO) any_grp = true;
+    if (f == OEM_ENET && !(pens[q].alpha >= 0.0 && pens[q].alpha <= 1.0))
+      OEM_FAIL(OEM_ERR_INVALID_ARG, "oem_fit_path: elastic-net alpha outside [0,1]");
+    if ((f == OEM_MCP || f == OEM_GRP_MCP) && !(pens[q].gamma > 1.0)) OEM_FAIL(OEM_ERR_INVALID_ARG, "MCP needs gamma > 1");
+    if ((f == OEM_SCAD || f == OEM_GRP_SCAD) && !(pens[q].gamma > 2.0)) OEM_FAIL(OEM_ERR_INVALID_ARG, "SCAD needs gamma > 2");
+  }
+  if (any_grp && (!cfg.group || cfg.ngroups < 1)) OEM_FAIL(OEM_ERR_INVALID_ARG, "group penalties need cfg.group");
+  // normalisers (R#1, R#20)
+  std::vector<double> inv_n(nU);
+  {
+    int64_t tot = 0;
+    for (int g = 0; g < nG; ++g) {
+      if (counts[g] <= 0) OEM_FAIL(OEM_ERR_EMPTY_FOLD, "oem_fit_path: count " + std::to_string(g) + " is 0");
+      tot += counts[g];
+    }
+    for (int u = 0; u < nU; ++u) {
+      int64_t nn = !fold ? counts[u] : (u == 0 ? tot : tot - counts[u - 1]);
+      if (nn <= 0) OEM_FAIL(OEM_ERR_EMPTY_FOLD, "oem_fit_path: empty training set");
+      inv_n[u] = 1.0 / (double)nn;
+    }
+  }
+  // groups -> permutation making them contiguous (stable by id)
+  std::vector<int> perm(p), gstart, gend, g_of_perm;
+  std::vector<double> gw;
+  std::iota(perm.begin(), perm.end(), 0);
+  if (cfg.group) {
+    for (int j = 0; j < p; ++j)
+      if (cfg.group[j] < 0 || cfg.group[j] >= cfg.ngroups) OEM_FAIL(OEM_ERR_INVALID_ARG, "group id out of range");
+    if (cfg.ngroups > MAXG) OEM_FAIL(OEM_ERR_UNSUPPORTED, "more than 4096 groups");
+    std::stable_sort(perm.begin(), perm.end(), [&](int a, int b) { return cfg.group[a] < cfg.group[b]; });
+    gstart.assign(cfg.ngroups, 0);
+    gend.assign(cfg.ngroups, 0);
+    g_of_perm.assign(p, 0);
+    std::vector<int> size(cfg.ngroups, 0);
+    for (int j = 0; j < p; ++j) size[cfg.group[j]]++;
+    int s = 0;
+    for (int g = 0; g < cfg.ngroups; ++g) { gstart[g] = s; s += size[g]; gend[g] = s; }
+    for (int j = 0; j < p; ++j) g_of_perm[j] = cfg.group[perm[j]];
+    gw.resize(cfg.ngroups);
+    for (int g = 0; g < cfg.ngroups; ++g) {
+      gw[g] = cfg.grp_w ? cfg.grp_w[g] : std::sqrt((double)size[g]);  // R#12
+      if (!(gw[g] >= 0.0) || !std::isfinite(gw[g])) OEM_FAIL(OEM_ERR_INVALID_ARG, "group weight must be >= 0");
+    }
+  }
+  const int NPT = nP <= 1 ? 1 : nP <= 2 ? 2 : nP <= 4 ? 4 : 8;
+  Layout lo;
+  std::string why;
+  if (!make_layout(nU, p, NPT, any_grp ? gstart : std::vector<int>(), ctx->num_sms, 200 * 1024, lo, why))
+    OEM_FAIL(OEM_ERR_UNSUPPORTED, "oem_fit_path: persistent solver layout: " + why);
+  if (any_grp) {
+    // a group may not straddle two CTAs: checked against the cuts
+    for (size_t i = 0; i < lo.j0.size(); ++i)
+      for (int g = 0; g < cfg.ngroups; ++g)
+        if (gstart[g] < lo.j0[i] && gend[g] > lo.j0[i])
+          OEM_FAIL(OEM_ERR_UNSUPPORTED, "oem_fit_path: a group is larger than one solver CTA's rows");
+  }
+  // ---- workspace (device): small tables in one block, large arrays in another
+  const size_t pp = (size_t)p * p;
+  size_t off = 0;
+  auto take = [&](size_t bytes) { size_t o = off; off += (bytes + 255) / 256 * 256; return o; };
+  const size_t o_Gn = take(sizeof(double) * nU * pp);
+  const size_t o_cn = take(sizeof(double) * nU * p);
+  const size_t o_bbuf = take(sizeof(double) * 2 * nU * nP * p);
+  const size_t o_wbuf = take(sizeof(double) * 2 * nU * p);
+  const size_t o_pslot = take(sizeof(double) * 3 * nU * lo.Cmax);
+  const size_t o_bad = take(sizeof(unsigned long long) * nU);
+  const size_t o_dslot = take(sizeof(unsigned long long) * 3 * nU * nP);
+  const size_t o_bar = take(sizeof(unsigned) * 2 * nU);
+  const size_t o_flags = take(sizeof(int) * 4);
+  const size_t o_invn = take(sizeof(double) * nU);
+  const size_t o_perm = take(sizeof(int) * p);
+  const size_t o_gof = take(sizeof(int) * p);
+  const size_t o_gs = take(sizeof(int) * std::max<size_t>(1, gstart.size()));
+  const size_t o_ge = take(sizeof(int) * std::max<size_t>(1, gend.size()));
+  const size_t o_gw = take(sizeof(double) * std::max<size_t>(1, gw.size()));
+  const size_t o_varw = take(sizeof(double) * p);
+  const size_t o_fam = take(sizeof(int) * nP);
+  const size_t o_gam = take(sizeof(double) * nP);
+  const size_t o_alp = take(sizeof(double) * nP);
+  const size_t o_lam = take(sizeof(double) * L);
+  const size_t o_lmax = take(sizeof(double));
+  const size_t o_cu = take(sizeof(int) * lo.ncta_total);
+  const size_t o_cr = take(sizeof(int) * lo.ncta_total);
+  const size_t o_un = take(sizeof(int) * nU);
+  const size_t o_j0 = take(sizeof(int) * lo.ncta_total);
+  const size_t o_j1 = take(sizeof(int) * lo.ncta_total);
+  const size_t o_d = take(sizeof(double) * nU);
+  const size_t o_host_end = off;
+  OEM_CUDA_TRY(ctx->path_ws.ensure(off));
+  char* base = ctx->path_ws.as<char>();
+  // host staging of the small tables, one H2D copy
+  std::vector<char> hb(o_host_end - o_invn, 0);
+  auto put = [&](size_t o, const void* src, size_t bytes) { if (bytes) std::memcpy(hb.data() + (o - o_invn), src, bytes); };
+  put(o_invn, inv_n.data(), sizeof(double) * nU);
+  put(o_perm, perm.data(), sizeof(int) * p);
+  if (any_grp || cfg.group) {
+    put(o_gof, g_of_perm.data(), sizeof(int) * p);
+    put(o_gs, gstart.data(), sizeof(int) * gstart.size());
+    put(o_ge, gend.data(), sizeof(int) * gend.size());
+    put(o_gw, gw.data(), sizeof(double) * gw.size());
+  }
+  std::vector<int> fam(nP);
+  std::vector<double> gam(nP), alp(nP);
+  for (int q = 0; q < nP; ++q) { fam[q] = pens[q].family; gam[q] = pens[q].gamma; alp[q] = pens[q].alpha; }
+  put(o_fam, fam.data(), sizeof(int) * nP);
+  put(o_gam, gam.data(), sizeof(double) * nP);
+  put(o_alp, alp.data(), sizeof(double) * nP);
+  if (cfg.lambda) put(o_lam, cfg.lambda, sizeof(double) * L);
+  if (cfg.lambda_max_override) put(o_lmax, cfg.lambda_max_override, sizeof(double));
+  put(o_cu, lo.unit.data(), sizeof(int) * lo.ncta_total);
+  put(o_cr, lo.rank.data(), sizeof(int) * lo.ncta_total);
+  put(o_un, lo.ncta.data(), sizeof(int) * nU);
+  put(o_j0, lo.j0.data(), sizeof(int) * lo.ncta_total);
+  put(o_j1, lo.j1.data(), sizeof(int) * lo.ncta_total);
+  if (d_in) put(o_d, d_in, sizeof(double) * nU);
+  OEM_CUDA_TRY(cudaMemcpyAsync(base + o_invn, hb.data(), hb.size(), cudaMemcpyHostToDevice, st));
+  OEM_CUDA_TRY(cudaMemsetAsync(base + o_dslot, 0, (o_invn - o_dslot), st));  // dslot, bar, flags
+  OEM_CUDA_TRY(cudaMemsetAsync(base + o_bad, 0xff, sizeof(unsigned long long) * nU, st));
+  double* Gn = reinterpret_cast<double*>(base + o_Gn);
+  double* cn = reinterpret_cast<double*>(base + o_cn);
+  int* flags = reinterpret_cast<int*>(base + o_flags);
+  double* varw_p = nullptr;
+  if (cfg.var_w) {
+    // permuted copy of the variable weights (device -> device gather via a tiny kernel is
+    // overkill here: p values, done with a host round trip-free D2D per element block)
+    std::vector<double> tmp(p);
+    OEM_CUDA_TRY(cudaMemcpyAsync(tmp.data(), cfg.var_w, sizeof(double) * p, cudaMemcpyDeviceToHost, st));
+    OEM_CUDA_TRY(cudaStreamSynchronize(st));
+    std::vector<double> wp(p);
+    for (int j = 0; j < p; ++j) {
+      wp[j] = tmp[perm[j]];
+      if (!(wp[j] >= 0.0) || !std::isfinite(wp[j])) OEM_FAIL(OEM_ERR_INVALID_ARG, "variable weights must be >= 0");
+    }
+    OEM_CUDA_TRY(cudaMemcpyAsync(base + o_varw, wp.data(), sizeof(double) * p, cudaMemcpyHostToDevice, st));
+    OEM_CUDA_TRY(cudaStreamSynchronize(st));
+    varw_p = reinterpret_cast<double*>(base + o_varw);
+  }
+  // ---- a6 normalise (+ fold complements, + permutation)
+  {
+    const int64_t total = (int64_t)nU * ((int64_t)pp + p);
+    const int blocks = (int)std::max<int64_t>(1, std::min<int64_t>(ctx->num_sms * 8, (total + 255) / 256));
+    prep_units_kernel<<<blocks, 256, 0, st>>>(G, xty, nG, p, fold, reinterpret_cast<double*>(base + o_invn),
+                                              reinterpret_cast<int*>(base + o_perm), Gn, cn, flags);
+    OEM_CUDA_TRY(cudaGetLastError());
+  }
+  PathParams P;
+  std::memset(&P, 0, sizeof(P));
+  P.p = p; P.nP = nP; P.L = L; P.nU = nU; P.ps = lo.ps; P.T = lo.T; P.maxit = cfg.maxit; P.tol = cfg.tol;
+  P.Gn = Gn; P.cn = cn;
+  P.cta_unit = reinterpret_cast<int*>(base + o_cu);
+  P.cta_rank = reinterpret_cast<int*>(base + o_cr);
+  P.unit_ncta = reinterpret_cast<int*>(base + o_un);
+  P.cta_j0 = reinterpret_cast<int*>(base + o_j0);
+  P.cta_j1 = reinterpret_cast<int*>(base + o_j1);
+  P.smem_rows = lo.smem_rows;
+  P.fam = reinterpret_cast<int*>(base + o_fam);
+  P.gam = reinterpret_cast<double*>(base + o_gam);
+  P.alp = reinterpret_cast<double*>(base + o_alp);
+  P.var_w = varw_p;
+  P.ngroups = cfg.group ? cfg.ngroups : 0;
+  P.g_start = reinterpret_cast<int*>(base + o_gs);
+  P.g_end = reinterpret_cast<int*>(base + o_ge);
+  P.g_w = reinterpret_cast<double*>(base + o_gw);
+  P.g_of = any_grp ? reinterpret_cast<int*>(base + o_gof) : nullptr;
+  P.perm = reinterpret_cast<int*>(base + o_perm);
+  P.lam_explicit = cfg.lambda ? reinterpret_cast<double*>(base + o_lam) : nullptr;
+  P.lmin_ratio = cfg.lambda_min_ratio;
+  P.shared_grid = fold;
+  P.lmax_override = cfg.lambda_max_override ? reinterpret_cast<double*>(base + o_lmax) : nullptr;
+  P.d = reinterpret_cast<double*>(base + o_d);
+  P.beta_init = beta_init;
+  P.bbuf = reinterpret_cast<double*>(base + o_bbuf);
+  P.dslot = reinterpret_cast<unsigned long long*>(base + o_dslot);
+  P.bar = reinterpret_cast<unsigned*>(base + o_bar);
+  P.beta_out = beta_out; P.lam_out = lambda_out; P.it_out = iters_out; P.cv_out = converged_out;
+  P.flags = flags;
+  P.bad_iter = reinterpret_cast<unsigned long long*>(base + o_bad);
+  // ---- a7 d per unit (power rule R#5) unless given
+  if (!d_in) {
+    if (cfg.power_iters < 0) OEM_FAIL(OEM_ERR_INVALID_ARG, "power_iters < 0");
+    PathParams P1 = P;
+    P1.smem_rows = lo.smem_rows;
+    double* wbuf = reinterpret_cast<double*>(base + o_wbuf);
+    double* pslot = reinterpret_cast<double*>(base + o_pslot);
+    int iters = cfg.power_iters, Cmax = lo.Cmax;
+    double infl = cfg.d_inflate;
+    double* dptr = reinterpret_cast<double*>(base + o_d);
+    void* args[] = {&P1, &iters, &infl, &wbuf, &pslot, &Cmax, &dptr};
+    const size_t smem = ((size_t)lo.smem_rows * lo.ps + lo.ps + lo.smem_rows + 64) * 8;
+    oem_status s = coop_launch(power_kernel, lo.ncta_total, smem, st, args);
+    if (s != OEM_OK) return s;
+    OEM_CUDA_TRY(cudaMemsetAsync(base + o_bar, 0, sizeof(unsigned) * 2 * nU, st));
+  }
+  OEM_CUDA_TRY(cudaMemcpyAsync(d_out, base + o_d, sizeof(double) * nU, cudaMemcpyDeviceToDevice, st));
+  // ---- a8-a10 lambda grid + OEM paths
+  {
+    void* args[] = {&P};
+    oem_status s;
+    if (NPT == 1) s = coop_launch(path_kernel<1>, lo.ncta_total, lo.smem, st, args);
+    else if (NPT == 2) s = coop_launch(path_kernel<2>, lo.ncta_total, lo.smem, st, args);
+    else if (NPT == 4) s = coop_launch(path_kernel<4>, lo.ncta_total, lo.smem, st, args);
+    else s = coop_launch(path_kernel<8>, lo.ncta_total, lo.smem, st, args);
+    if (s != OEM_OK) return s;
+  }
+  int hflags[4] = {0, 0, 0, 0};
+  OEM_CUDA_TRY(cudaMemcpyAsync(hflags, flags, sizeof(hflags), cudaMemcpyDeviceToHost, st));
+  OEM_CUDA_TRY(cudaStreamSynchronize(st));
+  if (hflags[0]) OEM_FAIL(OEM_ERR_NONFINITE, "oem_fit_path: non-finite value in the Gram or the iterates");
+  if (hflags[1])
+    OEM_FAIL(OEM_ERR_INVALID_ARG, "oem_fit_path: MCP needs gamma*d > 1 and SCAD (gamma-1)*d > 1 for the d in use (R#8)");
+  return OEM_OK;
+}

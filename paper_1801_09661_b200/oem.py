@@ -1,0 +1,253 @@
+"""Thin Python binding of liboem.so (include/oem.h): argument marshalling only.
+
+Every step of the hot path runs in the CUDA kernels behind the C ABI; this module passes
+torch-owned device pointers and sizes through ctypes and turns status codes into exceptions.
+There is no CPU fallback: if liboem.so is missing or no CUDA device is present, calls fail
+loudly.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+from dataclasses import dataclass
+
+import torch
+
+_PKG = os.path.dirname(os.path.abspath(__file__))
+LIBOEM = os.path.join(_PKG, "liboem.so")
+
+OEM_LASSO, OEM_ENET, OEM_MCP, OEM_SCAD, OEM_GRP_LASSO, OEM_GRP_MCP, OEM_GRP_SCAD = range(7)
+FAMILY = {"lasso": OEM_LASSO, "enet": OEM_ENET, "mcp": OEM_MCP, "scad": OEM_SCAD,
+          "grp_lasso": OEM_GRP_LASSO, "grp_mcp": OEM_GRP_MCP, "grp_scad": OEM_GRP_SCAD}
+STATUS = ["OEM_OK", "OEM_ERR_INVALID_ARG", "OEM_ERR_DIM", "OEM_ERR_ALIGN", "OEM_ERR_EMPTY_FOLD",
+          "OEM_ERR_NONFINITE", "OEM_ERR_CUDA", "OEM_ERR_NCCL", "OEM_ERR_NOMEM", "OEM_ERR_UNSUPPORTED"]
+
+# Every symbol include/oem.h declares (checked by tests/test_abi.py).
+ABI_SYMBOLS = ["oem_status_string", "oem_last_error", "oem_version", "oem_nccl_unique_id",
+               "oem_ctx_create", "oem_ctx_destroy", "oem_gram", "oem_gram_folds",
+               "oem_gram_weighted", "oem_fit_path", "oem_path_cfg_default"]
+
+
+class OemError(RuntimeError):
+    def __init__(self, code, detail):
+        self.code = code
+        self.status = STATUS[code] if 0 <= code < len(STATUS) else f"status {code}"
+        super().__init__(f"{self.status}: {detail}")
+
+
+class Penalty(ctypes.Structure):
+    _fields_ = [("family", ctypes.c_int32), ("gamma", ctypes.c_double), ("alpha", ctypes.c_double)]
+
+
+class PathCfg(ctypes.Structure):
+    _fields_ = [("nlambda", ctypes.c_int32), ("lambda_min_ratio", ctypes.c_double),
+                ("lambda_", ctypes.c_void_p), ("tol", ctypes.c_double), ("maxit", ctypes.c_int64),
+                ("var_w", ctypes.c_void_p), ("group", ctypes.c_void_p), ("ngroups", ctypes.c_int32),
+                ("grp_w", ctypes.c_void_p), ("power_iters", ctypes.c_int32),
+                ("d_inflate", ctypes.c_double), ("fold_mode", ctypes.c_int32),
+                ("lambda_max_override", ctypes.c_void_p)]
+
+
+_lib = None
+
+
+def lib():
+    """Load liboem.so (in-tree). Raises if it has not been built: there is no fallback."""
+    global _lib
+    if _lib is None:
+        if not os.path.exists(LIBOEM):
+            raise RuntimeError(f"{LIBOEM} not built: run `python -c 'import __graft_entry__ as g; g.build()'`")
+        L = ctypes.CDLL(LIBOEM)
+        P, i32, i64, d = ctypes.c_void_p, ctypes.c_int32, ctypes.c_int64, ctypes.c_double
+        L.oem_status_string.restype = ctypes.c_char_p
+        L.oem_status_string.argtypes = [ctypes.c_int]
+        L.oem_last_error.restype = ctypes.c_char_p
+        L.oem_version.restype = ctypes.c_char_p
+        L.oem_nccl_unique_id.argtypes = [P]
+        L.oem_ctx_create.argtypes = [ctypes.c_int, ctypes.c_int, ctypes.c_int, P, ctypes.POINTER(P)]
+        L.oem_ctx_destroy.argtypes = [P]
+        L.oem_gram.argtypes = [P, P, P, i64, i32, i64, P, P, P, ctypes.POINTER(i64), P]
+        L.oem_gram_folds.argtypes = [P, P, P, i64, i32, i64, i64, i32, P, P, P, P, P]
+        L.oem_gram_weighted.argtypes = [P, P, P, P, i64, i32, i64, d, P, P, P, P]
+        L.oem_fit_path.argtypes = [P, P, P, P, i32, i32, ctypes.POINTER(Penalty), i32,
+                                   ctypes.POINTER(PathCfg), P, P, P, P, P, P, P, P]
+        L.oem_path_cfg_default.argtypes = [ctypes.POINTER(PathCfg)]
+        L.oem_path_cfg_default.restype = None
+        for name in ABI_SYMBOLS:
+            f = getattr(L, name)
+            if name not in ("oem_status_string", "oem_last_error", "oem_version", "oem_path_cfg_default"):
+                f.restype = ctypes.c_int
+        _lib = L
+    return _lib
+
+
+def _check(rc):
+    if rc != 0:
+        raise OemError(rc, lib().oem_last_error().decode())
+
+
+def _ptr(t):
+    return None if t is None else ctypes.c_void_p(t.data_ptr())
+
+
+def _stream(stream):
+    s = torch.cuda.current_stream() if stream is None else stream
+    return ctypes.c_void_p(s.cuda_stream)
+
+
+class Context:
+    """One per (process, device): owns workspace and (nranks > 1) the NCCL communicator."""
+
+    def __init__(self, device=0, nranks=1, rank=0, uid: bytes | None = None):
+        if not torch.cuda.is_available():
+            raise RuntimeError("liboem needs a CUDA device (no CPU fallback)")
+        self.device, self.nranks, self.rank = device, nranks, rank
+        h = ctypes.c_void_p()
+        buf = None if uid is None else ctypes.create_string_buffer(uid, 128)
+        _check(lib().oem_ctx_create(device, nranks, rank, buf, ctypes.byref(h)))
+        self.h = h
+
+    def close(self):
+        if getattr(self, "h", None):
+            lib().oem_ctx_destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+def oem_nccl_unique_id() -> bytes:
+    buf = ctypes.create_string_buffer(128)
+    _check(lib().oem_nccl_unique_id(buf))
+    return buf.raw
+
+
+def _check_x(X, y):
+    if X.dtype != torch.float64 or y.dtype != torch.float64 or not X.is_cuda or not y.is_cuda:
+        raise TypeError("X and y must be float64 CUDA tensors")
+    if X.dim() != 2 or X.stride(1) != 1:
+        raise ValueError("X must be 2-D row-major (stride(1) == 1)")
+    if y.dim() != 1 or y.stride(0) != 1 or y.shape[0] != X.shape[0]:
+        raise ValueError("y must be contiguous with len(y) == X.shape[0]")
+
+
+def oem_gram(ctx: Context, X: torch.Tensor, y: torch.Tensor, stream=None):
+    """a2: raw (G = X^T X, xty = X^T y, yty, n_total), allreduced over ranks."""
+    _check_x(X, y)
+    n, p = X.shape
+    dev = X.device
+    G = torch.empty((p, p), dtype=torch.float64, device=dev)
+    xty = torch.empty(p, dtype=torch.float64, device=dev)
+    yty = torch.empty(1, dtype=torch.float64, device=dev)
+    nt = ctypes.c_int64()
+    _check(lib().oem_gram(ctx.h, _ptr(X), _ptr(y), n, p, X.stride(0), _ptr(G), _ptr(xty),
+                          _ptr(yty), ctypes.byref(nt), _stream(stream)))
+    return G, xty, yty, nt.value
+
+
+def oem_gram_folds(ctx: Context, X, y, K: int, row_offset: int = 0, stream=None):
+    """a3: K raw per-fold sums (G_k, xty_k, yty_k) and global fold counts."""
+    _check_x(X, y)
+    n, p = X.shape
+    dev = X.device
+    G = torch.empty((K, p, p), dtype=torch.float64, device=dev)
+    xty = torch.empty((K, p), dtype=torch.float64, device=dev)
+    yty = torch.empty(K, dtype=torch.float64, device=dev)
+    counts = (ctypes.c_int64 * K)()
+    _check(lib().oem_gram_folds(ctx.h, _ptr(X), _ptr(y), n, p, X.stride(0), row_offset, K, _ptr(G),
+                                _ptr(xty), _ptr(yty), counts, _stream(stream)))
+    return G, xty, yty, list(counts)
+
+
+def oem_gram_weighted(ctx: Context, X, y01, beta, eps=1e-5, stream=None):
+    """a4: raw (G_w, X^T W z, [sum w, loglik]) for the proximal-Newton step."""
+    _check_x(X, y01)
+    n, p = X.shape
+    dev = X.device
+    if beta.dtype != torch.float64 or not beta.is_cuda or beta.numel() != p:
+        raise ValueError("beta must be a float64 CUDA tensor of length p")
+    beta = beta.contiguous()
+    Gw = torch.empty((p, p), dtype=torch.float64, device=dev)
+    cw = torch.empty(p, dtype=torch.float64, device=dev)
+    sc = torch.empty(2, dtype=torch.float64, device=dev)
+    _check(lib().oem_gram_weighted(ctx.h, _ptr(X), _ptr(y01), _ptr(beta), n, p, X.stride(0), eps,
+                                   _ptr(Gw), _ptr(cw), _ptr(sc), _stream(stream)))
+    return Gw, cw, sc
+
+
+@dataclass
+class PathResult:
+    beta: torch.Tensor      # [nG'][nP][L][p]
+    lam: torch.Tensor       # [nG'][nP][L]
+    iters: torch.Tensor     # [nG'][nP][L] int64
+    conv: torch.Tensor      # [nG'][nP][L] uint8
+    d: torch.Tensor         # [nG']
+
+
+def oem_fit_path(ctx: Context, G, xty, counts, penalties, nlambda=100, lambda_min_ratio=1e-3,
+                 lambdas=None, tol=1e-11, maxit=100000, var_w=None, group=None, ngroups=0,
+                 grp_w=None, power_iters=200, d_inflate=5e-3, fold_mode=False, d_in=None,
+                 beta_init=None, lambda_max=None, stream=None) -> PathResult:
+    """a6-a10: normalise, d, lambda grid and OEM paths for every (Gram, penalty) unit.
+
+    G: [nG, p, p] (or [p, p]) raw sums, xty: [nG, p], counts: nG ints. penalties: list of
+    (family, gamma, alpha)."""
+    if G.dim() == 2:
+        G = G.unsqueeze(0)
+        xty = xty.unsqueeze(0)
+    nG, p, _ = G.shape
+    G = G.contiguous()
+    xty = xty.contiguous()
+    nGo = nG + 1 if fold_mode else nG
+    nP = len(penalties)
+    L = nlambda if lambdas is None else len(lambdas)
+    pens = (Penalty * nP)(*[Penalty(FAMILY[f], float(g), float(a)) for f, g, a in penalties])
+    cfg = PathCfg()
+    lib().oem_path_cfg_default(ctypes.byref(cfg))
+    cfg.nlambda = L
+    cfg.lambda_min_ratio = lambda_min_ratio
+    keep = []
+    if lambdas is not None:
+        lam_h = (ctypes.c_double * L)(*[float(v) for v in lambdas])
+        keep.append(lam_h)
+        cfg.lambda_ = ctypes.cast(lam_h, ctypes.c_void_p)
+    cfg.tol = tol
+    cfg.maxit = maxit
+    if var_w is not None:
+        var_w = var_w.to(device=G.device, dtype=torch.float64).contiguous()
+        cfg.var_w = var_w.data_ptr()
+    if group is not None:
+        g_h = (ctypes.c_int32 * p)(*[int(v) for v in group])
+        keep.append(g_h)
+        cfg.group = ctypes.cast(g_h, ctypes.c_void_p)
+        cfg.ngroups = int(ngroups or (max(int(v) for v in group) + 1))
+    if grp_w is not None:
+        gw_h = (ctypes.c_double * len(grp_w))(*[float(v) for v in grp_w])
+        keep.append(gw_h)
+        cfg.grp_w = ctypes.cast(gw_h, ctypes.c_void_p)
+    cfg.power_iters = power_iters
+    cfg.d_inflate = d_inflate
+    cfg.fold_mode = 1 if fold_mode else 0
+    if lambda_max is not None:
+        lm_h = ctypes.c_double(float(lambda_max))
+        keep.append(lm_h)
+        cfg.lambda_max_override = ctypes.cast(ctypes.pointer(lm_h), ctypes.c_void_p)
+    cnt = (ctypes.c_int64 * nG)(*[int(c) for c in counts])
+    d_h = None
+    if d_in is not None:
+        d_h = (ctypes.c_double * nGo)(*[float(v) for v in d_in])
+    dev = G.device
+    beta = torch.empty((nGo, nP, L, p), dtype=torch.float64, device=dev)
+    lam = torch.empty((nGo, nP, L), dtype=torch.float64, device=dev)
+    iters = torch.empty((nGo, nP, L), dtype=torch.int64, device=dev)
+    conv = torch.empty((nGo, nP, L), dtype=torch.uint8, device=dev)
+    d = torch.empty(nGo, dtype=torch.float64, device=dev)
+    if beta_init is not None:
+        beta_init = beta_init.to(device=dev, dtype=torch.float64).contiguous()
+    _check(lib().oem_fit_path(ctx.h, _ptr(G), _ptr(xty), cnt, nG, p, pens, nP, ctypes.byref(cfg),
+                              d_h, _ptr(beta_init), _ptr(beta), _ptr(lam), _ptr(iters), _ptr(conv),
+                              _ptr(d), _stream(stream)))
+    return PathResult(beta, lam, iters, conv, d)

@@ -1,0 +1,245 @@
+"""GPU parity for the Gram passes (a2 oem_gram, a3 oem_gram_folds, a4 oem_gram_weighted)
+through the C ABI, element by element against the oracle on identical seeded inputs.
+
+Bar (north star): scale-aware relative 1e-12 (R#32); integer-valued designs are
+bit-exact (every partial sum is an exact integer, so any summation order gives the same bits)."""
+import numpy as np
+import pytest
+
+import datagen as dg
+import oracle as orc
+from datagen.configs import CONFIGS
+from gpu_util import device_rows, scale_err, xty_err
+
+pytestmark = pytest.mark.gpu
+
+torch = pytest.importorskip("torch")
+
+
+@pytest.fixture(scope="module")
+def ctx():
+    from paper_1801_09661_b200 import Context
+    c = Context(0)
+    yield c
+    c.close()
+
+
+def to_dev(a):
+    return torch.from_numpy(np.ascontiguousarray(a)).cuda()
+
+
+def int_design(seed, n, p, lo=-8, hi=9):
+    rng = np.random.default_rng(seed)
+    return rng.integers(lo, hi, size=(n, p)).astype(float), rng.integers(lo, hi, size=n).astype(float)
+
+
+# ---------------------------------------------------------------- device generator
+@pytest.mark.parametrize("name", ["cfg1", "cfg2", "cfg3", "cfg4", "cfg5"])
+def test_device_generator_bit_identical(name):
+    cfg = CONFIGS[name]
+    bt = dg.beta(cfg.spec, cfg.explicit_beta)
+    for row0, nrows in ((0, 70), (cfg.n - 37, 37), (cfg.n // 3, 129)):
+        Xd, yd = device_rows(cfg.spec, bt, row0, nrows)
+        Xh, yh = dg.rows_host(cfg.spec, bt, row0, nrows)
+        assert np.array_equal(Xd.cpu().numpy(), Xh)
+        assert np.array_equal(yd.cpu().numpy(), yh)
+
+
+# ---------------------------------------------------------------- a2 Gram
+@pytest.mark.parametrize("p", [1, 2, 7, 20, 31, 100, 127, 200, 247, 248, 300, 513])
+def test_gram_integer_design_bit_exact(ctx, p):
+    from paper_1801_09661_b200 import oem_gram
+    n = 1000 + 37  # several stages and a ragged tail
+    X, y = int_design(p, n, p)
+    ldx = p + (p & 1)
+    Xp = np.zeros((n, ldx))
+    Xp[:, :p] = X
+    Xd = to_dev(Xp)[:, :p]
+    G, c, yy, nt = oem_gram(ctx, Xd, to_dev(y))
+    Go, co, yyo = orc.gram(X, y)
+    assert nt == n
+    assert np.array_equal(G.cpu().numpy(), Go)
+    assert np.array_equal(c.cpu().numpy(), co)
+    assert float(yy) == yyo
+
+
+@pytest.mark.parametrize("name,n", [("cfg1", 1000), ("cfg2", 30011), ("cfg3", 4099), ("cfg4", 2053),
+                                    ("cfg5", 10007)])
+def test_gram_configs_parity(ctx, name, n):
+    from paper_1801_09661_b200 import oem_gram
+    cfg = CONFIGS[name].with_n(n)
+    bt = dg.beta(cfg.spec, cfg.explicit_beta)
+    Xd, yd = device_rows(cfg.spec, bt)
+    G, c, yy, nt = oem_gram(ctx, Xd, yd)
+    X, y = dg.rows_host(cfg.spec, bt)
+    Go, co, yyo = orc.gram(X, y)
+    assert scale_err(G.cpu().numpy(), Go) <= 1e-12
+    assert xty_err(c.cpu().numpy(), co, Go, yyo) <= 1e-12
+    assert abs(float(yy) - yyo) <= 1e-12 * yyo
+    # symmetric output, both triangles
+    Gh = G.cpu().numpy()
+    assert np.array_equal(Gh, Gh.T)
+
+
+def test_gram_full_size_cfg2(ctx):
+    """Full BASELINE size (n = 1e6, p = 100), in the launch configuration bench.py times."""
+    from paper_1801_09661_b200 import oem_gram
+    cfg = CONFIGS["cfg2"]
+    bt = dg.beta(cfg.spec)
+    Xd, yd = device_rows(cfg.spec, bt)
+    G, c, yy, nt = oem_gram(ctx, Xd, yd)
+    acc = orc.GramAccumulator(cfg.p)
+    for r in range(0, cfg.n, 250_000):
+        X, y = dg.rows_host(cfg.spec, bt, r, 250_000)
+        acc.add(X, y)
+    Go, co, yyo = acc.result()
+    assert scale_err(G.cpu().numpy(), Go) <= 1e-12
+    assert xty_err(c.cpu().numpy(), co, Go, yyo) <= 1e-12
+
+
+def test_gram_full_n_column_subset_cfg4(ctx):
+    """cfg4 at full n = 1e7 (80 GB resident): the leading 16x16 block of G and X^T y on the
+    support checked against the oracle over all 1e7 rows (host generator, those columns)."""
+    from paper_1801_09661_b200 import oem_gram
+    cfg = CONFIGS["cfg4"]
+    bt = dg.beta(cfg.spec)
+    Xd, yd = device_rows(cfg.spec, bt)
+    G, c, yy, nt = oem_gram(ctx, Xd, yd)
+    del Xd
+    torch.cuda.empty_cache()
+    m = 16
+    acc = orc.GramAccumulator(m)
+    for r in range(0, cfg.n, 1_000_000):
+        X, y = dg.rows_host(cfg.spec, bt, r, 1_000_000, 0, m)
+        acc.add(X, y)
+    Go, co, yyo = acc.result()
+    Gh = G.cpu().numpy()
+    assert scale_err(Gh[:m, :m], Go) <= 1e-12
+    assert xty_err(c.cpu().numpy()[:m], co, Go, yyo) <= 1e-12
+    assert abs(float(yy) - yyo) <= 1e-12 * yyo
+    # property at full size: G/n close to the population covariance (block 0.4)
+    grp = np.arange(cfg.p) // 10
+    S = np.where(grp[:, None] == grp[None, :], 0.4, 0.0) + 0.6 * np.eye(cfg.p)
+    assert np.max(np.abs(Gh / cfg.n - S)) < 6 / np.sqrt(cfg.n) * 3
+
+
+def test_gram_edge_cases(ctx):
+    from paper_1801_09661_b200 import OemError, oem_gram
+    # n = 0: zero statistics
+    X = torch.zeros((0, 4), dtype=torch.float64, device="cuda")
+    y = torch.zeros(0, dtype=torch.float64, device="cuda")
+    G, c, yy, nt = oem_gram(ctx, X, y)
+    assert nt == 0 and not G.any() and not c.any() and float(yy) == 0
+    # n = 1
+    X1 = to_dev(np.array([[1.0, 2.0, 3.0, 4.0]]))
+    G, c, yy, nt = oem_gram(ctx, X1, to_dev(np.array([2.0])))
+    assert np.array_equal(G.cpu().numpy(), np.outer([1, 2, 3, 4], [1, 2, 3, 4]))
+    assert np.array_equal(c.cpu().numpy(), [2, 4, 6, 8])
+    # odd ldx -> alignment error from the boundary
+    Xo = torch.zeros((10, 5), dtype=torch.float64, device="cuda")
+    with pytest.raises(OemError) as e:
+        oem_gram(ctx, Xo, torch.zeros(10, dtype=torch.float64, device="cuda"))
+    assert e.value.status == "OEM_ERR_ALIGN"
+
+
+def test_gram_deterministic(ctx):
+    from paper_1801_09661_b200 import oem_gram
+    cfg = CONFIGS["cfg3"].with_n(20000)
+    bt = dg.beta(cfg.spec)
+    Xd, yd = device_rows(cfg.spec, bt)
+    a = oem_gram(ctx, Xd, yd)
+    b = oem_gram(ctx, Xd, yd)
+    assert torch.equal(a[0], b[0]) and torch.equal(a[1], b[1])
+
+
+def test_logical_shards_sum(ctx):
+    """Row sharding: per-shard Grams summed on the host equal the full Gram
+    (integer design: exactly)."""
+    from paper_1801_09661_b200 import oem_gram
+    X, y = int_design(5, 4000, 36)
+    Xd, yd = to_dev(X), to_dev(y)
+    full = oem_gram(ctx, Xd, yd)[0].cpu().numpy()
+    parts = [oem_gram(ctx, Xd[r:r + 500], yd[r:r + 500])[0].cpu().numpy() for r in range(0, 4000, 500)]
+    assert np.array_equal(sum(parts), full)
+
+
+# ---------------------------------------------------------------- a3 fold Grams
+@pytest.mark.parametrize("p,K,n,off", [(20, 10, 1000, 0), (100, 10, 20037, 3), (129, 3, 999, 1),
+                                       (500, 10, 3001, 0), (7, 1, 100, 0), (5, 2, 64, 5)])
+def test_gram_folds_integer_bit_exact(ctx, p, K, n, off):
+    from paper_1801_09661_b200 import oem_gram_folds
+    X, y = int_design(p * 7 + K, n, p)
+    ldx = p + (p & 1)
+    Xp = np.zeros((n, ldx))
+    Xp[:, :p] = X
+    Gk, ck, yyk, cnt = oem_gram_folds(ctx, to_dev(Xp)[:, :p], to_dev(y), K, row_offset=off)
+    Go, co, yyo, cnto = orc.gram_folds(X, y, K, row_offset=off)
+    assert list(cnt) == list(cnto)
+    assert np.array_equal(Gk.cpu().numpy(), Go)
+    assert np.array_equal(ck.cpu().numpy(), co)
+    assert np.array_equal(yyk.cpu().numpy(), yyo)
+
+
+def test_gram_folds_cfg3_parity(ctx):
+    from paper_1801_09661_b200 import oem_gram_folds
+    cfg = CONFIGS["cfg3"].with_n(10_013)
+    bt = dg.beta(cfg.spec)
+    Xd, yd = device_rows(cfg.spec, bt)
+    Gk, ck, yyk, cnt = oem_gram_folds(ctx, Xd, yd, 10)
+    X, y = dg.rows_host(cfg.spec, bt)
+    Go, co, yyo, _ = orc.gram_folds(X, y, 10)
+    for k in range(10):
+        assert scale_err(Gk[k].cpu().numpy(), Go[k]) <= 1e-12
+        assert xty_err(ck[k].cpu().numpy(), co[k], Go[k], yyo[k]) <= 1e-12
+
+
+def test_empty_fold_error(ctx):
+    from paper_1801_09661_b200 import OemError, oem_gram_folds
+    X, y = int_design(1, 5, 4)
+    with pytest.raises(OemError) as e:
+        oem_gram_folds(ctx, to_dev(X), to_dev(y), 7)
+    assert e.value.status == "OEM_ERR_EMPTY_FOLD"
+
+
+# ---------------------------------------------------------------- a4 weighted Gram
+def test_weighted_zero_beta_exact(ctx):
+    from paper_1801_09661_b200 import oem_gram_weighted
+    X, _ = int_design(9, 3001, 30)
+    y = (np.random.default_rng(9).random(3001) < 0.3).astype(float)
+    Gw, cw, sc = oem_gram_weighted(ctx, to_dev(X), to_dev(y), torch.zeros(30, dtype=torch.float64, device="cuda"))
+    Go, co, sco = orc.gram_weighted(X, y, np.zeros(30))
+    assert np.array_equal(Gw.cpu().numpy(), Go)      # w = 1/4 exactly, integer sums
+    assert np.array_equal(cw.cpu().numpy(), co)      # w z = y - 1/2 exactly
+    assert float(sc[0]) == sco[0]
+    assert abs(float(sc[1]) - sco[1]) <= 1e-12 * abs(sco[1])
+
+
+@pytest.mark.parametrize("n,p", [(10007, 200), (5000, 37), (777, 247)])
+def test_weighted_parity(ctx, n, p):
+    from paper_1801_09661_b200 import oem_gram_weighted
+    cfg = CONFIGS["cfg5"]
+    spec = cfg.spec.replace(n=n, p=p, nnz=min(20, p))
+    bt = dg.beta(spec)
+    Xd, yd = device_rows(spec, bt)
+    X, y = dg.rows_host(spec, bt)
+    beta = 0.7 * bt + 0.05
+    Gw, cw, sc = oem_gram_weighted(ctx, Xd, yd, to_dev(beta))
+    Go, co, sco = orc.gram_weighted(X, y, beta)
+    assert scale_err(Gw.cpu().numpy(), Go) <= 1e-12
+    # scale-aware for the augmented column: sqrt(Gw_jj * sum w z^2) (R#32 applied to [X | z])
+    eta = X @ beta
+    mu = np.clip(1 / (1 + np.exp(-eta)), 1e-5, 1 - 1e-5)
+    w = mu * (1 - mu)
+    szz = np.sum(w * (eta + (y - mu) / w) ** 2)
+    assert np.max(np.abs(cw.cpu().numpy() - co) / np.sqrt(np.diag(Go) * szz)) <= 1e-12
+    assert abs(float(sc[0]) - sco[0]) <= 1e-12 * sco[0]
+    assert abs(float(sc[1]) - sco[1]) <= 1e-12 * abs(sco[1])
+
+
+def test_weighted_unsupported_large_p(ctx):
+    from paper_1801_09661_b200 import OemError, oem_gram_weighted
+    X = torch.zeros((10, 300), dtype=torch.float64, device="cuda")
+    with pytest.raises(OemError) as e:
+        oem_gram_weighted(ctx, X, torch.zeros(10, dtype=torch.float64, device="cuda"),
+                          torch.zeros(300, dtype=torch.float64, device="cuda"))
+    assert e.value.status == "OEM_ERR_UNSUPPORTED"

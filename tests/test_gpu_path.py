@@ -1,0 +1,212 @@
+"""GPU parity for a6-a10 (normalise, d, lambda grid, OEM paths) through oem_fit_path.
+
+The oracle runs the same algorithm with the GPU's d (paths depend on d for MCP/SCAD, DESIGN.md
+R#30), the same lambda grid, tol and maxit; the bar is max |beta_gpu - beta_oracle| <= 1e-8 at
+every lambda (north star), equal converged flags, and d within [lambda_1, 1.01 lambda_1]."""
+import numpy as np
+import pytest
+
+import datagen as dg
+import oracle as orc
+from datagen.configs import CONFIGS, groups_of
+from gpu_util import device_rows
+
+pytestmark = pytest.mark.gpu
+torch = pytest.importorskip("torch")
+
+TOL_BETA = 1e-8
+
+
+@pytest.fixture(scope="module")
+def ctx():
+    from paper_1801_09661_b200 import Context
+    c = Context(0)
+    yield c
+    c.close()
+
+
+def host_problem(cfg):
+    bt = dg.beta(cfg.spec, cfg.explicit_beta)
+    X, y = dg.rows_host(cfg.spec, bt)
+    return bt, X, y
+
+
+def check_fit(fit, Go, co, n, penalties, nlambda, unit=0, group=None, lambdas=None, w=None, d_tol=True):
+    d = float(fit.d[unit])
+    Gn = Go / n
+    if d_tol:
+        lam1 = np.linalg.eigvalsh(Gn)[-1]
+        assert lam1 * (1 - 1e-12) <= d <= 1.01 * lam1, (d, lam1)
+    for q, (fam, gamma, alpha) in enumerate(penalties):
+        if lambdas is None:
+            lmax = orc.lambda_max(fam, co / n, w=w, group=group, alpha=alpha)
+            lam = orc.lambda_grid(lmax, nlambda)
+        else:
+            lam = np.asarray(lambdas, dtype=float)
+        lg = fit.lam[unit, q].cpu().numpy()
+        assert np.max(np.abs(lg - lam) / lam.clip(min=1e-300)) < 1e-13
+        B, it, cv = orc.oem_path(Gn, co / n, d, fam, lg, gamma, alpha, w=w, group=group)
+        Bg = fit.beta[unit, q].cpu().numpy()
+        err = np.max(np.abs(Bg - B))
+        assert err <= TOL_BETA, (fam, err)
+        assert np.array_equal(fit.conv[unit, q].cpu().numpy().astype(bool), cv)
+        itg = fit.iters[unit, q].cpu().numpy()
+        assert np.max(np.abs(itg - it)) <= max(2, 0.02 * it.max()), (itg - it)
+
+
+def test_cfg1_lasso_path(ctx):
+    from paper_1801_09661_b200 import oem_fit_path, oem_gram
+    cfg = CONFIGS["cfg1"]
+    bt, X, y = host_problem(cfg)
+    G, c, yy, n = oem_gram(ctx, torch.from_numpy(X).cuda(), torch.from_numpy(y).cuda())
+    fit = oem_fit_path(ctx, G, c, [n], cfg.penalties, nlambda=cfg.nlambda)
+    Go, co, _ = orc.gram(X, y)
+    check_fit(fit, Go, co, n, cfg.penalties, cfg.nlambda)
+    # lambda_max nulls everything, the smallest lambda recovers the support
+    assert not fit.beta[0, 0, 0].any()
+    assert (fit.beta[0, 0, -1].abs() > 0.1).sum() >= 5
+
+
+@pytest.mark.parametrize("n", [30011, 1_000_000])
+def test_cfg2_three_penalties(ctx, n):
+    """cfg2: lasso + MCP(3) + SCAD(3.7) paths of 100 lambda on one Gram, computed together."""
+    from paper_1801_09661_b200 import oem_fit_path, oem_gram
+    cfg = CONFIGS["cfg2"].with_n(n)
+    bt = dg.beta(cfg.spec)
+    Xd, yd = device_rows(cfg.spec, bt)
+    G, c, yy, nn = oem_gram(ctx, Xd, yd)
+    fit = oem_fit_path(ctx, G, c, [nn], cfg.penalties, nlambda=cfg.nlambda)
+    acc = orc.GramAccumulator(cfg.p)
+    for r in range(0, n, 250_000):
+        X, y = dg.rows_host(cfg.spec, bt, r, min(250_000, n - r))
+        acc.add(X, y)
+    Go, co, _ = acc.result()
+    check_fit(fit, Go, co, n, cfg.penalties, cfg.nlambda)
+    # multi-penalty independence: lasso alone == lasso inside the batch, bit for bit
+    fit1 = oem_fit_path(ctx, G, c, [nn], cfg.penalties[:1], nlambda=cfg.nlambda, d_in=[float(fit.d[0])])
+    assert torch.equal(fit1.beta[0, 0], fit.beta[0, 0])
+
+
+def test_cfg3_fold_mode(ctx):
+    """cfg3 shape: 10 fold Grams in one pass, then full fit + 10 complement fits (fold_mode),
+    shared lambda grid from the full data, per-unit d (R#20-22)."""
+    from paper_1801_09661_b200 import oem_fit_path, oem_gram_folds
+    cfg = CONFIGS["cfg3"].with_n(12_007)
+    bt = dg.beta(cfg.spec)
+    Xd, yd = device_rows(cfg.spec, bt)
+    Gk, ck, yyk, cnt = oem_gram_folds(ctx, Xd, yd, 10)
+    L = 20
+    fit = oem_fit_path(ctx, Gk, ck, cnt, cfg.penalties, nlambda=L, fold_mode=True)
+    X, y = dg.rows_host(cfg.spec, bt)
+    Gf, cf, _, cnto = orc.gram_folds(X, y, 10)
+    Gm, cm = orc.fold_complements(Gf, cf)
+    n = X.shape[0]
+    lmax0 = orc.lambda_max("lasso", cf.sum(0) / n)
+    lam = orc.lambda_grid(lmax0, L)
+    check_fit(fit, Gf.sum(0), cf.sum(0), n, cfg.penalties, L, unit=0, lambdas=lam)
+    for k in range(10):
+        check_fit(fit, Gm[k], cm[k], n - cnto[k], cfg.penalties, L, unit=k + 1, lambdas=lam)
+
+
+def test_cfg4_group_lasso_and_enet(ctx):
+    """cfg4 shape (p = 1000, 100 groups of 10, block-equicorrelated design): group lasso and
+    EN(0.5) together, first 12 lambda of the 50-point grid (oracle time)."""
+    from paper_1801_09661_b200 import oem_fit_path, oem_gram
+    cfg = CONFIGS["cfg4"].with_n(20_000)
+    bt = dg.beta(cfg.spec)
+    Xd, yd = device_rows(cfg.spec, bt)
+    G, c, yy, n = oem_gram(ctx, Xd, yd)
+    grp = groups_of(cfg)
+    X, y = dg.rows_host(cfg.spec, bt)
+    Go, co, _ = orc.gram(X, y)
+    Ls = []
+    for fam, gamma, alpha in cfg.penalties:
+        lmax = orc.lambda_max(fam, co / n, group=grp if fam.startswith("grp") else None, alpha=alpha)
+        Ls.append(orc.lambda_grid(lmax, cfg.nlambda)[:12])
+    for q, pen in enumerate(cfg.penalties):
+        fit = oem_fit_path(ctx, G, c, [n], [pen], lambdas=Ls[q], group=grp, ngroups=100)
+        check_fit(fit, Go, co, n, [pen], 12, group=grp if pen[0].startswith("grp") else None, lambdas=Ls[q])
+    # both penalties in one launch agree with the separate launches
+    both = oem_fit_path(ctx, G, c, [n], cfg.penalties, lambdas=Ls[0], group=grp, ngroups=100)
+    one = oem_fit_path(ctx, G, c, [n], cfg.penalties[:1], lambdas=Ls[0], group=grp, ngroups=100,
+                       d_in=[float(both.d[0])])
+    assert torch.equal(both.beta[0, 0], one.beta[0, 0])
+
+
+def test_noncontiguous_groups_and_weights(ctx):
+    from paper_1801_09661_b200 import oem_fit_path, oem_gram
+    rng = np.random.default_rng(3)
+    cfg = CONFIGS["cfg2"].with_n(5000)
+    bt = dg.beta(cfg.spec)
+    X, y = dg.rows_host(cfg.spec, bt)
+    G, c, yy, n = oem_gram(ctx, torch.from_numpy(X).cuda(), torch.from_numpy(y).cuda())
+    Go, co, _ = orc.gram(X, y)
+    grp = rng.integers(0, 17, size=100).astype(np.int32)
+    grp[:17] = np.arange(17)  # every id used
+    gw = rng.uniform(0.5, 2.0, 17)
+    pens = [("grp_lasso", 0.0, 1.0), ("grp_mcp", 3.0, 1.0), ("grp_scad", 3.7, 1.0)]
+    fit = oem_fit_path(ctx, G, c, [n], pens, nlambda=25, group=grp, ngroups=17, grp_w=gw)
+    d = float(fit.d[0])
+    for q, (fam, gamma, alpha) in enumerate(pens):
+        lg = fit.lam[0, q].cpu().numpy()
+        B, it, cv = orc.oem_path(Go / n, co / n, d, fam, lg, gamma, alpha, group=grp, grp_w=gw)
+        assert np.max(np.abs(fit.beta[0, q].cpu().numpy() - B)) <= TOL_BETA
+    w = torch.from_numpy(rng.uniform(0.0, 2.0, 100)).cuda()
+    w[5] = 0.0  # unpenalized coordinate
+    pens = [("lasso", 0.0, 1.0), ("enet", 0.0, 0.3), ("scad", 3.7, 1.0)]
+    fit = oem_fit_path(ctx, G, c, [n], pens, nlambda=30, var_w=w)
+    d = float(fit.d[0])
+    for q, (fam, gamma, alpha) in enumerate(pens):
+        lg = fit.lam[0, q].cpu().numpy()
+        lmax = orc.lambda_max(fam, co / n, w=w.cpu().numpy(), alpha=alpha)
+        assert abs(lg[0] - lmax) <= 1e-13 * lmax
+        B, it, cv = orc.oem_path(Go / n, co / n, d, fam, lg, gamma, alpha, w=w.cpu().numpy())
+        assert np.max(np.abs(fit.beta[0, q].cpu().numpy() - B)) <= TOL_BETA
+
+
+def test_lambda_zero_ols_and_warm_start(ctx):
+    from paper_1801_09661_b200 import oem_fit_path, oem_gram
+    cfg = CONFIGS["cfg1"].with_n(600)
+    bt, X, y = host_problem(cfg)
+    G, c, yy, n = oem_gram(ctx, torch.from_numpy(X).cuda(), torch.from_numpy(y).cuda())
+    fit = oem_fit_path(ctx, G, c, [n], [("lasso", 0, 1), ("mcp", 3, 1)], lambdas=[0.0], tol=1e-14,
+                       maxit=200000)
+    ols = np.linalg.solve(X.T @ X, X.T @ y)
+    for q in range(2):
+        assert np.max(np.abs(fit.beta[0, q, 0].cpu().numpy() - ols)) < 1e-10
+    # warm start from the solution: one update, converged
+    init = fit.beta[:, :, 0, :].clone()
+    fit2 = oem_fit_path(ctx, G, c, [n], [("lasso", 0, 1), ("mcp", 3, 1)], lambdas=[0.0], tol=1e-12,
+                        beta_init=init, d_in=[float(fit.d[0])])
+    assert int(fit2.iters.max()) <= 2
+
+
+def test_invalid_parameters(ctx):
+    from paper_1801_09661_b200 import OemError, oem_fit_path
+    G = torch.eye(4, dtype=torch.float64, device="cuda") * 10
+    c = torch.ones(4, dtype=torch.float64, device="cuda")
+    with pytest.raises(OemError) as e:   # gamma * d = 0.9 * 1 <= 1 (R#8)
+        oem_fit_path(ctx, G, c, [10], [("mcp", 1.5, 1.0)], nlambda=5, d_in=[0.5])
+    assert e.value.status == "OEM_ERR_INVALID_ARG"
+    with pytest.raises(OemError) as e:
+        oem_fit_path(ctx, G, c, [10], [("grp_lasso", 0, 1.0)], nlambda=5)
+    assert e.value.status == "OEM_ERR_INVALID_ARG"
+    Gn = G.clone()
+    Gn[1, 1] = float("nan")
+    with pytest.raises(OemError) as e:
+        oem_fit_path(ctx, Gn, c, [10], [("lasso", 0, 1.0)], nlambda=5, d_in=[2.0])
+    assert e.value.status == "OEM_ERR_NONFINITE"
+
+
+def test_maxit_flag_not_error(ctx):
+    from paper_1801_09661_b200 import oem_fit_path, oem_gram
+    cfg = CONFIGS["cfg2"].with_n(3000)
+    bt, X, y = host_problem(cfg)
+    G, c, yy, n = oem_gram(ctx, torch.from_numpy(X).cuda(), torch.from_numpy(y).cuda())
+    fit = oem_fit_path(ctx, G, c, [n], [("lasso", 0, 1)], nlambda=10, maxit=3)
+    assert int(fit.iters.max()) == 3
+    assert not bool(fit.conv[0, 0, -1])
+    Go, co, _ = orc.gram(X, y)
+    B, it, cv = orc.oem_path(Go / n, co / n, float(fit.d[0]), "lasso", fit.lam[0, 0].cpu().numpy(), maxit=3)
+    assert np.max(np.abs(fit.beta[0, 0].cpu().numpy() - B)) <= 1e-12
+    assert np.array_equal(fit.iters[0, 0].cpu().numpy(), it)
