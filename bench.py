@@ -1,0 +1,349 @@
+"""bench.py — the OEM hot path on B200: Gram fp64 TFLOP/s and full-path fit seconds.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--workload cfg4] [--impl oem|reference]
+
+For N > 1 the driver launches one process per GPU with torch.distributed.run; X is row-sharded
+(rank r owns global rows [r n/N, (r+1) n/N), generated in place on its GPU) and the raw Gram is
+combined with one NCCL allreduce inside oem_gram; n is fixed as N grows
+("scaling": "strong"). One step = the whole hot path over the workload: a2 Gram pass
+(+ a5 combine) -> a6 normalise -> a7 d -> a8 lambda grid -> a9/a10 the OEM paths for every
+penalty. `value` = whole-job Gram TFLOP/s (algorithmic n p (p+3) flops, all ranks, over the max
+over ranks of the Gram-phase device time); `fit_seconds` = device time of the whole step.
+Inputs (80 GB for cfg4) are far larger than the 126 MB L2, so no flush is needed.
+
+The reference arm (--impl reference) is the repo's CPU oracle (oracle/), timed as it stands on
+the host cores on a bounded row sample of the same workload: this run has no reference
+implementation to install (the reference is a paper), see DESIGN.md §8.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import numpy as np  # noqa: E402
+
+import datagen as dg  # noqa: E402
+from datagen.configs import CONFIGS, groups_of  # noqa: E402
+
+METRIC = "Gram fp64 TFLOP/s (X^TX+X^Ty) and full-path fit seconds at 1/2/4/8 B200"
+FP64_PEAK_TFLOPS = 37.06   # measured DMMA peak, profiles/fp64_peak_r01.log (MEASURED_PEAKS.json has no fp64)
+HBM_PEAK_GBS = 6541.5      # MEASURED_PEAKS.json
+
+
+def gram_flops(n, p):
+    """Algorithmic flops of the Gram pass: n p (p+1) (SYRK upper + diagonal) + 2 n p (X^T y)."""
+    return float(n) * p * (p + 3)
+
+
+# ------------------------------------------------------------------ clocks sampler
+class Clocks:
+    def __init__(self, index=0):
+        self.index = index
+        self.samples = []
+        self._stop = threading.Event()
+        self._t = None
+
+    def start(self):
+        def run():
+            q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
+                 "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+                 "clocks_event_reasons.sw_power_cap")
+            while not self._stop.is_set():
+                try:
+                    out = subprocess.run(["nvidia-smi", "-i", str(self.index), f"--query-gpu={q}",
+                                          "--format=csv,noheader,nounits"], capture_output=True, text=True,
+                                         timeout=5).stdout.strip()
+                    if out:
+                        self.samples.append([s.strip() for s in out.split(",")])
+                except Exception:
+                    pass
+                self._stop.wait(0.2)
+        self._t = threading.Thread(target=run, daemon=True)
+        self._t.start()
+
+    def stop(self):
+        self._stop.set()
+        if self._t:
+            self._t.join(timeout=10)
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        sm = [float(s[0]) for s in self.samples if s[0].replace(".", "").isdigit()]
+        mx = [float(s[1]) for s in self.samples if s[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for s in self.samples for i in range(4)
+                          if len(s) > 3 + i and s[3 + i].lower() == "active"})
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(self.samples)}
+
+
+# ------------------------------------------------------------------ CPU oracle baseline
+def cpu_baseline(cfg, budget_s=15.0):
+    """The oracle's Gram (oracle/oracle.c, compensated fp64, all host cores) on a bounded row
+    sample of the workload; rows come from the host generator (untimed)."""
+    import oracle as orc
+    cores = os.cpu_count() or 1
+    bt = dg.beta(cfg.spec, cfg.explicit_beta)
+    probe = max(64, min(2000, int(2e8 / (cfg.p * cfg.p))))
+    X, y = dg.rows_host(cfg.spec, bt, 0, probe)
+    t0 = time.perf_counter()
+    orc.gram(X, y, nthreads=cores)
+    dt = time.perf_counter() - t0
+    rows = int(min(cfg.n, max(probe, probe * budget_s / max(dt, 1e-6))))
+    rows = min(rows, probe * 64)
+    X, y = dg.rows_host(cfg.spec, bt, 0, rows)
+    t0 = time.perf_counter()
+    orc.gram(X, y, nthreads=cores)
+    dt = time.perf_counter() - t0
+    return {"value": gram_flops(rows, cfg.p) / dt / 1e12, "unit": "TFLOP/s", "cores": cores, "kind": "oracle",
+            "sample": f"oracle Gram (compensated fp64, {cores} threads) over rows 0..{rows} of {cfg.name} "
+                      f"(n={cfg.n}, p={cfg.p}), {dt:.2f} s"}
+
+
+# ------------------------------------------------------------------ reference arm (the oracle)
+def run_reference(args, cfg):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return 0
+    import oracle as orc
+    cores = os.cpu_count() or 1
+    bt = dg.beta(cfg.spec, cfg.explicit_beta)
+    rows = max(256, int(3e9 / (cfg.p * (cfg.p + 3))))  # a few seconds of oracle work per step
+    X, y = dg.rows_host(cfg.spec, bt, 0, rows)
+    times = []
+    for s in range(args.warmup + args.steps):
+        t0 = time.perf_counter()
+        G, c, yy = orc.gram(X, y, nthreads=cores)
+        dt = time.perf_counter() - t0
+        if s >= args.warmup:
+            times.append(dt)
+    v = gram_flops(rows, cfg.p) / (sum(times) / len(times)) / 1e12
+    line = {"impl": "reference", "metric": METRIC, "value": v, "unit": "TFLOP/s", "n_gpus": args.gpus,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * sum(times) / len(times),
+            "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic (seeded Philox generator, DESIGN.md §4)",
+            "config": {"workload": cfg.name, "n": cfg.n, "p": cfg.p, "sample_rows": rows},
+            "cpu_baseline": {"value": v, "unit": "TFLOP/s", "cores": cores, "kind": "oracle",
+                             "sample": f"oracle Gram over rows 0..{rows} of {cfg.name} per step"},
+            "e2e": {"value": v, "unit": "TFLOP/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+# ------------------------------------------------------------------ the GPU arm
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--workload", default="cfg4", choices=sorted(CONFIGS))
+    ap.add_argument("--impl", default="oem", choices=["oem", "reference"])
+    ap.add_argument("--e2e-steps", type=int, default=2)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--n", type=int, default=0, help="override n (development only; not a bench number)")
+    args = ap.parse_args()
+    cfg = CONFIGS[args.workload]
+    if args.n:
+        cfg = cfg.with_n(args.n)
+    if args.impl == "reference":
+        return run_reference(args, cfg)
+
+    import torch
+    import torch.distributed as dist
+    from paper_1801_09661_b200 import Context, oem, oem_fit_path, oem_gram, oem_gram_folds
+    from paper_1801_09661_b200.oem import oem_fit_logistic
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world != args.gpus:
+        raise SystemExit(f"--gpus {args.gpus} but WORLD_SIZE={world}")
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        obj = [oem.oem_nccl_unique_id() if rank == 0 else None]
+        dist.broadcast_object_list(obj, src=0)
+        ctx = Context(local, world, rank, obj[0])
+    else:
+        ctx = Context(local)
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+
+    def max_over_ranks(x):
+        if world == 1:
+            return x
+        t = torch.tensor([x], dtype=torch.float64, device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t)
+
+    # ---- a1: this rank's rows, generated in place on its GPU (untimed)
+    n, p = cfg.n, cfg.p
+    r0, r1 = rank * n // world, (rank + 1) * n // world
+    nl = r1 - r0
+    bt = dg.beta(cfg.spec, cfg.explicit_beta)
+    ldx = p + (p & 1)
+    Xs = torch.empty((nl, ldx), dtype=torch.float64, device="cuda")
+    Xd = Xs[:, :p]
+    yd = torch.empty(nl, dtype=torch.float64, device="cuda")
+    btd = torch.from_numpy(bt).cuda()
+    dg.rows_cuda(cfg.spec, btd.data_ptr(), r0, nl, Xs.data_ptr(), ldx, yd.data_ptr(),
+                 torch.cuda.current_stream().cuda_stream)
+    torch.cuda.synchronize()
+    grp = groups_of(cfg)
+    ngroups = p // cfg.group_size if grp is not None else 0
+
+    def step(X, y):
+        """One pass of the whole hot path; returns the fit result (device tensors)."""
+        if cfg.logistic:
+            return oem_fit_logistic(ctx, X, y, cfg.penalties[0], nlambda=cfg.nlambda)
+        if cfg.folds:
+            G, c, yy, cnt = oem_gram_folds(ctx, X, y, cfg.folds, row_offset=r0)
+        else:
+            G, c, yy, nn = oem_gram(ctx, X, y)
+            cnt = [nn]
+        return oem_fit_path(ctx, G, c, cnt, cfg.penalties, nlambda=cfg.nlambda, fold_mode=bool(cfg.folds),
+                            group=grp, ngroups=ngroups)
+
+    for _ in range(args.warmup):
+        res = step(Xd, yd)
+    torch.cuda.synchronize()
+    oem.set_timing(ctx, True)
+    oem.stats(ctx, reset=True)
+    clocks = Clocks(local)
+    clocks.start()
+    barrier()
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for _ in range(args.steps):
+        res = step(Xd, yd)
+    e1.record()
+    torch.cuda.synchronize()
+    barrier()
+    clk = clocks.stop()
+    st = oem.stats(ctx, reset=True)
+    oem.set_timing(ctx, False)
+    total_ms = e0.elapsed_time(e1)
+    gram_phase_ms = st["gram_ms"] + st["reduce_ms"] + st["allreduce_ms"]
+    step_ms = max_over_ranks(total_ms / args.steps)
+    gram_step_ms = max_over_ranks(gram_phase_ms / args.steps)
+    kernel_ms = max_over_ranks(st["gram_ms"] / args.steps)
+    passes = 1
+    if cfg.logistic:
+        passes = max(1, round(st["launches"] / max(1, args.steps)))  # informational only
+    flops_step = gram_flops(n, p)
+    if cfg.logistic:
+        # every outer step is one weighted pass; count them from the fit
+        outer = sum(res.outer_iters)
+        flops_step = (gram_flops(n, p) + 5.0 * n * p) * outer
+    value = flops_step / (gram_step_ms * 1e-3) / 1e12
+    # roofline of the dominant kernel (the tensor-core Gram kernel): algorithmic flops per
+    # launch over its event-timed launch duration on this rank
+    per_launch_flops = gram_flops(nl, p) * (sum(res.outer_iters) if cfg.logistic else 1)
+    achieved = per_launch_flops / (st["gram_ms"] / args.steps * 1e-3) / 1e12
+    traffic = None
+    prof = os.path.join(ROOT, "profiles", "ncu_summary_r01.json")
+    if os.path.exists(prof):
+        try:
+            traffic = json.load(open(prof)).get(cfg.name, {}).get("dram_bytes_per_launch")
+        except Exception:
+            traffic = None
+    roofline = {"bound": "tensor", "achieved": achieved, "peak": FP64_PEAK_TFLOPS, "unit": "TFLOP/s",
+                "frac": achieved / FP64_PEAK_TFLOPS, "traffic": traffic,
+                "kernel": "oem::gram_kernel (TMA + DMMA.8x8x4)",
+                "peak_source": "measured FP64 DMMA microbenchmark (profiles/fp64_peak_r01.log); "
+                               "MEASURED_PEAKS.json carries no fp64 figure",
+                "share_of_step": st["gram_ms"] / max(total_ms, 1e-9),
+                "hbm_gbs": 8.0 * nl * (p + 1) / (st["gram_ms"] / args.steps * 1e-3) / 1e9}
+    launches = int(st["launches"])
+
+    # ---- e2e: the same metric through the public API with HOST buffers (pinned), the H2D of
+    # the step's inputs and the D2H of its result inside the timed region
+    e2e = None
+    if args.e2e_steps > 0:
+        try:
+            Xh = torch.empty((nl, ldx), dtype=torch.float64, pin_memory=True)
+            yh = torch.empty(nl, dtype=torch.float64, pin_memory=True)
+            Xh.copy_(Xs)
+            yh.copy_(yd)
+            torch.cuda.synchronize()
+            out_bytes = 0
+            barrier()
+            t0 = torch.cuda.Event(enable_timing=True)
+            t1 = torch.cuda.Event(enable_timing=True)
+            t2 = torch.cuda.Event(enable_timing=True)
+            h2d_gram_ms = 0.0
+            t0.record()
+            for _ in range(args.e2e_steps):
+                ta = torch.cuda.Event(enable_timing=True)
+                tb = torch.cuda.Event(enable_timing=True)
+                ta.record()
+                Xs.copy_(Xh, non_blocking=True)
+                yd.copy_(yh, non_blocking=True)
+                oem.set_timing(ctx, True)
+                r = step(Xd, yd)
+                tb.record()
+                if cfg.logistic:
+                    hb = r.beta.cpu()
+                else:
+                    hb = r.beta.cpu()
+                out_bytes = hb.numel() * 8
+                torch.cuda.synchronize()
+                s2 = oem.stats(ctx, reset=True)
+                oem.set_timing(ctx, False)
+                h2d_gram_ms += ta.elapsed_time(tb) - s2["power_ms"] - s2["path_ms"]
+            t2.record()
+            torch.cuda.synchronize()
+            barrier()
+            e2e_step_ms = max_over_ranks(t0.elapsed_time(t2) / args.e2e_steps)
+            e2e_gram_ms = max_over_ranks(h2d_gram_ms / args.e2e_steps)
+            e2e = {"value": flops_step / (e2e_gram_ms * 1e-3) / 1e12, "unit": "TFLOP/s",
+                   "h2d_bytes_per_step": int(nl * ldx * 8 + nl * 8) * world,
+                   "d2h_bytes_per_step": int(out_bytes) * world,
+                   "fit_seconds": e2e_step_ms / 1e3,
+                   "note": "H2D of X,y from pinned host memory + Gram phase; fit_seconds is the whole "
+                           "step incl. H2D, paths and the D2H of the coefficient paths"}
+            del Xh, yh
+        except Exception as ex:  # pinned memory exhausted etc.: report, do not fake
+            e2e = {"value": None, "unit": "TFLOP/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0,
+                   "error": repr(ex)[:200]}
+
+    if rank == 0:
+        cpu = None
+        if world == 1 and not args.no_cpu_baseline:
+            cpu = cpu_baseline(cfg)
+        line = {
+            "metric": METRIC, "value": value, "unit": "TFLOP/s", "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": step_ms, "fit_seconds": step_ms / 1e3,
+            "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic (seeded Philox4x32-10 generator, generated in place on each GPU)",
+            "config": {"workload": cfg.name, "n": n, "p": p, "penalties": [f for f, _, _ in cfg.penalties],
+                       "nlambda": cfg.nlambda, "folds": cfg.folds, "logistic": cfg.logistic,
+                       "parallelism": f"rows sharded over {world} GPU(s), NCCL allreduce of the packed Gram",
+                       "l2": "inputs larger than L2 (no flush needed)",
+                       "step": "Gram pass (+allreduce) -> normalise -> d -> lambda grid -> OEM paths"},
+            "gram_phase_ms": gram_step_ms, "gram_kernel_ms": kernel_ms,
+            "path_phase_ms": max_over_ranks((st["power_ms"] + st["path_ms"]) / args.steps),
+            "iters": int(res.iters.sum()) if not cfg.logistic else int(sum(res.inner_iters)),
+            "roofline": roofline, "clocks": clk, "gpu_launches": launches, "e2e": e2e,
+            "cpu_baseline": cpu,
+        }
+        print(json.dumps(line), flush=True)
+    ctx.close()
+    if world > 1:
+        dist.destroy_process_group()
+    return 0
+
+
+if __name__ == "__main__":
+    sys.exit(main())

@@ -137,6 +137,41 @@ oem_status oem_fit_path(oem_ctx* ctx, const double* G, const double* xty, const 
 /* Default-initialise a path config (values listed above). */
 void oem_path_cfg_default(oem_path_cfg* cfg);
 
+/* ---- a4 + a6-a9 driven to convergence: the proximal-Newton logistic path (§4,
+ * glmnet-style outer loop with OEM as the inner solver; R#23-27). For each lambda (warm start
+ * from the previous solution): repeat { oem_gram_weighted at beta (allreduced over ranks);
+ * normalise by n; d_w by the power rule; single-lambda OEM solve from beta } until
+ * max_j |beta_new - beta| <= tol_out or outer_maxit. The lambda grid runs from
+ * lambda_max = max_j |(1/n) sum_i x_ij (y_i - 1/2)| / (w_j [alpha for EN]) (R#14, no intercept)
+ * down to ratio * lambda_max (R#15), unless an explicit grid is given. Coordinate-wise
+ * families only (lasso, EN, MCP, SCAD). Host loop: one scalar device->host read per outer step.
+ * Outputs: beta_out (device, L*p), lambda_out (device, L), outer_iters / inner_iters /
+ * converged (host, L). Errors: as oem_gram_weighted and oem_fit_path. */
+typedef struct {
+  int32_t nlambda; double lambda_min_ratio; const double* lambda /*host, optional*/;
+  double tol_in; int64_t maxit_in; double tol_out; int32_t outer_maxit;
+  double eps; int32_t power_iters; double d_inflate; const double* var_w /*device p or NULL*/;
+} oem_logistic_cfg;
+void oem_logistic_cfg_default(oem_logistic_cfg* cfg);  /* 50, 1e-3, NULL, 1e-11, 1e5, 1e-10, 100, 1e-5, 200, 5e-3, NULL */
+oem_status oem_fit_logistic(oem_ctx* ctx, const double* X, const double* y01, int64_t n_local, int32_t p,
+                            int64_t ldx, const oem_penalty* pen /*host, one*/, const oem_logistic_cfg* cfg /*host*/,
+                            double* beta_out, double* lambda_out, int32_t* outer_iters /*host L*/,
+                            int64_t* inner_iters /*host L*/, uint8_t* converged /*host L*/, void* stream);
+
+/* ---- instrumentation (used by bench.py; no effect on results).
+ * With timing enabled the library records CUDA events around its phases on the launching
+ * stream; oem_ctx_stats synchronises those events and returns the accumulated device times. */
+typedef struct {
+  int64_t launches;      /* kernels this context launched (all phases) */
+  double gram_ms;        /* Gram-pass tensor-core kernels (a2/a3/a4) */
+  double reduce_ms;      /* split-n reduction, fold tail, unpack */
+  double allreduce_ms;   /* NCCL combine (a5) */
+  double power_ms;       /* d (a7) */
+  double path_ms;        /* normalise + lambda grid + OEM path solver (a6, a8-a10) */
+} oem_stats;
+oem_status oem_ctx_set_timing(oem_ctx* ctx, int enable);
+oem_status oem_ctx_stats(oem_ctx* ctx, oem_stats* out /*host*/, int reset);
+
 #ifdef __cplusplus
 }
 #endif

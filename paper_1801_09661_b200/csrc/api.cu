@@ -16,6 +16,7 @@ void set_error(const std::string& msg) { g_last_error = msg; }
 
 oem_status allreduce_sum(oem_ctx* ctx, double* buf, size_t count, cudaStream_t st) {
   if (ctx->nranks <= 1 || count == 0) return OEM_OK;
+  PhaseTimer tm(ctx, PH_ALLREDUCE, st);
   ncclResult_t r = ncclAllReduce(buf, buf, count, ncclFloat64, ncclSum, (ncclComm_t)ctx->nccl_comm, st);
   if (r != ncclSuccess) OEM_FAIL(OEM_ERR_NCCL, std::string("ncclAllReduce: ") + ncclGetErrorString(r));
   return OEM_OK;
@@ -130,7 +131,40 @@ oem_status oem_ctx_destroy(oem_ctx* ctx) {
   ctx->plan_tables.release();
   ctx->path_ws.release();
   ctx->path_small.release();
+  for (auto& pe : ctx->pending) { cudaEventDestroy(pe.a); cudaEventDestroy(pe.b); }
+  for (auto e : ctx->event_pool) cudaEventDestroy(e);
   delete ctx;
+  return OEM_OK;
+}
+
+oem_status oem_ctx_set_timing(oem_ctx* ctx, int enable) {
+  if (!ctx) OEM_FAIL(OEM_ERR_INVALID_ARG, "null oem_ctx");
+  ctx->timing = enable != 0;
+  return OEM_OK;
+}
+
+oem_status oem_ctx_stats(oem_ctx* ctx, oem_stats* out, int reset) {
+  if (!ctx || !out) OEM_FAIL(OEM_ERR_INVALID_ARG, "null argument");
+  OEM_CUDA_TRY(cudaSetDevice(ctx->device));
+  for (auto& pe : ctx->pending) {
+    OEM_CUDA_TRY(cudaEventSynchronize(pe.b));
+    float ms = 0.f;
+    OEM_CUDA_TRY(cudaEventElapsedTime(&ms, pe.a, pe.b));
+    ctx->phase_ms[pe.phase] += ms;
+    ctx->event_pool.push_back(pe.a);
+    ctx->event_pool.push_back(pe.b);
+  }
+  ctx->pending.clear();
+  out->launches = ctx->launches;
+  out->gram_ms = ctx->phase_ms[PH_GRAM];
+  out->reduce_ms = ctx->phase_ms[PH_REDUCE];
+  out->allreduce_ms = ctx->phase_ms[PH_ALLREDUCE];
+  out->power_ms = ctx->phase_ms[PH_POWER];
+  out->path_ms = ctx->phase_ms[PH_PATH];
+  if (reset) {
+    ctx->launches = 0;
+    for (double& v : ctx->phase_ms) v = 0.0;
+  }
   return OEM_OK;
 }
 
@@ -146,7 +180,7 @@ oem_status oem_gram(oem_ctx* ctx, const double* X, const double* y, int64_t n_lo
   double* packed = ctx->packed.as<double>();
   if ((s = gram_pass(ctx, MODE_PLAIN, X, y, nullptr, 0.0, n_local, p, ldx, 0, 1, packed, st)) != OEM_OK) return s;
   if ((s = allreduce_sum(ctx, packed, psize, st)) != OEM_OK) return s;
-  if ((s = gram_unpack(packed, 1, p, G, xty, yty, st)) != OEM_OK) return s;
+  if ((s = gram_unpack(ctx, packed, 1, p, G, xty, yty, st)) != OEM_OK) return s;
   if (n_total) {
     int64_t n = n_local;
     if ((s = host_allreduce_i64(ctx, &n, 1)) != OEM_OK) return s;
@@ -179,7 +213,7 @@ oem_status oem_gram_folds(oem_ctx* ctx, const double* X, const double* y, int64_
   if ((s = gram_pass(ctx, MODE_FOLD, X, y, nullptr, 0.0, n_local, p, ldx, row_offset, K, packed, st)) != OEM_OK)
     return s;
   if ((s = allreduce_sum(ctx, packed, (size_t)psize * K, st)) != OEM_OK) return s;
-  return gram_unpack(packed, K, p, G_folds, xty_folds, yty_folds, st);
+  return gram_unpack(ctx, packed, K, p, G_folds, xty_folds, yty_folds, st);
 }
 
 oem_status oem_gram_weighted(oem_ctx* ctx, const double* X, const double* y01, const double* beta, int64_t n_local,
@@ -196,7 +230,7 @@ oem_status oem_gram_weighted(oem_ctx* ctx, const double* X, const double* y01, c
   double* packed = ctx->packed.as<double>();
   if ((s = gram_pass(ctx, MODE_WEIGHTED, X, y01, beta, eps, n_local, p, ldx, 0, 1, packed, st)) != OEM_OK) return s;
   if ((s = allreduce_sum(ctx, packed, psize + 2, st)) != OEM_OK) return s;
-  if ((s = gram_unpack(packed, 1, p, Gw, xtwz, nullptr, st)) != OEM_OK) return s;
+  if ((s = gram_unpack(ctx, packed, 1, p, Gw, xtwz, nullptr, st)) != OEM_OK) return s;
   OEM_CUDA_TRY(cudaMemcpyAsync(scalars, packed + psize, 2 * sizeof(double), cudaMemcpyDeviceToDevice, st));
   return OEM_OK;
 }

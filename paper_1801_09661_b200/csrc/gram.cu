@@ -7,22 +7,26 @@
 // column (w_i = mu(1-mu), z_i = eta + (y - mu)/w, eta = x_i^T beta).
 //
 // How (B200-first):
-//  * Row blocks of X (BK = 32 rows) stream HBM -> shared memory through TMA
-//    (cp.async.bulk.tensor, mbarrier complete_tx) in a multi-stage ring fed by one producer
-//    warp; y (or y01) rides along as an extra column filled by the producer's lanes.
+//  * Row blocks of X (BK = 32 rows) and of y stream HBM -> shared memory through TMA
+//    (cp.async.bulk.tensor, mbarrier complete_tx) in a multi-stage ring fed by one elected
+//    producer thread; consumers release stages through a second mbarrier ring.
 //  * The contraction runs on the FP64 tensor cores: mma.sync m8n8k4 f64 (SASS DMMA.8x8x4;
-//    tcgen05 has no f64 kind on sm_100a). Each consumer warp owns a rectangle of R x C 8x8
-//    output blocks of the upper triangle with register accumulators; blocks below the
-//    diagonal are skipped. The smem row pitch is ld = 4 or 12 (mod 16) doubles so the
-//    fragment loads (4 rows x 8 columns per half-warp pair) are bank-conflict free.
-//  * Small p (p+1 <= 248): the whole augmented row fits one TMA box ("single panel"); the
-//    triangle's rectangles are spread over U CTA types that all stream the same rows
-//    (the weighted pass computes eta/w/z per row from the full row in smem, fused).
-//    Large p: 128-column panel pairs (I, J), I <= J, one CTA type per tile, 4x8 rectangles.
-//  * Rows are split into segments (split-n); every (CTA type, segment) writes its own
-//    partial blocks and a second kernel sums segments in a fixed order -> deterministic,
-//    no atomics. The result is packed (upper triangle of the augmented matrix) for a single
-//    NCCL allreduce when the rows are sharded over GPUs.
+//    tcgen05 has no f64 kind on sm_100a). Each consumer warp owns one "job": a rectangle of 8x8
+//    output blocks of the upper triangle with register accumulators. Jobs have compile-time
+//    shapes (full 4x4 / 4x8 / 4xk rectangles, and upper triangles on the diagonal) so the
+//    warp issues exactly the useful DMMAs: a predicated-off DMMA still costs a full pipe slot
+//    on B200 (tools/fp64_mma_patterns.cu: 10 of 16 active -> 62% of peak).
+//  * The smem row pitch is ld = 4 or 12 (mod 16) doubles so the fragment loads (4 rows x 8
+//    columns per half-warp pair) are bank-conflict free; fragment addresses are one base
+//    register plus compile-time offsets.
+//  * Small p (8 ceil((p+1)/8) + 4 <= 256): one TMA box holds the whole augmented row ("single
+//    panel"); jobs are spread over U CTA types that stream the same rows (the weighted pass
+//    computes eta/w/z per row from the full row in smem, fused). Large p: 128-column panel
+//    pairs (I, J), I <= J, one CTA type per tile, 4x8 jobs.
+//  * Rows are split into segments (split-n); every (CTA type, segment) writes its own partial
+//    blocks and a second kernel sums segments in a fixed order -> deterministic, no atomics.
+//    The result is packed (upper triangle of the augmented matrix) for one NCCL allreduce
+//    when the rows are sharded over GPUs.
 #include <algorithm>
 #include <cstring>
 #include <vector>
@@ -34,18 +38,39 @@ namespace oem {
 
 constexpr int BK = 32;      // rows per pipeline stage
 constexpr int MAXST = 6;    // max pipeline stages
-constexpr int MAXNW = 12;   // max consumer warps
+constexpr int NWC = 8;      // consumer warps per CTA
 
-struct RectDesc {
+// job kinds: shape (R x C blocks) and which blocks are issued
+enum JobKind { J_NONE = 0, J_F44, J_T4, J_F41, J_F42, J_F43, J_T1, J_T2, J_T3, J_F48, J_T4F4, J_NKIND };
+__host__ __device__ constexpr int kind_R(int k) {
+  return k == J_NONE ? 0 : k == J_T1 ? 1 : k == J_T2 ? 2 : k == J_T3 ? 3 : 4;
+}
+__host__ __device__ constexpr int kind_C(int k) {
+  return k == J_NONE ? 0 : k == J_F41 || k == J_T1 ? 1 : k == J_F42 || k == J_T2 ? 2
+       : k == J_F43 || k == J_T3 ? 3 : k == J_F48 || k == J_T4F4 ? 8 : 4;
+}
+__host__ __device__ constexpr bool kind_tri(int k) {
+  return k == J_T4 || k == J_T1 || k == J_T2 || k == J_T3 || k == J_T4F4;
+}
+// block (r, c) of the job is issued: all blocks for full kinds, c >= r for triangular ones
+__host__ __device__ constexpr bool kind_active(int k, int r, int c) { return kind_tri(k) ? c >= r : true; }
+__host__ __device__ constexpr int kind_cost(int k) {
+  int n = 0;
+  for (int r = 0; r < kind_R(k); ++r)
+    for (int c = 0; c < kind_C(k); ++c) n += kind_active(k, r, c) ? 1 : 0;
+  return n;
+}
+
+struct Job {
   int32_t bi0, bj0;   // top-left 8x8 block (global block coordinates)
-  uint32_t mask;      // active blocks, bit r*C + c  (block (bi0+r, bj0+c) with bi <= bj < nb)
+  int32_t kind;
   int32_t pad;
 };
 struct CtaDesc {
   int32_t a0, b0;     // first column of panel A / panel B
   int32_t same;       // panel B == panel A
-  int32_t nrect;
-  RectDesc rect[MAXNW];
+  int32_t njob;       // consumer warps with work (arrivals per stage release)
+  Job job[NWC];       // slot w = consumer warp w (SMSP w % 4); J_NONE = idle
 };
 
 struct GramParams {
@@ -53,136 +78,77 @@ struct GramParams {
   int64_t nrows;      // PLAIN/WEIGHTED: n_local rows; FOLD: nq = floor(n_local / K) full groups
   int64_t seg_rows;   // rows (FOLD: groups) per segment, multiple of BK
   int K, off_mod;     // FOLD
-  const double* y;
+  int ytma, ystride;  // y through TMA (1D map, or 2D [nq][Kpad] map for folds); ys row stride
+  const double* y;    // LDG fallback (odd K folds)
   const double* beta;
   double eps;
   double* partial;        // [nfold][nseg][nblk][64]
   double* partial_scal;   // WEIGHTED: [nseg][2]
   const CtaDesc* ctas;
-  const int32_t* blk_of;  // [nb*nb] -> packed upper block index or -1
-  uint32_t tma_bytes;     // bytes of one TMA box (one per panel per stage)
+  const int32_t* blk_of;  // [nb*nb] -> packed upper block index
+  uint32_t xbox_bytes;    // one X box
+  uint32_t ybox_bytes;    // y box per stage (0 if LDG fallback)
   int stage_doubles;      // per-stage smem footprint (doubles)
+  int ys_off;             // offset of ys within a stage (doubles)
 };
 
-template <int R, int C, int NW, int MODE>
-__global__ void __launch_bounds__((NW + 1) * 32, 1)
-gram_kernel(const __grid_constant__ CUtensorMap tmX, const GramParams P) {
-  extern __shared__ __align__(128) double smem[];
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int u = blockIdx.x % P.U;
-  const int rest = blockIdx.x / P.U;
-  const int seg = rest % P.nseg;
-  const int fold = rest / P.nseg;  // 0 unless MODE_FOLD
-  const int ld = P.ld;
+struct Cons {
+  double* smem;
+  uint64_t* full;
+  uint64_t* empty;
+  int warp, lane, nst, seg, fold, kprime;
+  int64_t r0, r1;
+  int a0, b0;
+  bool two;
+  Job job;
+  const double* beta_s;
+  double* scal_s;     // WEIGHTED: [NWC][2] per-warp (sum w, loglik)
+};
 
-  double* beta_s = smem + (size_t)P.ST * P.stage_doubles;                       // WEIGHTED: ld doubles
-  uint64_t* full = reinterpret_cast<uint64_t*>(beta_s + (MODE == MODE_WEIGHTED ? ld : 0));
-  uint64_t* empty = full + MAXST;
-  __shared__ double scal_s[MAXNW][2];
-
-  const int64_t r0 = (int64_t)seg * P.seg_rows;
-  const int64_t r1 = min(P.nrows, r0 + P.seg_rows);
-  const int nst = r1 > r0 ? (int)((r1 - r0 + BK - 1) / BK) : 0;
-  const int kprime = (MODE == MODE_FOLD) ? ((fold - P.off_mod) % P.K + P.K) % P.K : 0;
-
-  const CtaDesc* cd = P.ctas + u;
-  const int a0 = cd->a0, b0 = cd->b0;
-  const bool two = P.two_panel && !cd->same;
-
-  if (threadIdx.x == 0) {
-    for (int s = 0; s < P.ST; ++s) {
-      mbar_init(&full[s], 32);
-      mbar_init(&empty[s], NW);
-    }
-    fence_mbar_init();
-    tma_prefetch(&tmX);
-  }
-  if (MODE == MODE_WEIGHTED)
-    for (int j = threadIdx.x; j < ld; j += blockDim.x) beta_s[j] = j < P.p ? P.beta[j] : 0.0;
-  __syncthreads();
-
-  if (warp == NW) {
-    // ------------------------------------------------------------ producer warp
-    for (int s = 0; s < nst; ++s) {
-      const int st = s % P.ST;
-      const uint32_t ph = (uint32_t)(s / P.ST) & 1u;
-      mbar_wait(&empty[st], ph ^ 1u);
-      double* pa = smem + (size_t)st * P.stage_doubles;
-      double* pb = pa + (size_t)BK * ld;
-      double* ys = pa + (size_t)(P.two_panel ? 2 : 1) * BK * ld;
-      const int64_t rr = r0 + (int64_t)s * BK;
-      if (lane == 0) {
-        asm volatile("mbarrier.expect_tx.relaxed.cta.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(&full[st])),
-                     "r"(two ? 2u * P.tma_bytes : P.tma_bytes)
-                     : "memory");
-        if (MODE == MODE_FOLD) {
-          tma_load_3d(pa, &tmX, &full[st], a0, kprime, (int)rr);
-          if (two) tma_load_3d(pb, &tmX, &full[st], b0, kprime, (int)rr);
-        } else {
-          tma_load_2d(pa, &tmX, &full[st], a0, (int)rr);
-          if (two) tma_load_2d(pb, &tmX, &full[st], b0, (int)rr);
-        }
-      }
-      // the augmented column: y rows of this stage (0 beyond the end)
-      const int64_t row = rr + lane;
-      double yv = 0.0;
-      if (row < r1) {
-        if (MODE == MODE_FOLD) yv = P.y[row * P.K + kprime];
-        else yv = P.y[row];
-      }
-      ys[lane] = yv;
-      mbar_arrive(&full[st]);
-    }
-    return;
-  }
-
-  // -------------------------------------------------------------- consumer warps
-  RectDesc rd;
-  if (warp < cd->nrect) rd = cd->rect[warp];
-  else { rd.bi0 = 0; rd.bj0 = 0; rd.mask = 0u; }
-  uint32_t rowmask = 0, colmask = 0;
+template <int MODE, int KIND>
+__device__ __forceinline__ void consume(const GramParams& P, const Cons& cs) {
+  constexpr int R = kind_R(KIND), C = kind_C(KIND);
+  constexpr int RR = R > 0 ? R : 1, CC = C > 0 ? C : 1;
+  const int ld = P.ld, lane = cs.lane;
+  double acc[RR][CC][2];
 #pragma unroll
-  for (int r = 0; r < R; ++r)
+  for (int r = 0; r < RR; ++r)
 #pragma unroll
-    for (int c = 0; c < C; ++c)
-      if ((rd.mask >> (r * C + c)) & 1u) { rowmask |= 1u << r; colmask |= 1u << c; }
-  int offA[R], offB[C];
-#pragma unroll
-  for (int r = 0; r < R; ++r) offA[r] = (lane & 3) * ld + 8 * (rd.bi0 + r) + (lane >> 2) - a0;
-#pragma unroll
-  for (int c = 0; c < C; ++c) offB[c] = (lane & 3) * ld + 8 * (rd.bj0 + c) + (lane >> 2) - b0;
-
-  double acc[R][C][2];
-#pragma unroll
-  for (int r = 0; r < R; ++r)
-#pragma unroll
-    for (int c = 0; c < C; ++c) { acc[r][c][0] = 0.0; acc[r][c][1] = 0.0; }
-
-  double sw = 0.0, sll = 0.0;  // WEIGHTED scalars (lane 0 of each warp)
-  const int ycol_b = P.p - b0;  // column of y inside panel B (valid if 0 <= ycol_b < ld)
-
-  for (int s = 0; s < nst; ++s) {
-    const int st = s % P.ST;
-    const uint32_t ph = (uint32_t)(s / P.ST) & 1u;
-    mbar_wait(&full[st], ph);
-    double* pa = smem + (size_t)st * P.stage_doubles;
-    double* pb = two ? pa + (size_t)BK * ld : pa;
-    double* ys = pa + (size_t)(P.two_panel ? 2 : 1) * BK * ld;
-    double* ws = ys + BK;
-
+    for (int c = 0; c < CC; ++c) { acc[r][c][0] = 0.0; acc[r][c][1] = 0.0; }
+  const int aoff = (lane & 3) * ld + 8 * cs.job.bi0 + (lane >> 2) - cs.a0;
+  const int boff = (lane & 3) * ld + 8 * cs.job.bj0 + (lane >> 2) - cs.b0;
+  // does this job's column range hold the augmented y column (copy it into the panel)?
+  const int ycol = P.p - cs.b0;
+  const bool ycopy = (MODE != MODE_WEIGHTED) && C > 0 && P.p >= 8 * cs.job.bj0 && P.p < 8 * (cs.job.bj0 + C);
+  const int yidx = lane * P.ystride + (MODE == MODE_FOLD ? cs.kprime : 0);
+  double sw = 0.0, sll = 0.0;
+  int st = 0;
+  uint32_t ph = 0;
+  for (int s = 0; s < cs.nst; ++s) {
+    mbar_wait(&cs.full[st], ph);
+    double* pa = cs.smem + (size_t)st * P.stage_doubles;
+    double* pb = cs.two ? pa + (size_t)BK * ld : pa;
+    double* ys = pa + P.ys_off;
+    double* ws = ys + BK * P.ystride;
     if (MODE != MODE_WEIGHTED) {
-      if (warp == 0 && ycol_b >= 0 && ycol_b < ld) pb[lane * ld + ycol_b] = ys[lane];
+      if (ycopy) {
+        pb[lane * ld + ycol] = ys[yidx];
+        __syncwarp();
+      }
     } else {
       // fused proximal-Newton row quantities: eta, mu (clamped), w, z
-      const int64_t rr = r0 + (int64_t)s * BK;
-      for (int k = warp; k < BK; k += NW) {
+      // BK / NWC = 4 rows per warp, 8 lanes per row; the 4 row leaders do the scalar math at once
+      static_assert(BK == 4 * NWC, "weighted prologue assumes 4 rows per consumer warp");
+      const int64_t rr = cs.r0 + (int64_t)s * BK;
+      {
+        const int k = cs.warp * 4 + (lane >> 3), sub = lane & 7;
         double e = 0.0;
-        for (int j = lane; j < P.p; j += 32) e = fma(pa[k * ld + j], beta_s[j], e);
+        for (int j = sub; j < P.p; j += 8) e = fma(pa[k * ld + j], cs.beta_s[j], e);
 #pragma unroll
-        for (int o = 16; o > 0; o >>= 1) e += __shfl_xor_sync(0xffffffffu, e, o);
-        if (lane == 0) {
+        for (int o = 4; o > 0; o >>= 1) e += __shfl_xor_sync(0xffffffffu, e, o);
+        if (sub == 0) {
           double w = 0.0, z = 0.0;
-          if (rr + k < r1) {
+          if (rr + k < cs.r1) {
             double mu = 1.0 / (1.0 + exp(-e));
             mu = fmin(fmax(mu, P.eps), 1.0 - P.eps);
             w = mu * (1.0 - mu);
@@ -195,57 +161,164 @@ gram_kernel(const __grid_constant__ CUtensorMap tmX, const GramParams P) {
           pa[k * ld + P.p] = z;
         }
       }
+      named_bar_sync(1, NWC * 32);
     }
-    named_bar_sync(1, NW * 32);
-
+    if (KIND != J_NONE) {
+      const double* pak = pa + aoff;
+      const double* pbk = pb + boff;
 #pragma unroll
-    for (int ks = 0; ks < BK / 4; ++ks) {
-      const double* pak = pa + ks * 4 * ld;
-      const double* pbk = pb + ks * 4 * ld;
-      double a[R], b[C];
-      double wk = 1.0;
-      if (MODE == MODE_WEIGHTED) wk = ws[ks * 4 + (lane & 3)];
+      for (int ks = 0; ks < BK / 4; ++ks) {
+        double a[RR], b[CC];
 #pragma unroll
-      for (int r = 0; r < R; ++r) {
-        a[r] = 0.0;
-        if ((rowmask >> r) & 1u) {
-          a[r] = pak[offA[r]];
-          if (MODE == MODE_WEIGHTED) a[r] *= wk;
+        for (int r = 0; r < R; ++r) a[r] = pak[8 * r];
+        if (MODE == MODE_WEIGHTED) {
+          const double wk = ws[ks * 4 + (lane & 3)];
+#pragma unroll
+          for (int r = 0; r < R; ++r) a[r] *= wk;
         }
+#pragma unroll
+        for (int c = 0; c < C; ++c) b[c] = pbk[8 * c];
+#pragma unroll
+        for (int r = 0; r < R; ++r)
+#pragma unroll
+          for (int c = 0; c < C; ++c)
+            if (kind_active(KIND, r, c)) dmma_8x8x4(acc[r][c][0], acc[r][c][1], a[r], b[c]);
+        pak += 4 * ld;
+        pbk += 4 * ld;
       }
-#pragma unroll
-      for (int c = 0; c < C; ++c) b[c] = ((colmask >> c) & 1u) ? pbk[offB[c]] : 0.0;
-#pragma unroll
-      for (int r = 0; r < R; ++r)
-#pragma unroll
-        for (int c = 0; c < C; ++c)
-          if ((rd.mask >> (r * C + c)) & 1u) dmma_8x8x4(acc[r][c][0], acc[r][c][1], a[r], b[c]);
     }
-    fence_proxy_async_smem();  // generic-proxy smem writes above precede the next TMA refill
+    if (ycopy || MODE == MODE_WEIGHTED) fence_proxy_async_smem();  // generic smem writes precede the next TMA refill
     __syncwarp();
-    if (lane == 0) mbar_arrive(&empty[st]);
+    if (cs.lane == 0) mbar_arrive(&cs.empty[st]);
+    if (++st == P.ST) { st = 0; ph ^= 1u; }
   }
-
-  // -------------------------------------------------------------- epilogue
-  double* out = P.partial + ((size_t)(fold * P.nseg + seg) * P.nblk) * 64;
+  // epilogue: this (fold, segment)'s partial blocks
+  if (KIND != J_NONE) {
+    double* out = P.partial + ((size_t)(cs.fold * P.nseg + cs.seg) * P.nblk) * 64;
 #pragma unroll
-  for (int r = 0; r < R; ++r)
+    for (int r = 0; r < R; ++r)
 #pragma unroll
-    for (int c = 0; c < C; ++c)
-      if ((rd.mask >> (r * C + c)) & 1u) {
-        const int idx = P.blk_of[(rd.bi0 + r) * P.nb + rd.bj0 + c];
-        double2 v = make_double2(acc[r][c][0], acc[r][c][1]);
-        *reinterpret_cast<double2*>(out + (size_t)idx * 64 + (lane >> 2) * 8 + 2 * (lane & 3)) = v;
-      }
+      for (int c = 0; c < C; ++c)
+        if (kind_active(KIND, r, c)) {
+          const int idx = P.blk_of[(cs.job.bi0 + r) * P.nb + cs.job.bj0 + c];
+          *reinterpret_cast<double2*>(out + (size_t)idx * 64 + (lane >> 2) * 8 + 2 * (lane & 3)) =
+              make_double2(acc[r][c][0], acc[r][c][1]);
+        }
+  }
   if (MODE == MODE_WEIGHTED) {
-    if (lane == 0) { scal_s[warp][0] = sw; scal_s[warp][1] = sll; }
-    named_bar_sync(1, NW * 32);
-    if (threadIdx.x == 0 && u == 0) {
+    // row leaders (lanes 0, 8, 16, 24) hold the sums of their rows: fixed-order warp reduction
+    sw += __shfl_xor_sync(0xffffffffu, sw, 8);
+    sll += __shfl_xor_sync(0xffffffffu, sll, 8);
+    sw += __shfl_xor_sync(0xffffffffu, sw, 16);
+    sll += __shfl_xor_sync(0xffffffffu, sll, 16);
+    if (lane == 0) { cs.scal_s[2 * cs.warp] = sw; cs.scal_s[2 * cs.warp + 1] = sll; }
+    named_bar_sync(1, NWC * 32);
+    if (cs.warp == 0 && lane == 0 && blockIdx.x % P.U == 0) {
       double a = 0.0, b = 0.0;
-      for (int w = 0; w < NW; ++w) { a += scal_s[w][0]; b += scal_s[w][1]; }
-      P.partial_scal[seg * 2 + 0] = a;
-      P.partial_scal[seg * 2 + 1] = b;
+      for (int w = 0; w < NWC; ++w) { a += cs.scal_s[2 * w]; b += cs.scal_s[2 * w + 1]; }
+      P.partial_scal[cs.seg * 2 + 0] = a;
+      P.partial_scal[cs.seg * 2 + 1] = b;
     }
+  }
+}
+
+template <int MODE, bool TWO>
+__global__ void __launch_bounds__((NWC + 1) * 32, (TWO || MODE == MODE_WEIGHTED) ? 1 : 2)
+gram_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ CUtensorMap tmY, const GramParams P) {
+  extern __shared__ __align__(128) double smem[];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int u = blockIdx.x % P.U;
+  const int rest = blockIdx.x / P.U;
+  __shared__ double scal_s[2 * NWC];
+  Cons cs;
+  cs.scal_s = scal_s;
+  cs.seg = rest % P.nseg;
+  cs.fold = rest / P.nseg;  // 0 unless MODE_FOLD
+  cs.smem = smem;
+  double* beta_s = smem + (size_t)P.ST * P.stage_doubles;  // WEIGHTED: ld doubles
+  cs.full = reinterpret_cast<uint64_t*>(beta_s + (MODE == MODE_WEIGHTED ? P.ld : 0));
+  cs.empty = cs.full + MAXST;
+  cs.beta_s = beta_s;
+  cs.r0 = (int64_t)cs.seg * P.seg_rows;
+  cs.r1 = min(P.nrows, cs.r0 + P.seg_rows);
+  cs.nst = cs.r1 > cs.r0 ? (int)((cs.r1 - cs.r0 + BK - 1) / BK) : 0;
+  cs.kprime = (MODE == MODE_FOLD) ? ((cs.fold - P.off_mod) % P.K + P.K) % P.K : 0;
+  const CtaDesc* cd = P.ctas + u;
+  cs.a0 = cd->a0;
+  cs.b0 = cd->b0;
+  cs.two = TWO && !cd->same;
+  const int njob = cd->njob;
+  const int nconsumers = (MODE == MODE_WEIGHTED) ? NWC : njob;  // arrivals per stage release
+  const int full_count = P.ytma ? 1 : 32;
+
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < P.ST; ++s) {
+      mbar_init(&cs.full[s], full_count);
+      mbar_init(&cs.empty[s], nconsumers);
+    }
+    fence_mbar_init();
+    tma_prefetch(&tmX);
+    if (P.ytma) tma_prefetch(&tmY);
+  }
+  if (MODE == MODE_WEIGHTED)
+    for (int j = threadIdx.x; j < P.ld; j += blockDim.x) beta_s[j] = j < P.p ? P.beta[j] : 0.0;
+  __syncthreads();
+
+  if (warp == NWC) {
+    // ------------------------------------------------------------ producer warp
+    if (!P.ytma || lane == 0) {
+      int st = 0;
+      uint32_t ph = 0;
+      const uint32_t bytes = (cs.two ? 2u : 1u) * P.xbox_bytes + P.ybox_bytes;
+      for (int s = 0; s < cs.nst; ++s) {
+        mbar_wait(&cs.empty[st], ph ^ 1u);
+        double* pa = smem + (size_t)st * P.stage_doubles;
+        double* pb = pa + (size_t)BK * P.ld;
+        double* ys = pa + P.ys_off;
+        const int rr = (int)(cs.r0 + (int64_t)s * BK);
+        if (lane == 0) {
+          asm volatile("mbarrier.expect_tx.relaxed.cta.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(&cs.full[st])),
+                       "r"(bytes)
+                       : "memory");
+          if (MODE == MODE_FOLD) {
+            tma_load_3d(pa, &tmX, &cs.full[st], cs.a0, cs.kprime, rr);
+            if (cs.two) tma_load_3d(pb, &tmX, &cs.full[st], cs.b0, cs.kprime, rr);
+            if (P.ytma) tma_load_2d(ys, &tmY, &cs.full[st], 0, rr);
+          } else {
+            tma_load_2d(pa, &tmX, &cs.full[st], cs.a0, rr);
+            if (cs.two) tma_load_2d(pb, &tmX, &cs.full[st], cs.b0, rr);
+            if (P.ytma) tma_load_1d(ys, &tmY, &cs.full[st], rr);
+          }
+        }
+        if (!P.ytma) {  // odd-K folds: strided y through the producer's lanes
+          const int64_t row = (int64_t)rr + lane;
+          double yv = 0.0;
+          if (row < cs.r1) yv = P.y[row * P.K + cs.kprime];
+          ys[lane * P.ystride + cs.kprime] = yv;
+        }
+        mbar_arrive(&cs.full[st]);
+        if (++st == P.ST) { st = 0; ph ^= 1u; }
+      }
+    }
+    return;
+  }
+  // -------------------------------------------------------------- consumer warps
+  cs.warp = warp;
+  cs.lane = lane;
+  cs.job = cd->job[warp];
+  if (MODE != MODE_WEIGHTED && cs.job.kind == J_NONE) return;
+  switch (cs.job.kind) {
+    case J_F44: consume<MODE, J_F44>(P, cs); break;
+    case J_T4: consume<MODE, J_T4>(P, cs); break;
+    case J_F41: consume<MODE, J_F41>(P, cs); break;
+    case J_F42: consume<MODE, J_F42>(P, cs); break;
+    case J_F43: consume<MODE, J_F43>(P, cs); break;
+    case J_T1: consume<MODE, J_T1>(P, cs); break;
+    case J_T2: consume<MODE, J_T2>(P, cs); break;
+    case J_T3: consume<MODE, J_T3>(P, cs); break;
+    case J_F48: if (TWO) consume<MODE, J_F48>(P, cs); break;
+    case J_T4F4: if (TWO) consume<MODE, J_T4F4>(P, cs); break;
+    default: consume<MODE, J_NONE>(P, cs); break;
   }
 }
 
@@ -328,11 +401,10 @@ __global__ void gram_unpack_kernel(const double* __restrict__ packed, int nfold,
 // ------------------------------------------------------------------ host side: plans
 struct GramPlan {
   int mode = 0, p = 0, nb = 0, ld = 0, two_panel = 0, U = 0, nseg = 0, ST = 0, nblk = 0;
-  int R = 4, C = 4, NW = 12;
   int64_t seg_rows = 0;
   size_t smem = 0;
-  uint32_t tma_bytes = 0;
-  int stage_doubles = 0;
+  int stage_doubles = 0, ys_off = 0, ystride = 1, ytma = 1;
+  uint32_t ybox_bytes = 0;
   std::vector<CtaDesc> ctas;
   CtaDesc* d_ctas = nullptr;
   int32_t* d_blk_of = nullptr;
@@ -344,46 +416,40 @@ struct GramPlan {
   }
 };
 
-static int popc(uint32_t x) { return __builtin_popcount(x); }
-
-// Assign rectangles to CTA types (longest-processing-time first), then order each CTA's
-// rectangles so the 4 SM sub-partitions (warp w -> SMSP w % 4) carry similar DMMA counts.
-static void pack_rects(std::vector<RectDesc>& rects, int NW, int a0, int b0, int same, std::vector<CtaDesc>& out) {
-  std::sort(rects.begin(), rects.end(), [](const RectDesc& x, const RectDesc& y) { return popc(x.mask) > popc(y.mask); });
-  const int U = std::max<int>(1, ((int)rects.size() + NW - 1) / NW);
-  std::vector<std::vector<RectDesc>> bins(U);
+// Spread jobs over CTA types (longest-processing-time first), then order each CTA's jobs so
+// the 4 SM sub-partitions (warp w -> SMSP w % 4) carry similar DMMA counts.
+static void pack_jobs(std::vector<Job>& jobs, int a0, int b0, int same, std::vector<CtaDesc>& out) {
+  std::sort(jobs.begin(), jobs.end(),
+            [](const Job& x, const Job& y) { return kind_cost(x.kind) > kind_cost(y.kind); });
+  const int U = std::max<int>(1, ((int)jobs.size() + NWC - 1) / NWC);
+  std::vector<std::vector<Job>> bins(U);
   std::vector<int> load(U, 0);
-  for (auto& r : rects) {
+  for (auto& j : jobs) {
     int best = -1;
     for (int b = 0; b < U; ++b)
-      if ((int)bins[b].size() < NW && (best < 0 || load[b] < load[best])) best = b;
-    bins[best].push_back(r);
-    load[best] += popc(r.mask);
+      if ((int)bins[b].size() < NWC && (best < 0 || load[b] < load[best])) best = b;
+    bins[best].push_back(j);
+    load[best] += kind_cost(j.kind);
   }
   for (auto& bin : bins) {
     CtaDesc cd;
     std::memset(&cd, 0, sizeof(cd));
     cd.a0 = a0; cd.b0 = b0; cd.same = same;
-    // SMSP balancing: LPT over 4 sub-partitions, slot w = sub + 4 * k
-    std::vector<std::vector<RectDesc>> sub(4);
+    std::vector<std::vector<Job>> sub(4);
     std::vector<int> sl(4, 0);
-    for (auto& r : bin) {  // bin is sorted by cost already
+    for (auto& j : bin) {  // already sorted by cost
       int best = -1;
       for (int q = 0; q < 4; ++q)
-        if ((int)sub[q].size() * 4 + q < NW && (best < 0 || sl[q] < sl[best])) best = q;
-      sub[best].push_back(r);
-      sl[best] += popc(r.mask);
+        if ((int)sub[q].size() * 4 + q < NWC && (best < 0 || sl[q] < sl[best])) best = q;
+      sub[best].push_back(j);
+      sl[best] += kind_cost(j.kind);
     }
-    int nrect = 0;
-    RectDesc empty_rect{0, 0, 0u, 0};
-    for (int w = 0; w < NW; ++w) cd.rect[w] = empty_rect;
+    // warp w runs slot w (SMSP w % 4); idle slots hold J_NONE and exit early
+    for (int w = 0; w < NWC; ++w) cd.job[w] = Job{0, 0, J_NONE, 0};
+    int nj = 0;
     for (int q = 0; q < 4; ++q)
-      for (size_t k = 0; k < sub[q].size(); ++k) {
-        int w = q + 4 * (int)k;
-        cd.rect[w] = sub[q][k];
-        nrect = std::max(nrect, w + 1);
-      }
-    cd.nrect = nrect;
+      for (size_t k = 0; k < sub[q].size(); ++k) { cd.job[q + 4 * k] = sub[q][k]; ++nj; }
+    cd.njob = nj;  // busy warps = arrivals per stage release
     out.push_back(cd);
   }
 }
@@ -392,12 +458,13 @@ static oem_status build_plan(oem_ctx* ctx, int mode, int p, int64_t nrows, int K
   pl.mode = mode;
   pl.p = p;
   const int Pa = p + 1;
-  pl.nb = (Pa + 7) / 8;
-  const int r8 = pl.nb * 8;
-  const bool single = (r8 + 4) <= 256;
+  const int nb_exact = (Pa + 7) / 8;
+  const bool single = (8 * nb_exact + 4) <= 256;
   if (mode == MODE_WEIGHTED && !single)
     OEM_FAIL(OEM_ERR_UNSUPPORTED, "oem_gram_weighted: p > 247 is not supported by the fused single-panel kernel");
   pl.two_panel = single ? 0 : 1;
+  // two-panel plans pad the block count to whole 128-column panels (zero columns, TMA fill)
+  pl.nb = single ? nb_exact : (nb_exact + 15) / 16 * 16;
   pl.nblk = pl.nb * (pl.nb + 1) / 2;
   std::vector<int32_t> blk_of((size_t)pl.nb * pl.nb, -1);
   std::vector<int2> coord(pl.nblk);
@@ -406,59 +473,67 @@ static oem_status build_plan(oem_ctx* ctx, int mode, int p, int64_t nrows, int K
     for (int bi = 0; bi < pl.nb; ++bi)
       for (int bj = bi; bj < pl.nb; ++bj) { blk_of[(size_t)bi * pl.nb + bj] = idx; coord[idx] = make_int2(bi, bj); ++idx; }
   }
-  auto mk_mask = [&](int bi0, int bj0, int R, int C) {
-    uint32_t m = 0;
-    for (int r = 0; r < R; ++r)
-      for (int c = 0; c < C; ++c) {
-        int bi = bi0 + r, bj = bj0 + c;
-        if (bi <= bj && bj < pl.nb) m |= 1u << (r * C + c);
-      }
-    return m;
-  };
   if (single) {
-    pl.R = 4; pl.C = 4; pl.NW = 12;
-    pl.ld = r8 + 4;  // = 4 or 12 (mod 16): conflict-free fragment loads
-    std::vector<RectDesc> rects;
+    pl.ld = 8 * pl.nb + 4;  // = 4 or 12 (mod 16): conflict-free fragment loads
+    std::vector<Job> jobs;
     for (int bi0 = 0; bi0 < pl.nb; bi0 += 4)
       for (int bj0 = bi0; bj0 < pl.nb; bj0 += 4) {
-        uint32_t m = mk_mask(bi0, bj0, 4, 4);
-        if (m) rects.push_back(RectDesc{bi0, bj0, m, 0});
+        const int Rr = std::min(4, pl.nb - bi0), Cc = std::min(4, pl.nb - bj0);
+        int kind;
+        if (bi0 == bj0) kind = Rr == 4 ? J_T4 : Rr == 3 ? J_T3 : Rr == 2 ? J_T2 : J_T1;
+        else kind = Cc == 4 ? J_F44 : Cc == 3 ? J_F43 : Cc == 2 ? J_F42 : J_F41;
+        jobs.push_back(Job{bi0, bj0, kind, 0});
       }
-    pack_rects(rects, pl.NW, 0, 0, 1, pl.ctas);
+    pack_jobs(jobs, 0, 0, 1, pl.ctas);
   } else {
-    pl.R = 4; pl.C = 8; pl.NW = 8;
     pl.ld = 132;  // 128-column panel + 4 (mod 16 = 4)
-    const int np = (Pa + 127) / 128;
+    const int np = pl.nb / 16;
     for (int I = 0; I < np; ++I)
       for (int J = I; J < np; ++J) {
-        std::vector<RectDesc> rects;
+        std::vector<Job> jobs;
         for (int r = 0; r < 4; ++r)
           for (int c = 0; c < 2; ++c) {
-            int bi0 = 16 * I + 4 * r, bj0 = 16 * J + 8 * c;
-            uint32_t m = mk_mask(bi0, bj0, 4, 8);
-            if (m) rects.push_back(RectDesc{bi0, bj0, m, 0});
+            const int bi0 = 16 * I + 4 * r, bj0 = 16 * J + 8 * c;
+            if (I < J) { jobs.push_back(Job{bi0, bj0, J_F48, 0}); continue; }
+            const int lr = 4 * r, lc = 8 * c;  // local block coordinates on a diagonal tile
+            if (lc >= lr + 4) jobs.push_back(Job{bi0, bj0, J_F48, 0});
+            else if (lc == lr) jobs.push_back(Job{bi0, bj0, J_T4F4, 0});
+            else if (lc + 4 == lr) jobs.push_back(Job{bi0, bj0 + 4, J_T4, 0});
           }
-        if (rects.empty()) continue;
-        pack_rects(rects, pl.NW, 128 * I, 128 * J, I == J, pl.ctas);
+        pack_jobs(jobs, 128 * I, 128 * J, I == J, pl.ctas);
       }
   }
   pl.U = (int)pl.ctas.size();
+  // y staging: 1D TMA box (PLAIN/WEIGHTED); FOLD: 2D box [BK][Kpad] over y viewed as [nq][K]
+  // (needs K*8 % 16 == 0, i.e. even K), else the producer's lanes load it
+  if (mode == MODE_FOLD) {
+    pl.ytma = (K % 2 == 0) && K <= 256;
+    pl.ystride = pl.ytma ? K : K;  // smem row stride of ys in doubles
+  } else {
+    pl.ytma = 1;
+    pl.ystride = 1;
+  }
+  pl.ybox_bytes = pl.ytma ? (uint32_t)(BK * pl.ystride * 8) : 0;
   const int panels = pl.two_panel ? 2 : 1;
-  pl.stage_doubles = panels * BK * pl.ld + BK * (mode == MODE_WEIGHTED ? 2 : 1);
+  pl.ys_off = panels * BK * pl.ld;
+  pl.stage_doubles = pl.ys_off + BK * pl.ystride + (mode == MODE_WEIGHTED ? BK : 0);
   pl.stage_doubles = (pl.stage_doubles + 15) / 16 * 16;  // 128-byte aligned stages
-  const size_t budget = 220 * 1024;
   const size_t fixed = (mode == MODE_WEIGHTED ? pl.ld * 8 : 0) + 2 * MAXST * 8;
-  pl.ST = (int)std::min<size_t>(4, (budget - fixed) / ((size_t)pl.stage_doubles * 8));
+  // two CTAs per SM for single-panel plans when at least 3 stages fit in half the SM
+  const size_t half = 110 * 1024, whole = 220 * 1024;
+  int st_half = (int)std::min<size_t>(4, (half - fixed) / ((size_t)pl.stage_doubles * 8));
+  const bool two_per_sm = !pl.two_panel && mode != MODE_WEIGHTED && st_half >= 3;
+  pl.ST = two_per_sm ? st_half : (int)std::min<size_t>(4, (whole - fixed) / ((size_t)pl.stage_doubles * 8));
   if (pl.ST < 2) OEM_FAIL(OEM_ERR_UNSUPPORTED, "gram: stage does not fit shared memory");
   pl.smem = (size_t)pl.ST * pl.stage_doubles * 8 + fixed;
-  // segments: enough (CTA type, segment) items for several waves over the SMs
-  const int64_t units = std::max<int64_t>(1, (nrows + BK - 1) / BK);  // BK-row units
+  // segments: enough (CTA type, segment) items for ~4 waves over the SMs
+  const int64_t units = std::max<int64_t>(1, (nrows + BK - 1) / BK);
   const int nfold = mode == MODE_FOLD ? K : 1;
-  int64_t want = (int64_t)ctx->num_sms * 4 / std::max(1, pl.U * nfold);
-  want = std::max<int64_t>(1, std::min<int64_t>(want, units / 4 > 0 ? units / 4 : 1));
+  const int per_sm = two_per_sm ? 2 : 1;
+  int64_t want = (int64_t)ctx->num_sms * per_sm * 4 / std::max(1, pl.U * nfold);
+  want = std::max<int64_t>(1, std::min<int64_t>(want, std::max<int64_t>(1, units / 8)));
   pl.seg_rows = ((units + want - 1) / want) * BK;
   pl.nseg = (int)std::max<int64_t>(1, (nrows + pl.seg_rows - 1) / pl.seg_rows);
-  // device tables
   cudaError_t e;
   if ((e = cudaMalloc(&pl.d_ctas, sizeof(CtaDesc) * pl.ctas.size())) != cudaSuccess ||
       (e = cudaMemcpy(pl.d_ctas, pl.ctas.data(), sizeof(CtaDesc) * pl.ctas.size(), cudaMemcpyHostToDevice)) != cudaSuccess ||
@@ -494,20 +569,30 @@ static oem_status make_map(CUtensorMap* map, const double* X, int rank, const cu
   CUresult r = enc(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, rank, const_cast<double*>(X), dims, strides_bytes, box, estr,
                    CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
                    CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
-  if (r != CUDA_SUCCESS) OEM_FAIL(OEM_ERR_CUDA, "cuTensorMapEncodeTiled failed (code " + std::to_string((int)r) + ")");
+  if (r != CUDA_SUCCESS) {
+    std::string d = "cuTensorMapEncodeTiled failed (code " + std::to_string((int)r) + ") rank " + std::to_string(rank) +
+                    " addr%16=" + std::to_string((uintptr_t)X % 16) + " dims";
+    for (int i = 0; i < rank; ++i) d += " " + std::to_string((unsigned long long)dims[i]);
+    d += " box";
+    for (int i = 0; i < rank; ++i) d += " " + std::to_string(box[i]);
+    d += " strides";
+    for (int i = 0; i + 1 < rank; ++i) d += " " + std::to_string((unsigned long long)strides_bytes[i]);
+    OEM_FAIL(OEM_ERR_CUDA, d);
+  }
   return OEM_OK;
 }
 
-template <int R, int C, int NW, int MODE>
-static oem_status launch_t(const GramPlan& pl, const CUtensorMap& map, const GramParams& P, int nfold, cudaStream_t st) {
-  auto kern = gram_kernel<R, C, NW, MODE>;
+template <int MODE, bool TWO>
+static oem_status launch_t(const GramPlan& pl, const CUtensorMap& mx, const CUtensorMap& my, const GramParams& P,
+                           int nfold, cudaStream_t st) {
+  auto kern = gram_kernel<MODE, TWO>;
   static size_t attr_smem = 0;  // opt-in dynamic shared memory, raised on demand
   if (pl.smem > attr_smem) {
     OEM_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)pl.smem));
     attr_smem = pl.smem;
   }
   dim3 grid((unsigned)(pl.U * pl.nseg * nfold));
-  kern<<<grid, (NW + 1) * 32, pl.smem, st>>>(map, P);
+  kern<<<grid, (NWC + 1) * 32, pl.smem, st>>>(mx, my, P);
   OEM_CUDA_TRY(cudaGetLastError());
   return OEM_OK;
 }
@@ -518,7 +603,6 @@ oem_status gram_pass(oem_ctx* ctx, int mode, const double* X, const double* y, c
   const int64_t psize = packed_size(p);
   const int64_t nq = mode == MODE_FOLD ? n_local / K : n_local;
   if (n_local == 0 || nq == 0) {
-    // nothing to stream through the tensor-core kernel
     OEM_CUDA_TRY(cudaMemsetAsync(packed, 0, sizeof(double) * (nfold * psize + (mode == MODE_WEIGHTED ? 2 : 0)), st));
     if (mode != MODE_FOLD || n_local == 0) return OEM_OK;
   }
@@ -533,7 +617,6 @@ oem_status gram_pass(oem_ctx* ctx, int mode, const double* X, const double* y, c
     ctx->plans[key] = plp;
   }
   const GramPlan& pl = *plp;
-  // workspace
   const size_t part_bytes = sizeof(double) * (size_t)nfold * pl.nseg * pl.nblk * 64;
   OEM_CUDA_TRY(ctx->partial.ensure(part_bytes));
   OEM_CUDA_TRY(ctx->partial_scal.ensure(sizeof(double) * 2 * (size_t)pl.nseg + 16));
@@ -543,19 +626,32 @@ oem_status gram_pass(oem_ctx* ctx, int mode, const double* X, const double* y, c
     tail = ctx->tail.as<double>();
   }
   if (nq > 0) {
-    CUtensorMap map;
+    CUtensorMap mx, my;
+    std::memset(&my, 0, sizeof(my));
     const cuuint32_t boxw = (cuuint32_t)pl.ld;
     oem_status s;
     if (mode == MODE_FOLD) {
       cuuint64_t dims[3] = {(cuuint64_t)p, (cuuint64_t)K, (cuuint64_t)nq};
       cuuint64_t strides[2] = {(cuuint64_t)ldx * 8, (cuuint64_t)ldx * 8 * K};
       cuuint32_t box[3] = {boxw, 1, (cuuint32_t)BK};
-      s = make_map(&map, X, 3, dims, strides, box);
+      s = make_map(&mx, X, 3, dims, strides, box);
+      if (s == OEM_OK && pl.ytma) {
+        cuuint64_t yd[2] = {(cuuint64_t)K, (cuuint64_t)nq};
+        cuuint64_t ys[1] = {(cuuint64_t)K * 8};
+        cuuint32_t yb[2] = {(cuuint32_t)K, (cuuint32_t)BK};
+        s = make_map(&my, y, 2, yd, ys, yb);
+      }
     } else {
       cuuint64_t dims[2] = {(cuuint64_t)p, (cuuint64_t)n_local};
       cuuint64_t strides[1] = {(cuuint64_t)ldx * 8};
       cuuint32_t box[2] = {boxw, (cuuint32_t)BK};
-      s = make_map(&map, X, 2, dims, strides, box);
+      s = make_map(&mx, X, 2, dims, strides, box);
+      if (s == OEM_OK) {
+        cuuint64_t yd[1] = {(cuuint64_t)n_local};
+        cuuint32_t yb[1] = {(cuuint32_t)BK};
+        cuuint64_t ydummy[1] = {(cuuint64_t)n_local * 8};  // rank 1: strides unused but must be non-null
+        s = make_map(&my, y, 1, yd, ydummy, yb);
+      }
     }
     if (s != OEM_OK) return s;
     GramParams P;
@@ -563,24 +659,31 @@ oem_status gram_pass(oem_ctx* ctx, int mode, const double* X, const double* y, c
     P.p = p; P.nb = pl.nb; P.ld = pl.ld; P.U = pl.U; P.nseg = pl.nseg; P.ST = pl.ST; P.two_panel = pl.two_panel;
     P.nblk = pl.nblk; P.nrows = nq; P.seg_rows = pl.seg_rows; P.K = K;
     P.off_mod = mode == MODE_FOLD ? (int)(((row_offset % K) + K) % K) : 0;
+    P.ytma = pl.ytma; P.ystride = pl.ystride;
     P.y = y; P.beta = beta; P.eps = eps;
     P.partial = ctx->partial.as<double>();
     P.partial_scal = ctx->partial_scal.as<double>();
     P.ctas = pl.d_ctas; P.blk_of = pl.d_blk_of;
-    P.tma_bytes = (uint32_t)(BK * pl.ld * 8);  // bytes of one box; off-diagonal tiles load two
+    P.xbox_bytes = (uint32_t)(BK * pl.ld * 8);
+    P.ybox_bytes = pl.ybox_bytes;
     P.stage_doubles = pl.stage_doubles;
+    P.ys_off = pl.ys_off;
     oem_status ls;
+    PhaseTimer tm(ctx, PH_GRAM, st);
+    ++ctx->launches;
     if (!pl.two_panel) {
-      if (mode == MODE_PLAIN) ls = launch_t<4, 4, 12, MODE_PLAIN>(pl, map, P, nfold, st);
-      else if (mode == MODE_FOLD) ls = launch_t<4, 4, 12, MODE_FOLD>(pl, map, P, nfold, st);
-      else ls = launch_t<4, 4, 12, MODE_WEIGHTED>(pl, map, P, nfold, st);
+      if (mode == MODE_PLAIN) ls = launch_t<MODE_PLAIN, false>(pl, mx, my, P, nfold, st);
+      else if (mode == MODE_FOLD) ls = launch_t<MODE_FOLD, false>(pl, mx, my, P, nfold, st);
+      else ls = launch_t<MODE_WEIGHTED, false>(pl, mx, my, P, nfold, st);
     } else {
-      if (mode == MODE_PLAIN) ls = launch_t<4, 8, 8, MODE_PLAIN>(pl, map, P, nfold, st);
-      else ls = launch_t<4, 8, 8, MODE_FOLD>(pl, map, P, nfold, st);
+      if (mode == MODE_PLAIN) ls = launch_t<MODE_PLAIN, true>(pl, mx, my, P, nfold, st);
+      else ls = launch_t<MODE_FOLD, true>(pl, mx, my, P, nfold, st);
     }
     if (ls != OEM_OK) return ls;
   }
+  PhaseTimer tm_red(ctx, PH_REDUCE, st);
   if (tail) {
+    ++ctx->launches;
     gram_fold_tail_kernel<<<std::max(1, std::min(1024, (int)((K * (int64_t)pl.nblk * 64 + 255) / 256))), 256, 0, st>>>(
         X, y, ldx, n_local, nq, K, (int)(((row_offset % K) + K) % K), p, pl.nblk, pl.d_blk_coord, tail);
     OEM_CUDA_TRY(cudaGetLastError());
@@ -588,6 +691,7 @@ oem_status gram_pass(oem_ctx* ctx, int mode, const double* X, const double* y, c
   {
     const int64_t total = (int64_t)nfold * pl.nblk * 64;
     const int blocks = (int)std::max<int64_t>(1, std::min<int64_t>(ctx->num_sms * 8, (total + 255) / 256));
+    ++ctx->launches;
     gram_reduce_kernel<<<blocks, 256, 0, st>>>(ctx->partial.as<double>(), nfold, nq > 0 ? pl.nseg : 0, pl.nblk,
                                                pl.d_blk_coord, p, tail, packed, psize, ctx->partial_scal.as<double>(),
                                                mode == MODE_WEIGHTED);
@@ -596,7 +700,10 @@ oem_status gram_pass(oem_ctx* ctx, int mode, const double* X, const double* y, c
   return OEM_OK;
 }
 
-oem_status gram_unpack(const double* packed, int nfold, int p, double* G, double* xty, double* yty, cudaStream_t st) {
+oem_status gram_unpack(oem_ctx* ctx, const double* packed, int nfold, int p, double* G, double* xty, double* yty,
+                       cudaStream_t st) {
+  PhaseTimer tm(ctx, PH_REDUCE, st);
+  ++ctx->launches;
   const int64_t total = (int64_t)nfold * ((int64_t)p * p + p + 1);
   const int blocks = (int)std::max<int64_t>(1, std::min<int64_t>(4096, (total + 255) / 256));
   gram_unpack_kernel<<<blocks, 256, 0, st>>>(packed, nfold, p, G, xty, yty);

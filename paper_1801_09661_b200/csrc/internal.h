@@ -41,16 +41,51 @@ struct GramPlan;  // gram.cu
 
 }  // namespace oem
 
+namespace oem {
+enum Phase { PH_GRAM = 0, PH_REDUCE = 1, PH_ALLREDUCE = 2, PH_POWER = 3, PH_PATH = 4, PH_NPHASE = 5 };
+}
+
 struct oem_ctx {
   int device = 0;
   int nranks = 1, rank = 0;
   int num_sms = 148;
   void* nccl_comm = nullptr;  // ncclComm_t
-  oem::DevBuf partial, partial_scal, packed, tail, plan_tables, path_ws, path_small;
+  oem::DevBuf partial, partial_scal, packed, tail, plan_tables, path_ws, path_small, logi;
   std::map<std::tuple<int, int, int64_t, int>, std::shared_ptr<oem::GramPlan>> plans;
+  // instrumentation (oem_ctx_set_timing / oem_ctx_stats)
+  bool timing = false;
+  int64_t launches = 0;
+  double phase_ms[oem::PH_NPHASE] = {0, 0, 0, 0, 0};
+  struct Pending { int phase; cudaEvent_t a, b; };
+  std::vector<Pending> pending;
+  std::vector<cudaEvent_t> event_pool;
 };
 
 namespace oem {
+
+// Records CUDA events around a phase on the launching stream when timing is enabled.
+struct PhaseTimer {
+  oem_ctx* ctx;
+  int phase;
+  cudaStream_t st;
+  cudaEvent_t a = nullptr;
+  PhaseTimer(oem_ctx* c, int ph, cudaStream_t s) : ctx(c), phase(ph), st(s) {
+    if (ctx->timing) { a = take(); cudaEventRecord(a, st); }
+  }
+  ~PhaseTimer() {
+    if (a) {
+      cudaEvent_t b = take();
+      cudaEventRecord(b, st);
+      ctx->pending.push_back({phase, a, b});
+    }
+  }
+  cudaEvent_t take() {
+    if (!ctx->event_pool.empty()) { cudaEvent_t e = ctx->event_pool.back(); ctx->event_pool.pop_back(); return e; }
+    cudaEvent_t e;
+    cudaEventCreate(&e);
+    return e;
+  }
+};
 
 enum GramMode { MODE_PLAIN = 0, MODE_FOLD = 1, MODE_WEIGHTED = 2 };
 
@@ -61,7 +96,7 @@ oem_status gram_pass(oem_ctx* ctx, int mode, const double* X, const double* y, c
                      int64_t n_local, int p, int64_t ldx, int64_t row_offset, int K, double* packed,
                      cudaStream_t st);
 // packed (nfold blocks) -> full symmetric G (nfold*p*p), xty (nfold*p), yty (nfold)
-oem_status gram_unpack(const double* packed, int nfold, int p, double* G, double* xty, double* yty, cudaStream_t st);
+oem_status gram_unpack(oem_ctx* ctx, const double* packed, int nfold, int p, double* G, double* xty, double* yty, cudaStream_t st);
 inline int64_t packed_size(int p) { return (int64_t)(p + 1) * (p + 2) / 2; }
 
 oem_status allreduce_sum(oem_ctx* ctx, double* buf, size_t count, cudaStream_t st);

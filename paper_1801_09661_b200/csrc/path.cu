@@ -22,7 +22,8 @@
 #include <numeric>
 #include <vector>
 
-#include <cooperative_groups.h>
+#include <cstdlib>
+#include <string>
 
 #include "common.cuh"
 #include "internal.h"
@@ -531,6 +532,492 @@ __global__ void __launch_bounds__(PT, 1) path_kernel(const PathParams P) {
   }
 }
 
+// ---------------------------------------------------------------- K4+K5 fused: the cluster solver
+// One thread-block cluster per unit Gram (C <= 16 CTAs, one per SM). CTA `rank` owns rows
+// [j0, j1) of the unit's normalised Gram; each thread keeps its share of those rows in
+// registers (first EREG elements) and shared memory (the rest, thread-major so warp reads are
+// conflict free) for the whole launch: d by power iteration (R#5), the lambda grid (R#14-15) and
+// the OEM paths all run from on-chip copies of G.
+// Per iteration every CTA pushes its rows of the new beta (and its partial max |dbeta|) into the
+// shared memory of every CTA of the cluster (DSMEM stores), then the cluster meets at one
+// hardware barrier (barrier.cluster arrive.release / wait.acquire). beta and the partials are
+// double-buffered by iteration parity, so no CTA overwrites data another may still read.
+struct ClusterArgs {
+  int C;          // CTAs per cluster (= per unit)
+  int T;          // lanes per row
+  int RG;         // row groups per CTA (= threads / T)
+  int KPR;        // columns per thread per row = ceil(p / T)
+  int NRT;        // rows per thread = ceil(max rows / RG)
+  int S;          // shared-memory G slots per thread
+  int pv;         // padded vector length (>= p)
+  int power_iters;
+  double inflate;
+  int compute_d;
+  int maxrows;    // max rows per CTA (shared-memory row tables)
+  double* d_out;  // [nU]
+};
+
+__device__ __forceinline__ void cluster_sync_all() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+__device__ __forceinline__ uint32_t cluster_rank() {
+  uint32_t r;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+  return r;
+}
+// store a double into the shared memory of CTA `rank` of this cluster, at the address that
+// `local` has in the calling CTA
+__device__ __forceinline__ void st_cluster(double* local, uint32_t rank, double v) {
+  if (gridDim.x == 0) return;  // (never) keeps the signature uniform for C == 1 callers
+  uint32_t a = smem_u32(local), ra;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(ra) : "r"(a), "r"(rank));
+  asm volatile("st.shared::cluster.f64 [%0], %1;" ::"r"(ra), "d"(v) : "memory");
+}
+
+template <int NPT, int EREG>
+__global__ void __launch_bounds__(PT, 1) fit_cluster_kernel(const PathParams P, const ClusterArgs A) {
+  extern __shared__ __align__(16) double sm[];
+  const int p = P.p, nP = P.nP, L = P.L, C = A.C, T = A.T, RG = A.RG, KPR = A.KPR, NRT = A.NRT;
+  const int tid = threadIdx.x, rg = tid / T, tl = tid % T;
+  const int rank = (int)cluster_rank();
+  const int unit = blockIdx.x / C;
+  const int cta = blockIdx.x;
+  const int j0 = P.cta_j0[cta], j1 = P.cta_j1[cta], nr = j1 - j0;
+  const double* Gu = P.Gn + (size_t)unit * p * p;
+  const double* c = P.cn + (size_t)unit * p;
+  // shared memory: G slots [S][PT] | vec [2][NPT][pv] | dl [2][C][NPT+2] | red [32][NPT+1] | uv [NPT][nr]
+  double* gsm = sm;
+  double* vec = gsm + (size_t)A.S * PT;
+  double* dl = vec + (size_t)2 * NPT * A.pv;
+  double* red = dl + (size_t)2 * C * (NPT + 2);
+  double* uv = red + 32 * (NPT + 1);
+  // per-row / per-group constants staged once: global loads after a cluster barrier miss L1
+  double* c_s = uv + (size_t)NPT * A.maxrows;       // c_j, own rows
+  double* w_s = c_s + A.maxrows;                     // var_w_j, own rows
+  double* gw_s = w_s + A.maxrows;                    // group weights, local groups
+  int* ga_s = reinterpret_cast<int*>(gw_s + A.maxrows);  // group start - j0
+  int* gb_s = ga_s + A.maxrows;                          // group end - j0
+  for (int r = tid; r < nr; r += PT) {
+    c_s[r] = c[j0 + r];
+    w_s[r] = P.var_w ? P.var_w[j0 + r] : 1.0;
+  }
+  const int g0 = (P.g_of && nr > 0) ? P.g_of[j0] : 0;
+  const int ng_loc = (P.g_of && nr > 0) ? P.g_of[j1 - 1] + 1 - g0 : 0;
+  for (int g = tid; g < ng_loc; g += PT) {
+    gw_s[g] = P.g_w[g0 + g];
+    ga_s[g] = P.g_start[g0 + g] - j0;
+    gb_s[g] = P.g_end[g0 + g] - j0;
+  }
+  int famq[NPT];
+  double gamq[NPT], alpq[NPT];
+#pragma unroll
+  for (int q = 0; q < NPT; ++q) {
+    famq[q] = q < nP ? P.fam[q] : 0;
+    gamq[q] = q < nP ? P.gam[q] : 0.0;
+    alpq[q] = q < nP ? P.alp[q] : 0.0;
+  }
+  // ---- this thread's share of G: rows r = rg + ri*RG, columns k = tl + ci*T
+  double greg[EREG];
+#pragma unroll
+  for (int e = 0; e < EREG; ++e) {
+    const int r = rg, k = tl + e * T;
+    greg[e] = (e < KPR && r < nr && k < p) ? Gu[(size_t)(j0 + r) * p + k] : 0.0;
+  }
+  for (int ri = 0; ri < NRT; ++ri)
+    for (int ci = (ri == 0 ? EREG : 0); ci < KPR; ++ci) {
+      const int slot = (ri == 0) ? ci - EREG : (KPR > EREG ? KPR - EREG : 0) + (ri - 1) * KPR + ci;
+      const int r = rg + ri * RG, k = tl + ci * T;
+      gsm[(size_t)slot * PT + tid] = (r < nr && k < p) ? Gu[(size_t)(j0 + r) * p + k] : 0.0;
+    }
+  // row-dot of this thread's elements against vector v (one penalty): partial sum
+  auto rowdot = [&](int ri, const double* v) -> double {
+    double a = 0.0;
+    if (ri == 0) {
+#pragma unroll
+      for (int e = 0; e < EREG; ++e)
+        if (e < KPR) a = fma(greg[e], v[tl + e * T], a);
+      for (int ci = EREG; ci < KPR; ++ci) a = fma(gsm[(size_t)(ci - EREG) * PT + tid], v[tl + ci * T], a);
+    } else {
+      const int base = (KPR > EREG ? KPR - EREG : 0) + (ri - 1) * KPR;
+      for (int ci = 0; ci < KPR; ++ci) a = fma(gsm[(size_t)(base + ci) * PT + tid], v[tl + ci * T], a);
+    }
+    return a;
+  };
+  auto reduce_T = [&](double a) -> double {
+    for (int o = T >> 1; o > 0; o >>= 1) a += __shfl_xor_sync(0xffffffffu, a, o, T);
+    return a;
+  };
+  const int warp = tid >> 5, lane = tid & 31, nwarps = PT / 32;
+
+  // ======================================================= a7: d by power iteration (R#5)
+  double d;
+  if (A.compute_d) {
+    const double v0 = 1.0 / sqrt((double)p);
+    for (int k = tid; k < A.pv; k += PT) vec[k] = k < p ? v0 : 0.0;
+    // Gershgorin: max row sum of |G| over this CTA's rows
+    double gm = 0.0;
+    for (int ri = 0; ri < NRT; ++ri) {
+      double a = 0.0;
+      if (ri == 0) {
+#pragma unroll
+        for (int e = 0; e < EREG; ++e) a += fabs(greg[e]);
+        for (int ci = EREG; ci < KPR; ++ci) a += fabs(gsm[(size_t)(ci - EREG) * PT + tid]);
+      } else {
+        const int base = (KPR > EREG ? KPR - EREG : 0) + (ri - 1) * KPR;
+        for (int ci = 0; ci < KPR; ++ci) a += fabs(gsm[(size_t)(base + ci) * PT + tid]);
+      }
+      gm = fmax(gm, reduce_T(a));
+    }
+    for (int o = 16; o > 0; o >>= 1) gm = fmax(gm, __shfl_xor_sync(0xffffffffu, gm, o));
+    if (lane == 0) red[warp] = gm;
+    __syncthreads();
+    if (tid == 0) {
+      double m = 0.0;
+      for (int w = 0; w < nwarps; ++w) m = fmax(m, red[w]);
+      for (int r = 0; r < C; ++r) st_cluster(&dl[(size_t)(0 * C + rank) * (NPT + 2) + NPT + 1], r, m);
+    }
+    double rq = 0.0, gersh = 0.0;
+    for (int it = 0; it <= A.power_iters; ++it) {
+      const int cur = it & 1, nxt = cur ^ 1;
+      const double* v = vec + (size_t)cur * NPT * A.pv;
+      double part = 0.0;
+      for (int ri = 0; ri < NRT; ++ri) {
+        const double w = reduce_T(rowdot(ri, v));
+        const int r = rg + ri * RG;
+        if (tl == 0 && r < nr) {
+          const int j = j0 + r;
+          if (it < A.power_iters) {
+            part += w * w;
+            if (C == 1) vec[(size_t)nxt * NPT * A.pv + j] = w;
+            else for (int q = 0; q < C; ++q) st_cluster(&vec[(size_t)nxt * NPT * A.pv + j], q, w);
+          } else {
+            part += v[j] * w;  // Rayleigh quotient partial
+          }
+        }
+      }
+      for (int o = 16; o > 0; o >>= 1) part += __shfl_xor_sync(0xffffffffu, part, o);
+      if (lane == 0) red[warp] = part;
+      __syncthreads();
+      if (tid == 0) {
+        double s = 0.0;
+        for (int w = 0; w < nwarps; ++w) s += red[w];  // fixed order
+        for (int r = 0; r < C; ++r) st_cluster(&dl[(size_t)(cur * C + rank) * (NPT + 2)], r, s);
+      }
+      cluster_sync_all();
+      double tot = 0.0;
+      for (int r = 0; r < C; ++r) tot += dl[(size_t)(cur * C + r) * (NPT + 2)];
+      if (it == 0) {
+        for (int r = 0; r < C; ++r) gersh = fmax(gersh, dl[(size_t)(0 * C + r) * (NPT + 2) + NPT + 1]);
+      }
+      if (it < A.power_iters) {
+        const double nrm = sqrt(tot);
+        double* vn = vec + (size_t)nxt * NPT * A.pv;
+        if (nrm > 0.0)
+          for (int k = tid; k < p; k += PT) vn[k] = vn[k] / nrm;
+        else
+          for (int k = tid; k < p; k += PT) vn[k] = v[k];
+        __syncthreads();
+      } else {
+        rq = tot;
+      }
+    }
+    const double dd = (1.0 + A.inflate) * rq;
+    d = gersh < dd ? gersh : dd;
+    if (rank == 0 && tid == 0) A.d_out[unit] = d;
+    cluster_sync_all();  // everyone is done with vec / dl before the path reuses them
+  } else {
+    d = P.d[unit];
+  }
+
+  // ======================================================= a8: lambda grid (R#14-16, R#22)
+  double lmax[NPT], lam[NPT];
+  int lidx[NPT];
+  int itc[NPT];
+#pragma unroll
+  for (int q = 0; q < NPT; ++q) {
+    lmax[q] = 0.0;
+    lidx[q] = L;
+    itc[q] = 0;
+    lam[q] = 0.0;
+    if (q >= nP) continue;
+    const int fam = P.fam[q];
+    const double* cc = P.shared_grid ? P.cn : c;
+    double lm = 0.0;
+    if (P.lmax_override) {
+      lm = *P.lmax_override;
+    } else if (fam >= OEM_GRP_LASSO) {
+      for (int g = 0; g < P.ngroups; ++g) {
+        const double cg = P.g_w[g];
+        if (!(cg > 0.0)) continue;
+        double s = 0.0;
+        for (int j = P.g_start[g]; j < P.g_end[g]; ++j) s += cc[j] * cc[j];
+        lm = fmax(lm, sqrt(s) / cg);
+      }
+    } else {
+      const double sc = fam == OEM_ENET ? P.alp[q] : 1.0;
+      for (int j = 0; j < p; ++j) {
+        const double wj = P.var_w ? P.var_w[j] : 1.0;
+        if (!(wj > 0.0)) continue;
+        lm = fmax(lm, fabs(cc[j]) / (sc * wj));
+      }
+    }
+    lmax[q] = lm;
+    // parameter validity against the d in use (R#8)
+    const double g = P.gam[q];
+    bool bad = false;
+    if (fam == OEM_MCP || fam == OEM_GRP_MCP) bad = !(g > 1.0) || !(g * d > 1.0);
+    if (fam == OEM_SCAD || fam == OEM_GRP_SCAD) bad = !(g > 2.0) || !((g - 1.0) * d > 1.0);
+    if (fam == OEM_ENET) bad = !(P.alp[q] >= 0.0 && P.alp[q] <= 1.0);
+    if (bad) {
+      if (tid == 0) atomicExch(&P.flags[1], 1);
+      continue;
+    }
+    lidx[q] = 0;
+    lam[q] = P.lam_explicit ? P.lam_explicit[0] : lm;
+    if (rank == 0)
+      for (int l = tid; l < L; l += PT)
+        P.lam_out[((size_t)unit * nP + q) * L + l] =
+            P.lam_explicit ? P.lam_explicit[l]
+                           : (L == 1 ? lm : lm * exp(((double)l / (double)(L - 1)) * log(P.lmin_ratio)));
+  }
+  // warm or cold start (permuted order), both parity buffers hold beta^(0) in slot 0
+  for (int q = 0; q < NPT; ++q)
+    for (int k = tid; k < A.pv; k += PT)
+      vec[(size_t)q * A.pv + k] =
+          (q < nP && k < p && P.beta_init) ? P.beta_init[((size_t)unit * nP + q) * p + P.perm[k]] : 0.0;
+  __syncthreads();
+  const bool grp = P.g_of != nullptr;
+
+  // ======================================================= a9: OEM iterations
+  for (int t = 0;; ++t) {
+    uint32_t qmask = 0;
+#pragma unroll
+    for (int q = 0; q < NPT; ++q)
+      if (q < nP && lidx[q] < L) qmask |= 1u << q;
+    if (!qmask) break;
+    const int cur = t & 1, nxt = cur ^ 1;
+    const double* vc = vec + (size_t)cur * NPT * A.pv;
+    double* vn = vec + (size_t)nxt * NPT * A.pv;
+    double dmax[NPT];
+    bool bad = false;
+#pragma unroll
+    for (int q = 0; q < NPT; ++q) dmax[q] = 0.0;
+    // ---- E-step + M-step: u = c + d beta - G beta for this CTA's rows
+    for (int ri = 0; ri < NRT; ++ri) {
+      double acc[NPT];
+#pragma unroll
+      for (int q = 0; q < NPT; ++q) acc[q] = 0.0;
+      if (ri == 0) {
+#pragma unroll
+        for (int e = 0; e < EREG; ++e) {
+          if (e < KPR) {
+            const int k = tl + e * T;
+#pragma unroll
+            for (int q = 0; q < NPT; ++q)
+              if ((qmask >> q) & 1u) acc[q] = fma(greg[e], vc[q * A.pv + k], acc[q]);
+          }
+        }
+        for (int ci = EREG; ci < KPR; ++ci) {
+          const double g = gsm[(size_t)(ci - EREG) * PT + tid];
+          const int k = tl + ci * T;
+#pragma unroll
+          for (int q = 0; q < NPT; ++q)
+            if ((qmask >> q) & 1u) acc[q] = fma(g, vc[q * A.pv + k], acc[q]);
+        }
+      } else {
+        const int base = (KPR > EREG ? KPR - EREG : 0) + (ri - 1) * KPR;
+        for (int ci = 0; ci < KPR; ++ci) {
+          const double g = gsm[(size_t)(base + ci) * PT + tid];
+          const int k = tl + ci * T;
+#pragma unroll
+          for (int q = 0; q < NPT; ++q)
+            if ((qmask >> q) & 1u) acc[q] = fma(g, vc[q * A.pv + k], acc[q]);
+        }
+      }
+      const int r = rg + ri * RG;
+#pragma unroll
+      for (int q = 0; q < NPT; ++q) {
+        if (!((qmask >> q) & 1u)) continue;
+        const double a = reduce_T(acc[q]);
+        if (tl == 0 && r < nr) {
+          const int j = j0 + r;
+          const double bj = vc[q * A.pv + j];
+          const double u = c_s[r] + d * bj - a;
+          if (!isfinite(u)) bad = true;
+          if (!grp) {
+            const double nb = th_coord(famq[q], u, w_s[r] * lam[q], gamq[q], alpq[q], d);
+            dmax[q] = fmax(dmax[q], fabs(nb - bj));
+            if (C == 1) vn[q * A.pv + j] = nb;
+            else for (int rr = 0; rr < C; ++rr) st_cluster(&vn[q * A.pv + j], rr, nb);
+          } else {
+            uv[q * nr + r] = u;
+          }
+        }
+      }
+    }
+    if (grp) {
+      // group M-step (eqs glasso / gmcp / gscad); groups lie inside [j0, j1)
+      __syncthreads();
+      if (nr > 0) {
+        for (int e = tid; e < ng_loc * nP; e += PT) {
+          const int q = e % nP, gl = e / nP;
+          if (!((qmask >> q) & 1u)) continue;
+          const int a = ga_s[gl], b = gb_s[gl];
+          const double* ug = uv + q * nr;
+          double s = 0.0;
+          for (int r = a; r < b; ++r) s += ug[r] * ug[r];
+          const double nu = sqrt(s);
+          double lamq = 0.0, gq = 0.0;
+          int fam = 0;
+#pragma unroll
+          for (int qq = 0; qq < NPT; ++qq)
+            if (qq == q) { lamq = lam[qq]; gq = gamq[qq]; fam = famq[qq]; }
+          const double lw = gw_s[gl] * lamq;
+          double f;
+          if (fam == OEM_GRP_LASSO) f = nu > 0.0 ? pos(1.0 - lw / nu) : 0.0;
+          else f = nu > 0.0 ? (fam == OEM_GRP_MCP ? th_mcp(nu, lw, gq, d) : th_scad(nu, lw, gq, d)) / nu : 0.0;
+          double m = 0.0;
+          for (int r = a; r < b; ++r) {
+            const double nb = fam == OEM_GRP_LASSO ? ug[r] / d * f : f * ug[r];
+            const int j = j0 + r;
+            m = fmax(m, fabs(nb - vc[q * A.pv + j]));
+            if (C == 1) vn[q * A.pv + j] = nb;
+            else for (int rr = 0; rr < C; ++rr) st_cluster(&vn[q * A.pv + j], rr, nb);
+          }
+#pragma unroll
+          for (int qq = 0; qq < NPT; ++qq)
+            if (qq == q) dmax[qq] = fmax(dmax[qq], m);
+        }
+      }
+    }
+    // ---- max |dbeta| per penalty: warp -> CTA -> every CTA of the cluster
+#pragma unroll
+    for (int q = 0; q < NPT; ++q) {
+      double m = dmax[q];
+      for (int o = 16; o > 0; o >>= 1) m = fmax(m, __shfl_xor_sync(0xffffffffu, m, o));
+      if (lane == 0) red[warp * (NPT + 1) + q] = m;
+    }
+    {
+      const unsigned anybad = __ballot_sync(0xffffffffu, bad);
+      if (lane == 0) red[warp * (NPT + 1) + NPT] = anybad ? 1.0 : 0.0;
+    }
+    __syncthreads();
+    if (tid <= NPT) {
+      double m = 0.0;
+      for (int w = 0; w < nwarps; ++w) m = fmax(m, red[w * (NPT + 1) + tid]);
+      for (int rr = 0; rr < C; ++rr) st_cluster(&dl[(size_t)(cur * C + rank) * (NPT + 2) + tid], rr, m);
+    }
+    cluster_sync_all();
+    // ---- identical bookkeeping in every thread of every CTA of the cluster
+    double delta[NPT];
+    bool stop = false;
+#pragma unroll
+    for (int q = 0; q < NPT; ++q) delta[q] = 0.0;
+    for (int r = 0; r < C; ++r) {
+      const double* dr = dl + (size_t)(cur * C + r) * (NPT + 2);
+#pragma unroll
+      for (int q = 0; q < NPT; ++q) delta[q] = fmax(delta[q], dr[q]);
+      if (dr[NPT] != 0.0) stop = true;
+    }
+    if (stop) {
+      if (tid == 0) atomicExch(&P.flags[0], 1);
+      break;
+    }
+#pragma unroll
+    for (int q = 0; q < NPT; ++q) {
+      if (!((qmask >> q) & 1u)) continue;
+      const int it = itc[q] + 1;
+      const bool conv = delta[q] <= P.tol;   // R#17
+      if (conv || it >= P.maxit) {
+        const int l = lidx[q];
+        double* out = P.beta_out + (((size_t)unit * nP + q) * L + l) * p;
+        for (int r = tid; r < nr; r += PT) out[P.perm[j0 + r]] = vn[q * A.pv + j0 + r];
+        if (rank == 0 && tid == 0) {
+          P.it_out[((size_t)unit * nP + q) * L + l] = it;
+          P.cv_out[((size_t)unit * nP + q) * L + l] = conv ? 1 : 0;
+        }
+        lidx[q] = l + 1;
+        itc[q] = 0;
+        if (l + 1 < L)
+          lam[q] = P.lam_explicit ? P.lam_explicit[l + 1]
+                                  : (L == 1 ? lmax[q]
+                                            : lmax[q] * exp(((double)(l + 1) / (double)(L - 1)) * log(P.lmin_ratio)));
+      } else {
+        itc[q] = it;
+      }
+    }
+  }
+}
+
+// cluster layout: smallest C whose per-thread share fits registers + shared memory
+struct ClusterLayout {
+  int C = 0, T = 1, RG = PT, KPR = 0, NRT = 1, S = 0, pv = 0, ereg = 32, maxrows = 0;
+  size_t smem = 0;
+  std::vector<int> j0, j1;
+};
+
+static bool make_cluster_layout(int nU, int p, int NPT, const std::vector<int>& gstart, int num_sms, int ereg,
+                                ClusterLayout& lo) {
+  lo.ereg = ereg;
+  lo.pv = (p + 1) / 2 * 2 + 2;
+  for (int C = 1; C <= 16; ++C) {
+    // group-aligned cuts
+    std::vector<int> cuts{0};
+    for (int c = 1; c < C; ++c) {
+      const int target = (int)((int64_t)p * c / C);
+      int best = target;
+      if (!gstart.empty()) {
+        best = -1;
+        for (int b : gstart)
+          if (b > cuts.back() && b < p && (best < 0 || std::abs(b - target) < std::abs(best - target))) best = b;
+        if (best < 0) break;
+      }
+      if (best > cuts.back() && best < p) cuts.push_back(best);
+    }
+    cuts.push_back(p);
+    if ((int)cuts.size() - 1 != C) continue;
+    int maxrows = 0;
+    for (int c = 0; c < C; ++c) maxrows = std::max(maxrows, cuts[c + 1] - cuts[c]);
+    int T = 32;
+    while (T > 1 && PT / T < maxrows) T >>= 1;
+    const int RG = PT / T;
+    const int NRT = (maxrows + RG - 1) / RG;
+    const int KPR = (p + T - 1) / T;
+    const int S = std::max(0, KPR - ereg) + (NRT - 1) * KPR;
+    const size_t smem = ((size_t)S * PT + (size_t)2 * NPT * lo.pv + (size_t)2 * C * (NPT + 2) + 32 * (NPT + 1) +
+                         (size_t)NPT * maxrows + (size_t)5 * maxrows + 8) * 8;
+    if (smem > 200 * 1024) continue;
+    if ((int64_t)nU * C > 8L * num_sms) return false;
+    lo.C = C; lo.T = T; lo.RG = RG; lo.KPR = KPR; lo.NRT = NRT; lo.S = S; lo.smem = smem; lo.maxrows = maxrows;
+    lo.j0.clear(); lo.j1.clear();
+    for (int u = 0; u < nU; ++u)
+      for (int c = 0; c < C; ++c) { lo.j0.push_back(cuts[c]); lo.j1.push_back(cuts[c + 1]); }
+    return true;
+  }
+  return false;
+}
+
+template <int NPT>
+static oem_status launch_cluster(const PathParams& P, const ClusterArgs& A, int nU, size_t smem, cudaStream_t st) {
+  auto kern = fit_cluster_kernel<NPT, (NPT <= 1 ? 32 : NPT == 2 ? 24 : NPT == 4 ? 16 : 8)>;
+  OEM_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  if (A.C > 8) OEM_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3((unsigned)(nU * A.C));
+  cfg.blockDim = dim3(PT);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = (unsigned)A.C;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  OEM_CUDA_TRY(cudaLaunchKernelEx(&cfg, kern, P, A));
+  return OEM_OK;
+}
+
 // ---------------------------------------------------------------- host side
 struct Layout {
   std::vector<int> unit, rank, ncta, j0, j1;
@@ -622,6 +1109,8 @@ static oem_status coop_launch(K kern, int grid, size_t smem, cudaStream_t st, vo
   return OEM_OK;
 }
 
+static int ereg_for(int NPT) { return NPT <= 1 ? 32 : NPT == 2 ? 24 : NPT == 4 ? 16 : 8; }
+
 extern "C" oem_status oem_fit_path(oem_ctx* ctx, const double* G, const double* xty, const int64_t* counts,
                                    int32_t nG, int32_t p, const oem_penalty* pens, int32_t nP,
                                    const oem_path_cfg* cfg_in, const double* d_in, const double* beta_init,
@@ -642,6 +1131,8 @@ extern "C" oem_status oem_fit_path(oem_ctx* ctx, const double* G, const double* 
   if (!cfg.lambda && !(cfg.lambda_min_ratio > 0.0 && cfg.lambda_min_ratio < 1.0) && cfg.nlambda > 1)
     OEM_FAIL(OEM_ERR_INVALID_ARG, "oem_fit_path: need 0 < lambda_min_ratio < 1");
   if (!(cfg.tol > 0.0) || cfg.maxit < 1) OEM_FAIL(OEM_ERR_INVALID_ARG, "oem_fit_path: need tol > 0, maxit >= 1");
+  if (cfg.maxit > 2000000000LL) cfg.maxit = 2000000000LL;
+  if (cfg.power_iters < 0) OEM_FAIL(OEM_ERR_INVALID_ARG, "power_iters < 0");
   const int fold = cfg.fold_mode ? 1 : 0;
   const int nU = fold ? nG + 1 : nG;
   const int L = cfg.nlambda;
@@ -694,18 +1185,37 @@ extern "C" oem_status oem_fit_path(oem_ctx* ctx, const double* G, const double* 
     }
   }
   const int NPT = nP <= 1 ? 1 : nP <= 2 ? 2 : nP <= 4 ? 4 : 8;
+  // ---- solver layout: a thread-block cluster per unit when the rows fit on-chip (C <= 16),
+  // else the cooperative global-barrier solver
+  const char* force = std::getenv("OEM_PATH_SOLVER");
+  ClusterLayout cl;
   Layout lo;
+  bool use_cluster = !(force && std::string(force) == "global") &&
+                     make_cluster_layout(nU, p, NPT, any_grp ? gstart : std::vector<int>(), ctx->num_sms,
+                                         ereg_for(NPT), cl);
   std::string why;
-  if (!make_layout(nU, p, NPT, any_grp ? gstart : std::vector<int>(), ctx->num_sms, 200 * 1024, lo, why))
+  if (!use_cluster &&
+      !make_layout(nU, p, NPT, any_grp ? gstart : std::vector<int>(), ctx->num_sms, 200 * 1024, lo, why))
     OEM_FAIL(OEM_ERR_UNSUPPORTED, "oem_fit_path: persistent solver layout: " + why);
+  std::vector<int> t_unit, t_rank, t_ncta, t_j0, t_j1;
+  if (use_cluster) {
+    for (int u = 0; u < nU; ++u)
+      for (int c = 0; c < cl.C; ++c) { t_unit.push_back(u); t_rank.push_back(c); }
+    t_ncta.assign(nU, cl.C);
+    t_j0 = cl.j0;
+    t_j1 = cl.j1;
+  } else {
+    t_unit = lo.unit; t_rank = lo.rank; t_ncta = lo.ncta; t_j0 = lo.j0; t_j1 = lo.j1;
+  }
+  const int ncta_total = (int)t_unit.size();
   if (any_grp) {
-    // a group may not straddle two CTAs: checked against the cuts
-    for (size_t i = 0; i < lo.j0.size(); ++i)
+    for (size_t i = 0; i < t_j0.size(); ++i)
       for (int g = 0; g < cfg.ngroups; ++g)
-        if (gstart[g] < lo.j0[i] && gend[g] > lo.j0[i])
+        if (gstart[g] < t_j0[i] && gend[g] > t_j0[i])
           OEM_FAIL(OEM_ERR_UNSUPPORTED, "oem_fit_path: a group is larger than one solver CTA's rows");
   }
-  // ---- workspace (device): small tables in one block, large arrays in another
+  const int Cmax = use_cluster ? cl.C : lo.Cmax;
+  // ---- workspace (device)
   const size_t pp = (size_t)p * p;
   size_t off = 0;
   auto take = [&](size_t bytes) { size_t o = off; off += (bytes + 255) / 256 * 256; return o; };
@@ -713,7 +1223,7 @@ extern "C" oem_status oem_fit_path(oem_ctx* ctx, const double* G, const double* 
   const size_t o_cn = take(sizeof(double) * nU * p);
   const size_t o_bbuf = take(sizeof(double) * 2 * nU * nP * p);
   const size_t o_wbuf = take(sizeof(double) * 2 * nU * p);
-  const size_t o_pslot = take(sizeof(double) * 3 * nU * lo.Cmax);
+  const size_t o_pslot = take(sizeof(double) * 3 * nU * Cmax);
   const size_t o_bad = take(sizeof(unsigned long long) * nU);
   const size_t o_dslot = take(sizeof(unsigned long long) * 3 * nU * nP);
   const size_t o_bar = take(sizeof(unsigned) * 2 * nU);
@@ -730,21 +1240,20 @@ extern "C" oem_status oem_fit_path(oem_ctx* ctx, const double* G, const double* 
   const size_t o_alp = take(sizeof(double) * nP);
   const size_t o_lam = take(sizeof(double) * L);
   const size_t o_lmax = take(sizeof(double));
-  const size_t o_cu = take(sizeof(int) * lo.ncta_total);
-  const size_t o_cr = take(sizeof(int) * lo.ncta_total);
+  const size_t o_cu = take(sizeof(int) * ncta_total);
+  const size_t o_cr = take(sizeof(int) * ncta_total);
   const size_t o_un = take(sizeof(int) * nU);
-  const size_t o_j0 = take(sizeof(int) * lo.ncta_total);
-  const size_t o_j1 = take(sizeof(int) * lo.ncta_total);
+  const size_t o_j0 = take(sizeof(int) * ncta_total);
+  const size_t o_j1 = take(sizeof(int) * ncta_total);
   const size_t o_d = take(sizeof(double) * nU);
   const size_t o_host_end = off;
   OEM_CUDA_TRY(ctx->path_ws.ensure(off));
   char* base = ctx->path_ws.as<char>();
-  // host staging of the small tables, one H2D copy
   std::vector<char> hb(o_host_end - o_invn, 0);
   auto put = [&](size_t o, const void* src, size_t bytes) { if (bytes) std::memcpy(hb.data() + (o - o_invn), src, bytes); };
   put(o_invn, inv_n.data(), sizeof(double) * nU);
   put(o_perm, perm.data(), sizeof(int) * p);
-  if (any_grp || cfg.group) {
+  if (cfg.group) {
     put(o_gof, g_of_perm.data(), sizeof(int) * p);
     put(o_gs, gstart.data(), sizeof(int) * gstart.size());
     put(o_ge, gend.data(), sizeof(int) * gend.size());
@@ -758,56 +1267,51 @@ extern "C" oem_status oem_fit_path(oem_ctx* ctx, const double* G, const double* 
   put(o_alp, alp.data(), sizeof(double) * nP);
   if (cfg.lambda) put(o_lam, cfg.lambda, sizeof(double) * L);
   if (cfg.lambda_max_override) put(o_lmax, cfg.lambda_max_override, sizeof(double));
-  put(o_cu, lo.unit.data(), sizeof(int) * lo.ncta_total);
-  put(o_cr, lo.rank.data(), sizeof(int) * lo.ncta_total);
-  put(o_un, lo.ncta.data(), sizeof(int) * nU);
-  put(o_j0, lo.j0.data(), sizeof(int) * lo.ncta_total);
-  put(o_j1, lo.j1.data(), sizeof(int) * lo.ncta_total);
+  put(o_cu, t_unit.data(), sizeof(int) * ncta_total);
+  put(o_cr, t_rank.data(), sizeof(int) * ncta_total);
+  put(o_un, t_ncta.data(), sizeof(int) * nU);
+  put(o_j0, t_j0.data(), sizeof(int) * ncta_total);
+  put(o_j1, t_j1.data(), sizeof(int) * ncta_total);
   if (d_in) put(o_d, d_in, sizeof(double) * nU);
+  if (cfg.var_w) {
+    std::vector<double> tmp(p), wp(p);
+    OEM_CUDA_TRY(cudaMemcpyAsync(tmp.data(), cfg.var_w, sizeof(double) * p, cudaMemcpyDeviceToHost, st));
+    OEM_CUDA_TRY(cudaStreamSynchronize(st));
+    for (int j = 0; j < p; ++j) {
+      wp[j] = tmp[perm[j]];
+      if (!(wp[j] >= 0.0) || !std::isfinite(wp[j])) OEM_FAIL(OEM_ERR_INVALID_ARG, "variable weights must be >= 0");
+    }
+    put(o_varw, wp.data(), sizeof(double) * p);
+  }
   OEM_CUDA_TRY(cudaMemcpyAsync(base + o_invn, hb.data(), hb.size(), cudaMemcpyHostToDevice, st));
   OEM_CUDA_TRY(cudaMemsetAsync(base + o_dslot, 0, (o_invn - o_dslot), st));  // dslot, bar, flags
   OEM_CUDA_TRY(cudaMemsetAsync(base + o_bad, 0xff, sizeof(unsigned long long) * nU, st));
   double* Gn = reinterpret_cast<double*>(base + o_Gn);
   double* cn = reinterpret_cast<double*>(base + o_cn);
   int* flags = reinterpret_cast<int*>(base + o_flags);
-  double* varw_p = nullptr;
-  if (cfg.var_w) {
-    // permuted copy of the variable weights (device -> device gather via a tiny kernel is
-    // overkill here: p values, done with a host round trip-free D2D per element block)
-    std::vector<double> tmp(p);
-    OEM_CUDA_TRY(cudaMemcpyAsync(tmp.data(), cfg.var_w, sizeof(double) * p, cudaMemcpyDeviceToHost, st));
-    OEM_CUDA_TRY(cudaStreamSynchronize(st));
-    std::vector<double> wp(p);
-    for (int j = 0; j < p; ++j) {
-      wp[j] = tmp[perm[j]];
-      if (!(wp[j] >= 0.0) || !std::isfinite(wp[j])) OEM_FAIL(OEM_ERR_INVALID_ARG, "variable weights must be >= 0");
-    }
-    OEM_CUDA_TRY(cudaMemcpyAsync(base + o_varw, wp.data(), sizeof(double) * p, cudaMemcpyHostToDevice, st));
-    OEM_CUDA_TRY(cudaStreamSynchronize(st));
-    varw_p = reinterpret_cast<double*>(base + o_varw);
-  }
   // ---- a6 normalise (+ fold complements, + permutation)
   {
     const int64_t total = (int64_t)nU * ((int64_t)pp + p);
     const int blocks = (int)std::max<int64_t>(1, std::min<int64_t>(ctx->num_sms * 8, (total + 255) / 256));
+    PhaseTimer tm(ctx, PH_PATH, st);
+    ++ctx->launches;
     prep_units_kernel<<<blocks, 256, 0, st>>>(G, xty, nG, p, fold, reinterpret_cast<double*>(base + o_invn),
                                               reinterpret_cast<int*>(base + o_perm), Gn, cn, flags);
     OEM_CUDA_TRY(cudaGetLastError());
   }
   PathParams P;
   std::memset(&P, 0, sizeof(P));
-  P.p = p; P.nP = nP; P.L = L; P.nU = nU; P.ps = lo.ps; P.T = lo.T; P.maxit = cfg.maxit; P.tol = cfg.tol;
+  P.p = p; P.nP = nP; P.L = L; P.nU = nU; P.maxit = cfg.maxit; P.tol = cfg.tol;
   P.Gn = Gn; P.cn = cn;
   P.cta_unit = reinterpret_cast<int*>(base + o_cu);
   P.cta_rank = reinterpret_cast<int*>(base + o_cr);
   P.unit_ncta = reinterpret_cast<int*>(base + o_un);
   P.cta_j0 = reinterpret_cast<int*>(base + o_j0);
   P.cta_j1 = reinterpret_cast<int*>(base + o_j1);
-  P.smem_rows = lo.smem_rows;
   P.fam = reinterpret_cast<int*>(base + o_fam);
   P.gam = reinterpret_cast<double*>(base + o_gam);
   P.alp = reinterpret_cast<double*>(base + o_alp);
-  P.var_w = varw_p;
+  P.var_w = cfg.var_w ? reinterpret_cast<double*>(base + o_varw) : nullptr;
   P.ngroups = cfg.group ? cfg.ngroups : 0;
   P.g_start = reinterpret_cast<int*>(base + o_gs);
   P.g_end = reinterpret_cast<int*>(base + o_ge);
@@ -826,26 +1330,43 @@ extern "C" oem_status oem_fit_path(oem_ctx* ctx, const double* G, const double* 
   P.beta_out = beta_out; P.lam_out = lambda_out; P.it_out = iters_out; P.cv_out = converged_out;
   P.flags = flags;
   P.bad_iter = reinterpret_cast<unsigned long long*>(base + o_bad);
-  // ---- a7 d per unit (power rule R#5) unless given
-  if (!d_in) {
-    if (cfg.power_iters < 0) OEM_FAIL(OEM_ERR_INVALID_ARG, "power_iters < 0");
-    PathParams P1 = P;
-    P1.smem_rows = lo.smem_rows;
-    double* wbuf = reinterpret_cast<double*>(base + o_wbuf);
-    double* pslot = reinterpret_cast<double*>(base + o_pslot);
-    int iters = cfg.power_iters, Cmax = lo.Cmax;
-    double infl = cfg.d_inflate;
-    double* dptr = reinterpret_cast<double*>(base + o_d);
-    void* args[] = {&P1, &iters, &infl, &wbuf, &pslot, &Cmax, &dptr};
-    const size_t smem = ((size_t)lo.smem_rows * lo.ps + lo.ps + lo.smem_rows + 64) * 8;
-    oem_status s = coop_launch(power_kernel, lo.ncta_total, smem, st, args);
+  double* dptr = reinterpret_cast<double*>(base + o_d);
+  if (use_cluster) {
+    // ---- a7-a10 fused in one cluster launch (d, lambda grid, paths)
+    P.ps = 0; P.T = cl.T; P.smem_rows = 0;
+    ClusterArgs A;
+    A.C = cl.C; A.T = cl.T; A.RG = cl.RG; A.KPR = cl.KPR; A.NRT = cl.NRT; A.S = cl.S; A.pv = cl.pv;
+    A.power_iters = cfg.power_iters; A.inflate = cfg.d_inflate; A.compute_d = d_in ? 0 : 1; A.d_out = dptr;
+    A.maxrows = cl.maxrows;
+    PhaseTimer tm(ctx, PH_PATH, st);
+    ++ctx->launches;
+    oem_status s;
+    if (NPT == 1) s = launch_cluster<1>(P, A, nU, cl.smem, st);
+    else if (NPT == 2) s = launch_cluster<2>(P, A, nU, cl.smem, st);
+    else if (NPT == 4) s = launch_cluster<4>(P, A, nU, cl.smem, st);
+    else s = launch_cluster<8>(P, A, nU, cl.smem, st);
     if (s != OEM_OK) return s;
-    OEM_CUDA_TRY(cudaMemsetAsync(base + o_bar, 0, sizeof(unsigned) * 2 * nU, st));
-  }
-  OEM_CUDA_TRY(cudaMemcpyAsync(d_out, base + o_d, sizeof(double) * nU, cudaMemcpyDeviceToDevice, st));
-  // ---- a8-a10 lambda grid + OEM paths
-  {
+  } else {
+    P.ps = lo.ps; P.T = lo.T; P.smem_rows = lo.smem_rows;
+    // ---- a7 d per unit (power rule R#5) unless given
+    if (!d_in) {
+      PathParams P1 = P;
+      double* wbuf = reinterpret_cast<double*>(base + o_wbuf);
+      double* pslot = reinterpret_cast<double*>(base + o_pslot);
+      int iters = cfg.power_iters, Cm = lo.Cmax;
+      double infl = cfg.d_inflate;
+      void* args[] = {&P1, &iters, &infl, &wbuf, &pslot, &Cm, &dptr};
+      const size_t smem = ((size_t)lo.smem_rows * lo.ps + lo.ps + lo.smem_rows + 64) * 8;
+      PhaseTimer tm(ctx, PH_POWER, st);
+      ++ctx->launches;
+      oem_status s = coop_launch(power_kernel, lo.ncta_total, smem, st, args);
+      if (s != OEM_OK) return s;
+      OEM_CUDA_TRY(cudaMemsetAsync(base + o_bar, 0, sizeof(unsigned) * 2 * nU, st));
+    }
+    // ---- a8-a10 lambda grid + OEM paths
     void* args[] = {&P};
+    PhaseTimer tm(ctx, PH_PATH, st);
+    ++ctx->launches;
     oem_status s;
     if (NPT == 1) s = coop_launch(path_kernel<1>, lo.ncta_total, lo.smem, st, args);
     else if (NPT == 2) s = coop_launch(path_kernel<2>, lo.ncta_total, lo.smem, st, args);
@@ -853,6 +1374,7 @@ extern "C" oem_status oem_fit_path(oem_ctx* ctx, const double* G, const double* 
     else s = coop_launch(path_kernel<8>, lo.ncta_total, lo.smem, st, args);
     if (s != OEM_OK) return s;
   }
+  OEM_CUDA_TRY(cudaMemcpyAsync(d_out, dptr, sizeof(double) * nU, cudaMemcpyDeviceToDevice, st));
   int hflags[4] = {0, 0, 0, 0};
   OEM_CUDA_TRY(cudaMemcpyAsync(hflags, flags, sizeof(hflags), cudaMemcpyDeviceToHost, st));
   OEM_CUDA_TRY(cudaStreamSynchronize(st));

@@ -25,7 +25,10 @@ STATUS = ["OEM_OK", "OEM_ERR_INVALID_ARG", "OEM_ERR_DIM", "OEM_ERR_ALIGN", "OEM_
 # Every symbol include/oem.h declares (checked by tests/test_abi.py).
 ABI_SYMBOLS = ["oem_status_string", "oem_last_error", "oem_version", "oem_nccl_unique_id",
                "oem_ctx_create", "oem_ctx_destroy", "oem_gram", "oem_gram_folds",
-               "oem_gram_weighted", "oem_fit_path", "oem_path_cfg_default"]
+               "oem_gram_weighted", "oem_fit_path", "oem_path_cfg_default", "oem_fit_logistic",
+               "oem_logistic_cfg_default", "oem_ctx_set_timing", "oem_ctx_stats"]
+_VOID = ("oem_status_string", "oem_last_error", "oem_version", "oem_path_cfg_default",
+         "oem_logistic_cfg_default")
 
 
 class OemError(RuntimeError):
@@ -46,6 +49,24 @@ class PathCfg(ctypes.Structure):
                 ("grp_w", ctypes.c_void_p), ("power_iters", ctypes.c_int32),
                 ("d_inflate", ctypes.c_double), ("fold_mode", ctypes.c_int32),
                 ("lambda_max_override", ctypes.c_void_p)]
+
+
+class LogisticCfg(ctypes.Structure):
+    _fields_ = [("nlambda", ctypes.c_int32), ("lambda_min_ratio", ctypes.c_double),
+                ("lambda_", ctypes.c_void_p), ("tol_in", ctypes.c_double),
+                ("maxit_in", ctypes.c_int64), ("tol_out", ctypes.c_double),
+                ("outer_maxit", ctypes.c_int32), ("eps", ctypes.c_double),
+                ("power_iters", ctypes.c_int32), ("d_inflate", ctypes.c_double),
+                ("var_w", ctypes.c_void_p)]
+
+
+class Stats(ctypes.Structure):
+    _fields_ = [("launches", ctypes.c_int64), ("gram_ms", ctypes.c_double),
+                ("reduce_ms", ctypes.c_double), ("allreduce_ms", ctypes.c_double),
+                ("power_ms", ctypes.c_double), ("path_ms", ctypes.c_double)]
+
+    def as_dict(self):
+        return {k: getattr(self, k) for k, _ in self._fields_}
 
 
 _lib = None
@@ -73,9 +94,15 @@ def lib():
                                    ctypes.POINTER(PathCfg), P, P, P, P, P, P, P, P]
         L.oem_path_cfg_default.argtypes = [ctypes.POINTER(PathCfg)]
         L.oem_path_cfg_default.restype = None
+        L.oem_logistic_cfg_default.argtypes = [ctypes.POINTER(LogisticCfg)]
+        L.oem_logistic_cfg_default.restype = None
+        L.oem_fit_logistic.argtypes = [P, P, P, i64, i32, i64, ctypes.POINTER(Penalty),
+                                       ctypes.POINTER(LogisticCfg), P, P, P, P, P, P]
+        L.oem_ctx_set_timing.argtypes = [P, ctypes.c_int]
+        L.oem_ctx_stats.argtypes = [P, ctypes.POINTER(Stats), ctypes.c_int]
         for name in ABI_SYMBOLS:
             f = getattr(L, name)
-            if name not in ("oem_status_string", "oem_last_error", "oem_version", "oem_path_cfg_default"):
+            if name not in _VOID:
                 f.restype = ctypes.c_int
         _lib = L
     return _lib
@@ -251,3 +278,59 @@ def oem_fit_path(ctx: Context, G, xty, counts, penalties, nlambda=100, lambda_mi
                               d_h, _ptr(beta_init), _ptr(beta), _ptr(lam), _ptr(iters), _ptr(conv),
                               _ptr(d), _stream(stream)))
     return PathResult(beta, lam, iters, conv, d)
+
+
+@dataclass
+class LogisticResult:
+    beta: torch.Tensor        # [L][p]
+    lam: torch.Tensor         # [L]
+    outer_iters: list
+    inner_iters: list
+    conv: list
+
+
+def oem_fit_logistic(ctx: Context, X, y01, penalty=("lasso", 0.0, 1.0), nlambda=50,
+                     lambda_min_ratio=1e-3, lambdas=None, tol_in=1e-11, maxit_in=100000,
+                     tol_out=1e-10, outer_maxit=100, eps=1e-5, power_iters=200, d_inflate=5e-3,
+                     var_w=None, stream=None) -> LogisticResult:
+    """a4 + a6-a9 to convergence: proximal-Newton logistic path."""
+    _check_x(X, y01)
+    n, p = X.shape
+    L = nlambda if lambdas is None else len(lambdas)
+    cfg = LogisticCfg()
+    lib().oem_logistic_cfg_default(ctypes.byref(cfg))
+    cfg.nlambda = L
+    cfg.lambda_min_ratio = lambda_min_ratio
+    keep = []
+    if lambdas is not None:
+        lam_h = (ctypes.c_double * L)(*[float(v) for v in lambdas])
+        keep.append(lam_h)
+        cfg.lambda_ = ctypes.cast(lam_h, ctypes.c_void_p)
+    cfg.tol_in, cfg.maxit_in, cfg.tol_out, cfg.outer_maxit = tol_in, maxit_in, tol_out, outer_maxit
+    cfg.eps, cfg.power_iters, cfg.d_inflate = eps, power_iters, d_inflate
+    if var_w is not None:
+        var_w = var_w.to(device=X.device, dtype=torch.float64).contiguous()
+        cfg.var_w = var_w.data_ptr()
+    f, g, a = penalty
+    pen = Penalty(FAMILY[f], float(g), float(a))
+    beta = torch.empty((L, p), dtype=torch.float64, device=X.device)
+    lam = torch.empty(L, dtype=torch.float64, device=X.device)
+    oi = (ctypes.c_int32 * L)()
+    ii = (ctypes.c_int64 * L)()
+    cv = (ctypes.c_uint8 * L)()
+    _check(lib().oem_fit_logistic(ctx.h, _ptr(X), _ptr(y01), n, p, X.stride(0), ctypes.byref(pen),
+                                  ctypes.byref(cfg), _ptr(beta), _ptr(lam), oi, ii, cv,
+                                  _stream(stream)))
+    return LogisticResult(beta, lam, list(oi), list(ii), [bool(v) for v in cv])
+
+
+def set_timing(ctx: Context, enable: bool = True):
+    _check(lib().oem_ctx_set_timing(ctx.h, 1 if enable else 0))
+
+
+def stats(ctx: Context, reset: bool = False) -> dict:
+    """Accumulated device time per phase (CUDA events on the launching stream) and the number
+    of kernels the context launched."""
+    s = Stats()
+    _check(lib().oem_ctx_stats(ctx.h, ctypes.byref(s), 1 if reset else 0))
+    return s.as_dict()
