@@ -1,0 +1,8 @@
+set -x
+nvidia-smi --query-gpu=name,clocks.sm,clocks.max.sm,memory.total --format=csv
+nproc; free -g | head -2; lscpu | grep -i 'model name'
+timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/smoke.log 2>&1; echo smoke=$?
+timeout 900 python -m pytest tests -m gpu -x -q > gpurun_out/gpu_tests.log 2>&1; echo tests=$?
+timeout 900 python bench.py > gpurun_out/bench_cfg4.log 2>&1; echo bench=$?
+for w in cfg2 cfg3 cfg5; do timeout 600 python bench.py --workload $w --no-cpu-baseline --e2e-steps 1 > gpurun_out/bench_$w.log 2>&1; echo bench_$w=$?; done
+timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv --log-file gpurun_out/launches_cfg4.csv python bench.py --steps 2 --warmup 3 --e2e-steps 0 --no-cpu-baseline > gpurun_out/ncu_launch.log 2>&1; echo ncu1=$?
