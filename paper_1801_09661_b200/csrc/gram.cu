@@ -39,6 +39,8 @@ namespace oem {
 constexpr int BK = 32;      // rows per pipeline stage
 constexpr int MAXST = 6;    // max pipeline stages
 constexpr int NWC = 8;      // consumer warps per CTA
+constexpr int NRW = 4;      // WEIGHTED: row warps (eta, mu, w, z per row, one stage ahead of the MMA warps)
+__host__ __device__ constexpr int gram_threads(int mode) { return (NWC + (mode == 2 ? NRW : 0) + 1) * 32; }
 
 // job kinds: shape (R x C blocks) and which blocks are issued
 enum JobKind { J_NONE = 0, J_F44, J_T4, J_F41, J_F42, J_F43, J_T1, J_T2, J_T3, J_F48, J_T4F4, J_NKIND };
@@ -96,6 +98,7 @@ struct Cons {
   double* smem;
   uint64_t* full;
   uint64_t* empty;
+  uint64_t* ready;    // WEIGHTED: row quantities of the stage are in shared memory
   int warp, lane, nst, seg, fold, kprime;
   int64_t r0, r1;
   int a0, b0;
@@ -121,47 +124,18 @@ __device__ __forceinline__ void consume(const GramParams& P, const Cons& cs) {
   const int ycol = P.p - cs.b0;
   const bool ycopy = (MODE != MODE_WEIGHTED) && C > 0 && P.p >= 8 * cs.job.bj0 && P.p < 8 * (cs.job.bj0 + C);
   const int yidx = lane * P.ystride + (MODE == MODE_FOLD ? cs.kprime : 0);
-  double sw = 0.0, sll = 0.0;
   int st = 0;
   uint32_t ph = 0;
   for (int s = 0; s < cs.nst; ++s) {
     mbar_wait(&cs.full[st], ph);
+    if (MODE == MODE_WEIGHTED) mbar_wait(&cs.ready[st], ph);  // w_i and z_i of the stage's rows
     double* pa = cs.smem + (size_t)st * P.stage_doubles;
     double* pb = cs.two ? pa + (size_t)BK * ld : pa;
     double* ys = pa + P.ys_off;
     double* ws = ys + BK * P.ystride;
-    if (MODE != MODE_WEIGHTED) {
-      if (ycopy) {
-        pb[lane * ld + ycol] = ys[yidx];
-        __syncwarp();
-      }
-    } else {
-      // fused proximal-Newton row quantities: eta, mu (clamped), w, z
-      // BK / NWC = 4 rows per warp, 8 lanes per row; the 4 row leaders do the scalar math at once
-      static_assert(BK == 4 * NWC, "weighted prologue assumes 4 rows per consumer warp");
-      const int64_t rr = cs.r0 + (int64_t)s * BK;
-      {
-        const int k = cs.warp * 4 + (lane >> 3), sub = lane & 7;
-        double e = 0.0;
-        for (int j = sub; j < P.p; j += 8) e = fma(pa[k * ld + j], cs.beta_s[j], e);
-#pragma unroll
-        for (int o = 4; o > 0; o >>= 1) e += __shfl_xor_sync(0xffffffffu, e, o);
-        if (sub == 0) {
-          double w = 0.0, z = 0.0;
-          if (rr + k < cs.r1) {
-            double mu = 1.0 / (1.0 + exp(-e));
-            mu = fmin(fmax(mu, P.eps), 1.0 - P.eps);
-            w = mu * (1.0 - mu);
-            const double yk = ys[k];
-            z = e + (yk - mu) / w;
-            sw += w;
-            sll += yk * e - (e > 0.0 ? e + log1p(exp(-e)) : log1p(exp(e)));
-          }
-          ws[k] = w;
-          pa[k * ld + P.p] = z;
-        }
-      }
-      named_bar_sync(1, NWC * 32);
+    if (MODE != MODE_WEIGHTED && ycopy) {
+      pb[lane * ld + ycol] = ys[yidx];
+      __syncwarp();
     }
     if (KIND != J_NONE) {
       const double* pak = pa + aoff;
@@ -187,7 +161,7 @@ __device__ __forceinline__ void consume(const GramParams& P, const Cons& cs) {
         pbk += 4 * ld;
       }
     }
-    if (ycopy || MODE == MODE_WEIGHTED) fence_proxy_async_smem();  // generic smem writes precede the next TMA refill
+    if (ycopy) fence_proxy_async_smem();  // generic smem writes precede the next TMA refill
     __syncwarp();
     if (cs.lane == 0) mbar_arrive(&cs.empty[st]);
     if (++st == P.ST) { st = 0; ph ^= 1u; }
@@ -205,31 +179,84 @@ __device__ __forceinline__ void consume(const GramParams& P, const Cons& cs) {
               make_double2(acc[r][c][0], acc[r][c][1]);
         }
   }
-  if (MODE == MODE_WEIGHTED) {
-    // row leaders (lanes 0, 8, 16, 24) hold the sums of their rows: fixed-order warp reduction
-    sw += __shfl_xor_sync(0xffffffffu, sw, 8);
-    sll += __shfl_xor_sync(0xffffffffu, sll, 8);
-    sw += __shfl_xor_sync(0xffffffffu, sw, 16);
-    sll += __shfl_xor_sync(0xffffffffu, sll, 16);
-    if (lane == 0) { cs.scal_s[2 * cs.warp] = sw; cs.scal_s[2 * cs.warp + 1] = sll; }
-    named_bar_sync(1, NWC * 32);
-    if (cs.warp == 0 && lane == 0 && blockIdx.x % P.U == 0) {
-      double a = 0.0, b = 0.0;
-      for (int w = 0; w < NWC; ++w) { a += cs.scal_s[2 * w]; b += cs.scal_s[2 * w + 1]; }
-      P.partial_scal[cs.seg * 2 + 0] = a;
-      P.partial_scal[cs.seg * 2 + 1] = b;
+}
+
+// WEIGHTED row warps (R#25): per row of the stage, eta = x_i^T beta,
+// mu = sigma(eta) clamped to [eps, 1-eps], w = mu(1-mu), z = eta + (y - mu)/w; w goes to ws[k]
+// and z into the augmented column of the smem tile, so the MMA warps form sum w [x|z][x|z]^T.
+// Running one stage ahead of the MMA warps (ready[] ring) keeps the DMMA pipe busy.
+__device__ __forceinline__ void weighted_rows(const GramParams& P, const Cons& cs, int rw) {
+  const int ld = P.ld, lane = cs.lane;
+  const int k = rw * (BK / NRW) + (lane >> 2), sub = lane & 3;  // 4 lanes per row
+  double sw = 0.0, sll = 0.0;
+  int st = 0;
+  uint32_t ph = 0;
+  for (int s = 0; s < cs.nst; ++s) {
+    mbar_wait(&cs.full[st], ph);
+    double* pa = cs.smem + (size_t)st * P.stage_doubles;
+    double* ys = pa + P.ys_off;
+    double* ws = ys + BK * P.ystride;
+    const double* xr = pa + k * ld;
+    double e0 = 0.0, e1 = 0.0;
+    int j = sub;
+    for (; j + 4 < P.p; j += 8) {
+      e0 = fma(xr[j], cs.beta_s[j], e0);
+      e1 = fma(xr[j + 4], cs.beta_s[j + 4], e1);
     }
+    if (j < P.p) e0 = fma(xr[j], cs.beta_s[j], e0);
+    double e = e0 + e1;
+    e += __shfl_xor_sync(0xffffffffu, e, 1);
+    e += __shfl_xor_sync(0xffffffffu, e, 2);
+    const int64_t row = cs.r0 + (int64_t)s * BK + k;
+    double w = 0.0, z = 0.0;
+    if (row < cs.r1) {
+      double mu = 1.0 / (1.0 + exp(-e));
+      mu = fmin(fmax(mu, P.eps), 1.0 - P.eps);
+      w = mu * (1.0 - mu);
+      const double yk = ys[k];
+      z = e + (yk - mu) / w;
+      if (sub == 0) {
+        sw += w;
+        sll += yk * e - (e > 0.0 ? e + log1p(exp(-e)) : log1p(exp(e)));
+      }
+    }
+    if (sub == 0) {
+      ws[k] = w;
+      pa[k * ld + P.p] = z;
+    }
+    fence_proxy_async_smem();  // these generic writes precede the stage's next TMA refill
+    __syncwarp();
+    if (lane == 0) {
+      mbar_arrive(&cs.ready[st]);
+      mbar_arrive(&cs.empty[st]);
+    }
+    if (++st == P.ST) { st = 0; ph ^= 1u; }
+  }
+  // fixed-order reductions: lanes 0,4,..,28 hold their rows' sums; then warps in order
+#pragma unroll
+  for (int o = 4; o < 32; o <<= 1) {
+    sw += __shfl_xor_sync(0xffffffffu, sw, o);
+    sll += __shfl_xor_sync(0xffffffffu, sll, o);
+  }
+  if (lane == 0) { cs.scal_s[2 * rw] = sw; cs.scal_s[2 * rw + 1] = sll; }
+  named_bar_sync(1, NRW * 32);
+  if (rw == 0 && lane == 0 && blockIdx.x % P.U == 0) {
+    double a = 0.0, b = 0.0;
+    for (int w = 0; w < NRW; ++w) { a += cs.scal_s[2 * w]; b += cs.scal_s[2 * w + 1]; }
+    P.partial_scal[cs.seg * 2 + 0] = a;
+    P.partial_scal[cs.seg * 2 + 1] = b;
   }
 }
 
 template <int MODE, bool TWO>
-__global__ void __launch_bounds__((NWC + 1) * 32, (TWO || MODE == MODE_WEIGHTED) ? 1 : 2)
+__global__ void __launch_bounds__(gram_threads(MODE), (TWO || MODE == MODE_WEIGHTED) ? 1 : 2)
 gram_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ CUtensorMap tmY, const GramParams P) {
   extern __shared__ __align__(128) double smem[];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int u = blockIdx.x % P.U;
   const int rest = blockIdx.x / P.U;
-  __shared__ double scal_s[2 * NWC];
+  __shared__ double scal_s[2 * NRW];
+  __shared__ __align__(8) uint64_t ready_s[MAXST];
   Cons cs;
   cs.scal_s = scal_s;
   cs.seg = rest % P.nseg;
@@ -238,6 +265,7 @@ gram_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ CUt
   double* beta_s = smem + (size_t)P.ST * P.stage_doubles;  // WEIGHTED: ld doubles
   cs.full = reinterpret_cast<uint64_t*>(beta_s + (MODE == MODE_WEIGHTED ? P.ld : 0));
   cs.empty = cs.full + MAXST;
+  cs.ready = ready_s;
   cs.beta_s = beta_s;
   cs.r0 = (int64_t)cs.seg * P.seg_rows;
   cs.r1 = min(P.nrows, cs.r0 + P.seg_rows);
@@ -248,13 +276,14 @@ gram_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ CUt
   cs.b0 = cd->b0;
   cs.two = TWO && !cd->same;
   const int njob = cd->njob;
-  const int nconsumers = (MODE == MODE_WEIGHTED) ? NWC : njob;  // arrivals per stage release
+  const int nconsumers = njob + (MODE == MODE_WEIGHTED ? NRW : 0);  // arrivals per stage release
   const int full_count = P.ytma ? 1 : 32;
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < P.ST; ++s) {
       mbar_init(&cs.full[s], full_count);
       mbar_init(&cs.empty[s], nconsumers);
+      if (MODE == MODE_WEIGHTED) mbar_init(&cs.ready[s], NRW);
     }
     fence_mbar_init();
     tma_prefetch(&tmX);
@@ -264,7 +293,13 @@ gram_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ CUt
     for (int j = threadIdx.x; j < P.ld; j += blockDim.x) beta_s[j] = j < P.p ? P.beta[j] : 0.0;
   __syncthreads();
 
-  if (warp == NWC) {
+  cs.warp = warp;
+  cs.lane = lane;
+  if (MODE == MODE_WEIGHTED && warp >= NWC && warp < NWC + NRW) {
+    weighted_rows(P, cs, warp - NWC);
+    return;
+  }
+  if (warp == gram_threads(MODE) / 32 - 1) {
     // ------------------------------------------------------------ producer warp
     if (!P.ytma || lane == 0) {
       int st = 0;
@@ -303,10 +338,8 @@ gram_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ CUt
     return;
   }
   // -------------------------------------------------------------- consumer warps
-  cs.warp = warp;
-  cs.lane = lane;
   cs.job = cd->job[warp];
-  if (MODE != MODE_WEIGHTED && cs.job.kind == J_NONE) return;
+  if (cs.job.kind == J_NONE) return;
   switch (cs.job.kind) {
     case J_F44: consume<MODE, J_F44>(P, cs); break;
     case J_T4: consume<MODE, J_T4>(P, cs); break;
@@ -592,7 +625,7 @@ static oem_status launch_t(const GramPlan& pl, const CUtensorMap& mx, const CUte
     attr_smem = pl.smem;
   }
   dim3 grid((unsigned)(pl.U * pl.nseg * nfold));
-  kern<<<grid, (NWC + 1) * 32, pl.smem, st>>>(mx, my, P);
+  kern<<<grid, gram_threads(MODE), pl.smem, st>>>(mx, my, P);
   OEM_CUDA_TRY(cudaGetLastError());
   return OEM_OK;
 }

@@ -601,6 +601,10 @@ __global__ void __launch_bounds__(PT, 1) fit_cluster_kernel(const PathParams P, 
     c_s[r] = c[j0 + r];
     w_s[r] = P.var_w ? P.var_w[j0 + r] : 1.0;
   }
+  // both vector buffers start at zero (padding beyond p is read by the row dots and must stay 0);
+  // the cluster barrier orders the zeroing before any remote (DSMEM) write of a peer CTA
+  for (int k = tid; k < 2 * NPT * A.pv; k += PT) vec[k] = 0.0;
+  cluster_sync_all();
   const int g0 = (P.g_of && nr > 0) ? P.g_of[j0] : 0;
   const int ng_loc = (P.g_of && nr > 0) ? P.g_of[j1 - 1] + 1 - g0 : 0;
   for (int g = tid; g < ng_loc; g += PT) {
@@ -984,6 +988,8 @@ static bool make_cluster_layout(int nU, int p, int NPT, const std::vector<int>& 
     const int NRT = (maxrows + RG - 1) / RG;
     const int KPR = (p + T - 1) / T;
     const int S = std::max(0, KPR - ereg) + (NRT - 1) * KPR;
+    // vectors are read at every column index a thread owns (tl + ci*T < KPR*T): pad to that
+    lo.pv = std::max((p + 1) / 2 * 2 + 2, (KPR * T + 1) / 2 * 2);
     const size_t smem = ((size_t)S * PT + (size_t)2 * NPT * lo.pv + (size_t)2 * C * (NPT + 2) + 32 * (NPT + 1) +
                          (size_t)NPT * maxrows + (size_t)5 * maxrows + 8) * 8;
     if (smem > 200 * 1024) continue;

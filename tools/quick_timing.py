@@ -59,12 +59,15 @@ def main():
                                group=grp, ngroups=(p // cfg.group_size) if grp is not None else 0)
         e2.record()
         torch.cuda.synchronize()
-        if r == 0:
+        if r == 0 and a.reps > 0:
             continue
         g_ms = e0.elapsed_time(e1)
         f_ms = e1.elapsed_time(e2)
         out.setdefault("gram_ms", []).append(g_ms)
         out.setdefault("fit_ms", []).append(f_ms)
+    if a.reps == 0:
+        print(json.dumps(out))
+        return
     out["gram_tflops"] = flops / (min(out["gram_ms"]) * 1e-3) / 1e12
     if not a.nofit and not cfg.logistic:
         out["iters_total"] = int(fit.iters.sum())
