@@ -574,6 +574,410 @@ __device__ __forceinline__ void st_cluster(double* local, uint32_t rank, double 
   asm volatile("st.shared::cluster.f64 [%0], %1;" ::"r"(ra), "d"(v) : "memory");
 }
 
+// ---------------------------------------------------------------- K4+K5 lean: register-resident G
+// For p <= 256 and nP <= 4 (cfg1, cfg2 and the logistic inner solves of cfg5). One cluster of
+// C <= 4 CTAs per unit Gram; every thread keeps an R x KC tile of G in registers for the whole
+// launch (rows rg + i*RG, columns tl + m*T), and the nP penalty vectors are multiplied together
+// (the batched matvec: several penalties share A = dI - X^T X). One iteration:
+// KC*NPT shared-memory loads, R*KC*NPT FMAs, a width-T reduce-scatter that leaves each
+// (row, penalty) sum u_j on a single lane, the thresholding M-step on that lane,
+// DSMEM stores of the new coordinate into every CTA of the cluster, a warp OR of the
+// "|dbeta_j| > tol" bits and one hardware cluster barrier. The stopping rule (R#17,
+// max_j |dbeta_j| <= tol) only needs that OR, so no floating-point max is reduced.
+struct LeanArgs {
+  int C;            // CTAs per unit (cluster size)
+  int rows;         // max rows per CTA (= R * RG)
+  int pvl;          // padded vector length (= KC * T >= p)
+  int power_iters;
+  double inflate;
+  int compute_d;
+  double* d_out;    // [nU]
+};
+
+__device__ __forceinline__ void st_cl_f64(double* local, uint32_t rank, double v) {
+  uint32_t a = smem_u32(local), ra;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(ra) : "r"(a), "r"(rank));
+  asm volatile("st.shared::cluster.f64 [%0], %1;" ::"r"(ra), "d"(v) : "memory");
+}
+__device__ __forceinline__ void red_or_cl(uint32_t* local, uint32_t rank, uint32_t v) {
+  uint32_t a = smem_u32(local), ra;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(ra) : "r"(a), "r"(rank));
+  asm volatile("red.shared::cluster.or.b32 [%0], %1;" ::"r"(ra), "r"(v) : "memory");
+}
+
+// Reduce-scatter of V partial sums (padded to VP, a power of two dividing T) over the T lanes of a
+// row group: recursive halving, then a butterfly; lane tl ends with the full sum of value index
+// lean_vidx<VP,T>(tl). Fixed order of additions (deterministic).
+template <int VP, int T>
+__device__ __forceinline__ double lean_rs(double (&a)[VP], int tl) {
+#pragma unroll
+  for (int cnt = VP; cnt > 1; cnt >>= 1) {
+    const int o = T * cnt / (2 * VP), half = cnt / 2;
+    const bool up = (tl & o) != 0;
+#pragma unroll
+    for (int i = 0; i < half; ++i) {
+      const double send = up ? a[i] : a[i + half];
+      const double keep = up ? a[i + half] : a[i];
+      a[i] = keep + __shfl_xor_sync(0xffffffffu, send, o);
+    }
+  }
+#pragma unroll
+  for (int o = T / (2 * VP); o >= 1; o >>= 1) a[0] += __shfl_xor_sync(0xffffffffu, a[0], o);
+  return a[0];
+}
+template <int VP, int T>
+__device__ __forceinline__ int lean_vidx(int tl) {
+  int v = 0;
+#pragma unroll
+  for (int cnt = VP; cnt > 1; cnt >>= 1)
+    if (tl & (T * cnt / (2 * VP))) v += cnt / 2;
+  return v;
+}
+__host__ __device__ constexpr int pow2ceil(int v) { return v <= 1 ? 1 : 2 * pow2ceil((v + 1) / 2); }
+
+// beta vectors in shared memory: penalties in pairs, [pair][k][2], so one 16-byte load per lane
+// fetches two penalties and T consecutive lanes read T*16 contiguous bytes (conflict free)
+template <int NPT>
+__device__ __forceinline__ int vix(int q, int k, int pvl) {
+  return NPT == 1 ? k : (q >> 1) * 2 * pvl + 2 * k + (q & 1);
+}
+
+template <int NPT, int R, int KC, int T>
+__global__ void __launch_bounds__(PT, 1) fit_lean_kernel(const PathParams P, const LeanArgs A) {
+  constexpr int RG = PT / T, V = R * NPT, VP = pow2ceil(V), NW = PT / 32;
+  constexpr int NV = NPT == 1 ? 1 : 2 * ((NPT + 1) / 2);  // doubles per k in the vector layout
+  static_assert(VP <= T && (T & (T - 1)) == 0 && T <= 32, "lean layout");
+  extern __shared__ __align__(16) double sm[];
+  __shared__ int s_fam[NPT], s_skip[NPT];
+  __shared__ double s_gam[NPT], s_alp[NPT], s_lmax[NPT];
+  __shared__ uint32_t F[3];
+  const int p = P.p, nP = P.nP, L = P.L, C = A.C, pvl = A.pvl, rows = A.rows;
+  const int tid = threadIdx.x, rg = tid / T, tl = tid % T, warp = tid >> 5, lane = tid & 31;
+  const uint32_t rank = cluster_rank();
+  const int unit = blockIdx.x / C;
+  const int j0 = P.cta_j0[blockIdx.x], j1 = P.cta_j1[blockIdx.x], nr = j1 - j0;
+  const int kcu = (p + T - 1) / T;                       // column slots in use (warp-uniform)
+  const bool wrows = (warp * (32 / T)) * R < nr;         // this warp owns at least one row
+  const double* Gu = P.Gn + (size_t)unit * p * p;
+  const double* cu = P.cn + (size_t)unit * p;
+  // shared memory: vec [2][pvl*NV] | slots [2][C*NW] | uv [NPT][rows] | gw [rows] | ga, gb [rows]
+  double* vec = sm;
+  const int vstride = pvl * NV;
+  double* slots = vec + (size_t)2 * vstride;
+  double* uv = slots + (size_t)2 * C * NW;
+  double* gw_s = uv + (size_t)NPT * rows;
+  int* ga_s = reinterpret_cast<int*>(gw_s + rows);
+  int* gb_s = ga_s + rows;
+  auto sync_all = [&]() {
+    if (C == 1) __syncthreads();
+    else cluster_sync_all();
+  };
+  const bool grp = P.g_of != nullptr;
+  const int g0 = (grp && nr > 0) ? P.g_of[j0] : 0;
+  const int ng_loc = (grp && nr > 0) ? P.g_of[j1 - 1] + 1 - g0 : 0;
+  for (int gg = tid; gg < ng_loc; gg += PT) {
+    gw_s[gg] = P.g_w[g0 + gg];
+    ga_s[gg] = P.g_start[g0 + gg] - j0;
+    gb_s[gg] = P.g_end[g0 + gg] - j0;
+  }
+  for (int k = tid; k < 2 * vstride; k += PT) vec[k] = 0.0;
+  for (int k = tid; k < 2 * C * NW; k += PT) slots[k] = 0.0;
+  if (tid < 3) F[tid] = 0u;
+  // this thread's tile of G (rows rg*R + i, columns tl + m*T), resident in registers
+  double g[R][KC];
+#pragma unroll
+  for (int i = 0; i < R; ++i)
+#pragma unroll
+    for (int m = 0; m < KC; ++m) {
+      const int r = rg * R + i, k = tl + m * T;
+      g[i][m] = (r < nr && k < p) ? Gu[(size_t)(j0 + r) * p + k] : 0.0;
+    }
+  // the (row, penalty) sum this lane owns after the reduce-scatter
+  const int vidx = lean_vidx<VP, T>(tl);
+  const int mi = vidx / NPT, mq = vidx % NPT, mr = rg * R + mi;
+  const bool owner = (tl & (T / VP - 1)) == 0;
+  const bool act = owner && vidx < V && mr < nr;
+  const int mj = j0 + mr;
+  const double c_my = act ? cu[mj] : 0.0;
+  const double w_my = (act && P.var_w) ? P.var_w[mj] : 1.0;
+  // power iteration: an R-value reduce-scatter; the lane owns row rg*R + vidx1
+  constexpr int RP = pow2ceil(R);
+  const int vidx1 = lean_vidx<RP, T>(tl);
+  const int pr = rg * R + vidx1;
+  const bool pact = (tl & (T / RP - 1)) == 0 && vidx1 < R && pr < nr;
+  cluster_sync_all();  // peers' buffers are zeroed before any remote store
+
+  // ======================================================= a7: d by power iteration (R#5)
+  double d;
+  if (A.compute_d) {
+    // Gershgorin bound: max_j sum_k |G_jk|
+    double gm = 0.0;
+#pragma unroll
+    for (int i = 0; i < R; ++i) {
+      double s = 0.0;
+#pragma unroll
+      for (int m = 0; m < KC; ++m) s += fabs(g[i][m]);
+#pragma unroll
+      for (int o = T / 2; o >= 1; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+      if (rg * R + i < nr) gm = fmax(gm, s);
+    }
+#pragma unroll
+    for (int o = 16; o >= 1; o >>= 1) gm = fmax(gm, __shfl_xor_sync(0xffffffffu, gm, o));
+    if (lane == 0)
+      for (int rr = 0; rr < C; ++rr) st_cl_f64(&slots[NW * C + rank * NW + warp], rr, gm);  // parity-1 slots
+    const double v0 = 1.0 / sqrt((double)p);
+    for (int k = tid; k < p; k += PT) vec[vix<NPT>(0, k, pvl)] = v0;  // buffer 0, vector 0
+    cluster_sync_all();
+    double gersh = 0.0;
+    for (int e = 0; e < C * NW; ++e) gersh = fmax(gersh, slots[NW * C + e]);
+    cluster_sync_all();  // every CTA has read the Gershgorin slots before they are reused
+    // buffer b holds w (unnormalised); the iterate is v = w * sc
+    double sc = 1.0, rq = 0.0;
+    for (int it = 0; it <= A.power_iters; ++it) {
+      const int cur = it & 1, nxt = cur ^ 1;
+      const double* vc = vec + (size_t)cur * vstride;
+      double a[RP];
+#pragma unroll
+      for (int i = 0; i < RP; ++i) a[i] = 0.0;
+      if (wrows) {
+#pragma unroll
+        for (int m = 0; m < KC; ++m) {
+          if (m >= kcu) break;
+          const double b = vc[vix<NPT>(0, tl + m * T, pvl)];
+#pragma unroll
+          for (int i = 0; i < R; ++i) a[i] = fma(g[i][m], b, a[i]);
+        }
+      }
+      const double s = lean_rs<RP, T>(a, tl);
+      double part = 0.0;
+      if (pact) {
+        const int j = j0 + pr;
+        if (it < A.power_iters) {
+          const double y = s * sc;                 // (G v)_j
+          part = y * y;
+          double* dst = &vec[(size_t)nxt * vstride + vix<NPT>(0, j, pvl)];
+          if (C == 1) *dst = y;
+          else for (int rr = 0; rr < C; ++rr) st_cl_f64(dst, rr, y);
+        } else {
+          part = vc[vix<NPT>(0, j, pvl)] * s;      // w_j (G w)_j
+        }
+      }
+#pragma unroll
+      for (int o = 16; o >= 1; o >>= 1) part += __shfl_xor_sync(0xffffffffu, part, o);
+      if (lane == 0) {
+        if (C == 1) slots[cur * NW + warp] = part;
+        else for (int rr = 0; rr < C; ++rr) st_cl_f64(&slots[cur * NW * C + rank * NW + warp], rr, part);
+      }
+      sync_all();
+      double tot = 0.0;
+      for (int e = 0; e < C * NW; ++e) tot += slots[cur * NW * C + e];  // fixed order
+      if (it < A.power_iters) {
+        if (tot > 0.0) sc = 1.0 / sqrt(tot);
+      } else {
+        rq = tot * sc * sc;                         // v^T G v
+      }
+    }
+    const double dd = (1.0 + A.inflate) * rq;
+    d = gersh < dd ? gersh : dd;
+    if (rank == 0 && tid == 0) A.d_out[unit] = d;
+    cluster_sync_all();  // all reads of vec / slots are done before the path reuses them
+    for (int k = tid; k < 2 * vstride; k += PT) vec[k] = 0.0;
+  } else {
+    d = P.d[unit];
+  }
+
+  // ======================================================= a8: lambda grid (R#14-16, R#22)
+  if (warp < NPT) {
+    const int q = warp;
+    double lm = 0.0;
+    int fam = 0;
+    double gq = 0.0, aq = 0.0;
+    if (q < nP) {
+      fam = P.fam[q]; gq = P.gam[q]; aq = P.alp[q];
+      const double* cc = P.shared_grid ? P.cn : cu;
+      if (P.lmax_override) {
+        lm = *P.lmax_override;
+      } else if (fam >= OEM_GRP_LASSO) {
+        for (int gg = lane; gg < P.ngroups; gg += 32) {
+          const double cg = P.g_w[gg];
+          if (!(cg > 0.0)) continue;
+          double s = 0.0;
+          for (int j = P.g_start[gg]; j < P.g_end[gg]; ++j) s += cc[j] * cc[j];
+          lm = fmax(lm, sqrt(s) / cg);
+        }
+      } else {
+        const double scl = fam == OEM_ENET ? aq : 1.0;
+        for (int j = lane; j < p; j += 32) {
+          const double wj = P.var_w ? P.var_w[j] : 1.0;
+          if (!(wj > 0.0)) continue;
+          lm = fmax(lm, fabs(cc[j]) / (scl * wj));
+        }
+      }
+#pragma unroll
+      for (int o = 16; o >= 1; o >>= 1) lm = fmax(lm, __shfl_xor_sync(0xffffffffu, lm, o));
+    }
+    if (lane == 0) {
+      s_fam[q] = fam; s_gam[q] = gq; s_alp[q] = aq; s_lmax[q] = lm;
+      bool bad = false;  // parameter validity against the d in use (R#8)
+      if (q < nP) {
+        if (fam == OEM_MCP || fam == OEM_GRP_MCP) bad = !(gq > 1.0) || !(gq * d > 1.0);
+        if (fam == OEM_SCAD || fam == OEM_GRP_SCAD) bad = !(gq > 2.0) || !((gq - 1.0) * d > 1.0);
+        if (fam == OEM_ENET) bad = !(aq >= 0.0 && aq <= 1.0);
+        if (bad && rank == 0) atomicExch(&P.flags[1], 1);
+      }
+      s_skip[q] = (q >= nP || bad) ? 1 : 0;
+    }
+  }
+  // warm or cold start (permuted order) into buffer 0
+  if (P.beta_init)
+    for (int e = tid; e < nP * p; e += PT) {
+      const int q = e / p, k = e % p;
+      vec[vix<NPT>(q, k, pvl)] = P.beta_init[((size_t)unit * nP + q) * p + P.perm[k]];
+    }
+  __syncthreads();
+  auto lam_at = [&](int q, int l) -> double {
+    if (P.lam_explicit) return P.lam_explicit[l];
+    if (L == 1) return s_lmax[q];
+    return s_lmax[q] * exp(((double)l / (double)(L - 1)) * log(P.lmin_ratio));  // R#15
+  };
+  if (rank == 0)
+    for (int e = tid; e < nP * L; e += PT) {
+      const int q = e / L, l = e % L;
+      P.lam_out[((size_t)unit * nP + q) * L + l] = lam_at(q, l);
+    }
+  int lidx[NPT], itc[NPT];
+  double lam[NPT];
+#pragma unroll
+  for (int q = 0; q < NPT; ++q) {
+    lidx[q] = s_skip[q] ? L : 0;
+    itc[q] = 0;
+    lam[q] = s_skip[q] ? 0.0 : lam_at(q, 0);
+  }
+  const int fam_my = s_fam[mq];
+  const double gam_my = s_gam[mq], alp_my = s_alp[mq];
+  cluster_sync_all();  // every CTA's buffers are initialised before the first remote store
+
+  // ======================================================= a9: OEM iterations
+  for (int t = 0;; ++t) {
+    uint32_t qmask = 0;
+#pragma unroll
+    for (int q = 0; q < NPT; ++q)
+      if (lidx[q] < L) qmask |= 1u << q;
+    if (!qmask) break;
+    const int cur = t & 1, nxt = cur ^ 1;
+    const double* vc = vec + (size_t)cur * vstride;
+    double* vn = vec + (size_t)nxt * vstride;
+    if (tid == 0) F[(t + 1) % 3] = 0u;
+    // ---- E-step + M-step: u = c + d beta - G beta, all penalties at once
+    double a[VP];
+#pragma unroll
+    for (int v = 0; v < VP; ++v) a[v] = 0.0;
+    if (wrows) {
+#pragma unroll
+      for (int m = 0; m < KC; ++m) {
+        if (m >= kcu) break;
+        const int k = tl + m * T;
+        double b[NV];
+        if (NPT == 1) {
+          b[0] = vc[k];
+        } else {
+#pragma unroll
+          for (int h = 0; h < NV / 2; ++h) {
+            const double2 t2 = *reinterpret_cast<const double2*>(vc + h * 2 * pvl + 2 * k);
+            b[2 * h] = t2.x;
+            b[2 * h + 1] = t2.y;
+          }
+        }
+#pragma unroll
+        for (int i = 0; i < R; ++i)
+#pragma unroll
+          for (int q = 0; q < NPT; ++q) a[i * NPT + q] = fma(g[i][m], b[q], a[i * NPT + q]);
+      }
+    }
+    const double s = lean_rs<VP, T>(a, tl);
+    uint32_t bits = 0;
+    if (act && ((qmask >> mq) & 1u)) {
+      const int vi = vix<NPT>(mq, mj, pvl);
+      const double bj = vc[vi];
+      const double u = c_my + d * bj - s;
+      if (!isfinite(u)) bits |= 0x80000000u;
+      if (!grp) {
+        double lq = 0.0;
+#pragma unroll
+        for (int q = 0; q < NPT; ++q)
+          if (q == mq) lq = lam[q];
+        const double nb = th_coord(fam_my, u, w_my * lq, gam_my, alp_my, d);
+        if (!(fabs(nb - bj) <= P.tol)) bits |= 1u << mq;
+        if (C == 1) vn[vi] = nb;
+        else for (int rr = 0; rr < C; ++rr) st_cl_f64(&vn[vi], rr, nb);
+      } else {
+        uv[mq * rows + mr] = u;
+      }
+    }
+    if (grp) {
+      // group M-step (eqs glasso / gmcp / gscad); groups lie inside [j0, j1)
+      __syncthreads();
+      for (int e = tid; e < ng_loc * nP; e += PT) {
+        const int q = e % nP, gl = e / nP;
+        if (!((qmask >> q) & 1u)) continue;
+        const int ra = ga_s[gl], rb = gb_s[gl];
+        const double* ug = uv + q * rows;
+        double ss = 0.0;
+        for (int r = ra; r < rb; ++r) ss += ug[r] * ug[r];
+        const double nu = sqrt(ss);
+        double lq = 0.0;
+#pragma unroll
+        for (int qq = 0; qq < NPT; ++qq)
+          if (qq == q) lq = lam[qq];
+        const int fam = s_fam[q];
+        const double gq = s_gam[q], lw = gw_s[gl] * lq;
+        double f;
+        if (fam == OEM_GRP_LASSO) f = nu > 0.0 ? pos(1.0 - lw / nu) : 0.0;
+        else f = nu > 0.0 ? (fam == OEM_GRP_MCP ? th_mcp(nu, lw, gq, d) : th_scad(nu, lw, gq, d)) / nu : 0.0;
+        for (int r = ra; r < rb; ++r) {
+          const double nb = fam == OEM_GRP_LASSO ? ug[r] / d * f : f * ug[r];
+          const int vi = vix<NPT>(q, j0 + r, pvl);
+          if (!(fabs(nb - vc[vi]) <= P.tol)) bits |= 1u << q;
+          if (C == 1) vn[vi] = nb;
+          else for (int rr = 0; rr < C; ++rr) st_cl_f64(&vn[vi], rr, nb);
+        }
+      }
+    }
+    bits = __reduce_or_sync(0xffffffffu, bits);
+    if (lane == 0 && bits) {
+      if (C == 1) atomicOr(&F[t % 3], bits);
+      else for (int rr = 0; rr < C; ++rr) red_or_cl(&F[t % 3], rr, bits);
+    }
+    sync_all();
+    const uint32_t f = F[t % 3];
+    if (f & 0x80000000u) {
+      if (tid == 0) atomicExch(&P.flags[0], 1);
+      break;
+    }
+    // ---- identical bookkeeping in every thread of every CTA of the cluster
+#pragma unroll
+    for (int q = 0; q < NPT; ++q) {
+      if (!((qmask >> q) & 1u)) continue;
+      const int it = itc[q] + 1;
+      const bool conv = !((f >> q) & 1u);   // every |dbeta_j| <= tol (R#17)
+      if (conv || it >= P.maxit) {
+        const int l = lidx[q];
+        double* out = P.beta_out + (((size_t)unit * nP + q) * L + l) * p;
+        for (int r = tid; r < nr; r += PT) out[P.perm[j0 + r]] = vn[vix<NPT>(q, j0 + r, pvl)];
+        if (rank == 0 && tid == 0) {
+          P.it_out[((size_t)unit * nP + q) * L + l] = it;
+          P.cv_out[((size_t)unit * nP + q) * L + l] = conv ? 1 : 0;
+        }
+        lidx[q] = l + 1;
+        itc[q] = 0;
+        if (l + 1 < L) lam[q] = lam_at(q, l + 1);
+      } else {
+        itc[q] = it;
+      }
+    }
+  }
+}
+
 template <int NPT, int EREG>
 __global__ void __launch_bounds__(PT, 1) fit_cluster_kernel(const PathParams P, const ClusterArgs A) {
   extern __shared__ __align__(16) double sm[];
@@ -1024,6 +1428,80 @@ static oem_status launch_cluster(const PathParams& P, const ClusterArgs& A, int 
   return OEM_OK;
 }
 
+// ---------------------------------------------------------------- lean solver: host layout / launch
+struct LeanLayout {
+  int variant = -1;  // 0: R1 KC8 T8 (p <= 64), 1: R2 KC16 T8 (p <= 128), 2: R2 KC16 T16 (p <= 256)
+  int C = 1, rows = 0, pvl = 0;
+  size_t smem = 0;
+  std::vector<int> cuts;  // C + 1 row cuts (group aligned)
+};
+
+static bool make_lean_layout(int p, int NPT, const std::vector<int>& gstart, LeanLayout& lo) {
+  static const int R_[3] = {1, 2, 2}, KC_[3] = {8, 16, 16}, T_[3] = {8, 8, 16};
+  int v = p <= 64 ? 0 : p <= 128 ? 1 : p <= 256 ? 2 : -1;
+  if (v < 0 || NPT > 4) return false;
+  const int rows = R_[v] * (PT / T_[v]);
+  // contiguous row blocks of <= rows rows, cut only at group starts (greedy packing)
+  std::vector<int> cuts{0};
+  if (gstart.empty()) {
+    const int C = (p + rows - 1) / rows;
+    for (int c = 1; c <= C; ++c) cuts.push_back((int)((int64_t)p * c / C));
+  } else {
+    std::vector<int> starts(gstart);
+    std::sort(starts.begin(), starts.end());
+    starts.push_back(p);
+    int last = 0;  // last feasible cut candidate inside the current block
+    for (size_t i = 1; i < starts.size(); ++i) {
+      const int b = starts[i];
+      if (b - cuts.back() > rows) {
+        if (last <= cuts.back()) return false;  // a group larger than one CTA's rows
+        cuts.push_back(last);
+        if (b - cuts.back() > rows) return false;
+      }
+      last = b;
+    }
+    if (cuts.back() != p) cuts.push_back(p);
+  }
+  const int C = (int)cuts.size() - 1;
+  if (C < 1 || C > 8) return false;
+  lo.variant = v;
+  lo.C = C;
+  lo.rows = rows;
+  lo.pvl = KC_[v] * T_[v];
+  lo.cuts = cuts;
+  const int NV = NPT == 1 ? 1 : 2 * ((NPT + 1) / 2);
+  lo.smem = ((size_t)2 * NV * lo.pvl + (size_t)2 * C * (PT / 32) + (size_t)NPT * rows + rows) * 8 +
+            (size_t)2 * rows * 4 + 16;
+  return true;
+}
+
+template <int NPT, int R, int KC, int T>
+static oem_status launch_lean_t(const PathParams& P, const LeanArgs& A, int nU, size_t smem, cudaStream_t st) {
+  auto kern = fit_lean_kernel<NPT, R, KC, T>;
+  OEM_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3((unsigned)(nU * A.C));
+  cfg.blockDim = dim3(PT);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = (unsigned)A.C;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  OEM_CUDA_TRY(cudaLaunchKernelEx(&cfg, kern, P, A));
+  return OEM_OK;
+}
+
+template <int NPT>
+static oem_status launch_lean_v(const PathParams& P, const LeanArgs& A, int nU, const LeanLayout& lo, cudaStream_t st) {
+  if (lo.variant == 0) return launch_lean_t<NPT, 1, 8, 8>(P, A, nU, lo.smem, st);
+  if (lo.variant == 1) return launch_lean_t<NPT, 2, 16, 8>(P, A, nU, lo.smem, st);
+  return launch_lean_t<NPT, 2, 16, 16>(P, A, nU, lo.smem, st);
+}
+
 // ---------------------------------------------------------------- host side
 struct Layout {
   std::vector<int> unit, rank, ncta, j0, j1;
@@ -1196,15 +1674,24 @@ extern "C" oem_status oem_fit_path(oem_ctx* ctx, const double* G, const double* 
   const char* force = std::getenv("OEM_PATH_SOLVER");
   ClusterLayout cl;
   Layout lo;
-  bool use_cluster = !(force && std::string(force) == "global") &&
+  LeanLayout ll;
+  const bool use_lean = !(force && (std::string(force) == "global" || std::string(force) == "cluster")) &&
+                        make_lean_layout(p, nP, any_grp ? gstart : std::vector<int>(), ll);
+  bool use_cluster = !use_lean && !(force && std::string(force) == "global") &&
                      make_cluster_layout(nU, p, NPT, any_grp ? gstart : std::vector<int>(), ctx->num_sms,
                                          ereg_for(NPT), cl);
   std::string why;
-  if (!use_cluster &&
+  if (!use_lean && !use_cluster &&
       !make_layout(nU, p, NPT, any_grp ? gstart : std::vector<int>(), ctx->num_sms, 200 * 1024, lo, why))
     OEM_FAIL(OEM_ERR_UNSUPPORTED, "oem_fit_path: persistent solver layout: " + why);
   std::vector<int> t_unit, t_rank, t_ncta, t_j0, t_j1;
-  if (use_cluster) {
+  if (use_lean) {
+    for (int u = 0; u < nU; ++u)
+      for (int c = 0; c < ll.C; ++c) {
+        t_unit.push_back(u); t_rank.push_back(c); t_j0.push_back(ll.cuts[c]); t_j1.push_back(ll.cuts[c + 1]);
+      }
+    t_ncta.assign(nU, ll.C);
+  } else if (use_cluster) {
     for (int u = 0; u < nU; ++u)
       for (int c = 0; c < cl.C; ++c) { t_unit.push_back(u); t_rank.push_back(c); }
     t_ncta.assign(nU, cl.C);
@@ -1220,7 +1707,7 @@ extern "C" oem_status oem_fit_path(oem_ctx* ctx, const double* G, const double* 
         if (gstart[g] < t_j0[i] && gend[g] > t_j0[i])
           OEM_FAIL(OEM_ERR_UNSUPPORTED, "oem_fit_path: a group is larger than one solver CTA's rows");
   }
-  const int Cmax = use_cluster ? cl.C : lo.Cmax;
+  const int Cmax = use_lean ? ll.C : use_cluster ? cl.C : lo.Cmax;
   // ---- workspace (device)
   const size_t pp = (size_t)p * p;
   size_t off = 0;
@@ -1337,7 +1824,21 @@ extern "C" oem_status oem_fit_path(oem_ctx* ctx, const double* G, const double* 
   P.flags = flags;
   P.bad_iter = reinterpret_cast<unsigned long long*>(base + o_bad);
   double* dptr = reinterpret_cast<double*>(base + o_d);
-  if (use_cluster) {
+  if (use_lean) {
+    // ---- a7-a10 fused in one launch: register-resident G, one cluster per unit
+    P.ps = 0; P.T = 0; P.smem_rows = 0;
+    LeanArgs A;
+    A.C = ll.C; A.rows = ll.rows; A.pvl = ll.pvl;
+    A.power_iters = cfg.power_iters; A.inflate = cfg.d_inflate; A.compute_d = d_in ? 0 : 1; A.d_out = dptr;
+    PhaseTimer tm(ctx, PH_PATH, st);
+    ++ctx->launches;
+    oem_status s;
+    if (nP == 1) s = launch_lean_v<1>(P, A, nU, ll, st);
+    else if (nP == 2) s = launch_lean_v<2>(P, A, nU, ll, st);
+    else if (nP == 3) s = launch_lean_v<3>(P, A, nU, ll, st);
+    else s = launch_lean_v<4>(P, A, nU, ll, st);
+    if (s != OEM_OK) return s;
+  } else if (use_cluster) {
     // ---- a7-a10 fused in one cluster launch (d, lambda grid, paths)
     P.ps = 0; P.T = cl.T; P.smem_rows = 0;
     ClusterArgs A;
