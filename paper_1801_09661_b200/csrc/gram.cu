@@ -42,20 +42,32 @@ constexpr int NWC = 8;      // consumer warps per CTA
 constexpr int NRW = 4;      // WEIGHTED: row warps (eta, mu, w, z per row, one stage ahead of the MMA warps)
 __host__ __device__ constexpr int gram_threads(int mode) { return (NWC + (mode == 2 ? NRW : 0) + 1) * 32; }
 
-// job kinds: shape (R x C blocks) and which blocks are issued
-enum JobKind { J_NONE = 0, J_F44, J_T4, J_F41, J_F42, J_F43, J_T1, J_T2, J_T3, J_F48, J_T4F4, J_NKIND };
+// job kinds: shape (R x C blocks) and which blocks are issued. Full kinds F4c issue all 4 x c
+// blocks; triangular kinds (T1..T4 and T4Fk = T4 followed by k full columns) issue (r, c) with
+// c >= r. The Fxx/T4Fk kinds with C > 4 appear only in two-panel plans (128-column panels);
+// F45..F47 and T4F1..T4F3 are trimmed jobs at the last panel (columns beyond the augmented
+// matrix are never issued).
+enum JobKind { J_NONE = 0, J_F44, J_T4, J_F41, J_F42, J_F43, J_T1, J_T2, J_T3, J_F48, J_T4F4,
+               J_F45, J_F46, J_F47, J_T4F1, J_T4F2, J_T4F3, J_NKIND };
 __host__ __device__ constexpr int kind_R(int k) {
   return k == J_NONE ? 0 : k == J_T1 ? 1 : k == J_T2 ? 2 : k == J_T3 ? 3 : 4;
 }
 __host__ __device__ constexpr int kind_C(int k) {
   return k == J_NONE ? 0 : k == J_F41 || k == J_T1 ? 1 : k == J_F42 || k == J_T2 ? 2
-       : k == J_F43 || k == J_T3 ? 3 : k == J_F48 || k == J_T4F4 ? 8 : 4;
+       : k == J_F43 || k == J_T3 ? 3 : k == J_F48 || k == J_T4F4 ? 8 : k == J_F45 || k == J_T4F1 ? 5
+       : k == J_F46 || k == J_T4F2 ? 6 : k == J_F47 || k == J_T4F3 ? 7 : 4;
 }
 __host__ __device__ constexpr bool kind_tri(int k) {
-  return k == J_T4 || k == J_T1 || k == J_T2 || k == J_T3 || k == J_T4F4;
+  return k == J_T4 || k == J_T1 || k == J_T2 || k == J_T3 || k == J_T4F4 || k == J_T4F1 || k == J_T4F2 || k == J_T4F3;
 }
 // block (r, c) of the job is issued: all blocks for full kinds, c >= r for triangular ones
 __host__ __device__ constexpr bool kind_active(int k, int r, int c) { return kind_tri(k) ? c >= r : true; }
+// the kind with this shape (J_NONE if there is none)
+static int kind_of(int R, int C, bool tri) {
+  for (int k = 1; k < J_NKIND; ++k)
+    if (kind_R(k) == R && kind_C(k) == C && kind_tri(k) == tri) return k;
+  return J_NONE;
+}
 __host__ __device__ constexpr int kind_cost(int k) {
   int n = 0;
   for (int r = 0; r < kind_R(k); ++r)
@@ -77,6 +89,7 @@ struct CtaDesc {
 
 struct GramParams {
   int p, nb, ld, U, nseg, ST, two_panel, nblk;
+  int U_off;          // CTA types [0, U_off) are dispatched first (the costlier off-diagonal tiles)
   int64_t nrows;      // PLAIN/WEIGHTED: n_local rows; FOLD: nq = floor(n_local / K) full groups
   int64_t seg_rows;   // rows (FOLD: groups) per segment, multiple of BK
   int K, off_mod;     // FOLD
@@ -99,7 +112,7 @@ struct Cons {
   uint64_t* full;
   uint64_t* empty;
   uint64_t* ready;    // WEIGHTED: row quantities of the stage are in shared memory
-  int warp, lane, nst, seg, fold, kprime;
+  int warp, lane, nst, seg, fold, kprime, u;
   int64_t r0, r1;
   int a0, b0;
   bool two;
@@ -240,7 +253,7 @@ __device__ __forceinline__ void weighted_rows(const GramParams& P, const Cons& c
   }
   if (lane == 0) { cs.scal_s[2 * rw] = sw; cs.scal_s[2 * rw + 1] = sll; }
   named_bar_sync(1, NRW * 32);
-  if (rw == 0 && lane == 0 && blockIdx.x % P.U == 0) {
+  if (rw == 0 && lane == 0 && cs.u == 0) {
     double a = 0.0, b = 0.0;
     for (int w = 0; w < NRW; ++w) { a += cs.scal_s[2 * w]; b += cs.scal_s[2 * w + 1]; }
     P.partial_scal[cs.seg * 2 + 0] = a;
@@ -253,12 +266,25 @@ __global__ void __launch_bounds__(gram_threads(MODE), (TWO || MODE == MODE_WEIGH
 gram_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ CUtensorMap tmY, const GramParams P) {
   extern __shared__ __align__(128) double smem[];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int u = blockIdx.x % P.U;
-  const int rest = blockIdx.x / P.U;
+  // work items (CTA type u, segment, fold): the U_off costlier types first (longest-processing-
+  // time order keeps the last wave short), each group ordered segment-major so CTAs running
+  // together stream the same rows (L2 reuse across tile types)
+  const int nf = MODE == MODE_FOLD ? P.K : 1;
+  const int off_items = P.U_off * P.nseg * nf;
+  int u, rest;
+  if ((int)blockIdx.x < off_items) {
+    u = blockIdx.x % P.U_off;
+    rest = blockIdx.x / P.U_off;
+  } else {
+    const int b2 = blockIdx.x - off_items, ud = P.U - P.U_off;
+    u = P.U_off + b2 % ud;
+    rest = b2 / ud;
+  }
   __shared__ double scal_s[2 * NRW];
   __shared__ __align__(8) uint64_t ready_s[MAXST];
   Cons cs;
   cs.scal_s = scal_s;
+  cs.u = u;
   cs.seg = rest % P.nseg;
   cs.fold = rest / P.nseg;  // 0 unless MODE_FOLD
   cs.smem = smem;
@@ -351,6 +377,12 @@ gram_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ CUt
     case J_T3: consume<MODE, J_T3>(P, cs); break;
     case J_F48: if (TWO) consume<MODE, J_F48>(P, cs); break;
     case J_T4F4: if (TWO) consume<MODE, J_T4F4>(P, cs); break;
+    case J_F45: if (TWO) consume<MODE, J_F45>(P, cs); break;
+    case J_F46: if (TWO) consume<MODE, J_F46>(P, cs); break;
+    case J_F47: if (TWO) consume<MODE, J_F47>(P, cs); break;
+    case J_T4F1: if (TWO) consume<MODE, J_T4F1>(P, cs); break;
+    case J_T4F2: if (TWO) consume<MODE, J_T4F2>(P, cs); break;
+    case J_T4F3: if (TWO) consume<MODE, J_T4F3>(P, cs); break;
     default: consume<MODE, J_NONE>(P, cs); break;
   }
 }
@@ -433,7 +465,7 @@ __global__ void gram_unpack_kernel(const double* __restrict__ packed, int nfold,
 
 // ------------------------------------------------------------------ host side: plans
 struct GramPlan {
-  int mode = 0, p = 0, nb = 0, ld = 0, two_panel = 0, U = 0, nseg = 0, ST = 0, nblk = 0;
+  int mode = 0, p = 0, nb = 0, ld = 0, two_panel = 0, U = 0, U_off = 0, nseg = 0, ST = 0, nblk = 0;
   int64_t seg_rows = 0;
   size_t smem = 0;
   int stage_doubles = 0, ys_off = 0, ystride = 1, ytma = 1;
@@ -521,8 +553,15 @@ static oem_status build_plan(oem_ctx* ctx, int mode, int p, int64_t nrows, int K
   } else {
     pl.ld = 132;  // 128-column panel + 4 (mod 16 = 4)
     const int np = pl.nb / 16;
+    // off-diagonal tiles (I < J, 256 blocks) first, then the diagonal ones (136 blocks)
+    std::vector<std::pair<int, int>> tiles;
     for (int I = 0; I < np; ++I)
-      for (int J = I; J < np; ++J) {
+      for (int J = I + 1; J < np; ++J) tiles.push_back({I, J});
+    pl.U_off = (int)tiles.size();
+    for (int I = 0; I < np; ++I) tiles.push_back({I, I});
+    for (auto& tij : tiles) {
+      const int I = tij.first, J = tij.second;
+      {
         std::vector<Job> jobs;
         for (int r = 0; r < 4; ++r)
           for (int c = 0; c < 2; ++c) {
@@ -533,10 +572,22 @@ static oem_status build_plan(oem_ctx* ctx, int mode, int p, int64_t nrows, int K
             else if (lc == lr) jobs.push_back(Job{bi0, bj0, J_T4F4, 0});
             else if (lc + 4 == lr) jobs.push_back(Job{bi0, bj0 + 4, J_T4, 0});
           }
-        pack_jobs(jobs, 128 * I, 128 * J, I == J, pl.ctas);
+        // trim blocks beyond the augmented matrix (last panel): block rows/cols >= nb_exact
+        std::vector<Job> kept;
+        for (auto& jb : jobs) {
+          const int R0 = kind_R(jb.kind), C0 = kind_C(jb.kind);
+          const int ru = std::min(R0, nb_exact - jb.bi0), cu = std::min(C0, nb_exact - jb.bj0);
+          if (ru <= 0 || cu <= 0) continue;
+          if (ru == R0 && cu == C0) { kept.push_back(jb); continue; }
+          const int k = kind_of(ru, cu, kind_tri(jb.kind));
+          kept.push_back(Job{jb.bi0, jb.bj0, k != J_NONE ? k : jb.kind, 0});
+        }
+        pack_jobs(kept, 128 * I, 128 * J, I == J, pl.ctas);
       }
+    }
   }
   pl.U = (int)pl.ctas.size();
+  if (!pl.two_panel || pl.U_off == 0) pl.U_off = pl.U;
   // y staging: 1D TMA box (PLAIN/WEIGHTED); FOLD: 2D box [BK][Kpad] over y viewed as [nq][K]
   // (needs K*8 % 16 == 0, i.e. even K), else the producer's lanes load it
   if (mode == MODE_FOLD) {
@@ -559,11 +610,11 @@ static oem_status build_plan(oem_ctx* ctx, int mode, int p, int64_t nrows, int K
   pl.ST = two_per_sm ? st_half : (int)std::min<size_t>(4, (whole - fixed) / ((size_t)pl.stage_doubles * 8));
   if (pl.ST < 2) OEM_FAIL(OEM_ERR_UNSUPPORTED, "gram: stage does not fit shared memory");
   pl.smem = (size_t)pl.ST * pl.stage_doubles * 8 + fixed;
-  // segments: enough (CTA type, segment) items for ~4 waves over the SMs
+  // segments: enough (CTA type, segment) items for ~8 waves over the SMs (short tail)
   const int64_t units = std::max<int64_t>(1, (nrows + BK - 1) / BK);
   const int nfold = mode == MODE_FOLD ? K : 1;
   const int per_sm = two_per_sm ? 2 : 1;
-  int64_t want = (int64_t)ctx->num_sms * per_sm * 4 / std::max(1, pl.U * nfold);
+  int64_t want = (int64_t)ctx->num_sms * per_sm * 8 / std::max(1, pl.U * nfold);
   want = std::max<int64_t>(1, std::min<int64_t>(want, std::max<int64_t>(1, units / 8)));
   pl.seg_rows = ((units + want - 1) / want) * BK;
   pl.nseg = (int)std::max<int64_t>(1, (nrows + pl.seg_rows - 1) / pl.seg_rows);
@@ -689,7 +740,7 @@ oem_status gram_pass(oem_ctx* ctx, int mode, const double* X, const double* y, c
     if (s != OEM_OK) return s;
     GramParams P;
     std::memset(&P, 0, sizeof(P));
-    P.p = p; P.nb = pl.nb; P.ld = pl.ld; P.U = pl.U; P.nseg = pl.nseg; P.ST = pl.ST; P.two_panel = pl.two_panel;
+    P.p = p; P.nb = pl.nb; P.ld = pl.ld; P.U = pl.U; P.U_off = pl.U_off; P.nseg = pl.nseg; P.ST = pl.ST; P.two_panel = pl.two_panel;
     P.nblk = pl.nblk; P.nrows = nq; P.seg_rows = pl.seg_rows; P.K = K;
     P.off_mod = mode == MODE_FOLD ? (int)(((row_offset % K) + K) % K) : 0;
     P.ytma = pl.ytma; P.ystride = pl.ystride;
