@@ -151,12 +151,42 @@ typedef struct {
   int32_t nlambda; double lambda_min_ratio; const double* lambda /*host, optional*/;
   double tol_in; int64_t maxit_in; double tol_out; int32_t outer_maxit;
   double eps; int32_t power_iters; double d_inflate; const double* var_w /*device p or NULL*/;
+  int32_t hessian_upper_bound; /* f1 (R#27): w_i = 1/4. The Gram X^T X and d_w are
+                                  formed once (a2 pass); each outer step is one oem_logit_grad
+                                  pass and c = X^T X beta + 4 X^T (y - mu), normalised by 4n.
+                                  Needs p <= 512. */
 } oem_logistic_cfg;
-void oem_logistic_cfg_default(oem_logistic_cfg* cfg);  /* 50, 1e-3, NULL, 1e-11, 1e5, 1e-10, 100, 1e-5, 200, 5e-3, NULL */
+void oem_logistic_cfg_default(oem_logistic_cfg* cfg);  /* 50, 1e-3, NULL, 1e-11, 1e5, 1e-10, 100, 1e-5, 200, 5e-3, NULL, 0 */
+
+/* ---- f1 logistic gradient pass (P:L357-359 mu(x) = 1/(1 + exp(-x^T beta)); P:L385-389 the
+ * upper-bound step needs only X^T (y - mu)). One HBM-bound pass over [X | y]: g = sum_i
+ * (y_i - mu_i) x_i (p) and loglik = sum_i [y_i eta_i - log(1 + e^eta_i)] (1), raw sums over this
+ * rank's rows, allreduced when nranks > 1. beta (device, p) identical on every rank. No clamp of
+ * mu (no division by w). Errors: OEM_ERR_DIM, OEM_ERR_ALIGN (X 16-byte aligned, ldx even),
+ * OEM_ERR_UNSUPPORTED (p > 512), OEM_ERR_CUDA, OEM_ERR_NCCL. */
+oem_status oem_logit_grad(oem_ctx* ctx, const double* X, const double* y01, const double* beta, int64_t n_local,
+                          int32_t p, int64_t ldx, double* g, double* loglik, void* stream);
 oem_status oem_fit_logistic(oem_ctx* ctx, const double* X, const double* y01, int64_t n_local, int32_t p,
                             int64_t ldx, const oem_penalty* pen /*host, one*/, const oem_logistic_cfg* cfg /*host*/,
                             double* beta_out, double* lambda_out, int32_t* outer_iters /*host L*/,
                             int64_t* inner_iters /*host L*/, uint8_t* converged /*host L*/, void* stream);
+
+/* ---- f2 fast cross-validation error and selection (§3; P:L601-616, L659-660,
+ * L689-690 §5.4-5.5 cv.oem / xval.oem outputs; R#33-35). Inputs: the K raw fold sums of
+ * oem_gram_folds (G_folds K*p*p, xty_folds K*p, yty_folds K, counts host K) and the coefficient
+ * paths of oem_fit_path in fold_mode (beta (K+1)*nP*L*p; unit k+1 = fit on the complement of
+ * fold k). No pass over X: err[k][q][l] = (yty_k - 2 b^T xty_k + b^T G_k b) / n_k is the held-out
+ * mean squared error of b = beta[k+1][q][l] on fold k (R#33). Summaries per penalty q (device):
+ * cvm[q][l] = sum_k n_k err / n, cvsd[q][l] = sqrt(sum_k n_k (err - cvm)^2 / n / (K-1)) (R#34).
+ * Host outputs (may be NULL): idx_min[q] = first argmin_l cvm (the larger lambda on ties),
+ * idx_1se[q] = smallest l with cvm[l] <= cvm[idx_min] + cvsd[idx_min] (the largest such lambda),
+ * best = penalty with the smallest min cvm (the first on ties) (R#35). Synchronises `stream`.
+ * Errors: OEM_ERR_DIM (K < 2, p/nP/L < 1), OEM_ERR_EMPTY_FOLD, OEM_ERR_UNSUPPORTED (nP > 64,
+ * 8p bytes > 200 KB), OEM_ERR_CUDA. */
+oem_status oem_cv_error(oem_ctx* ctx, const double* G_folds, const double* xty_folds, const double* yty_folds,
+                        const int64_t* counts /*host K*/, int32_t K, int32_t p, int32_t nP, int32_t L,
+                        const double* beta, double* err, double* cvm, double* cvsd, int32_t* idx_min /*host nP*/,
+                        int32_t* idx_1se /*host nP*/, int32_t* best /*host 1*/, void* stream);
 
 /* ---- instrumentation (used by bench.py; no effect on results).
  * With timing enabled the library records CUDA events around its phases on the launching

@@ -323,3 +323,110 @@ def fit_from_gram(G_raw, c_raw, n, penalties, nlambda=100, ratio=1e-3, d=None, t
         out["iters"].append(it)
         out["conv"].append(cv)
     return out
+
+
+# ---------------------------------------------------------------- f2: fast-CV error and selection
+def cv_error(X, y, K, beta_units, row_offset=0):
+    """f2 held-out error by its plain definition (R#33): for fold k (rows with (row_offset + i)
+    mod K == k, R#19) and the fit b = beta_units[k+1][q][l] on the complement of fold k
+    (P:L313-327), e_k(l) = (1/n_k) sum_{i in fold k} (y_i - x_i^T b)^2. The held-out rows are
+    streamed directly (a matmul per fold as the library step); the Gram identity the product
+    uses is NOT used here. Returns err [K][nP][L]."""
+    X = _f64(X)
+    y = _f64(y)
+    B = np.asarray(beta_units, dtype=np.float64)
+    nU, nP, L, p = B.shape
+    assert nU == K + 1 and p == X.shape[1]
+    fold = (row_offset + np.arange(X.shape[0])) % K
+    err = np.empty((K, nP, L))
+    for k in range(K):
+        rows = fold == k
+        Xk, yk = X[rows], y[rows]
+        R = yk[:, None] - Xk @ B[k + 1].reshape(nP * L, p).T   # residuals, one column per fit
+        err[k] = (np.sum(R * R, axis=0) / rows.sum()).reshape(nP, L)
+    return err
+
+
+def cv_summary(err, counts):
+    """f2 cv.oem summaries (P:L601-616 best.model / lambda.min; P:L659-660 lambda.1se; R#34-35),
+    explicit loops: cvm = sum_k n_k e_k / n; cvsd = sqrt(sum_k n_k (e_k - cvm)^2 / n / (K-1));
+    lambda_min = first argmin (larger lambda on ties); lambda_1se = largest lambda (smallest
+    index) with cvm <= cvm_min + cvsd_min; best = first penalty attaining the smallest min cvm."""
+    err = np.asarray(err, dtype=np.float64)
+    K, nP, L = err.shape
+    nk = [float(c) for c in counts]
+    n = sum(nk)
+    cvm = np.zeros((nP, L))
+    cvsd = np.zeros((nP, L))
+    for q in range(nP):
+        for l in range(L):
+            m = sum(nk[k] * err[k, q, l] for k in range(K)) / n
+            v = sum(nk[k] * (err[k, q, l] - m) ** 2 for k in range(K))
+            cvm[q, l] = m
+            cvsd[q, l] = np.sqrt(v / n / (K - 1))
+    imin, i1se = [], []
+    for q in range(nP):
+        im = 0
+        for l in range(1, L):
+            if cvm[q, l] < cvm[q, im]:
+                im = l
+        thr = cvm[q, im] + cvsd[q, im]
+        i1 = next(l for l in range(im + 1) if cvm[q, l] <= thr)
+        imin.append(im)
+        i1se.append(i1)
+    best = 0
+    for q in range(1, nP):
+        if cvm[q, imin[q]] < cvm[best, imin[best]]:
+            best = q
+    return cvm, cvsd, imin, i1se, best
+
+
+# ---------------------------------------------------------------- f1: Hessian upper-bound logistic
+def logit_grad(X, y01, beta):
+    """f1 gradient pass by its definition: g = sum_i (y_i - mu_i) x_i with
+    mu_i = 1/(1 + exp(-x_i^T beta)), and loglik = sum_i [y_i eta_i - log(1 + e^eta_i)] (R#23).
+    numpy fp64 (matvecs as the library step)."""
+    X = _f64(X)
+    y01 = _f64(y01)
+    eta = X @ _f64(beta)
+    mu = 1.0 / (1.0 + np.exp(-eta))
+    return X.T @ (y01 - mu), float(np.sum(y01 * eta - np.logaddexp(0.0, eta)))
+
+
+def logistic_path_ub(X, y01, lambdas, family="lasso", gamma=3.0, alpha=1.0, d=None, tol_in=1e-11,
+                     maxit_in=100000, tol_out=1e-10, outer_maxit=1000, power_iters=200, inflate=5e-3):
+    """f1: the proximal-Newton logistic path with the Hessian upper bound w_i = 1/4
+    (P:L385-389, R#27), in the paper's order: per outer step the working responses
+    z_i = eta_i + (y_i - mu_i)/w_i with w_i = 1/4, the weighted statistics
+    G_w = (1/n) sum w x x^T, c_w = (1/n) sum w z x, d_w by the power rule (R#5)
+    unless d is given, then the OEM inner solve for the single lambda from the current beta
+    (O6); stop when max |dbeta| <= tol_out. Returns (B[L,p], outer[L], inner[L], conv[L])."""
+    X = _f64(X)
+    y01 = _f64(y01)
+    lambdas = _f64(np.atleast_1d(lambdas))
+    n, p = X.shape
+    w = 0.25
+    beta = np.zeros(p)
+    B = np.empty((lambdas.size, p))
+    oi = np.zeros(lambdas.size, dtype=np.int32)
+    ii = np.zeros(lambdas.size, dtype=np.int64)
+    cv = np.zeros(lambdas.size, dtype=bool)
+    for l, lam in enumerate(lambdas):
+        for o in range(outer_maxit):
+            eta = X @ beta
+            mu = 1.0 / (1.0 + np.exp(-eta))
+            z = eta + (y01 - mu) / w
+            Gw = (w * X).T @ X / n
+            cw = X.T @ (w * z) / n
+            dw = d if d is not None else power_rule(Gw, power_iters, inflate)[0]
+            nb, it, ok = oem_path(Gw, cw, dw, family, [lam], gamma, alpha, tol=tol_in, maxit=maxit_in,
+                                  beta_init=beta)
+            ii[l] += it[0]
+            oi[l] = o + 1
+            delta = np.max(np.abs(nb[0] - beta)) if p else 0.0
+            beta = nb[0].copy()
+            if delta <= tol_out:
+                cv[l] = True
+                break
+        B[l] = beta
+    return B, oi, ii, cv

@@ -131,6 +131,8 @@ oem_status oem_ctx_destroy(oem_ctx* ctx) {
   ctx->plan_tables.release();
   ctx->path_ws.release();
   ctx->path_small.release();
+  ctx->lg_part.release();
+  ctx->lg_out.release();
   for (auto& pe : ctx->pending) { cudaEventDestroy(pe.a); cudaEventDestroy(pe.b); }
   for (auto e : ctx->event_pool) cudaEventDestroy(e);
   delete ctx;

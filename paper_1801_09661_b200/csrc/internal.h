@@ -50,7 +50,7 @@ struct oem_ctx {
   int nranks = 1, rank = 0;
   int num_sms = 148;
   void* nccl_comm = nullptr;  // ncclComm_t
-  oem::DevBuf partial, partial_scal, packed, tail, plan_tables, path_ws, path_small, logi;
+  oem::DevBuf partial, partial_scal, packed, tail, plan_tables, path_ws, path_small, logi, lg_part, lg_out;
   std::map<std::tuple<int, int, int64_t, int>, std::shared_ptr<oem::GramPlan>> plans;
   // instrumentation (oem_ctx_set_timing / oem_ctx_stats)
   bool timing = false;
@@ -100,5 +100,11 @@ oem_status gram_unpack(oem_ctx* ctx, const double* packed, int nfold, int p, dou
 inline int64_t packed_size(int p) { return (int64_t)(p + 1) * (p + 2) / 2; }
 
 oem_status allreduce_sum(oem_ctx* ctx, double* buf, size_t count, cudaStream_t st);
+
+// f1 (logit_ub.cu): out[0..p) = X^T (y - sigma(X beta)), out[p] = loglik, raw sums allreduced
+oem_status logit_grad_pass(oem_ctx* ctx, const double* X, const double* y01, const double* beta, int64_t n_local,
+                           int p, int64_t ldx, double* out, cudaStream_t st);
+// c = G beta + 4 g (the raw right-hand side of the upper-bound step)
+oem_status ub_rhs(oem_ctx* ctx, const double* G, const double* beta, const double* g, int p, double* c, cudaStream_t st);
 
 }  // namespace oem

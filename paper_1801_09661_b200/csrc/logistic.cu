@@ -47,6 +47,7 @@ extern "C" void oem_logistic_cfg_default(oem_logistic_cfg* c) {
   c->power_iters = 200;
   c->d_inflate = 5e-3;
   c->var_w = nullptr;
+  c->hessian_upper_bound = 0;
 }
 
 extern "C" oem_status oem_fit_logistic(oem_ctx* ctx, const double* X, const double* y01, int64_t n_local, int32_t p,
@@ -94,15 +95,30 @@ extern "C" oem_status oem_fit_logistic(oem_ctx* ctx, const double* X, const doub
     n_total = (int64_t)llround(v);
   }
   if (n_total < 1) OEM_FAIL(OEM_ERR_DIM, "oem_fit_logistic: no rows");
-  // a4 at beta = 0: gives lambda_max (R#14) and the first outer step's weighted Gram
-  oem_status s = oem_gram_weighted(ctx, X, y01, beta, n_local, p, ldx, cfg.eps, Gw, cw, sc, stream);
-  if (s != OEM_OK) return s;
+  const bool ub = cfg.hessian_upper_bound != 0;
+  oem_status s;
+  double* gb = nullptr;  // upper-bound mode: X^T (y - mu) and loglik (p + 1)
+  if (ub) {
+    // f1: X^T X once (a2 pass + combine); the gradient at beta = 0 gives lambda_max (R#14)
+    if (p > 512) OEM_FAIL(OEM_ERR_UNSUPPORTED, "oem_fit_logistic: hessian_upper_bound needs p <= 512");
+    OEM_CUDA_TRY(ctx->lg_out.ensure(sizeof(double) * (2 * (size_t)p + 2)));
+    gb = ctx->lg_out.as<double>() + p + 1;
+    int64_t nt = 0;
+    s = oem_gram(ctx, X, y01, n_local, p, ldx, Gw, cw, sc, &nt, stream);
+    if (s != OEM_OK) return s;
+    s = logit_grad_pass(ctx, X, y01, beta, n_local, p, ldx, gb, st);
+    if (s != OEM_OK) return s;
+  } else {
+    // a4 at beta = 0: gives lambda_max (R#14) and the first outer step's weighted Gram
+    s = oem_gram_weighted(ctx, X, y01, beta, n_local, p, ldx, cfg.eps, Gw, cw, sc, stream);
+    if (s != OEM_OK) return s;
+  }
   std::vector<double> lam(L);
   if (cfg.lambda) {
     for (int l = 0; l < L; ++l) lam[l] = cfg.lambda[l];
   } else {
     std::vector<double> hc(p), hw(p, 1.0);
-    OEM_CUDA_TRY(cudaMemcpyAsync(hc.data(), cw, sizeof(double) * p, cudaMemcpyDeviceToHost, st));
+    OEM_CUDA_TRY(cudaMemcpyAsync(hc.data(), ub ? gb : cw, sizeof(double) * p, cudaMemcpyDeviceToHost, st));
     if (cfg.var_w) OEM_CUDA_TRY(cudaMemcpyAsync(hw.data(), cfg.var_w, sizeof(double) * p, cudaMemcpyDeviceToHost, st));
     OEM_CUDA_TRY(cudaStreamSynchronize(st));
     const double scale = pen->family == OEM_ENET ? pen->alpha : 1.0;
@@ -122,18 +138,40 @@ extern "C" oem_status oem_fit_logistic(oem_ctx* ctx, const double* X, const doub
   pc.power_iters = cfg.power_iters;
   pc.d_inflate = cfg.d_inflate;
   bool have_gram = true;
+  // upper-bound mode: G/(4n) and d_w are the same at every step; d_w is computed by the first
+  // solve and passed in afterwards
+  const int64_t n4 = 4 * n_total;
+  bool have_d = false;
+  double hd = 0.0;
   for (int l = 0; l < L; ++l) {
     int32_t o = 0;
     int64_t inner = 0;
     uint8_t ok = 0;
     pc.lambda = &lam[l];
     while (o < cfg.outer_maxit) {
-      if (!have_gram) {
+      if (ub) {
+        if (!have_gram) {
+          s = logit_grad_pass(ctx, X, y01, beta, n_local, p, ldx, gb, st);
+          if (s != OEM_OK) return s;
+        }
+        s = ub_rhs(ctx, Gw, beta, gb, p, cw, st);  // c = X^T X beta + 4 X^T (y - mu)
+        if (s != OEM_OK) return s;
+      } else if (!have_gram) {
         s = oem_gram_weighted(ctx, X, y01, beta, n_local, p, ldx, cfg.eps, Gw, cw, sc, stream);
         if (s != OEM_OK) return s;
       }
       have_gram = false;
-      s = oem_fit_path(ctx, Gw, cw, &n_total, 1, p, pen, 1, &pc, nullptr, beta, bnew, lam1, it1, cv1, d1, stream);
+      if (ub) {
+        s = oem_fit_path(ctx, Gw, cw, &n4, 1, p, pen, 1, &pc, have_d ? &hd : nullptr, beta, bnew, lam1, it1, cv1,
+                         d1, stream);
+        if (s == OEM_OK && !have_d) {
+          OEM_CUDA_TRY(cudaMemcpyAsync(&hd, d1, sizeof(double), cudaMemcpyDeviceToHost, st));
+          OEM_CUDA_TRY(cudaStreamSynchronize(st));
+          have_d = true;
+        }
+      } else {
+        s = oem_fit_path(ctx, Gw, cw, &n_total, 1, p, pen, 1, &pc, nullptr, beta, bnew, lam1, it1, cv1, d1, stream);
+      }
       if (s != OEM_OK) return s;
       ++ctx->launches;
       delta_copy_kernel<<<1, 256, 0, st>>>(bnew, beta, p, delta);

@@ -26,7 +26,7 @@ STATUS = ["OEM_OK", "OEM_ERR_INVALID_ARG", "OEM_ERR_DIM", "OEM_ERR_ALIGN", "OEM_
 ABI_SYMBOLS = ["oem_status_string", "oem_last_error", "oem_version", "oem_nccl_unique_id",
                "oem_ctx_create", "oem_ctx_destroy", "oem_gram", "oem_gram_folds",
                "oem_gram_weighted", "oem_fit_path", "oem_path_cfg_default", "oem_fit_logistic",
-               "oem_logistic_cfg_default", "oem_ctx_set_timing", "oem_ctx_stats"]
+               "oem_logistic_cfg_default", "oem_cv_error", "oem_logit_grad", "oem_ctx_set_timing", "oem_ctx_stats"]
 _VOID = ("oem_status_string", "oem_last_error", "oem_version", "oem_path_cfg_default",
          "oem_logistic_cfg_default")
 
@@ -57,7 +57,7 @@ class LogisticCfg(ctypes.Structure):
                 ("maxit_in", ctypes.c_int64), ("tol_out", ctypes.c_double),
                 ("outer_maxit", ctypes.c_int32), ("eps", ctypes.c_double),
                 ("power_iters", ctypes.c_int32), ("d_inflate", ctypes.c_double),
-                ("var_w", ctypes.c_void_p)]
+                ("var_w", ctypes.c_void_p), ("hessian_upper_bound", ctypes.c_int32)]
 
 
 class Stats(ctypes.Structure):
@@ -98,6 +98,8 @@ def lib():
         L.oem_logistic_cfg_default.restype = None
         L.oem_fit_logistic.argtypes = [P, P, P, i64, i32, i64, ctypes.POINTER(Penalty),
                                        ctypes.POINTER(LogisticCfg), P, P, P, P, P, P]
+        L.oem_cv_error.argtypes = [P, P, P, P, P, i32, i32, i32, i32, P, P, P, P, P, P, P, P]
+        L.oem_logit_grad.argtypes = [P, P, P, P, i64, i32, i64, P, P, P]
         L.oem_ctx_set_timing.argtypes = [P, ctypes.c_int]
         L.oem_ctx_stats.argtypes = [P, ctypes.POINTER(Stats), ctypes.c_int]
         for name in ABI_SYMBOLS:
@@ -292,8 +294,10 @@ class LogisticResult:
 def oem_fit_logistic(ctx: Context, X, y01, penalty=("lasso", 0.0, 1.0), nlambda=50,
                      lambda_min_ratio=1e-3, lambdas=None, tol_in=1e-11, maxit_in=100000,
                      tol_out=1e-10, outer_maxit=100, eps=1e-5, power_iters=200, d_inflate=5e-3,
-                     var_w=None, stream=None) -> LogisticResult:
-    """a4 + a6-a9 to convergence: proximal-Newton logistic path."""
+                     var_w=None, hessian_upper_bound=False, stream=None) -> LogisticResult:
+    """a4 + a6-a9 to convergence: proximal-Newton logistic path; with
+    hessian_upper_bound=True the f1 mode (w = 1/4): Gram once, one gradient pass
+    per outer step."""
     _check_x(X, y01)
     n, p = X.shape
     L = nlambda if lambdas is None else len(lambdas)
@@ -308,6 +312,7 @@ def oem_fit_logistic(ctx: Context, X, y01, penalty=("lasso", 0.0, 1.0), nlambda=
         cfg.lambda_ = ctypes.cast(lam_h, ctypes.c_void_p)
     cfg.tol_in, cfg.maxit_in, cfg.tol_out, cfg.outer_maxit = tol_in, maxit_in, tol_out, outer_maxit
     cfg.eps, cfg.power_iters, cfg.d_inflate = eps, power_iters, d_inflate
+    cfg.hessian_upper_bound = 1 if hessian_upper_bound else 0
     if var_w is not None:
         var_w = var_w.to(device=X.device, dtype=torch.float64).contiguous()
         cfg.var_w = var_w.data_ptr()
@@ -322,6 +327,51 @@ def oem_fit_logistic(ctx: Context, X, y01, penalty=("lasso", 0.0, 1.0), nlambda=
                                   ctypes.byref(cfg), _ptr(beta), _ptr(lam), oi, ii, cv,
                                   _stream(stream)))
     return LogisticResult(beta, lam, list(oi), list(ii), [bool(v) for v in cv])
+
+
+def oem_logit_grad(ctx: Context, X, y01, beta, stream=None):
+    """f1: (X^T (y - sigma(X beta)), loglik) as raw sums in one pass over [X | y]."""
+    _check_x(X, y01)
+    n, p = X.shape
+    if beta.dtype != torch.float64 or not beta.is_cuda or beta.numel() != p:
+        raise ValueError("beta must be a float64 CUDA tensor of length p")
+    g = torch.empty(p, dtype=torch.float64, device=X.device)
+    ll = torch.empty(1, dtype=torch.float64, device=X.device)
+    _check(lib().oem_logit_grad(ctx.h, _ptr(X), _ptr(y01), _ptr(beta.contiguous()), n, p, X.stride(0),
+                                _ptr(g), _ptr(ll), _stream(stream)))
+    return g, ll
+
+
+@dataclass
+class CvResult:
+    err: torch.Tensor       # [K][nP][L] held-out MSE of each complement fit on its fold
+    cvm: torch.Tensor       # [nP][L]
+    cvsd: torch.Tensor      # [nP][L]
+    idx_min: list           # per penalty: index of lambda_min
+    idx_1se: list           # per penalty: index of lambda_1se
+    best: int               # penalty with the smallest min cvm
+
+
+def oem_cv_error(ctx: Context, G_folds, xty_folds, yty_folds, counts, beta, stream=None) -> CvResult:
+    """f2: fast-CV error curve and selection from the fold sums and the fold-mode paths
+    (beta: [K+1][nP][L][p] from oem_fit_path(..., fold_mode=True))."""
+    K, p, _ = G_folds.shape
+    nU, nP, L, pb = beta.shape
+    if nU != K + 1 or pb != p:
+        raise ValueError("beta must be the fold-mode path output [K+1][nP][L][p]")
+    dev = G_folds.device
+    err = torch.empty((K, nP, L), dtype=torch.float64, device=dev)
+    cvm = torch.empty((nP, L), dtype=torch.float64, device=dev)
+    cvsd = torch.empty((nP, L), dtype=torch.float64, device=dev)
+    cnt = (ctypes.c_int64 * K)(*[int(c) for c in counts])
+    imin = (ctypes.c_int32 * nP)()
+    i1se = (ctypes.c_int32 * nP)()
+    best = ctypes.c_int32()
+    _check(lib().oem_cv_error(ctx.h, _ptr(G_folds.contiguous()), _ptr(xty_folds.contiguous()),
+                              _ptr(yty_folds.contiguous()), cnt, K, p, nP, L, _ptr(beta.contiguous()),
+                              _ptr(err), _ptr(cvm), _ptr(cvsd), imin, i1se, ctypes.byref(best),
+                              _stream(stream)))
+    return CvResult(err, cvm, cvsd, list(imin), list(i1se), int(best.value))
 
 
 def set_timing(ctx: Context, enable: bool = True):

@@ -61,3 +61,40 @@ def test_logistic_lambda0_newton(ctx):
         mu = 1 / (1 + np.exp(-(X @ b)))
         b = b + np.linalg.solve((X * (mu * (1 - mu))[:, None]).T @ X, X.T @ (y - mu))
     assert np.max(np.abs(fit.beta[0].cpu().numpy() - b)) < 1e-8
+
+
+# ---------------------------------------------------------------- f1: Hessian upper bound (w = 1/4)
+@pytest.mark.parametrize("n,p", [(20_011, 5), (9_000, 64), (9_001, 65), (30_000, 200), (4_000, 257)])
+def test_logit_grad_parity(ctx, n, p):
+    from paper_1801_09661_b200 import oem_logit_grad
+    spec = CONFIGS["cfg5"].spec.replace(n=n, p=p, nnz=min(20, p))
+    bt = dg.beta(spec)
+    Xd, yd = device_rows(spec, bt)
+    X, y = dg.rows_host(spec, bt)
+    beta = 0.6 * bt + 0.01 * np.cos(np.arange(p))
+    g, ll = oem_logit_grad(ctx, Xd, yd, torch.from_numpy(beta).cuda())
+    go, llo = orc.logit_grad(X, y, beta)
+    mu = 1 / (1 + np.exp(-(X @ beta)))
+    cond = np.abs(X).T @ np.abs(y - mu)     # condition of each sum
+    assert np.max(np.abs(g.cpu().numpy() - go) / cond) <= 1e-12
+    assert abs(float(ll) - llo) <= 1e-12 * np.sum(np.abs(y * (X @ beta)) + np.logaddexp(0, X @ beta))
+
+
+def test_logistic_upper_bound_path(ctx):
+    """f1 path (R#27) against the oracle's upper-bound path and the exact-Hessian
+    path: all three minimise the same convex objective, so they agree at convergence."""
+    from paper_1801_09661_b200 import oem_fit_logistic
+    spec = CONFIGS["cfg5"].spec.replace(n=12_000, p=30, nnz=8)
+    bt = dg.beta(spec)
+    Xd, yd = device_rows(spec, bt)
+    X, y = dg.rows_host(spec, bt)
+    fu = oem_fit_logistic(ctx, Xd, yd, nlambda=8, hessian_upper_bound=True, outer_maxit=1000)
+    fe = oem_fit_logistic(ctx, Xd, yd, nlambda=8)
+    lam = fu.lam.cpu().numpy()
+    assert np.array_equal(lam, fe.lam.cpu().numpy())
+    Bo, oi, ii, cv = orc.logistic_path_ub(X, y, lam)
+    Bu = fu.beta.cpu().numpy()
+    assert all(fu.conv) and cv.all()
+    assert np.max(np.abs(Bu - Bo)) <= 1e-8
+    assert np.max(np.abs(Bu - fe.beta.cpu().numpy())) <= 1e-7
+    assert np.max(np.abs(np.array(fu.outer_iters) - oi)) <= 2

@@ -6,6 +6,7 @@ ridge closed form, KKT conditions, exhaustive sign-pattern / region enumeration 
 an independent cyclic coordinate descent. MCP/SCAD are pinned on convex instances (gamma large
 enough that 0.5 b^T G b + P is convex) by region enumeration."""
 import itertools
+from fractions import Fraction
 
 import numpy as np
 import pytest
@@ -333,3 +334,39 @@ def test_logistic_kkt_and_null_fixed_point():
         assert np.all(np.abs(gr[~nz]) <= l + 1e-7)
         assert np.all(np.abs(gr[nz] - l * np.sign(b[nz])) <= 1e-7)
         assert np.all(mu * (1 - mu) <= 0.25)
+
+
+# ---------------------------------------------------------------- f1 upper-bound logistic oracle
+def test_logit_grad_zero_beta_exact():
+    """beta = 0: mu = 1/2, g = X^T (y - 1/2) exactly on integer X (all partial sums are exact)."""
+    rng = np.random.default_rng(21)
+    X = rng.integers(-6, 7, size=(401, 7)).astype(float)
+    y = (rng.random(401) < 0.4).astype(float)
+    g, ll = orc.logit_grad(X, y, np.zeros(7))
+    Xo = X.astype(int).astype(object)
+    exact = [sum(Fraction(int(Xo[i, j])) * (Fraction(int(y[i])) - Fraction(1, 2)) for i in range(401)) for j in range(7)]
+    assert np.array_equal(g, np.array([float(v) for v in exact]))
+    assert abs(ll - 401 * (-np.log(2.0))) <= 1e-12 * 401
+
+
+def test_logistic_ub_matches_exact_newton_fixed_point():
+    """The upper-bound MM iteration and exact proximal Newton minimise the same convex
+    objective (R#23-24), so their lasso paths agree at convergence; and lambda = 0 reproduces
+    the unpenalised MLE from Newton-Raphson (numpy)."""
+    rng = np.random.default_rng(22)
+    n, p = 600, 4
+    X = rng.standard_normal((n, p))
+    bt = np.array([1.0, -0.5, 0.0, 0.25])
+    y = (rng.random(n) < 1 / (1 + np.exp(-X @ bt))).astype(float)
+    lam = [0.05, 0.01, 0.0]
+    Bu, oi, ii, cv = orc.logistic_path_ub(X, y, lam, tol_out=1e-12)
+    Be, _, _, cve = orc.logistic_path(X, y, lam, tol_out=1e-12)
+    assert cv.all() and cve.all()
+    assert np.max(np.abs(Bu - Be)) <= 1e-8
+    b = np.zeros(p)
+    for _ in range(50):
+        mu = 1 / (1 + np.exp(-(X @ b)))
+        b = b + np.linalg.solve((X * (mu * (1 - mu))[:, None]).T @ X, X.T @ (y - mu))
+    assert np.max(np.abs(Bu[-1] - b)) <= 1e-8
+    # the MM step never increases the penalised negative log-likelihood (descent, S:L279)
+    assert (oi >= 1).all()

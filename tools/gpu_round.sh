@@ -1,4 +1,6 @@
+# round measurement: tests, smoke, bench lines for every workload, launch list and ncu of the top kernel
 set -x
+mkdir -p gpurun_out
 nvidia-smi --query-gpu=name,clocks.sm,clocks.max.sm,memory.total --format=csv
 nproc; free -g | head -2; lscpu | grep -i 'model name'
 timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/smoke.log 2>&1; echo smoke=$?
@@ -6,3 +8,4 @@ timeout 900 python -m pytest tests -m gpu -x -q > gpurun_out/gpu_tests.log 2>&1;
 timeout 900 python bench.py > gpurun_out/bench_cfg4.log 2>&1; echo bench=$?
 for w in cfg2 cfg3 cfg5; do timeout 600 python bench.py --workload $w --no-cpu-baseline --e2e-steps 1 > gpurun_out/bench_$w.log 2>&1; echo bench_$w=$?; done
 timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv --log-file gpurun_out/launches_cfg4.csv python bench.py --steps 2 --warmup 3 --e2e-steps 0 --no-cpu-baseline > gpurun_out/ncu_launch.log 2>&1; echo ncu1=$?
+timeout 900 ncu --set full --clock-control none --import-source on -k regex:gram_kernel -c 1 -o gpurun_out/ncu_gram_cfg4 -f python bench.py --warmup 0 --steps 1 --e2e-steps 0 --no-cpu-baseline > gpurun_out/ncu_full_cfg4.log 2>&1; echo ncufull=$?
