@@ -96,7 +96,9 @@ oem_status oem_gram_weighted(oem_ctx* ctx, const double* X, const double* y01, c
  * P:L239-289 thresholding M-steps; §5.2 several penalties share A and X^T y).
  * Penalty families of Table 1, update equations at P:L243-289. */
 typedef enum { OEM_LASSO = 0, OEM_ENET = 1, OEM_MCP = 2, OEM_SCAD = 3,
-               OEM_GRP_LASSO = 4, OEM_GRP_MCP = 5, OEM_GRP_SCAD = 6 } oem_family;
+               OEM_GRP_LASSO = 4, OEM_GRP_MCP = 5, OEM_GRP_SCAD = 6,
+               OEM_SGL = 7 /* sparse group lasso (Table 1), tau in the alpha field;
+                              exact d-scaled composition of the two proximal maps (R#11) */ } oem_family;
 typedef struct { int32_t family; double gamma; double alpha; } oem_penalty;
 typedef struct {
   int32_t nlambda;          /* L >= 1 */

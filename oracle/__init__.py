@@ -23,9 +23,10 @@ import numpy as np
 _HERE = os.path.dirname(os.path.abspath(__file__))
 _SO = os.path.join(_HERE, "liboracle.so")
 
-LASSO, ENET, MCP, SCAD, GRP_LASSO, GRP_MCP, GRP_SCAD = range(7)
+LASSO, ENET, MCP, SCAD, GRP_LASSO, GRP_MCP, GRP_SCAD, SGL = range(8)
 FAMILY = {"lasso": LASSO, "enet": ENET, "mcp": MCP, "scad": SCAD,
-          "grp_lasso": GRP_LASSO, "grp_mcp": GRP_MCP, "grp_scad": GRP_SCAD}
+          "grp_lasso": GRP_LASSO, "grp_mcp": GRP_MCP, "grp_scad": GRP_SCAD,
+          "sgl": SGL}   # sparse group lasso: tau is passed as alpha (R#11)
 
 
 def build(force: bool = False) -> str:
@@ -64,6 +65,7 @@ def lib():
             "orc_grp_lasso": (None, [p, i32, d, d, p]),
             "orc_grp_mcp": (None, [p, i32, d, d, d, p]),
             "orc_grp_scad": (None, [p, i32, d, d, d, p]),
+            "orc_sgl": (None, [p, p, i32, d, d, d, d, p]),
             "orc_lambda_max": (d, [ctypes.c_int, d, p, i32, p, p, i32, p]),
             "orc_lambda_grid": (None, [d, i32, d, p]),
             "orc_oem_path": (ctypes.c_int, [p, p, i32, d, ctypes.c_int, d, d, p, p, i32, p, p, i32,
@@ -223,6 +225,14 @@ def grp_scad(u, lam, gamma, d):
     u = _f64(u)
     out = np.empty_like(u)
     lib().orc_grp_scad(_ptr(u), u.size, lam, gamma, d, _ptr(out))
+    return out
+
+
+def sgl(u, lam, tau, c, d, w=None):
+    """Sparse group lasso M-step for one group, exact d-scaled composition (R#11)."""
+    u = _f64(u)
+    out = np.empty_like(u)
+    lib().orc_sgl(_ptr(u), _ptr(_f64(w)), u.size, lam, tau, c, d, _ptr(out))
     return out
 
 

@@ -325,8 +325,43 @@ void orc_grp_scad(const double* u, int32_t m, double lam, double gamma, double d
   for (int32_t i = 0; i < m; ++i) out[i] = s * u[i];
 }
 
+/* Sparse group lasso (P:L291-297 eq sglasso). The printed G(v, c lam (1 - tau), 1) is the
+   proximal map only at d = 1; the M-step minimises (d/2)||b||^2 - u^T b + lam tau sum w|b| +
+   lam (1 - tau) c ||b||, whose minimiser is the soft threshold followed by the group shrink of
+   v = S(u, w lam tau, d) at level c lam (1 - tau) / d (R#11). */
+void orc_sgl(const double* u, const double* w, int32_t m, double lam, double tau, double c, double d, double* out) {
+  for (int32_t i = 0; i < m; ++i) out[i] = orc_soft(u[i], (w ? w[i] : 1.0) * lam * tau, d);
+  double nv = norm2(out, m);
+  double f = nv > 0.0 ? pos(1.0 - c * lam * (1.0 - tau) / (d * nv)) : 0.0;
+  for (int32_t i = 0; i < m; ++i) out[i] *= f;
+}
+
 /* ---------------- lambda grid ---------------- */
 static int is_group(int family) { return family >= ORC_GRP_LASSO; }
+
+/* sparse group lasso: the smallest lambda at which beta_g = 0 is a fixed point from beta = 0 is
+   the root of ||S(c_g, lam tau w_g, 1)|| = lam (1 - tau) c_g (decreasing in lam), by bisection
+   (R#36) */
+static double sgl_group_lmax(const double* cg_vec, const double* wg, int32_t m, double cg, double tau) {
+  double hi = 0.0;
+  for (int32_t i = 0; i < m; ++i) {
+    double wi = wg ? wg[i] : 1.0;
+    if (tau > 0.0 && wi > 0.0) hi = fmax(hi, fabs(cg_vec[i]) / (tau * wi));
+  }
+  if (tau < 1.0 && cg > 0.0) hi = fmax(hi, norm2(cg_vec, m) / ((1.0 - tau) * cg));
+  double lo = 0.0;
+  for (int it = 0; it < 200 && hi > lo; ++it) {
+    double mid = 0.5 * (lo + hi);
+    if (mid <= lo || mid >= hi) break;
+    double s = 0.0;
+    for (int32_t i = 0; i < m; ++i) {
+      double t = pos(fabs(cg_vec[i]) - mid * tau * (wg ? wg[i] : 1.0));
+      s += t * t;
+    }
+    if (sqrt(s) > mid * (1.0 - tau) * cg) lo = mid; else hi = mid;
+  }
+  return hi * (1.0 + 1e-12);  /* R#36: clear of the rounding at the root, so the operator is exactly 0 there */
+}
 
 static double group_weight(const int32_t* group, int32_t p, int32_t g, const double* grp_w) {
   if (grp_w) return grp_w[g];
@@ -338,6 +373,21 @@ static double group_weight(const int32_t* group, int32_t p, int32_t g, const dou
 double orc_lambda_max(int family, double alpha, const double* c, int32_t p, const double* w,
                       const int32_t* group, int32_t ngroups, const double* grp_w) {
   double lmax = 0.0;
+  if (family == ORC_SGL) {
+    double* cgv = (double*)malloc(sizeof(double) * (size_t)p);
+    double* wgv = (double*)malloc(sizeof(double) * (size_t)p);
+    for (int32_t g = 0; g < ngroups; ++g) {
+      double cg = group_weight(group, p, g, grp_w);
+      int32_t m = 0;
+      for (int32_t j = 0; j < p; ++j)
+        if (group[j] == g) { cgv[m] = c[j]; wgv[m] = w ? w[j] : 1.0; ++m; }
+      double v = sgl_group_lmax(cgv, wgv, m, cg, alpha);
+      if (v > lmax) lmax = v;
+    }
+    free(cgv);
+    free(wgv);
+    return lmax;
+  }
   if (is_group(family)) {
     for (int32_t g = 0; g < ngroups; ++g) {
       double cg = group_weight(group, p, g, grp_w);
@@ -383,12 +433,14 @@ static void threshold_all(int family, const double* u, int32_t p, double d, doub
   }
   double* ug = (double*)malloc(sizeof(double) * (size_t)p);
   double* og = (double*)malloc(sizeof(double) * (size_t)p);
+  double* wg = (double*)malloc(sizeof(double) * (size_t)p);
   for (int32_t g = 0; g < ngroups; ++g) {
     int32_t m = 0;
     for (int32_t j = 0; j < p; ++j)
-      if (group[j] == g) ug[m++] = u[j];
+      if (group[j] == g) { wg[m] = w ? w[j] : 1.0; ug[m++] = u[j]; }
     double lam = group_weight(group, p, g, grp_w) * lambda;
-    if (family == ORC_GRP_LASSO) orc_grp_lasso(ug, m, lam, d, og);
+    if (family == ORC_SGL) orc_sgl(ug, wg, m, lambda, alpha, group_weight(group, p, g, grp_w), d, og);
+    else if (family == ORC_GRP_LASSO) orc_grp_lasso(ug, m, lam, d, og);
     else if (family == ORC_GRP_MCP) orc_grp_mcp(ug, m, lam, gamma, d, og);
     else orc_grp_scad(ug, m, lam, gamma, d, og);
     m = 0;
@@ -397,6 +449,7 @@ static void threshold_all(int family, const double* u, int32_t p, double d, doub
   }
   free(ug);
   free(og);
+  free(wg);
 }
 
 int orc_oem_path(const double* G, const double* c, int32_t p, double d, int family, double gamma,
@@ -408,6 +461,7 @@ int orc_oem_path(const double* G, const double* c, int32_t p, double d, int fami
   if (family == ORC_SCAD || family == ORC_GRP_SCAD) { if (!(gamma > 2.0) || !((gamma - 1.0) * d > 1.0)) return -1; }
   if (family == ORC_ENET && !(alpha >= 0.0 && alpha <= 1.0)) return -1;
   if (is_group(family) && (!group || ngroups < 1)) return -1;
+  if (family == ORC_SGL && !(alpha >= 0.0 && alpha <= 1.0)) return -1;
   double* beta = (double*)malloc(sizeof(double) * (size_t)p);
   double* u = (double*)malloc(sizeof(double) * (size_t)p);
   double* nb = (double*)malloc(sizeof(double) * (size_t)p);
@@ -480,7 +534,11 @@ double orc_objective(const double* G, const double* c, int32_t p, const double* 
       for (int32_t j = 0; j < p; ++j)
         if (group[j] == g) s += beta[j] * beta[j];
       double nb = sqrt(s), cg = group_weight(group, p, g, grp_w);
-      if (family == ORC_GRP_LASSO) pen += lambda * cg * nb;
+      if (family == ORC_SGL) {  /* Table 1: lam (1 - tau) sum c_k ||b_g|| + lam tau sum w_j |b_j| */
+        pen += lambda * (1.0 - alpha) * cg * nb;
+        for (int32_t j = 0; j < p; ++j)
+          if (group[j] == g) pen += lambda * alpha * (w ? w[j] : 1.0) * fabs(beta[j]);
+      } else if (family == ORC_GRP_LASSO) pen += lambda * cg * nb;
       else if (family == ORC_GRP_MCP) pen += p_mcp(nb, lambda * cg, gamma); /* R#9: no extra leading lambda */
       else pen += p_scad(nb, lambda * cg, gamma);
     }

@@ -64,10 +64,14 @@ double orc_scad(double u, double lam, double gamma, double d);            /* eq 
 /* group forms: u (m), out (m) */
 void orc_grp_lasso(const double* u, int32_t m, double lam, double d, double* out);            /* eq (glasso) */
 void orc_grp_mcp(const double* u, int32_t m, double lam, double gamma, double d, double* out); /* eq (gmcp) */
+/* sparse group lasso M-step, exact d-scaled composition (R#11): v_i = S(u_i, w_i lam tau, d),
+   out = v (1 - c lam (1 - tau) / (d ||v||))_+ ; w may be NULL (= 1) */
+void orc_sgl(const double* u, const double* w, int32_t m, double lam, double tau, double c, double d, double* out);
 void orc_grp_scad(const double* u, int32_t m, double lam, double gamma, double d, double* out);/* eq (gscad) */
 
 /* ---- penalty families (Table 1) ---- */
-enum { ORC_LASSO = 0, ORC_ENET = 1, ORC_MCP = 2, ORC_SCAD = 3, ORC_GRP_LASSO = 4, ORC_GRP_MCP = 5, ORC_GRP_SCAD = 6 };
+enum { ORC_LASSO = 0, ORC_ENET = 1, ORC_MCP = 2, ORC_SCAD = 3, ORC_GRP_LASSO = 4, ORC_GRP_MCP = 5, ORC_GRP_SCAD = 6,
+       ORC_SGL = 7 /* sparse group lasso, tau passed as alpha (R#11) */ };
 
 /* lambda_max (R#14): smallest lambda for which beta = 0 is a fixed point. c is the normalized
  * X^T y / n. w: p or NULL (=1). group: p ids or NULL; grp_w: ngroups or NULL (= sqrt(size), R#12). */

@@ -131,6 +131,44 @@ __device__ __forceinline__ double th_coord(int fam, double u, double lam, double
   }
 }
 
+// Sparse group lasso (eq sglasso; Table 1 with tau in the alpha field): the M-step
+// minimiser is v_r = S(u_r, w_r lam tau, d) followed by the group shrink at level
+// c lam (1 - tau) / d (exact composition, R#11). Returns f with beta_r = f * v_r.
+__device__ __forceinline__ double sgl_factor(const double* ug, int a, int b, int stride, const double* wv, int wj0,
+                                            double lam, double tau, double c, double d) {
+  double s = 0.0;
+  for (int r = a; r < b; ++r) {
+    const double v = th_soft(ug[(size_t)r * stride], (wv ? wv[wj0 + r] : 1.0) * lam * tau, d);
+    s += v * v;
+  }
+  const double nv = sqrt(s);
+  return nv > 0.0 ? pos(1.0 - c * lam * (1.0 - tau) / (d * nv)) : 0.0;
+}
+// lambda_max of one group for the sparse group lasso (R#36): root of
+// ||S(c_g, lam tau w_g, 1)|| = lam (1 - tau) c_g by bisection, nudged clear of the rounding
+__device__ double sgl_lmax_group(const double* cc, int a, int b, const double* wv, double cg, double tau) {
+  double hi = 0.0, s = 0.0;
+  for (int j = a; j < b; ++j) {
+    const double wj = wv ? wv[j] : 1.0;
+    if (tau > 0.0 && wj > 0.0) hi = fmax(hi, fabs(cc[j]) / (tau * wj));
+    s += cc[j] * cc[j];
+  }
+  if (tau < 1.0 && cg > 0.0) hi = fmax(hi, sqrt(s) / ((1.0 - tau) * cg));
+  double lo = 0.0;
+  for (int it = 0; it < 200 && hi > lo; ++it) {
+    const double mid = 0.5 * (lo + hi);
+    if (mid <= lo || mid >= hi) break;
+    double t2 = 0.0;
+    for (int j = a; j < b; ++j) {
+      const double t = pos(fabs(cc[j]) - mid * tau * (wv ? wv[j] : 1.0));
+      t2 += t * t;
+    }
+    if (sqrt(t2) > mid * (1.0 - tau) * cg) lo = mid;
+    else hi = mid;
+  }
+  return hi * (1.0 + 1e-12);
+}
+
 __device__ __forceinline__ void atomic_max_pos(unsigned long long* slot, double v) {
   // v >= 0: IEEE order equals unsigned-integer order of the bit patterns
   atomicMax(slot, (unsigned long long)__double_as_longlong(v));
@@ -352,6 +390,9 @@ __global__ void __launch_bounds__(PT, 1) path_kernel(const PathParams P) {
     double lm = 0.0;
     if (P.lmax_override) {
       lm = *P.lmax_override;
+    } else if (fam == OEM_SGL) {
+      for (int g = 0; g < P.ngroups; ++g)
+        lm = fmax(lm, sgl_lmax_group(cc, P.g_start[g], P.g_end[g], P.var_w, P.g_w[g], P.alp[q]));
     } else if (fam >= OEM_GRP_LASSO) {
       for (int g = 0; g < P.ngroups; ++g) {
         const double cg = P.g_w[g];
@@ -452,7 +493,12 @@ __global__ void __launch_bounds__(PT, 1) path_kernel(const PathParams P) {
         const double nu = sqrt(s);
         const double lam = P.g_w[gid] * s_lam[q];
         const int fam = P.fam[q];
-        if (fam == OEM_GRP_LASSO) {
+        if (fam == OEM_SGL) {
+          const double tau = P.alp[q];
+          const double f = sgl_factor(ug, a, b, 1, P.var_w, v.j0, s_lam[q], tau, P.g_w[gid], d);
+          for (int r = a; r < b; ++r)
+            ug[r] = f * th_soft(ug[r], (P.var_w ? P.var_w[v.j0 + r] : 1.0) * s_lam[q] * tau, d);
+        } else if (fam == OEM_GRP_LASSO) {
           const double f = nu > 0.0 ? pos(1.0 - lam / nu) : 0.0;     // (u/d)(1 - c lam/||u||)_+
           for (int r = a; r < b; ++r) ug[r] = ug[r] / d * f;
         } else {
@@ -797,6 +843,9 @@ __global__ void __launch_bounds__(PT, 1) fit_lean_kernel(const PathParams P, con
       const double* cc = P.shared_grid ? P.cn : cu;
       if (P.lmax_override) {
         lm = *P.lmax_override;
+      } else if (fam == OEM_SGL) {
+        for (int gg = lane; gg < P.ngroups; gg += 32)
+          lm = fmax(lm, sgl_lmax_group(cc, P.g_start[gg], P.g_end[gg], P.var_w, P.g_w[gg], aq));
       } else if (fam >= OEM_GRP_LASSO) {
         for (int gg = lane; gg < P.ngroups; gg += 32) {
           const double cg = P.g_w[gg];
@@ -932,10 +981,13 @@ __global__ void __launch_bounds__(PT, 1) fit_lean_kernel(const PathParams P, con
         const int fam = s_fam[q];
         const double gq = s_gam[q], lw = gw_s[gl] * lq;
         double f;
-        if (fam == OEM_GRP_LASSO) f = nu > 0.0 ? pos(1.0 - lw / nu) : 0.0;
+        const double tau = s_alp[q];
+        if (fam == OEM_SGL) f = sgl_factor(ug, ra, rb, 1, P.var_w, j0, lq, tau, gw_s[gl], d);
+        else if (fam == OEM_GRP_LASSO) f = nu > 0.0 ? pos(1.0 - lw / nu) : 0.0;
         else f = nu > 0.0 ? (fam == OEM_GRP_MCP ? th_mcp(nu, lw, gq, d) : th_scad(nu, lw, gq, d)) / nu : 0.0;
         for (int r = ra; r < rb; ++r) {
-          const double nb = fam == OEM_GRP_LASSO ? ug[r] / d * f : f * ug[r];
+          const double nb = fam == OEM_SGL ? f * th_soft(ug[r], (P.var_w ? P.var_w[j0 + r] : 1.0) * lq * tau, d)
+                          : fam == OEM_GRP_LASSO ? ug[r] / d * f : f * ug[r];
           const int vi = vix<NPT>(q, j0 + r, pvl);
           if (!(fabs(nb - vc[vi]) <= P.tol)) bits |= 1u << q;
           if (C == 1) vn[vi] = nb;
@@ -1153,6 +1205,9 @@ __global__ void __launch_bounds__(PT, 1) fit_cluster_kernel(const PathParams P, 
     double lm = 0.0;
     if (P.lmax_override) {
       lm = *P.lmax_override;
+    } else if (fam == OEM_SGL) {
+      for (int g = 0; g < P.ngroups; ++g)
+        lm = fmax(lm, sgl_lmax_group(cc, P.g_start[g], P.g_end[g], P.var_w, P.g_w[g], P.alp[q]));
     } else if (fam >= OEM_GRP_LASSO) {
       for (int g = 0; g < P.ngroups; ++g) {
         const double cg = P.g_w[g];
@@ -1282,11 +1337,17 @@ __global__ void __launch_bounds__(PT, 1) fit_cluster_kernel(const PathParams P, 
             if (qq == q) { lamq = lam[qq]; gq = gamq[qq]; fam = famq[qq]; }
           const double lw = gw_s[gl] * lamq;
           double f;
-          if (fam == OEM_GRP_LASSO) f = nu > 0.0 ? pos(1.0 - lw / nu) : 0.0;
+          double tau = 0.0;
+#pragma unroll
+          for (int qq = 0; qq < NPT; ++qq)
+            if (qq == q) tau = alpq[qq];
+          if (fam == OEM_SGL) f = sgl_factor(ug, a, b, 1, P.var_w, j0, lamq, tau, gw_s[gl], d);
+          else if (fam == OEM_GRP_LASSO) f = nu > 0.0 ? pos(1.0 - lw / nu) : 0.0;
           else f = nu > 0.0 ? (fam == OEM_GRP_MCP ? th_mcp(nu, lw, gq, d) : th_scad(nu, lw, gq, d)) / nu : 0.0;
           double m = 0.0;
           for (int r = a; r < b; ++r) {
-            const double nb = fam == OEM_GRP_LASSO ? ug[r] / d * f : f * ug[r];
+            const double nb = fam == OEM_SGL ? f * th_soft(ug[r], (P.var_w ? P.var_w[j0 + r] : 1.0) * lamq * tau, d)
+                            : fam == OEM_GRP_LASSO ? ug[r] / d * f : f * ug[r];
             const int j = j0 + r;
             m = fmax(m, fabs(nb - vc[q * A.pv + j]));
             if (C == 1) vn[q * A.pv + j] = nb;
@@ -1623,7 +1684,9 @@ extern "C" oem_status oem_fit_path(oem_ctx* ctx, const double* G, const double* 
   bool any_grp = false;
   for (int q = 0; q < nP; ++q) {
     const int f = pens[q].family;
-    if (f < OEM_LASSO || f > OEM_GRP_SCAD) OEM_FAIL(OEM_ERR_INVALID_ARG, "oem_fit_path: unknown penalty family");
+    if (f < OEM_LASSO || f > OEM_SGL) OEM_FAIL(OEM_ERR_INVALID_ARG, "oem_fit_path: unknown penalty family");
+    if (f == OEM_SGL && !(pens[q].alpha >= 0.0 && pens[q].alpha <= 1.0))
+      OEM_FAIL(OEM_ERR_INVALID_ARG, "oem_fit_path: sparse group lasso tau (alpha field) outside [0,1]");
     if (f >= OEM_GRP_LASSO) any_grp = true;
     if (f == OEM_ENET && !(pens[q].alpha >= 0.0 && pens[q].alpha <= 1.0))
       OEM_FAIL(OEM_ERR_INVALID_ARG, "oem_fit_path: elastic-net alpha outside [0,1]");

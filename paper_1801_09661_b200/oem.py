@@ -16,9 +16,10 @@ import torch
 _PKG = os.path.dirname(os.path.abspath(__file__))
 LIBOEM = os.path.join(_PKG, "liboem.so")
 
-OEM_LASSO, OEM_ENET, OEM_MCP, OEM_SCAD, OEM_GRP_LASSO, OEM_GRP_MCP, OEM_GRP_SCAD = range(7)
+OEM_LASSO, OEM_ENET, OEM_MCP, OEM_SCAD, OEM_GRP_LASSO, OEM_GRP_MCP, OEM_GRP_SCAD, OEM_SGL = range(8)
 FAMILY = {"lasso": OEM_LASSO, "enet": OEM_ENET, "mcp": OEM_MCP, "scad": OEM_SCAD,
-          "grp_lasso": OEM_GRP_LASSO, "grp_mcp": OEM_GRP_MCP, "grp_scad": OEM_GRP_SCAD}
+          "grp_lasso": OEM_GRP_LASSO, "grp_mcp": OEM_GRP_MCP, "grp_scad": OEM_GRP_SCAD,
+          "sgl": OEM_SGL}   # sparse group lasso: (family, gamma unused, tau)
 STATUS = ["OEM_OK", "OEM_ERR_INVALID_ARG", "OEM_ERR_DIM", "OEM_ERR_ALIGN", "OEM_ERR_EMPTY_FOLD",
           "OEM_ERR_NONFINITE", "OEM_ERR_CUDA", "OEM_ERR_NCCL", "OEM_ERR_NOMEM", "OEM_ERR_UNSUPPORTED"]
 

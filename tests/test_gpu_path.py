@@ -210,3 +210,40 @@ def test_maxit_flag_not_error(ctx):
     B, it, cv = orc.oem_path(Go / n, co / n, float(fit.d[0]), "lasso", fit.lam[0, 0].cpu().numpy(), maxit=3)
     assert np.max(np.abs(fit.beta[0, 0].cpu().numpy() - B)) <= 1e-12
     assert np.array_equal(fit.iters[0, 0].cpu().numpy(), it)
+
+
+@pytest.mark.parametrize("p,solver", [(100, None), (100, "cluster"), (120, "global"), (400, None)])
+def test_sparse_group_lasso(ctx, p, solver, monkeypatch):
+    """f3 sparse group lasso (exact composition R#11, lambda_max R#36) on every
+    solver kernel (lean / cluster / global), with non-contiguous groups, group and variable
+    weights, against the oracle at the GPU's d and lambda grid."""
+    from paper_1801_09661_b200 import oem_fit_path, oem_gram
+    if solver:
+        monkeypatch.setenv("OEM_PATH_SOLVER", solver)
+    rng = np.random.default_rng(p)
+    spec = CONFIGS["cfg2"].spec.replace(n=6000, p=p, nnz=min(10, p))
+    bt = dg.beta(spec)
+    X, y = dg.rows_host(spec, bt)
+    Xp = np.zeros((X.shape[0], p + (p & 1)))
+    Xp[:, :p] = X
+    G, c, yy, n = oem_gram(ctx, torch.from_numpy(Xp).cuda()[:, :p], torch.from_numpy(y).cuda())
+    Go, co, _ = orc.gram(X, y)
+    ng = p // 8
+    grp = rng.integers(0, ng, size=p).astype(np.int32)
+    grp[:ng] = np.arange(ng)
+    gw = rng.uniform(0.5, 2.0, ng)
+    w = rng.uniform(0.5, 1.5, p)
+    pens = [("sgl", 0.0, 0.3), ("sgl", 0.0, 0.7), ("grp_lasso", 0.0, 1.0)]
+    fit = oem_fit_path(ctx, G, c, [n], pens, nlambda=20, group=grp, ngroups=ng, grp_w=gw,
+                       var_w=torch.from_numpy(w).cuda())
+    d = float(fit.d[0])
+    for q, (fam, gamma, alpha) in enumerate(pens):
+        lg = fit.lam[0, q].cpu().numpy()
+        lmax = orc.lambda_max(fam, co / n, w=w, group=grp, ngroups=ng, grp_w=gw, alpha=alpha)
+        assert abs(lg[0] - lmax) <= 1e-12 * lmax, (fam, lg[0], lmax)
+        B, it, cv = orc.oem_path(Go / n, co / n, d, fam, lg, gamma, alpha, w=w, group=grp, ngroups=ng,
+                                 grp_w=gw)
+        Bg = fit.beta[0, q].cpu().numpy()
+        assert np.max(np.abs(Bg - B)) <= TOL_BETA, (fam, np.max(np.abs(Bg - B)))
+        assert np.array_equal(fit.conv[0, q].cpu().numpy().astype(bool), cv)
+        assert np.max(np.abs(Bg[0])) <= 1e-12   # lambda_max: null up to the rounding at the root

@@ -184,3 +184,71 @@ def test_group_zero_norm():
     assert not orc.grp_lasso(z, 1.0, 2.0).any()
     assert not orc.grp_mcp(z, 1.0, 3.0, 2.0).any()
     assert not orc.grp_scad(z, 1.0, 3.7, 2.0).any()
+
+
+# ---------------------------------------------------------------- sparse group lasso (f3, R#11)
+def _sgl_objective(b, u, lam, tau, c, d, w):
+    return 0.5 * d * b @ b - u @ b + lam * tau * np.sum(w * np.abs(b)) + lam * (1 - tau) * c * np.linalg.norm(b)
+
+
+def test_sgl_paper_formula_at_d1():
+    """At d = 1 the operator is the paper's printed composition G(v, c lam (1 - tau), 1) with
+    v_j = S(u_j, w_j lam tau, 1), written out here from the equations."""
+    rng = np.random.default_rng(31)
+    for _ in range(200):
+        m = int(rng.integers(1, 6))
+        u = rng.normal(0, 2, m)
+        w = rng.uniform(0.5, 2.0, m)
+        lam, tau, c = rng.uniform(0.05, 1.5), rng.uniform(0, 1), rng.uniform(0.5, 3)
+        v = np.sign(u) * np.maximum(np.abs(u) - w * lam * tau, 0.0)          # eq (lasso), d = 1
+        nv = np.linalg.norm(v)
+        g = v * max(0.0, 1 - c * lam * (1 - tau) / nv) if nv > 0 else 0 * v  # eq (glasso), d = 1
+        assert np.allclose(orc.sgl(u, lam, tau, c, 1.0, w), g, rtol=0, atol=1e-15)
+
+
+def test_sgl_is_the_exact_prox_at_any_d():
+    """For d in {2, 3} the composed operator minimises the M-step objective
+    (d/2)||b||^2 - u^T b + P_sgl(b) (numeric minimiser, Nelder-Mead from the closed form and from
+    zero); the printed d = 1 composition does not (R#11)."""
+    from scipy.optimize import minimize
+    rng = np.random.default_rng(32)
+    worse = 0
+    for _ in range(60):
+        m = int(rng.integers(2, 4))
+        u = rng.normal(0, 3, m)
+        w = rng.uniform(0.5, 1.5, m)
+        lam, tau, c, d = rng.uniform(0.1, 1.0), rng.uniform(0.1, 0.9), rng.uniform(0.5, 2), float(rng.choice([2.0, 3.0]))
+        b = orc.sgl(u, lam, tau, c, d, w)
+        f = lambda x: _sgl_objective(x, u, lam, tau, c, d, w)  # noqa: E731
+        best = min((minimize(f, x0, method="Nelder-Mead", options={"xatol": 1e-12, "fatol": 1e-14, "maxiter": 20000})
+                    for x0 in (b + 1e-3, np.zeros(m), u / d)), key=lambda r: r.fun)
+        assert f(b) <= best.fun + 1e-9
+        v = np.sign(u) * np.maximum(np.abs(u) - w * lam * tau, 0.0) / d
+        nv = np.linalg.norm(v)
+        printed = v * max(0.0, 1 - c * lam * (1 - tau) / nv) if nv > 0 else 0 * v
+        worse += f(printed) > f(b) + 1e-9
+    assert worse > 0   # the printed d = 1 form is not the M-step minimiser in general
+
+
+def test_sgl_limits():
+    """tau = 0: group lasso; tau = 1: coordinate-wise lasso."""
+    rng = np.random.default_rng(33)
+    for _ in range(50):
+        u = rng.normal(0, 2, 4)
+        lam, c, d = rng.uniform(0.1, 2), rng.uniform(0.5, 2), rng.uniform(1, 3)
+        assert np.allclose(orc.sgl(u, lam, 0.0, c, d), orc.grp_lasso(u, c * lam, d), atol=1e-14)
+        assert np.allclose(orc.sgl(u, lam, 1.0, c, d), [orc.soft(x, lam, d) for x in u], atol=1e-14)
+
+
+def test_sgl_lambda_max_is_smallest_null_fixed_point():
+    rng = np.random.default_rng(34)
+    p, ng = 12, 4
+    group = np.repeat(np.arange(ng), 3)
+    c = rng.normal(0, 1, p)
+    w = rng.uniform(0.5, 1.5, p)
+    for tau in (0.0, 0.3, 0.8, 1.0):
+        lm = orc.lambda_max("sgl", c, w, group, ng, alpha=tau)
+        G = np.eye(p)
+        B0, _, _ = orc.oem_path(G, c, 1.0, "sgl", [lm], alpha=tau, w=w, group=group, ngroups=ng, maxit=1)
+        B1, _, _ = orc.oem_path(G, c, 1.0, "sgl", [lm * (1 - 1e-3)], alpha=tau, w=w, group=group, ngroups=ng, maxit=1)
+        assert not B0.any() and B1.any()

@@ -252,11 +252,12 @@ def test_coordinate_descent_agreement():
 
 
 # ------------------------------------------------------------------ algorithm properties
-@pytest.mark.parametrize("family", ["lasso", "mcp", "scad", "enet", "grp_lasso", "grp_mcp", "grp_scad"])
+@pytest.mark.parametrize("family", ["lasso", "mcp", "scad", "enet", "grp_lasso", "grp_mcp", "grp_scad", "sgl"])
 def test_descent_each_iteration(family):
-    """EM/MM: the objective never increases across OEM iterations when d >= lambda_1."""
+    """EM/MM: the objective never increases across OEM iterations when d >= lambda_1.
+    For the sparse group lasso this also checks the exact composition (R#11) is the M-step."""
     G, c = small_problem(18, 500, 6, rho=0.5)
-    grp = np.array([0, 0, 1, 1, 2, 2], dtype=np.int32) if family.startswith("grp") else None
+    grp = np.array([0, 0, 1, 1, 2, 2], dtype=np.int32) if family.startswith("grp") or family == "sgl" else None
     d = orc.power_rule(G)[0]
     lam = 0.2 * orc.lambda_max(family, c, group=grp, alpha=0.5)
     b = np.zeros(6)
@@ -370,3 +371,40 @@ def test_logistic_ub_matches_exact_newton_fixed_point():
     assert np.max(np.abs(Bu[-1] - b)) <= 1e-8
     # the MM step never increases the penalised negative log-likelihood (descent)
     assert (oi >= 1).all()
+
+
+def test_sgl_kkt_and_limits_on_path():
+    """Sparse group lasso path (tau = 0.4): at the fixed point the subgradient conditions of
+    0.5 b^T G b - c^T b + lam (1-tau) sum c_k ||b_g|| + lam tau sum |b_j| hold per group; tau = 0
+    reproduces the group-lasso path and tau = 1 the lasso path."""
+    G, c = small_problem(23, 800, 9, rho=0.4)
+    grp = np.repeat(np.arange(3), 3).astype(np.int32)
+    d = orc.power_rule(G)[0]
+    tau = 0.4
+    lams = orc.lambda_grid(orc.lambda_max("sgl", c, group=grp, alpha=tau), 12)
+    B, _, cv = orc.oem_path(G, c, d, "sgl", lams, alpha=tau, group=grp, tol=1e-14)
+    assert cv.all()
+    ck = np.sqrt(3.0)
+    for b, lam in zip(B, lams):
+        r = c - G @ b                                   # = subgradient of the penalty
+        for g in range(3):
+            idx = grp == g
+            bg, rg = b[idx], r[idx]
+            if not bg.any():
+                # 0 in the subdifferential: exists s in [-1,1]^m with ||rg - lam tau s|| <= lam (1-tau) ck
+                z = np.sign(rg) * np.maximum(np.abs(rg) - lam * tau, 0)
+                assert np.linalg.norm(z) <= lam * (1 - tau) * ck * (1 + 1e-9) + 1e-12
+            else:
+                nz = bg != 0
+                s = np.where(nz, np.sign(bg), 0.0)
+                res = rg - lam * tau * s - lam * (1 - tau) * ck * bg / np.linalg.norm(bg)
+                assert np.all(np.abs(res[nz]) <= 1e-9)
+                assert np.all(np.abs(rg[~nz] - lam * (1 - tau) * ck * bg[~nz] / np.linalg.norm(bg)) <= lam * tau + 1e-9)
+    lg = orc.lambda_grid(orc.lambda_max("grp_lasso", c, group=grp), 8)
+    B0, _, _ = orc.oem_path(G, c, d, "sgl", lg, alpha=0.0, group=grp, tol=1e-14)
+    Bg, _, _ = orc.oem_path(G, c, d, "grp_lasso", lg, group=grp, tol=1e-14)
+    assert np.max(np.abs(B0 - Bg)) <= 1e-12
+    ll = orc.lambda_grid(orc.lambda_max("lasso", c), 8)
+    B1, _, _ = orc.oem_path(G, c, d, "sgl", ll, alpha=1.0, group=grp, tol=1e-14)
+    Bl, _, _ = orc.oem_path(G, c, d, "lasso", ll, tol=1e-14)
+    assert np.max(np.abs(B1 - Bl)) <= 1e-12
