@@ -114,6 +114,16 @@ typedef struct {
   double d_inflate;         /* d rule (R#5): default 5e-3 */
   int32_t fold_mode;        /* 1: inputs are K fold sums -> fit full data + K complements (R#20-22) */
   const double* lambda_max_override; /* host, optional: use this lambda_max for every unit */
+  /* f3 (R#2-3): with xsum/ysum (device: nG*p raw column sums X^T 1 and nG raw 1^T y, in the
+   * same layout as G/xty, e.g. from oem_gram_moments) the fit has an intercept: each unit's
+   * statistics are centred, G - n xbar xbar^T and c - n xbar ybar, and intercept_out (device,
+   * nG'*nP*L, may be NULL) receives b0 = ybar - xbar^T beta. standardize = 1 scales the
+   * (centred) columns to unit variance before the fit and returns beta on the
+   * original scale; columns of zero variance get beta = 0. */
+  int32_t standardize;
+  const double* xsum;
+  const double* ysum;
+  double* intercept_out;
 } oem_path_cfg;
 
 /* Fit paths from raw sufficient statistics. Inputs G (nG*p*p, full symmetric), xty (nG*p),
@@ -172,6 +182,24 @@ oem_status oem_fit_logistic(oem_ctx* ctx, const double* X, const double* y01, in
                             int64_t ldx, const oem_penalty* pen /*host, one*/, const oem_logistic_cfg* cfg /*host*/,
                             double* beta_out, double* lambda_out, int32_t* outer_iters /*host L*/,
                             int64_t* inner_iters /*host L*/, uint8_t* converged /*host L*/, void* stream);
+
+/* ---- f3 column sums for the intercept / standardization (R#2-3): xsum[k*p + j] = sum of
+ * x_ij over this rank's rows i of fold k (fold(i) = (row_offset + i) mod K, R#19; K = 1 for the
+ * whole data), ysum[k] = sum of y_i; raw sums, allreduced when nranks > 1. One HBM-bound pass.
+ * Errors: OEM_ERR_DIM, OEM_ERR_INVALID_ARG (K < 1), OEM_ERR_UNSUPPORTED (K > 64), OEM_ERR_CUDA. */
+oem_status oem_gram_moments(oem_ctx* ctx, const double* X, const double* y, int64_t n_local, int32_t p,
+                            int64_t ldx, int64_t row_offset, int32_t K, double* xsum /*K*p*/,
+                            double* ysum /*K*/, void* stream);
+
+/* ---- f3 compute.loss: the loss of every fitted path point from the unit's
+ * sufficient statistics alone (no pass over X, R#37): loss[g][q][l] = (yty_g - 2 b^T xty_g +
+ * b^T G_g b) / n_g, the mean squared residual of b = beta[g][q][l] (no intercept; for a fit with
+ * intercept pass the centred statistics). Inputs: raw G (nG*p*p), xty (nG*p), yty (nG), counts
+ * (host nG), beta (nG*nP*L*p). The Gaussian log-likelihood is -n/2 (log(2 pi loss) + 1).
+ * Errors: OEM_ERR_DIM, OEM_ERR_EMPTY_FOLD (count 0), OEM_ERR_UNSUPPORTED, OEM_ERR_CUDA. */
+oem_status oem_path_loss(oem_ctx* ctx, const double* G, const double* xty, const double* yty,
+                         const int64_t* counts /*host nG*/, int32_t nG, int32_t p, int32_t nP, int32_t L,
+                         const double* beta, double* loss, void* stream);
 
 /* ---- f2 fast cross-validation error and selection (§3; P:L601-616, L659-660,
  * L689-690 §5.4-5.5 cv.oem / xval.oem outputs; R#33-35). Inputs: the K raw fold sums of

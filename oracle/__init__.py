@@ -440,3 +440,51 @@ def logistic_path_ub(X, y01, lambdas, family="lasso", gamma=3.0, alpha=1.0, d=No
                 break
         B[l] = beta
     return B, oi, ii, cv
+
+
+# ---------------------------------------------------------------- f3: intercept, standardization, loss
+def fit_transformed(X, y, penalties, nlambda=100, ratio=1e-3, standardize=False, intercept=False, d=None,
+                    lambdas=None, tol=1e-11, maxit=100000, w=None, group=None, ngroups=0, grp_w=None,
+                    power_iters=200, inflate=5e-3):
+    """f3 by transforming the DATA (R#2-3), not the Gram: with an intercept, X and y are centred
+    explicitly (x_ij - xbar_j, y_i - ybar); with standardization the (centred) columns are divided
+    by sd_j = sqrt(mean(x_ij^2)) (P:L173-177 with the /n convention of R#1); then O1 Gram -> a6-a9
+    (fit_from_gram, the given d and lambda grid if any) and the map back to the original scale:
+    beta_j = beta~_j / sd_j (0 for a zero-variance column), b0 = ybar - xbar^T beta.
+    Returns dict(beta [nP][L][p], intercept [nP][L], d, lambda)."""
+    X = _f64(X).copy()
+    y = _f64(y).copy()
+    n, p = X.shape
+    xbar = X.mean(axis=0) if intercept else np.zeros(p)
+    ybar = float(y.mean()) if intercept else 0.0
+    X -= xbar
+    y -= ybar
+    sd = np.sqrt(np.mean(X * X, axis=0)) if standardize else np.ones(p)
+    inv = np.where(sd > 0, 1.0 / np.where(sd > 0, sd, 1.0), 0.0)
+    X *= inv
+    G, c, _ = gram(X, y)
+    out = {"beta": [], "intercept": [], "lambda": []}
+    if d is None:
+        d = power_rule(G / n, power_iters, inflate)[0]
+    out["d"] = d
+    for q, (fam, gamma, alpha) in enumerate(penalties):
+        if lambdas is None:
+            lm = lambda_max(fam, c / n, w, group, ngroups, grp_w, alpha)
+            lam = lambda_grid(lm, nlambda, ratio)
+        else:
+            lam = _f64(lambdas[q])
+        B, _, _ = oem_path(G / n, c / n, d, fam, lam, gamma, alpha, w, group, ngroups, grp_w, tol, maxit)
+        B = B * inv
+        out["beta"].append(B)
+        out["intercept"].append(ybar - B @ xbar)
+        out["lambda"].append(lam)
+    return out
+
+
+def path_loss(X, y, B):
+    """f3 compute.loss by its definition (R#37): mean((y - X b)^2) for every b in B[..., p]."""
+    X = _f64(X)
+    y = _f64(y)
+    B = np.asarray(B, dtype=np.float64)
+    R = y[:, None] - X @ B.reshape(-1, B.shape[-1]).T
+    return (np.sum(R * R, axis=0) / X.shape[0]).reshape(B.shape[:-1])

@@ -133,6 +133,8 @@ oem_status oem_ctx_destroy(oem_ctx* ctx) {
   ctx->path_small.release();
   ctx->lg_part.release();
   ctx->lg_out.release();
+  ctx->mom_part.release();
+  ctx->mom_out.release();
   for (auto& pe : ctx->pending) { cudaEventDestroy(pe.a); cudaEventDestroy(pe.b); }
   for (auto e : ctx->event_pool) cudaEventDestroy(e);
   delete ctx;

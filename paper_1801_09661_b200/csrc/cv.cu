@@ -26,15 +26,16 @@ constexpr int CV_THREADS = 256;
 
 __global__ void __launch_bounds__(CV_THREADS) cv_err_kernel(const double* __restrict__ Gf, const double* __restrict__ cf,
                                                              const double* __restrict__ yyf, const double* __restrict__ nk,
-                                                             const double* __restrict__ beta, int p, int nP, int L, int LB,
-                                                             double* __restrict__ err) {
+                                                             const double* __restrict__ beta, int boff, int p, int nP, int L,
+                                                             int LB, double* __restrict__ err) {
   extern __shared__ __align__(16) double bs[];  // [LB][p]
   __shared__ double red[CV_THREADS / 32][2 * CV_LB];
   const int l0 = blockIdx.x * LB, q = blockIdx.y, k = blockIdx.z;
   const int nb = min(LB, L - l0);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = CV_THREADS / 32;
-  // the complement fit of fold k is unit k+1 of the fold-mode path output
-  const double* b0 = beta + (((size_t)(k + 1) * nP + q) * L + l0) * p;
+  // CV: the complement fit of fold k is unit k+1 of the fold-mode path output (boff = 1);
+  // compute.loss: unit k's own fit (boff = 0)
+  const double* b0 = beta + (((size_t)(k + boff) * nP + q) * L + l0) * p;
   for (int e = threadIdx.x; e < nb * p; e += CV_THREADS) bs[e] = b0[e];
   __syncthreads();
   const double* G = Gf + (size_t)k * p * p;
@@ -151,7 +152,7 @@ extern "C" oem_status oem_cv_error(oem_ctx* ctx, const double* G_folds, const do
   OEM_CUDA_TRY(cudaFuncSetAttribute(cv_err_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)std::max<size_t>(smem, 1)));
   dim3 grid((unsigned)((L + LB - 1) / LB), (unsigned)nP, (unsigned)K);
   ++ctx->launches;
-  cv_err_kernel<<<grid, CV_THREADS, smem, st>>>(G_folds, xty_folds, yty_folds, nk, beta, p, nP, L, LB, err);
+  cv_err_kernel<<<grid, CV_THREADS, smem, st>>>(G_folds, xty_folds, yty_folds, nk, beta, 1, p, nP, L, LB, err);
   OEM_CUDA_TRY(cudaGetLastError());
   ++ctx->launches;
   cv_summary_kernel<<<1, 256, 0, st>>>(err, nk, K, nP, L, cvm, cvsd, sel);
@@ -164,5 +165,32 @@ extern "C" oem_status oem_cv_error(oem_ctx* ctx, const double* G_folds, const do
     if (idx_1se) idx_1se[q] = hs[nP + q];
   }
   if (best) *best = hs[2 * nP];
+  return OEM_OK;
+}
+
+extern "C" oem_status oem_path_loss(oem_ctx* ctx, const double* G, const double* xty, const double* yty,
+                                    const int64_t* counts, int32_t nG, int32_t p, int32_t nP, int32_t L,
+                                    const double* beta, double* loss, void* stream) {
+  if (!ctx) OEM_FAIL(OEM_ERR_INVALID_ARG, "null oem_ctx");
+  OEM_CUDA_TRY(cudaSetDevice(ctx->device));
+  if (!G || !xty || !yty || !counts || !beta || !loss) OEM_FAIL(OEM_ERR_INVALID_ARG, "oem_path_loss: null pointer");
+  if (nG < 1 || p < 1 || nP < 1 || L < 1) OEM_FAIL(OEM_ERR_DIM, "oem_path_loss: need nG, p, nP, L >= 1");
+  for (int g = 0; g < nG; ++g)
+    if (counts[g] <= 0) OEM_FAIL(OEM_ERR_EMPTY_FOLD, "oem_path_loss: count " + std::to_string(g) + " is 0");
+  int LB = std::min(CV_LB, L);
+  if ((size_t)p * 8 > 200 * 1024) OEM_FAIL(OEM_ERR_UNSUPPORTED, "oem_path_loss: p too large");
+  while (LB > 1 && (size_t)LB * p * 8 > 200 * 1024) --LB;
+  cudaStream_t st = (cudaStream_t)stream;
+  OEM_CUDA_TRY(ctx->path_small.ensure(sizeof(double) * (nG + 8)));
+  double* nk = ctx->path_small.as<double>();
+  std::vector<double> hn(nG);
+  for (int g = 0; g < nG; ++g) hn[g] = (double)counts[g];
+  OEM_CUDA_TRY(cudaMemcpyAsync(nk, hn.data(), sizeof(double) * nG, cudaMemcpyHostToDevice, st));
+  const size_t smem = (size_t)LB * p * 8;
+  OEM_CUDA_TRY(cudaFuncSetAttribute(cv_err_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)std::max<size_t>(smem, 1)));
+  dim3 grid((unsigned)((L + LB - 1) / LB), (unsigned)nP, (unsigned)nG);
+  ++ctx->launches;
+  cv_err_kernel<<<grid, CV_THREADS, smem, st>>>(G, xty, yty, nk, beta, 0, p, nP, L, LB, loss);
+  OEM_CUDA_TRY(cudaGetLastError());
   return OEM_OK;
 }

@@ -50,7 +50,7 @@ struct oem_ctx {
   int nranks = 1, rank = 0;
   int num_sms = 148;
   void* nccl_comm = nullptr;  // ncclComm_t
-  oem::DevBuf partial, partial_scal, packed, tail, plan_tables, path_ws, path_small, logi, lg_part, lg_out;
+  oem::DevBuf partial, partial_scal, packed, tail, plan_tables, path_ws, path_small, logi, lg_part, lg_out, mom_part, mom_out;
   std::map<std::tuple<int, int, int64_t, int>, std::shared_ptr<oem::GramPlan>> plans;
   // instrumentation (oem_ctx_set_timing / oem_ctx_stats)
   bool timing = false;

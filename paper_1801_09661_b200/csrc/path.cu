@@ -177,8 +177,58 @@ __device__ __forceinline__ void atomic_max_pos(unsigned long long* slot, double 
 // ---------------------------------------------------------------- prep: normalise unit Grams
 // fold_mode = 0: unit g = G[g]/n_g. fold_mode = 1: unit 0 = (sum_k G_k)/n, unit k = (sum - G_{k-1})/(n - n_{k-1}).
 // Coordinates are permuted so every group is contiguous: Gn[u][j][l] = Graw[perm[j]][perm[l]].
+// f3 (R#2-3): per unit, in original coordinates, xbar_j = (X^T 1)_j / n, ybar = 1^T y / n (0 without
+// an intercept) and inv_s_j = 1 / sd_j of the centred column (1 without standardization; 0 for a
+// zero-variance column, which then drops out: its row/column of the unit Gram become 0).
+__device__ __forceinline__ double unit_raw(const double* src, int nG, int u, int fold_mode, size_t stride, size_t off) {
+  if (!fold_mode) return src[(size_t)u * stride + off];
+  double s = 0.0;
+  for (int k = 0; k < nG; ++k) s += src[(size_t)k * stride + off];  // fixed order
+  return (u == 0) ? s : s - src[(size_t)(u - 1) * stride + off];    // total minus fold (R#20)
+}
+__global__ void unit_stats_kernel(const double* __restrict__ G, const double* __restrict__ xsum,
+                                  const double* __restrict__ ysum, int nG, int p, int fold_mode,
+                                  const double* __restrict__ inv_n, int standardize, double* __restrict__ mean,
+                                  double* __restrict__ ybar, double* __restrict__ inv_s) {
+  const int u = blockIdx.x;
+  const double in = inv_n[u];
+  if (threadIdx.x == 0) ybar[u] = ysum ? unit_raw(ysum, nG, u, fold_mode, 1, 0) * in : 0.0;
+  for (int j = threadIdx.x; j < p; j += blockDim.x) {
+    const double m = xsum ? unit_raw(xsum, nG, u, fold_mode, p, j) * in : 0.0;
+    mean[(size_t)u * p + j] = m;
+    double is = 1.0;
+    if (standardize) {
+      const double v = unit_raw(G, nG, u, fold_mode, (size_t)p * p, (size_t)j * p + j) * in - m * m;
+      is = v > 0.0 ? 1.0 / sqrt(v) : 0.0;
+    }
+    inv_s[(size_t)u * p + j] = is;
+  }
+}
+
+// After the solver: beta (original order) back to the original scale, beta_j = beta~_j inv_s_j,
+// and the intercept b0 = ybar - xbar^T beta (one warp per (unit, penalty, lambda), fixed order).
+__global__ void backtransform_kernel(double* __restrict__ beta, int nU, int nP, int L, int p,
+                                     const double* __restrict__ mean, const double* __restrict__ ybar,
+                                     const double* __restrict__ inv_s, double* __restrict__ b0) {
+  const int w = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
+  if (w >= nU * nP * L) return;
+  const int u = w / (nP * L);
+  double* b = beta + (size_t)w * p;
+  double s = 0.0;
+  for (int j = lane; j < p; j += 32) {
+    const double v = b[j] * inv_s[(size_t)u * p + j];
+    b[j] = v;
+    s = fma(mean[(size_t)u * p + j], v, s);
+  }
+#pragma unroll
+  for (int o = 16; o >= 1; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+  if (lane == 0 && b0) b0[w] = ybar[u] - s;
+}
+
 __global__ void prep_units_kernel(const double* __restrict__ G, const double* __restrict__ xty, int nG, int p,
                                   int fold_mode, const double* __restrict__ inv_n, const int* __restrict__ perm,
+                                  const double* __restrict__ mean, const double* __restrict__ ybar,
+                                  const double* __restrict__ inv_s,
                                   double* __restrict__ Gn, double* __restrict__ cn, int* flags) {
   const int nU = fold_mode ? nG + 1 : nG;
   const int64_t per = (int64_t)p * p + p;
@@ -211,6 +261,16 @@ __global__ void prep_units_kernel(const double* __restrict__ G, const double* __
       v = (u == 0) ? s : s - src[(size_t)(u - 1) * stride + off];    // total minus fold (R#20)
     }
     v = v * inv_n[u];
+    if (mean) {  // centring and standardization (R#2-3); identity (bit for bit) when not requested
+      const size_t mo = (size_t)u * p;
+      if (q < (int64_t)p * p) {
+        const int a = perm[(int)(q / p)], b = perm[(int)(q % p)];
+        v = (v - mean[mo + a] * mean[mo + b]) * inv_s[mo + a] * inv_s[mo + b];
+      } else {
+        const int a = perm[(int)(q - (int64_t)p * p)];
+        v = (v - mean[mo + a] * ybar[u]) * inv_s[mo + a];
+      }
+    }
     if (!isfinite(v)) flags[0] = 1;
     *dst = v;
   }
@@ -1645,6 +1705,10 @@ extern "C" void oem_path_cfg_default(oem_path_cfg* cfg) {
   cfg->d_inflate = 5e-3;
   cfg->fold_mode = 0;
   cfg->lambda_max_override = nullptr;
+  cfg->standardize = 0;
+  cfg->xsum = nullptr;
+  cfg->ysum = nullptr;
+  cfg->intercept_out = nullptr;
 }
 
 template <typename K>
@@ -1802,6 +1866,12 @@ extern "C" oem_status oem_fit_path(oem_ctx* ctx, const double* G, const double* 
   const size_t o_j0 = take(sizeof(int) * ncta_total);
   const size_t o_j1 = take(sizeof(int) * ncta_total);
   const size_t o_d = take(sizeof(double) * nU);
+  const bool centre = cfg.xsum != nullptr || cfg.ysum != nullptr;
+  const bool xform = centre || cfg.standardize;
+  if (centre && !(cfg.xsum && cfg.ysum)) OEM_FAIL(OEM_ERR_INVALID_ARG, "oem_fit_path: intercept needs both xsum and ysum");
+  const size_t o_mean = take(sizeof(double) * (xform ? (size_t)nU * p : 1));
+  const size_t o_ybar = take(sizeof(double) * nU);
+  const size_t o_invs = take(sizeof(double) * (xform ? (size_t)nU * p : 1));
   const size_t o_host_end = off;
   OEM_CUDA_TRY(ctx->path_ws.ensure(off));
   char* base = ctx->path_ws.as<char>();
@@ -1851,8 +1921,18 @@ extern "C" oem_status oem_fit_path(oem_ctx* ctx, const double* G, const double* 
     const int blocks = (int)std::max<int64_t>(1, std::min<int64_t>(ctx->num_sms * 8, (total + 255) / 256));
     PhaseTimer tm(ctx, PH_PATH, st);
     ++ctx->launches;
+    if (xform) {
+      ++ctx->launches;
+      unit_stats_kernel<<<nU, 256, 0, st>>>(G, cfg.xsum, cfg.ysum, nG, p, fold, reinterpret_cast<double*>(base + o_invn),
+                                             cfg.standardize ? 1 : 0, reinterpret_cast<double*>(base + o_mean),
+                                             reinterpret_cast<double*>(base + o_ybar), reinterpret_cast<double*>(base + o_invs));
+      OEM_CUDA_TRY(cudaGetLastError());
+    }
     prep_units_kernel<<<blocks, 256, 0, st>>>(G, xty, nG, p, fold, reinterpret_cast<double*>(base + o_invn),
-                                              reinterpret_cast<int*>(base + o_perm), Gn, cn, flags);
+                                              reinterpret_cast<int*>(base + o_perm),
+                                              xform ? reinterpret_cast<double*>(base + o_mean) : nullptr,
+                                              reinterpret_cast<double*>(base + o_ybar),
+                                              reinterpret_cast<double*>(base + o_invs), Gn, cn, flags);
     OEM_CUDA_TRY(cudaGetLastError());
   }
   PathParams P;
@@ -1943,6 +2023,16 @@ extern "C" oem_status oem_fit_path(oem_ctx* ctx, const double* G, const double* 
     else if (NPT == 4) s = coop_launch(path_kernel<4>, lo.ncta_total, lo.smem, st, args);
     else s = coop_launch(path_kernel<8>, lo.ncta_total, lo.smem, st, args);
     if (s != OEM_OK) return s;
+  }
+  if (xform) {
+    const int warps = nU * nP * L;
+    ++ctx->launches;
+    backtransform_kernel<<<(warps * 32 + 255) / 256, 256, 0, st>>>(
+        beta_out, nU, nP, L, p, reinterpret_cast<double*>(base + o_mean), reinterpret_cast<double*>(base + o_ybar),
+        reinterpret_cast<double*>(base + o_invs), centre ? cfg.intercept_out : nullptr);
+    OEM_CUDA_TRY(cudaGetLastError());
+  } else if (cfg.intercept_out) {
+    OEM_CUDA_TRY(cudaMemsetAsync(cfg.intercept_out, 0, sizeof(double) * (size_t)nU * nP * L, st));
   }
   OEM_CUDA_TRY(cudaMemcpyAsync(d_out, dptr, sizeof(double) * nU, cudaMemcpyDeviceToDevice, st));
   int hflags[4] = {0, 0, 0, 0};

@@ -27,7 +27,7 @@ STATUS = ["OEM_OK", "OEM_ERR_INVALID_ARG", "OEM_ERR_DIM", "OEM_ERR_ALIGN", "OEM_
 ABI_SYMBOLS = ["oem_status_string", "oem_last_error", "oem_version", "oem_nccl_unique_id",
                "oem_ctx_create", "oem_ctx_destroy", "oem_gram", "oem_gram_folds",
                "oem_gram_weighted", "oem_fit_path", "oem_path_cfg_default", "oem_fit_logistic",
-               "oem_logistic_cfg_default", "oem_cv_error", "oem_logit_grad", "oem_ctx_set_timing", "oem_ctx_stats"]
+               "oem_logistic_cfg_default", "oem_cv_error", "oem_logit_grad", "oem_gram_moments", "oem_path_loss", "oem_ctx_set_timing", "oem_ctx_stats"]
 _VOID = ("oem_status_string", "oem_last_error", "oem_version", "oem_path_cfg_default",
          "oem_logistic_cfg_default")
 
@@ -49,7 +49,8 @@ class PathCfg(ctypes.Structure):
                 ("var_w", ctypes.c_void_p), ("group", ctypes.c_void_p), ("ngroups", ctypes.c_int32),
                 ("grp_w", ctypes.c_void_p), ("power_iters", ctypes.c_int32),
                 ("d_inflate", ctypes.c_double), ("fold_mode", ctypes.c_int32),
-                ("lambda_max_override", ctypes.c_void_p)]
+                ("lambda_max_override", ctypes.c_void_p), ("standardize", ctypes.c_int32),
+                ("xsum", ctypes.c_void_p), ("ysum", ctypes.c_void_p), ("intercept_out", ctypes.c_void_p)]
 
 
 class LogisticCfg(ctypes.Structure):
@@ -101,6 +102,8 @@ def lib():
                                        ctypes.POINTER(LogisticCfg), P, P, P, P, P, P]
         L.oem_cv_error.argtypes = [P, P, P, P, P, i32, i32, i32, i32, P, P, P, P, P, P, P, P]
         L.oem_logit_grad.argtypes = [P, P, P, P, i64, i32, i64, P, P, P]
+        L.oem_gram_moments.argtypes = [P, P, P, i64, i32, i64, i64, i32, P, P, P]
+        L.oem_path_loss.argtypes = [P, P, P, P, P, i32, i32, i32, i32, P, P, P]
         L.oem_ctx_set_timing.argtypes = [P, ctypes.c_int]
         L.oem_ctx_stats.argtypes = [P, ctypes.POINTER(Stats), ctypes.c_int]
         for name in ABI_SYMBOLS:
@@ -215,12 +218,14 @@ class PathResult:
     iters: torch.Tensor     # [nG'][nP][L] int64
     conv: torch.Tensor      # [nG'][nP][L] uint8
     d: torch.Tensor         # [nG']
+    intercept: torch.Tensor = None   # [nG'][nP][L] when fitted with an intercept (f3)
 
 
 def oem_fit_path(ctx: Context, G, xty, counts, penalties, nlambda=100, lambda_min_ratio=1e-3,
                  lambdas=None, tol=1e-11, maxit=100000, var_w=None, group=None, ngroups=0,
                  grp_w=None, power_iters=200, d_inflate=5e-3, fold_mode=False, d_in=None,
-                 beta_init=None, lambda_max=None, stream=None) -> PathResult:
+                 beta_init=None, lambda_max=None, standardize=False, xsum=None, ysum=None,
+                 stream=None) -> PathResult:
     """a6-a10: normalise, d, lambda grid and OEM paths for every (Gram, penalty) unit.
 
     G: [nG, p, p] (or [p, p]) raw sums, xty: [nG, p], counts: nG ints. penalties: list of
@@ -265,6 +270,15 @@ def oem_fit_path(ctx: Context, G, xty, counts, penalties, nlambda=100, lambda_mi
         lm_h = ctypes.c_double(float(lambda_max))
         keep.append(lm_h)
         cfg.lambda_max_override = ctypes.cast(ctypes.pointer(lm_h), ctypes.c_void_p)
+    cfg.standardize = 1 if standardize else 0
+    icpt = None
+    if xsum is not None or ysum is not None:
+        xsum = xsum.reshape(nG, p).to(device=G.device, dtype=torch.float64).contiguous()
+        ysum = ysum.reshape(nG).to(device=G.device, dtype=torch.float64).contiguous()
+        keep += [xsum, ysum]
+        cfg.xsum, cfg.ysum = xsum.data_ptr(), ysum.data_ptr()
+        icpt = torch.empty((nGo, nP, L), dtype=torch.float64, device=G.device)
+        cfg.intercept_out = icpt.data_ptr()
     cnt = (ctypes.c_int64 * nG)(*[int(c) for c in counts])
     d_h = None
     if d_in is not None:
@@ -280,7 +294,34 @@ def oem_fit_path(ctx: Context, G, xty, counts, penalties, nlambda=100, lambda_mi
     _check(lib().oem_fit_path(ctx.h, _ptr(G), _ptr(xty), cnt, nG, p, pens, nP, ctypes.byref(cfg),
                               d_h, _ptr(beta_init), _ptr(beta), _ptr(lam), _ptr(iters), _ptr(conv),
                               _ptr(d), _stream(stream)))
-    return PathResult(beta, lam, iters, conv, d)
+    return PathResult(beta, lam, iters, conv, d, icpt)
+
+
+def oem_gram_moments(ctx: Context, X, y, K: int = 1, row_offset: int = 0, stream=None):
+    """f3: per-fold column sums (X^T 1 [K][p], 1^T y [K]) for the intercept / standardization."""
+    _check_x(X, y)
+    n, p = X.shape
+    xs = torch.empty((K, p), dtype=torch.float64, device=X.device)
+    ys = torch.empty(K, dtype=torch.float64, device=X.device)
+    _check(lib().oem_gram_moments(ctx.h, _ptr(X), _ptr(y), n, p, X.stride(0), row_offset, K, _ptr(xs),
+                                  _ptr(ys), _stream(stream)))
+    return xs, ys
+
+
+def oem_path_loss(ctx: Context, G, xty, yty, counts, beta, stream=None):
+    """f3 compute.loss: mean squared residual of every path point from the raw unit statistics
+    (G [nG][p][p], xty [nG][p], yty [nG], beta [nG][nP][L][p]) -> [nG][nP][L]."""
+    if G.dim() == 2:
+        G, xty, yty = G.unsqueeze(0), xty.unsqueeze(0), yty.reshape(1)
+    nG, p, _ = G.shape
+    nU, nP, L, pb = beta.shape
+    if nU != nG or pb != p:
+        raise ValueError("beta must be [nG][nP][L][p]")
+    loss = torch.empty((nG, nP, L), dtype=torch.float64, device=G.device)
+    cnt = (ctypes.c_int64 * nG)(*[int(c) for c in counts])
+    _check(lib().oem_path_loss(ctx.h, _ptr(G.contiguous()), _ptr(xty.contiguous()), _ptr(yty.contiguous()), cnt,
+                               nG, p, nP, L, _ptr(beta.contiguous()), _ptr(loss), _stream(stream)))
+    return loss
 
 
 @dataclass
