@@ -183,6 +183,23 @@ oem_status oem_fit_logistic(oem_ctx* ctx, const double* X, const double* y01, in
                             double* beta_out, double* lambda_out, int32_t* outer_iters /*host L*/,
                             int64_t* inner_iters /*host L*/, uint8_t* converged /*host L*/, void* stream);
 
+/* ---- f4 out-of-core Gram passes (the big.oem analogue, §5.7: X kept out of core,
+ * the p x p statistics accumulated block by block). X (row-major, ldx even) and y are HOST
+ * pointers, ideally pinned (cudaHostAlloc / torch pin_memory) so the copies run asynchronously:
+ * blocks of block_rows rows are copied to two device staging buffers on an internal copy stream
+ * while the Gram kernel consumes the other buffer on `stream`, and the block results are added
+ * in block order (deterministic). Outputs and errors as oem_gram / oem_gram_folds (device
+ * outputs), plus OEM_ERR_INVALID_ARG for block_rows < 32. Device memory used: 2 blocks.
+ * The caller must keep X and y unchanged until `stream` has passed the call (the copies are
+ * asynchronous). */
+oem_status oem_gram_host(oem_ctx* ctx, const double* X /*host*/, const double* y /*host*/, int64_t n_local,
+                         int32_t p, int64_t ldx, int64_t block_rows, double* G, double* xty, double* yty,
+                         int64_t* n_total, void* stream);
+oem_status oem_gram_folds_host(oem_ctx* ctx, const double* X /*host*/, const double* y /*host*/, int64_t n_local,
+                               int32_t p, int64_t ldx, int64_t row_offset, int32_t K, int64_t block_rows,
+                               double* G_folds, double* xty_folds, double* yty_folds, int64_t* counts /*host K*/,
+                               void* stream);
+
 /* ---- f3 column sums for the intercept / standardization (R#2-3): xsum[k*p + j] = sum of
  * x_ij over this rank's rows i of fold k (fold(i) = (row_offset + i) mod K, R#19; K = 1 for the
  * whole data), ysum[k] = sum of y_i; raw sums, allreduced when nranks > 1. One HBM-bound pass.

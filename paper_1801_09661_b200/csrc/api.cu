@@ -42,7 +42,7 @@ static oem_status check_x(const double* X, const double* y, int64_t n_local, int
   return OEM_OK;
 }
 
-static oem_status host_allreduce_i64(oem_ctx* ctx, int64_t* vals, int n) {
+oem_status host_allreduce_i64(oem_ctx* ctx, int64_t* vals, int n) {
   // small integer sums (row counts) across ranks: via a device buffer and NCCL int64
   if (ctx->nranks <= 1) return OEM_OK;
   int64_t* d = nullptr;
@@ -135,6 +135,13 @@ oem_status oem_ctx_destroy(oem_ctx* ctx) {
   ctx->lg_out.release();
   ctx->mom_part.release();
   ctx->mom_out.release();
+  ctx->stage0.release();
+  ctx->stage1.release();
+  if (ctx->copy_stream) cudaStreamDestroy(ctx->copy_stream);
+  for (int i = 0; i < 2; ++i) {
+    if (ctx->ev_copied[i]) cudaEventDestroy(ctx->ev_copied[i]);
+    if (ctx->ev_used[i]) cudaEventDestroy(ctx->ev_used[i]);
+  }
   for (auto& pe : ctx->pending) { cudaEventDestroy(pe.a); cudaEventDestroy(pe.b); }
   for (auto e : ctx->event_pool) cudaEventDestroy(e);
   delete ctx;

@@ -392,7 +392,7 @@ gram_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ CUt
 __global__ void gram_reduce_kernel(const double* __restrict__ partial, int nfold, int nseg, int nblk,
                                    const int2* __restrict__ blk_coord, int p, const double* __restrict__ tail,
                                    double* __restrict__ packed, int64_t psize, const double* __restrict__ pscal,
-                                   int with_scal) {
+                                   int with_scal, int accumulate) {
   const int64_t total = (int64_t)nfold * nblk * 64;
   for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < total; t += (int64_t)gridDim.x * blockDim.x) {
     const int e = (int)(t & 63);
@@ -406,12 +406,13 @@ __global__ void gram_reduce_kernel(const double* __restrict__ partial, int nfold
     const double* src = partial + ((size_t)f * nseg * nblk + idx) * 64 + e;
     for (int g = 0; g < nseg; ++g) s += src[(size_t)g * nblk * 64];
     if (tail) s += tail[((size_t)f * nblk + idx) * 64 + e];
-    packed[(size_t)f * psize + (int64_t)j * (p + 1) - (int64_t)j * (j - 1) / 2 + (l - j)] = s;
+    double* dst = packed + (size_t)f * psize + (int64_t)j * (p + 1) - (int64_t)j * (j - 1) / 2 + (l - j);
+    *dst = accumulate ? *dst + s : s;   // streamed row blocks add in block order (f4)
   }
   if (with_scal && blockIdx.x == 0 && threadIdx.x < 2) {
     double s = 0.0;
     for (int g = 0; g < nseg; ++g) s += pscal[g * 2 + threadIdx.x];
-    packed[psize + threadIdx.x] = s;
+    packed[psize + threadIdx.x] = accumulate ? packed[psize + threadIdx.x] + s : s;
   }
 }
 
@@ -682,12 +683,14 @@ static oem_status launch_t(const GramPlan& pl, const CUtensorMap& mx, const CUte
 }
 
 oem_status gram_pass(oem_ctx* ctx, int mode, const double* X, const double* y, const double* beta, double eps,
-                     int64_t n_local, int p, int64_t ldx, int64_t row_offset, int K, double* packed, cudaStream_t st) {
+                     int64_t n_local, int p, int64_t ldx, int64_t row_offset, int K, double* packed, cudaStream_t st,
+                     int accumulate) {
   const int nfold = mode == MODE_FOLD ? K : 1;
   const int64_t psize = packed_size(p);
   const int64_t nq = mode == MODE_FOLD ? n_local / K : n_local;
   if (n_local == 0 || nq == 0) {
-    OEM_CUDA_TRY(cudaMemsetAsync(packed, 0, sizeof(double) * (nfold * psize + (mode == MODE_WEIGHTED ? 2 : 0)), st));
+    if (!accumulate)
+      OEM_CUDA_TRY(cudaMemsetAsync(packed, 0, sizeof(double) * (nfold * psize + (mode == MODE_WEIGHTED ? 2 : 0)), st));
     if (mode != MODE_FOLD || n_local == 0) return OEM_OK;
   }
   auto key = std::make_tuple(mode, p, nq, K);
@@ -778,7 +781,7 @@ oem_status gram_pass(oem_ctx* ctx, int mode, const double* X, const double* y, c
     ++ctx->launches;
     gram_reduce_kernel<<<blocks, 256, 0, st>>>(ctx->partial.as<double>(), nfold, nq > 0 ? pl.nseg : 0, pl.nblk,
                                                pl.d_blk_coord, p, tail, packed, psize, ctx->partial_scal.as<double>(),
-                                               mode == MODE_WEIGHTED);
+                                               mode == MODE_WEIGHTED, accumulate);
     OEM_CUDA_TRY(cudaGetLastError());
   }
   return OEM_OK;

@@ -50,7 +50,9 @@ struct oem_ctx {
   int nranks = 1, rank = 0;
   int num_sms = 148;
   void* nccl_comm = nullptr;  // ncclComm_t
-  oem::DevBuf partial, partial_scal, packed, tail, plan_tables, path_ws, path_small, logi, lg_part, lg_out, mom_part, mom_out;
+  oem::DevBuf partial, partial_scal, packed, tail, plan_tables, path_ws, path_small, logi, lg_part, lg_out, mom_part, mom_out, stage0, stage1;
+  cudaStream_t copy_stream = nullptr;  // f4 host streaming: H2D copies overlap the Gram kernel
+  cudaEvent_t ev_copied[2] = {nullptr, nullptr}, ev_used[2] = {nullptr, nullptr};
   std::map<std::tuple<int, int, int64_t, int>, std::shared_ptr<oem::GramPlan>> plans;
   // instrumentation (oem_ctx_set_timing / oem_ctx_stats)
   bool timing = false;
@@ -94,12 +96,14 @@ enum GramMode { MODE_PLAIN = 0, MODE_FOLD = 1, MODE_WEIGHTED = 2 };
 // packed: nfold * psize (+2 scalars for MODE_WEIGHTED), psize = (p+1)(p+2)/2.
 oem_status gram_pass(oem_ctx* ctx, int mode, const double* X, const double* y, const double* beta, double eps,
                      int64_t n_local, int p, int64_t ldx, int64_t row_offset, int K, double* packed,
-                     cudaStream_t st);
+                     cudaStream_t st, int accumulate = 0);
 // packed (nfold blocks) -> full symmetric G (nfold*p*p), xty (nfold*p), yty (nfold)
 oem_status gram_unpack(oem_ctx* ctx, const double* packed, int nfold, int p, double* G, double* xty, double* yty, cudaStream_t st);
 inline int64_t packed_size(int p) { return (int64_t)(p + 1) * (p + 2) / 2; }
 
 oem_status allreduce_sum(oem_ctx* ctx, double* buf, size_t count, cudaStream_t st);
+// small host integer sums over ranks (row counts)
+oem_status host_allreduce_i64(oem_ctx* ctx, int64_t* vals, int n);
 
 // f1 (logit_ub.cu): out[0..p) = X^T (y - sigma(X beta)), out[p] = loglik, raw sums allreduced
 oem_status logit_grad_pass(oem_ctx* ctx, const double* X, const double* y01, const double* beta, int64_t n_local,

@@ -27,7 +27,7 @@ STATUS = ["OEM_OK", "OEM_ERR_INVALID_ARG", "OEM_ERR_DIM", "OEM_ERR_ALIGN", "OEM_
 ABI_SYMBOLS = ["oem_status_string", "oem_last_error", "oem_version", "oem_nccl_unique_id",
                "oem_ctx_create", "oem_ctx_destroy", "oem_gram", "oem_gram_folds",
                "oem_gram_weighted", "oem_fit_path", "oem_path_cfg_default", "oem_fit_logistic",
-               "oem_logistic_cfg_default", "oem_cv_error", "oem_logit_grad", "oem_gram_moments", "oem_path_loss", "oem_ctx_set_timing", "oem_ctx_stats"]
+               "oem_logistic_cfg_default", "oem_cv_error", "oem_logit_grad", "oem_gram_moments", "oem_path_loss", "oem_gram_host", "oem_gram_folds_host", "oem_ctx_set_timing", "oem_ctx_stats"]
 _VOID = ("oem_status_string", "oem_last_error", "oem_version", "oem_path_cfg_default",
          "oem_logistic_cfg_default")
 
@@ -103,6 +103,8 @@ def lib():
         L.oem_cv_error.argtypes = [P, P, P, P, P, i32, i32, i32, i32, P, P, P, P, P, P, P, P]
         L.oem_logit_grad.argtypes = [P, P, P, P, i64, i32, i64, P, P, P]
         L.oem_gram_moments.argtypes = [P, P, P, i64, i32, i64, i64, i32, P, P, P]
+        L.oem_gram_host.argtypes = [P, P, P, i64, i32, i64, i64, P, P, P, ctypes.POINTER(i64), P]
+        L.oem_gram_folds_host.argtypes = [P, P, P, i64, i32, i64, i64, i32, i64, P, P, P, P, P]
         L.oem_path_loss.argtypes = [P, P, P, P, P, i32, i32, i32, i32, P, P, P]
         L.oem_ctx_set_timing.argtypes = [P, ctypes.c_int]
         L.oem_ctx_stats.argtypes = [P, ctypes.POINTER(Stats), ctypes.c_int]
@@ -295,6 +297,44 @@ def oem_fit_path(ctx: Context, G, xty, counts, penalties, nlambda=100, lambda_mi
                               d_h, _ptr(beta_init), _ptr(beta), _ptr(lam), _ptr(iters), _ptr(conv),
                               _ptr(d), _stream(stream)))
     return PathResult(beta, lam, iters, conv, d, icpt)
+
+
+def _check_host(X, y):
+    if X.device.type != "cpu" or y.device.type != "cpu":
+        raise ValueError("X and y must be host (CPU) tensors; pin them for overlapped copies")
+    if X.dtype != torch.float64 or y.dtype != torch.float64:
+        raise ValueError("X and y must be float64")
+    if X.dim() != 2 or X.stride(1) != 1 or y.dim() != 1 or y.stride(0) != 1 or y.shape[0] != X.shape[0]:
+        raise ValueError("X must be row-major [n, p] (unit column stride) and y [n] contiguous")
+
+
+def oem_gram_host(ctx: Context, X, y, block_rows: int = 1 << 20, device=None, stream=None):
+    """f4: the a2 Gram pass over host-resident (pinned) X, y streamed in row blocks."""
+    _check_host(X, y)
+    n, p = X.shape
+    dev = device or torch.device("cuda", torch.cuda.current_device())
+    G = torch.empty((p, p), dtype=torch.float64, device=dev)
+    xty = torch.empty(p, dtype=torch.float64, device=dev)
+    yty = torch.empty(1, dtype=torch.float64, device=dev)
+    nt = ctypes.c_int64(0)
+    _check(lib().oem_gram_host(ctx.h, X.data_ptr(), y.data_ptr(), n, p, X.stride(0), int(block_rows), _ptr(G),
+                               _ptr(xty), _ptr(yty), ctypes.byref(nt), _stream(stream)))
+    return G, xty, yty, nt.value
+
+
+def oem_gram_folds_host(ctx: Context, X, y, K: int, row_offset: int = 0, block_rows: int = 1 << 20, device=None,
+                        stream=None):
+    """f4: the a3 fold-segmented pass over host-resident (pinned) X, y streamed in row blocks."""
+    _check_host(X, y)
+    n, p = X.shape
+    dev = device or torch.device("cuda", torch.cuda.current_device())
+    G = torch.empty((K, p, p), dtype=torch.float64, device=dev)
+    xty = torch.empty((K, p), dtype=torch.float64, device=dev)
+    yty = torch.empty(K, dtype=torch.float64, device=dev)
+    counts = (ctypes.c_int64 * K)()
+    _check(lib().oem_gram_folds_host(ctx.h, X.data_ptr(), y.data_ptr(), n, p, X.stride(0), row_offset, K,
+                                     int(block_rows), _ptr(G), _ptr(xty), _ptr(yty), counts, _stream(stream)))
+    return G, xty, yty, list(counts)
 
 
 def oem_gram_moments(ctx: Context, X, y, K: int = 1, row_offset: int = 0, stream=None):

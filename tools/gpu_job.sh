@@ -1,3 +1,3 @@
 set -x
 mkdir -p gpurun_out
-timeout 900 python -m pytest tests/test_gpu_f3.py -m gpu -q > gpurun_out/t_new.log 2>&1; echo tests=$?
+timeout 900 python -m pytest tests/test_gpu_stream.py -m gpu -q > gpurun_out/t_new.log 2>&1; echo tests=$?
