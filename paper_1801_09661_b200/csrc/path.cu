@@ -530,7 +530,7 @@ __global__ void __launch_bounds__(PT, 1) path_kernel(const PathParams P) {
           const int j = v.j0 + r;
           const double u = c[j] + d * vec[q * P.ps + j] - a;
           if (!isfinite(u)) s_bad = 1;
-          if (!grp) {
+          if (!grp || P.fam[q] < OEM_GRP_LASSO) {  // coordinate-wise family (also when mixed with group ones)
             const double wj = P.var_w ? P.var_w[j] : 1.0;
             uv[q * P.smem_rows + r] = th_coord(P.fam[q], u, wj * s_lam[q], P.gam[q], P.alp[q], d);
           } else {
@@ -545,7 +545,7 @@ __global__ void __launch_bounds__(PT, 1) path_kernel(const PathParams P) {
       const int g0 = P.g_of[v.j0], g1 = P.g_of[v.j1 - 1] + 1;
       for (int e = threadIdx.x; e < (g1 - g0) * nP; e += blockDim.x) {
         const int q = e % nP, gid = g0 + e / nP;
-        if (!((qmask >> q) & 1u)) continue;
+        if (!((qmask >> q) & 1u) || P.fam[q] < OEM_GRP_LASSO) continue;
         const int a = P.g_start[gid] - v.j0, b = P.g_end[gid] - v.j0;
         double* ug = uv + q * P.smem_rows;
         double s = 0.0;
@@ -1010,7 +1010,7 @@ __global__ void __launch_bounds__(PT, 1) fit_lean_kernel(const PathParams P, con
       const double bj = vc[vi];
       const double u = c_my + d * bj - s;
       if (!isfinite(u)) bits |= 0x80000000u;
-      if (!grp) {
+      if (!grp || fam_my < OEM_GRP_LASSO) {  // coordinate-wise family (also when mixed with group ones)
         double lq = 0.0;
 #pragma unroll
         for (int q = 0; q < NPT; ++q)
@@ -1028,7 +1028,7 @@ __global__ void __launch_bounds__(PT, 1) fit_lean_kernel(const PathParams P, con
       __syncthreads();
       for (int e = tid; e < ng_loc * nP; e += PT) {
         const int q = e % nP, gl = e / nP;
-        if (!((qmask >> q) & 1u)) continue;
+        if (!((qmask >> q) & 1u) || s_fam[q] < OEM_GRP_LASSO) continue;
         const int ra = ga_s[gl], rb = gb_s[gl];
         const double* ug = uv + q * rows;
         double ss = 0.0;
@@ -1072,6 +1072,426 @@ __global__ void __launch_bounds__(PT, 1) fit_lean_kernel(const PathParams P, con
       if (!((qmask >> q) & 1u)) continue;
       const int it = itc[q] + 1;
       const bool conv = !((f >> q) & 1u);   // every |dbeta_j| <= tol (R#17)
+      if (conv || it >= P.maxit) {
+        const int l = lidx[q];
+        double* out = P.beta_out + (((size_t)unit * nP + q) * L + l) * p;
+        for (int r = tid; r < nr; r += PT) out[P.perm[j0 + r]] = vn[vix<NPT>(q, j0 + r, pvl)];
+        if (rank == 0 && tid == 0) {
+          P.it_out[((size_t)unit * nP + q) * L + l] = it;
+          P.cv_out[((size_t)unit * nP + q) * L + l] = conv ? 1 : 0;
+        }
+        lidx[q] = l + 1;
+        itc[q] = 0;
+        if (l + 1 < L) lam[q] = lam_at(q, l + 1);
+      } else {
+        itc[q] = it;
+      }
+    }
+  }
+}
+
+// ---------------------------------------------------------------- K4+K5 lean, grid-wide variant
+// For units too large for one cluster (p up to 1024, e.g. cfg4's p = 1000 split over ~63-100
+// CTAs): the same register-resident G tiles, batched penalties, reduce-scatter and OR-reduced
+// stopping rule as fit_lean_kernel, but the C CTAs of a unit exchange through L2 instead of
+// DSMEM: each CTA writes its new coordinates to a global double buffer and its "not converged"
+// bits to a per-CTA slot, meets the unit's other CTAs at a counter barrier (release add /
+// acquire poll, one per iteration), then copies the whole new vector back into shared memory
+// (ld.global.cg: L2, never a stale L1 line). Cooperative launch: every CTA is co-resident.
+struct GlobArgs {
+  int Cmax;             // max CTAs per unit (slot stride)
+  int rows, pvl, power_iters, compute_d;
+  double inflate;
+  double* d_out;        // [nU]
+  double* gvec;         // [2][nU][NV * pvl]
+  uint32_t* gflag;      // [2][nU][Cmax]
+  double* gslot;        // [2][nU][Cmax]
+  unsigned* gcnt;       // [nU] barrier counters (zero at launch)
+};
+
+__device__ __forceinline__ void red_release_add(unsigned* p, unsigned v) {
+  asm volatile("red.release.gpu.global.add.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+__device__ __forceinline__ unsigned ld_relaxed(const unsigned* p) {
+  unsigned v;
+  asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void fence_acquire_gpu() { asm volatile("fence.acq_rel.gpu;" ::: "memory"); }
+
+template <int NPT, int R, int KC, int T>
+__global__ void __launch_bounds__(PT, 1) fit_glob_kernel(const PathParams P, const GlobArgs A) {
+  constexpr int RG = PT / T, V = R * NPT, VP = pow2ceil(V), NW = PT / 32;
+  constexpr int NV = NPT == 1 ? 1 : 2 * ((NPT + 1) / 2);
+  static_assert(VP <= T && (T & (T - 1)) == 0 && T <= 32, "lean layout");
+  extern __shared__ __align__(16) double sm[];
+  __shared__ int s_fam[NPT], s_skip[NPT];
+  __shared__ double s_gam[NPT], s_alp[NPT], s_lmax[NPT];
+  __shared__ uint32_t s_bits, s_all;
+  __shared__ double s_red[NW], s_tot;
+  const int p = P.p, nP = P.nP, L = P.L, pvl = A.pvl, rows = A.rows;
+  const int tid = threadIdx.x, rg = tid / T, tl = tid % T, warp = tid >> 5, lane = tid & 31;
+  const int unit = P.cta_unit[blockIdx.x], rank = P.cta_rank[blockIdx.x], C = P.unit_ncta[unit];
+  const int j0 = P.cta_j0[blockIdx.x], j1 = P.cta_j1[blockIdx.x], nr = j1 - j0;
+  const int kcu = (p + T - 1) / T;
+  const bool wrows = (warp * (32 / T)) * R < nr;
+  const double* Gu = P.Gn + (size_t)unit * p * p;
+  const double* cu = P.cn + (size_t)unit * p;
+  const int vstride = pvl * NV;
+  double* vec = sm;                                   // [2][vstride] (local copies)
+  double* uv = vec + (size_t)2 * vstride;             // [NPT][rows]
+  double* gw_s = uv + (size_t)NPT * rows;
+  int* ga_s = reinterpret_cast<int*>(gw_s + rows);
+  int* gb_s = ga_s + rows;
+  double* gvec = A.gvec + (size_t)unit * vstride;     // + par * nU * vstride
+  const size_t gpar = (size_t)P.nU * vstride;
+  uint32_t* gflag = A.gflag + (size_t)unit * A.Cmax;  // + par * nU * Cmax
+  double* gslot = A.gslot + (size_t)unit * A.Cmax;
+  const size_t spar = (size_t)P.nU * A.Cmax;
+  unsigned epoch = 0;
+  // unit barrier: every CTA of the unit has published its writes (grid.sync pattern, per unit)
+  // (bar.sync orders the CTA's writes before thread 0's release, which is cumulative; relaxed
+  // polling, then one acquire fence: no L1 invalidation per poll)
+  auto unit_sync = [&]() {
+    __syncthreads();
+    if (tid == 0) {
+      red_release_add(&A.gcnt[unit], 1u);
+      const unsigned target = (epoch + 1) * (unsigned)C;
+      while (ld_relaxed(&A.gcnt[unit]) < target) {}
+      fence_acquire_gpu();
+    }
+    ++epoch;
+    __syncthreads();
+  };
+  const bool grp = P.g_of != nullptr;
+  const int g0 = (grp && nr > 0) ? P.g_of[j0] : 0;
+  const int ng_loc = (grp && nr > 0) ? P.g_of[j1 - 1] + 1 - g0 : 0;
+  for (int gg = tid; gg < ng_loc; gg += PT) {
+    gw_s[gg] = P.g_w[g0 + gg];
+    ga_s[gg] = P.g_start[g0 + gg] - j0;
+    gb_s[gg] = P.g_end[g0 + gg] - j0;
+  }
+  for (int k = tid; k < 2 * vstride; k += PT) vec[k] = 0.0;
+  double g[R][KC];
+#pragma unroll
+  for (int i = 0; i < R; ++i)
+#pragma unroll
+    for (int m = 0; m < KC; ++m) {
+      const int r = rg * R + i, k = tl + m * T;
+      g[i][m] = (r < nr && k < p) ? Gu[(size_t)(j0 + r) * p + k] : 0.0;
+    }
+  const int vidx = lean_vidx<VP, T>(tl);
+  const int mi = vidx / NPT, mq = vidx % NPT, mr = rg * R + mi;
+  const bool owner = (tl & (T / VP - 1)) == 0;
+  const bool act = owner && vidx < V && mr < nr;
+  const int mj = j0 + mr;
+  const double c_my = act ? cu[mj] : 0.0;
+  const double w_my = (act && P.var_w) ? P.var_w[mj] : 1.0;
+  constexpr int RP = pow2ceil(R);
+  const int vidx1 = lean_vidx<RP, T>(tl);
+  const int pr = rg * R + vidx1;
+  const bool pact = (tl & (T / RP - 1)) == 0 && vidx1 < R && pr < nr;
+  // CTA sum of one double per thread, in warp order; result in s_tot after the call
+  auto cta_sum = [&](double x) {
+#pragma unroll
+    for (int o = 16; o >= 1; o >>= 1) x += __shfl_xor_sync(0xffffffffu, x, o);
+    if (lane == 0) s_red[warp] = x;
+    __syncthreads();
+    if (tid == 0) {
+      double t = 0.0;
+      for (int w = 0; w < NW; ++w) t += s_red[w];
+      s_tot = t;
+    }
+    __syncthreads();
+    return s_tot;
+  };
+  // sum (or max) over the unit's CTAs of a per-CTA value, through the slots; fixed CTA order
+  auto unit_reduce = [&](double mine, int par, bool is_max) -> double {
+    if (tid == 0) gslot[par * spar + rank] = mine;
+    unit_sync();
+    if (warp == 0) {  // lane-strided loads, then a fixed butterfly: same order on every CTA
+      double r = 0.0;
+      for (int c = lane; c < C; c += 32) {
+        const double v = __ldcg(&gslot[par * spar + c]);
+        r = is_max ? fmax(r, v) : r + v;
+      }
+#pragma unroll
+      for (int o = 16; o >= 1; o >>= 1) {
+        const double v = __shfl_xor_sync(0xffffffffu, r, o);
+        r = is_max ? fmax(r, v) : r + v;
+      }
+      if (lane == 0) s_tot = r;
+    }
+    __syncthreads();
+    const double r = s_tot;
+    __syncthreads();
+    return r;
+  };
+
+  // ======================================================= a7: d by power iteration (R#5)
+  double d;
+  int par = 0;
+  if (A.compute_d) {
+    double gm = 0.0;
+#pragma unroll
+    for (int i = 0; i < R; ++i) {
+      double s = 0.0;
+#pragma unroll
+      for (int m = 0; m < KC; ++m) s += fabs(g[i][m]);
+#pragma unroll
+      for (int o = T / 2; o >= 1; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+      if (rg * R + i < nr) gm = fmax(gm, s);
+    }
+#pragma unroll
+    for (int o = 16; o >= 1; o >>= 1) gm = fmax(gm, __shfl_xor_sync(0xffffffffu, gm, o));
+    if (lane == 0) s_red[warp] = gm;
+    __syncthreads();
+    if (tid == 0) {
+      double t = 0.0;
+      for (int w = 0; w < NW; ++w) t = fmax(t, s_red[w]);
+      s_tot = t;
+    }
+    __syncthreads();
+    const double gersh = unit_reduce(s_tot, par, true);
+    par ^= 1;
+    const double v0 = 1.0 / sqrt((double)p);
+    for (int k = tid; k < p; k += PT) vec[vix<NPT>(0, k, pvl)] = v0;
+    __syncthreads();
+    double sc = 1.0, rq = 0.0;
+    for (int it = 0; it <= A.power_iters; ++it) {
+      const int cur = it & 1, nxt = cur ^ 1;
+      const double* vc = vec + (size_t)cur * vstride;
+      double a[RP];
+#pragma unroll
+      for (int i = 0; i < RP; ++i) a[i] = 0.0;
+      if (wrows) {
+#pragma unroll
+        for (int m = 0; m < KC; ++m) {
+          if (m >= kcu) break;
+          const double b = vc[vix<NPT>(0, tl + m * T, pvl)];
+#pragma unroll
+          for (int i = 0; i < R; ++i) a[i] = fma(g[i][m], b, a[i]);
+        }
+      }
+      const double s = lean_rs<RP, T>(a, tl);
+      double part = 0.0;
+      if (pact) {
+        const int j = j0 + pr;
+        if (it < A.power_iters) {
+          const double y = s * sc;
+          part = y * y;
+          gvec[nxt * gpar + vix<NPT>(0, j, pvl)] = y;
+        } else {
+          part = vc[vix<NPT>(0, j, pvl)] * s;
+        }
+      }
+      const double tot = unit_reduce(cta_sum(part), par, false);
+      par ^= 1;
+      if (it < A.power_iters) {
+        for (int k = tid; k < p; k += PT) vec[(size_t)nxt * vstride + vix<NPT>(0, k, pvl)] = __ldcg(&gvec[nxt * gpar + vix<NPT>(0, k, pvl)]);
+        __syncthreads();
+        if (tot > 0.0) sc = 1.0 / sqrt(tot);
+      } else {
+        rq = tot * sc * sc;
+      }
+    }
+    const double dd = (1.0 + A.inflate) * rq;
+    d = gersh < dd ? gersh : dd;
+    if (rank == 0 && tid == 0) A.d_out[unit] = d;
+    __syncthreads();
+    for (int k = tid; k < 2 * vstride; k += PT) vec[k] = 0.0;
+  } else {
+    d = P.d[unit];
+  }
+
+  // ======================================================= a8: lambda grid (R#14-16, R#22)
+  if (warp < NPT) {
+    const int q = warp;
+    double lm = 0.0;
+    int fam = 0;
+    double gq = 0.0, aq = 0.0;
+    if (q < nP) {
+      fam = P.fam[q]; gq = P.gam[q]; aq = P.alp[q];
+      const double* cc = P.shared_grid ? P.cn : cu;
+      if (P.lmax_override) {
+        lm = *P.lmax_override;
+      } else if (fam == OEM_SGL) {
+        for (int gg = lane; gg < P.ngroups; gg += 32)
+          lm = fmax(lm, sgl_lmax_group(cc, P.g_start[gg], P.g_end[gg], P.var_w, P.g_w[gg], aq));
+      } else if (fam >= OEM_GRP_LASSO) {
+        for (int gg = lane; gg < P.ngroups; gg += 32) {
+          const double cg = P.g_w[gg];
+          if (!(cg > 0.0)) continue;
+          double s = 0.0;
+          for (int j = P.g_start[gg]; j < P.g_end[gg]; ++j) s += cc[j] * cc[j];
+          lm = fmax(lm, sqrt(s) / cg);
+        }
+      } else {
+        const double scl = fam == OEM_ENET ? aq : 1.0;
+        for (int j = lane; j < p; j += 32) {
+          const double wj = P.var_w ? P.var_w[j] : 1.0;
+          if (!(wj > 0.0)) continue;
+          lm = fmax(lm, fabs(cc[j]) / (scl * wj));
+        }
+      }
+#pragma unroll
+      for (int o = 16; o >= 1; o >>= 1) lm = fmax(lm, __shfl_xor_sync(0xffffffffu, lm, o));
+    }
+    if (lane == 0) {
+      s_fam[q] = fam; s_gam[q] = gq; s_alp[q] = aq; s_lmax[q] = lm;
+      bool bad = false;
+      if (q < nP) {
+        if (fam == OEM_MCP || fam == OEM_GRP_MCP) bad = !(gq > 1.0) || !(gq * d > 1.0);
+        if (fam == OEM_SCAD || fam == OEM_GRP_SCAD) bad = !(gq > 2.0) || !((gq - 1.0) * d > 1.0);
+        if (fam == OEM_ENET) bad = !(aq >= 0.0 && aq <= 1.0);
+        if (bad && rank == 0) atomicExch(&P.flags[1], 1);
+      }
+      s_skip[q] = (q >= nP || bad) ? 1 : 0;
+    }
+  }
+  if (P.beta_init)
+    for (int e = tid; e < nP * p; e += PT) {
+      const int q = e / p, k = e % p;
+      vec[vix<NPT>(q, k, pvl)] = P.beta_init[((size_t)unit * nP + q) * p + P.perm[k]];
+    }
+  if (tid == 0) s_bits = 0u;
+  __syncthreads();
+  auto lam_at = [&](int q, int l) -> double {
+    if (P.lam_explicit) return P.lam_explicit[l];
+    if (L == 1) return s_lmax[q];
+    return s_lmax[q] * exp(((double)l / (double)(L - 1)) * log(P.lmin_ratio));  // R#15
+  };
+  if (rank == 0)
+    for (int e = tid; e < nP * L; e += PT) {
+      const int q = e / L, l = e % L;
+      P.lam_out[((size_t)unit * nP + q) * L + l] = lam_at(q, l);
+    }
+  int lidx[NPT], itc[NPT];
+  double lam[NPT];
+#pragma unroll
+  for (int q = 0; q < NPT; ++q) {
+    lidx[q] = s_skip[q] ? L : 0;
+    itc[q] = 0;
+    lam[q] = s_skip[q] ? 0.0 : lam_at(q, 0);
+  }
+  const int fam_my = s_fam[mq];
+  const double gam_my = s_gam[mq], alp_my = s_alp[mq];
+
+  // ======================================================= a9: OEM iterations
+  for (int t = 0;; ++t) {
+    uint32_t qmask = 0;
+#pragma unroll
+    for (int q = 0; q < NPT; ++q)
+      if (lidx[q] < L) qmask |= 1u << q;
+    if (!qmask) break;
+    const int cur = t & 1, nxt = cur ^ 1;
+    const double* vc = vec + (size_t)cur * vstride;
+    double* vn = vec + (size_t)nxt * vstride;
+    double* gn = gvec + nxt * gpar;
+    double a[VP];
+#pragma unroll
+    for (int v = 0; v < VP; ++v) a[v] = 0.0;
+    if (wrows) {
+#pragma unroll
+      for (int m = 0; m < KC; ++m) {
+        if (m >= kcu) break;
+        const int k = tl + m * T;
+        double b[NV];
+        if (NPT == 1) {
+          b[0] = vc[k];
+        } else {
+#pragma unroll
+          for (int h = 0; h < NV / 2; ++h) {
+            const double2 t2 = *reinterpret_cast<const double2*>(vc + h * 2 * pvl + 2 * k);
+            b[2 * h] = t2.x;
+            b[2 * h + 1] = t2.y;
+          }
+        }
+#pragma unroll
+        for (int i = 0; i < R; ++i)
+#pragma unroll
+          for (int q = 0; q < NPT; ++q) a[i * NPT + q] = fma(g[i][m], b[q], a[i * NPT + q]);
+      }
+    }
+    const double s = lean_rs<VP, T>(a, tl);
+    uint32_t bits = 0;
+    if (act && ((qmask >> mq) & 1u)) {
+      const int vi = vix<NPT>(mq, mj, pvl);
+      const double bj = vc[vi];
+      const double u = c_my + d * bj - s;
+      if (!isfinite(u)) bits |= 0x80000000u;
+      if (!grp || fam_my < OEM_GRP_LASSO) {  // coordinate-wise family (also when mixed with group ones)
+        double lq = 0.0;
+#pragma unroll
+        for (int q = 0; q < NPT; ++q)
+          if (q == mq) lq = lam[q];
+        const double nb = th_coord(fam_my, u, w_my * lq, gam_my, alp_my, d);
+        if (!(fabs(nb - bj) <= P.tol)) bits |= 1u << mq;
+        gn[vi] = nb;
+      } else {
+        uv[mq * rows + mr] = u;
+      }
+    }
+    if (grp) {
+      __syncthreads();
+      for (int e = tid; e < ng_loc * nP; e += PT) {
+        const int q = e % nP, gl = e / nP;
+        if (!((qmask >> q) & 1u) || s_fam[q] < OEM_GRP_LASSO) continue;
+        const int ra = ga_s[gl], rb = gb_s[gl];
+        const double* ug = uv + q * rows;
+        double ss = 0.0;
+        for (int r = ra; r < rb; ++r) ss += ug[r] * ug[r];
+        const double nu = sqrt(ss);
+        double lq = 0.0;
+#pragma unroll
+        for (int qq = 0; qq < NPT; ++qq)
+          if (qq == q) lq = lam[qq];
+        const int fam = s_fam[q];
+        const double gq = s_gam[q], lw = gw_s[gl] * lq, tau = s_alp[q];
+        double f;
+        if (fam == OEM_SGL) f = sgl_factor(ug, ra, rb, 1, P.var_w, j0, lq, tau, gw_s[gl], d);
+        else if (fam == OEM_GRP_LASSO) f = nu > 0.0 ? pos(1.0 - lw / nu) : 0.0;
+        else f = nu > 0.0 ? (fam == OEM_GRP_MCP ? th_mcp(nu, lw, gq, d) : th_scad(nu, lw, gq, d)) / nu : 0.0;
+        for (int r = ra; r < rb; ++r) {
+          const double nb = fam == OEM_SGL ? f * th_soft(ug[r], (P.var_w ? P.var_w[j0 + r] : 1.0) * lq * tau, d)
+                          : fam == OEM_GRP_LASSO ? ug[r] / d * f : f * ug[r];
+          const int vi = vix<NPT>(q, j0 + r, pvl);
+          if (!(fabs(nb - vc[vi]) <= P.tol)) bits |= 1u << q;
+          gn[vi] = nb;
+        }
+      }
+    }
+    bits = __reduce_or_sync(0xffffffffu, bits);
+    if (lane == 0 && bits) atomicOr(&s_bits, bits);
+    __syncthreads();
+    if (tid == 0) {
+      gflag[(t & 1) * spar + rank] = s_bits;
+      s_bits = 0u;
+    }
+    unit_sync();
+    // the unit's new vector and flags, from L2
+    for (int q = 0; q < nP; ++q)
+      for (int k = tid; k < p; k += PT) {
+        const int vi = vix<NPT>(q, k, pvl);
+        vn[vi] = __ldcg(&gn[vi]);
+      }
+    if (warp == 0) {
+      uint32_t w = 0;
+      for (int c = lane; c < C; c += 32) w |= __ldcg(&gflag[(t & 1) * spar + c]);
+      w = __reduce_or_sync(0xffffffffu, w);
+      if (lane == 0) s_all = w;
+    }
+    __syncthreads();
+    const uint32_t f = s_all;
+    if (f & 0x80000000u) {
+      if (tid == 0) atomicExch(&P.flags[0], 1);
+      break;
+    }
+#pragma unroll
+    for (int q = 0; q < NPT; ++q) {
+      if (!((qmask >> q) & 1u)) continue;
+      const int it = itc[q] + 1;
+      const bool conv = !((f >> q) & 1u);
       if (conv || it >= P.maxit) {
         const int l = lidx[q];
         double* out = P.beta_out + (((size_t)unit * nP + q) * L + l) * p;
@@ -1367,7 +1787,7 @@ __global__ void __launch_bounds__(PT, 1) fit_cluster_kernel(const PathParams P, 
           const double bj = vc[q * A.pv + j];
           const double u = c_s[r] + d * bj - a;
           if (!isfinite(u)) bad = true;
-          if (!grp) {
+          if (!grp || famq[q] < OEM_GRP_LASSO) {  // coordinate-wise family (also when mixed with group ones)
             const double nb = th_coord(famq[q], u, w_s[r] * lam[q], gamq[q], alpq[q], d);
             dmax[q] = fmax(dmax[q], fabs(nb - bj));
             if (C == 1) vn[q * A.pv + j] = nb;
@@ -1384,7 +1804,7 @@ __global__ void __launch_bounds__(PT, 1) fit_cluster_kernel(const PathParams P, 
       if (nr > 0) {
         for (int e = tid; e < ng_loc * nP; e += PT) {
           const int q = e % nP, gl = e / nP;
-          if (!((qmask >> q) & 1u)) continue;
+          if (!((qmask >> q) & 1u) || P.fam[q] < OEM_GRP_LASSO) continue;
           const int a = ga_s[gl], b = gb_s[gl];
           const double* ug = uv + q * nr;
           double s = 0.0;
@@ -1623,6 +2043,83 @@ static oem_status launch_lean_v(const PathParams& P, const LeanArgs& A, int nU, 
   return launch_lean_t<NPT, 2, 16, 16>(P, A, nU, lo.smem, st);
 }
 
+template <typename K>
+static oem_status coop_launch(K kern, int grid, size_t smem, cudaStream_t st, void** args) {
+  OEM_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  OEM_CUDA_TRY(cudaLaunchCooperativeKernel((const void*)kern, dim3(grid), dim3(PT), args, smem, st));
+  return OEM_OK;
+}
+
+// ---------------------------------------------------------------- grid-wide lean solver: layout / launch
+struct GlobLayout {
+  int variant = -1;  // 0: R1 KC32 T32 (16 rows / CTA, p <= 1024), 1: R2 KC16 T32 (32 rows, p <= 512)
+  int C = 0, rows = 0, pvl = 0;
+  size_t smem = 0;
+  std::vector<int> cuts;
+};
+
+template <int NPT, int R, int KC, int T>
+static int glob_capacity(size_t smem, int num_sms) {
+  int per = 0;
+  if (cudaFuncSetAttribute(fit_glob_kernel<NPT, R, KC, T>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) !=
+          cudaSuccess ||
+      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, fit_glob_kernel<NPT, R, KC, T>, PT, smem) != cudaSuccess)
+    return 0;
+  return per * num_sms;
+}
+
+static bool make_glob_layout(int nU, int p, int nP, const std::vector<int>& gstart, int num_sms, GlobLayout& lo) {
+  if (nP > 4 || p > 1024) return false;
+  const int v = p <= 512 ? 1 : 0;
+  const int rows = v == 1 ? 32 : 16, pvl = v == 1 ? 16 * 32 : 32 * 32;
+  std::vector<int> cuts{0};
+  if (gstart.empty()) {
+    const int C = (p + rows - 1) / rows;
+    for (int c = 1; c <= C; ++c) cuts.push_back((int)((int64_t)p * c / C));
+  } else {
+    std::vector<int> starts(gstart);
+    std::sort(starts.begin(), starts.end());
+    starts.push_back(p);
+    int last = 0;
+    for (size_t i = 1; i < starts.size(); ++i) {
+      const int b = starts[i];
+      if (b - cuts.back() > rows) {
+        if (last <= cuts.back()) return false;
+        cuts.push_back(last);
+        if (b - cuts.back() > rows) return false;
+      }
+      last = b;
+    }
+    if (cuts.back() != p) cuts.push_back(p);
+  }
+  const int C = (int)cuts.size() - 1;
+  const int NV = nP == 1 ? 1 : 2 * ((nP + 1) / 2);
+  const size_t smem = ((size_t)2 * NV * pvl + (size_t)nP * rows + rows) * 8 + (size_t)2 * rows * 4 + 16;
+  int cap = 0;
+  if (v == 0) {
+    cap = nP == 1 ? glob_capacity<1, 1, 32, 32>(smem, num_sms) : nP == 2 ? glob_capacity<2, 1, 32, 32>(smem, num_sms)
+        : nP == 3 ? glob_capacity<3, 1, 32, 32>(smem, num_sms) : glob_capacity<4, 1, 32, 32>(smem, num_sms);
+  } else {
+    cap = nP == 1 ? glob_capacity<1, 2, 16, 32>(smem, num_sms) : nP == 2 ? glob_capacity<2, 2, 16, 32>(smem, num_sms)
+        : nP == 3 ? glob_capacity<3, 2, 16, 32>(smem, num_sms) : glob_capacity<4, 2, 16, 32>(smem, num_sms);
+  }
+  if ((int64_t)nU * C > cap) return false;
+  lo.variant = v;
+  lo.C = C;
+  lo.rows = rows;
+  lo.pvl = pvl;
+  lo.smem = smem;
+  lo.cuts = cuts;
+  return true;
+}
+
+template <int NPT>
+static oem_status launch_glob_v(const PathParams& P, const GlobArgs& A, int grid, const GlobLayout& lo, cudaStream_t st) {
+  void* args[] = {const_cast<PathParams*>(&P), const_cast<GlobArgs*>(&A)};
+  if (lo.variant == 0) return coop_launch(fit_glob_kernel<NPT, 1, 32, 32>, grid, lo.smem, st, args);
+  return coop_launch(fit_glob_kernel<NPT, 2, 16, 32>, grid, lo.smem, st, args);
+}
+
 // ---------------------------------------------------------------- host side
 struct Layout {
   std::vector<int> unit, rank, ncta, j0, j1;
@@ -1711,12 +2208,6 @@ extern "C" void oem_path_cfg_default(oem_path_cfg* cfg) {
   cfg->intercept_out = nullptr;
 }
 
-template <typename K>
-static oem_status coop_launch(K kern, int grid, size_t smem, cudaStream_t st, void** args) {
-  OEM_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-  OEM_CUDA_TRY(cudaLaunchCooperativeKernel((const void*)kern, dim3(grid), dim3(PT), args, smem, st));
-  return OEM_OK;
-}
 
 static int ereg_for(int NPT) { return NPT <= 1 ? 32 : NPT == 2 ? 24 : NPT == 4 ? 16 : 8; }
 
@@ -1804,11 +2295,14 @@ extern "C" oem_status oem_fit_path(oem_ctx* ctx, const double* G, const double* 
   LeanLayout ll;
   const bool use_lean = !(force && (std::string(force) == "global" || std::string(force) == "cluster")) &&
                         make_lean_layout(p, nP, any_grp ? gstart : std::vector<int>(), ll);
-  bool use_cluster = !use_lean && !(force && std::string(force) == "global") &&
+  GlobLayout gl;
+  const bool use_glob = !use_lean && !(force && (std::string(force) == "global" || std::string(force) == "cluster")) &&
+                        make_glob_layout(nU, p, nP, any_grp ? gstart : std::vector<int>(), ctx->num_sms, gl);
+  bool use_cluster = !use_lean && !use_glob && !(force && std::string(force) == "global") &&
                      make_cluster_layout(nU, p, NPT, any_grp ? gstart : std::vector<int>(), ctx->num_sms,
                                          ereg_for(NPT), cl);
   std::string why;
-  if (!use_lean && !use_cluster &&
+  if (!use_lean && !use_glob && !use_cluster &&
       !make_layout(nU, p, NPT, any_grp ? gstart : std::vector<int>(), ctx->num_sms, 200 * 1024, lo, why))
     OEM_FAIL(OEM_ERR_UNSUPPORTED, "oem_fit_path: persistent solver layout: " + why);
   std::vector<int> t_unit, t_rank, t_ncta, t_j0, t_j1;
@@ -1818,6 +2312,12 @@ extern "C" oem_status oem_fit_path(oem_ctx* ctx, const double* G, const double* 
         t_unit.push_back(u); t_rank.push_back(c); t_j0.push_back(ll.cuts[c]); t_j1.push_back(ll.cuts[c + 1]);
       }
     t_ncta.assign(nU, ll.C);
+  } else if (use_glob) {
+    for (int u = 0; u < nU; ++u)
+      for (int c = 0; c < gl.C; ++c) {
+        t_unit.push_back(u); t_rank.push_back(c); t_j0.push_back(gl.cuts[c]); t_j1.push_back(gl.cuts[c + 1]);
+      }
+    t_ncta.assign(nU, gl.C);
   } else if (use_cluster) {
     for (int u = 0; u < nU; ++u)
       for (int c = 0; c < cl.C; ++c) { t_unit.push_back(u); t_rank.push_back(c); }
@@ -1834,7 +2334,7 @@ extern "C" oem_status oem_fit_path(oem_ctx* ctx, const double* G, const double* 
         if (gstart[g] < t_j0[i] && gend[g] > t_j0[i])
           OEM_FAIL(OEM_ERR_UNSUPPORTED, "oem_fit_path: a group is larger than one solver CTA's rows");
   }
-  const int Cmax = use_lean ? ll.C : use_cluster ? cl.C : lo.Cmax;
+  const int Cmax = use_lean ? ll.C : use_glob ? gl.C : use_cluster ? cl.C : lo.Cmax;
   // ---- workspace (device)
   const size_t pp = (size_t)p * p;
   size_t off = 0;
@@ -1866,6 +2366,10 @@ extern "C" oem_status oem_fit_path(oem_ctx* ctx, const double* G, const double* 
   const size_t o_j0 = take(sizeof(int) * ncta_total);
   const size_t o_j1 = take(sizeof(int) * ncta_total);
   const size_t o_d = take(sizeof(double) * nU);
+  const int gNV = nP == 1 ? 1 : 2 * ((nP + 1) / 2);
+  const size_t o_gvec = take(use_glob ? sizeof(double) * 2 * (size_t)nU * gNV * gl.pvl : 8);
+  const size_t o_gflag = take(use_glob ? sizeof(uint32_t) * 2 * (size_t)nU * Cmax : 8);
+  const size_t o_gslot = take(use_glob ? sizeof(double) * 2 * (size_t)nU * Cmax : 8);
   const bool centre = cfg.xsum != nullptr || cfg.ysum != nullptr;
   const bool xform = centre || cfg.standardize;
   if (centre && !(cfg.xsum && cfg.ysum)) OEM_FAIL(OEM_ERR_INVALID_ARG, "oem_fit_path: intercept needs both xsum and ysum");
@@ -1967,7 +2471,26 @@ extern "C" oem_status oem_fit_path(oem_ctx* ctx, const double* G, const double* 
   P.flags = flags;
   P.bad_iter = reinterpret_cast<unsigned long long*>(base + o_bad);
   double* dptr = reinterpret_cast<double*>(base + o_d);
-  if (use_lean) {
+  if (use_glob) {
+    // ---- a7-a10 fused in one cooperative launch: register-resident G, C CTAs per unit over L2
+    P.ps = 0; P.T = 0; P.smem_rows = 0;
+    GlobArgs A;
+    A.Cmax = Cmax; A.rows = gl.rows; A.pvl = gl.pvl;
+    A.power_iters = cfg.power_iters; A.inflate = cfg.d_inflate; A.compute_d = d_in ? 0 : 1; A.d_out = dptr;
+    A.gvec = reinterpret_cast<double*>(base + o_gvec);
+    A.gflag = reinterpret_cast<uint32_t*>(base + o_gflag);
+    A.gslot = reinterpret_cast<double*>(base + o_gslot);
+    A.gcnt = reinterpret_cast<unsigned*>(base + o_bar);   // zeroed with dslot / bar / flags
+    PhaseTimer tm(ctx, PH_PATH, st);
+    ++ctx->launches;
+    oem_status s;
+    const int grid = nU * gl.C;
+    if (nP == 1) s = launch_glob_v<1>(P, A, grid, gl, st);
+    else if (nP == 2) s = launch_glob_v<2>(P, A, grid, gl, st);
+    else if (nP == 3) s = launch_glob_v<3>(P, A, grid, gl, st);
+    else s = launch_glob_v<4>(P, A, grid, gl, st);
+    if (s != OEM_OK) return s;
+  } else if (use_lean) {
     // ---- a7-a10 fused in one launch: register-resident G, one cluster per unit
     P.ps = 0; P.T = 0; P.smem_rows = 0;
     LeanArgs A;

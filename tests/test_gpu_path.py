@@ -247,3 +247,29 @@ def test_sparse_group_lasso(ctx, p, solver, monkeypatch):
         assert np.max(np.abs(Bg - B)) <= TOL_BETA, (fam, np.max(np.abs(Bg - B)))
         assert np.array_equal(fit.conv[0, q].cpu().numpy().astype(bool), cv)
         assert np.max(np.abs(Bg[0])) <= 1e-12   # lambda_max: null up to the rounding at the root
+
+
+@pytest.mark.parametrize("p,solver", [(60, None), (60, "cluster"), (60, "global"), (700, None)])
+def test_mixed_group_and_coordinate_penalties(ctx, p, solver, monkeypatch):
+    """Group and coordinate-wise families fitted in ONE launch (cfg4 runs group lasso + EN
+    together): every penalty must match its own oracle path (each family keeps its own M-step)."""
+    from paper_1801_09661_b200 import oem_fit_path, oem_gram
+    if solver:
+        monkeypatch.setenv("OEM_PATH_SOLVER", solver)
+    spec = CONFIGS["cfg4"].spec.replace(n=4000, p=p, nnz=2)
+    bt = dg.beta(spec)
+    X, y = dg.rows_host(spec, bt)
+    G, c, yy, n = oem_gram(ctx, torch.from_numpy(X).cuda(), torch.from_numpy(y).cuda())
+    Go, co, _ = orc.gram(X, y)
+    grp = (np.arange(p) // 10).astype(np.int32)
+    pens = [("grp_lasso", 0.0, 1.0), ("enet", 0.0, 0.5), ("mcp", 3.0, 1.0), ("sgl", 0.0, 0.5)]
+    fit = oem_fit_path(ctx, G, c, [n], pens, nlambda=12, group=grp, ngroups=p // 10)
+    d = float(fit.d[0])
+    for q, (fam, gamma, alpha) in enumerate(pens):
+        g = grp if fam in ("grp_lasso", "sgl") else None
+        lg = fit.lam[0, q].cpu().numpy()
+        lmax = orc.lambda_max(fam, co / n, group=g, ngroups=p // 10 if g is not None else 0, alpha=alpha)
+        assert abs(lg[0] - lmax) <= 1e-12 * lmax
+        B, it, cv = orc.oem_path(Go / n, co / n, d, fam, lg, gamma, alpha, group=g,
+                                 ngroups=p // 10 if g is not None else 0)
+        assert np.max(np.abs(fit.beta[0, q].cpu().numpy() - B)) <= TOL_BETA, fam
