@@ -169,6 +169,34 @@ __device__ double sgl_lmax_group(const double* cc, int a, int b, const double* w
   return hi * (1.0 + 1e-12);
 }
 
+// One group's M-step by a whole warp (eqs glasso / gmcp / gscad / sglasso): lanes
+// own rows ra + lane + 32i, the norms are butterfly sums (fixed order), then every lane emits its
+// rows' new coordinates through emit(r, nb). ug: u of the group's rows (index r).
+template <class Emit>
+__device__ __forceinline__ void group_mstep_warp(const double* ug, int ra, int rb, int fam, double lq, double gq,
+                                                 double tau, double cg, double d, const double* wv, int j0, int lane,
+                                                 Emit&& emit) {
+  const bool sgl = fam == OEM_SGL;
+  double ss = 0.0;
+  for (int r = ra + lane; r < rb; r += 32) {
+    const double v = sgl ? th_soft(ug[r], (wv ? wv[j0 + r] : 1.0) * lq * tau, d) : ug[r];
+    ss += v * v;
+  }
+#pragma unroll
+  for (int o = 16; o >= 1; o >>= 1) ss += __shfl_xor_sync(0xffffffffu, ss, o);
+  const double nu = sqrt(ss);
+  const double lw = cg * lq;
+  double f;
+  if (sgl) f = nu > 0.0 ? pos(1.0 - cg * lq * (1.0 - tau) / (d * nu)) : 0.0;   // R#11 (nu = ||v||)
+  else if (fam == OEM_GRP_LASSO) f = nu > 0.0 ? pos(1.0 - lw / nu) : 0.0;
+  else f = nu > 0.0 ? (fam == OEM_GRP_MCP ? th_mcp(nu, lw, gq, d) : th_scad(nu, lw, gq, d)) / nu : 0.0;
+  for (int r = ra + lane; r < rb; r += 32) {
+    const double nb = sgl ? f * th_soft(ug[r], (wv ? wv[j0 + r] : 1.0) * lq * tau, d)
+                    : fam == OEM_GRP_LASSO ? ug[r] / d * f : f * ug[r];
+    emit(r, nb);
+  }
+}
+
 __device__ __forceinline__ void atomic_max_pos(unsigned long long* slot, double v) {
   // v >= 0: IEEE order equals unsigned-integer order of the bit patterns
   atomicMax(slot, (unsigned long long)__double_as_longlong(v));
@@ -1026,33 +1054,20 @@ __global__ void __launch_bounds__(PT, 1) fit_lean_kernel(const PathParams P, con
     if (grp) {
       // group M-step (eqs glasso / gmcp / gscad); groups lie inside [j0, j1)
       __syncthreads();
-      for (int e = tid; e < ng_loc * nP; e += PT) {
+      for (int e = warp; e < ng_loc * nP; e += NW) {   // one warp per (group, penalty)
         const int q = e % nP, gl = e / nP;
         if (!((qmask >> q) & 1u) || s_fam[q] < OEM_GRP_LASSO) continue;
-        const int ra = ga_s[gl], rb = gb_s[gl];
-        const double* ug = uv + q * rows;
-        double ss = 0.0;
-        for (int r = ra; r < rb; ++r) ss += ug[r] * ug[r];
-        const double nu = sqrt(ss);
         double lq = 0.0;
 #pragma unroll
         for (int qq = 0; qq < NPT; ++qq)
           if (qq == q) lq = lam[qq];
-        const int fam = s_fam[q];
-        const double gq = s_gam[q], lw = gw_s[gl] * lq;
-        double f;
-        const double tau = s_alp[q];
-        if (fam == OEM_SGL) f = sgl_factor(ug, ra, rb, 1, P.var_w, j0, lq, tau, gw_s[gl], d);
-        else if (fam == OEM_GRP_LASSO) f = nu > 0.0 ? pos(1.0 - lw / nu) : 0.0;
-        else f = nu > 0.0 ? (fam == OEM_GRP_MCP ? th_mcp(nu, lw, gq, d) : th_scad(nu, lw, gq, d)) / nu : 0.0;
-        for (int r = ra; r < rb; ++r) {
-          const double nb = fam == OEM_SGL ? f * th_soft(ug[r], (P.var_w ? P.var_w[j0 + r] : 1.0) * lq * tau, d)
-                          : fam == OEM_GRP_LASSO ? ug[r] / d * f : f * ug[r];
-          const int vi = vix<NPT>(q, j0 + r, pvl);
-          if (!(fabs(nb - vc[vi]) <= P.tol)) bits |= 1u << q;
-          if (C == 1) vn[vi] = nb;
-          else for (int rr = 0; rr < C; ++rr) st_cl_f64(&vn[vi], rr, nb);
-        }
+        group_mstep_warp(uv + q * rows, ga_s[gl], gb_s[gl], s_fam[q], lq, s_gam[q], s_alp[q], gw_s[gl], d, P.var_w, j0,
+                         lane, [&](int r, double nb) {
+                           const int vi = vix<NPT>(q, j0 + r, pvl);
+                           if (!(fabs(nb - vc[vi]) <= P.tol)) bits |= 1u << q;
+                           if (C == 1) vn[vi] = nb;
+                           else for (int rr = 0; rr < C; ++rr) st_cl_f64(&vn[vi], rr, nb);
+                         });
       }
     }
     bits = __reduce_or_sync(0xffffffffu, bits);
@@ -1104,7 +1119,7 @@ struct GlobArgs {
   double inflate;
   double* d_out;        // [nU]
   double* gvec;         // [2][nU][NV * pvl]
-  uint32_t* gflag;      // [2][nU][Cmax]
+  unsigned long long* gflag;  // [2][nU][Cmax] (iteration tag << 32) | not-converged bits (zero at launch)
   double* gslot;        // [2][nU][Cmax]
   unsigned* gcnt;       // [nU] barrier counters (zero at launch)
 };
@@ -1118,6 +1133,14 @@ __device__ __forceinline__ unsigned ld_relaxed(const unsigned* p) {
   return v;
 }
 __device__ __forceinline__ void fence_acquire_gpu() { asm volatile("fence.acq_rel.gpu;" ::: "memory"); }
+__device__ __forceinline__ void st_release_u64(unsigned long long* p, unsigned long long v) {
+  asm volatile("st.release.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+__device__ __forceinline__ unsigned long long ld_relaxed_u64(const unsigned long long* p) {
+  unsigned long long v;
+  asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
+}
 
 template <int NPT, int R, int KC, int T>
 __global__ void __launch_bounds__(PT, 1) fit_glob_kernel(const PathParams P, const GlobArgs A) {
@@ -1145,7 +1168,7 @@ __global__ void __launch_bounds__(PT, 1) fit_glob_kernel(const PathParams P, con
   int* gb_s = ga_s + rows;
   double* gvec = A.gvec + (size_t)unit * vstride;     // + par * nU * vstride
   const size_t gpar = (size_t)P.nU * vstride;
-  uint32_t* gflag = A.gflag + (size_t)unit * A.Cmax;  // + par * nU * Cmax
+  unsigned long long* gflag = A.gflag + (size_t)unit * A.Cmax;  // + par * nU * Cmax
   double* gslot = A.gslot + (size_t)unit * A.Cmax;
   const size_t spar = (size_t)P.nU * A.Cmax;
   unsigned epoch = 0;
@@ -1434,31 +1457,19 @@ __global__ void __launch_bounds__(PT, 1) fit_glob_kernel(const PathParams P, con
     }
     if (grp) {
       __syncthreads();
-      for (int e = tid; e < ng_loc * nP; e += PT) {
+      for (int e = warp; e < ng_loc * nP; e += NW) {   // one warp per (group, penalty)
         const int q = e % nP, gl = e / nP;
         if (!((qmask >> q) & 1u) || s_fam[q] < OEM_GRP_LASSO) continue;
-        const int ra = ga_s[gl], rb = gb_s[gl];
-        const double* ug = uv + q * rows;
-        double ss = 0.0;
-        for (int r = ra; r < rb; ++r) ss += ug[r] * ug[r];
-        const double nu = sqrt(ss);
         double lq = 0.0;
 #pragma unroll
         for (int qq = 0; qq < NPT; ++qq)
           if (qq == q) lq = lam[qq];
-        const int fam = s_fam[q];
-        const double gq = s_gam[q], lw = gw_s[gl] * lq, tau = s_alp[q];
-        double f;
-        if (fam == OEM_SGL) f = sgl_factor(ug, ra, rb, 1, P.var_w, j0, lq, tau, gw_s[gl], d);
-        else if (fam == OEM_GRP_LASSO) f = nu > 0.0 ? pos(1.0 - lw / nu) : 0.0;
-        else f = nu > 0.0 ? (fam == OEM_GRP_MCP ? th_mcp(nu, lw, gq, d) : th_scad(nu, lw, gq, d)) / nu : 0.0;
-        for (int r = ra; r < rb; ++r) {
-          const double nb = fam == OEM_SGL ? f * th_soft(ug[r], (P.var_w ? P.var_w[j0 + r] : 1.0) * lq * tau, d)
-                          : fam == OEM_GRP_LASSO ? ug[r] / d * f : f * ug[r];
-          const int vi = vix<NPT>(q, j0 + r, pvl);
-          if (!(fabs(nb - vc[vi]) <= P.tol)) bits |= 1u << q;
-          gn[vi] = nb;
-        }
+        group_mstep_warp(uv + q * rows, ga_s[gl], gb_s[gl], s_fam[q], lq, s_gam[q], s_alp[q], gw_s[gl], d, P.var_w, j0,
+                         lane, [&](int r, double nb) {
+                           const int vi = vix<NPT>(q, j0 + r, pvl);
+                           if (!(fabs(nb - vc[vi]) <= P.tol)) bits |= 1u << q;
+                           gn[vi] = nb;
+                         });
       }
     }
     bits = __reduce_or_sync(0xffffffffu, bits);
@@ -1477,12 +1488,11 @@ __global__ void __launch_bounds__(PT, 1) fit_glob_kernel(const PathParams P, con
       }
     if (warp == 0) {
       uint32_t w = 0;
-      for (int c = lane; c < C; c += 32) w |= __ldcg(&gflag[(t & 1) * spar + c]);
+      for (int c = lane; c < C; c += 32) w |= (uint32_t)__ldcg(&gflag[(t & 1) * spar + c]);
       w = __reduce_or_sync(0xffffffffu, w);
       if (lane == 0) s_all = w;
     }
-    __syncthreads();
-    const uint32_t f = s_all;
+    __syncthreads();    const uint32_t f = s_all;
     if (f & 0x80000000u) {
       if (tid == 0) atomicExch(&P.flags[0], 1);
       break;
@@ -2368,7 +2378,7 @@ extern "C" oem_status oem_fit_path(oem_ctx* ctx, const double* G, const double* 
   const size_t o_d = take(sizeof(double) * nU);
   const int gNV = nP == 1 ? 1 : 2 * ((nP + 1) / 2);
   const size_t o_gvec = take(use_glob ? sizeof(double) * 2 * (size_t)nU * gNV * gl.pvl : 8);
-  const size_t o_gflag = take(use_glob ? sizeof(uint32_t) * 2 * (size_t)nU * Cmax : 8);
+  const size_t o_gflag = take(use_glob ? sizeof(unsigned long long) * 2 * (size_t)nU * Cmax : 8);
   const size_t o_gslot = take(use_glob ? sizeof(double) * 2 * (size_t)nU * Cmax : 8);
   const bool centre = cfg.xsum != nullptr || cfg.ysum != nullptr;
   const bool xform = centre || cfg.standardize;
@@ -2478,7 +2488,8 @@ extern "C" oem_status oem_fit_path(oem_ctx* ctx, const double* G, const double* 
     A.Cmax = Cmax; A.rows = gl.rows; A.pvl = gl.pvl;
     A.power_iters = cfg.power_iters; A.inflate = cfg.d_inflate; A.compute_d = d_in ? 0 : 1; A.d_out = dptr;
     A.gvec = reinterpret_cast<double*>(base + o_gvec);
-    A.gflag = reinterpret_cast<uint32_t*>(base + o_gflag);
+    A.gflag = reinterpret_cast<unsigned long long*>(base + o_gflag);
+    OEM_CUDA_TRY(cudaMemsetAsync(A.gflag, 0, sizeof(unsigned long long) * 2 * (size_t)nU * Cmax, st));
     A.gslot = reinterpret_cast<double*>(base + o_gslot);
     A.gcnt = reinterpret_cast<unsigned*>(base + o_bar);   // zeroed with dslot / bar / flags
     PhaseTimer tm(ctx, PH_PATH, st);
