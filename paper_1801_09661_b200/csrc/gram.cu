@@ -28,6 +28,7 @@
 //    The result is packed (upper triangle of the augmented matrix) for one NCCL allreduce
 //    when the rows are sharded over GPUs.
 #include <algorithm>
+#include <cstdlib>
 #include <cstring>
 #include <vector>
 
@@ -200,7 +201,8 @@ __device__ __forceinline__ void consume(const GramParams& P, const Cons& cs) {
 // Running one stage ahead of the MMA warps (ready[] ring) keeps the DMMA pipe busy.
 __device__ __forceinline__ void weighted_rows(const GramParams& P, const Cons& cs, int rw) {
   const int ld = P.ld, lane = cs.lane;
-  const int k = rw * (BK / NRW) + (lane >> 2), sub = lane & 3;  // 4 lanes per row
+  constexpr int LPR = 32 * NRW / BK;                       // lanes per row
+  const int k = rw * (BK / NRW) + lane / LPR, sub = lane % LPR;
   double sw = 0.0, sll = 0.0;
   int st = 0;
   uint32_t ph = 0;
@@ -212,26 +214,23 @@ __device__ __forceinline__ void weighted_rows(const GramParams& P, const Cons& c
     const double* xr = pa + k * ld;
     double e0 = 0.0, e1 = 0.0;
     int j = sub;
-    for (; j + 4 < P.p; j += 8) {
+    for (; j + LPR < P.p; j += 2 * LPR) {
       e0 = fma(xr[j], cs.beta_s[j], e0);
-      e1 = fma(xr[j + 4], cs.beta_s[j + 4], e1);
+      e1 = fma(xr[j + LPR], cs.beta_s[j + LPR], e1);
     }
     if (j < P.p) e0 = fma(xr[j], cs.beta_s[j], e0);
     double e = e0 + e1;
-    e += __shfl_xor_sync(0xffffffffu, e, 1);
-    e += __shfl_xor_sync(0xffffffffu, e, 2);
+#pragma unroll
+    for (int o = 1; o < LPR; o <<= 1) e += __shfl_xor_sync(0xffffffffu, e, o);
     const int64_t row = cs.r0 + (int64_t)s * BK + k;
+    const bool valid = row < cs.r1;
+    const double yk = ys[k];
     double w = 0.0, z = 0.0;
-    if (row < cs.r1) {
+    if (valid) {
       double mu = 1.0 / (1.0 + exp(-e));
       mu = fmin(fmax(mu, P.eps), 1.0 - P.eps);
       w = mu * (1.0 - mu);
-      const double yk = ys[k];
       z = e + (yk - mu) / w;
-      if (sub == 0) {
-        sw += w;
-        sll += yk * e - (e > 0.0 ? e + log1p(exp(-e)) : log1p(exp(e)));
-      }
     }
     if (sub == 0) {
       ws[k] = w;
@@ -243,11 +242,17 @@ __device__ __forceinline__ void weighted_rows(const GramParams& P, const Cons& c
       mbar_arrive(&cs.ready[st]);
       mbar_arrive(&cs.empty[st]);
     }
+    // off the critical path (the MMA warps already have the stage): sum w and the
+    // log-likelihood, needed once per segment (CTA type 0 writes them)
+    if (cs.u == 0 && valid && sub == 0) {
+      sw += w;
+      sll += yk * e - (e > 0.0 ? e + log1p(exp(-e)) : log1p(exp(e)));
+    }
     if (++st == P.ST) { st = 0; ph ^= 1u; }
   }
-  // fixed-order reductions: lanes 0,4,..,28 hold their rows' sums; then warps in order
+  // fixed-order reductions: lanes 0, LPR, 2 LPR, .. hold their rows' sums; then warps in order
 #pragma unroll
-  for (int o = 4; o < 32; o <<= 1) {
+  for (int o = LPR; o < 32; o <<= 1) {
     sw += __shfl_xor_sync(0xffffffffu, sw, o);
     sll += __shfl_xor_sync(0xffffffffu, sll, o);
   }
@@ -366,6 +371,7 @@ gram_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ CUt
   // -------------------------------------------------------------- consumer warps
   cs.job = cd->job[warp];
   if (cs.job.kind == J_NONE) return;
+  constexpr bool BIGJ = TWO || MODE == MODE_WEIGHTED;  // 4x8 jobs only where registers allow
   switch (cs.job.kind) {
     case J_F44: consume<MODE, J_F44>(P, cs); break;
     case J_T4: consume<MODE, J_T4>(P, cs); break;
@@ -375,14 +381,14 @@ gram_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ CUt
     case J_T1: consume<MODE, J_T1>(P, cs); break;
     case J_T2: consume<MODE, J_T2>(P, cs); break;
     case J_T3: consume<MODE, J_T3>(P, cs); break;
-    case J_F48: if (TWO) consume<MODE, J_F48>(P, cs); break;
-    case J_T4F4: if (TWO) consume<MODE, J_T4F4>(P, cs); break;
-    case J_F45: if (TWO) consume<MODE, J_F45>(P, cs); break;
-    case J_F46: if (TWO) consume<MODE, J_F46>(P, cs); break;
-    case J_F47: if (TWO) consume<MODE, J_F47>(P, cs); break;
-    case J_T4F1: if (TWO) consume<MODE, J_T4F1>(P, cs); break;
-    case J_T4F2: if (TWO) consume<MODE, J_T4F2>(P, cs); break;
-    case J_T4F3: if (TWO) consume<MODE, J_T4F3>(P, cs); break;
+    case J_F48: if (BIGJ) consume<MODE, J_F48>(P, cs); break;
+    case J_T4F4: if (BIGJ) consume<MODE, J_T4F4>(P, cs); break;
+    case J_F45: if (BIGJ) consume<MODE, J_F45>(P, cs); break;
+    case J_F46: if (BIGJ) consume<MODE, J_F46>(P, cs); break;
+    case J_F47: if (BIGJ) consume<MODE, J_F47>(P, cs); break;
+    case J_T4F1: if (BIGJ) consume<MODE, J_T4F1>(P, cs); break;
+    case J_T4F2: if (BIGJ) consume<MODE, J_T4F2>(P, cs); break;
+    case J_T4F3: if (BIGJ) consume<MODE, J_T4F3>(P, cs); break;
     default: consume<MODE, J_NONE>(P, cs); break;
   }
 }
@@ -542,14 +548,35 @@ static oem_status build_plan(oem_ctx* ctx, int mode, int p, int64_t nrows, int K
   if (single) {
     pl.ld = 8 * pl.nb + 4;  // = 4 or 12 (mod 16): conflict-free fragment loads
     std::vector<Job> jobs;
-    for (int bi0 = 0; bi0 < pl.nb; bi0 += 4)
-      for (int bj0 = bi0; bj0 < pl.nb; bj0 += 4) {
-        const int Rr = std::min(4, pl.nb - bi0), Cc = std::min(4, pl.nb - bj0);
-        int kind;
-        if (bi0 == bj0) kind = Rr == 4 ? J_T4 : Rr == 3 ? J_T3 : Rr == 2 ? J_T2 : J_T1;
-        else kind = Cc == 4 ? J_F44 : Cc == 3 ? J_F43 : Cc == 2 ? J_F42 : J_F41;
-        jobs.push_back(Job{bi0, bj0, kind, 0});
+    // 4x4-block jobs (<= 96 registers: plain / fold passes run two CTAs per SM). The 4x8 strips
+    // (OEM_GRAM_STRIPS=1, weighted pass only) spill at 128 registers on sm_100a and measured
+    // slower (cfg5 16.5 vs 11.5 ms), so they stay opt-in.
+    const char* tile_env = std::getenv("OEM_GRAM_STRIPS");
+    if (mode != MODE_WEIGHTED || !(tile_env && tile_env[0] == '1')) {
+      // 4x4-block jobs
+      for (int bi0 = 0; bi0 < pl.nb; bi0 += 4)
+        for (int bj0 = bi0; bj0 < pl.nb; bj0 += 4) {
+          const int Rr = std::min(4, pl.nb - bi0), Cc = std::min(4, pl.nb - bj0);
+          int kind;
+          if (bi0 == bj0) kind = Rr == 4 ? J_T4 : Rr == 3 ? J_T3 : Rr == 2 ? J_T2 : J_T1;
+          else kind = Cc == 4 ? J_F44 : Cc == 3 ? J_F43 : Cc == 2 ? J_F42 : J_F41;
+          jobs.push_back(Job{bi0, bj0, kind, 0});
+        }
+    } else {
+      // 4-row strips: a T4Fk head on the diagonal (triangle + up to 4 full columns), then 4x8
+      // F48 jobs and one ragged F4c: up to 32 independent DMMA chains per warp per k-step
+      for (int bi0 = 0; bi0 < pl.nb; bi0 += 4) {
+        const int Rr = std::min(4, pl.nb - bi0);
+        if (Rr < 4) {
+          jobs.push_back(Job{bi0, bi0, Rr == 3 ? J_T3 : Rr == 2 ? J_T2 : J_T1, 0});
+          continue;
+        }
+        const int head = std::min(8, pl.nb - bi0);  // 4..8 columns
+        jobs.push_back(Job{bi0, bi0, kind_of(4, head, true), 0});
+        for (int bj0 = bi0 + head; bj0 < pl.nb; bj0 += 8)
+          jobs.push_back(Job{bi0, bj0, kind_of(4, std::min(8, pl.nb - bj0), false), 0});
       }
+    }
     pack_jobs(jobs, 0, 0, 1, pl.ctas);
   } else {
     pl.ld = 132;  // 128-column panel + 4 (mod 16 = 4)
