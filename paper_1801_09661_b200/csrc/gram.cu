@@ -39,9 +39,10 @@ namespace oem {
 
 constexpr int BK = 32;      // rows per pipeline stage
 constexpr int MAXST = 6;    // max pipeline stages
-constexpr int NWC = 8;      // consumer warps per CTA
-constexpr int NRW = 4;      // WEIGHTED: row warps (eta, mu, w, z per row, one stage ahead of the MMA warps)
-__host__ __device__ constexpr int gram_threads(int mode) { return (NWC + (mode == 2 ? NRW : 0) + 1) * 32; }
+constexpr int NWC_MAX = 16; // consumer (MMA) warps per CTA: 16 for single-panel plans, 8 for two-panel ones
+__host__ __device__ constexpr int nwc_of(bool two) { return two ? 8 : 16; }
+constexpr int NRW = 2;      // WEIGHTED: row warps (eta, mu, w, z per row, one stage ahead of the MMA warps)
+__host__ __device__ constexpr int gram_threads(int mode, bool two) { return (nwc_of(two) + (mode == 2 ? NRW : 0) + 1) * 32; }
 
 // job kinds: shape (R x C blocks) and which blocks are issued. Full kinds F4c issue all 4 x c
 // blocks; triangular kinds (T1..T4 and T4Fk = T4 followed by k full columns) issue (r, c) with
@@ -85,7 +86,7 @@ struct CtaDesc {
   int32_t a0, b0;     // first column of panel A / panel B
   int32_t same;       // panel B == panel A
   int32_t njob;       // consumer warps with work (arrivals per stage release)
-  Job job[NWC];       // slot w = consumer warp w (SMSP w % 4); J_NONE = idle
+  Job job[NWC_MAX];   // slot w = consumer warp w (SMSP w % 4); J_NONE = idle
 };
 
 struct GramParams {
@@ -119,7 +120,7 @@ struct Cons {
   bool two;
   Job job;
   const double* beta_s;
-  double* scal_s;     // WEIGHTED: [NWC][2] per-warp (sum w, loglik)
+  double* scal_s;     // WEIGHTED: [NRW][2] per-row-warp (sum w, loglik)
 };
 
 template <int MODE, int KIND>
@@ -267,7 +268,7 @@ __device__ __forceinline__ void weighted_rows(const GramParams& P, const Cons& c
 }
 
 template <int MODE, bool TWO>
-__global__ void __launch_bounds__(gram_threads(MODE), (TWO || MODE == MODE_WEIGHTED) ? 1 : 2)
+__global__ void __launch_bounds__(gram_threads(MODE, TWO), 1)
 gram_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ CUtensorMap tmY, const GramParams P) {
   extern __shared__ __align__(128) double smem[];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -326,11 +327,12 @@ gram_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ CUt
 
   cs.warp = warp;
   cs.lane = lane;
+  constexpr int NWC = nwc_of(TWO);
   if (MODE == MODE_WEIGHTED && warp >= NWC && warp < NWC + NRW) {
     weighted_rows(P, cs, warp - NWC);
     return;
   }
-  if (warp == gram_threads(MODE) / 32 - 1) {
+  if (warp == gram_threads(MODE, TWO) / 32 - 1) {
     // ------------------------------------------------------------ producer warp
     if (!P.ytma || lane == 0) {
       int st = 0;
@@ -371,7 +373,7 @@ gram_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ CUt
   // -------------------------------------------------------------- consumer warps
   cs.job = cd->job[warp];
   if (cs.job.kind == J_NONE) return;
-  constexpr bool BIGJ = TWO || MODE == MODE_WEIGHTED;  // 4x8 jobs only where registers allow
+  constexpr bool BIGJ = TWO;  // 4x8 jobs only in two-panel plans (registers)
   switch (cs.job.kind) {
     case J_F44: consume<MODE, J_F44>(P, cs); break;
     case J_T4: consume<MODE, J_T4>(P, cs); break;
@@ -490,7 +492,7 @@ struct GramPlan {
 
 // Spread jobs over CTA types (longest-processing-time first), then order each CTA's jobs so
 // the 4 SM sub-partitions (warp w -> SMSP w % 4) carry similar DMMA counts.
-static void pack_jobs(std::vector<Job>& jobs, int a0, int b0, int same, std::vector<CtaDesc>& out) {
+static void pack_jobs(std::vector<Job>& jobs, int a0, int b0, int same, std::vector<CtaDesc>& out, int NWC) {
   std::sort(jobs.begin(), jobs.end(),
             [](const Job& x, const Job& y) { return kind_cost(x.kind) > kind_cost(y.kind); });
   const int U = std::max<int>(1, ((int)jobs.size() + NWC - 1) / NWC);
@@ -517,7 +519,7 @@ static void pack_jobs(std::vector<Job>& jobs, int a0, int b0, int same, std::vec
       sl[best] += kind_cost(j.kind);
     }
     // warp w runs slot w (SMSP w % 4); idle slots hold J_NONE and exit early
-    for (int w = 0; w < NWC; ++w) cd.job[w] = Job{0, 0, J_NONE, 0};
+    for (int w = 0; w < NWC_MAX; ++w) cd.job[w] = Job{0, 0, J_NONE, 0};
     int nj = 0;
     for (int q = 0; q < 4; ++q)
       for (size_t k = 0; k < sub[q].size(); ++k) { cd.job[q + 4 * k] = sub[q][k]; ++nj; }
@@ -547,37 +549,40 @@ static oem_status build_plan(oem_ctx* ctx, int mode, int p, int64_t nrows, int K
   }
   if (single) {
     pl.ld = 8 * pl.nb + 4;  // = 4 or 12 (mod 16): conflict-free fragment loads
-    std::vector<Job> jobs;
-    // 4x4-block jobs (<= 96 registers: plain / fold passes run two CTAs per SM). The 4x8 strips
-    // (OEM_GRAM_STRIPS=1, weighted pass only) spill at 128 registers on sm_100a and measured
-    // slower (cfg5 16.5 vs 11.5 ms), so they stay opt-in.
-    const char* tile_env = std::getenv("OEM_GRAM_STRIPS");
-    if (mode != MODE_WEIGHTED || !(tile_env && tile_env[0] == '1')) {
-      // 4x4-block jobs
+    // One CTA per SM with 16 MMA warps (4 per SM sub-partition). Jobs are 4x4-block tiles of
+    // the upper triangle, optionally with every full 4x4 tile split into two 4x2 ones; the tiling
+    // whose packing gives the smaller (CTA types x busiest sub-partition) is kept: every CTA type
+    // streams all rows, and a CTA's stage time is that of its busiest sub-partition.
+    auto tile = [&](bool split) {
+      std::vector<Job> jobs;
       for (int bi0 = 0; bi0 < pl.nb; bi0 += 4)
         for (int bj0 = bi0; bj0 < pl.nb; bj0 += 4) {
           const int Rr = std::min(4, pl.nb - bi0), Cc = std::min(4, pl.nb - bj0);
-          int kind;
-          if (bi0 == bj0) kind = Rr == 4 ? J_T4 : Rr == 3 ? J_T3 : Rr == 2 ? J_T2 : J_T1;
-          else kind = Cc == 4 ? J_F44 : Cc == 3 ? J_F43 : Cc == 2 ? J_F42 : J_F41;
-          jobs.push_back(Job{bi0, bj0, kind, 0});
+          if (bi0 == bj0) { jobs.push_back(Job{bi0, bj0, Rr == 4 ? J_T4 : Rr == 3 ? J_T3 : Rr == 2 ? J_T2 : J_T1, 0}); continue; }
+          if (split && Cc == 4) {
+            jobs.push_back(Job{bi0, bj0, J_F42, 0});
+            jobs.push_back(Job{bi0, bj0 + 2, J_F42, 0});
+          } else {
+            jobs.push_back(Job{bi0, bj0, Cc == 4 ? J_F44 : Cc == 3 ? J_F43 : Cc == 2 ? J_F42 : J_F41, 0});
+          }
         }
-    } else {
-      // 4-row strips: a T4Fk head on the diagonal (triangle + up to 4 full columns), then 4x8
-      // F48 jobs and one ragged F4c: up to 32 independent DMMA chains per warp per k-step
-      for (int bi0 = 0; bi0 < pl.nb; bi0 += 4) {
-        const int Rr = std::min(4, pl.nb - bi0);
-        if (Rr < 4) {
-          jobs.push_back(Job{bi0, bi0, Rr == 3 ? J_T3 : Rr == 2 ? J_T2 : J_T1, 0});
-          continue;
+      return jobs;
+    };
+    auto score = [&](const std::vector<CtaDesc>& ctas) {
+      int worst = 0;
+      for (const auto& cd : ctas)
+        for (int q = 0; q < 4; ++q) {
+          int l = 0;
+          for (int w = q; w < NWC_MAX; w += 4) l += kind_cost(cd.job[w].kind);
+          worst = std::max(worst, l);
         }
-        const int head = std::min(8, pl.nb - bi0);  // 4..8 columns
-        jobs.push_back(Job{bi0, bi0, kind_of(4, head, true), 0});
-        for (int bj0 = bi0 + head; bj0 < pl.nb; bj0 += 8)
-          jobs.push_back(Job{bi0, bj0, kind_of(4, std::min(8, pl.nb - bj0), false), 0});
-      }
-    }
-    pack_jobs(jobs, 0, 0, 1, pl.ctas);
+      return (int64_t)ctas.size() * worst;
+    };
+    std::vector<CtaDesc> c0, c1;
+    auto j0 = tile(false), j1 = tile(true);
+    pack_jobs(j0, 0, 0, 1, c0, nwc_of(false));
+    pack_jobs(j1, 0, 0, 1, c1, nwc_of(false));
+    pl.ctas = score(c1) < score(c0) ? c1 : c0;
   } else {
     pl.ld = 132;  // 128-column panel + 4 (mod 16 = 4)
     const int np = pl.nb / 16;
@@ -610,7 +615,7 @@ static oem_status build_plan(oem_ctx* ctx, int mode, int p, int64_t nrows, int K
           const int k = kind_of(ru, cu, kind_tri(jb.kind));
           kept.push_back(Job{jb.bi0, jb.bj0, k != J_NONE ? k : jb.kind, 0});
         }
-        pack_jobs(kept, 128 * I, 128 * J, I == J, pl.ctas);
+        pack_jobs(kept, 128 * I, 128 * J, I == J, pl.ctas, nwc_of(true));
       }
     }
   }
@@ -633,9 +638,9 @@ static oem_status build_plan(oem_ctx* ctx, int mode, int p, int64_t nrows, int K
   const size_t fixed = (mode == MODE_WEIGHTED ? pl.ld * 8 : 0) + 2 * MAXST * 8;
   // two CTAs per SM for single-panel plans when at least 3 stages fit in half the SM
   const size_t half = 110 * 1024, whole = 220 * 1024;
-  int st_half = (int)std::min<size_t>(4, (half - fixed) / ((size_t)pl.stage_doubles * 8));
-  const bool two_per_sm = !pl.two_panel && mode != MODE_WEIGHTED && st_half >= 3;
-  pl.ST = two_per_sm ? st_half : (int)std::min<size_t>(4, (whole - fixed) / ((size_t)pl.stage_doubles * 8));
+  (void)half;
+  const bool two_per_sm = false;  // one CTA per SM (16 MMA warps for single-panel plans)
+  pl.ST = (int)std::min<size_t>(pl.two_panel ? 4 : MAXST, (whole - fixed) / ((size_t)pl.stage_doubles * 8));
   if (pl.ST < 2) OEM_FAIL(OEM_ERR_UNSUPPORTED, "gram: stage does not fit shared memory");
   pl.smem = (size_t)pl.ST * pl.stage_doubles * 8 + fixed;
   // segments: enough (CTA type, segment) items for ~8 waves over the SMs (short tail)
@@ -704,7 +709,7 @@ static oem_status launch_t(const GramPlan& pl, const CUtensorMap& mx, const CUte
     attr_smem = pl.smem;
   }
   dim3 grid((unsigned)(pl.U * pl.nseg * nfold));
-  kern<<<grid, gram_threads(MODE), pl.smem, st>>>(mx, my, P);
+  kern<<<grid, gram_threads(MODE, TWO), pl.smem, st>>>(mx, my, P);
   OEM_CUDA_TRY(cudaGetLastError());
   return OEM_OK;
 }

@@ -1988,8 +1988,13 @@ struct LeanLayout {
 };
 
 static bool make_lean_layout(int p, int NPT, const std::vector<int>& gstart, LeanLayout& lo) {
-  static const int R_[3] = {1, 2, 2}, KC_[3] = {8, 16, 16}, T_[3] = {8, 8, 16};
+  // variants: rows per CTA = R * 512 / T, columns = KC * T
+  static const int R_[5] = {1, 2, 2, 1, 1}, KC_[5] = {8, 16, 16, 8, 16}, T_[5] = {8, 8, 16, 16, 16};
   int v = p <= 64 ? 0 : p <= 128 ? 1 : p <= 256 ? 2 : -1;
+  if (const char* ev = std::getenv("OEM_LEAN_VARIANT")) {  // developer override (timing studies)
+    const int f = std::atoi(ev);
+    if (f >= 0 && f < 5 && KC_[f] * T_[f] >= p) v = f;
+  }
   if (v < 0 || NPT > 4) return false;
   const int rows = R_[v] * (PT / T_[v]);
   // contiguous row blocks of <= rows rows, cut only at group starts (greedy packing)
@@ -2050,6 +2055,8 @@ template <int NPT>
 static oem_status launch_lean_v(const PathParams& P, const LeanArgs& A, int nU, const LeanLayout& lo, cudaStream_t st) {
   if (lo.variant == 0) return launch_lean_t<NPT, 1, 8, 8>(P, A, nU, lo.smem, st);
   if (lo.variant == 1) return launch_lean_t<NPT, 2, 16, 8>(P, A, nU, lo.smem, st);
+  if (lo.variant == 3) return launch_lean_t<NPT, 1, 8, 16>(P, A, nU, lo.smem, st);
+  if (lo.variant == 4) return launch_lean_t<NPT, 1, 16, 16>(P, A, nU, lo.smem, st);
   return launch_lean_t<NPT, 2, 16, 16>(P, A, nU, lo.smem, st);
 }
 
