@@ -125,6 +125,7 @@ oem_status oem_ctx_destroy(oem_ctx* ctx) {
   if (ctx->nccl_comm) ncclCommDestroy((ncclComm_t)ctx->nccl_comm);
   ctx->plans.clear();
   ctx->partial.release();
+  ctx->partial2.release();
   ctx->partial_scal.release();
   ctx->packed.release();
   ctx->tail.release();

@@ -424,6 +424,32 @@ __global__ void gram_reduce_kernel(const double* __restrict__ partial, int nfold
   }
 }
 
+// First level of the split-n reduction when there are many segments: chunk c of S sums the
+// segments [c*per, (c+1)*per) in order; the output has the partial buffer's layout with nseg = S
+// (so gram_reduce_kernel finishes it). Deterministic; spreads the segment loop over many threads.
+__global__ void gram_chunk_kernel(const double* __restrict__ partial, int nfold, int nseg, int nblk, int S, int per,
+                                  double* __restrict__ out, const double* __restrict__ pscal, double* __restrict__ oscal) {
+  const int64_t total = (int64_t)nfold * S * nblk * 64;
+  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < total; t += (int64_t)gridDim.x * blockDim.x) {
+    const int e = (int)(t & 63);
+    const int64_t r = t >> 6;
+    const int idx = (int)(r % nblk);
+    const int64_t fc = r / nblk;
+    const int c = (int)(fc % S), f = (int)(fc / S);
+    const int g0 = c * per, g1 = min(nseg, g0 + per);
+    double s = 0.0;
+    for (int g = g0; g < g1; ++g) s += partial[(((size_t)f * nseg + g) * nblk + idx) * 64 + e];
+    out[(((size_t)f * S + c) * nblk + idx) * 64 + e] = s;
+  }
+  if (pscal && blockIdx.x == 0)
+    for (int i = threadIdx.x; i < 2 * S; i += blockDim.x) {
+      const int c = i / 2, k = i % 2;
+      double s = 0.0;
+      for (int g = c * per; g < min(nseg, (c + 1) * per); ++g) s += pscal[g * 2 + k];
+      oscal[i] = s;
+    }
+}
+
 // FOLD tail: rows i in [nq*K, n_local) (fewer than K, so at most one per fold) as outer products.
 __global__ void gram_fold_tail_kernel(const double* __restrict__ X, const double* __restrict__ y, int64_t ldx,
                                       int64_t n_local, int64_t nq, int K, int off_mod, int p, int nblk,
@@ -808,11 +834,28 @@ oem_status gram_pass(oem_ctx* ctx, int mode, const double* X, const double* y, c
     OEM_CUDA_TRY(cudaGetLastError());
   }
   {
+    const double* src = ctx->partial.as<double>();
+    const double* sscal = ctx->partial_scal.as<double>();
+    int nseg = nq > 0 ? pl.nseg : 0;
+    if (nseg > 64) {  // two-level: chunks of `per` segments in parallel, then the final sum
+      const int per = 16, S = (nseg + per - 1) / per;
+      OEM_CUDA_TRY(ctx->partial2.ensure(sizeof(double) * (size_t)nfold * S * pl.nblk * 64 + sizeof(double) * (2 * S + 16)));
+      double* out = ctx->partial2.as<double>();
+      double* oscal = out + (size_t)nfold * S * pl.nblk * 64;
+      const int64_t total = (int64_t)nfold * S * pl.nblk * 64;
+      const int blocks = (int)std::max<int64_t>(1, std::min<int64_t>(ctx->num_sms * 16, (total + 255) / 256));
+      ++ctx->launches;
+      gram_chunk_kernel<<<blocks, 256, 0, st>>>(src, nfold, nseg, pl.nblk, S, per, out,
+                                                mode == MODE_WEIGHTED ? sscal : nullptr, oscal);
+      OEM_CUDA_TRY(cudaGetLastError());
+      src = out;
+      sscal = oscal;
+      nseg = S;
+    }
     const int64_t total = (int64_t)nfold * pl.nblk * 64;
     const int blocks = (int)std::max<int64_t>(1, std::min<int64_t>(ctx->num_sms * 8, (total + 255) / 256));
     ++ctx->launches;
-    gram_reduce_kernel<<<blocks, 256, 0, st>>>(ctx->partial.as<double>(), nfold, nq > 0 ? pl.nseg : 0, pl.nblk,
-                                               pl.d_blk_coord, p, tail, packed, psize, ctx->partial_scal.as<double>(),
+    gram_reduce_kernel<<<blocks, 256, 0, st>>>(src, nfold, nseg, pl.nblk, pl.d_blk_coord, p, tail, packed, psize, sscal,
                                                mode == MODE_WEIGHTED, accumulate);
     OEM_CUDA_TRY(cudaGetLastError());
   }

@@ -785,7 +785,8 @@ __global__ void __launch_bounds__(PT, 1) fit_lean_kernel(const PathParams P, con
   __shared__ int s_fam[NPT], s_skip[NPT];
   __shared__ double s_gam[NPT], s_alp[NPT], s_lmax[NPT];
   __shared__ uint32_t F[3];
-  const int p = P.p, nP = P.nP, L = P.L, C = A.C, pvl = A.pvl, rows = A.rows;
+  const int p = P.p, nP = P.nP, L = P.L, C = A.C;
+  constexpr int pvl = KC * T, rows = R * RG;  // == A.pvl, A.rows (compile-time: immediate offsets)
   const int tid = threadIdx.x, rg = tid / T, tl = tid % T, warp = tid >> 5, lane = tid & 31;
   const uint32_t rank = cluster_rank();
   const int unit = blockIdx.x / C;
@@ -796,7 +797,7 @@ __global__ void __launch_bounds__(PT, 1) fit_lean_kernel(const PathParams P, con
   const double* cu = P.cn + (size_t)unit * p;
   // shared memory: vec [2][pvl*NV] | slots [2][C*NW] | uv [NPT][rows] | gw [rows] | ga, gb [rows]
   double* vec = sm;
-  const int vstride = pvl * NV;
+  constexpr int vstride = pvl * NV;
   double* slots = vec + (size_t)2 * vstride;
   double* uv = slots + (size_t)2 * C * NW;
   double* gw_s = uv + (size_t)NPT * rows;
@@ -1152,7 +1153,8 @@ __global__ void __launch_bounds__(PT, 1) fit_glob_kernel(const PathParams P, con
   __shared__ double s_gam[NPT], s_alp[NPT], s_lmax[NPT];
   __shared__ uint32_t s_bits, s_all;
   __shared__ double s_red[NW], s_tot;
-  const int p = P.p, nP = P.nP, L = P.L, pvl = A.pvl, rows = A.rows;
+  const int p = P.p, nP = P.nP, L = P.L;
+  constexpr int pvl = KC * T, rows = R * RG;  // == A.pvl, A.rows
   const int tid = threadIdx.x, rg = tid / T, tl = tid % T, warp = tid >> 5, lane = tid & 31;
   const int unit = P.cta_unit[blockIdx.x], rank = P.cta_rank[blockIdx.x], C = P.unit_ncta[unit];
   const int j0 = P.cta_j0[blockIdx.x], j1 = P.cta_j1[blockIdx.x], nr = j1 - j0;
@@ -1160,7 +1162,7 @@ __global__ void __launch_bounds__(PT, 1) fit_glob_kernel(const PathParams P, con
   const bool wrows = (warp * (32 / T)) * R < nr;
   const double* Gu = P.Gn + (size_t)unit * p * p;
   const double* cu = P.cn + (size_t)unit * p;
-  const int vstride = pvl * NV;
+  constexpr int vstride = pvl * NV;
   double* vec = sm;                                   // [2][vstride] (local copies)
   double* uv = vec + (size_t)2 * vstride;             // [NPT][rows]
   double* gw_s = uv + (size_t)NPT * rows;
