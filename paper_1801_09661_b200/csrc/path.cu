@@ -112,13 +112,21 @@ __device__ __forceinline__ double th_soft(double u, double lam, double d) {     
 __device__ __forceinline__ double th_enet(double u, double lam, double a, double d) {  // eq (net)
   return sgn(u) * pos((fabs(u) - lam * a) / (d + lam * (1.0 - a)));
 }
+// (a zero numerator is returned without dividing: 0/x takes the slow path of the fp64 division
+// routine on the GPU, and the thresholded coordinates of a sparse path are mostly zero)
 __device__ __forceinline__ double th_mcp(double u, double lam, double g, double d) {   // eq (mcp)
-  if (fabs(u) <= lam * g * d) return sgn(u) * g * pos(fabs(u) - lam) / (g * d - 1.0);
+  if (fabs(u) <= lam * g * d) {
+    const double t = pos(fabs(u) - lam);
+    return t > 0.0 ? sgn(u) * g * t / (g * d - 1.0) : 0.0;
+  }
   return u / d;
 }
 __device__ __forceinline__ double th_scad(double u, double lam, double g, double d) {  // eq (scad)
   const double a = fabs(u);
-  if (a <= (d + 1.0) * lam) return sgn(u) * pos(a - lam) / d;
+  if (a <= (d + 1.0) * lam) {
+    const double t = pos(a - lam);
+    return t > 0.0 ? sgn(u) * t / d : 0.0;
+  }
   if (a <= lam * g * d) return sgn(u) * ((g - 1.0) * a - lam * g) / ((g - 1.0) * d - 1.0);
   return u / d;
 }
