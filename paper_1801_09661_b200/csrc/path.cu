@@ -784,9 +784,13 @@ __device__ __forceinline__ int vix(int q, int k, int pvl) {
   return NPT == 1 ? k : (q >> 1) * 2 * pvl + 2 * k + (q & 1);
 }
 
-template <int NPT, int R, int KC, int T>
+// RS > 0: each thread row group also owns RS rows kept in SHARED memory (for units whose rows do
+// not fit the register file, e.g. cfg3's eleven p = 500 Grams in clusters of 8). Thread (rg, tl)
+// owns local rows rg*RT + i, i < RT = R + RS: i < R from registers, i >= R from shared memory.
+template <int NPT, int R, int KC, int T, int RS = 0>
 __global__ void __launch_bounds__(PT, 1) fit_lean_kernel(const PathParams P, const LeanArgs A) {
-  constexpr int RG = PT / T, V = R * NPT, VP = pow2ceil(V), NW = PT / 32;
+  constexpr int RT = R + RS;
+  constexpr int RG = PT / T, V = RT * NPT, VP = pow2ceil(V), NW = PT / 32;
   constexpr int NV = NPT == 1 ? 1 : 2 * ((NPT + 1) / 2);  // doubles per k in the vector layout
   static_assert(VP <= T && (T & (T - 1)) == 0 && T <= 32, "lean layout");
   extern __shared__ __align__(16) double sm[];
@@ -794,19 +798,20 @@ __global__ void __launch_bounds__(PT, 1) fit_lean_kernel(const PathParams P, con
   __shared__ double s_gam[NPT], s_alp[NPT], s_lmax[NPT];
   __shared__ uint32_t F[3];
   const int p = P.p, nP = P.nP, L = P.L, C = A.C;
-  constexpr int pvl = KC * T, rows = R * RG;  // == A.pvl, A.rows (compile-time: immediate offsets)
+  constexpr int pvl = KC * T, rows = RT * RG;  // == A.pvl, A.rows (compile-time: immediate offsets)
   const int tid = threadIdx.x, rg = tid / T, tl = tid % T, warp = tid >> 5, lane = tid & 31;
   const uint32_t rank = cluster_rank();
   const int unit = blockIdx.x / C;
   const int j0 = P.cta_j0[blockIdx.x], j1 = P.cta_j1[blockIdx.x], nr = j1 - j0;
   const int kcu = (p + T - 1) / T;                       // column slots in use (warp-uniform)
-  const bool wrows = (warp * (32 / T)) * R < nr;         // this warp owns at least one row
+  const bool wrows = (warp * (32 / T)) * RT < nr;        // this warp owns at least one row
   const double* Gu = P.Gn + (size_t)unit * p * p;
   const double* cu = P.cn + (size_t)unit * p;
-  // shared memory: vec [2][pvl*NV] | slots [2][C*NW] | uv [NPT][rows] | gw [rows] | ga, gb [rows]
+  // shared memory: vec [2][pvl*NV] | gsm [RS*RG][pvl] | slots [2][C*NW] | uv [NPT][rows] | gw [rows] | ga, gb [rows]
   double* vec = sm;
   constexpr int vstride = pvl * NV;
-  double* slots = vec + (size_t)2 * vstride;
+  double* gsm = vec + (size_t)2 * vstride;
+  double* slots = gsm + (size_t)RS * RG * pvl;
   double* uv = slots + (size_t)2 * C * NW;
   double* gw_s = uv + (size_t)NPT * rows;
   int* ga_s = reinterpret_cast<int*>(gw_s + rows);
@@ -826,28 +831,40 @@ __global__ void __launch_bounds__(PT, 1) fit_lean_kernel(const PathParams P, con
   for (int k = tid; k < 2 * vstride; k += PT) vec[k] = 0.0;
   for (int k = tid; k < 2 * C * NW; k += PT) slots[k] = 0.0;
   if (tid < 3) F[tid] = 0u;
-  // this thread's tile of G (rows rg*R + i, columns tl + m*T), resident in registers
+  // this thread's tile of G (rows rg*RT + i, columns tl + m*T): i < R in registers for the whole
+  // launch, i >= R in shared memory (row rg*RS + i - R of gsm)
   double g[R][KC];
 #pragma unroll
   for (int i = 0; i < R; ++i)
 #pragma unroll
     for (int m = 0; m < KC; ++m) {
-      const int r = rg * R + i, k = tl + m * T;
+      const int r = rg * RT + i, k = tl + m * T;
       g[i][m] = (r < nr && k < p) ? Gu[(size_t)(j0 + r) * p + k] : 0.0;
     }
+#pragma unroll
+  for (int i = R; i < RT; ++i)
+#pragma unroll
+    for (int m = 0; m < KC; ++m) {
+      const int r = rg * RT + i, k = tl + m * T;
+      gsm[(size_t)(rg * RS + i - R) * pvl + k] = (r < nr && k < p) ? Gu[(size_t)(j0 + r) * p + k] : 0.0;
+    }
+  // element (i, m) of the thread's tile
+  auto gel = [&](int i, int m) -> double {
+    return i < R ? g[i < R ? i : 0][m] : gsm[(size_t)(rg * RS + i - R) * pvl + tl + m * T];
+  };
   // the (row, penalty) sum this lane owns after the reduce-scatter
   const int vidx = lean_vidx<VP, T>(tl);
-  const int mi = vidx / NPT, mq = vidx % NPT, mr = rg * R + mi;
+  const int mi = vidx / NPT, mq = vidx % NPT, mr = rg * RT + mi;
   const bool owner = (tl & (T / VP - 1)) == 0;
   const bool act = owner && vidx < V && mr < nr;
   const int mj = j0 + mr;
   const double c_my = act ? cu[mj] : 0.0;
   const double w_my = (act && P.var_w) ? P.var_w[mj] : 1.0;
-  // power iteration: an R-value reduce-scatter; the lane owns row rg*R + vidx1
-  constexpr int RP = pow2ceil(R);
+  // power iteration: an RT-value reduce-scatter; the lane owns row rg*RT + vidx1
+  constexpr int RP = pow2ceil(RT);
   const int vidx1 = lean_vidx<RP, T>(tl);
-  const int pr = rg * R + vidx1;
-  const bool pact = (tl & (T / RP - 1)) == 0 && vidx1 < R && pr < nr;
+  const int pr = rg * RT + vidx1;
+  const bool pact = (tl & (T / RP - 1)) == 0 && vidx1 < RT && pr < nr;
   cluster_sync_all();  // peers' buffers are zeroed before any remote store
 
   // ======================================================= a7: d by power iteration (R#5)
@@ -856,13 +873,13 @@ __global__ void __launch_bounds__(PT, 1) fit_lean_kernel(const PathParams P, con
     // Gershgorin bound: max_j sum_k |G_jk|
     double gm = 0.0;
 #pragma unroll
-    for (int i = 0; i < R; ++i) {
+    for (int i = 0; i < RT; ++i) {
       double s = 0.0;
 #pragma unroll
-      for (int m = 0; m < KC; ++m) s += fabs(g[i][m]);
+      for (int m = 0; m < KC; ++m) s += fabs(gel(i, m));
 #pragma unroll
       for (int o = T / 2; o >= 1; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
-      if (rg * R + i < nr) gm = fmax(gm, s);
+      if (rg * RT + i < nr) gm = fmax(gm, s);
     }
 #pragma unroll
     for (int o = 16; o >= 1; o >>= 1) gm = fmax(gm, __shfl_xor_sync(0xffffffffu, gm, o));
@@ -888,7 +905,7 @@ __global__ void __launch_bounds__(PT, 1) fit_lean_kernel(const PathParams P, con
           if (m >= kcu) break;
           const double b = vc[vix<NPT>(0, tl + m * T, pvl)];
 #pragma unroll
-          for (int i = 0; i < R; ++i) a[i] = fma(g[i][m], b, a[i]);
+          for (int i = 0; i < RT; ++i) a[i] = fma(gel(i, m), b, a[i]);
         }
       }
       const double s = lean_rs<RP, T>(a, tl);
@@ -1035,9 +1052,11 @@ __global__ void __launch_bounds__(PT, 1) fit_lean_kernel(const PathParams P, con
           }
         }
 #pragma unroll
-        for (int i = 0; i < R; ++i)
+        for (int i = 0; i < RT; ++i) {
+          const double gv = gel(i, m);
 #pragma unroll
-          for (int q = 0; q < NPT; ++q) a[i * NPT + q] = fma(g[i][m], b[q], a[i * NPT + q]);
+          for (int q = 0; q < NPT; ++q) a[i * NPT + q] = fma(gv, b[q], a[i * NPT + q]);
+        }
       }
     }
     const double s = lean_rs<VP, T>(a, tl);
@@ -1999,14 +2018,16 @@ struct LeanLayout {
 
 static bool make_lean_layout(int p, int NPT, const std::vector<int>& gstart, LeanLayout& lo) {
   // variants: rows per CTA = R * 512 / T, columns = KC * T
-  static const int R_[5] = {1, 2, 2, 1, 1}, KC_[5] = {8, 16, 16, 8, 16}, T_[5] = {8, 8, 16, 16, 16};
-  int v = p <= 64 ? 0 : p <= 128 ? 1 : p <= 256 ? 2 : -1;
+  // variant 5: 32 register rows + 32 shared-memory rows per CTA (p <= 512, clusters of <= 8)
+  static const int R_[6] = {1, 2, 2, 1, 1, 2}, KC_[6] = {8, 16, 16, 8, 16, 16}, T_[6] = {8, 8, 16, 16, 16, 32},
+                   RS_[6] = {0, 0, 0, 0, 0, 2};
+  int v = p <= 64 ? 0 : p <= 128 ? 1 : p <= 256 ? 2 : p <= 512 ? 5 : -1;
   if (const char* ev = std::getenv("OEM_LEAN_VARIANT")) {  // developer override (timing studies)
     const int f = std::atoi(ev);
-    if (f >= 0 && f < 5 && KC_[f] * T_[f] >= p) v = f;
+    if (f >= 0 && f < 6 && KC_[f] * T_[f] >= p) v = f;
   }
   if (v < 0 || NPT > 4) return false;
-  const int rows = R_[v] * (PT / T_[v]);
+  const int rows = (R_[v] + RS_[v]) * (PT / T_[v]);
   // contiguous row blocks of <= rows rows, cut only at group starts (greedy packing)
   std::vector<int> cuts{0};
   if (gstart.empty()) {
@@ -2036,7 +2057,8 @@ static bool make_lean_layout(int p, int NPT, const std::vector<int>& gstart, Lea
   lo.pvl = KC_[v] * T_[v];
   lo.cuts = cuts;
   const int NV = NPT == 1 ? 1 : 2 * ((NPT + 1) / 2);
-  lo.smem = ((size_t)2 * NV * lo.pvl + (size_t)2 * C * (PT / 32) + (size_t)NPT * rows + rows) * 8 +
+  lo.smem = ((size_t)2 * NV * lo.pvl + (size_t)RS_[v] * (PT / T_[v]) * lo.pvl + (size_t)2 * C * (PT / 32) +
+             (size_t)NPT * rows + rows) * 8 +
             (size_t)2 * rows * 4 + 16;
   return true;
 }
@@ -2062,11 +2084,32 @@ static oem_status launch_lean_t(const PathParams& P, const LeanArgs& A, int nU, 
 }
 
 template <int NPT>
+static oem_status launch_lean_t5(const PathParams& P, const LeanArgs& A, int nU, size_t smem, cudaStream_t st) {
+  auto kern = fit_lean_kernel<NPT, 2, 16, 32, 2>;
+  OEM_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3((unsigned)(nU * A.C));
+  cfg.blockDim = dim3(PT);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = (unsigned)A.C;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  OEM_CUDA_TRY(cudaLaunchKernelEx(&cfg, kern, P, A));
+  return OEM_OK;
+}
+
+template <int NPT>
 static oem_status launch_lean_v(const PathParams& P, const LeanArgs& A, int nU, const LeanLayout& lo, cudaStream_t st) {
   if (lo.variant == 0) return launch_lean_t<NPT, 1, 8, 8>(P, A, nU, lo.smem, st);
   if (lo.variant == 1) return launch_lean_t<NPT, 2, 16, 8>(P, A, nU, lo.smem, st);
   if (lo.variant == 3) return launch_lean_t<NPT, 1, 8, 16>(P, A, nU, lo.smem, st);
   if (lo.variant == 4) return launch_lean_t<NPT, 1, 16, 16>(P, A, nU, lo.smem, st);
+  if (lo.variant == 5) return launch_lean_t5<NPT>(P, A, nU, lo.smem, st);
   return launch_lean_t<NPT, 2, 16, 16>(P, A, nU, lo.smem, st);
 }
 
