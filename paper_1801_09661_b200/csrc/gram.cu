@@ -213,14 +213,26 @@ __device__ __forceinline__ void weighted_rows(const GramParams& P, const Cons& c
     double* ys = pa + P.ys_off;
     double* ws = ys + BK * P.ystride;
     const double* xr = pa + k * ld;
-    double e0 = 0.0, e1 = 0.0;
-    int j = sub;
-    for (; j + LPR < P.p; j += 2 * LPR) {
-      e0 = fma(xr[j], cs.beta_s[j], e0);
-      e1 = fma(xr[j + LPR], cs.beta_s[j + LPR], e1);
+    // eta = x_i^T beta: lane `sub` takes the column pairs 2 sub + 2 LPR t (16-byte loads; the
+    // row pitch and beta_s are even and zero beyond p), four pairs in flight per step
+    double e0 = 0.0, e1 = 0.0, e2 = 0.0, e3 = 0.0;
+    const double2* x2 = reinterpret_cast<const double2*>(xr);
+    const double2* b2 = reinterpret_cast<const double2*>(cs.beta_s);
+    const int np2 = (P.p + 1) >> 1;  // column pairs covering p (beta_s[p] == 0)
+    int t = sub;
+    for (; t + 3 * LPR < np2; t += 4 * LPR) {
+      const double2 xa = x2[t], xb = x2[t + LPR], xc = x2[t + 2 * LPR], xd = x2[t + 3 * LPR];
+      const double2 ba = b2[t], bb = b2[t + LPR], bc = b2[t + 2 * LPR], bd = b2[t + 3 * LPR];
+      e0 = fma(xa.x, ba.x, fma(xa.y, ba.y, e0));
+      e1 = fma(xb.x, bb.x, fma(xb.y, bb.y, e1));
+      e2 = fma(xc.x, bc.x, fma(xc.y, bc.y, e2));
+      e3 = fma(xd.x, bd.x, fma(xd.y, bd.y, e3));
     }
-    if (j < P.p) e0 = fma(xr[j], cs.beta_s[j], e0);
-    double e = e0 + e1;
+    for (; t < np2; t += LPR) {
+      const double2 xa = x2[t], ba = b2[t];
+      e0 = fma(xa.x, ba.x, fma(xa.y, ba.y, e0));
+    }
+    double e = (e0 + e1) + (e2 + e3);
 #pragma unroll
     for (int o = 1; o < LPR; o <<= 1) e += __shfl_xor_sync(0xffffffffu, e, o);
     const int64_t row = cs.r0 + (int64_t)s * BK + k;

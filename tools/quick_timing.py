@@ -28,6 +28,7 @@ def main():
     ap.add_argument("--n", type=int, default=0)
     ap.add_argument("--reps", type=int, default=3)
     ap.add_argument("--nofit", action="store_true")
+    ap.add_argument("--plain", action="store_true", help="plain Gram pass even for folds / logistic workloads")
     a = ap.parse_args()
     cfg = CONFIGS[a.cfg]
     if a.n:
@@ -45,7 +46,10 @@ def main():
     for r in range(a.reps + 1):
         e0, e1, e2 = ev(), ev(), ev()
         e0.record()
-        if cfg.folds:
+        if a.plain:
+            G, c, yy, nn = oem_gram(ctx, Xd, yd)
+            cnt = [nn]
+        elif cfg.folds:
             G, c, yy, cnt = oem_gram_folds(ctx, Xd, yd, cfg.folds)
         elif cfg.logistic:
             G, c, sc = oem_gram_weighted(ctx, Xd, yd, torch.zeros(p, dtype=torch.float64, device="cuda"))
@@ -54,7 +58,7 @@ def main():
             G, c, yy, nn = oem_gram(ctx, Xd, yd)
             cnt = [nn]
         e1.record()
-        if not a.nofit and not cfg.logistic:
+        if not a.nofit and not cfg.logistic and not a.plain:
             fit = oem_fit_path(ctx, G, c, cnt, cfg.penalties, nlambda=cfg.nlambda, fold_mode=bool(cfg.folds),
                                group=grp, ngroups=(p // cfg.group_size) if grp is not None else 0)
         e2.record()
@@ -69,7 +73,7 @@ def main():
         print(json.dumps(out))
         return
     out["gram_tflops"] = flops / (min(out["gram_ms"]) * 1e-3) / 1e12
-    if not a.nofit and not cfg.logistic:
+    if not a.nofit and not cfg.logistic and not a.plain:
         out["iters_total"] = int(fit.iters.sum())
         out["iters_max_unit"] = int(fit.iters.sum(-1).max())
         out["us_per_iter"] = min(out["fit_ms"]) * 1e3 / max(1, out["iters_max_unit"])
