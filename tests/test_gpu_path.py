@@ -273,3 +273,29 @@ def test_mixed_group_and_coordinate_penalties(ctx, p, solver, monkeypatch):
         B, it, cv = orc.oem_path(Go / n, co / n, d, fam, lg, gamma, alpha, group=g,
                                  ngroups=p // 10 if g is not None else 0)
         assert np.max(np.abs(fit.beta[0, q].cpu().numpy() - B)) <= TOL_BETA, fam
+
+
+def test_many_penalties_and_wide_p_fallbacks(ctx):
+    """Shapes outside the lean / grid solvers' templates take the fallback kernels: six penalties
+    at once (NPT = 8) and p = 1100 (> 1024); both against the oracle."""
+    from paper_1801_09661_b200 import oem_fit_path, oem_gram
+    spec = CONFIGS["cfg2"].spec.replace(n=3000, p=40, nnz=6)
+    bt = dg.beta(spec)
+    X, y = dg.rows_host(spec, bt)
+    G, c, yy, n = oem_gram(ctx, torch.from_numpy(X).cuda(), torch.from_numpy(y).cuda())
+    Go, co, _ = orc.gram(X, y)
+    pens = [("lasso", 0.0, 1.0), ("enet", 0.0, 0.3), ("mcp", 3.0, 1.0), ("scad", 3.7, 1.0),
+            ("enet", 0.0, 0.8), ("mcp", 5.0, 1.0)]
+    fit = oem_fit_path(ctx, G, c, [n], pens, nlambda=15)
+    d = float(fit.d[0])
+    for q, (fam, gamma, alpha) in enumerate(pens):
+        B, it, cv = orc.oem_path(Go / n, co / n, d, fam, fit.lam[0, q].cpu().numpy(), gamma, alpha)
+        assert np.max(np.abs(fit.beta[0, q].cpu().numpy() - B)) <= TOL_BETA, fam
+    spec = CONFIGS["cfg4"].spec.replace(n=2500, p=1100, nnz=3)
+    bt = dg.beta(spec)
+    X, y = dg.rows_host(spec, bt)
+    G, c, yy, n = oem_gram(ctx, torch.from_numpy(X).cuda(), torch.from_numpy(y).cuda())
+    Go, co, _ = orc.gram(X, y)
+    fit = oem_fit_path(ctx, G, c, [n], [("lasso", 0.0, 1.0)], nlambda=6)
+    B, it, cv = orc.oem_path(Go / n, co / n, float(fit.d[0]), "lasso", fit.lam[0, 0].cpu().numpy())
+    assert np.max(np.abs(fit.beta[0, 0].cpu().numpy() - B)) <= TOL_BETA
