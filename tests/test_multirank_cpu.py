@@ -46,8 +46,16 @@ def worker(rank, world, port, n, p, K, q):
         assert list(cnt) == fold_counts(r1 - r0, r0, K)
         tf = torch.from_numpy(np.concatenate([Gk.ravel(), ck.ravel(), yyk, cnt.astype(float)]))
         dist.all_reduce(tf, op=dist.ReduceOp.SUM)
+        # weighted Gram and logistic gradient (a4 / f1): per-rank raw sums combine to the
+        # single-process ones (beta replicated on every rank)
+        y01 = (ys > 0).astype(float)
+        beta = np.linspace(-0.3, 0.2, p)
+        Gw, cw, sw = orc.gram_weighted(Xs, y01, beta, nthreads=1)
+        g, ll = orc.logit_grad(Xs, y01, beta)
+        tw = torch.from_numpy(np.concatenate([Gw.ravel(), cw, sw, g, [ll]]))
+        dist.all_reduce(tw, op=dist.ReduceOp.SUM)
         if rank == 0:
-            q.put((t.numpy().copy(), tf.numpy().copy()))
+            q.put((t.numpy().copy(), tf.numpy().copy(), tw.numpy().copy()))
     finally:
         dist.destroy_process_group()
 
@@ -61,7 +69,7 @@ def test_sharded_combine_equals_single_process(world):
     procs = [ctx.Process(target=worker, args=(r, world, port, n, p, K, q)) for r in range(world)]
     for pr in procs:
         pr.start()
-    t, tf = q.get(timeout=120)
+    t, tf, tw = q.get(timeout=120)
     for pr in procs:
         pr.join(timeout=120)
         assert pr.exitcode == 0
@@ -78,6 +86,13 @@ def test_sharded_combine_equals_single_process(world):
     off += K * p
     assert np.array_equal(tf[off: off + K], yyk)
     assert np.array_equal(tf[off + K:], cnt.astype(float))
+    # combined weighted statistics equal the single-process ones (up to the order of the sums)
+    y01 = (y > 0).astype(float)
+    beta = np.linspace(-0.3, 0.2, p)
+    Gw, cw, sw = orc.gram_weighted(X, y01, beta)
+    g, ll = orc.logit_grad(X, y01, beta)
+    ref = np.concatenate([Gw.ravel(), cw, sw, g, [ll]])
+    assert np.allclose(tw, ref, rtol=1e-12, atol=1e-9)
 
 
 def test_row_range_and_fold_counts():
