@@ -1,4 +1,4 @@
-# round measurement: tests, smoke, bench lines for every workload, launch list and ncu of the top kernel
+# round measurement: tests, smoke, bench lines for every workload, launch lists, reference arm
 set -x
 mkdir -p gpurun_out
 nvidia-smi --query-gpu=name,clocks.sm,clocks.max.sm,memory.total --format=csv
@@ -8,7 +8,5 @@ timeout 900 python -m pytest tests -m gpu -x -q > gpurun_out/gpu_tests.log 2>&1;
 timeout 900 python bench.py > gpurun_out/bench_cfg4.log 2>&1; echo bench=$?
 for w in cfg2 cfg3 cfg5; do timeout 600 python bench.py --workload $w --no-cpu-baseline --e2e-steps 1 > gpurun_out/bench_$w.log 2>&1; echo bench_$w=$?; done
 timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv --log-file gpurun_out/launches_cfg4.csv python bench.py --steps 2 --warmup 3 --e2e-steps 0 --no-cpu-baseline > gpurun_out/ncu_launch.log 2>&1; echo ncu1=$?
-timeout 900 ncu --set full --clock-control none --import-source on -k regex:gram_kernel -c 1 -o gpurun_out/ncu_gram_cfg4 -f python bench.py --warmup 0 --steps 1 --e2e-steps 0 --no-cpu-baseline > gpurun_out/ncu_full_cfg4.log 2>&1; echo ncufull=$?
-timeout 900 ncu --set full --clock-control none --import-source on -k regex:gram_kernel -c 1 -o gpurun_out/ncu_gram_cfg5 -f python bench.py --workload cfg5 --warmup 0 --steps 1 --e2e-steps 0 --no-cpu-baseline > gpurun_out/ncu_full_cfg5.log 2>&1; echo ncufull5=$?
-timeout 900 ncu --set full --clock-control none --import-source on -k regex:gram_kernel -c 1 -o gpurun_out/ncu_gram_cfg2 -f python bench.py --workload cfg2 --warmup 0 --steps 1 --e2e-steps 0 --no-cpu-baseline > gpurun_out/ncu_full_cfg2.log 2>&1; echo ncufull2=$?
 timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -c 3000 --csv --log-file gpurun_out/launches_cfg5.csv python bench.py --workload cfg5 --steps 1 --warmup 3 --e2e-steps 0 --no-cpu-baseline > gpurun_out/ncu_launch5.log 2>&1; echo ncu5=$?
+timeout 900 python bench.py --impl reference --steps 3 --warmup 1 > gpurun_out/bench_reference.log 2>&1; echo ref=$?
