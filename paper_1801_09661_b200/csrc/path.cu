@@ -1509,14 +1509,36 @@ __global__ void __launch_bounds__(PT, 1) fit_glob_kernel(const PathParams P, con
       s_bits = 0u;
     }
     unit_sync();
-    // the unit's new vector and flags, from L2
-    for (int q = 0; q < nP; ++q)
-      for (int k = tid; k < p; k += PT) {
-        const int vi = vix<NPT>(q, k, pvl);
-        vn[vi] = __ldcg(&gn[vi]);
+    // the unit's new vector and flags, from L2: every load issued before any is used (one L2
+    // round trip); 16-byte loads of penalty pairs (p <= 1024 = 2 PT in this kernel)
+    if (NPT == 1) {
+      double tv[2];
+#pragma unroll
+      for (int u = 0; u < 2; ++u) {
+        const int k = tid + u * PT;
+        tv[u] = k < p ? __ldcg(&gn[k]) : 0.0;
       }
+#pragma unroll
+      for (int u = 0; u < 2; ++u)
+        if (tid + u * PT < p) vn[tid + u * PT] = tv[u];
+    } else {
+      double2 tv[NV / 2 > 0 ? NV / 2 : 1][2];
+#pragma unroll
+      for (int h = 0; h < NV / 2; ++h)
+#pragma unroll
+        for (int u = 0; u < 2; ++u) {
+          const int k = tid + u * PT;
+          tv[h][u] = k < p ? __ldcg(reinterpret_cast<const double2*>(gn + h * 2 * pvl) + k) : make_double2(0.0, 0.0);
+        }
+#pragma unroll
+      for (int h = 0; h < NV / 2; ++h)
+#pragma unroll
+        for (int u = 0; u < 2; ++u)
+          if (tid + u * PT < p) reinterpret_cast<double2*>(vn + h * 2 * pvl)[tid + u * PT] = tv[h][u];
+    }
     if (warp == 0) {
       uint32_t w = 0;
+#pragma unroll 5
       for (int c = lane; c < C; c += 32) w |= (uint32_t)__ldcg(&gflag[(t & 1) * spar + c]);
       w = __reduce_or_sync(0xffffffffu, w);
       if (lane == 0) s_all = w;
