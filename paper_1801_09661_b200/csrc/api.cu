@@ -3,6 +3,7 @@
 #include <nccl.h>
 
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 
@@ -13,6 +14,13 @@ namespace oem {
 
 static thread_local std::string g_last_error;
 void set_error(const std::string& msg) { g_last_error = msg; }
+bool poison_enabled() {
+  static const bool on = [] {
+    const char* e = std::getenv("OEM_POISON");
+    return e && e[0] == '1';
+  }();
+  return on;
+}
 
 oem_status allreduce_sum(oem_ctx* ctx, double* buf, size_t count, cudaStream_t st) {
   if (ctx->nranks <= 1 || count == 0) return OEM_OK;

@@ -17,17 +17,24 @@ namespace oem {
 void set_error(const std::string& msg);
 
 // Grown-on-demand device scratch owned by the context (freed in oem_ctx_destroy).
+// With OEM_POISON=1 in the environment (a test mode) every ensure() fills the requested bytes
+// with 0xFF (a NaN pattern for doubles), so a kernel that reads scratch it did not write shows up
+// as a non-finite result instead of silently reusing a previous call's data.
+bool poison_enabled();
 struct DevBuf {
   void* ptr = nullptr;
   size_t bytes = 0;
   cudaError_t ensure(size_t need) {
-    if (need <= bytes) return cudaSuccess;
-    if (ptr) cudaFree(ptr);
-    ptr = nullptr;
-    bytes = 0;
-    cudaError_t e = cudaMalloc(&ptr, need);
-    if (e == cudaSuccess) bytes = need;
-    return e;
+    if (need > bytes) {
+      if (ptr) cudaFree(ptr);
+      ptr = nullptr;
+      bytes = 0;
+      cudaError_t e = cudaMalloc(&ptr, need);
+      if (e != cudaSuccess) return e;
+      bytes = need;
+    }
+    if (poison_enabled() && need > 0) return cudaMemset(ptr, 0xFF, need);
+    return cudaSuccess;
   }
   template <typename T> T* as() const { return static_cast<T*>(ptr); }
   void release() {

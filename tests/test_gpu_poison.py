@@ -1,0 +1,23 @@
+"""Scratch-poisoning run (OEM_POISON=1: every workspace the library hands a kernel is first filled
+with a NaN pattern): the cfg1 fit, a fold-mode CV fit and the logistic path must still match the
+oracle, i.e. no kernel reads scratch it did not write in the same call."""
+import os
+import subprocess
+import sys
+
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def test_poisoned_workspace_subprocess():
+    env = dict(os.environ, OEM_POISON="1")
+    cmd = [sys.executable, "-m", "pytest", "-q", "-m", "gpu", "-p", "no:cacheprovider",
+           os.path.join(ROOT, "tests", "test_gpu_path.py") + "::test_cfg1_lasso_path",
+           os.path.join(ROOT, "tests", "test_gpu_path.py") + "::test_cfg3_fold_mode",
+           os.path.join(ROOT, "tests", "test_gpu_cv.py"),
+           os.path.join(ROOT, "tests", "test_gpu_logistic.py")]
+    r = subprocess.run(cmd, env=env, cwd=ROOT, capture_output=True, text=True, timeout=900)
+    assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-2000:]
