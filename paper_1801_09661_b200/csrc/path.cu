@@ -776,6 +776,38 @@ __device__ __forceinline__ int lean_vidx(int tl) {
   return v;
 }
 __host__ __device__ constexpr int pow2ceil(int v) { return v <= 1 ? 1 : 2 * pow2ceil((v + 1) / 2); }
+// General form (VP may exceed T): halving over the offsets T/2 .. 1 while more than one value is
+// left, then a butterfly if VP < T. Lane tl ends with CNT = max(1, VP/T) full sums in a[0..CNT),
+// for the value indices lean_base<VP,T>(tl) + s.
+template <int VP, int T>
+__device__ __forceinline__ void lean_rs_gen(double (&a)[VP], int tl) {
+#pragma unroll
+  for (int k = 0; (T >> (k + 1)) >= 1; ++k) {
+    const int o = T >> (k + 1), cnt = VP >> k;
+    if (cnt > 1) {
+      const int half = cnt / 2;
+      const bool up = (tl & o) != 0;
+#pragma unroll
+      for (int i = 0; i < half; ++i) {
+        const double send = up ? a[i] : a[i + half];
+        const double keep = up ? a[i + half] : a[i];
+        a[i] = keep + __shfl_xor_sync(0xffffffffu, send, o);
+      }
+    } else {
+      a[0] += __shfl_xor_sync(0xffffffffu, a[0], o);
+    }
+  }
+}
+template <int VP, int T>
+__device__ __forceinline__ int lean_base(int tl) {
+  int v = 0;
+#pragma unroll
+  for (int k = 0; (T >> (k + 1)) >= 1; ++k) {
+    const int o = T >> (k + 1), cnt = VP >> k;
+    if (cnt > 1 && (tl & o)) v += cnt / 2;
+  }
+  return v;
+}
 
 // beta vectors in shared memory: penalties in pairs, [pair][k][2], so one 16-byte load per lane
 // fetches two penalties and T consecutive lanes read T*16 contiguous bytes (conflict free)
@@ -787,12 +819,13 @@ __device__ __forceinline__ int vix(int q, int k, int pvl) {
 // RS > 0: each thread row group also owns RS rows kept in SHARED memory (for units whose rows do
 // not fit the register file, e.g. cfg3's eleven p = 500 Grams in clusters of 8). Thread (rg, tl)
 // owns local rows rg*RT + i, i < RT = R + RS: i < R from registers, i >= R from shared memory.
-template <int NPT, int R, int KC, int T, int RS = 0>
-__global__ void __launch_bounds__(PT, 1) fit_lean_kernel(const PathParams P, const LeanArgs A) {
+template <int NPT, int R, int KC, int T, int RS = 0, int NTH = PT>
+__global__ void __launch_bounds__(NTH, 1) fit_lean_kernel(const PathParams P, const LeanArgs A) {
   constexpr int RT = R + RS;
-  constexpr int RG = PT / T, V = RT * NPT, VP = pow2ceil(V), NW = PT / 32;
+  constexpr int RG = NTH / T, V = RT * NPT, VP = pow2ceil(V), NW = NTH / 32;
   constexpr int NV = NPT == 1 ? 1 : 2 * ((NPT + 1) / 2);  // doubles per k in the vector layout
-  static_assert(VP <= T && (T & (T - 1)) == 0 && T <= 32, "lean layout");
+  static_assert((T & (T - 1)) == 0 && T <= 32 && (VP <= T || VP % T == 0), "lean layout");
+  constexpr int CNT = VP >= T ? VP / T : 1;  // (row, penalty) sums each lane owns after the reduce-scatter
   extern __shared__ __align__(16) double sm[];
   __shared__ int s_fam[NPT], s_skip[NPT];
   __shared__ double s_gam[NPT], s_alp[NPT], s_lmax[NPT];
@@ -823,13 +856,13 @@ __global__ void __launch_bounds__(PT, 1) fit_lean_kernel(const PathParams P, con
   const bool grp = P.g_of != nullptr;
   const int g0 = (grp && nr > 0) ? P.g_of[j0] : 0;
   const int ng_loc = (grp && nr > 0) ? P.g_of[j1 - 1] + 1 - g0 : 0;
-  for (int gg = tid; gg < ng_loc; gg += PT) {
+  for (int gg = tid; gg < ng_loc; gg += NTH) {
     gw_s[gg] = P.g_w[g0 + gg];
     ga_s[gg] = P.g_start[g0 + gg] - j0;
     gb_s[gg] = P.g_end[g0 + gg] - j0;
   }
-  for (int k = tid; k < 2 * vstride; k += PT) vec[k] = 0.0;
-  for (int k = tid; k < 2 * C * NW; k += PT) slots[k] = 0.0;
+  for (int k = tid; k < 2 * vstride; k += NTH) vec[k] = 0.0;
+  for (int k = tid; k < 2 * C * NW; k += NTH) slots[k] = 0.0;
   if (tid < 3) F[tid] = 0u;
   // this thread's tile of G (rows rg*RT + i, columns tl + m*T): i < R in registers for the whole
   // launch, i >= R in shared memory (row rg*RS + i - R of gsm)
@@ -853,13 +886,21 @@ __global__ void __launch_bounds__(PT, 1) fit_lean_kernel(const PathParams P, con
     return i < R ? g[i < R ? i : 0][m] : gsm[(size_t)(rg * RS + i - R) * pvl + tl + m * T];
   };
   // the (row, penalty) sum this lane owns after the reduce-scatter
-  const int vidx = lean_vidx<VP, T>(tl);
-  const int mi = vidx / NPT, mq = vidx % NPT, mr = rg * RT + mi;
-  const bool owner = (tl & (T / VP - 1)) == 0;
-  const bool act = owner && vidx < V && mr < nr;
-  const int mj = j0 + mr;
-  const double c_my = act ? cu[mj] : 0.0;
-  const double w_my = (act && P.var_w) ? P.var_w[mj] : 1.0;
+  const int vbase = lean_base<VP, T>(tl);
+  const bool owner = VP >= T || (tl & (T / VP - 1)) == 0;
+  int mq[CNT], mr[CNT], mj[CNT];
+  bool act[CNT];
+  double c_my[CNT], w_my[CNT];
+#pragma unroll
+  for (int s2 = 0; s2 < CNT; ++s2) {
+    const int vidx = vbase + s2;
+    mq[s2] = vidx % NPT;
+    mr[s2] = rg * RT + vidx / NPT;
+    act[s2] = owner && vidx < V && mr[s2] < nr;
+    mj[s2] = j0 + mr[s2];
+    c_my[s2] = act[s2] ? cu[mj[s2]] : 0.0;
+    w_my[s2] = (act[s2] && P.var_w) ? P.var_w[mj[s2]] : 1.0;
+  }
   // power iteration: an RT-value reduce-scatter; the lane owns row rg*RT + vidx1
   constexpr int RP = pow2ceil(RT);
   const int vidx1 = lean_vidx<RP, T>(tl);
@@ -886,7 +927,7 @@ __global__ void __launch_bounds__(PT, 1) fit_lean_kernel(const PathParams P, con
     if (lane == 0)
       for (int rr = 0; rr < C; ++rr) st_cl_f64(&slots[NW * C + rank * NW + warp], rr, gm);  // parity-1 slots
     const double v0 = 1.0 / sqrt((double)p);
-    for (int k = tid; k < p; k += PT) vec[vix<NPT>(0, k, pvl)] = v0;  // buffer 0, vector 0
+    for (int k = tid; k < p; k += NTH) vec[vix<NPT>(0, k, pvl)] = v0;  // buffer 0, vector 0
     cluster_sync_all();
     double gersh = 0.0;
     for (int e = 0; e < C * NW; ++e) gersh = fmax(gersh, slots[NW * C + e]);
@@ -941,7 +982,7 @@ __global__ void __launch_bounds__(PT, 1) fit_lean_kernel(const PathParams P, con
     d = gersh < dd ? gersh : dd;
     if (rank == 0 && tid == 0) A.d_out[unit] = d;
     cluster_sync_all();  // all reads of vec / slots are done before the path reuses them
-    for (int k = tid; k < 2 * vstride; k += PT) vec[k] = 0.0;
+    for (int k = tid; k < 2 * vstride; k += NTH) vec[k] = 0.0;
   } else {
     d = P.d[unit];
   }
@@ -993,7 +1034,7 @@ __global__ void __launch_bounds__(PT, 1) fit_lean_kernel(const PathParams P, con
   }
   // warm or cold start (permuted order) into buffer 0
   if (P.beta_init)
-    for (int e = tid; e < nP * p; e += PT) {
+    for (int e = tid; e < nP * p; e += NTH) {
       const int q = e / p, k = e % p;
       vec[vix<NPT>(q, k, pvl)] = P.beta_init[((size_t)unit * nP + q) * p + P.perm[k]];
     }
@@ -1004,7 +1045,7 @@ __global__ void __launch_bounds__(PT, 1) fit_lean_kernel(const PathParams P, con
     return s_lmax[q] * exp(((double)l / (double)(L - 1)) * log(P.lmin_ratio));  // R#15
   };
   if (rank == 0)
-    for (int e = tid; e < nP * L; e += PT) {
+    for (int e = tid; e < nP * L; e += NTH) {
       const int q = e / L, l = e % L;
       P.lam_out[((size_t)unit * nP + q) * L + l] = lam_at(q, l);
     }
@@ -1016,8 +1057,14 @@ __global__ void __launch_bounds__(PT, 1) fit_lean_kernel(const PathParams P, con
     itc[q] = 0;
     lam[q] = s_skip[q] ? 0.0 : lam_at(q, 0);
   }
-  const int fam_my = s_fam[mq];
-  const double gam_my = s_gam[mq], alp_my = s_alp[mq];
+  int fam_my[CNT];
+  double gam_my[CNT], alp_my[CNT];
+#pragma unroll
+  for (int s2 = 0; s2 < CNT; ++s2) {
+    fam_my[s2] = s_fam[mq[s2]];
+    gam_my[s2] = s_gam[mq[s2]];
+    alp_my[s2] = s_alp[mq[s2]];
+  }
   cluster_sync_all();  // every CTA's buffers are initialised before the first remote store
 
   // ======================================================= a9: OEM iterations
@@ -1059,24 +1106,26 @@ __global__ void __launch_bounds__(PT, 1) fit_lean_kernel(const PathParams P, con
         }
       }
     }
-    const double s = lean_rs<VP, T>(a, tl);
+    lean_rs_gen<VP, T>(a, tl);
     uint32_t bits = 0;
-    if (act && ((qmask >> mq) & 1u)) {
-      const int vi = vix<NPT>(mq, mj, pvl);
+#pragma unroll
+    for (int s2 = 0; s2 < CNT; ++s2) {
+      if (!(act[s2] && ((qmask >> mq[s2]) & 1u))) continue;
+      const int vi = vix<NPT>(mq[s2], mj[s2], pvl);
       const double bj = vc[vi];
-      const double u = c_my + d * bj - s;
+      const double u = c_my[s2] + d * bj - a[s2];
       if (!isfinite(u)) bits |= 0x80000000u;
-      if (!grp || fam_my < OEM_GRP_LASSO) {  // coordinate-wise family (also when mixed with group ones)
+      if (!grp || fam_my[s2] < OEM_GRP_LASSO) {  // coordinate-wise family (also when mixed with group ones)
         double lq = 0.0;
 #pragma unroll
         for (int q = 0; q < NPT; ++q)
-          if (q == mq) lq = lam[q];
-        const double nb = th_coord(fam_my, u, w_my * lq, gam_my, alp_my, d);
-        if (!(fabs(nb - bj) <= P.tol)) bits |= 1u << mq;
+          if (q == mq[s2]) lq = lam[q];
+        const double nb = th_coord(fam_my[s2], u, w_my[s2] * lq, gam_my[s2], alp_my[s2], d);
+        if (!(fabs(nb - bj) <= P.tol)) bits |= 1u << mq[s2];
         if (C == 1) vn[vi] = nb;
         else for (int rr = 0; rr < C; ++rr) st_cl_f64(&vn[vi], rr, nb);
       } else {
-        uv[mq * rows + mr] = u;
+        uv[mq[s2] * rows + mr[s2]] = u;
       }
     }
     if (grp) {
@@ -1118,7 +1167,7 @@ __global__ void __launch_bounds__(PT, 1) fit_lean_kernel(const PathParams P, con
       if (conv || it >= P.maxit) {
         const int l = lidx[q];
         double* out = P.beta_out + (((size_t)unit * nP + q) * L + l) * p;
-        for (int r = tid; r < nr; r += PT) out[P.perm[j0 + r]] = vn[vix<NPT>(q, j0 + r, pvl)];
+        for (int r = tid; r < nr; r += NTH) out[P.perm[j0 + r]] = vn[vix<NPT>(q, j0 + r, pvl)];
         if (rank == 0 && tid == 0) {
           P.it_out[((size_t)unit * nP + q) * L + l] = it;
           P.cv_out[((size_t)unit * nP + q) * L + l] = conv ? 1 : 0;
@@ -2041,15 +2090,17 @@ struct LeanLayout {
 static bool make_lean_layout(int p, int NPT, const std::vector<int>& gstart, LeanLayout& lo) {
   // variants: rows per CTA = R * 512 / T, columns = KC * T
   // variant 5: 32 register rows + 32 shared-memory rows per CTA (p <= 512, clusters of <= 8)
-  static const int R_[6] = {1, 2, 2, 1, 1, 2}, KC_[6] = {8, 16, 16, 8, 16, 16}, T_[6] = {8, 8, 16, 16, 16, 32},
-                   RS_[6] = {0, 0, 0, 0, 0, 2};
+  // variant 6: 256 threads (8 warps, 4 rows per thread): less per-iteration overhead at p <= 128
+  static const int R_[7] = {1, 2, 2, 1, 1, 2, 4}, KC_[7] = {8, 16, 16, 8, 16, 16, 16},
+                   T_[7] = {8, 8, 16, 16, 16, 32, 8}, RS_[7] = {0, 0, 0, 0, 0, 2, 0},
+                   NTH_[7] = {PT, PT, PT, PT, PT, PT, 256};
   int v = p <= 64 ? 0 : p <= 128 ? 1 : p <= 256 ? 2 : p <= 512 ? 5 : -1;
   if (const char* ev = std::getenv("OEM_LEAN_VARIANT")) {  // developer override (timing studies)
     const int f = std::atoi(ev);
-    if (f >= 0 && f < 6 && KC_[f] * T_[f] >= p) v = f;
+    if (f >= 0 && f < 7 && KC_[f] * T_[f] >= p) v = f;
   }
   if (v < 0 || NPT > 4) return false;
-  const int rows = (R_[v] + RS_[v]) * (PT / T_[v]);
+  const int rows = (R_[v] + RS_[v]) * (NTH_[v] / T_[v]);
   // contiguous row blocks of <= rows rows, cut only at group starts (greedy packing)
   std::vector<int> cuts{0};
   if (gstart.empty()) {
@@ -2079,7 +2130,7 @@ static bool make_lean_layout(int p, int NPT, const std::vector<int>& gstart, Lea
   lo.pvl = KC_[v] * T_[v];
   lo.cuts = cuts;
   const int NV = NPT == 1 ? 1 : 2 * ((NPT + 1) / 2);
-  lo.smem = ((size_t)2 * NV * lo.pvl + (size_t)RS_[v] * (PT / T_[v]) * lo.pvl + (size_t)2 * C * (PT / 32) +
+  lo.smem = ((size_t)2 * NV * lo.pvl + (size_t)RS_[v] * (NTH_[v] / T_[v]) * lo.pvl + (size_t)2 * C * (NTH_[v] / 32) +
              (size_t)NPT * rows + rows) * 8 +
             (size_t)2 * rows * 4 + 16;
   return true;
@@ -2126,12 +2177,33 @@ static oem_status launch_lean_t5(const PathParams& P, const LeanArgs& A, int nU,
 }
 
 template <int NPT>
+static oem_status launch_lean_t6(const PathParams& P, const LeanArgs& A, int nU, size_t smem, cudaStream_t st) {
+  auto kern = fit_lean_kernel<NPT, 4, 16, 8, 0, 256>;
+  OEM_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3((unsigned)(nU * A.C));
+  cfg.blockDim = dim3(256);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = (unsigned)A.C;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  OEM_CUDA_TRY(cudaLaunchKernelEx(&cfg, kern, P, A));
+  return OEM_OK;
+}
+
+template <int NPT>
 static oem_status launch_lean_v(const PathParams& P, const LeanArgs& A, int nU, const LeanLayout& lo, cudaStream_t st) {
   if (lo.variant == 0) return launch_lean_t<NPT, 1, 8, 8>(P, A, nU, lo.smem, st);
   if (lo.variant == 1) return launch_lean_t<NPT, 2, 16, 8>(P, A, nU, lo.smem, st);
   if (lo.variant == 3) return launch_lean_t<NPT, 1, 8, 16>(P, A, nU, lo.smem, st);
   if (lo.variant == 4) return launch_lean_t<NPT, 1, 16, 16>(P, A, nU, lo.smem, st);
   if (lo.variant == 5) return launch_lean_t5<NPT>(P, A, nU, lo.smem, st);
+  if (lo.variant == 6) return launch_lean_t6<NPT>(P, A, nU, lo.smem, st);
   return launch_lean_t<NPT, 2, 16, 16>(P, A, nU, lo.smem, st);
 }
 
