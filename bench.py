@@ -86,9 +86,22 @@ class Clocks:
 
 
 # ------------------------------------------------------------------ CPU oracle baseline
-def cpu_baseline(cfg, budget_s=15.0):
+def cpu_model():
+    try:
+        for line in subprocess.run(["lscpu"], capture_output=True, text=True, timeout=10).stdout.splitlines():
+            if line.lower().startswith("model name"):
+                return line.split(":", 1)[1].strip()
+    except Exception:
+        pass
+    return None
+
+
+def cpu_baseline(cfg, budget_s=15.0, path_inputs=None):
     """The oracle's Gram (oracle/oracle.c, compensated fp64, all host cores) on a bounded row
-    sample of the workload; rows come from the host generator (untimed)."""
+    sample of the workload; rows come from the host generator (untimed). With path_inputs (the
+    full-data raw Gram, X^T y, n, d and grid from the GPU step, linear non-fold workloads) the
+    oracle's path solve (O6, single thread) is timed on the same problem, when its estimated cost
+    fits the budget, and an oracle fit-seconds estimate is reported."""
     import oracle as orc
     cores = os.cpu_count() or 1
     bt = dg.beta(cfg.spec, cfg.explicit_beta)
@@ -103,9 +116,25 @@ def cpu_baseline(cfg, budget_s=15.0):
     t0 = time.perf_counter()
     orc.gram(X, y, nthreads=cores)
     dt = time.perf_counter() - t0
-    return {"value": gram_flops(rows, cfg.p) / dt / 1e12, "unit": "TFLOP/s", "cores": cores, "kind": "oracle",
-            "sample": f"oracle Gram (compensated fp64, {cores} threads) over rows 0..{rows} of {cfg.name} "
-                      f"(n={cfg.n}, p={cfg.p}), {dt:.2f} s"}
+    out = {"value": gram_flops(rows, cfg.p) / dt / 1e12, "unit": "TFLOP/s", "cores": cores, "kind": "oracle",
+           "cpu_model": cpu_model(),
+           "sample": f"oracle Gram (compensated fp64, {cores} threads) over rows 0..{rows} of {cfg.name} "
+                     f"(n={cfg.n}, p={cfg.p}), {dt:.2f} s"}
+    if path_inputs is not None:
+        G, c, n, d, lams, grp, ngroups, est = path_inputs
+        if est <= 4 * budget_s:
+            t0 = time.perf_counter()
+            for q, (fam, gamma, alpha) in enumerate(cfg.penalties):
+                g = grp if fam.startswith("grp") or fam == "sgl" else None
+                orc.oem_path(G / n, c / n, d, fam, lams[q], gamma, alpha, group=g,
+                             ngroups=ngroups if g is not None else 0)
+            tp = time.perf_counter() - t0
+            gram_s = dt * cfg.n / rows
+            out["path_seconds"] = tp
+            out["fit_seconds_est"] = gram_s + tp
+            out["sample"] += f"; oracle path solve (1 thread) of the full problem {tp:.1f} s; fit estimate = " \
+                             f"Gram extrapolated to n + path"
+    return out
 
 
 # ------------------------------------------------------------------ reference arm (the oracle)
@@ -168,6 +197,9 @@ def main():
         raise SystemExit(f"--gpus {args.gpus} but WORLD_SIZE={world}")
     torch.cuda.set_device(local)
     if world > 1:
+        # a fixed NCCL algorithm / protocol: bitwise-reproducible combines
+        os.environ.setdefault("NCCL_ALGO", "Ring")
+        os.environ.setdefault("NCCL_PROTO", "Simple")
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
         obj = [oem.oem_nccl_unique_id() if rank == 0 else None]
         dist.broadcast_object_list(obj, src=0)
@@ -343,7 +375,14 @@ def main():
     if rank == 0:
         cpu = None
         if world == 1 and not args.no_cpu_baseline:
-            cpu = cpu_baseline(cfg)
+            pin = None
+            if not cfg.logistic and not cfg.folds:
+                Gf, cf, _, nf = oem_gram(ctx, Xd, yd)
+                iters = int(res.iters.sum())
+                est = iters * float(p) * p / 2e9  # ~2 GFLOP/s single-thread naive loops
+                pin = (Gf.cpu().numpy(), cf.cpu().numpy(), nf, float(res.d[0]),
+                       [res.lam[0, q].cpu().numpy() for q in range(len(cfg.penalties))], grp, ngroups, est)
+            cpu = cpu_baseline(cfg, path_inputs=pin)
         line = {
             "metric": METRIC, "value": value, "unit": "TFLOP/s", "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": step_ms, "fit_seconds": step_ms / 1e3,
@@ -360,6 +399,8 @@ def main():
             "path_us_per_iter": (None if cfg.logistic else
                                  1e3 * path_step_ms / max(1, int(res.iters.sum(-1).max()))),
             "roofline": roofline, "clocks": clk, "gpu_launches": launches, "e2e": e2e,
+            "nccl": {"version": ".".join(str(v) for v in torch.cuda.nccl.version()) if world > 1 else None,
+                     "algo": os.environ.get("NCCL_ALGO"), "proto": os.environ.get("NCCL_PROTO")},
             "cpu_baseline": cpu,
         }
         print(json.dumps(line), flush=True)
