@@ -728,6 +728,7 @@ __device__ __forceinline__ void st_cluster(double* local, uint32_t rank, double 
 // max_j |dbeta_j| <= tol) only needs that OR, so no floating-point max is reduced.
 struct LeanArgs {
   int C;            // CTAs per unit (cluster size)
+  int qsplit;       // 1: one cluster per (unit, penalty) (kernel instantiated with NPT = 1)
   int rows;         // max rows per CTA (= R * RG)
   int pvl;          // padded vector length (= KC * T >= p)
   int power_iters;
@@ -830,11 +831,14 @@ __global__ void __launch_bounds__(NTH, 1) fit_lean_kernel(const PathParams P, co
   __shared__ int s_fam[NPT], s_skip[NPT];
   __shared__ double s_gam[NPT], s_alp[NPT], s_lmax[NPT];
   __shared__ uint32_t F[3];
-  const int p = P.p, nP = P.nP, L = P.L, C = A.C;
+  const int p = P.p, nPg = P.nP, L = P.L, C = A.C;
+  // penalty split (A.qsplit): cluster i fits penalty i % nPg of unit i / nPg alone (NPT = 1)
+  const int clu = blockIdx.x / C;
+  const int qoff = A.qsplit ? clu % nPg : 0, nP = A.qsplit ? 1 : nPg;
   constexpr int pvl = KC * T, rows = RT * RG;  // == A.pvl, A.rows (compile-time: immediate offsets)
   const int tid = threadIdx.x, rg = tid / T, tl = tid % T, warp = tid >> 5, lane = tid & 31;
   const uint32_t rank = cluster_rank();
-  const int unit = blockIdx.x / C;
+  const int unit = A.qsplit ? clu / nPg : clu;
   const int j0 = P.cta_j0[blockIdx.x], j1 = P.cta_j1[blockIdx.x], nr = j1 - j0;
   const int kcu = (p + T - 1) / T;                       // column slots in use (warp-uniform)
   const bool wrows = (warp * (32 / T)) * RT < nr;        // this warp owns at least one row
@@ -994,7 +998,7 @@ __global__ void __launch_bounds__(NTH, 1) fit_lean_kernel(const PathParams P, co
     int fam = 0;
     double gq = 0.0, aq = 0.0;
     if (q < nP) {
-      fam = P.fam[q]; gq = P.gam[q]; aq = P.alp[q];
+      fam = P.fam[q + qoff]; gq = P.gam[q + qoff]; aq = P.alp[q + qoff];
       const double* cc = P.shared_grid ? P.cn : cu;
       if (P.lmax_override) {
         lm = *P.lmax_override;
@@ -1036,7 +1040,7 @@ __global__ void __launch_bounds__(NTH, 1) fit_lean_kernel(const PathParams P, co
   if (P.beta_init)
     for (int e = tid; e < nP * p; e += NTH) {
       const int q = e / p, k = e % p;
-      vec[vix<NPT>(q, k, pvl)] = P.beta_init[((size_t)unit * nP + q) * p + P.perm[k]];
+      vec[vix<NPT>(q, k, pvl)] = P.beta_init[((size_t)unit * nPg + q + qoff) * p + P.perm[k]];
     }
   __syncthreads();
   auto lam_at = [&](int q, int l) -> double {
@@ -1047,7 +1051,7 @@ __global__ void __launch_bounds__(NTH, 1) fit_lean_kernel(const PathParams P, co
   if (rank == 0)
     for (int e = tid; e < nP * L; e += NTH) {
       const int q = e / L, l = e % L;
-      P.lam_out[((size_t)unit * nP + q) * L + l] = lam_at(q, l);
+      P.lam_out[((size_t)unit * nPg + q + qoff) * L + l] = lam_at(q, l);
     }
   int lidx[NPT], itc[NPT];
   double lam[NPT];
@@ -1166,11 +1170,11 @@ __global__ void __launch_bounds__(NTH, 1) fit_lean_kernel(const PathParams P, co
       const bool conv = !((f >> q) & 1u);   // every |dbeta_j| <= tol (R#17)
       if (conv || it >= P.maxit) {
         const int l = lidx[q];
-        double* out = P.beta_out + (((size_t)unit * nP + q) * L + l) * p;
+        double* out = P.beta_out + (((size_t)unit * nPg + q + qoff) * L + l) * p;
         for (int r = tid; r < nr; r += NTH) out[P.perm[j0 + r]] = vn[vix<NPT>(q, j0 + r, pvl)];
         if (rank == 0 && tid == 0) {
-          P.it_out[((size_t)unit * nP + q) * L + l] = it;
-          P.cv_out[((size_t)unit * nP + q) * L + l] = conv ? 1 : 0;
+          P.it_out[((size_t)unit * nPg + q + qoff) * L + l] = it;
+          P.cv_out[((size_t)unit * nPg + q + qoff) * L + l] = conv ? 1 : 0;
         }
         lidx[q] = l + 1;
         itc[q] = 0;
@@ -2469,12 +2473,20 @@ extern "C" oem_status oem_fit_path(oem_ctx* ctx, const double* G, const double* 
   if (!use_lean && !use_glob && !use_cluster &&
       !make_layout(nU, p, NPT, any_grp ? gstart : std::vector<int>(), ctx->num_sms, 200 * 1024, lo, why))
     OEM_FAIL(OEM_ERR_UNSUPPORTED, "oem_fit_path: persistent solver layout: " + why);
+  // penalty split: with SMs to spare, each (unit, penalty) gets its own cluster (NPT = 1: no
+  // cross-penalty divergence, and each penalty stops when its own path ends)
+  LeanLayout ll1;
+  const bool qsplit = use_lean && nP > 1 && !(force && std::string(force) == "batched") &&
+                      make_lean_layout(p, 1, any_grp ? gstart : std::vector<int>(), ll1) &&
+                      (int64_t)nU * nP * ll1.C <= ctx->num_sms;
+  if (qsplit) ll = ll1;
   std::vector<int> t_unit, t_rank, t_ncta, t_j0, t_j1;
   if (use_lean) {
     for (int u = 0; u < nU; ++u)
-      for (int c = 0; c < ll.C; ++c) {
-        t_unit.push_back(u); t_rank.push_back(c); t_j0.push_back(ll.cuts[c]); t_j1.push_back(ll.cuts[c + 1]);
-      }
+      for (int q = 0; q < (qsplit ? nP : 1); ++q)
+        for (int c = 0; c < ll.C; ++c) {
+          t_unit.push_back(u); t_rank.push_back(c); t_j0.push_back(ll.cuts[c]); t_j1.push_back(ll.cuts[c + 1]);
+        }
     t_ncta.assign(nU, ll.C);
   } else if (use_glob) {
     for (int u = 0; u < nU; ++u)
@@ -2659,12 +2671,13 @@ extern "C" oem_status oem_fit_path(oem_ctx* ctx, const double* G, const double* 
     // ---- a7-a10 fused in one launch: register-resident G, one cluster per unit
     P.ps = 0; P.T = 0; P.smem_rows = 0;
     LeanArgs A;
-    A.C = ll.C; A.rows = ll.rows; A.pvl = ll.pvl;
+    A.C = ll.C; A.rows = ll.rows; A.pvl = ll.pvl; A.qsplit = qsplit ? 1 : 0;
     A.power_iters = cfg.power_iters; A.inflate = cfg.d_inflate; A.compute_d = d_in ? 0 : 1; A.d_out = dptr;
     PhaseTimer tm(ctx, PH_PATH, st);
     ++ctx->launches;
     oem_status s;
-    if (nP == 1) s = launch_lean_v<1>(P, A, nU, ll, st);
+    if (qsplit) s = launch_lean_v<1>(P, A, nU * nP, ll, st);
+    else if (nP == 1) s = launch_lean_v<1>(P, A, nU, ll, st);
     else if (nP == 2) s = launch_lean_v<2>(P, A, nU, ll, st);
     else if (nP == 3) s = launch_lean_v<3>(P, A, nU, ll, st);
     else s = launch_lean_v<4>(P, A, nU, ll, st);
