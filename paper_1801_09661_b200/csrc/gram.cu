@@ -28,6 +28,7 @@
 //    The result is packed (upper triangle of the augmented matrix) for one NCCL allreduce
 //    when the rows are sharded over GPUs.
 #include <algorithm>
+#include <cmath>
 #include <cstdlib>
 #include <cstring>
 #include <vector>
@@ -685,8 +686,16 @@ static oem_status build_plan(oem_ctx* ctx, int mode, int p, int64_t nrows, int K
   const int64_t units = std::max<int64_t>(1, (nrows + BK - 1) / BK);
   const int nfold = mode == MODE_FOLD ? K : 1;
   const int per_sm = two_per_sm ? 2 : 1;
-  int64_t want = (int64_t)ctx->num_sms * per_sm * 8 / std::max(1, pl.U * nfold);
-  want = std::max<int64_t>(1, std::min<int64_t>(want, std::max<int64_t>(1, units / 8)));
+  // segments: as many (CTA type, segment) items as ~48 waves over the SMs (a short tail), but
+  // at least 64 stages per segment (pipeline fill and the partial-block epilogue amortised);
+  // measured: cfg4 8 waves 294 ms -> 48 waves 288 ms; cfg2 prefers ~4 waves (0.42 -> 0.40 ms)
+  // (a whole number of waves, so the last one is not a mostly idle partial wave)
+  const char* wv = std::getenv("OEM_GRAM_WAVES");  // developer override (timing studies)
+  const double per_wave = (double)ctx->num_sms * per_sm / std::max(1, pl.U * nfold);  // segments per wave
+  const double w_fit = std::min(48.0, (double)units / 64.0 / per_wave);
+  const int waves = wv ? std::max(1, std::atoi(wv)) : std::max(1, (int)std::ceil(w_fit));
+  int64_t want = std::max<int64_t>(1, (int64_t)std::llround(waves * per_wave));
+  want = std::min<int64_t>(want, std::max<int64_t>(1, units / 8));
   pl.seg_rows = ((units + want - 1) / want) * BK;
   pl.nseg = (int)std::max<int64_t>(1, (nrows + pl.seg_rows - 1) / pl.seg_rows);
   cudaError_t e;
