@@ -660,6 +660,8 @@ static oem_status build_plan(oem_ctx* ctx, int mode, int p, int64_t nrows, int K
   }
   pl.U = (int)pl.ctas.size();
   if (!pl.two_panel || pl.U_off == 0) pl.U_off = pl.U;
+  if (const char* e = std::getenv("OEM_GRAM_NO_LPT"))  // developer override: one group, segment-major
+    if (e[0] == '1') pl.U_off = pl.U;
   // y staging: 1D TMA box (PLAIN/WEIGHTED); FOLD: 2D box [BK][Kpad] over y viewed as [nq][K]
   // (needs K*8 % 16 == 0, i.e. even K), else the producer's lanes load it
   if (mode == MODE_FOLD) {
