@@ -123,6 +123,57 @@ def test_gram_full_n_column_subset_cfg4(ctx):
     assert np.max(np.abs(Gh / cfg.n - S)) < 6 / np.sqrt(cfg.n) * 3
 
 
+def test_gram_folds_full_size_cfg3(ctx):
+    """cfg3 at full size (n = 1e7, p = 500, K = 10 folds, 40 GB resident), in the launch
+    configuration bench.py times: the leading 16x16 block of every fold Gram against the oracle's
+    fold sums over all 1e7 rows (host generator, those columns only: y would need every column,
+    and X^T y per fold is checked at the smaller sizes of test_gram_folds_cfg3_parity)."""
+    from paper_1801_09661_b200 import oem_gram_folds
+    cfg = CONFIGS["cfg3"]
+    bt = dg.beta(cfg.spec)
+    Xd, yd = device_rows(cfg.spec, bt)
+    Gk, ck, yyk, cnt = oem_gram_folds(ctx, Xd, yd, cfg.folds)
+    del Xd
+    torch.cuda.empty_cache()
+    m, K = 16, cfg.folds
+    Gs = np.zeros((K, m, m))
+    for r in range(0, cfg.n, 1_000_000):
+        X, _ = dg.rows_host(cfg.spec, bt, r, 1_000_000, 0, m, want_y=False)
+        G1, _, _, _ = orc.gram_folds(X, np.zeros(X.shape[0]), K, row_offset=r)
+        Gs += G1
+    Gh = Gk.cpu().numpy()
+    for k in range(K):
+        assert scale_err(Gh[k, :m, :m], Gs[k]) <= 1e-12
+    assert list(cnt) == [cfg.n // K] * K
+
+
+def test_weighted_full_size_cfg5(ctx):
+    """cfg5's weighted pass at full size (n = 5e6, p = 200, 8 GB resident) at a nonzero beta,
+    against the oracle's compensated weighted Gram accumulated over 1e6-row blocks."""
+    from paper_1801_09661_b200 import oem_gram_weighted
+    cfg = CONFIGS["cfg5"]
+    bt = dg.beta(cfg.spec)
+    Xd, yd = device_rows(cfg.spec, bt)
+    beta = 0.5 * bt + 0.01
+    Gw, cw, sc = oem_gram_weighted(ctx, Xd, yd, to_dev(beta))
+    del Xd
+    torch.cuda.empty_cache()
+    Go = np.zeros((cfg.p, cfg.p)); co = np.zeros(cfg.p); so = np.zeros(2); szz = 0.0
+    for r in range(0, cfg.n, 1_000_000):
+        X, y = dg.rows_host(cfg.spec, bt, r, 1_000_000)
+        G1, c1, s1 = orc.gram_weighted(X, y, beta)
+        Go += G1; co += c1; so += s1
+        eta = X @ beta
+        mu = np.clip(1 / (1 + np.exp(-eta)), 1e-5, 1 - 1e-5)
+        w = mu * (1 - mu)
+        szz += np.sum(w * (eta + (y - mu) / w) ** 2)
+    assert scale_err(Gw.cpu().numpy(), Go) <= 1e-12
+    # scale-aware for the augmented column: sqrt(Gw_jj * sum w z^2) (R#32 applied to [X | z])
+    assert np.max(np.abs(cw.cpu().numpy() - co) / np.sqrt(np.diag(Go) * szz)) <= 1e-12
+    assert abs(float(sc[0]) - so[0]) <= 1e-12 * so[0]
+    assert abs(float(sc[1]) - so[1]) <= 1e-12 * abs(so[1])
+
+
 def test_gram_edge_cases(ctx):
     from paper_1801_09661_b200 import OemError, oem_gram
     # n = 0: zero statistics
