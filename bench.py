@@ -44,6 +44,12 @@ def gram_flops(n, p):
     return float(n) * p * (p + 3)
 
 
+def weighted_flops(n, p):
+    """Algorithmic flops of one weighted pass: n p (p+1) (SYRK) + 2 n p (X^T W z)
+    + 2 n p (eta = X beta) + n p (weight scaling) = n p (p+6)."""
+    return float(n) * p * (p + 6)
+
+
 # ------------------------------------------------------------------ clocks sampler
 class Clocks:
     def __init__(self, index=0):
@@ -278,11 +284,11 @@ def main():
     if cfg.logistic:
         # every outer step is one weighted pass; count them from the fit
         outer = sum(res.outer_iters)
-        flops_step = (gram_flops(n, p) + 5.0 * n * p) * outer
+        flops_step = weighted_flops(n, p) * outer
     value = flops_step / (gram_step_ms * 1e-3) / 1e12
     # roofline of the dominant kernel (the tensor-core Gram kernel): algorithmic flops per
     # launch over its event-timed launch duration on this rank
-    per_launch_flops = gram_flops(nl, p) * (sum(res.outer_iters) if cfg.logistic else 1)
+    per_launch_flops = (weighted_flops(nl, p) * sum(res.outer_iters)) if cfg.logistic else gram_flops(nl, p)
     achieved = per_launch_flops / (st["gram_ms"] / args.steps * 1e-3) / 1e12
     traffic = None
     prof = os.path.join(ROOT, "profiles", "ncu_summary_r01.json")
