@@ -1196,6 +1196,8 @@ __global__ void __launch_bounds__(NTH, 1) fit_lean_kernel(const PathParams P, co
 // (ld.global.cg: L2, never a stale L1 line). Cooperative launch: every CTA is co-resident.
 struct GlobArgs {
   int Cmax;             // max CTAs per unit (slot stride)
+  int qsplit;           // 1: one virtual unit per (unit, penalty), kernel instantiated with NPT = 1
+  int nvu;              // virtual units (nU, or nU * nP with qsplit)
   int rows, pvl, power_iters, compute_d;
   double inflate;
   double* d_out;        // [nU]
@@ -1223,9 +1225,10 @@ __device__ __forceinline__ unsigned long long ld_relaxed_u64(const unsigned long
   return v;
 }
 
-template <int NPT, int R, int KC, int T>
+template <int NPT, int R, int KC, int T, int RS = 0>
 __global__ void __launch_bounds__(PT, 1) fit_glob_kernel(const PathParams P, const GlobArgs A) {
-  constexpr int RG = PT / T, V = R * NPT, VP = pow2ceil(V), NW = PT / 32;
+  constexpr int RT = R + RS;  // rows per thread row group: R in registers, RS in shared memory
+  constexpr int RG = PT / T, V = RT * NPT, VP = pow2ceil(V), NW = PT / 32;
   constexpr int NV = NPT == 1 ? 1 : 2 * ((NPT + 1) / 2);
   static_assert(VP <= T && (T & (T - 1)) == 0 && T <= 32, "lean layout");
   extern __shared__ __align__(16) double sm[];
@@ -1233,26 +1236,29 @@ __global__ void __launch_bounds__(PT, 1) fit_glob_kernel(const PathParams P, con
   __shared__ double s_gam[NPT], s_alp[NPT], s_lmax[NPT];
   __shared__ uint32_t s_bits, s_all;
   __shared__ double s_red[NW], s_tot;
-  const int p = P.p, nP = P.nP, L = P.L;
-  constexpr int pvl = KC * T, rows = R * RG;  // == A.pvl, A.rows
+  const int p = P.p, nPg = P.nP, L = P.L;
+  constexpr int pvl = KC * T, rows = RT * RG;  // == A.pvl, A.rows
   const int tid = threadIdx.x, rg = tid / T, tl = tid % T, warp = tid >> 5, lane = tid & 31;
-  const int unit = P.cta_unit[blockIdx.x], rank = P.cta_rank[blockIdx.x], C = P.unit_ncta[unit];
+  // virtual unit: a unit Gram, or with A.qsplit one (unit, penalty) pair fitted alone (NPT = 1)
+  const int vu = P.cta_unit[blockIdx.x], rank = P.cta_rank[blockIdx.x], C = P.unit_ncta[vu];
+  const int unit = A.qsplit ? vu / nPg : vu, qoff = A.qsplit ? vu % nPg : 0, nP = A.qsplit ? 1 : nPg;
   const int j0 = P.cta_j0[blockIdx.x], j1 = P.cta_j1[blockIdx.x], nr = j1 - j0;
   const int kcu = (p + T - 1) / T;
-  const bool wrows = (warp * (32 / T)) * R < nr;
+  const bool wrows = (warp * (32 / T)) * RT < nr;
   const double* Gu = P.Gn + (size_t)unit * p * p;
   const double* cu = P.cn + (size_t)unit * p;
   constexpr int vstride = pvl * NV;
   double* vec = sm;                                   // [2][vstride] (local copies)
-  double* uv = vec + (size_t)2 * vstride;             // [NPT][rows]
+  double* gsm = vec + (size_t)2 * vstride;            // [RS*RG][pvl] shared-memory rows of G
+  double* uv = gsm + (size_t)RS * RG * pvl;           // [NPT][rows]
   double* gw_s = uv + (size_t)NPT * rows;
   int* ga_s = reinterpret_cast<int*>(gw_s + rows);
   int* gb_s = ga_s + rows;
-  double* gvec = A.gvec + (size_t)unit * vstride;     // + par * nU * vstride
-  const size_t gpar = (size_t)P.nU * vstride;
-  unsigned long long* gflag = A.gflag + (size_t)unit * A.Cmax;  // + par * nU * Cmax
-  double* gslot = A.gslot + (size_t)unit * A.Cmax;
-  const size_t spar = (size_t)P.nU * A.Cmax;
+  double* gvec = A.gvec + (size_t)vu * vstride;       // + par * nvu * vstride
+  const size_t gpar = (size_t)A.nvu * vstride;
+  unsigned long long* gflag = A.gflag + (size_t)vu * A.Cmax;  // + par * nvu * Cmax
+  double* gslot = A.gslot + (size_t)vu * A.Cmax;
+  const size_t spar = (size_t)A.nvu * A.Cmax;
   unsigned epoch = 0;
   // unit barrier: every CTA of the unit has published its writes (grid.sync pattern, per unit)
   // (bar.sync orders the CTA's writes before thread 0's release, which is cumulative; relaxed
@@ -1260,9 +1266,9 @@ __global__ void __launch_bounds__(PT, 1) fit_glob_kernel(const PathParams P, con
   auto unit_sync = [&]() {
     __syncthreads();
     if (tid == 0) {
-      red_release_add(&A.gcnt[unit], 1u);
+      red_release_add(&A.gcnt[vu], 1u);
       const unsigned target = (epoch + 1) * (unsigned)C;
-      while (ld_relaxed(&A.gcnt[unit]) < target) {}
+      while (ld_relaxed(&A.gcnt[vu]) < target) {}
       fence_acquire_gpu();
     }
     ++epoch;
@@ -1282,20 +1288,30 @@ __global__ void __launch_bounds__(PT, 1) fit_glob_kernel(const PathParams P, con
   for (int i = 0; i < R; ++i)
 #pragma unroll
     for (int m = 0; m < KC; ++m) {
-      const int r = rg * R + i, k = tl + m * T;
+      const int r = rg * RT + i, k = tl + m * T;
       g[i][m] = (r < nr && k < p) ? Gu[(size_t)(j0 + r) * p + k] : 0.0;
     }
+#pragma unroll
+  for (int i = R; i < RT; ++i)
+#pragma unroll
+    for (int m = 0; m < KC; ++m) {
+      const int r = rg * RT + i, k = tl + m * T;
+      gsm[(size_t)(rg * RS + i - R) * pvl + k] = (r < nr && k < p) ? Gu[(size_t)(j0 + r) * p + k] : 0.0;
+    }
+  auto gel = [&](int i, int m) -> double {
+    return i < R ? g[i < R ? i : 0][m] : gsm[(size_t)(rg * RS + i - R) * pvl + tl + m * T];
+  };
   const int vidx = lean_vidx<VP, T>(tl);
-  const int mi = vidx / NPT, mq = vidx % NPT, mr = rg * R + mi;
+  const int mi = vidx / NPT, mq = vidx % NPT, mr = rg * RT + mi;
   const bool owner = (tl & (T / VP - 1)) == 0;
   const bool act = owner && vidx < V && mr < nr;
   const int mj = j0 + mr;
   const double c_my = act ? cu[mj] : 0.0;
   const double w_my = (act && P.var_w) ? P.var_w[mj] : 1.0;
-  constexpr int RP = pow2ceil(R);
+  constexpr int RP = pow2ceil(RT);
   const int vidx1 = lean_vidx<RP, T>(tl);
-  const int pr = rg * R + vidx1;
-  const bool pact = (tl & (T / RP - 1)) == 0 && vidx1 < R && pr < nr;
+  const int pr = rg * RT + vidx1;
+  const bool pact = (tl & (T / RP - 1)) == 0 && vidx1 < RT && pr < nr;
   // CTA sum of one double per thread, in warp order; result in s_tot after the call
   auto cta_sum = [&](double x) {
 #pragma unroll
@@ -1339,13 +1355,13 @@ __global__ void __launch_bounds__(PT, 1) fit_glob_kernel(const PathParams P, con
   if (A.compute_d) {
     double gm = 0.0;
 #pragma unroll
-    for (int i = 0; i < R; ++i) {
+    for (int i = 0; i < RT; ++i) {
       double s = 0.0;
 #pragma unroll
-      for (int m = 0; m < KC; ++m) s += fabs(g[i][m]);
+      for (int m = 0; m < KC; ++m) s += fabs(gel(i, m));
 #pragma unroll
       for (int o = T / 2; o >= 1; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
-      if (rg * R + i < nr) gm = fmax(gm, s);
+      if (rg * RT + i < nr) gm = fmax(gm, s);
     }
 #pragma unroll
     for (int o = 16; o >= 1; o >>= 1) gm = fmax(gm, __shfl_xor_sync(0xffffffffu, gm, o));
@@ -1375,7 +1391,7 @@ __global__ void __launch_bounds__(PT, 1) fit_glob_kernel(const PathParams P, con
           if (m >= kcu) break;
           const double b = vc[vix<NPT>(0, tl + m * T, pvl)];
 #pragma unroll
-          for (int i = 0; i < R; ++i) a[i] = fma(g[i][m], b, a[i]);
+          for (int i = 0; i < RT; ++i) a[i] = fma(gel(i, m), b, a[i]);
         }
       }
       const double s = lean_rs<RP, T>(a, tl);
@@ -1416,7 +1432,7 @@ __global__ void __launch_bounds__(PT, 1) fit_glob_kernel(const PathParams P, con
     int fam = 0;
     double gq = 0.0, aq = 0.0;
     if (q < nP) {
-      fam = P.fam[q]; gq = P.gam[q]; aq = P.alp[q];
+      fam = P.fam[q + qoff]; gq = P.gam[q + qoff]; aq = P.alp[q + qoff];
       const double* cc = P.shared_grid ? P.cn : cu;
       if (P.lmax_override) {
         lm = *P.lmax_override;
@@ -1457,7 +1473,7 @@ __global__ void __launch_bounds__(PT, 1) fit_glob_kernel(const PathParams P, con
   if (P.beta_init)
     for (int e = tid; e < nP * p; e += PT) {
       const int q = e / p, k = e % p;
-      vec[vix<NPT>(q, k, pvl)] = P.beta_init[((size_t)unit * nP + q) * p + P.perm[k]];
+      vec[vix<NPT>(q, k, pvl)] = P.beta_init[((size_t)unit * nPg + q + qoff) * p + P.perm[k]];
     }
   if (tid == 0) s_bits = 0u;
   __syncthreads();
@@ -1469,7 +1485,7 @@ __global__ void __launch_bounds__(PT, 1) fit_glob_kernel(const PathParams P, con
   if (rank == 0)
     for (int e = tid; e < nP * L; e += PT) {
       const int q = e / L, l = e % L;
-      P.lam_out[((size_t)unit * nP + q) * L + l] = lam_at(q, l);
+      P.lam_out[((size_t)unit * nPg + q + qoff) * L + l] = lam_at(q, l);
     }
   int lidx[NPT], itc[NPT];
   double lam[NPT];
@@ -1513,9 +1529,11 @@ __global__ void __launch_bounds__(PT, 1) fit_glob_kernel(const PathParams P, con
           }
         }
 #pragma unroll
-        for (int i = 0; i < R; ++i)
+        for (int i = 0; i < RT; ++i) {
+          const double gv = gel(i, m);
 #pragma unroll
-          for (int q = 0; q < NPT; ++q) a[i * NPT + q] = fma(g[i][m], b[q], a[i * NPT + q]);
+          for (int q = 0; q < NPT; ++q) a[i * NPT + q] = fma(gv, b[q], a[i * NPT + q]);
+        }
       }
     }
     const double s = lean_rs<VP, T>(a, tl);
@@ -1608,11 +1626,11 @@ __global__ void __launch_bounds__(PT, 1) fit_glob_kernel(const PathParams P, con
       const bool conv = !((f >> q) & 1u);
       if (conv || it >= P.maxit) {
         const int l = lidx[q];
-        double* out = P.beta_out + (((size_t)unit * nP + q) * L + l) * p;
+        double* out = P.beta_out + (((size_t)unit * nPg + q + qoff) * L + l) * p;
         for (int r = tid; r < nr; r += PT) out[P.perm[j0 + r]] = vn[vix<NPT>(q, j0 + r, pvl)];
         if (rank == 0 && tid == 0) {
-          P.it_out[((size_t)unit * nP + q) * L + l] = it;
-          P.cv_out[((size_t)unit * nP + q) * L + l] = conv ? 1 : 0;
+          P.it_out[((size_t)unit * nPg + q + qoff) * L + l] = it;
+          P.cv_out[((size_t)unit * nPg + q + qoff) * L + l] = conv ? 1 : 0;
         }
         lidx[q] = l + 1;
         itc[q] = 0;
@@ -2220,26 +2238,33 @@ static oem_status coop_launch(K kern, int grid, size_t smem, cudaStream_t st, vo
 
 // ---------------------------------------------------------------- grid-wide lean solver: layout / launch
 struct GlobLayout {
-  int variant = -1;  // 0: R1 KC32 T32 (16 rows / CTA, p <= 1024), 1: R2 KC16 T32 (32 rows, p <= 512)
+  int variant = -1;  // 0: R1 KC32 T32 (16 rows / CTA, p <= 1024), 1: R2 KC16 T32 (32 rows, p <= 512),
+                     // 2: R1 RS1 KC32 T32 (16 register + 16 shared-memory rows, p <= 1024, split)
+  bool split = false;
+  int nvu = 0;
   int C = 0, rows = 0, pvl = 0;
   size_t smem = 0;
   std::vector<int> cuts;
 };
 
-template <int NPT, int R, int KC, int T>
+template <int NPT, int R, int KC, int T, int RS = 0>
 static int glob_capacity(size_t smem, int num_sms) {
   int per = 0;
-  if (cudaFuncSetAttribute(fit_glob_kernel<NPT, R, KC, T>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) !=
+  if (cudaFuncSetAttribute(fit_glob_kernel<NPT, R, KC, T, RS>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) !=
           cudaSuccess ||
-      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, fit_glob_kernel<NPT, R, KC, T>, PT, smem) != cudaSuccess)
+      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, fit_glob_kernel<NPT, R, KC, T, RS>, PT, smem) != cudaSuccess)
     return 0;
   return per * num_sms;
 }
 
-static bool make_glob_layout(int nU, int p, int nP, const std::vector<int>& gstart, int num_sms, GlobLayout& lo) {
+// split = true: one virtual unit per (unit, penalty), NPT = 1, 32 rows per CTA (16 of them in
+// shared memory for p > 512) so that nU * nP units stay co-resident.
+static bool make_glob_layout(int nU, int p, int nP, const std::vector<int>& gstart, int num_sms, GlobLayout& lo,
+                             bool split = false) {
   if (nP > 4 || p > 1024) return false;
-  const int v = p <= 512 ? 1 : 0;
-  const int rows = v == 1 ? 32 : 16, pvl = v == 1 ? 16 * 32 : 32 * 32;
+  const int v = p <= 512 ? 1 : split ? 2 : 0;
+  const int rows = v == 0 ? 16 : 32, pvl = v == 1 ? 16 * 32 : 32 * 32, rs = v == 2 ? 16 : 0;
+  const int nvu = split ? nU * nP : nU, NPTe = split ? 1 : nP;
   std::vector<int> cuts{0};
   if (gstart.empty()) {
     const int C = (p + rows - 1) / rows;
@@ -2261,23 +2286,28 @@ static bool make_glob_layout(int nU, int p, int nP, const std::vector<int>& gsta
     if (cuts.back() != p) cuts.push_back(p);
   }
   const int C = (int)cuts.size() - 1;
-  const int NV = nP == 1 ? 1 : 2 * ((nP + 1) / 2);
-  const size_t smem = ((size_t)2 * NV * pvl + (size_t)nP * rows + rows) * 8 + (size_t)2 * rows * 4 + 16;
+  const int NV = NPTe == 1 ? 1 : 2 * ((NPTe + 1) / 2);
+  const size_t smem = ((size_t)2 * NV * pvl + (size_t)rs * pvl + (size_t)NPTe * rows + rows) * 8 +
+                      (size_t)2 * rows * 4 + 16;
   int cap = 0;
-  if (v == 0) {
-    cap = nP == 1 ? glob_capacity<1, 1, 32, 32>(smem, num_sms) : nP == 2 ? glob_capacity<2, 1, 32, 32>(smem, num_sms)
-        : nP == 3 ? glob_capacity<3, 1, 32, 32>(smem, num_sms) : glob_capacity<4, 1, 32, 32>(smem, num_sms);
+  if (v == 2) {
+    cap = glob_capacity<1, 1, 32, 32, 1>(smem, num_sms);
+  } else if (v == 0) {
+    cap = NPTe == 1 ? glob_capacity<1, 1, 32, 32>(smem, num_sms) : NPTe == 2 ? glob_capacity<2, 1, 32, 32>(smem, num_sms)
+        : NPTe == 3 ? glob_capacity<3, 1, 32, 32>(smem, num_sms) : glob_capacity<4, 1, 32, 32>(smem, num_sms);
   } else {
-    cap = nP == 1 ? glob_capacity<1, 2, 16, 32>(smem, num_sms) : nP == 2 ? glob_capacity<2, 2, 16, 32>(smem, num_sms)
-        : nP == 3 ? glob_capacity<3, 2, 16, 32>(smem, num_sms) : glob_capacity<4, 2, 16, 32>(smem, num_sms);
+    cap = NPTe == 1 ? glob_capacity<1, 2, 16, 32>(smem, num_sms) : NPTe == 2 ? glob_capacity<2, 2, 16, 32>(smem, num_sms)
+        : NPTe == 3 ? glob_capacity<3, 2, 16, 32>(smem, num_sms) : glob_capacity<4, 2, 16, 32>(smem, num_sms);
   }
-  if ((int64_t)nU * C > cap) return false;
+  if ((int64_t)nvu * C > cap) return false;
   lo.variant = v;
   lo.C = C;
   lo.rows = rows;
   lo.pvl = pvl;
   lo.smem = smem;
   lo.cuts = cuts;
+  lo.split = split;
+  lo.nvu = nvu;
   return true;
 }
 
@@ -2285,6 +2315,7 @@ template <int NPT>
 static oem_status launch_glob_v(const PathParams& P, const GlobArgs& A, int grid, const GlobLayout& lo, cudaStream_t st) {
   void* args[] = {const_cast<PathParams*>(&P), const_cast<GlobArgs*>(&A)};
   if (lo.variant == 0) return coop_launch(fit_glob_kernel<NPT, 1, 32, 32>, grid, lo.smem, st, args);
+  if (lo.variant == 2) return coop_launch(fit_glob_kernel<1, 1, 32, 32, 1>, grid, lo.smem, st, args);
   return coop_launch(fit_glob_kernel<NPT, 2, 16, 32>, grid, lo.smem, st, args);
 }
 
@@ -2464,8 +2495,11 @@ extern "C" oem_status oem_fit_path(oem_ctx* ctx, const double* G, const double* 
   const bool use_lean = !(force && (std::string(force) == "global" || std::string(force) == "cluster")) &&
                         make_lean_layout(p, nP, any_grp ? gstart : std::vector<int>(), ll);
   GlobLayout gl;
-  const bool use_glob = !use_lean && !(force && (std::string(force) == "global" || std::string(force) == "cluster")) &&
-                        make_glob_layout(nU, p, nP, any_grp ? gstart : std::vector<int>(), ctx->num_sms, gl);
+  const bool glob_ok = !use_lean && !(force && (std::string(force) == "global" || std::string(force) == "cluster"));
+  const bool use_glob =
+      glob_ok && ((nP > 1 && !(force && std::string(force) == "batched") &&
+                   make_glob_layout(nU, p, nP, any_grp ? gstart : std::vector<int>(), ctx->num_sms, gl, true)) ||
+                  make_glob_layout(nU, p, nP, any_grp ? gstart : std::vector<int>(), ctx->num_sms, gl, false));
   bool use_cluster = !use_lean && !use_glob && !(force && std::string(force) == "global") &&
                      make_cluster_layout(nU, p, NPT, any_grp ? gstart : std::vector<int>(), ctx->num_sms,
                                          ereg_for(NPT), cl);
@@ -2489,11 +2523,11 @@ extern "C" oem_status oem_fit_path(oem_ctx* ctx, const double* G, const double* 
         }
     t_ncta.assign(nU, ll.C);
   } else if (use_glob) {
-    for (int u = 0; u < nU; ++u)
+    for (int u = 0; u < gl.nvu; ++u)  // virtual units (unit, or (unit, penalty) when split)
       for (int c = 0; c < gl.C; ++c) {
         t_unit.push_back(u); t_rank.push_back(c); t_j0.push_back(gl.cuts[c]); t_j1.push_back(gl.cuts[c + 1]);
       }
-    t_ncta.assign(nU, gl.C);
+    t_ncta.assign(gl.nvu, gl.C);
   } else if (use_cluster) {
     for (int u = 0; u < nU; ++u)
       for (int c = 0; c < cl.C; ++c) { t_unit.push_back(u); t_rank.push_back(c); }
@@ -2522,7 +2556,8 @@ extern "C" oem_status oem_fit_path(oem_ctx* ctx, const double* G, const double* 
   const size_t o_pslot = take(sizeof(double) * 3 * nU * Cmax);
   const size_t o_bad = take(sizeof(unsigned long long) * nU);
   const size_t o_dslot = take(sizeof(unsigned long long) * 3 * nU * nP);
-  const size_t o_bar = take(sizeof(unsigned) * 2 * nU);
+  const int nvu_ws = use_glob ? std::max(nU, gl.nvu) : nU;  // virtual units (grid solver split)
+  const size_t o_bar = take(sizeof(unsigned) * 2 * nvu_ws);
   const size_t o_flags = take(sizeof(int) * 4);
   const size_t o_invn = take(sizeof(double) * nU);
   const size_t o_perm = take(sizeof(int) * p);
@@ -2538,14 +2573,15 @@ extern "C" oem_status oem_fit_path(oem_ctx* ctx, const double* G, const double* 
   const size_t o_lmax = take(sizeof(double));
   const size_t o_cu = take(sizeof(int) * ncta_total);
   const size_t o_cr = take(sizeof(int) * ncta_total);
-  const size_t o_un = take(sizeof(int) * nU);
+  const size_t o_un = take(sizeof(int) * nvu_ws);
   const size_t o_j0 = take(sizeof(int) * ncta_total);
   const size_t o_j1 = take(sizeof(int) * ncta_total);
   const size_t o_d = take(sizeof(double) * nU);
   const int gNV = nP == 1 ? 1 : 2 * ((nP + 1) / 2);
-  const size_t o_gvec = take(use_glob ? sizeof(double) * 2 * (size_t)nU * gNV * gl.pvl : 8);
-  const size_t o_gflag = take(use_glob ? sizeof(unsigned long long) * 2 * (size_t)nU * Cmax : 8);
-  const size_t o_gslot = take(use_glob ? sizeof(double) * 2 * (size_t)nU * Cmax : 8);
+  const int gNVe = (use_glob && gl.split) ? 1 : gNV;
+  const size_t o_gvec = take(use_glob ? sizeof(double) * 2 * (size_t)nvu_ws * gNVe * gl.pvl : 8);
+  const size_t o_gflag = take(use_glob ? sizeof(unsigned long long) * 2 * (size_t)nvu_ws * Cmax : 8);
+  const size_t o_gslot = take(use_glob ? sizeof(double) * 2 * (size_t)nvu_ws * Cmax : 8);
   const bool centre = cfg.xsum != nullptr || cfg.ysum != nullptr;
   const bool xform = centre || cfg.standardize;
   if (centre && !(cfg.xsum && cfg.ysum)) OEM_FAIL(OEM_ERR_INVALID_ARG, "oem_fit_path: intercept needs both xsum and ysum");
@@ -2575,7 +2611,7 @@ extern "C" oem_status oem_fit_path(oem_ctx* ctx, const double* G, const double* 
   if (cfg.lambda_max_override) put(o_lmax, cfg.lambda_max_override, sizeof(double));
   put(o_cu, t_unit.data(), sizeof(int) * ncta_total);
   put(o_cr, t_rank.data(), sizeof(int) * ncta_total);
-  put(o_un, t_ncta.data(), sizeof(int) * nU);
+  put(o_un, t_ncta.data(), sizeof(int) * t_ncta.size());
   put(o_j0, t_j0.data(), sizeof(int) * ncta_total);
   put(o_j1, t_j1.data(), sizeof(int) * ncta_total);
   if (d_in) put(o_d, d_in, sizeof(double) * nU);
@@ -2651,18 +2687,19 @@ extern "C" oem_status oem_fit_path(oem_ctx* ctx, const double* G, const double* 
     // ---- a7-a10 fused in one cooperative launch: register-resident G, C CTAs per unit over L2
     P.ps = 0; P.T = 0; P.smem_rows = 0;
     GlobArgs A;
-    A.Cmax = Cmax; A.rows = gl.rows; A.pvl = gl.pvl;
+    A.Cmax = Cmax; A.rows = gl.rows; A.pvl = gl.pvl; A.qsplit = gl.split ? 1 : 0; A.nvu = gl.nvu;
     A.power_iters = cfg.power_iters; A.inflate = cfg.d_inflate; A.compute_d = d_in ? 0 : 1; A.d_out = dptr;
     A.gvec = reinterpret_cast<double*>(base + o_gvec);
     A.gflag = reinterpret_cast<unsigned long long*>(base + o_gflag);
-    OEM_CUDA_TRY(cudaMemsetAsync(A.gflag, 0, sizeof(unsigned long long) * 2 * (size_t)nU * Cmax, st));
+    OEM_CUDA_TRY(cudaMemsetAsync(A.gflag, 0, sizeof(unsigned long long) * 2 * (size_t)nvu_ws * Cmax, st));
     A.gslot = reinterpret_cast<double*>(base + o_gslot);
     A.gcnt = reinterpret_cast<unsigned*>(base + o_bar);   // zeroed with dslot / bar / flags
     PhaseTimer tm(ctx, PH_PATH, st);
     ++ctx->launches;
     oem_status s;
-    const int grid = nU * gl.C;
-    if (nP == 1) s = launch_glob_v<1>(P, A, grid, gl, st);
+    const int grid = gl.nvu * gl.C;
+    if (gl.split) s = launch_glob_v<1>(P, A, grid, gl, st);
+    else if (nP == 1) s = launch_glob_v<1>(P, A, grid, gl, st);
     else if (nP == 2) s = launch_glob_v<2>(P, A, grid, gl, st);
     else if (nP == 3) s = launch_glob_v<3>(P, A, grid, gl, st);
     else s = launch_glob_v<4>(P, A, grid, gl, st);
