@@ -1061,6 +1061,9 @@ __global__ void __launch_bounds__(NTH, 1) fit_lean_kernel(const PathParams P, co
     itc[q] = 0;
     lam[q] = s_skip[q] ? 0.0 : lam_at(q, 0);
   }
+  // the group M-step runs only if one of this cluster's penalties is a group family
+  bool grpm = false;
+  for (int q = 0; q < nP; ++q) grpm = grpm || (grp && s_fam[q] >= OEM_GRP_LASSO);
   int fam_my[CNT];
   double gam_my[CNT], alp_my[CNT];
 #pragma unroll
@@ -1132,7 +1135,7 @@ __global__ void __launch_bounds__(NTH, 1) fit_lean_kernel(const PathParams P, co
         uv[mq[s2] * rows + mr[s2]] = u;
       }
     }
-    if (grp) {
+    if (grpm) {
       // group M-step (eqs glasso / gmcp / gscad); groups lie inside [j0, j1)
       __syncthreads();
       for (int e = warp; e < ng_loc * nP; e += NW) {   // one warp per (group, penalty)
@@ -1495,6 +1498,8 @@ __global__ void __launch_bounds__(PT, 1) fit_glob_kernel(const PathParams P, con
     itc[q] = 0;
     lam[q] = s_skip[q] ? 0.0 : lam_at(q, 0);
   }
+  bool grpm = false;  // the group M-step runs only if one of this unit's penalties is a group family
+  for (int q = 0; q < nP; ++q) grpm = grpm || (grp && s_fam[q] >= OEM_GRP_LASSO);
   const int fam_my = s_fam[mq];
   const double gam_my = s_gam[mq], alp_my = s_alp[mq];
 
@@ -1555,7 +1560,7 @@ __global__ void __launch_bounds__(PT, 1) fit_glob_kernel(const PathParams P, con
         uv[mq * rows + mr] = u;
       }
     }
-    if (grp) {
+    if (grpm) {
       __syncthreads();
       for (int e = warp; e < ng_loc * nP; e += NW) {   // one warp per (group, penalty)
         const int q = e % nP, gl = e / nP;
