@@ -299,3 +299,31 @@ def test_many_penalties_and_wide_p_fallbacks(ctx):
     fit = oem_fit_path(ctx, G, c, [n], [("lasso", 0.0, 1.0)], nlambda=6)
     B, it, cv = orc.oem_path(Go / n, co / n, float(fit.d[0]), "lasso", fit.lam[0, 0].cpu().numpy())
     assert np.max(np.abs(fit.beta[0, 0].cpu().numpy() - B)) <= TOL_BETA
+
+
+@pytest.mark.parametrize("p", [1, 7, 64, 65, 128, 129, 256, 257, 512, 513, 1024])
+def test_solver_variant_boundaries(ctx, p):
+    """Every solver layout boundary (lean register / shared-memory variants, cluster sizes, the
+    grid-wide solver, penalty split) with two units and two penalties, against the oracle."""
+    from paper_1801_09661_b200 import oem_fit_path, oem_gram
+    spec = CONFIGS["cfg2"].spec.replace(n=1500 + 3 * p, p=p, nnz=min(5, p))
+    bt = dg.beta(spec)
+    X, y = dg.rows_host(spec, bt)
+    Xp = np.zeros((X.shape[0], p + (p & 1)))
+    Xp[:, :p] = X
+    Xd = torch.from_numpy(Xp).cuda()[:, :p]
+    yd = torch.from_numpy(y).cuda()
+    h = (X.shape[0] // 2) & ~1   # 16-byte aligned second block (TMA)
+    G0, c0, _, n0 = oem_gram(ctx, Xd[:h], yd[:h])
+    G1, c1, _, n1 = oem_gram(ctx, Xd[h:], yd[h:])
+    G = torch.stack([G0, G1]); c = torch.stack([c0, c1])
+    pens = [("lasso", 0.0, 1.0), ("mcp", 3.0, 1.0)]
+    fit = oem_fit_path(ctx, G, c, [n0, n1], pens, nlambda=6)
+    for u, (lo, hi, nn) in enumerate([(0, h, n0), (h, X.shape[0], n1)]):
+        Go, co, _ = orc.gram(X[lo:hi], y[lo:hi])
+        d = float(fit.d[u])
+        lam1 = np.linalg.eigvalsh(Go / nn)[-1]
+        assert lam1 * (1 - 1e-12) <= d <= 1.01 * lam1 + 1e-300
+        for q, (fam, gamma, alpha) in enumerate(pens):
+            B, it, cv = orc.oem_path(Go / nn, co / nn, d, fam, fit.lam[u, q].cpu().numpy(), gamma, alpha)
+            assert np.max(np.abs(fit.beta[u, q].cpu().numpy() - B)) <= TOL_BETA, (p, u, fam)
