@@ -84,7 +84,9 @@ oem_status oem_gram_folds(oem_ctx* ctx, const double* X, const double* y, int64_
  * responses z_i and weights w_i at P:L376-380; R#23-25). Per row: eta = x_i^T beta,
  * mu = 1/(1+exp(-eta)) clamped to [eps, 1-eps], w = mu(1-mu), z = eta + (y - mu)/w.
  * Outputs raw sums: Gw = sum w x x^T (full symmetric p*p), xtwz = sum w z x (p),
- * scalars[0] = sum w, scalars[1] = sum [y eta - log(1 + e^eta)] (log-likelihood).
+ * scalars (device, 2, or NULL) = {sum w, sum [y eta - log(1 + e^eta)] (log-likelihood)};
+ * with scalars = NULL neither is formed (the row work is then ~5% cheaper; the logistic fit,
+ * whose stopping rule is the change in beta, passes NULL).
  * beta (p, device) must be identical on every rank. y01 must hold 0.0/1.0 (not checked on the
  * device; the binding checks once per fit). Errors: as oem_gram, plus OEM_ERR_UNSUPPORTED when
  * p > 247 (this build fuses eta into the single-panel kernel only). */

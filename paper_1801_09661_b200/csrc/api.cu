@@ -242,16 +242,19 @@ oem_status oem_gram_weighted(oem_ctx* ctx, const double* X, const double* y01, c
   oem_status s;
   if ((s = check_ctx(ctx)) != OEM_OK) return s;
   if ((s = check_x(X, y01, n_local, p, ldx, "oem_gram_weighted")) != OEM_OK) return s;
-  if (!beta || !Gw || !xtwz || !scalars) OEM_FAIL(OEM_ERR_INVALID_ARG, "oem_gram_weighted: null pointer");
+  if (!beta || !Gw || !xtwz) OEM_FAIL(OEM_ERR_INVALID_ARG, "oem_gram_weighted: null pointer");
   if (!(eps > 0.0 && eps < 0.5)) OEM_FAIL(OEM_ERR_INVALID_ARG, "oem_gram_weighted: need 0 < eps < 0.5");
   cudaStream_t st = (cudaStream_t)stream;
   const int64_t psize = packed_size(p);
   OEM_CUDA_TRY(ctx->packed.ensure(sizeof(double) * (psize + 2)));
   double* packed = ctx->packed.as<double>();
-  if ((s = gram_pass(ctx, MODE_WEIGHTED, X, y01, beta, eps, n_local, p, ldx, 0, 1, packed, st)) != OEM_OK) return s;
+  const int want_scal = scalars != nullptr;
+  if ((s = gram_pass(ctx, MODE_WEIGHTED, X, y01, beta, eps, n_local, p, ldx, 0, 1, packed, st, 0, want_scal)) != OEM_OK)
+    return s;
   if ((s = allreduce_sum(ctx, packed, psize + 2, st)) != OEM_OK) return s;
   if ((s = gram_unpack(ctx, packed, 1, p, Gw, xtwz, nullptr, st)) != OEM_OK) return s;
-  OEM_CUDA_TRY(cudaMemcpyAsync(scalars, packed + psize, 2 * sizeof(double), cudaMemcpyDeviceToDevice, st));
+  if (scalars)
+    OEM_CUDA_TRY(cudaMemcpyAsync(scalars, packed + psize, 2 * sizeof(double), cudaMemcpyDeviceToDevice, st));
   return OEM_OK;
 }
 

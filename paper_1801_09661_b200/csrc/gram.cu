@@ -100,6 +100,7 @@ struct GramParams {
   const double* y;    // LDG fallback (odd K folds)
   const double* beta;
   double eps;
+  int want_scal;          // WEIGHTED: accumulate sum w and the log-likelihood (else zeros)
   double* partial;        // [nfold][nseg][nblk][64]
   double* partial_scal;   // WEIGHTED: [nseg][2]
   const CtaDesc* ctas;
@@ -161,13 +162,13 @@ __device__ __forceinline__ void consume(const GramParams& P, const Cons& cs) {
         double a[RR], b[CC];
 #pragma unroll
         for (int r = 0; r < R; ++r) a[r] = pak[8 * r];
-        if (MODE == MODE_WEIGHTED) {
+#pragma unroll
+        for (int c = 0; c < C; ++c) b[c] = pbk[8 * c];
+        if (MODE == MODE_WEIGHTED) {  // w_k scales row k (lane & 3) of the A fragments
           const double wk = ws[ks * 4 + (lane & 3)];
 #pragma unroll
           for (int r = 0; r < R; ++r) a[r] *= wk;
         }
-#pragma unroll
-        for (int c = 0; c < C; ++c) b[c] = pbk[8 * c];
 #pragma unroll
         for (int r = 0; r < R; ++r)
 #pragma unroll
@@ -239,9 +240,10 @@ __device__ __forceinline__ void weighted_rows(const GramParams& P, const Cons& c
     const int64_t row = cs.r0 + (int64_t)s * BK + k;
     const bool valid = row < cs.r1;
     const double yk = ys[k];
-    double w = 0.0, z = 0.0;
+    double w = 0.0, z = 0.0, ex = 0.0;
     if (valid) {
-      double mu = 1.0 / (1.0 + exp(-e));
+      ex = exp(-e);
+      double mu = 1.0 / (1.0 + ex);
       mu = fmin(fmax(mu, P.eps), 1.0 - P.eps);
       w = mu * (1.0 - mu);
       z = e + (yk - mu) / w;
@@ -257,10 +259,13 @@ __device__ __forceinline__ void weighted_rows(const GramParams& P, const Cons& c
       mbar_arrive(&cs.empty[st]);
     }
     // off the critical path (the MMA warps already have the stage): sum w and the
-    // log-likelihood, needed once per segment (CTA type 0 writes them)
-    if (cs.u == 0 && valid && sub == 0) {
+    // log-likelihood, once per segment (CTA type 0 writes them), only when the caller asked:
+    // the row warps' scalar fp64 work shares the sub-partitions with the DMMA warps (measured:
+    // 0.5 ms of an 8.7 ms cfg5 pass). log(1 + e^eta) = eta + log1p(e^-eta) reuses ex; when ex
+    // overflows (eta < -709) the term is e^eta = 0 to double precision.
+    if (P.want_scal && cs.u == 0 && valid && sub == 0) {
       sw += w;
-      sll += yk * e - (e > 0.0 ? e + log1p(exp(-e)) : log1p(exp(e)));
+      sll += yk * e - (isinf(ex) ? 0.0 : e + log1p(ex));
     }
     if (++st == P.ST) { st = 0; ph ^= 1u; }
   }
@@ -765,7 +770,7 @@ static oem_status launch_t(const GramPlan& pl, const CUtensorMap& mx, const CUte
 
 oem_status gram_pass(oem_ctx* ctx, int mode, const double* X, const double* y, const double* beta, double eps,
                      int64_t n_local, int p, int64_t ldx, int64_t row_offset, int K, double* packed, cudaStream_t st,
-                     int accumulate) {
+                     int accumulate, int want_scal) {
   const int nfold = mode == MODE_FOLD ? K : 1;
   const int64_t psize = packed_size(p);
   const int64_t nq = mode == MODE_FOLD ? n_local / K : n_local;
@@ -828,7 +833,7 @@ oem_status gram_pass(oem_ctx* ctx, int mode, const double* X, const double* y, c
     P.nblk = pl.nblk; P.nrows = nq; P.seg_rows = pl.seg_rows; P.K = K;
     P.off_mod = mode == MODE_FOLD ? (int)(((row_offset % K) + K) % K) : 0;
     P.ytma = pl.ytma; P.ystride = pl.ystride;
-    P.y = y; P.beta = beta; P.eps = eps;
+    P.y = y; P.beta = beta; P.eps = eps; P.want_scal = want_scal;
     P.partial = ctx->partial.as<double>();
     P.partial_scal = ctx->partial_scal.as<double>();
     P.ctas = pl.d_ctas; P.blk_of = pl.d_blk_of;

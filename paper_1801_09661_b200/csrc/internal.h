@@ -103,7 +103,7 @@ enum GramMode { MODE_PLAIN = 0, MODE_FOLD = 1, MODE_WEIGHTED = 2 };
 // packed: nfold * psize (+2 scalars for MODE_WEIGHTED), psize = (p+1)(p+2)/2.
 oem_status gram_pass(oem_ctx* ctx, int mode, const double* X, const double* y, const double* beta, double eps,
                      int64_t n_local, int p, int64_t ldx, int64_t row_offset, int K, double* packed,
-                     cudaStream_t st, int accumulate = 0);
+                     cudaStream_t st, int accumulate = 0, int want_scal = 1);
 // packed (nfold blocks) -> full symmetric G (nfold*p*p), xty (nfold*p), yty (nfold)
 oem_status gram_unpack(oem_ctx* ctx, const double* packed, int nfold, int p, double* G, double* xty, double* yty, cudaStream_t st);
 inline int64_t packed_size(int p) { return (int64_t)(p + 1) * (p + 2) / 2; }

@@ -110,7 +110,7 @@ extern "C" oem_status oem_fit_logistic(oem_ctx* ctx, const double* X, const doub
     if (s != OEM_OK) return s;
   } else {
     // a4 at beta = 0: gives lambda_max (R#14) and the first outer step's weighted Gram
-    s = oem_gram_weighted(ctx, X, y01, beta, n_local, p, ldx, cfg.eps, Gw, cw, sc, stream);
+    s = oem_gram_weighted(ctx, X, y01, beta, n_local, p, ldx, cfg.eps, Gw, cw, nullptr, stream);
     if (s != OEM_OK) return s;
   }
   std::vector<double> lam(L);
@@ -157,7 +157,7 @@ extern "C" oem_status oem_fit_logistic(oem_ctx* ctx, const double* X, const doub
         s = ub_rhs(ctx, Gw, beta, gb, p, cw, st);  // c = X^T X beta + 4 X^T (y - mu)
         if (s != OEM_OK) return s;
       } else if (!have_gram) {
-        s = oem_gram_weighted(ctx, X, y01, beta, n_local, p, ldx, cfg.eps, Gw, cw, sc, stream);
+        s = oem_gram_weighted(ctx, X, y01, beta, n_local, p, ldx, cfg.eps, Gw, cw, nullptr, stream);
         if (s != OEM_OK) return s;
       }
       have_gram = false;

@@ -197,8 +197,10 @@ def oem_gram_folds(ctx: Context, X, y, K: int, row_offset: int = 0, stream=None)
     return G, xty, yty, list(counts)
 
 
-def oem_gram_weighted(ctx: Context, X, y01, beta, eps=1e-5, stream=None):
-    """a4: raw (G_w, X^T W z, [sum w, loglik]) for the proximal-Newton step."""
+def oem_gram_weighted(ctx: Context, X, y01, beta, eps=1e-5, stream=None, scalars=True):
+    """a4: raw (G_w, X^T W z, [sum w, loglik]) for the proximal-Newton step.
+
+    scalars=False skips the sum of w and the log-likelihood (third result None)."""
     _check_x(X, y01)
     n, p = X.shape
     dev = X.device
@@ -207,7 +209,7 @@ def oem_gram_weighted(ctx: Context, X, y01, beta, eps=1e-5, stream=None):
     beta = beta.contiguous()
     Gw = torch.empty((p, p), dtype=torch.float64, device=dev)
     cw = torch.empty(p, dtype=torch.float64, device=dev)
-    sc = torch.empty(2, dtype=torch.float64, device=dev)
+    sc = torch.empty(2, dtype=torch.float64, device=dev) if scalars else None
     _check(lib().oem_gram_weighted(ctx.h, _ptr(X), _ptr(y01), _ptr(beta), n, p, X.stride(0), eps,
                                    _ptr(Gw), _ptr(cw), _ptr(sc), _stream(stream)))
     return Gw, cw, sc

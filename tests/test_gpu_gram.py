@@ -287,6 +287,35 @@ def test_weighted_parity(ctx, n, p):
     assert abs(float(sc[1]) - sco[1]) <= 1e-12 * abs(sco[1])
 
 
+def test_weighted_extreme_eta_and_no_scalars(ctx):
+    """eta spanning [-800, 800] (exp(-eta) overflows below -709, mu clamps at both ends) against
+    the oracle; then scalars=False must give bit-identical G_w and X^T W z (the flag only drops
+    the sum of w and the log-likelihood)."""
+    from paper_1801_09661_b200 import oem_gram_weighted
+    rng = np.random.default_rng(17)
+    n, p = 4099, 24
+    X = rng.standard_normal((n, p))
+    X[:, 0] = np.linspace(-1.0, 1.0, n)          # eta = 800 x_0 + small terms
+    y = (rng.random(n) < 0.5).astype(float)
+    beta = np.zeros(p)
+    beta[0] = 800.0
+    beta[1:4] = [0.3, -0.2, 0.1]
+    Xd, yd, bd = to_dev(X), to_dev(y), to_dev(beta)
+    Gw, cw, sc = oem_gram_weighted(ctx, Xd, yd, bd)
+    Go, co, sco = orc.gram_weighted(X, y, beta)
+    assert scale_err(Gw.cpu().numpy(), Go) <= 1e-12
+    eta = X @ beta
+    mu = np.clip(1 / (1 + np.exp(-eta)), 1e-5, 1 - 1e-5)
+    w = mu * (1 - mu)
+    szz = np.sum(w * (eta + (y - mu) / w) ** 2)
+    assert np.max(np.abs(cw.cpu().numpy() - co) / np.sqrt(np.diag(Go) * szz)) <= 1e-12
+    assert abs(float(sc[0]) - sco[0]) <= 1e-12 * sco[0]
+    assert abs(float(sc[1]) - sco[1]) <= 1e-12 * abs(sco[1])
+    Gn, cn, sn = oem_gram_weighted(ctx, Xd, yd, bd, scalars=False)
+    assert sn is None
+    assert torch.equal(Gn, Gw) and torch.equal(cn, cw)
+
+
 def test_weighted_unsupported_large_p(ctx):
     from paper_1801_09661_b200 import OemError, oem_gram_weighted
     X = torch.zeros((10, 300), dtype=torch.float64, device="cuda")

@@ -29,6 +29,7 @@ def main():
     ap.add_argument("--reps", type=int, default=3)
     ap.add_argument("--nofit", action="store_true")
     ap.add_argument("--plain", action="store_true", help="plain Gram pass even for folds / logistic workloads")
+    ap.add_argument("--noscal", action="store_true", help="weighted pass without sum w / log-likelihood")
     a = ap.parse_args()
     cfg = CONFIGS[a.cfg]
     if a.n:
@@ -52,7 +53,8 @@ def main():
         elif cfg.folds:
             G, c, yy, cnt = oem_gram_folds(ctx, Xd, yd, cfg.folds)
         elif cfg.logistic:
-            G, c, sc = oem_gram_weighted(ctx, Xd, yd, torch.zeros(p, dtype=torch.float64, device="cuda"))
+            G, c, sc = oem_gram_weighted(ctx, Xd, yd, torch.zeros(p, dtype=torch.float64, device="cuda"),
+                                         scalars=not a.noscal)
             cnt = [n]
         else:
             G, c, yy, nn = oem_gram(ctx, Xd, yd)
