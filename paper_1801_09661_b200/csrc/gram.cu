@@ -664,9 +664,15 @@ static oem_status build_plan(oem_ctx* ctx, int mode, int p, int64_t nrows, int K
     }
   }
   pl.U = (int)pl.ctas.size();
-  if (!pl.two_panel || pl.U_off == 0) pl.U_off = pl.U;
-  if (const char* e = std::getenv("OEM_GRAM_NO_LPT"))  // developer override: one group, segment-major
-    if (e[0] == '1') pl.U_off = pl.U;
+  // Two-panel plans dispatch the costlier off-diagonal tiles first (U_off). The L2-friendly
+  // alternative - many short segments, segment-major, every tile of a segment dispatched together
+  // (OEM_GRAM_LPT=0 OEM_GRAM_WAVES=384) - cuts cfg4's DRAM reads from 350-404 GB to 98 GB
+  // (algorithmic 80 GB; L2 hit rate 44% -> 77%) at the same kernel time (288.3 ms) but adds 1 ms
+  // to the split-n reduction (6.4 GB of partial blocks): the kernel is DMMA-bound with HBM at
+  // ~19% of its peak, so the re-reads cost no time.
+  const char* lpt = std::getenv("OEM_GRAM_LPT");  // developer override (timing studies): 0 / 1
+  const bool use_lpt = lpt ? lpt[0] == '1' : true;
+  if (!pl.two_panel || pl.U_off == 0 || !use_lpt) pl.U_off = pl.U;
   // y staging: 1D TMA box (PLAIN/WEIGHTED); FOLD: 2D box [BK][Kpad] over y viewed as [nq][K]
   // (needs K*8 % 16 == 0, i.e. even K), else the producer's lanes load it
   if (mode == MODE_FOLD) {
@@ -695,7 +701,7 @@ static oem_status build_plan(oem_ctx* ctx, int mode, int p, int64_t nrows, int K
   const int per_sm = two_per_sm ? 2 : 1;
   // segments: as many (CTA type, segment) items as ~48 waves over the SMs (a short tail), but
   // at least 64 stages per segment (pipeline fill and the partial-block epilogue amortised);
-  // measured: cfg4 8 waves 294 ms -> 48 waves 288 ms; cfg2 prefers ~4 waves (0.42 -> 0.40 ms)
+  // measured: cfg4 8 waves 301 ms -> 48 waves 288 ms; cfg2 prefers ~4 waves (0.42 -> 0.40 ms)
   // (a whole number of waves, so the last one is not a mostly idle partial wave)
   const char* wv = std::getenv("OEM_GRAM_WAVES");  // developer override (timing studies)
   const double per_wave = (double)ctx->num_sms * per_sm / std::max(1, pl.U * nfold);  // segments per wave

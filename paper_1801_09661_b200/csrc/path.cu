@@ -817,6 +817,60 @@ __device__ __forceinline__ int vix(int q, int k, int pvl) {
   return NPT == 1 ? k : (q >> 1) * 2 * pvl + 2 * k + (q & 1);
 }
 
+// The matvec of one iteration, a[i*NPT + q] += sum_m G(i, m) b_q(tl + m T): the columns go in
+// chunks of four whose shared-memory loads are all issued before their FMAs (one load latency per
+// chunk instead of one per column; measured at cfg2, p = 100: the per-column form serialised 13
+// load latencies per iteration). Columns m >= kcu are skipped a chunk at a time: entries past p
+// are zero in the vector buffers and in the G tile, so the extra FMAs add exact zeros and each
+// accumulator sums in the same order as a column-by-column loop.
+template <int NPT, int RT, int KC, int T, int NV, int VP, class GEL>
+__device__ __forceinline__ void lean_matvec(double (&a)[VP], const double* vc, int pvl, int kcu, int tl, GEL gel) {
+  constexpr int MC = KC < 4 ? KC : 4;
+#pragma unroll
+  for (int m0 = 0; m0 < KC; m0 += MC) {
+    if (m0 >= kcu) break;
+    double b[MC][NV];
+#pragma unroll
+    for (int mm = 0; mm < MC; ++mm) {
+      const int k = tl + (m0 + mm) * T;
+      if (NPT == 1) {
+        b[mm][0] = vc[k];
+      } else {
+#pragma unroll
+        for (int h = 0; h < NV / 2; ++h) {
+          const double2 t2 = *reinterpret_cast<const double2*>(vc + h * 2 * pvl + 2 * k);
+          b[mm][2 * h] = t2.x;
+          b[mm][2 * h + 1] = t2.y;
+        }
+      }
+    }
+#pragma unroll
+    for (int mm = 0; mm < MC; ++mm)
+#pragma unroll
+      for (int i = 0; i < RT; ++i) {
+        const double gv = gel(i, m0 + mm);
+#pragma unroll
+        for (int q = 0; q < NPT; ++q) a[i * NPT + q] = fma(gv, b[mm][q], a[i * NPT + q]);
+      }
+  }
+}
+// the power iteration's matvec (one vector, penalty slot 0 of the layout: stride ST doubles)
+template <int RT, int KC, int T, int ST, int RP, class GEL>
+__device__ __forceinline__ void lean_matvec1(double (&a)[RP], const double* vc, int kcu, int tl, GEL gel) {
+  constexpr int MC = KC < 4 ? KC : 4;
+#pragma unroll
+  for (int m0 = 0; m0 < KC; m0 += MC) {
+    if (m0 >= kcu) break;
+    double b[MC];
+#pragma unroll
+    for (int mm = 0; mm < MC; ++mm) b[mm] = vc[ST * (tl + (m0 + mm) * T)];
+#pragma unroll
+    for (int mm = 0; mm < MC; ++mm)
+#pragma unroll
+      for (int i = 0; i < RT; ++i) a[i] = fma(gel(i, m0 + mm), b[mm], a[i]);
+  }
+}
+
 // RS > 0: each thread row group also owns RS rows kept in SHARED memory (for units whose rows do
 // not fit the register file, e.g. cfg3's eleven p = 500 Grams in clusters of 8). Thread (rg, tl)
 // owns local rows rg*RT + i, i < RT = R + RS: i < R from registers, i >= R from shared memory.
@@ -944,15 +998,7 @@ __global__ void __launch_bounds__(NTH, 1) fit_lean_kernel(const PathParams P, co
       double a[RP];
 #pragma unroll
       for (int i = 0; i < RP; ++i) a[i] = 0.0;
-      if (wrows) {
-#pragma unroll
-        for (int m = 0; m < KC; ++m) {
-          if (m >= kcu) break;
-          const double b = vc[vix<NPT>(0, tl + m * T, pvl)];
-#pragma unroll
-          for (int i = 0; i < RT; ++i) a[i] = fma(gel(i, m), b, a[i]);
-        }
-      }
+      if (wrows) lean_matvec1<RT, KC, T, NPT == 1 ? 1 : 2>(a, vc, kcu, tl, gel);
       const double s = lean_rs<RP, T>(a, tl);
       double part = 0.0;
       if (pact) {
@@ -1089,30 +1135,7 @@ __global__ void __launch_bounds__(NTH, 1) fit_lean_kernel(const PathParams P, co
     double a[VP];
 #pragma unroll
     for (int v = 0; v < VP; ++v) a[v] = 0.0;
-    if (wrows) {
-#pragma unroll
-      for (int m = 0; m < KC; ++m) {
-        if (m >= kcu) break;
-        const int k = tl + m * T;
-        double b[NV];
-        if (NPT == 1) {
-          b[0] = vc[k];
-        } else {
-#pragma unroll
-          for (int h = 0; h < NV / 2; ++h) {
-            const double2 t2 = *reinterpret_cast<const double2*>(vc + h * 2 * pvl + 2 * k);
-            b[2 * h] = t2.x;
-            b[2 * h + 1] = t2.y;
-          }
-        }
-#pragma unroll
-        for (int i = 0; i < RT; ++i) {
-          const double gv = gel(i, m);
-#pragma unroll
-          for (int q = 0; q < NPT; ++q) a[i * NPT + q] = fma(gv, b[q], a[i * NPT + q]);
-        }
-      }
-    }
+    if (wrows) lean_matvec<NPT, RT, KC, T, NV>(a, vc, pvl, kcu, tl, gel);
     lean_rs_gen<VP, T>(a, tl);
     uint32_t bits = 0;
 #pragma unroll
@@ -1388,15 +1411,7 @@ __global__ void __launch_bounds__(PT, 1) fit_glob_kernel(const PathParams P, con
       double a[RP];
 #pragma unroll
       for (int i = 0; i < RP; ++i) a[i] = 0.0;
-      if (wrows) {
-#pragma unroll
-        for (int m = 0; m < KC; ++m) {
-          if (m >= kcu) break;
-          const double b = vc[vix<NPT>(0, tl + m * T, pvl)];
-#pragma unroll
-          for (int i = 0; i < RT; ++i) a[i] = fma(gel(i, m), b, a[i]);
-        }
-      }
+      if (wrows) lean_matvec1<RT, KC, T, NPT == 1 ? 1 : 2>(a, vc, kcu, tl, gel);
       const double s = lean_rs<RP, T>(a, tl);
       double part = 0.0;
       if (pact) {
@@ -1517,30 +1532,7 @@ __global__ void __launch_bounds__(PT, 1) fit_glob_kernel(const PathParams P, con
     double a[VP];
 #pragma unroll
     for (int v = 0; v < VP; ++v) a[v] = 0.0;
-    if (wrows) {
-#pragma unroll
-      for (int m = 0; m < KC; ++m) {
-        if (m >= kcu) break;
-        const int k = tl + m * T;
-        double b[NV];
-        if (NPT == 1) {
-          b[0] = vc[k];
-        } else {
-#pragma unroll
-          for (int h = 0; h < NV / 2; ++h) {
-            const double2 t2 = *reinterpret_cast<const double2*>(vc + h * 2 * pvl + 2 * k);
-            b[2 * h] = t2.x;
-            b[2 * h + 1] = t2.y;
-          }
-        }
-#pragma unroll
-        for (int i = 0; i < RT; ++i) {
-          const double gv = gel(i, m);
-#pragma unroll
-          for (int q = 0; q < NPT; ++q) a[i * NPT + q] = fma(gv, b[q], a[i * NPT + q]);
-        }
-      }
-    }
+    if (wrows) lean_matvec<NPT, RT, KC, T, NV>(a, vc, pvl, kcu, tl, gel);
     const double s = lean_rs<VP, T>(a, tl);
     uint32_t bits = 0;
     if (act && ((qmask >> mq) & 1u)) {

@@ -1,7 +1,9 @@
 set -x
 mkdir -p gpurun_out
-timeout 900 python -m pytest tests/test_gpu_gram.py tests/test_gpu_logistic.py -m gpu -x -q > gpurun_out/w_tests.log 2>&1; echo tests=$?
-Q="timeout 300 python tools/quick_timing.py --cfg cfg5 --nofit --reps 3"
-$Q > gpurun_out/y_scal.log 2>&1; echo scal=$?
-$Q --noscal > gpurun_out/y_noscal.log 2>&1; echo noscal=$?
-timeout 600 python bench.py --workload cfg5 --no-cpu-baseline --e2e-steps 1 > gpurun_out/bench_cfg5.log 2>&1; echo bench5=$?
+for rep in 1 2; do
+for v in new head; do
+  if [ $v = head ]; then cp paper_1801_09661_b200/liboem.so /tmp/liboem_new.so; cp liboem_head.so paper_1801_09661_b200/liboem.so; fi
+  for w in cfg2 cfg3 cfg4; do timeout 600 python bench.py --workload $w --no-cpu-baseline --e2e-steps 0 --steps 3 > gpurun_out/v_${v}_${w}_$rep.log 2>&1; echo $v$w=$?; done
+  if [ $v = head ]; then cp /tmp/liboem_new.so paper_1801_09661_b200/liboem.so; fi
+done
+done
