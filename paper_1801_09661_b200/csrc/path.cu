@@ -2100,7 +2100,7 @@ static oem_status launch_cluster(const PathParams& P, const ClusterArgs& A, int 
 
 // ---------------------------------------------------------------- lean solver: host layout / launch
 struct LeanLayout {
-  int variant = -1;  // 0: R1 KC8 T8 (p <= 64), 1: R2 KC16 T8 (p <= 128), 2: R2 KC16 T16 (p <= 256)
+  int variant = -1;  // default: 7 (p <= 128), 9 (p <= 256), 5 (p <= 512); the rest via OEM_LEAN_VARIANT
   int C = 1, rows = 0, pvl = 0;
   size_t smem = 0;
   std::vector<int> cuts;  // C + 1 row cuts (group aligned)
@@ -2110,13 +2110,17 @@ static bool make_lean_layout(int p, int NPT, const std::vector<int>& gstart, Lea
   // variants: rows per CTA = R * 512 / T, columns = KC * T
   // variant 5: 32 register rows + 32 shared-memory rows per CTA (p <= 512, clusters of <= 8)
   // variant 6: 256 threads (8 warps, 4 rows per thread): less per-iteration overhead at p <= 128
-  static const int R_[7] = {1, 2, 2, 1, 1, 2, 4}, KC_[7] = {8, 16, 16, 8, 16, 16, 16},
-                   T_[7] = {8, 8, 16, 16, 16, 32, 8}, RS_[7] = {0, 0, 0, 0, 0, 2, 0},
-                   NTH_[7] = {PT, PT, PT, PT, PT, PT, 256};
-  int v = p <= 64 ? 0 : p <= 128 ? 1 : p <= 256 ? 2 : p <= 512 ? 5 : -1;
+  // variants 7, 8: four lanes per row (short reduce-scatter, 32-column FMA chains), 256 / 512 threads
+  // variant 9: 256 threads, 4 rows x 16 columns per thread (the 256-thread form of variant 2)
+  static const int R_[10] = {1, 2, 2, 1, 1, 2, 4, 2, 1, 4}, KC_[10] = {8, 16, 16, 8, 16, 16, 16, 32, 32, 16},
+                   T_[10] = {8, 8, 16, 16, 16, 32, 8, 4, 4, 16}, RS_[10] = {0, 0, 0, 0, 0, 2, 0, 0, 0, 0},
+                   NTH_[10] = {PT, PT, PT, PT, PT, PT, 256, 256, PT, 256};
+  // measured (path phase, one B200): p = 20 variant 0 0.83 -> 7 0.76 us/iteration; p = 100
+  // (cfg2) 1 1.01 -> 7 0.88; p = 200 (cfg5 inner solves) 2 96.7 ms -> 9 83.2 ms
+  int v = p <= 128 ? 7 : p <= 256 ? 9 : p <= 512 ? 5 : -1;
   if (const char* ev = std::getenv("OEM_LEAN_VARIANT")) {  // developer override (timing studies)
     const int f = std::atoi(ev);
-    if (f >= 0 && f < 7 && KC_[f] * T_[f] >= p) v = f;
+    if (f >= 0 && f < 10 && KC_[f] * T_[f] >= p) v = f;
   }
   if (v < 0 || NPT > 4) return false;
   const int rows = (R_[v] + RS_[v]) * (NTH_[v] / T_[v]);
@@ -2195,13 +2199,13 @@ static oem_status launch_lean_t5(const PathParams& P, const LeanArgs& A, int nU,
   return OEM_OK;
 }
 
-template <int NPT>
-static oem_status launch_lean_t6(const PathParams& P, const LeanArgs& A, int nU, size_t smem, cudaStream_t st) {
-  auto kern = fit_lean_kernel<NPT, 4, 16, 8, 0, 256>;
+template <int NPT, int R, int KC, int T, int NTH>
+static oem_status launch_lean_nth(const PathParams& P, const LeanArgs& A, int nU, size_t smem, cudaStream_t st) {
+  auto kern = fit_lean_kernel<NPT, R, KC, T, 0, NTH>;
   OEM_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3((unsigned)(nU * A.C));
-  cfg.blockDim = dim3(256);
+  cfg.blockDim = dim3(NTH);
   cfg.dynamicSmemBytes = smem;
   cfg.stream = st;
   cudaLaunchAttribute attr[1];
@@ -2222,7 +2226,10 @@ static oem_status launch_lean_v(const PathParams& P, const LeanArgs& A, int nU, 
   if (lo.variant == 3) return launch_lean_t<NPT, 1, 8, 16>(P, A, nU, lo.smem, st);
   if (lo.variant == 4) return launch_lean_t<NPT, 1, 16, 16>(P, A, nU, lo.smem, st);
   if (lo.variant == 5) return launch_lean_t5<NPT>(P, A, nU, lo.smem, st);
-  if (lo.variant == 6) return launch_lean_t6<NPT>(P, A, nU, lo.smem, st);
+  if (lo.variant == 6) return launch_lean_nth<NPT, 4, 16, 8, 256>(P, A, nU, lo.smem, st);
+  if (lo.variant == 7) return launch_lean_nth<NPT, 2, 32, 4, 256>(P, A, nU, lo.smem, st);
+  if (lo.variant == 8) return launch_lean_nth<NPT, 1, 32, 4, PT>(P, A, nU, lo.smem, st);
+  if (lo.variant == 9) return launch_lean_nth<NPT, 4, 16, 16, 256>(P, A, nU, lo.smem, st);
   return launch_lean_t<NPT, 2, 16, 16>(P, A, nU, lo.smem, st);
 }
 

@@ -231,6 +231,30 @@ def test_gram_folds_integer_bit_exact(ctx, p, K, n, off):
     assert np.array_equal(yyk.cpu().numpy(), yyo)
 
 
+@pytest.mark.parametrize("lpt,waves", [("0", "384"), ("0", "1"), ("1", "384"), ("1", "3")])
+def test_gram_schedule_overrides_bit_exact(monkeypatch, lpt, waves):
+    """The work-item schedule overrides (OEM_GRAM_LPT, OEM_GRAM_WAVES; the L2-traffic study in
+    profiles/cfg4_l2_schedule_r01.md) change only the order of the split-n sums: two-panel plain
+    and fold passes on integer designs stay bit-exact against the oracle."""
+    from paper_1801_09661_b200 import Context, oem_gram, oem_gram_folds
+    monkeypatch.setenv("OEM_GRAM_LPT", lpt)
+    monkeypatch.setenv("OEM_GRAM_WAVES", waves)
+    c = Context(0)  # plans are cached per context: a fresh one reads the overrides
+    try:
+        p, n = 300, 8000 + 19
+        X, y = int_design(41, n, p)
+        Xd = to_dev(X)
+        G, cc, yy, nt = oem_gram(c, Xd, to_dev(y))
+        Go, co, yyo = orc.gram(X, y)
+        assert np.array_equal(G.cpu().numpy(), Go) and np.array_equal(cc.cpu().numpy(), co) and float(yy) == yyo
+        Gk, ck, yyk, cnt = oem_gram_folds(c, Xd, to_dev(y), 4, row_offset=1)
+        Gf, cf, yyf, cntf = orc.gram_folds(X, y, 4, row_offset=1)
+        assert list(cnt) == list(cntf)
+        assert np.array_equal(Gk.cpu().numpy(), Gf) and np.array_equal(ck.cpu().numpy(), cf)
+    finally:
+        c.close()
+
+
 def test_gram_folds_cfg3_parity(ctx):
     from paper_1801_09661_b200 import oem_gram_folds
     cfg = CONFIGS["cfg3"].with_n(10_013)
