@@ -2100,7 +2100,7 @@ static oem_status launch_cluster(const PathParams& P, const ClusterArgs& A, int 
 
 // ---------------------------------------------------------------- lean solver: host layout / launch
 struct LeanLayout {
-  int variant = -1;  // default: 7 (p <= 128), 9 (p <= 256), 5 (p <= 512); the rest via OEM_LEAN_VARIANT
+  int variant = -1;  // default: 7 (p <= 128), 9 (p <= 256), 10 (p <= 512); the rest via OEM_LEAN_VARIANT
   int C = 1, rows = 0, pvl = 0;
   size_t smem = 0;
   std::vector<int> cuts;  // C + 1 row cuts (group aligned)
@@ -2112,15 +2112,18 @@ static bool make_lean_layout(int p, int NPT, const std::vector<int>& gstart, Lea
   // variant 6: 256 threads (8 warps, 4 rows per thread): less per-iteration overhead at p <= 128
   // variants 7, 8: four lanes per row (short reduce-scatter, 32-column FMA chains), 256 / 512 threads
   // variant 9: 256 threads, 4 rows x 16 columns per thread (the 256-thread form of variant 2)
-  static const int R_[10] = {1, 2, 2, 1, 1, 2, 4, 2, 1, 4}, KC_[10] = {8, 16, 16, 8, 16, 16, 16, 32, 32, 16},
-                   T_[10] = {8, 8, 16, 16, 16, 32, 8, 4, 4, 16}, RS_[10] = {0, 0, 0, 0, 0, 2, 0, 0, 0, 0},
-                   NTH_[10] = {PT, PT, PT, PT, PT, PT, 256, 256, PT, 256};
+  // variant 10: 256 threads, 4 register + 4 shared-memory rows per thread (the 256-thread form of 5)
+  static const int R_[11] = {1, 2, 2, 1, 1, 2, 4, 2, 1, 4, 4},
+                   KC_[11] = {8, 16, 16, 8, 16, 16, 16, 32, 32, 16, 16},
+                   T_[11] = {8, 8, 16, 16, 16, 32, 8, 4, 4, 16, 32}, RS_[11] = {0, 0, 0, 0, 0, 2, 0, 0, 0, 0, 4},
+                   NTH_[11] = {PT, PT, PT, PT, PT, PT, 256, 256, PT, 256, 256};
   // measured (path phase, one B200): p = 20 variant 0 0.83 -> 7 0.76 us/iteration; p = 100
-  // (cfg2) 1 1.01 -> 7 0.88; p = 200 (cfg5 inner solves) 2 96.7 ms -> 9 83.2 ms
-  int v = p <= 128 ? 7 : p <= 256 ? 9 : p <= 512 ? 5 : -1;
+  // (cfg2) 1 1.01 -> 7 0.88; p = 200 (cfg5 inner solves) 2 96.7 ms -> 9 83.2 ms; p = 500 (cfg3)
+  // 5 2.49 -> 10 2.18 us/iteration
+  int v = p <= 128 ? 7 : p <= 256 ? 9 : p <= 512 ? 10 : -1;
   if (const char* ev = std::getenv("OEM_LEAN_VARIANT")) {  // developer override (timing studies)
     const int f = std::atoi(ev);
-    if (f >= 0 && f < 10 && KC_[f] * T_[f] >= p) v = f;
+    if (f >= 0 && f < 11 && KC_[f] * T_[f] >= p) v = f;
   }
   if (v < 0 || NPT > 4) return false;
   const int rows = (R_[v] + RS_[v]) * (NTH_[v] / T_[v]);
@@ -2199,9 +2202,9 @@ static oem_status launch_lean_t5(const PathParams& P, const LeanArgs& A, int nU,
   return OEM_OK;
 }
 
-template <int NPT, int R, int KC, int T, int NTH>
+template <int NPT, int R, int KC, int T, int NTH, int RS = 0>
 static oem_status launch_lean_nth(const PathParams& P, const LeanArgs& A, int nU, size_t smem, cudaStream_t st) {
-  auto kern = fit_lean_kernel<NPT, R, KC, T, 0, NTH>;
+  auto kern = fit_lean_kernel<NPT, R, KC, T, RS, NTH>;
   OEM_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3((unsigned)(nU * A.C));
@@ -2230,6 +2233,7 @@ static oem_status launch_lean_v(const PathParams& P, const LeanArgs& A, int nU, 
   if (lo.variant == 7) return launch_lean_nth<NPT, 2, 32, 4, 256>(P, A, nU, lo.smem, st);
   if (lo.variant == 8) return launch_lean_nth<NPT, 1, 32, 4, PT>(P, A, nU, lo.smem, st);
   if (lo.variant == 9) return launch_lean_nth<NPT, 4, 16, 16, 256>(P, A, nU, lo.smem, st);
+  if (lo.variant == 10) return launch_lean_nth<NPT, 4, 16, 32, 256, 4>(P, A, nU, lo.smem, st);
   return launch_lean_t<NPT, 2, 16, 16>(P, A, nU, lo.smem, st);
 }
 
