@@ -1251,10 +1251,10 @@ __device__ __forceinline__ unsigned long long ld_relaxed_u64(const unsigned long
   return v;
 }
 
-template <int NPT, int R, int KC, int T, int RS = 0>
-__global__ void __launch_bounds__(PT, 1) fit_glob_kernel(const PathParams P, const GlobArgs A) {
+template <int NPT, int R, int KC, int T, int RS = 0, int NTH = PT>
+__global__ void __launch_bounds__(NTH, 1) fit_glob_kernel(const PathParams P, const GlobArgs A) {
   constexpr int RT = R + RS;  // rows per thread row group: R in registers, RS in shared memory
-  constexpr int RG = PT / T, V = RT * NPT, VP = pow2ceil(V), NW = PT / 32;
+  constexpr int RG = NTH / T, V = RT * NPT, VP = pow2ceil(V), NW = NTH / 32;
   constexpr int NV = NPT == 1 ? 1 : 2 * ((NPT + 1) / 2);
   static_assert(VP <= T && (T & (T - 1)) == 0 && T <= 32, "lean layout");
   extern __shared__ __align__(16) double sm[];
@@ -1303,12 +1303,12 @@ __global__ void __launch_bounds__(PT, 1) fit_glob_kernel(const PathParams P, con
   const bool grp = P.g_of != nullptr;
   const int g0 = (grp && nr > 0) ? P.g_of[j0] : 0;
   const int ng_loc = (grp && nr > 0) ? P.g_of[j1 - 1] + 1 - g0 : 0;
-  for (int gg = tid; gg < ng_loc; gg += PT) {
+  for (int gg = tid; gg < ng_loc; gg += NTH) {
     gw_s[gg] = P.g_w[g0 + gg];
     ga_s[gg] = P.g_start[g0 + gg] - j0;
     gb_s[gg] = P.g_end[g0 + gg] - j0;
   }
-  for (int k = tid; k < 2 * vstride; k += PT) vec[k] = 0.0;
+  for (int k = tid; k < 2 * vstride; k += NTH) vec[k] = 0.0;
   double g[R][KC];
 #pragma unroll
   for (int i = 0; i < R; ++i)
@@ -1402,7 +1402,7 @@ __global__ void __launch_bounds__(PT, 1) fit_glob_kernel(const PathParams P, con
     const double gersh = unit_reduce(s_tot, par, true);
     par ^= 1;
     const double v0 = 1.0 / sqrt((double)p);
-    for (int k = tid; k < p; k += PT) vec[vix<NPT>(0, k, pvl)] = v0;
+    for (int k = tid; k < p; k += NTH) vec[vix<NPT>(0, k, pvl)] = v0;
     __syncthreads();
     double sc = 1.0, rq = 0.0;
     for (int it = 0; it <= A.power_iters; ++it) {
@@ -1427,7 +1427,7 @@ __global__ void __launch_bounds__(PT, 1) fit_glob_kernel(const PathParams P, con
       const double tot = unit_reduce(cta_sum(part), par, false);
       par ^= 1;
       if (it < A.power_iters) {
-        for (int k = tid; k < p; k += PT) vec[(size_t)nxt * vstride + vix<NPT>(0, k, pvl)] = __ldcg(&gvec[nxt * gpar + vix<NPT>(0, k, pvl)]);
+        for (int k = tid; k < p; k += NTH) vec[(size_t)nxt * vstride + vix<NPT>(0, k, pvl)] = __ldcg(&gvec[nxt * gpar + vix<NPT>(0, k, pvl)]);
         __syncthreads();
         if (tot > 0.0) sc = 1.0 / sqrt(tot);
       } else {
@@ -1438,7 +1438,7 @@ __global__ void __launch_bounds__(PT, 1) fit_glob_kernel(const PathParams P, con
     d = gersh < dd ? gersh : dd;
     if (rank == 0 && tid == 0) A.d_out[unit] = d;
     __syncthreads();
-    for (int k = tid; k < 2 * vstride; k += PT) vec[k] = 0.0;
+    for (int k = tid; k < 2 * vstride; k += NTH) vec[k] = 0.0;
   } else {
     d = P.d[unit];
   }
@@ -1489,7 +1489,7 @@ __global__ void __launch_bounds__(PT, 1) fit_glob_kernel(const PathParams P, con
     }
   }
   if (P.beta_init)
-    for (int e = tid; e < nP * p; e += PT) {
+    for (int e = tid; e < nP * p; e += NTH) {
       const int q = e / p, k = e % p;
       vec[vix<NPT>(q, k, pvl)] = P.beta_init[((size_t)unit * nPg + q + qoff) * p + P.perm[k]];
     }
@@ -1501,7 +1501,7 @@ __global__ void __launch_bounds__(PT, 1) fit_glob_kernel(const PathParams P, con
     return s_lmax[q] * exp(((double)l / (double)(L - 1)) * log(P.lmin_ratio));  // R#15
   };
   if (rank == 0)
-    for (int e = tid; e < nP * L; e += PT) {
+    for (int e = tid; e < nP * L; e += NTH) {
       const int q = e / L, l = e % L;
       P.lam_out[((size_t)unit * nPg + q + qoff) * L + l] = lam_at(q, l);
     }
@@ -1578,31 +1578,32 @@ __global__ void __launch_bounds__(PT, 1) fit_glob_kernel(const PathParams P, con
     }
     unit_sync();
     // the unit's new vector and flags, from L2: every load issued before any is used (one L2
-    // round trip); 16-byte loads of penalty pairs (p <= 1024 = 2 PT in this kernel)
+    // round trip); 16-byte loads of penalty pairs (p <= 1024)
+    constexpr int NLD = (1024 + NTH - 1) / NTH;  // loads per thread covering p <= 1024
     if (NPT == 1) {
-      double tv[2];
+      double tv[NLD];
 #pragma unroll
-      for (int u = 0; u < 2; ++u) {
-        const int k = tid + u * PT;
+      for (int u = 0; u < NLD; ++u) {
+        const int k = tid + u * NTH;
         tv[u] = k < p ? __ldcg(&gn[k]) : 0.0;
       }
 #pragma unroll
-      for (int u = 0; u < 2; ++u)
-        if (tid + u * PT < p) vn[tid + u * PT] = tv[u];
+      for (int u = 0; u < NLD; ++u)
+        if (tid + u * NTH < p) vn[tid + u * NTH] = tv[u];
     } else {
-      double2 tv[NV / 2 > 0 ? NV / 2 : 1][2];
+      double2 tv[NV / 2 > 0 ? NV / 2 : 1][NLD];
 #pragma unroll
       for (int h = 0; h < NV / 2; ++h)
 #pragma unroll
-        for (int u = 0; u < 2; ++u) {
-          const int k = tid + u * PT;
+        for (int u = 0; u < NLD; ++u) {
+          const int k = tid + u * NTH;
           tv[h][u] = k < p ? __ldcg(reinterpret_cast<const double2*>(gn + h * 2 * pvl) + k) : make_double2(0.0, 0.0);
         }
 #pragma unroll
       for (int h = 0; h < NV / 2; ++h)
 #pragma unroll
-        for (int u = 0; u < 2; ++u)
-          if (tid + u * PT < p) reinterpret_cast<double2*>(vn + h * 2 * pvl)[tid + u * PT] = tv[h][u];
+        for (int u = 0; u < NLD; ++u)
+          if (tid + u * NTH < p) reinterpret_cast<double2*>(vn + h * 2 * pvl)[tid + u * NTH] = tv[h][u];
     }
     if (warp == 0) {
       uint32_t w = 0;
@@ -1624,7 +1625,7 @@ __global__ void __launch_bounds__(PT, 1) fit_glob_kernel(const PathParams P, con
       if (conv || it >= P.maxit) {
         const int l = lidx[q];
         double* out = P.beta_out + (((size_t)unit * nPg + q + qoff) * L + l) * p;
-        for (int r = tid; r < nr; r += PT) out[P.perm[j0 + r]] = vn[vix<NPT>(q, j0 + r, pvl)];
+        for (int r = tid; r < nr; r += NTH) out[P.perm[j0 + r]] = vn[vix<NPT>(q, j0 + r, pvl)];
         if (rank == 0 && tid == 0) {
           P.it_out[((size_t)unit * nPg + q + qoff) * L + l] = it;
           P.cv_out[((size_t)unit * nPg + q + qoff) * L + l] = conv ? 1 : 0;
@@ -2238,16 +2239,17 @@ static oem_status launch_lean_v(const PathParams& P, const LeanArgs& A, int nU, 
 }
 
 template <typename K>
-static oem_status coop_launch(K kern, int grid, size_t smem, cudaStream_t st, void** args) {
+static oem_status coop_launch(K kern, int grid, size_t smem, cudaStream_t st, void** args, int nth = PT) {
   OEM_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-  OEM_CUDA_TRY(cudaLaunchCooperativeKernel((const void*)kern, dim3(grid), dim3(PT), args, smem, st));
+  OEM_CUDA_TRY(cudaLaunchCooperativeKernel((const void*)kern, dim3(grid), dim3(nth), args, smem, st));
   return OEM_OK;
 }
 
 // ---------------------------------------------------------------- grid-wide lean solver: layout / launch
 struct GlobLayout {
   int variant = -1;  // 0: R1 KC32 T32 (16 rows / CTA, p <= 1024), 1: R2 KC16 T32 (32 rows, p <= 512),
-                     // 2: R1 RS1 KC32 T32 (16 register + 16 shared-memory rows, p <= 1024, split)
+                     // 2: R1 RS1 KC32 T32 (16 register + 16 shared-memory rows, p <= 1024, split),
+                     // 3: R2 RS2 KC32 T32 on 256 threads (the same 32 rows as 2)
   bool split = false;
   int nvu = 0;
   int C = 0, rows = 0, pvl = 0;
@@ -2255,12 +2257,13 @@ struct GlobLayout {
   std::vector<int> cuts;
 };
 
-template <int NPT, int R, int KC, int T, int RS = 0>
+template <int NPT, int R, int KC, int T, int RS = 0, int NTH = PT>
 static int glob_capacity(size_t smem, int num_sms) {
   int per = 0;
-  if (cudaFuncSetAttribute(fit_glob_kernel<NPT, R, KC, T, RS>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) !=
-          cudaSuccess ||
-      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, fit_glob_kernel<NPT, R, KC, T, RS>, PT, smem) != cudaSuccess)
+  if (cudaFuncSetAttribute(fit_glob_kernel<NPT, R, KC, T, RS, NTH>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                           (int)smem) != cudaSuccess ||
+      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, fit_glob_kernel<NPT, R, KC, T, RS, NTH>, NTH, smem) !=
+          cudaSuccess)
     return 0;
   return per * num_sms;
 }
@@ -2270,8 +2273,11 @@ static int glob_capacity(size_t smem, int num_sms) {
 static bool make_glob_layout(int nU, int p, int nP, const std::vector<int>& gstart, int num_sms, GlobLayout& lo,
                              bool split = false) {
   if (nP > 4 || p > 1024) return false;
-  const int v = p <= 512 ? 1 : split ? 2 : 0;
-  const int rows = v == 0 ? 16 : 32, pvl = v == 1 ? 16 * 32 : 32 * 32, rs = v == 2 ? 16 : 0;
+  // split, p > 512: the 256-thread layout (measured at cfg4: variant 2 4.66 -> 3 4.36 us/iteration)
+  int v = p <= 512 ? 1 : split ? 3 : 0;
+  if (const char* ev = std::getenv("OEM_GLOB_VARIANT"))  // developer override (timing studies)
+    if (split && p > 512 && std::atoi(ev) == 2) v = 2;
+  const int rows = v == 0 ? 16 : 32, pvl = v == 1 ? 16 * 32 : 32 * 32, rs = v == 2 || v == 3 ? 16 : 0;
   const int nvu = split ? nU * nP : nU, NPTe = split ? 1 : nP;
   std::vector<int> cuts{0};
   if (gstart.empty()) {
@@ -2298,7 +2304,9 @@ static bool make_glob_layout(int nU, int p, int nP, const std::vector<int>& gsta
   const size_t smem = ((size_t)2 * NV * pvl + (size_t)rs * pvl + (size_t)NPTe * rows + rows) * 8 +
                       (size_t)2 * rows * 4 + 16;
   int cap = 0;
-  if (v == 2) {
+  if (v == 3) {
+    cap = glob_capacity<1, 2, 32, 32, 2, 256>(smem, num_sms);
+  } else if (v == 2) {
     cap = glob_capacity<1, 1, 32, 32, 1>(smem, num_sms);
   } else if (v == 0) {
     cap = NPTe == 1 ? glob_capacity<1, 1, 32, 32>(smem, num_sms) : NPTe == 2 ? glob_capacity<2, 1, 32, 32>(smem, num_sms)
@@ -2324,6 +2332,7 @@ static oem_status launch_glob_v(const PathParams& P, const GlobArgs& A, int grid
   void* args[] = {const_cast<PathParams*>(&P), const_cast<GlobArgs*>(&A)};
   if (lo.variant == 0) return coop_launch(fit_glob_kernel<NPT, 1, 32, 32>, grid, lo.smem, st, args);
   if (lo.variant == 2) return coop_launch(fit_glob_kernel<1, 1, 32, 32, 1>, grid, lo.smem, st, args);
+  if (lo.variant == 3) return coop_launch(fit_glob_kernel<1, 2, 32, 32, 2, 256>, grid, lo.smem, st, args, 256);
   return coop_launch(fit_glob_kernel<NPT, 2, 16, 32>, grid, lo.smem, st, args);
 }
 

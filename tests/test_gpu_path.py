@@ -327,3 +327,28 @@ def test_solver_variant_boundaries(ctx, p):
         for q, (fam, gamma, alpha) in enumerate(pens):
             B, it, cv = orc.oem_path(Go / nn, co / nn, d, fam, fit.lam[u, q].cpu().numpy(), gamma, alpha)
             assert np.max(np.abs(fit.beta[u, q].cpu().numpy() - B)) <= TOL_BETA, (p, u, fam)
+
+
+@pytest.mark.parametrize("p", [100, 200, 300, 512])
+def test_batched_penalties_every_lean_layout(ctx, p, monkeypatch):
+    """Four penalties multiplied together in one CTA (NPT = 4, the layout used when the per-penalty
+    split does not fit the SMs) in each lean layout (2x32 / 4x16 / 4+4 shared-memory rows per
+    thread), two units, against the oracle."""
+    from paper_1801_09661_b200 import oem_fit_path, oem_gram
+    monkeypatch.setenv("OEM_PATH_SOLVER", "batched")
+    spec = CONFIGS["cfg2"].spec.replace(n=2000 + 3 * p, p=p, nnz=min(8, p))
+    bt = dg.beta(spec)
+    X, y = dg.rows_host(spec, bt)
+    Xd = torch.from_numpy(X).cuda()
+    yd = torch.from_numpy(y).cuda()
+    h = (X.shape[0] // 2) & ~1
+    G0, c0, _, n0 = oem_gram(ctx, Xd[:h], yd[:h])
+    G1, c1, _, n1 = oem_gram(ctx, Xd[h:], yd[h:])
+    pens = [("lasso", 0.0, 1.0), ("mcp", 3.0, 1.0), ("scad", 3.7, 1.0), ("enet", 0.0, 0.5)]
+    fit = oem_fit_path(ctx, torch.stack([G0, G1]), torch.stack([c0, c1]), [n0, n1], pens, nlambda=8)
+    for u, (lo, hi, nn) in enumerate([(0, h, n0), (h, X.shape[0], n1)]):
+        Go, co, _ = orc.gram(X[lo:hi], y[lo:hi])
+        d = float(fit.d[u])
+        for q, (fam, gamma, alpha) in enumerate(pens):
+            B, it, cv = orc.oem_path(Go / nn, co / nn, d, fam, fit.lam[u, q].cpu().numpy(), gamma, alpha)
+            assert np.max(np.abs(fit.beta[u, q].cpu().numpy() - B)) <= TOL_BETA, (p, u, fam)
