@@ -688,23 +688,19 @@ static oem_status build_plan(oem_ctx* ctx, int mode, int p, int64_t nrows, int K
   pl.stage_doubles = pl.ys_off + BK * pl.ystride + (mode == MODE_WEIGHTED ? BK : 0);
   pl.stage_doubles = (pl.stage_doubles + 15) / 16 * 16;  // 128-byte aligned stages
   const size_t fixed = (mode == MODE_WEIGHTED ? pl.ld * 8 : 0) + 2 * MAXST * 8;
-  // two CTAs per SM for single-panel plans when at least 3 stages fit in half the SM
-  const size_t half = 110 * 1024, whole = 220 * 1024;
-  (void)half;
-  const bool two_per_sm = false;  // one CTA per SM (16 MMA warps for single-panel plans)
+  // one CTA per SM (16 MMA warps for single-panel plans, 8 for two-panel ones): stages fill 220 KB
+  const size_t whole = 220 * 1024;
   pl.ST = (int)std::min<size_t>(pl.two_panel ? 4 : MAXST, (whole - fixed) / ((size_t)pl.stage_doubles * 8));
   if (pl.ST < 2) OEM_FAIL(OEM_ERR_UNSUPPORTED, "gram: stage does not fit shared memory");
   pl.smem = (size_t)pl.ST * pl.stage_doubles * 8 + fixed;
-  // segments: enough (CTA type, segment) items for ~8 waves over the SMs (short tail)
   const int64_t units = std::max<int64_t>(1, (nrows + BK - 1) / BK);
   const int nfold = mode == MODE_FOLD ? K : 1;
-  const int per_sm = two_per_sm ? 2 : 1;
   // segments: as many (CTA type, segment) items as ~48 waves over the SMs (a short tail), but
   // at least 64 stages per segment (pipeline fill and the partial-block epilogue amortised);
   // measured: cfg4 8 waves 301 ms -> 48 waves 288 ms; cfg2 prefers ~4 waves (0.42 -> 0.40 ms)
   // (a whole number of waves, so the last one is not a mostly idle partial wave)
   const char* wv = std::getenv("OEM_GRAM_WAVES");  // developer override (timing studies)
-  const double per_wave = (double)ctx->num_sms * per_sm / std::max(1, pl.U * nfold);  // segments per wave
+  const double per_wave = (double)ctx->num_sms / std::max(1, pl.U * nfold);  // segments per wave
   const double w_fit = std::min(48.0, (double)units / 64.0 / per_wave);
   const int waves = wv ? std::max(1, std::atoi(wv)) : std::max(1, (int)std::ceil(w_fit));
   int64_t want = std::max<int64_t>(1, (int64_t)std::llround(waves * per_wave));
