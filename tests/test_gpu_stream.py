@@ -73,3 +73,27 @@ def test_gram_host_float_matches_in_core(ctx):
     G, c, yy, nt = oem_gram_host(ctx, Xh, yh, block_rows=1600)
     Go, co, yyo = orc.gram(X, y)
     assert scale_err(G.cpu().numpy(), Go) <= 1e-12
+
+
+def test_stream_edge_cases(ctx):
+    """n = 0 gives zero statistics; block_rows below the minimum (32) and a fold with no rows are
+    reported through the status codes, never as wrong numbers; blocks of exactly one row-tile."""
+    from paper_1801_09661_b200 import OemError, oem_gram_folds_host, oem_gram_host
+    p = 6
+    X0 = torch.zeros((0, p), dtype=torch.float64).pin_memory()
+    y0 = torch.zeros(0, dtype=torch.float64).pin_memory()
+    G, c, yy, nt = oem_gram_host(ctx, X0, y0, block_rows=64)
+    assert nt == 0 and not G.any() and not c.any() and float(yy) == 0.0
+    rng = np.random.default_rng(5)
+    X = rng.integers(-8, 9, size=(100, p)).astype(float)
+    y = rng.integers(-8, 9, size=100).astype(float)
+    Xh, yh = _pinned(X, y, p)
+    with pytest.raises(OemError) as e:
+        oem_gram_host(ctx, Xh, yh, block_rows=31)
+    assert e.value.status == "OEM_ERR_INVALID_ARG"
+    with pytest.raises(OemError) as e:   # K = 200 > n = 100 rows: folds 100..199 are empty
+        oem_gram_folds_host(ctx, Xh, yh, 200, block_rows=64)
+    assert e.value.status == "OEM_ERR_EMPTY_FOLD"
+    G, c, yy, nt = oem_gram_host(ctx, Xh, yh, block_rows=32)   # 4 blocks, the last one ragged
+    Go, co, yyo = orc.gram(X, y)
+    assert nt == 100 and np.array_equal(G.cpu().numpy(), Go) and np.array_equal(c.cpu().numpy(), co)
