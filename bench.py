@@ -165,7 +165,9 @@ def run_reference(args, cfg):
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * sum(times) / len(times),
             "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
             "data": "synthetic (seeded Philox generator, DESIGN.md §4)",
-            "config": {"workload": cfg.name, "n": cfg.n, "p": cfg.p, "sample_rows": rows},
+            "config": {"workload": cfg.name, "n": cfg.n, "p": cfg.p, "penalties": [f for f, _, _ in cfg.penalties],
+                       "nlambda": cfg.nlambda, "folds": cfg.folds, "logistic": cfg.logistic,
+                       "parallelism": f"CPU oracle on {cores} host threads (no GPU)", "sample_rows": rows},
             "cpu_baseline": {"value": v, "unit": "TFLOP/s", "cores": cores, "kind": "oracle",
                              "sample": f"oracle Gram over rows 0..{rows} of {cfg.name} per step"},
             "e2e": {"value": v, "unit": "TFLOP/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
