@@ -695,13 +695,16 @@ static oem_status build_plan(oem_ctx* ctx, int mode, int p, int64_t nrows, int K
   pl.smem = (size_t)pl.ST * pl.stage_doubles * 8 + fixed;
   const int64_t units = std::max<int64_t>(1, (nrows + BK - 1) / BK);
   const int nfold = mode == MODE_FOLD ? K : 1;
-  // segments: as many (CTA type, segment) items as ~48 waves over the SMs (a short tail), but
-  // at least 64 stages per segment (pipeline fill and the partial-block epilogue amortised);
-  // measured: cfg4 8 waves 301 ms -> 48 waves 288 ms; cfg2 prefers ~4 waves (0.42 -> 0.40 ms)
-  // (a whole number of waves, so the last one is not a mostly idle partial wave)
+  // segments: as many (CTA type, segment) items as a few whole waves over the SMs (below), but at
+  // least 64 stages per segment (pipeline fill and the partial-block epilogue amortised; a whole
+  // number of waves, so the last one is not a mostly idle partial wave)
   const char* wv = std::getenv("OEM_GRAM_WAVES");  // developer override (timing studies)
   const double per_wave = (double)ctx->num_sms / std::max(1, pl.U * nfold);  // segments per wave
-  const double w_fit = std::min(48.0, (double)units / 64.0 / per_wave);
+  // single-panel plans (CTA types of equal cost) run best in very few waves: fewer segments, a
+  // smaller split-n reduction, fewer pipeline fills. Measured (whole call): cfg2 4 waves 0.396 ms,
+  // 2 waves 0.390, 1 wave 0.382; cfg5 weighted pass 33 waves 8.42 ms, 8 waves 8.19, 2 waves 8.16;
+  // two-panel plans need many waves to balance their unequal tiles (cfg4: 8 waves 301 ms, 48: 288)
+  const double w_fit = std::min(pl.two_panel ? 48.0 : 2.0, (double)units / 64.0 / per_wave);
   const int waves = wv ? std::max(1, std::atoi(wv)) : std::max(1, (int)std::ceil(w_fit));
   int64_t want = std::max<int64_t>(1, (int64_t)std::llround(waves * per_wave));
   want = std::min<int64_t>(want, std::max<int64_t>(1, units / 8));

@@ -1,6 +1,4 @@
 set -x
 mkdir -p gpurun_out
-timeout 240 python -m pytest tests/test_gpu_gram.py -m gpu -x -q -k "weighted" > gpurun_out/pr_tests.log 2>&1; echo tests=$?
-Q="timeout 200 python tools/quick_timing.py --cfg cfg5 --nofit --reps 5"
-$Q --noscal > gpurun_out/pr_pair.log 2>&1; echo pair=$?
-OEM_GRAM_WPAIR=0 $Q --noscal > gpurun_out/pr_nopair.log 2>&1; echo nopair=$?
+timeout 900 python -m pytest tests/test_gpu_gram.py tests/test_gpu_logistic.py tests/test_gpu_stream.py tests/test_gpu_poison.py -m gpu -x -q > gpurun_out/wf_tests.log 2>&1; echo tests=$?
+for w in cfg2 cfg5; do timeout 600 python bench.py --workload $w --no-cpu-baseline --e2e-steps 1 --steps 3 > gpurun_out/wf_$w.log 2>&1; echo b$w=$?; done
