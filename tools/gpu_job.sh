@@ -1,4 +1,4 @@
 set -x
 mkdir -p gpurun_out
-timeout 900 python -m pytest tests/test_gpu_gram.py tests/test_gpu_logistic.py tests/test_gpu_stream.py tests/test_gpu_poison.py -m gpu -x -q > gpurun_out/wf_tests.log 2>&1; echo tests=$?
-for w in cfg2 cfg5; do timeout 600 python bench.py --workload $w --no-cpu-baseline --e2e-steps 1 --steps 3 > gpurun_out/wf_$w.log 2>&1; echo b$w=$?; done
+timeout 300 python -m pytest tests/test_gpu_gram.py tests/test_gpu_logistic.py -m gpu -x -q -k "weighted or logistic or logit" > gpurun_out/sc_tests.log 2>&1; echo tests=$?
+for r in 1 2; do timeout 200 python tools/quick_timing.py --cfg cfg5 --nofit --reps 5 --noscal > gpurun_out/sc_time_$r.log 2>&1; done
