@@ -1,4 +1,4 @@
 set -x
 mkdir -p gpurun_out
-timeout 300 python -m pytest tests/test_gpu_gram.py tests/test_gpu_logistic.py -m gpu -x -q -k "weighted or logistic or logit" > gpurun_out/sc_tests.log 2>&1; echo tests=$?
-for r in 1 2; do timeout 200 python tools/quick_timing.py --cfg cfg5 --nofit --reps 5 --noscal > gpurun_out/sc_time_$r.log 2>&1; done
+for v in 3 4; do OEM_GLOB_VARIANT=$v timeout 600 python bench.py --workload cfg4 --no-cpu-baseline --e2e-steps 0 --steps 3 > gpurun_out/g4_$v.log 2>&1; echo v$v=$?; done
+OEM_GLOB_VARIANT=4 timeout 600 python -m pytest tests/test_gpu_path.py -m gpu -x -q -k "cfg4 or boundaries or mixed or sparse_group" > gpurun_out/g4_tests.log 2>&1; echo t=$?
