@@ -108,6 +108,28 @@ def test_cfg3_fold_mode(ctx):
         check_fit(fit, Gm[k], cm[k], n - cnto[k], cfg.penalties, L, unit=k + 1, lambdas=lam)
 
 
+def test_cfg3_full_size_cv_paths(ctx):
+    """cfg3 at full size in bench.py's launch configuration: the K = 10 fold Grams of all n = 1e7
+    rows (40 GB resident) in one pass, then the full-data fit and the 10 complement fits (fold
+    mode, 100 lambda, lasso) in one launch; every unit checked against the oracle's path solve on
+    the same statistics (the oracle forms the complements as sums of the other folds)."""
+    from paper_1801_09661_b200 import oem_fit_path, oem_gram_folds
+    cfg = CONFIGS["cfg3"]
+    bt = dg.beta(cfg.spec)
+    Xd, yd = device_rows(cfg.spec, bt)
+    Gk, ck, yyk, cnt = oem_gram_folds(ctx, Xd, yd, cfg.folds)
+    del Xd, yd
+    torch.cuda.empty_cache()
+    fit = oem_fit_path(ctx, Gk, ck, cnt, cfg.penalties, nlambda=cfg.nlambda, fold_mode=True)
+    Gf, cf = Gk.cpu().numpy(), ck.cpu().numpy()
+    Gm, cm = orc.fold_complements(Gf, cf)
+    n = int(sum(cnt))
+    lam = orc.lambda_grid(orc.lambda_max("lasso", cf.sum(0) / n), cfg.nlambda)
+    check_fit(fit, Gf.sum(0), cf.sum(0), n, cfg.penalties, cfg.nlambda, unit=0, lambdas=lam)
+    for k in range(cfg.folds):
+        check_fit(fit, Gm[k], cm[k], n - cnt[k], cfg.penalties, cfg.nlambda, unit=k + 1, lambdas=lam)
+
+
 def test_cfg4_group_lasso_and_enet(ctx):
     """cfg4 shape (p = 1000, 100 groups of 10, block-equicorrelated design): group lasso and
     EN(0.5) together, first 12 lambda of the 50-point grid (oracle time)."""
@@ -131,6 +153,36 @@ def test_cfg4_group_lasso_and_enet(ctx):
     one = oem_fit_path(ctx, G, c, [n], cfg.penalties[:1], lambdas=Ls[0], group=grp, ngroups=100,
                        d_in=[float(both.d[0])])
     assert torch.equal(both.beta[0, 0], one.beta[0, 0])
+
+
+def test_cfg4_full_size_paths(ctx):
+    """cfg4 at full size in bench.py's launch configuration: the Gram of all n = 1e7 rows (80 GB
+    resident), then both 50-lambda paths (group lasso, EN(0.5)) in one launch of the grid-wide
+    split solver, each checked against the oracle's path solve on the same Gram (host copy) at the
+    GPU's d: lambda grid, every beta, converged flags and iteration counts."""
+    from paper_1801_09661_b200 import oem_fit_path, oem_gram
+    cfg = CONFIGS["cfg4"]
+    bt = dg.beta(cfg.spec)
+    Xd, yd = device_rows(cfg.spec, bt)
+    G, c, yy, n = oem_gram(ctx, Xd, yd)
+    del Xd, yd
+    torch.cuda.empty_cache()
+    grp = groups_of(cfg)
+    fit = oem_fit_path(ctx, G, c, [n], cfg.penalties, nlambda=cfg.nlambda, group=grp, ngroups=100)
+    Gh, ch = G.cpu().numpy(), c.cpu().numpy()
+    d = float(fit.d[0])
+    lam1 = np.linalg.eigvalsh(Gh / n)[-1]
+    assert lam1 * (1 - 1e-12) <= d <= 1.01 * lam1, (d, lam1)
+    for q, (fam, gamma, alpha) in enumerate(cfg.penalties):
+        g = grp if fam.startswith("grp") else None
+        lam = orc.lambda_grid(orc.lambda_max(fam, ch / n, group=g, alpha=alpha), cfg.nlambda)
+        lg = fit.lam[0, q].cpu().numpy()
+        assert np.max(np.abs(lg - lam) / lam) < 1e-13
+        B, it, cv = orc.oem_path(Gh / n, ch / n, d, fam, lg, gamma, alpha, group=g)
+        assert np.max(np.abs(fit.beta[0, q].cpu().numpy() - B)) <= TOL_BETA, fam
+        assert np.array_equal(fit.conv[0, q].cpu().numpy().astype(bool), cv)
+        itg = fit.iters[0, q].cpu().numpy()
+        assert np.max(np.abs(itg - it)) <= max(2, 0.02 * it.max()), (fam, itg - it)
 
 
 def test_noncontiguous_groups_and_weights(ctx):
