@@ -100,19 +100,23 @@ def test_gram_full_size_cfg2(ctx):
 def test_gram_full_n_column_subset_cfg4(ctx):
     """cfg4 at full n = 1e7 (80 GB resident): the leading 16x16 block of G and X^T y on the
     support checked against the oracle over all 1e7 rows (host generator, those columns)."""
-    from paper_1801_09661_b200 import oem_gram
+    from paper_1801_09661_b200 import oem_gram, oem_gram_moments
     cfg = CONFIGS["cfg4"]
     bt = dg.beta(cfg.spec)
     Xd, yd = device_rows(cfg.spec, bt)
     G, c, yy, nt = oem_gram(ctx, Xd, yd)
+    xs, ysum = oem_gram_moments(ctx, Xd, yd, 1, 0)   # f3 column sums at full size, same launch shape
     del Xd
     torch.cuda.empty_cache()
     m = 16
     acc = orc.GramAccumulator(m)
+    xso = np.zeros(m); xabs = np.zeros(m)
     for r in range(0, cfg.n, 1_000_000):
         X, y = dg.rows_host(cfg.spec, bt, r, 1_000_000, 0, m)
         acc.add(X, y)
+        xso += X.sum(axis=0); xabs += np.abs(X).sum(axis=0)
     Go, co, yyo = acc.result()
+    assert np.max(np.abs(xs[0].cpu().numpy()[:m] - xso) / xabs) <= 1e-12
     Gh = G.cpu().numpy()
     assert scale_err(Gh[:m, :m], Go) <= 1e-12
     assert xty_err(c.cpu().numpy()[:m], co, Go, yyo) <= 1e-12
@@ -156,13 +160,21 @@ def test_weighted_full_size_cfg5(ctx):
     Xd, yd = device_rows(cfg.spec, bt)
     beta = 0.5 * bt + 0.01
     Gw, cw, sc = oem_gram_weighted(ctx, Xd, yd, to_dev(beta))
+    from paper_1801_09661_b200 import oem_logit_grad
+    g, ll = oem_logit_grad(ctx, Xd, yd, to_dev(beta))   # f1 gradient pass at full size
     del Xd
     torch.cuda.empty_cache()
     Go = np.zeros((cfg.p, cfg.p)); co = np.zeros(cfg.p); so = np.zeros(2); szz = 0.0
+    go = np.zeros(cfg.p); llo = 0.0; cond = np.zeros(cfg.p); llc = 0.0
     for r in range(0, cfg.n, 1_000_000):
         X, y = dg.rows_host(cfg.spec, bt, r, 1_000_000)
         G1, c1, s1 = orc.gram_weighted(X, y, beta)
         Go += G1; co += c1; so += s1
+        g1, l1 = orc.logit_grad(X, y, beta)
+        go += g1; llo += l1
+        eta1 = X @ beta
+        cond += np.abs(X).T @ np.abs(y - 1 / (1 + np.exp(-eta1)))
+        llc += np.sum(np.abs(y * eta1) + np.logaddexp(0, eta1))
         eta = X @ beta
         mu = np.clip(1 / (1 + np.exp(-eta)), 1e-5, 1 - 1e-5)
         w = mu * (1 - mu)
@@ -172,6 +184,8 @@ def test_weighted_full_size_cfg5(ctx):
     assert np.max(np.abs(cw.cpu().numpy() - co) / np.sqrt(np.diag(Go) * szz)) <= 1e-12
     assert abs(float(sc[0]) - so[0]) <= 1e-12 * so[0]
     assert abs(float(sc[1]) - so[1]) <= 1e-12 * abs(so[1])
+    assert np.max(np.abs(g.cpu().numpy() - go) / cond) <= 1e-12
+    assert abs(float(ll) - llo) <= 1e-12 * llc
 
 
 def test_gram_edge_cases(ctx):

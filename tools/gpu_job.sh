@@ -1,4 +1,3 @@
 set -x
 mkdir -p gpurun_out
-timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/smoke.log 2>&1; echo smoke=$?
-timeout 1200 python -m pytest tests -m gpu -x -q > gpurun_out/gpu_tests.log 2>&1; echo tests=$?
+timeout 900 python -m pytest tests/test_gpu_gram.py -m gpu -x -q -k "full_n_column_subset_cfg4 or weighted_full_size_cfg5" --durations=3 > gpurun_out/fs2_tests.log 2>&1; echo tests=$?
