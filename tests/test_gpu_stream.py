@@ -97,3 +97,27 @@ def test_stream_edge_cases(ctx):
     G, c, yy, nt = oem_gram_host(ctx, Xh, yh, block_rows=32)   # 4 blocks, the last one ragged
     Go, co, yyo = orc.gram(X, y)
     assert nt == 100 and np.array_equal(G.cpu().numpy(), Go) and np.array_equal(c.cpu().numpy(), co)
+
+
+def test_gram_host_full_size_cfg4(ctx):
+    """f4 at full size, as bench.py's e2e leg runs it: cfg4's 1e7 x 1000 design (80 GB) in pinned
+    host memory streamed through the Gram kernel in 2^20-row blocks, against the in-core pass over
+    the same rows (itself pinned to the oracle at full size in test_gpu_gram.py)."""
+    from paper_1801_09661_b200 import oem_gram, oem_gram_host
+    cfg = CONFIGS["cfg4"]
+    bt = dg.beta(cfg.spec)
+    from gpu_util import device_rows
+    Xd, yd = device_rows(cfg.spec, bt)
+    G, c, yy, nt = oem_gram(ctx, Xd, yd)
+    Xh = torch.empty(Xd.shape, dtype=torch.float64, pin_memory=True)
+    Xh.copy_(Xd)
+    yh = yd.cpu().pin_memory()
+    del Xd, yd
+    torch.cuda.empty_cache()
+    Gs, cs, yys, ns = oem_gram_host(ctx, Xh, yh, block_rows=1 << 20)
+    assert ns == nt == cfg.n
+    Gh = G.cpu().numpy()
+    assert scale_err(Gs.cpu().numpy(), Gh) <= 1e-12
+    d = np.sqrt(np.diag(Gh))
+    assert np.max(np.abs(cs.cpu().numpy() - c.cpu().numpy()) / (d * np.sqrt(float(yy)))) <= 1e-12
+    assert abs(float(yys) - float(yy)) <= 1e-12 * float(yy)
