@@ -50,18 +50,18 @@ static oem_status check_x(const double* X, const double* y, int64_t n_local, int
   return OEM_OK;
 }
 
-oem_status host_allreduce_i64(oem_ctx* ctx, int64_t* vals, int n) {
-  // small integer sums (row counts) across ranks: via a device buffer and NCCL int64
+oem_status host_allreduce_i64(oem_ctx* ctx, int64_t* vals, int n, cudaStream_t st) {
+  // small integer sums (row counts) across ranks: through a context-owned device buffer and NCCL
+  // int64 on the caller's stream (every collective of the communicator is issued on that stream,
+  // in the same order on every rank)
   if (ctx->nranks <= 1) return OEM_OK;
-  int64_t* d = nullptr;
-  OEM_CUDA_TRY(cudaMalloc(&d, sizeof(int64_t) * n));
-  cudaMemcpy(d, vals, sizeof(int64_t) * n, cudaMemcpyHostToDevice);
-  ncclResult_t r = ncclAllReduce(d, d, n, ncclInt64, ncclSum, (ncclComm_t)ctx->nccl_comm, 0);
-  cudaError_t e = cudaStreamSynchronize(0);
-  cudaMemcpy(vals, d, sizeof(int64_t) * n, cudaMemcpyDeviceToHost);
-  cudaFree(d);
+  OEM_CUDA_TRY(ctx->counts_dev.ensure(sizeof(int64_t) * (size_t)n));
+  int64_t* d = ctx->counts_dev.as<int64_t>();
+  OEM_CUDA_TRY(cudaMemcpyAsync(d, vals, sizeof(int64_t) * n, cudaMemcpyHostToDevice, st));
+  ncclResult_t r = ncclAllReduce(d, d, n, ncclInt64, ncclSum, (ncclComm_t)ctx->nccl_comm, st);
   if (r != ncclSuccess) OEM_FAIL(OEM_ERR_NCCL, std::string("ncclAllReduce(counts): ") + ncclGetErrorString(r));
-  if (e != cudaSuccess) OEM_FAIL(OEM_ERR_CUDA, cudaGetErrorString(e));
+  OEM_CUDA_TRY(cudaMemcpyAsync(vals, d, sizeof(int64_t) * n, cudaMemcpyDeviceToHost, st));
+  OEM_CUDA_TRY(cudaStreamSynchronize(st));
   return OEM_OK;
 }
 
@@ -134,6 +134,7 @@ oem_status oem_ctx_destroy(oem_ctx* ctx) {
   ctx->plans.clear();
   ctx->partial.release();
   ctx->partial2.release();
+  ctx->counts_dev.release();
   ctx->partial_scal.release();
   ctx->packed.release();
   ctx->tail.release();
@@ -203,7 +204,7 @@ oem_status oem_gram(oem_ctx* ctx, const double* X, const double* y, int64_t n_lo
   if ((s = gram_unpack(ctx, packed, 1, p, G, xty, yty, st)) != OEM_OK) return s;
   if (n_total) {
     int64_t n = n_local;
-    if ((s = host_allreduce_i64(ctx, &n, 1)) != OEM_OK) return s;
+    if ((s = host_allreduce_i64(ctx, &n, 1, st)) != OEM_OK) return s;
     *n_total = n;
   }
   return OEM_OK;
@@ -224,7 +225,7 @@ oem_status oem_gram_folds(oem_ctx* ctx, const double* X, const double* y, int64_
     const int64_t first = ((k - row_offset) % K + K) % K;  // first local row in fold k
     counts[k] = n_local > first ? (n_local - first + K - 1) / K : 0;
   }
-  if ((s = host_allreduce_i64(ctx, counts, K)) != OEM_OK) return s;
+  if ((s = host_allreduce_i64(ctx, counts, K, st)) != OEM_OK) return s;
   for (int k = 0; k < K; ++k)
     if (counts[k] == 0) OEM_FAIL(OEM_ERR_EMPTY_FOLD, "oem_gram_folds: fold " + std::to_string(k) + " has no rows");
   const int64_t psize = packed_size(p);

@@ -57,7 +57,7 @@ struct oem_ctx {
   int nranks = 1, rank = 0;
   int num_sms = 148;
   void* nccl_comm = nullptr;  // ncclComm_t
-  oem::DevBuf partial, partial2, partial_scal, packed, tail, plan_tables, path_ws, path_small, logi, lg_part, lg_out, mom_part, mom_out, stage0, stage1;
+  oem::DevBuf partial, partial2, counts_dev, partial_scal, packed, tail, plan_tables, path_ws, path_small, logi, lg_part, lg_out, mom_part, mom_out, stage0, stage1;
   cudaStream_t copy_stream = nullptr;  // f4 host streaming: H2D copies overlap the Gram kernel
   cudaEvent_t ev_copied[2] = {nullptr, nullptr}, ev_used[2] = {nullptr, nullptr};
   std::map<std::tuple<int, int, int64_t, int>, std::shared_ptr<oem::GramPlan>> plans;
@@ -110,7 +110,7 @@ inline int64_t packed_size(int p) { return (int64_t)(p + 1) * (p + 2) / 2; }
 
 oem_status allreduce_sum(oem_ctx* ctx, double* buf, size_t count, cudaStream_t st);
 // small host integer sums over ranks (row counts)
-oem_status host_allreduce_i64(oem_ctx* ctx, int64_t* vals, int n);
+oem_status host_allreduce_i64(oem_ctx* ctx, int64_t* vals, int n, cudaStream_t st);
 
 // f1 (logit_ub.cu): out[0..p) = X^T (y - sigma(X beta)), out[p] = loglik, raw sums allreduced
 oem_status logit_grad_pass(oem_ctx* ctx, const double* X, const double* y01, const double* beta, int64_t n_local,

@@ -99,7 +99,7 @@ extern "C" oem_status oem_gram_host(oem_ctx* ctx, const double* X, const double*
   if ((s = gram_unpack(ctx, packed, 1, p, G, xty, yty, st)) != OEM_OK) return s;
   if (n_total) {
     int64_t n = n_local;
-    if ((s = host_allreduce_i64(ctx, &n, 1)) != OEM_OK) return s;
+    if ((s = host_allreduce_i64(ctx, &n, 1, st)) != OEM_OK) return s;
     *n_total = n;
   }
   return OEM_OK;
@@ -121,7 +121,7 @@ extern "C" oem_status oem_gram_folds_host(oem_ctx* ctx, const double* X, const d
     const int64_t first = ((k - row_offset) % K + K) % K;
     counts[k] = n_local > first ? (n_local - first + K - 1) / K : 0;
   }
-  if ((s = host_allreduce_i64(ctx, counts, K)) != OEM_OK) return s;
+  if ((s = host_allreduce_i64(ctx, counts, K, st)) != OEM_OK) return s;
   for (int k = 0; k < K; ++k)
     if (counts[k] == 0) OEM_FAIL(OEM_ERR_EMPTY_FOLD, "oem_gram_folds_host: fold " + std::to_string(k) + " has no rows");
   const int64_t psize = packed_size(p);
