@@ -1,3 +1,5 @@
 set -x
 mkdir -p gpurun_out
-timeout 900 python -m pytest tests/test_gpu_stream.py -m gpu -x -q -k "full_size" --durations=3 > gpurun_out/fs3_tests.log 2>&1; echo tests=$?
+timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/smoke.log 2>&1; echo smoke=$?
+timeout 1500 python -m pytest tests -m gpu -x -q > gpurun_out/gpu_tests.log 2>&1; echo tests=$?
+timeout 900 python bench.py > gpurun_out/bench_cfg4.log 2>&1; echo bench=$?
