@@ -762,10 +762,15 @@ template <int MODE, bool TWO>
 static oem_status launch_t(const GramPlan& pl, const CUtensorMap& mx, const CUtensorMap& my, const GramParams& P,
                            int nfold, cudaStream_t st) {
   auto kern = gram_kernel<MODE, TWO>;
-  static size_t attr_smem = 0;  // opt-in dynamic shared memory, raised on demand
-  if (pl.smem > attr_smem) {
+  // opt-in dynamic shared memory, raised on demand; the attribute is per device (a process may
+  // drive several devices through several contexts), so the cache is too
+  static thread_local size_t attr_smem[64] = {};
+  int dev = 0;
+  OEM_CUDA_TRY(cudaGetDevice(&dev));
+  size_t& cur = attr_smem[dev & 63];
+  if (pl.smem > cur) {
     OEM_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)pl.smem));
-    attr_smem = pl.smem;
+    cur = pl.smem;
   }
   dim3 grid((unsigned)(pl.U * pl.nseg * nfold));
   kern<<<grid, gram_threads(MODE, TWO), pl.smem, st>>>(mx, my, P);
