@@ -1,4 +1,8 @@
+# Scratch job for one-off GPU studies (edit, then run through gpurun):
+#   /usr/local/graft/bin/gpurun --timeout 1200 -- 'bash tools/gpu_job.sh'
+# Outputs go under gpurun_out/ (merged back, <= 64 MiB). The round's measurement scripts are
+# tools/gpu_round.sh (tests, smoke, bench lines, launch lists, reference arm) and
+# tools/gpu_ncu_full.sh (one `ncu --set full` capture per Gram workload).
 set -x
 mkdir -p gpurun_out
-B="python bench.py --warmup 0 --steps 1 --e2e-steps 0 --no-cpu-baseline"
-timeout 900 ncu --set full --clock-control none --import-source on -k regex:fit_glob_kernel -c 1 -o gpurun_out/ncu_glob_cfg4 -f $B --workload cfg4 > gpurun_out/ncu_glob_cfg4.log 2>&1; echo glob=$?
+timeout 900 python -m pytest tests -m gpu -x -q > gpurun_out/gpu_tests.log 2>&1; echo tests=$?
