@@ -63,6 +63,27 @@ def test_gram_integer_design_bit_exact(ctx, p):
     assert float(yy) == yyo
 
 
+@pytest.mark.parametrize("p,n", [(1024, 301), (2047, 157), (4095, 67)])
+def test_gram_wide_p_bit_exact(ctx, p, n):
+    """Two-panel plans far wider than any config (8 to 32 panels, 36 to 528 tile types, a ragged
+    last panel): integer designs, bit-exact against the oracle, plain and fold passes."""
+    from paper_1801_09661_b200 import oem_gram, oem_gram_folds
+    X, y = int_design(p + n, n, p)
+    ldx = p + (p & 1)
+    Xp = np.zeros((n, ldx))
+    Xp[:, :p] = X
+    Xd = to_dev(Xp)[:, :p]
+    G, c, yy, nt = oem_gram(ctx, Xd, to_dev(y))
+    Go, co, yyo = orc.gram(X, y)
+    assert nt == n and np.array_equal(G.cpu().numpy(), Go) and np.array_equal(c.cpu().numpy(), co)
+    assert float(yy) == yyo
+    if p <= 2047:
+        Gk, ck, yyk, cnt = oem_gram_folds(ctx, Xd, to_dev(y), 3, row_offset=2)
+        Gf, cf, yyf, cntf = orc.gram_folds(X, y, 3, row_offset=2)
+        assert list(cnt) == list(cntf)
+        assert np.array_equal(Gk.cpu().numpy(), Gf) and np.array_equal(ck.cpu().numpy(), cf)
+
+
 @pytest.mark.parametrize("name,n", [("cfg1", 1000), ("cfg2", 30011), ("cfg3", 4099), ("cfg4", 2053),
                                     ("cfg5", 10007)])
 def test_gram_configs_parity(ctx, name, n):
