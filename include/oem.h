@@ -62,7 +62,8 @@ oem_status oem_ctx_destroy(oem_ctx* ctx);
  * computational step in OEM is in forming the matrix A"; P:L328-333 O(np^2 + np)).
  * One pass over [X | y]: G = X^T X (full symmetric p*p written, row-major), xty = X^T y (p),
  * yty = y^T y (1). Raw sums over this rank's rows, allreduced when nranks > 1; normalisation
- * (/n, R#1) happens in oem_fit_path. n_total (host, may be NULL) receives the global row count.
+ * (/n, R#1) happens in oem_fit_path. n_total (host, may be NULL) receives the global row count
+ * (with nranks > 1 a small NCCL allreduce on `stream`, after which the call synchronises it).
  * n_local = 0 is allowed (zero outputs). Errors: OEM_ERR_DIM (p < 1, ldx < p, n_local < 0),
  * OEM_ERR_ALIGN, OEM_ERR_UNSUPPORTED (p > 16383), OEM_ERR_CUDA, OEM_ERR_NCCL. */
 oem_status oem_gram(oem_ctx* ctx, const double* X, const double* y, int64_t n_local, int32_t p,
@@ -75,7 +76,8 @@ oem_status oem_gram(oem_ctx* ctx, const double* X, const double* y, int64_t n_lo
  * fold(i) = (row_offset + i) mod K for local row i (R#19); row_offset = this rank's first
  * global row. Errors: as oem_gram, plus OEM_ERR_INVALID_ARG (K < 1),
  * OEM_ERR_EMPTY_FOLD (a fold with no rows globally). Synchronises `stream` only if nranks > 1
- * (the counts allreduce is host-side arithmetic, no device sync needed). */
+ * (the per-rank counts are host arithmetic; their sum over ranks is one small NCCL allreduce on
+ * `stream`, read back before the pass). */
 oem_status oem_gram_folds(oem_ctx* ctx, const double* X, const double* y, int64_t n_local, int32_t p,
                           int64_t ldx, int64_t row_offset, int32_t K, double* G_folds,
                           double* xty_folds, double* yty_folds, int64_t* counts /*host K*/, void* stream);
