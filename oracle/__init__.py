@@ -57,7 +57,7 @@ def lib():
             "orc_fold_complements": (None, [p, p, i32, i32, p, p]),
             "orc_gram_weighted": (None, [p, p, p, i64, i32, i64, d, p, p, p, ctypes.c_int]),
             "orc_eig_jacobi": (None, [p, i32, p]),
-            "orc_power_rule": (d, [p, i32, i32, d, p, p]),
+            "orc_d_rule": (d, [p, i32, i32, p, p]),
             "orc_soft": (d, [d, d, d]),
             "orc_enet": (d, [d, d, d, d]),
             "orc_mcp": (d, [d, d, d, d]),
@@ -71,8 +71,9 @@ def lib():
             "orc_oem_path": (ctypes.c_int, [p, p, i32, d, ctypes.c_int, d, d, p, p, i32, p, p, i32,
                                             d, i64, p, p, p, p]),
             "orc_objective": (d, [p, p, i32, p, ctypes.c_int, d, d, d, p, p, i32, p]),
-            "orc_logistic_path": (ctypes.c_int, [p, p, i64, i32, i64, p, i32, d, d, i64, d, i32,
-                                                 i32, d, p, p, p, p, ctypes.c_int]),
+            "orc_logistic_path": (ctypes.c_int, [p, p, i64, i32, i64, ctypes.c_int, d, d, p, p, i32,
+                                                 p, p, i32, d, d, i64, d, i32, i32, p, p, p, p, p,
+                                                 ctypes.c_int]),
         }
         for name, (res, args) in sig.items():
             f = getattr(_lib, name)
@@ -181,13 +182,17 @@ def eig_jacobi(A):
     return ev
 
 
-def power_rule(A, iters=200, inflate=5e-3):
-    """O4: d = min(Gershgorin, (1+inflate) RQ_iters) from v0 = 1/sqrt(p) (R#5)."""
+SQUARINGS = 12   # R#5: S, so U_S is within a factor p^(1/4096) of lambda_1 (0.17% at p = 1000)
+
+
+def d_rule(A, squarings=SQUARINGS):
+    """O4: d = min(Gershgorin, U_S), U_S = trace(A^(2^S))^(1/2^S) >= lambda_1 (R#5
+    "d >= lambda_1 ... d = lambda_1 fastest"). Returns (d, U_S, Gershgorin)."""
     A = _f64(A)
-    rq = np.empty(1)
+    u = np.empty(1)
     gs = np.empty(1)
-    d = lib().orc_power_rule(_ptr(A), A.shape[0], iters, inflate, _ptr(rq), _ptr(gs))
-    return d, float(rq[0]), float(gs[0])
+    d = lib().orc_d_rule(_ptr(A), A.shape[0], squarings, _ptr(u), _ptr(gs))
+    return d, float(u[0]), float(gs[0])
 
 
 # ---------------------------------------------------------------- thresholds
@@ -292,36 +297,44 @@ def objective(G, c, beta, family, lam, gamma=3.0, alpha=1.0, w=None, group=None,
                                alpha, _ptr(_f64(w)), _ptr(g), ng, _ptr(_f64(grp_w)))
 
 
-def logistic_path(X, y01, lambdas, eps=1e-5, tol_in=1e-11, maxit_in=100000, tol_out=1e-10,
-                  outer_maxit=100, power_iters=200, inflate=5e-3, nthreads=None):
-    """O7: proximal-Newton lasso-logistic path with OEM inner solves (R#23-26)."""
+def logistic_path(X, y01, lambdas, family="lasso", gamma=3.0, alpha=1.0, w=None, group=None,
+                  ngroups=0, grp_w=None, eps=1e-5, tol_in=1e-11, maxit_in=100000, tol_out=1e-10,
+                  outer_maxit=100, squarings=SQUARINGS, nthreads=None, return_d=False):
+    """O7: proximal-Newton logistic path with OEM inner solves (R#23-26), any
+    Table 1 family (groups as in O6). Returns (B[L,p], outer[L], inner[L], conv[L]) and, with
+    return_d, the first outer step's d_w."""
     X = _f64(X)
     y01 = _f64(y01)
     lambdas = _f64(np.atleast_1d(lambdas))
     n, p = X.shape
     L = lambdas.size
+    g, ng = _groups(group, ngroups)
     B = np.empty((L, p))
     oi = np.empty(L, dtype=np.int32)
     ii = np.empty(L, dtype=np.int64)
     cv = np.empty(L, dtype=np.uint8)
-    rc = lib().orc_logistic_path(_ptr(X), _ptr(y01), n, p, p, _ptr(lambdas), L, eps, tol_in,
-                                 maxit_in, tol_out, outer_maxit, power_iters, inflate, _ptr(B),
-                                 _ptr(oi), _ptr(ii), _ptr(cv), nthreads or _nthreads(n))
+    d0 = np.zeros(1)
+    rc = lib().orc_logistic_path(_ptr(X), _ptr(y01), n, p, p, FAMILY[family], gamma, alpha,
+                                 _ptr(_f64(w)), _ptr(g), ng, _ptr(_f64(grp_w)), _ptr(lambdas), L,
+                                 eps, tol_in, maxit_in, tol_out, outer_maxit, squarings, _ptr(B),
+                                 _ptr(oi), _ptr(ii), _ptr(cv), _ptr(d0), nthreads or _nthreads(n))
     if rc != 0:
-        raise ValueError("oracle logistic_path: y must be 0/1")
+        raise ValueError("oracle logistic_path: y must be 0/1 and the penalty parameters valid")
+    if return_d:
+        return B, oi, ii, cv.astype(bool), float(d0[0])
     return B, oi, ii, cv.astype(bool)
 
 
 # ---------------------------------------------------------------- composed fit (§8(a) a6-a10)
 def fit_from_gram(G_raw, c_raw, n, penalties, nlambda=100, ratio=1e-3, d=None, tol=1e-11,
-                  maxit=100000, w=None, group=None, ngroups=0, grp_w=None, power_iters=200,
-                  inflate=5e-3, lambda_max_override=None):
+                  maxit=100000, w=None, group=None, ngroups=0, grp_w=None, squarings=SQUARINGS,
+                  lambda_max_override=None):
     """a6 normalize (/n, R#1) -> a7 d (rule R#5, or the d given) -> a8 grid per family (R#14-16)
     -> a9 path per penalty. penalties: list of (family, gamma, alpha). Returns dict."""
     Gn = np.asarray(G_raw, dtype=np.float64) / n
     cn = np.asarray(c_raw, dtype=np.float64) / n
     if d is None:
-        d = power_rule(Gn, power_iters, inflate)[0]
+        d = d_rule(Gn, squarings)[0]
     out = {"d": d, "beta": [], "lambda": [], "iters": [], "conv": []}
     for fam, gamma, alpha in penalties:
         lmax = lambda_max_override if lambda_max_override is not None else lambda_max(
@@ -404,11 +417,11 @@ def logit_grad(X, y01, beta):
 
 
 def logistic_path_ub(X, y01, lambdas, family="lasso", gamma=3.0, alpha=1.0, d=None, tol_in=1e-11,
-                     maxit_in=100000, tol_out=1e-10, outer_maxit=1000, power_iters=200, inflate=5e-3):
+                     maxit_in=100000, tol_out=1e-10, outer_maxit=1000, squarings=SQUARINGS):
     """f1: the proximal-Newton logistic path with the Hessian upper bound w_i = 1/4
     (P:L385-389, R#27), in the paper's order: per outer step the working responses
     z_i = eta_i + (y_i - mu_i)/w_i with w_i = 1/4, the weighted statistics
-    G_w = (1/n) sum w x x^T, c_w = (1/n) sum w z x, d_w by the power rule (R#5)
+    G_w = (1/n) sum w x x^T, c_w = (1/n) sum w z x, d_w by the d rule (R#5)
     unless d is given, then the OEM inner solve for the single lambda from the current beta
     (O6); stop when max |dbeta| <= tol_out. Returns (B[L,p], outer[L], inner[L], conv[L])."""
     X = _f64(X)
@@ -428,7 +441,7 @@ def logistic_path_ub(X, y01, lambdas, family="lasso", gamma=3.0, alpha=1.0, d=No
             z = eta + (y01 - mu) / w
             Gw = (w * X).T @ X / n
             cw = X.T @ (w * z) / n
-            dw = d if d is not None else power_rule(Gw, power_iters, inflate)[0]
+            dw = d if d is not None else d_rule(Gw, squarings)[0]
             nb, it, ok = oem_path(Gw, cw, dw, family, [lam], gamma, alpha, tol=tol_in, maxit=maxit_in,
                                   beta_init=beta)
             ii[l] += it[0]
@@ -445,7 +458,7 @@ def logistic_path_ub(X, y01, lambdas, family="lasso", gamma=3.0, alpha=1.0, d=No
 # ---------------------------------------------------------------- f3: intercept, standardization, loss
 def fit_transformed(X, y, penalties, nlambda=100, ratio=1e-3, standardize=False, intercept=False, d=None,
                     lambdas=None, tol=1e-11, maxit=100000, w=None, group=None, ngroups=0, grp_w=None,
-                    power_iters=200, inflate=5e-3):
+                    squarings=SQUARINGS):
     """f3 by transforming the DATA (R#2-3), not the Gram: with an intercept, X and y are centred
     explicitly (x_ij - xbar_j, y_i - ybar); with standardization the (centred) columns are divided
     by sd_j = sqrt(mean(x_ij^2)) (P:L173-177 with the /n convention of R#1); then O1 Gram -> a6-a9
@@ -465,7 +478,7 @@ def fit_transformed(X, y, penalties, nlambda=100, ratio=1e-3, standardize=False,
     G, c, _ = gram(X, y)
     out = {"beta": [], "intercept": [], "lambda": []}
     if d is None:
-        d = power_rule(G / n, power_iters, inflate)[0]
+        d = d_rule(G / n, squarings)[0]
     out["d"] = d
     for q, (fam, gamma, alpha) in enumerate(penalties):
         if lambdas is None:

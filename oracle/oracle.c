@@ -248,40 +248,53 @@ void orc_eig_jacobi(const double* A0, int32_t p, double* evals) {
   free(A);
 }
 
-double orc_power_rule(const double* A, int32_t p, int32_t iters, double inflate, double* rq_out, double* gersh_out) {
-  double* v = (double*)malloc(sizeof(double) * (size_t)p);
-  double* w = (double*)malloc(sizeof(double) * (size_t)p);
-  for (int32_t j = 0; j < p; ++j) v[j] = 1.0 / sqrt((double)p);
-  for (int32_t t = 0; t < iters; ++t) {
-    double nrm = 0.0;
-    for (int32_t j = 0; j < p; ++j) {
-      double s = 0.0;
-      for (int32_t k = 0; k < p; ++k) s += A[(size_t)j * p + k] * v[k];
-      w[j] = s;
-      nrm += s * s;
-    }
-    nrm = sqrt(nrm);
-    if (nrm == 0.0) break;
-    for (int32_t j = 0; j < p; ++j) v[j] = w[j] / nrm;
-  }
-  double rq = 0.0;
-  for (int32_t j = 0; j < p; ++j) {
-    double s = 0.0;
-    for (int32_t k = 0; k < p; ++k) s += A[(size_t)j * p + k] * v[k];
-    rq += v[j] * s;
-  }
+/* The d rule (R#5): d = min(Gershgorin, U_S), U_S = trace(A^(2^S))^(1/2^S).
+ * For symmetric PSD A with eigenvalues l_1 >= ... >= l_p >= 0, trace(A^m) = sum_i l_i^m, so
+ * l_1 <= trace(A^m)^(1/m) <= p^(1/m) l_1: U_S is an upper bound on l_1 for every A (whatever
+ * its eigenvectors), and within a factor p^(1/2^S) of it. A^(2^S) is formed by S squarings of
+ * the trace-normalised matrix (the power method applied to all p basis vectors at once):
+ *   B_0 = A; s_t = trace(B_t); B_{t+1} = (B_t / s_t)^2;
+ *   log U_S = log s_0 + sum_{t=1..S} 2^-t log s_t     (A^(2^t) = c_t B_t / s_t, c_t = c_{t-1}^2 s_t),
+ * times the rounding allowance (1 + 2 S p u).
+ * Naive triple-loop products (rows in parallel; each entry is one plain dot product). */
+double orc_d_rule(const double* A, int32_t p, int32_t squarings, double* U_out, double* gersh_out) {
+  size_t pp = (size_t)p * p;
   double gersh = 0.0;
   for (int32_t j = 0; j < p; ++j) {
     double s = 0.0;
     for (int32_t k = 0; k < p; ++k) s += fabs(A[(size_t)j * p + k]);
     if (s > gersh) gersh = s;
   }
-  free(v);
-  free(w);
-  if (rq_out) *rq_out = rq;
+  double* B = (double*)malloc(sizeof(double) * pp);
+  double* C = (double*)malloc(sizeof(double) * pp);
+  memcpy(B, A, sizeof(double) * pp);
+  double s = 0.0;
+  for (int32_t j = 0; j < p; ++j) s += B[(size_t)j * p + j];
+  double logU = s > 0.0 ? log(s) : -INFINITY;
+  for (int32_t t = 1; t <= squarings && s > 0.0; ++t) {
+    /* B <- B / s, then C = B B. B stays exactly symmetric (C_jk and C_kj are the same products
+     * summed in the same order), so B_mk is read as B_km: a row-by-row dot product. */
+    for (size_t e = 0; e < pp; ++e) B[e] /= s;
+#pragma omp parallel for schedule(static)
+    for (int32_t j = 0; j < p; ++j)
+      for (int32_t k = 0; k < p; ++k) {
+        double acc = 0.0;
+        for (int32_t m = 0; m < p; ++m) acc += B[(size_t)j * p + m] * B[(size_t)k * p + m];
+        C[(size_t)j * p + k] = acc;
+      }
+    double* tmp = B; B = C; C = tmp;
+    s = 0.0;
+    for (int32_t j = 0; j < p; ++j) s += B[(size_t)j * p + j];
+    logU += ldexp(log(s), -t);
+  }
+  free(B);
+  free(C);
+  /* rounding allowance: the S squarings perturb the top of the spectrum by about S p u
+   * relative (u = 2^-53), so U is inflated by (1 + 2 S p u) to stay >= lambda_1 in fp64 */
+  double U = exp(logU) * (1.0 + 2.0 * (double)squarings * (double)p * ldexp(1.0, -53));
+  if (U_out) *U_out = U;
   if (gersh_out) *gersh_out = gersh;
-  double d = (1.0 + inflate) * rq;
-  return gersh < d ? gersh : d;
+  return gersh < U ? gersh : U;
 }
 
 /* ---------------- thresholding operators ---------------- */
@@ -547,11 +560,12 @@ double orc_objective(const double* G, const double* c, int32_t p, const double* 
 }
 
 /* ---------------- O7 logistic ---------------- */
-int orc_logistic_path(const double* X, const double* y01, int64_t n, int32_t p, int64_t ldx,
-                      const double* lambdas, int32_t L, double eps, double tol_in, int64_t maxit_in,
-                      double tol_out, int32_t outer_maxit, int32_t power_iters, double inflate,
+int orc_logistic_path(const double* X, const double* y01, int64_t n, int32_t p, int64_t ldx, int family,
+                      double gamma, double alpha, const double* w, const int32_t* group, int32_t ngroups,
+                      const double* grp_w, const double* lambdas, int32_t L, double eps, double tol_in,
+                      int64_t maxit_in, double tol_out, int32_t outer_maxit, int32_t squarings,
                       double* beta_out, int32_t* outer_iters, int64_t* inner_iters, uint8_t* conv,
-                      int nthreads) {
+                      double* d_out, int nthreads) {
   for (int64_t i = 0; i < n; ++i)
     if (!(y01[i] == 0.0 || y01[i] == 1.0)) return -1;
   size_t pp = (size_t)p * p;
@@ -562,7 +576,8 @@ int orc_logistic_path(const double* X, const double* y01, int64_t n, int32_t p, 
   double sc[2];
   int64_t it1;
   uint8_t cv1;
-  for (int32_t l = 0; l < L; ++l) {
+  int rc = 0;
+  for (int32_t l = 0; l < L && rc == 0; ++l) {
     int32_t o = 0;
     int64_t inner = 0;
     uint8_t ok = 0;
@@ -570,9 +585,11 @@ int orc_logistic_path(const double* X, const double* y01, int64_t n, int32_t p, 
       orc_gram_weighted(X, y01, beta, n, p, ldx, eps, Gw, cw, sc, nthreads);
       for (size_t q = 0; q < pp; ++q) Gw[q] /= (double)n;
       for (int32_t j = 0; j < p; ++j) cw[j] /= (double)n;
-      double dw = orc_power_rule(Gw, p, power_iters, inflate, NULL, NULL);
-      orc_oem_path(Gw, cw, p, dw, ORC_LASSO, 0.0, 1.0, NULL, NULL, 0, NULL, &lambdas[l], 1, tol_in,
-                   maxit_in, beta, nb, &it1, &cv1);
+      double dw = orc_d_rule(Gw, p, squarings, NULL, NULL);
+      if (d_out && l == 0 && o == 0) *d_out = dw;
+      rc = orc_oem_path(Gw, cw, p, dw, family, gamma, alpha, w, group, ngroups, grp_w, &lambdas[l], 1,
+                        tol_in, maxit_in, beta, nb, &it1, &cv1);
+      if (rc != 0) break;
       inner += it1;
       ++o;
       double delta = 0.0;
@@ -592,5 +609,5 @@ int orc_logistic_path(const double* X, const double* y01, int64_t n, int32_t p, 
   free(cw);
   free(beta);
   free(nb);
-  return 0;
+  return rc;
 }

@@ -50,10 +50,11 @@ void orc_gram_weighted(const double* X, const double* y01, const double* beta, i
 
 /* ---- O4 d (§2.1: OEM converges for d >= lambda_1(X^T X); d = lambda_1 fastest).
  * orc_eig_jacobi: all eigenvalues of symmetric A (p*p) by cyclic Jacobi (textbook), ascending.
- * orc_power_rule: the d rule of R#5: v0 = 1/sqrt(p), `iters` power steps, RQ = v^T A v,
- *   d = min(Gershgorin max row sum, (1 + inflate) * RQ). Returns d; rq/gersh optional outputs. */
+ * orc_d_rule: the d rule of R#5: d = min(Gershgorin max row sum, U_S) with
+ *   U_S = trace(A^(2^S))^(1/2^S) >= lambda_1 (A symmetric PSD), formed by S squarings of the
+ *   trace-normalised matrix. Returns d; U / gersh optional outputs. */
 void orc_eig_jacobi(const double* A, int32_t p, double* evals);
-double orc_power_rule(const double* A, int32_t p, int32_t iters, double inflate, double* rq, double* gersh);
+double orc_d_rule(const double* A, int32_t p, int32_t squarings, double* U, double* gersh);
 
 /* ---- thresholding operators (§2.2, eqs lasso/net/mcp/scad/glasso/gmcp/gscad).
  * lam is the already-weighted level (w_j*lambda or c_k*lambda). */
@@ -98,15 +99,17 @@ double orc_objective(const double* G, const double* c, int32_t p, const double* 
                      const int32_t* group, int32_t ngroups, const double* grp_w);
 
 /* ---- O7 logistic proximal Newton (§4; R#23-26). For each lambda (warm start):
- * repeat outer: O3 at beta; normalize by n; d_w by the power rule (power_iters, inflate);
- * inner OEM for the single lambda from beta (tol_in, maxit_in); stop when
- * max|beta_new - beta| <= tol_out or outer_maxit. Lasso family only (cfg5).
- * outer_iters: L; inner_iters: L (sum over outer steps); conv: L. */
-int orc_logistic_path(const double* X, const double* y01, int64_t n, int32_t p, int64_t ldx,
-                      const double* lambdas, int32_t L, double eps, double tol_in, int64_t maxit_in,
-                      double tol_out, int32_t outer_maxit, int32_t power_iters, double inflate,
+ * repeat outer: O3 at beta; normalize by n; d_w by the d rule (squarings); inner OEM (O6) for
+ * the single lambda from beta with the given penalty family (any of Table 1, groups as in O6;
+ * tol_in, maxit_in); stop when max|beta_new - beta| <= tol_out or outer_maxit.
+ * outer_iters: L; inner_iters: L (sum over outer steps); conv: L; d_out (optional): d_w of the
+ * first outer step. Returns 0, -1 (y not 0/1) or -1 from O6 (invalid penalty parameters). */
+int orc_logistic_path(const double* X, const double* y01, int64_t n, int32_t p, int64_t ldx, int family,
+                      double gamma, double alpha, const double* w, const int32_t* group, int32_t ngroups,
+                      const double* grp_w, const double* lambdas, int32_t L, double eps, double tol_in,
+                      int64_t maxit_in, double tol_out, int32_t outer_maxit, int32_t squarings,
                       double* beta_out, int32_t* outer_iters, int64_t* inner_iters, uint8_t* conv,
-                      int nthreads);
+                      double* d_out, int nthreads);
 
 #ifdef __cplusplus
 }

@@ -14,37 +14,71 @@ import oracle as orc
 
 # ------------------------------------------------------------------ d
 def test_eigen_examples(golden):
-    for ex in golden["largest_eigenvalue"]:  # S:L94-95
+    """d(I_2) = 1 and d([[2,1],[1,2]]) = 3 EXACTLY: both are Gershgorin-tight
+    (constant row sums of a nonnegative matrix), so the rule's min takes the Gershgorin value."""
+    for ex in golden["largest_eigenvalue"]:
         A = np.array(ex["A"])
         assert abs(orc.eig_jacobi(A)[-1] - ex["lambda1"]) < 1e-15
-        d, rq, gs = orc.power_rule(A)
-        assert ex["lambda1"] <= d <= ex["lambda1"] * 1.01
+        d, U, gs = orc.d_rule(A)
+        assert d == ex["lambda1"] and gs == ex["lambda1"]
+        assert U > ex["lambda1"]            # the trace bound is the looser branch here
 
 
-def test_jacobi_matches_library_and_closed_forms():
-    rng = np.random.default_rng(7)
-    for p in (3, 10, 31):
-        B = rng.standard_normal((3 * p, p))
-        A = B.T @ B / (3 * p)
-        ev = orc.eig_jacobi(A)
-        assert np.max(np.abs(ev - np.linalg.eigvalsh(A))) < 1e-13 * ev[-1]
-    # block equicorrelation population matrix: eigenvalues 1 + (m-1) r (x groups), 1 - r
-    m, r, ng = 10, 0.4, 5
-    A = np.kron(np.eye(ng), np.full((m, m), r)) + (1 - r) * np.eye(m * ng)
-    ev = orc.eig_jacobi(A)
-    assert abs(ev[-1] - (1 + (m - 1) * r)) < 1e-13 and abs(ev[0] - (1 - r)) < 1e-13
-    # AR(1) Toeplitz: extremes approach (1+rho)/(1-rho), (1-rho)/(1+rho) as p grows
-    rho, p = 0.5, 200
-    T = rho ** np.abs(np.subtract.outer(np.arange(p), np.arange(p)))
-    ev = orc.eig_jacobi(T)
-    assert abs(ev[-1] - 3.0) < 3e-3 and abs(ev[0] - 1 / 3) < 3e-3
-    assert np.max(np.abs(ev - np.linalg.eigvalsh(T))) < 1e-12
+PHI2 = (3.0 + math.sqrt(5.0)) / 2.0        # largest eigenvalue of [[2,1],[1,1]]
+ALLOW = 2 * 12 * 2.0 ** -53                 # R#5 rounding allowance (1 + 2 S p u), per unit of p
 
 
-@pytest.mark.parametrize("kind", ["ar1_0.5", "ar1_0.3", "block_0.4", "iid"])
-def test_power_rule_brackets_lambda1(kind):
-    """R#5: d = min(Gershgorin, 1.005 RQ_200) satisfies lambda_1 <= d <= 1.01 lambda_1 on the
-    configs' population Grams and on sample Grams of those designs."""
+def test_d_rule_trace_branch_closed_forms():
+    """R#5 values by hand where the trace branch U_S is the one taken (Gershgorin = 3):
+    [[2,1],[1,1]] has eigenvalues phi^2, phi^-2, so U_S = phi^2 (1 + phi^(-4 * 2^S))^(2^-S) = phi^2
+    in fp64; two copies (block diagonal) double every eigenvalue's multiplicity, so
+    U_S = 2^(2^-S) phi^2 -- which pins the exponent S = 12 (S = 11 or 13 differ by 1.7e-4 / 8.5e-5
+    relative). A scalar multiple scales d exactly linearly."""
+    A = np.array([[2.0, 1.0], [1.0, 1.0]])
+    d, U, gs = orc.d_rule(A)
+    assert gs == 3.0 and abs(d - PHI2 * (1 + ALLOW * 2)) <= 4e-16 * PHI2
+    B = np.kron(np.eye(2), A)
+    d2, U2, gs2 = orc.d_rule(B)
+    assert gs2 == 3.0 and abs(d2 - PHI2 * 2.0 ** (1.0 / 4096) * (1 + ALLOW * 4)) <= 4e-16 * PHI2
+    assert abs(d2 / PHI2 - 1.0 - math.log(2.0) / 4096) < 1e-7
+    d7, _, _ = orc.d_rule(7.0 * B)
+    assert abs(d7 - 7.0 * d2) <= 1e-15 * d7
+    # p copies of one eigenvalue: U_S = c p^(2^-S) exactly, Gershgorin = c (d = c)
+    for p in (1, 3, 50):
+        dI, UI, gI = orc.d_rule(2.5 * np.eye(p))
+        assert dI == 2.5 and abs(UI - 2.5 * p ** (1.0 / 4096) * (1 + ALLOW * p)) <= 1e-15 * UI
+    # the number of squarings is an argument: S = 1 gives sqrt(trace(A^2)) = ||A||_F
+    _, U1, _ = orc.d_rule(A, squarings=1)
+    assert abs(U1 - math.sqrt(7.0) * (1 + 4 * 2.0 ** -53)) <= 1e-15 * U1
+
+
+def test_d_rule_eigenvector_orthogonal_to_ones():
+    """a rule seeded with 1/sqrt(p) under-estimated lambda_1 when the top
+    eigenvector is orthogonal to the all-ones vector. The trace bound does not depend on any
+    start vector: d >= lambda_1 on every such case."""
+    cases = []
+    cases.append(np.array([[1.0, -0.482], [-0.482, 1.0]]))        # standardized p = 2, rho < 0
+    cases.append(np.eye(3) - np.full((3, 3), 1.0 / 3.0))          # centred 3-simplex (1 in the null space)
+    rng = np.random.default_rng(11)
+    Xpm = rng.choice([-1.0, 1.0], size=(64, 6))
+    Xpm[:, 1] = -Xpm[:, 0]                                        # perfectly negatively correlated +-1 pair
+    cases.append(Xpm.T @ Xpm / 64)
+    D = np.eye(4)[rng.integers(0, 4, 200)]                         # one-hot dummies, centred
+    D -= D.mean(axis=0)
+    cases.append(D.T @ D / 200)
+    for A in cases:
+        lam1 = np.linalg.eigvalsh(A)[-1]
+        d, U, gs = orc.d_rule(A)
+        assert lam1 <= d * (1 + 1e-13)
+        assert d <= lam1 * A.shape[0] ** (1.0 / 4096) * (1 + ALLOW * A.shape[0] + 1e-14)
+
+
+@pytest.mark.parametrize("kind", ["ar1_0.5", "ar1_0.3", "block_0.4", "iid", "spike"])
+def test_d_rule_brackets_lambda1(kind):
+    """R#5: lambda_1 <= U_S <= p^(2^-S) lambda_1 (the trace inequality), so
+    lambda_1 <= d <= 1.0012 lambda_1 at p = 100, with lambda_1 from cyclic Jacobi and numpy, on
+    the configs' population Grams, on sample Grams of those designs, and on a spike barely above
+    a 99-fold bulk (the case a 200-step Rayleigh quotient misses by 0.5%)."""
     rng = np.random.default_rng(8)
     p = 100
     if kind.startswith("ar1"):
@@ -52,15 +86,38 @@ def test_power_rule_brackets_lambda1(kind):
         S = rho ** np.abs(np.subtract.outer(np.arange(p), np.arange(p)))
     elif kind.startswith("block"):
         S = np.kron(np.eye(10), np.full((10, 10), 0.4)) + 0.6 * np.eye(p)
+    elif kind == "spike":
+        Q, _ = np.linalg.qr(rng.standard_normal((p, p)))
+        S = Q @ np.diag(np.r_[1.0, np.full(p - 1, 0.99)]) @ Q.T
+        S = (S + S.T) / 2
     else:
         S = np.eye(p)
     L = np.linalg.cholesky(S)
     for A in (S, (lambda Z: Z.T @ Z / Z.shape[0])(rng.standard_normal((4000, p)) @ L.T)):
         lam1 = np.linalg.eigvalsh(A)[-1]
-        d, rq, gs = orc.power_rule(A)
-        assert rq <= lam1 * (1 + 1e-12)          # Rayleigh quotient never exceeds lambda_1
+        assert abs(orc.eig_jacobi(A)[-1] - lam1) <= 1e-13 * lam1
+        d, U, gs = orc.d_rule(A)
         assert gs >= lam1 * (1 - 1e-12)          # Gershgorin bound
-        assert lam1 * (1 - 1e-12) <= d <= 1.01 * lam1
+        assert U >= lam1 * (1 - 1e-13)           # trace bound
+        assert U <= lam1 * p ** (1.0 / 4096) * (1 + ALLOW * p + 1e-14)
+        assert d == min(gs, U)
+
+
+def test_d_rule_trace_sum_matches_eigenvalues():
+    """U_S^(2^S) = sum_i lambda_i^(2^S): for a matrix with a known spectrum the rule's value is
+    that sum's root, computed here in logs from the eigenvalues themselves."""
+    rng = np.random.default_rng(5)
+    p = 12
+    lam = np.sort(rng.uniform(0.5, 2.0, p))
+    lam[-3:] = [1.9, 1.95, 2.0]
+    Q, _ = np.linalg.qr(rng.standard_normal((p, p)))
+    A = Q @ np.diag(lam) @ Q.T
+    A = (A + A.T) / 2
+    _, U, _ = orc.d_rule(A)
+    m = 4096.0
+    expect = lam[-1] * np.exp(np.log(np.sum(np.exp(m * (np.log(lam) - np.log(lam[-1]))))) / m)
+    expect *= 1 + ALLOW * p
+    assert abs(U - expect) <= 1e-13 * expect
 
 
 # ------------------------------------------------------------------ thresholds: printed values

@@ -41,7 +41,7 @@ def test_lambda_max_is_smallest_null_fixed_point(family, alpha):
     """beta = 0 is a fixed point at lambda_max but not at lambda_max (1 - 1e-3)."""
     G, c = small_problem(12, 400, 6)
     grp = np.array([0, 0, 1, 1, 2, 2], dtype=np.int32) if family.startswith("grp") else None
-    d = orc.power_rule(G)[0]
+    d = orc.d_rule(G)[0]
     lm = orc.lambda_max(family, c, group=grp, alpha=alpha)
     b, it, _ = orc.oem_path(G, c, d, family, [lm], gamma=3.7, alpha=alpha, group=grp, maxit=1)
     assert not b.any()
@@ -61,7 +61,7 @@ def test_lambda_grid_shape():
 def test_lambda_zero_is_ols():
     """lambda = 0 -> the normal-equation solution (north star)."""
     G, c = small_problem(13, 500, 8)
-    d = orc.power_rule(G)[0]
+    d = orc.d_rule(G)[0]
     for fam in ("lasso", "mcp", "scad", "enet"):
         b, it, cv = orc.oem_path(G, c, d, fam, [0.0], gamma=3.0, alpha=0.5, tol=1e-14, maxit=200000)
         assert cv[0]
@@ -91,7 +91,7 @@ def test_orthogonal_design_one_step():
 
 def test_enet_alpha0_is_ridge():
     G, c = small_problem(15, 300, 7)
-    d = orc.power_rule(G)[0]
+    d = orc.d_rule(G)[0]
     for lam in (0.01, 0.3, 2.0):
         b, _, cv = orc.oem_path(G, c, d, "enet", [lam], alpha=0.0, tol=1e-14)
         assert cv[0]
@@ -122,7 +122,7 @@ def test_lasso_kkt_every_lambda_cfg1():
 def test_group_lasso_kkt():
     G, c = small_problem(16, 600, 9)
     grp = np.repeat(np.arange(3), 3).astype(np.int32)
-    d = orc.power_rule(G)[0]
+    d = orc.d_rule(G)[0]
     lm = orc.lambda_max("grp_lasso", c, group=grp)
     lams = orc.lambda_grid(lm, 20, 1e-2)
     B, _, cv = orc.oem_path(G, c, d, "grp_lasso", lams, group=grp, tol=1e-13)
@@ -213,7 +213,7 @@ def mcp_regions_enumerate(G, c, lam, gamma, kind):
 def test_lasso_brute_force_tiny_p():
     for seed in range(5):
         G, c = small_problem(100 + seed, 200, 3, rho=0.5)
-        d = orc.power_rule(G)[0]
+        d = orc.d_rule(G)[0]
         for frac in (0.9, 0.5, 0.1, 0.01):
             lam = frac * orc.lambda_max("lasso", c)
             b, _, cv = orc.oem_path(G, c, d, "lasso", [lam], tol=1e-14)
@@ -229,7 +229,7 @@ def test_nonconvex_brute_force_on_convex_instances(kind, gamma):
         G, c = small_problem(200 + seed, 300, 3, rho=0.2)
         lmin = np.linalg.eigvalsh(G)[0]
         assert lmin > (1 / gamma if kind == "mcp" else 1 / (gamma - 1))
-        d = orc.power_rule(G)[0]
+        d = orc.d_rule(G)[0]
         for frac in (0.8, 0.4, 0.1):
             lam = frac * orc.lambda_max(kind, c)
             b, _, cv = orc.oem_path(G, c, d, kind, [lam], gamma=gamma, tol=1e-14)
@@ -240,7 +240,7 @@ def test_nonconvex_brute_force_on_convex_instances(kind, gamma):
 def test_coordinate_descent_agreement():
     """An independent solver (cyclic coordinate descent, Friedman et al. 2010) on EN."""
     G, c = small_problem(17, 400, 10, rho=0.5)
-    d = orc.power_rule(G)[0]
+    d = orc.d_rule(G)[0]
     lam, alpha = 0.05, 0.5
     b_oem, _, _ = orc.oem_path(G, c, d, "enet", [lam], alpha=alpha, tol=1e-14)
     b = np.zeros(10)
@@ -258,7 +258,7 @@ def test_descent_each_iteration(family):
     For the sparse group lasso this also checks the exact composition (R#11) is the M-step."""
     G, c = small_problem(18, 500, 6, rho=0.5)
     grp = np.array([0, 0, 1, 1, 2, 2], dtype=np.int32) if family.startswith("grp") or family == "sgl" else None
-    d = orc.power_rule(G)[0]
+    d = orc.d_rule(G)[0]
     lam = 0.2 * orc.lambda_max(family, c, group=grp, alpha=0.5)
     b = np.zeros(6)
     f = orc.objective(G, c, b, family, lam, 3.0, 0.5, group=grp)
@@ -379,7 +379,7 @@ def test_sgl_kkt_and_limits_on_path():
     reproduces the group-lasso path and tau = 1 the lasso path."""
     G, c = small_problem(23, 800, 9, rho=0.4)
     grp = np.repeat(np.arange(3), 3).astype(np.int32)
-    d = orc.power_rule(G)[0]
+    d = orc.d_rule(G)[0]
     tau = 0.4
     lams = orc.lambda_grid(orc.lambda_max("sgl", c, group=grp, alpha=tau), 12)
     B, _, cv = orc.oem_path(G, c, d, "sgl", lams, alpha=tau, group=grp, tol=1e-14)
