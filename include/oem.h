@@ -114,8 +114,7 @@ typedef struct {
   const int32_t* group;     /* host, p group ids in [0, ngroups), or NULL */
   int32_t ngroups;
   const double* grp_w;      /* host, ngroups or NULL (= sqrt(group size), R#12) */
-  int32_t power_iters;      /* d rule (R#5): default 200 */
-  double d_inflate;         /* d rule (R#5): default 5e-3 */
+  int32_t d_squarings;      /* d rule (R#5): S in d = min(Gershgorin, trace(G^(2^S))^(1/2^S)); default 12 */
   int32_t fold_mode;        /* 1: inputs are K fold sums -> fit full data + K complements (R#20-22) */
   const double* lambda_max_override; /* host, optional: use this lambda_max for every unit */
   /* f3 (R#2-3): with xsum/ysum (device: nG*p raw column sums X^T 1 and nG raw 1^T y, in the
@@ -156,23 +155,26 @@ void oem_path_cfg_default(oem_path_cfg* cfg);
 /* ---- a4 + a6-a9 driven to convergence: the proximal-Newton logistic path (§4,
  * glmnet-style outer loop with OEM as the inner solver; R#23-27). For each lambda (warm start
  * from the previous solution): repeat { oem_gram_weighted at beta (allreduced over ranks);
- * normalise by n; d_w by the power rule; single-lambda OEM solve from beta } until
- * max_j |beta_new - beta| <= tol_out or outer_maxit. The lambda grid runs from
- * lambda_max = max_j |(1/n) sum_i x_ij (y_i - 1/2)| / (w_j [alpha for EN]) (R#14, no intercept)
- * down to ratio * lambda_max (R#15), unless an explicit grid is given. Coordinate-wise
- * families only (lasso, EN, MCP, SCAD). Host loop: one scalar device->host read per outer step.
+ * normalise by n; d_w by the d rule (R#5); single-lambda OEM solve from beta } until
+ * max_j |beta_new - beta| <= tol_out or outer_maxit. The lambda grid runs from lambda_max
+ * (R#14, no intercept; c = (1/n) sum_i x_i (y_i - 1/2), the working statistic at beta = 0):
+ * max_j |c_j| / (w_j [alpha for EN]) for the coordinate families, max_k ||c_{g_k}|| / c_k for
+ * group lasso / MCP / SCAD (§6.3 fits group penalties to logistic models), down to
+ * ratio * lambda_max (R#15), unless an explicit grid is given. The sparse group lasso is not
+ * offered here (OEM_ERR_INVALID_ARG). Host loop: one scalar device->host read per outer step.
  * Outputs: beta_out (device, L*p), lambda_out (device, L), outer_iters / inner_iters /
  * converged (host, L). Errors: as oem_gram_weighted and oem_fit_path. */
 typedef struct {
   int32_t nlambda; double lambda_min_ratio; const double* lambda /*host, optional*/;
   double tol_in; int64_t maxit_in; double tol_out; int32_t outer_maxit;
-  double eps; int32_t power_iters; double d_inflate; const double* var_w /*device p or NULL*/;
+  double eps; int32_t d_squarings; const double* var_w /*device p or NULL*/;
+  const int32_t* group; int32_t ngroups; const double* grp_w; /* host; group families as in oem_path_cfg */
   int32_t hessian_upper_bound; /* f1 (R#27): w_i = 1/4. The Gram X^T X and d_w are
                                   formed once (a2 pass); each outer step is one oem_logit_grad
                                   pass and c = X^T X beta + 4 X^T (y - mu), normalised by 4n.
                                   Needs p <= 512. */
 } oem_logistic_cfg;
-void oem_logistic_cfg_default(oem_logistic_cfg* cfg);  /* 50, 1e-3, NULL, 1e-11, 1e5, 1e-10, 100, 1e-5, 200, 5e-3, NULL, 0 */
+void oem_logistic_cfg_default(oem_logistic_cfg* cfg);  /* 50, 1e-3, NULL, 1e-11, 1e5, 1e-10, 100, 1e-5, 12, NULL, NULL, 0, NULL, 0 */
 
 /* ---- f1 logistic gradient pass (P:L357-359 mu(x) = 1/(1 + exp(-x^T beta)); P:L385-389 the
  * upper-bound step needs only X^T (y - mu)). One HBM-bound pass over [X | y]: g = sum_i

@@ -141,6 +141,8 @@ oem_status oem_ctx_destroy(oem_ctx* ctx) {
   ctx->plan_tables.release();
   ctx->path_ws.release();
   ctx->path_small.release();
+  ctx->logi.release();
+  ctx->drule_ws.release();
   ctx->lg_part.release();
   ctx->lg_out.release();
   ctx->mom_part.release();

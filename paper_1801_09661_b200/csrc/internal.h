@@ -57,7 +57,7 @@ struct oem_ctx {
   int nranks = 1, rank = 0;
   int num_sms = 148;
   void* nccl_comm = nullptr;  // ncclComm_t
-  oem::DevBuf partial, partial2, counts_dev, partial_scal, packed, tail, plan_tables, path_ws, path_small, logi, lg_part, lg_out, mom_part, mom_out, stage0, stage1;
+  oem::DevBuf partial, partial2, counts_dev, partial_scal, packed, tail, plan_tables, path_ws, path_small, logi, lg_part, lg_out, mom_part, mom_out, stage0, stage1, drule_ws;
   cudaStream_t copy_stream = nullptr;  // f4 host streaming: H2D copies overlap the Gram kernel
   cudaEvent_t ev_copied[2] = {nullptr, nullptr}, ev_used[2] = {nullptr, nullptr};
   std::map<std::tuple<int, int, int64_t, int>, std::shared_ptr<oem::GramPlan>> plans;
@@ -115,6 +115,9 @@ oem_status host_allreduce_i64(oem_ctx* ctx, int64_t* vals, int n, cudaStream_t s
 // f1 (logit_ub.cu): out[0..p) = X^T (y - sigma(X beta)), out[p] = loglik, raw sums allreduced
 oem_status logit_grad_pass(oem_ctx* ctx, const double* X, const double* y01, const double* beta, int64_t n_local,
                            int p, int64_t ldx, double* out, cudaStream_t st);
+// a7 (drule.cu): d[u] = min(Gershgorin, trace(G_u^(2^S))^(1/2^S) (1 + 2Spu)) for the nU normalised
+// p x p unit Grams Gn (R#5); d_out device [nU]
+oem_status d_rule(oem_ctx* ctx, const double* Gn, int nU, int p, int S, double* d_out, cudaStream_t st);
 // c = G beta + 4 g (the raw right-hand side of the upper-bound step)
 oem_status ub_rhs(oem_ctx* ctx, const double* G, const double* beta, const double* g, int p, double* c, cudaStream_t st);
 

@@ -44,9 +44,11 @@ extern "C" void oem_logistic_cfg_default(oem_logistic_cfg* c) {
   c->tol_out = 1e-10;
   c->outer_maxit = 100;
   c->eps = 1e-5;
-  c->power_iters = 200;
-  c->d_inflate = 5e-3;
+  c->d_squarings = 12;
   c->var_w = nullptr;
+  c->group = nullptr;
+  c->ngroups = 0;
+  c->grp_w = nullptr;
   c->hessian_upper_bound = 0;
 }
 
@@ -60,8 +62,13 @@ extern "C" oem_status oem_fit_logistic(oem_ctx* ctx, const double* X, const doub
   oem_logistic_cfg cfg;
   if (cfg_in) cfg = *cfg_in;
   else oem_logistic_cfg_default(&cfg);
-  if (pen->family > OEM_SCAD || pen->family < OEM_LASSO)
-    OEM_FAIL(OEM_ERR_INVALID_ARG, "oem_fit_logistic: coordinate-wise families only (lasso, EN, MCP, SCAD)");
+  if (pen->family > OEM_GRP_SCAD || pen->family < OEM_LASSO)
+    OEM_FAIL(OEM_ERR_INVALID_ARG, "oem_fit_logistic: families lasso, EN, MCP, SCAD, group lasso / MCP / SCAD");
+  const bool grp = pen->family >= OEM_GRP_LASSO;
+  if (grp && (!cfg.group || cfg.ngroups < 1)) OEM_FAIL(OEM_ERR_INVALID_ARG, "oem_fit_logistic: group penalty needs cfg.group");
+  if (cfg.group)
+    for (int j = 0; j < p; ++j)
+      if (cfg.group[j] < 0 || cfg.group[j] >= cfg.ngroups) OEM_FAIL(OEM_ERR_INVALID_ARG, "oem_fit_logistic: group id out of range");
   if (cfg.nlambda < 1 || cfg.outer_maxit < 1 || !(cfg.tol_out > 0.0))
     OEM_FAIL(OEM_ERR_INVALID_ARG, "oem_fit_logistic: need nlambda >= 1, outer_maxit >= 1, tol_out > 0");
   cudaStream_t st = (cudaStream_t)stream;
@@ -123,8 +130,22 @@ extern "C" oem_status oem_fit_logistic(oem_ctx* ctx, const double* X, const doub
     OEM_CUDA_TRY(cudaStreamSynchronize(st));
     const double scale = pen->family == OEM_ENET ? pen->alpha : 1.0;
     double lmax = 0.0;
-    for (int j = 0; j < p; ++j)  // c_w at beta = 0 is sum_i x_ij (y_i - 1/2)
-      if (hw[j] > 0.0) lmax = std::fmax(lmax, std::fabs(hc[j] / (double)n_total) / (scale * hw[j]));
+    if (!grp) {
+      for (int j = 0; j < p; ++j)  // c_w at beta = 0 is sum_i x_ij (y_i - 1/2)
+        if (hw[j] > 0.0) lmax = std::fmax(lmax, std::fabs(hc[j] / (double)n_total) / (scale * hw[j]));
+    } else {  // max_k ||c_{g_k}|| / c_k (R#12, R#14)
+      std::vector<double> ss(cfg.ngroups, 0.0);
+      std::vector<int> sz(cfg.ngroups, 0);
+      for (int j = 0; j < p; ++j) {
+        const double c = hc[j] / (double)n_total;
+        ss[cfg.group[j]] += c * c;
+        sz[cfg.group[j]]++;
+      }
+      for (int g = 0; g < cfg.ngroups; ++g) {
+        const double cg = cfg.grp_w ? cfg.grp_w[g] : std::sqrt((double)sz[g]);
+        if (cg > 0.0) lmax = std::fmax(lmax, std::sqrt(ss[g]) / cg);
+      }
+    }
     for (int l = 0; l < L; ++l)
       lam[l] = L == 1 ? lmax : lmax * std::exp(((double)l / (double)(L - 1)) * std::log(cfg.lambda_min_ratio));
   }
@@ -135,8 +156,10 @@ extern "C" oem_status oem_fit_logistic(oem_ctx* ctx, const double* X, const doub
   pc.tol = cfg.tol_in;
   pc.maxit = cfg.maxit_in;
   pc.var_w = cfg.var_w;
-  pc.power_iters = cfg.power_iters;
-  pc.d_inflate = cfg.d_inflate;
+  pc.d_squarings = cfg.d_squarings;
+  pc.group = cfg.group;
+  pc.ngroups = cfg.ngroups;
+  pc.grp_w = cfg.grp_w;
   bool have_gram = true;
   // upper-bound mode: G/(4n) and d_w are the same at every step; d_w is computed by the first
   // solve and passed in afterwards

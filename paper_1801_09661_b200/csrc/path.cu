@@ -1,11 +1,11 @@
-// path.cu — a6-a10 of the hot path on sm_100a: normalise the unit Grams, d by power iteration,
-// the lambda grid, and the OEM path iterations for every (Gram, penalty) unit.
+// path.cu — a6, a8-a10 of the hot path on sm_100a: normalise the unit Grams, the lambda grid, and
+// the OEM path iterations for every (Gram, penalty) unit (a7, d, runs in drule.cu in between).
 //
 // The method: OEM's EM step in closed form, u = X^T y + (dI - X^T X) beta
 // (P:L171-172), followed by the penalty's thresholding M-step (eqs lasso / net /
 // mcp / scad / glasso / gmcp / gscad), iterated to convergence along a warm-started lambda path
 // (R#17-18), for several penalties sharing one Gram (§5.2) and for the K fold
-// complements of fast CV (§3). d >= lambda_1 by the power rule R#5.
+// complements of fast CV (§3). d >= lambda_1 by the d rule R#5 (drule.cu).
 //
 // B200 design: one persistent cooperative launch. Each unit Gram g is owned by a group of C_g
 // CTAs; CTA c keeps its slice of rows of G resident in shared memory for the whole path (the
@@ -391,69 +391,6 @@ __device__ __forceinline__ void row_matvec(const PathParams& P, const CtaView& v
   }
 }
 
-// ---------------------------------------------------------------- K4: power iteration for d (R#5)
-// v0 = 1/sqrt(p); v <- Gv/||Gv|| for `iters` steps; RQ = v^T G v; d = min(Gershgorin, (1+inflate) RQ).
-// Cross-CTA sums go through per-CTA slots summed in rank order (deterministic); the new vector
-// is exchanged through L2 (double-buffered by step parity).
-__global__ void __launch_bounds__(PT, 1)
-power_kernel(const PathParams P, int iters, double inflate, double* wbuf /*[2][nU][p]*/,
-             double* pslot /*[3][nU][Cmax]*/, int Cmax, double* d_out) {
-  extern __shared__ __align__(16) double sm[];
-  const CtaView v = cta_view(P);
-  double* Gs = sm;
-  double* vec = Gs + (size_t)P.smem_rows * P.ps;
-  double* uv = vec + P.ps;
-  double* red = uv + P.smem_rows;
-  unsigned* bar = P.bar + 2 * v.unit;
-  load_rows(P, v, Gs);
-  const double v0 = 1.0 / sqrt((double)P.p);
-  for (int k = threadIdx.x; k < P.p; k += blockDim.x) vec[k] = v0;
-  __syncthreads();
-  // Gershgorin bound: local max row sum -> slot 2
-  row_matvec(P, v, Gs, vec, uv, true);
-  __syncthreads();
-  double gm = 0.0;
-  for (int r = threadIdx.x; r < v.nr; r += blockDim.x) gm = fmax(gm, uv[r]);
-  gm = block_max(gm, red);
-  double* gslot = pslot + ((size_t)2 * P.nU + v.unit) * Cmax;
-  if (threadIdx.x == 0) gslot[v.rank] = gm;
-  for (int it = 0; it <= iters; ++it) {
-    row_matvec(P, v, Gs, vec, uv, false);
-    __syncthreads();
-    const int par = it & 1;
-    double* wb = wbuf + ((size_t)par * P.nU + v.unit) * P.p;
-    double* ps = pslot + ((size_t)par * P.nU + v.unit) * Cmax;
-    double x = 0.0;
-    if (it < iters) {
-      for (int r = threadIdx.x; r < v.nr; r += blockDim.x) {
-        const double w = uv[r];
-        x += w * w;
-        if (v.C > 1) wb[v.j0 + r] = w;
-        else wb[r] = w;
-      }
-    } else {
-      for (int r = threadIdx.x; r < v.nr; r += blockDim.x) x += vec[v.j0 + r] * uv[r];  // RQ partial
-    }
-    const double s = block_sum(x, red);
-    if (threadIdx.x == 0) ps[v.rank] = s;
-    __threadfence();
-    group_barrier(bar, v.C);
-    double tot = 0.0;
-    for (int c = 0; c < v.C; ++c) tot += __ldcg(ps + c);
-    if (it < iters) {
-      const double nrm = sqrt(tot);
-      if (nrm > 0.0)
-        for (int k = threadIdx.x; k < P.p; k += blockDim.x) vec[k] = __ldcg(wb + k) / nrm;
-      __syncthreads();
-    } else if (v.rank == 0 && threadIdx.x == 0) {
-      double g = 0.0;
-      for (int c = 0; c < v.C; ++c) g = fmax(g, __ldcg(gslot + c));
-      const double dd = (1.0 + inflate) * tot;
-      d_out[v.unit] = g < dd ? g : dd;
-    }
-  }
-}
-
 // ---------------------------------------------------------------- K5: the persistent OEM path solver
 template <int NPT>
 __global__ void __launch_bounds__(PT, 1) path_kernel(const PathParams P) {
@@ -678,7 +615,7 @@ __global__ void __launch_bounds__(PT, 1) path_kernel(const PathParams P) {
 // One thread-block cluster per unit Gram (C <= 16 CTAs, one per SM). CTA `rank` owns rows
 // [j0, j1) of the unit's normalised Gram; each thread keeps its share of those rows in
 // registers (first EREG elements) and shared memory (the rest, thread-major so warp reads are
-// conflict free) for the whole launch: d by power iteration (R#5), the lambda grid (R#14-15) and
+// conflict free) for the whole launch: the lambda grid (R#14-15) and
 // the OEM paths all run from on-chip copies of G.
 // Per iteration every CTA pushes its rows of the new beta (and its partial max |dbeta|) into the
 // shared memory of every CTA of the cluster (DSMEM stores), then the cluster meets at one
@@ -692,11 +629,7 @@ struct ClusterArgs {
   int NRT;        // rows per thread = ceil(max rows / RG)
   int S;          // shared-memory G slots per thread
   int pv;         // padded vector length (>= p)
-  int power_iters;
-  double inflate;
-  int compute_d;
   int maxrows;    // max rows per CTA (shared-memory row tables)
-  double* d_out;  // [nU]
 };
 
 __device__ __forceinline__ void cluster_sync_all() {
@@ -731,10 +664,6 @@ struct LeanArgs {
   int qsplit;       // 1: one cluster per (unit, penalty) (kernel instantiated with NPT = 1)
   int rows;         // max rows per CTA (= R * RG)
   int pvl;          // padded vector length (= KC * T >= p)
-  int power_iters;
-  double inflate;
-  int compute_d;
-  double* d_out;    // [nU]
 };
 
 __device__ __forceinline__ void st_cl_f64(double* local, uint32_t rank, double v) {
@@ -854,23 +783,6 @@ __device__ __forceinline__ void lean_matvec(double (&a)[VP], const double* vc, i
       }
   }
 }
-// the power iteration's matvec (one vector, penalty slot 0 of the layout: stride ST doubles)
-template <int RT, int KC, int T, int ST, int RP, class GEL>
-__device__ __forceinline__ void lean_matvec1(double (&a)[RP], const double* vc, int kcu, int tl, GEL gel) {
-  constexpr int MC = KC < 4 ? KC : 4;
-#pragma unroll
-  for (int m0 = 0; m0 < KC; m0 += MC) {
-    if (m0 >= kcu) break;
-    double b[MC];
-#pragma unroll
-    for (int mm = 0; mm < MC; ++mm) b[mm] = vc[ST * (tl + (m0 + mm) * T)];
-#pragma unroll
-    for (int mm = 0; mm < MC; ++mm)
-#pragma unroll
-      for (int i = 0; i < RT; ++i) a[i] = fma(gel(i, m0 + mm), b[mm], a[i]);
-  }
-}
-
 // RS > 0: each thread row group also owns RS rows kept in SHARED memory (for units whose rows do
 // not fit the register file, e.g. cfg3's eleven p = 500 Grams in clusters of 8). Thread (rg, tl)
 // owns local rows rg*RT + i, i < RT = R + RS: i < R from registers, i >= R from shared memory.
@@ -959,83 +871,10 @@ __global__ void __launch_bounds__(NTH, 1) fit_lean_kernel(const PathParams P, co
     c_my[s2] = act[s2] ? cu[mj[s2]] : 0.0;
     w_my[s2] = (act[s2] && P.var_w) ? P.var_w[mj[s2]] : 1.0;
   }
-  // power iteration: an RT-value reduce-scatter; the lane owns row rg*RT + vidx1
-  constexpr int RP = pow2ceil(RT);
-  const int vidx1 = lean_vidx<RP, T>(tl);
-  const int pr = rg * RT + vidx1;
-  const bool pact = (tl & (T / RP - 1)) == 0 && vidx1 < RT && pr < nr;
   cluster_sync_all();  // peers' buffers are zeroed before any remote store
 
-  // ======================================================= a7: d by power iteration (R#5)
-  double d;
-  if (A.compute_d) {
-    // Gershgorin bound: max_j sum_k |G_jk|
-    double gm = 0.0;
-#pragma unroll
-    for (int i = 0; i < RT; ++i) {
-      double s = 0.0;
-#pragma unroll
-      for (int m = 0; m < KC; ++m) s += fabs(gel(i, m));
-#pragma unroll
-      for (int o = T / 2; o >= 1; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
-      if (rg * RT + i < nr) gm = fmax(gm, s);
-    }
-#pragma unroll
-    for (int o = 16; o >= 1; o >>= 1) gm = fmax(gm, __shfl_xor_sync(0xffffffffu, gm, o));
-    if (lane == 0)
-      for (int rr = 0; rr < C; ++rr) st_cl_f64(&slots[NW * C + rank * NW + warp], rr, gm);  // parity-1 slots
-    const double v0 = 1.0 / sqrt((double)p);
-    for (int k = tid; k < p; k += NTH) vec[vix<NPT>(0, k, pvl)] = v0;  // buffer 0, vector 0
-    cluster_sync_all();
-    double gersh = 0.0;
-    for (int e = 0; e < C * NW; ++e) gersh = fmax(gersh, slots[NW * C + e]);
-    cluster_sync_all();  // every CTA has read the Gershgorin slots before they are reused
-    // buffer b holds w (unnormalised); the iterate is v = w * sc
-    double sc = 1.0, rq = 0.0;
-    for (int it = 0; it <= A.power_iters; ++it) {
-      const int cur = it & 1, nxt = cur ^ 1;
-      const double* vc = vec + (size_t)cur * vstride;
-      double a[RP];
-#pragma unroll
-      for (int i = 0; i < RP; ++i) a[i] = 0.0;
-      if (wrows) lean_matvec1<RT, KC, T, NPT == 1 ? 1 : 2>(a, vc, kcu, tl, gel);
-      const double s = lean_rs<RP, T>(a, tl);
-      double part = 0.0;
-      if (pact) {
-        const int j = j0 + pr;
-        if (it < A.power_iters) {
-          const double y = s * sc;                 // (G v)_j
-          part = y * y;
-          double* dst = &vec[(size_t)nxt * vstride + vix<NPT>(0, j, pvl)];
-          if (C == 1) *dst = y;
-          else for (int rr = 0; rr < C; ++rr) st_cl_f64(dst, rr, y);
-        } else {
-          part = vc[vix<NPT>(0, j, pvl)] * s;      // w_j (G w)_j
-        }
-      }
-#pragma unroll
-      for (int o = 16; o >= 1; o >>= 1) part += __shfl_xor_sync(0xffffffffu, part, o);
-      if (lane == 0) {
-        if (C == 1) slots[cur * NW + warp] = part;
-        else for (int rr = 0; rr < C; ++rr) st_cl_f64(&slots[cur * NW * C + rank * NW + warp], rr, part);
-      }
-      sync_all();
-      double tot = 0.0;
-      for (int e = 0; e < C * NW; ++e) tot += slots[cur * NW * C + e];  // fixed order
-      if (it < A.power_iters) {
-        if (tot > 0.0) sc = 1.0 / sqrt(tot);
-      } else {
-        rq = tot * sc * sc;                         // v^T G v
-      }
-    }
-    const double dd = (1.0 + A.inflate) * rq;
-    d = gersh < dd ? gersh : dd;
-    if (rank == 0 && tid == 0) A.d_out[unit] = d;
-    cluster_sync_all();  // all reads of vec / slots are done before the path reuses them
-    for (int k = tid; k < 2 * vstride; k += NTH) vec[k] = 0.0;
-  } else {
-    d = P.d[unit];
-  }
+  // a7: d (>= lambda_1, R#5) was computed for every unit by d_rule (drule.cu) before this launch
+  const double d = P.d[unit];
 
   // ======================================================= a8: lambda grid (R#14-16, R#22)
   if (warp < NPT) {
@@ -1224,9 +1063,7 @@ struct GlobArgs {
   int Cmax;             // max CTAs per unit (slot stride)
   int qsplit;           // 1: one virtual unit per (unit, penalty), kernel instantiated with NPT = 1
   int nvu;              // virtual units (nU, or nU * nP with qsplit)
-  int rows, pvl, power_iters, compute_d;
-  double inflate;
-  double* d_out;        // [nU]
+  int rows, pvl;
   double* gvec;         // [2][nU][NV * pvl]
   unsigned long long* gflag;  // [2][nU][Cmax] (iteration tag << 32) | not-converged bits (zero at launch)
   double* gslot;        // [2][nU][Cmax]
@@ -1294,7 +1131,7 @@ __global__ void __launch_bounds__(NTH, 1) fit_glob_kernel(const PathParams P, co
     if (tid == 0) {
       red_release_add(&A.gcnt[vu], 1u);
       const unsigned target = (epoch + 1) * (unsigned)C;
-      while (ld_relaxed(&A.gcnt[vu]) < target) {}
+      while ((int)(ld_relaxed(&A.gcnt[vu]) - target) < 0) {}  // wrap-safe
       fence_acquire_gpu();
     }
     ++epoch;
@@ -1334,10 +1171,6 @@ __global__ void __launch_bounds__(NTH, 1) fit_glob_kernel(const PathParams P, co
   const int mj = j0 + mr;
   const double c_my = act ? cu[mj] : 0.0;
   const double w_my = (act && P.var_w) ? P.var_w[mj] : 1.0;
-  constexpr int RP = pow2ceil(RT);
-  const int vidx1 = lean_vidx<RP, T>(tl);
-  const int pr = rg * RT + vidx1;
-  const bool pact = (tl & (T / RP - 1)) == 0 && vidx1 < RT && pr < nr;
   // CTA sum of one double per thread, in warp order; result in s_tot after the call
   auto cta_sum = [&](double x) {
 #pragma unroll
@@ -1375,73 +1208,9 @@ __global__ void __launch_bounds__(NTH, 1) fit_glob_kernel(const PathParams P, co
     return r;
   };
 
-  // ======================================================= a7: d by power iteration (R#5)
-  double d;
+  // a7: d (>= lambda_1, R#5) from d_rule (drule.cu)
+  const double d = P.d[unit];
   int par = 0;
-  if (A.compute_d) {
-    double gm = 0.0;
-#pragma unroll
-    for (int i = 0; i < RT; ++i) {
-      double s = 0.0;
-#pragma unroll
-      for (int m = 0; m < KC; ++m) s += fabs(gel(i, m));
-#pragma unroll
-      for (int o = T / 2; o >= 1; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
-      if (rg * RT + i < nr) gm = fmax(gm, s);
-    }
-#pragma unroll
-    for (int o = 16; o >= 1; o >>= 1) gm = fmax(gm, __shfl_xor_sync(0xffffffffu, gm, o));
-    if (lane == 0) s_red[warp] = gm;
-    __syncthreads();
-    if (tid == 0) {
-      double t = 0.0;
-      for (int w = 0; w < NW; ++w) t = fmax(t, s_red[w]);
-      s_tot = t;
-    }
-    __syncthreads();
-    const double gersh = unit_reduce(s_tot, par, true);
-    par ^= 1;
-    const double v0 = 1.0 / sqrt((double)p);
-    for (int k = tid; k < p; k += NTH) vec[vix<NPT>(0, k, pvl)] = v0;
-    __syncthreads();
-    double sc = 1.0, rq = 0.0;
-    for (int it = 0; it <= A.power_iters; ++it) {
-      const int cur = it & 1, nxt = cur ^ 1;
-      const double* vc = vec + (size_t)cur * vstride;
-      double a[RP];
-#pragma unroll
-      for (int i = 0; i < RP; ++i) a[i] = 0.0;
-      if (wrows) lean_matvec1<RT, KC, T, NPT == 1 ? 1 : 2>(a, vc, kcu, tl, gel);
-      const double s = lean_rs<RP, T>(a, tl);
-      double part = 0.0;
-      if (pact) {
-        const int j = j0 + pr;
-        if (it < A.power_iters) {
-          const double y = s * sc;
-          part = y * y;
-          gvec[nxt * gpar + vix<NPT>(0, j, pvl)] = y;
-        } else {
-          part = vc[vix<NPT>(0, j, pvl)] * s;
-        }
-      }
-      const double tot = unit_reduce(cta_sum(part), par, false);
-      par ^= 1;
-      if (it < A.power_iters) {
-        for (int k = tid; k < p; k += NTH) vec[(size_t)nxt * vstride + vix<NPT>(0, k, pvl)] = __ldcg(&gvec[nxt * gpar + vix<NPT>(0, k, pvl)]);
-        __syncthreads();
-        if (tot > 0.0) sc = 1.0 / sqrt(tot);
-      } else {
-        rq = tot * sc * sc;
-      }
-    }
-    const double dd = (1.0 + A.inflate) * rq;
-    d = gersh < dd ? gersh : dd;
-    if (rank == 0 && tid == 0) A.d_out[unit] = d;
-    __syncthreads();
-    for (int k = tid; k < 2 * vstride; k += NTH) vec[k] = 0.0;
-  } else {
-    d = P.d[unit];
-  }
 
   // ======================================================= a8: lambda grid (R#14-16, R#22)
   if (warp < NPT) {
@@ -1719,85 +1488,8 @@ __global__ void __launch_bounds__(PT, 1) fit_cluster_kernel(const PathParams P, 
   };
   const int warp = tid >> 5, lane = tid & 31, nwarps = PT / 32;
 
-  // ======================================================= a7: d by power iteration (R#5)
-  double d;
-  if (A.compute_d) {
-    const double v0 = 1.0 / sqrt((double)p);
-    for (int k = tid; k < A.pv; k += PT) vec[k] = k < p ? v0 : 0.0;
-    // Gershgorin: max row sum of |G| over this CTA's rows
-    double gm = 0.0;
-    for (int ri = 0; ri < NRT; ++ri) {
-      double a = 0.0;
-      if (ri == 0) {
-#pragma unroll
-        for (int e = 0; e < EREG; ++e) a += fabs(greg[e]);
-        for (int ci = EREG; ci < KPR; ++ci) a += fabs(gsm[(size_t)(ci - EREG) * PT + tid]);
-      } else {
-        const int base = (KPR > EREG ? KPR - EREG : 0) + (ri - 1) * KPR;
-        for (int ci = 0; ci < KPR; ++ci) a += fabs(gsm[(size_t)(base + ci) * PT + tid]);
-      }
-      gm = fmax(gm, reduce_T(a));
-    }
-    for (int o = 16; o > 0; o >>= 1) gm = fmax(gm, __shfl_xor_sync(0xffffffffu, gm, o));
-    if (lane == 0) red[warp] = gm;
-    __syncthreads();
-    if (tid == 0) {
-      double m = 0.0;
-      for (int w = 0; w < nwarps; ++w) m = fmax(m, red[w]);
-      for (int r = 0; r < C; ++r) st_cluster(&dl[(size_t)(0 * C + rank) * (NPT + 2) + NPT + 1], r, m);
-    }
-    double rq = 0.0, gersh = 0.0;
-    for (int it = 0; it <= A.power_iters; ++it) {
-      const int cur = it & 1, nxt = cur ^ 1;
-      const double* v = vec + (size_t)cur * NPT * A.pv;
-      double part = 0.0;
-      for (int ri = 0; ri < NRT; ++ri) {
-        const double w = reduce_T(rowdot(ri, v));
-        const int r = rg + ri * RG;
-        if (tl == 0 && r < nr) {
-          const int j = j0 + r;
-          if (it < A.power_iters) {
-            part += w * w;
-            if (C == 1) vec[(size_t)nxt * NPT * A.pv + j] = w;
-            else for (int q = 0; q < C; ++q) st_cluster(&vec[(size_t)nxt * NPT * A.pv + j], q, w);
-          } else {
-            part += v[j] * w;  // Rayleigh quotient partial
-          }
-        }
-      }
-      for (int o = 16; o > 0; o >>= 1) part += __shfl_xor_sync(0xffffffffu, part, o);
-      if (lane == 0) red[warp] = part;
-      __syncthreads();
-      if (tid == 0) {
-        double s = 0.0;
-        for (int w = 0; w < nwarps; ++w) s += red[w];  // fixed order
-        for (int r = 0; r < C; ++r) st_cluster(&dl[(size_t)(cur * C + rank) * (NPT + 2)], r, s);
-      }
-      cluster_sync_all();
-      double tot = 0.0;
-      for (int r = 0; r < C; ++r) tot += dl[(size_t)(cur * C + r) * (NPT + 2)];
-      if (it == 0) {
-        for (int r = 0; r < C; ++r) gersh = fmax(gersh, dl[(size_t)(0 * C + r) * (NPT + 2) + NPT + 1]);
-      }
-      if (it < A.power_iters) {
-        const double nrm = sqrt(tot);
-        double* vn = vec + (size_t)nxt * NPT * A.pv;
-        if (nrm > 0.0)
-          for (int k = tid; k < p; k += PT) vn[k] = vn[k] / nrm;
-        else
-          for (int k = tid; k < p; k += PT) vn[k] = v[k];
-        __syncthreads();
-      } else {
-        rq = tot;
-      }
-    }
-    const double dd = (1.0 + A.inflate) * rq;
-    d = gersh < dd ? gersh : dd;
-    if (rank == 0 && tid == 0) A.d_out[unit] = d;
-    cluster_sync_all();  // everyone is done with vec / dl before the path reuses them
-  } else {
-    d = P.d[unit];
-  }
+  // a7: d (>= lambda_1, R#5) from d_rule (drule.cu)
+  const double d = P.d[unit];
 
   // ======================================================= a8: lambda grid (R#14-16, R#22)
   double lmax[NPT], lam[NPT];
@@ -2414,8 +2106,7 @@ extern "C" void oem_path_cfg_default(oem_path_cfg* cfg) {
   cfg->group = nullptr;
   cfg->ngroups = 0;
   cfg->grp_w = nullptr;
-  cfg->power_iters = 200;
-  cfg->d_inflate = 5e-3;
+  cfg->d_squarings = 12;
   cfg->fold_mode = 0;
   cfg->lambda_max_override = nullptr;
   cfg->standardize = 0;
@@ -2448,7 +2139,7 @@ extern "C" oem_status oem_fit_path(oem_ctx* ctx, const double* G, const double* 
     OEM_FAIL(OEM_ERR_INVALID_ARG, "oem_fit_path: need 0 < lambda_min_ratio < 1");
   if (!(cfg.tol > 0.0) || cfg.maxit < 1) OEM_FAIL(OEM_ERR_INVALID_ARG, "oem_fit_path: need tol > 0, maxit >= 1");
   if (cfg.maxit > 2000000000LL) cfg.maxit = 2000000000LL;
-  if (cfg.power_iters < 0) OEM_FAIL(OEM_ERR_INVALID_ARG, "power_iters < 0");
+  if (cfg.d_squarings < 0 || cfg.d_squarings > 60) OEM_FAIL(OEM_ERR_INVALID_ARG, "oem_fit_path: need 0 <= d_squarings <= 60");
   const int fold = cfg.fold_mode ? 1 : 0;
   const int nU = fold ? nG + 1 : nG;
   const int L = cfg.nlambda;
@@ -2569,8 +2260,6 @@ extern "C" oem_status oem_fit_path(oem_ctx* ctx, const double* G, const double* 
   const size_t o_Gn = take(sizeof(double) * nU * pp);
   const size_t o_cn = take(sizeof(double) * nU * p);
   const size_t o_bbuf = take(sizeof(double) * 2 * nU * nP * p);
-  const size_t o_wbuf = take(sizeof(double) * 2 * nU * p);
-  const size_t o_pslot = take(sizeof(double) * 3 * nU * Cmax);
   const size_t o_bad = take(sizeof(unsigned long long) * nU);
   const size_t o_dslot = take(sizeof(unsigned long long) * 3 * nU * nP);
   const int nvu_ws = use_glob ? std::max(nU, gl.nvu) : nU;  // virtual units (grid solver split)
@@ -2700,12 +2389,16 @@ extern "C" oem_status oem_fit_path(oem_ctx* ctx, const double* G, const double* 
   P.flags = flags;
   P.bad_iter = reinterpret_cast<unsigned long long*>(base + o_bad);
   double* dptr = reinterpret_cast<double*>(base + o_d);
+  // ---- a7 d per unit (R#5) unless given: one cooperative launch over all units (drule.cu)
+  if (!d_in) {
+    oem_status s = d_rule(ctx, Gn, nU, p, cfg.d_squarings, dptr, st);
+    if (s != OEM_OK) return s;
+  }
   if (use_glob) {
     // ---- a7-a10 fused in one cooperative launch: register-resident G, C CTAs per unit over L2
     P.ps = 0; P.T = 0; P.smem_rows = 0;
     GlobArgs A;
     A.Cmax = Cmax; A.rows = gl.rows; A.pvl = gl.pvl; A.qsplit = gl.split ? 1 : 0; A.nvu = gl.nvu;
-    A.power_iters = cfg.power_iters; A.inflate = cfg.d_inflate; A.compute_d = d_in ? 0 : 1; A.d_out = dptr;
     A.gvec = reinterpret_cast<double*>(base + o_gvec);
     A.gflag = reinterpret_cast<unsigned long long*>(base + o_gflag);
     OEM_CUDA_TRY(cudaMemsetAsync(A.gflag, 0, sizeof(unsigned long long) * 2 * (size_t)nvu_ws * Cmax, st));
@@ -2726,7 +2419,6 @@ extern "C" oem_status oem_fit_path(oem_ctx* ctx, const double* G, const double* 
     P.ps = 0; P.T = 0; P.smem_rows = 0;
     LeanArgs A;
     A.C = ll.C; A.rows = ll.rows; A.pvl = ll.pvl; A.qsplit = qsplit ? 1 : 0;
-    A.power_iters = cfg.power_iters; A.inflate = cfg.d_inflate; A.compute_d = d_in ? 0 : 1; A.d_out = dptr;
     PhaseTimer tm(ctx, PH_PATH, st);
     ++ctx->launches;
     oem_status s;
@@ -2741,7 +2433,6 @@ extern "C" oem_status oem_fit_path(oem_ctx* ctx, const double* G, const double* 
     P.ps = 0; P.T = cl.T; P.smem_rows = 0;
     ClusterArgs A;
     A.C = cl.C; A.T = cl.T; A.RG = cl.RG; A.KPR = cl.KPR; A.NRT = cl.NRT; A.S = cl.S; A.pv = cl.pv;
-    A.power_iters = cfg.power_iters; A.inflate = cfg.d_inflate; A.compute_d = d_in ? 0 : 1; A.d_out = dptr;
     A.maxrows = cl.maxrows;
     PhaseTimer tm(ctx, PH_PATH, st);
     ++ctx->launches;
@@ -2753,21 +2444,6 @@ extern "C" oem_status oem_fit_path(oem_ctx* ctx, const double* G, const double* 
     if (s != OEM_OK) return s;
   } else {
     P.ps = lo.ps; P.T = lo.T; P.smem_rows = lo.smem_rows;
-    // ---- a7 d per unit (power rule R#5) unless given
-    if (!d_in) {
-      PathParams P1 = P;
-      double* wbuf = reinterpret_cast<double*>(base + o_wbuf);
-      double* pslot = reinterpret_cast<double*>(base + o_pslot);
-      int iters = cfg.power_iters, Cm = lo.Cmax;
-      double infl = cfg.d_inflate;
-      void* args[] = {&P1, &iters, &infl, &wbuf, &pslot, &Cm, &dptr};
-      const size_t smem = ((size_t)lo.smem_rows * lo.ps + lo.ps + lo.smem_rows + 64) * 8;
-      PhaseTimer tm(ctx, PH_POWER, st);
-      ++ctx->launches;
-      oem_status s = coop_launch(power_kernel, lo.ncta_total, smem, st, args);
-      if (s != OEM_OK) return s;
-      OEM_CUDA_TRY(cudaMemsetAsync(base + o_bar, 0, sizeof(unsigned) * 2 * nU, st));
-    }
     // ---- a8-a10 lambda grid + OEM paths
     void* args[] = {&P};
     PhaseTimer tm(ctx, PH_PATH, st);

@@ -47,8 +47,8 @@ class PathCfg(ctypes.Structure):
     _fields_ = [("nlambda", ctypes.c_int32), ("lambda_min_ratio", ctypes.c_double),
                 ("lambda_", ctypes.c_void_p), ("tol", ctypes.c_double), ("maxit", ctypes.c_int64),
                 ("var_w", ctypes.c_void_p), ("group", ctypes.c_void_p), ("ngroups", ctypes.c_int32),
-                ("grp_w", ctypes.c_void_p), ("power_iters", ctypes.c_int32),
-                ("d_inflate", ctypes.c_double), ("fold_mode", ctypes.c_int32),
+                ("grp_w", ctypes.c_void_p), ("d_squarings", ctypes.c_int32),
+                ("fold_mode", ctypes.c_int32),
                 ("lambda_max_override", ctypes.c_void_p), ("standardize", ctypes.c_int32),
                 ("xsum", ctypes.c_void_p), ("ysum", ctypes.c_void_p), ("intercept_out", ctypes.c_void_p)]
 
@@ -58,8 +58,9 @@ class LogisticCfg(ctypes.Structure):
                 ("lambda_", ctypes.c_void_p), ("tol_in", ctypes.c_double),
                 ("maxit_in", ctypes.c_int64), ("tol_out", ctypes.c_double),
                 ("outer_maxit", ctypes.c_int32), ("eps", ctypes.c_double),
-                ("power_iters", ctypes.c_int32), ("d_inflate", ctypes.c_double),
-                ("var_w", ctypes.c_void_p), ("hessian_upper_bound", ctypes.c_int32)]
+                ("d_squarings", ctypes.c_int32), ("var_w", ctypes.c_void_p),
+                ("group", ctypes.c_void_p), ("ngroups", ctypes.c_int32), ("grp_w", ctypes.c_void_p),
+                ("hessian_upper_bound", ctypes.c_int32)]
 
 
 class Stats(ctypes.Structure):
@@ -227,7 +228,7 @@ class PathResult:
 
 def oem_fit_path(ctx: Context, G, xty, counts, penalties, nlambda=100, lambda_min_ratio=1e-3,
                  lambdas=None, tol=1e-11, maxit=100000, var_w=None, group=None, ngroups=0,
-                 grp_w=None, power_iters=200, d_inflate=5e-3, fold_mode=False, d_in=None,
+                 grp_w=None, d_squarings=12, fold_mode=False, d_in=None,
                  beta_init=None, lambda_max=None, standardize=False, xsum=None, ysum=None,
                  stream=None) -> PathResult:
     """a6-a10: normalise, d, lambda grid and OEM paths for every (Gram, penalty) unit.
@@ -267,8 +268,7 @@ def oem_fit_path(ctx: Context, G, xty, counts, penalties, nlambda=100, lambda_mi
         gw_h = (ctypes.c_double * len(grp_w))(*[float(v) for v in grp_w])
         keep.append(gw_h)
         cfg.grp_w = ctypes.cast(gw_h, ctypes.c_void_p)
-    cfg.power_iters = power_iters
-    cfg.d_inflate = d_inflate
+    cfg.d_squarings = d_squarings
     cfg.fold_mode = 1 if fold_mode else 0
     if lambda_max is not None:
         lm_h = ctypes.c_double(float(lambda_max))
@@ -377,8 +377,9 @@ class LogisticResult:
 
 def oem_fit_logistic(ctx: Context, X, y01, penalty=("lasso", 0.0, 1.0), nlambda=50,
                      lambda_min_ratio=1e-3, lambdas=None, tol_in=1e-11, maxit_in=100000,
-                     tol_out=1e-10, outer_maxit=100, eps=1e-5, power_iters=200, d_inflate=5e-3,
-                     var_w=None, hessian_upper_bound=False, stream=None) -> LogisticResult:
+                     tol_out=1e-10, outer_maxit=100, eps=1e-5, d_squarings=12,
+                     var_w=None, group=None, ngroups=0, grp_w=None, hessian_upper_bound=False,
+                     stream=None) -> LogisticResult:
     """a4 + a6-a9 to convergence: proximal-Newton logistic path; with
     hessian_upper_bound=True the f1 mode (w = 1/4): Gram once, one gradient pass
     per outer step."""
@@ -395,7 +396,16 @@ def oem_fit_logistic(ctx: Context, X, y01, penalty=("lasso", 0.0, 1.0), nlambda=
         keep.append(lam_h)
         cfg.lambda_ = ctypes.cast(lam_h, ctypes.c_void_p)
     cfg.tol_in, cfg.maxit_in, cfg.tol_out, cfg.outer_maxit = tol_in, maxit_in, tol_out, outer_maxit
-    cfg.eps, cfg.power_iters, cfg.d_inflate = eps, power_iters, d_inflate
+    cfg.eps, cfg.d_squarings = eps, d_squarings
+    if group is not None:
+        g_h = (ctypes.c_int32 * p)(*[int(v) for v in group])
+        keep.append(g_h)
+        cfg.group = ctypes.cast(g_h, ctypes.c_void_p)
+        cfg.ngroups = int(ngroups or (max(int(v) for v in group) + 1))
+    if grp_w is not None:
+        gw_h = (ctypes.c_double * len(grp_w))(*[float(v) for v in grp_w])
+        keep.append(gw_h)
+        cfg.grp_w = ctypes.cast(gw_h, ctypes.c_void_p)
     cfg.hessian_upper_bound = 1 if hessian_upper_bound else 0
     if var_w is not None:
         var_w = var_w.to(device=X.device, dtype=torch.float64).contiguous()

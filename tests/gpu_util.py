@@ -1,4 +1,6 @@
 """Helpers for the -m gpu parity tests: device-resident synthetic inputs and error metrics."""
+import functools
+
 import numpy as np
 
 import datagen as dg
@@ -31,3 +33,37 @@ def xty_err(c, co, Go, yy):
     s = np.sqrt(np.abs(np.diag(Go)) * abs(yy))
     s[s == 0] = 1.0
     return float(np.max(np.abs(c - co) / s)) if c.size else 0.0
+
+
+CFG4_COLUMN_BLOCKS = ((0, 8), (248, 8), (496, 8), (992, 8))
+
+
+@functools.lru_cache(maxsize=1)
+def cfg4_oracle_sample():
+    """The oracle's sums over ALL n = 1e7 rows of cfg4 for 32 columns in four 8-column blocks
+    that lie in four different 128-column panels of the two-panel Gram plan (columns 0-7, 248-255,
+    496-503, 992-999), so the 32 x 32 sub-Gram holds diagonal-panel entries and every kind of
+    off-diagonal panel pair. Rows come from the host generator, those columns only. Computed once
+    per session (shared by the in-core and the streamed full-size tests).
+    Returns (idx, G_sub, xty_sub, yty, xsum_sub, xabs_sub)."""
+    import oracle as orc
+    from datagen.configs import CONFIGS
+    cfg = CONFIGS["cfg4"]
+    bt = dg.beta(cfg.spec)
+    idx = np.concatenate([np.arange(c0, c0 + m) for c0, m in CFG4_COLUMN_BLOCKS])
+    acc = orc.GramAccumulator(idx.size)
+    xs = np.zeros(idx.size)
+    xa = np.zeros(idx.size)
+    for r in range(0, cfg.n, 1_000_000):
+        parts = []
+        y = None
+        for c0, m in CFG4_COLUMN_BLOCKS:
+            X, yb = dg.rows_host(cfg.spec, bt, r, 1_000_000, c0, m, want_y=y is None)
+            parts.append(X)
+            y = yb if y is None else y
+        X = np.ascontiguousarray(np.hstack(parts))
+        acc.add(X, y)
+        xs += X.sum(axis=0)
+        xa += np.abs(X).sum(axis=0)
+    Go, co, yyo = acc.result()
+    return idx, Go, co, yyo, xs, xa

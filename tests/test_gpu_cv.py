@@ -52,6 +52,10 @@ def test_cv_error_parity(ctx, n, p, K, pens, L):
         assert cvm_o[q, cv.idx_min[q]] <= cvm_o[q, imin_o[q]] + 1e-10 * s
         assert cvm_o[q, cv.idx_1se[q]] <= cvm_o[q, imin_o[q]] + cvsd_o[q, imin_o[q]] + 1e-10 * s
         assert cv.idx_1se[q] <= cv.idx_min[q]
+        # lambda_1se is the LARGEST lambda (smallest index) within one SE: no smaller index may
+        # satisfy the threshold by more than the rounding tolerance (R#35)
+        thr = cvm_o[q, cv.idx_min[q]] + cvsd_o[q, cv.idx_min[q]]
+        assert np.all(cvm_o[q, :cv.idx_1se[q]] > thr - 1e-10 * s), q
         if abs(cvm_o[q, imin_o[q]] - np.partition(cvm_o[q], 1)[1]) > 1e-9 * s:
             assert cv.idx_min[q] == imin_o[q]
     mins = [cvm_o[q, imin_o[q]] for q in range(len(pens))]

@@ -9,7 +9,7 @@ import pytest
 import datagen as dg
 import oracle as orc
 from datagen.configs import CONFIGS
-from gpu_util import device_rows, scale_err, xty_err
+from gpu_util import cfg4_oracle_sample, device_rows, scale_err, xty_err
 
 pytestmark = pytest.mark.gpu
 
@@ -119,8 +119,10 @@ def test_gram_full_size_cfg2(ctx):
 
 
 def test_gram_full_n_column_subset_cfg4(ctx):
-    """cfg4 at full n = 1e7 (80 GB resident): the leading 16x16 block of G and X^T y on the
-    support checked against the oracle over all 1e7 rows (host generator, those columns)."""
+    """cfg4 at full n = 1e7 (80 GB resident), in bench.py's launch configuration: a 32 x 32
+    sub-Gram over four column blocks in four different 128-column panels (diagonal and
+    off-diagonal panel pairs, 528 distinct entries), X^T y and the f3 column sums on those columns,
+    against the oracle's sums over all 1e7 rows (gpu_util.cfg4_oracle_sample)."""
     from paper_1801_09661_b200 import oem_gram, oem_gram_moments
     cfg = CONFIGS["cfg4"]
     bt = dg.beta(cfg.spec)
@@ -129,18 +131,11 @@ def test_gram_full_n_column_subset_cfg4(ctx):
     xs, ysum = oem_gram_moments(ctx, Xd, yd, 1, 0)   # f3 column sums at full size, same launch shape
     del Xd
     torch.cuda.empty_cache()
-    m = 16
-    acc = orc.GramAccumulator(m)
-    xso = np.zeros(m); xabs = np.zeros(m)
-    for r in range(0, cfg.n, 1_000_000):
-        X, y = dg.rows_host(cfg.spec, bt, r, 1_000_000, 0, m)
-        acc.add(X, y)
-        xso += X.sum(axis=0); xabs += np.abs(X).sum(axis=0)
-    Go, co, yyo = acc.result()
-    assert np.max(np.abs(xs[0].cpu().numpy()[:m] - xso) / xabs) <= 1e-12
+    idx, Go, co, yyo, xso, xabs = cfg4_oracle_sample()
+    assert np.max(np.abs(xs[0].cpu().numpy()[idx] - xso) / xabs) <= 1e-12
     Gh = G.cpu().numpy()
-    assert scale_err(Gh[:m, :m], Go) <= 1e-12
-    assert xty_err(c.cpu().numpy()[:m], co, Go, yyo) <= 1e-12
+    assert scale_err(Gh[np.ix_(idx, idx)], Go) <= 1e-12
+    assert xty_err(c.cpu().numpy()[idx], co, Go, yyo) <= 1e-12
     assert abs(float(yy) - yyo) <= 1e-12 * yyo
     # property at full size: G/n close to the population covariance (block 0.4)
     grp = np.arange(cfg.p) // 10

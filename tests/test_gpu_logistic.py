@@ -98,3 +98,84 @@ def test_logistic_upper_bound_path(ctx):
     assert np.max(np.abs(Bu - Bo)) <= 1e-8
     assert np.max(np.abs(Bu - fe.beta.cpu().numpy())) <= 1e-7
     assert np.max(np.abs(np.array(fu.outer_iters) - oi)) <= 2
+
+
+@pytest.mark.parametrize("pen,p,grouped", [
+    (("enet", 0.0, 0.5), 40, False),
+    (("mcp", 3.0, 1.0), 40, False),
+    (("scad", 3.7, 1.0), 40, False),
+    (("grp_lasso", 0.0, 1.0), 100, True),
+    (("grp_mcp", 3.0, 1.0), 100, True),
+    (("grp_scad", 3.7, 1.0), 100, True),
+])
+def test_logistic_every_family(ctx, pen, p, grouped):
+    """Proximal-Newton OEM with every Table 1 family (§6.3 P:L1143-1148 fits MCP
+    with gamma = 3 and group penalties with contiguous groups of 25 to logistic models), against
+    the oracle's O7 with the same family, groups and lambda grid: lambda_max of the working
+    statistic at beta = 0 (R#14), every beta at 1e-8, converged flags and outer step counts."""
+    from paper_1801_09661_b200 import oem_fit_logistic
+    n, L = 6000, 10
+    spec = CONFIGS["cfg5"].spec.replace(n=n, p=p, nnz=min(10, p))
+    bt = dg.beta(spec)
+    Xd, yd = device_rows(spec, bt)
+    X, y = dg.rows_host(spec, bt)
+    grp = (np.arange(p) // 25).astype(np.int32) if grouped else None
+    fam, gamma, alpha = pen
+    fit = oem_fit_logistic(ctx, Xd, yd, pen, nlambda=L, group=grp)
+    lam = fit.lam.cpu().numpy()
+    _, cw0, _ = orc.gram_weighted(X, y, np.zeros(p))
+    lmax = orc.lambda_max(fam, cw0 / n, group=grp, alpha=alpha)
+    assert abs(lam[0] - lmax) <= 1e-13 * lmax
+    assert np.allclose(lam, orc.lambda_grid(lmax, L), rtol=1e-13, atol=0)
+    B, oi, ii, cv = orc.logistic_path(X, y, lam, family=fam, gamma=gamma, alpha=alpha, group=grp)
+    Bg = fit.beta.cpu().numpy()
+    assert np.max(np.abs(Bg - B)) <= 1e-8, np.max(np.abs(Bg - B))
+    assert np.array_equal(np.array(fit.conv), cv)
+    assert np.max(np.abs(np.array(fit.outer_iters) - oi)) <= 1
+    assert not Bg[0].any()  # lambda_max: null model
+
+
+def test_logistic_upper_bound_groups(ctx):
+    """f1 upper-bound mode with the group lasso and group MCP ('For the MCP and
+    group lasso, oem() with the Hessian upper-bound option is the fastest'), against the oracle's
+    upper-bound path with the same groups."""
+    from paper_1801_09661_b200 import oem_fit_logistic
+    n, p, L = 8000, 100, 6
+    spec = CONFIGS["cfg5"].spec.replace(n=n, p=p, nnz=10)
+    bt = dg.beta(spec)
+    Xd, yd = device_rows(spec, bt)
+    X, y = dg.rows_host(spec, bt)
+    grp = (np.arange(p) // 25).astype(np.int32)
+    for pen in (("grp_lasso", 0.0, 1.0), ("grp_mcp", 3.0, 1.0)):
+        fit = oem_fit_logistic(ctx, Xd, yd, pen, nlambda=L, group=grp, hessian_upper_bound=True,
+                               outer_maxit=1000)
+        lam = fit.lam.cpu().numpy()
+        Bo, oi, ii, cv = orc.logistic_path_ub(X, y, lam, family=pen[0], gamma=pen[1], group=grp)
+        assert all(fit.conv) and cv.all()
+        assert np.max(np.abs(fit.beta.cpu().numpy() - Bo)) <= 1e-8, pen
+
+
+def test_logistic_full_size_cfg5(ctx):
+    """cfg5 at full size (n = 5e6, p = 200, 8 GB resident), in bench.py's launch configuration
+    (exact-Hessian proximal Newton, weighted Gram recomputed each outer step), on an explicit
+    grid of the first three lambda of the benched 50-point grid, against the oracle's O7 over all
+    5e6 rows (host generator): every beta at 1e-8 and equal converged flags / outer step counts."""
+    from paper_1801_09661_b200 import oem_fit_logistic
+    cfg = CONFIGS["cfg5"]
+    bt = dg.beta(cfg.spec)
+    Xd, yd = device_rows(cfg.spec, bt)
+    full = oem_fit_logistic(ctx, Xd, yd, cfg.penalties[0], nlambda=cfg.nlambda)
+    lam = full.lam.cpu().numpy()[:3]
+    fit = oem_fit_logistic(ctx, Xd, yd, cfg.penalties[0], lambdas=lam)
+    Bg = fit.beta.cpu().numpy()
+    assert np.array_equal(Bg, full.beta.cpu().numpy()[:3])  # explicit grid == the benched run's start
+    del Xd, yd
+    torch.cuda.empty_cache()
+    X, y = dg.rows_host(cfg.spec, bt)
+    _, cw0, _ = orc.gram_weighted(X, y, np.zeros(cfg.p))
+    lmax = np.max(np.abs(cw0 / cfg.n))
+    assert abs(lam[0] - lmax) <= 1e-13 * lmax
+    B, oi, ii, cv = orc.logistic_path(X, y, lam)
+    assert np.max(np.abs(Bg - B)) <= 1e-8, np.max(np.abs(Bg - B))
+    assert np.array_equal(np.array(fit.conv), cv) and cv.all()
+    assert np.max(np.abs(np.array(fit.outer_iters) - oi)) <= 1

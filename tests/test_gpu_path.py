@@ -31,12 +31,28 @@ def host_problem(cfg):
     return bt, X, y
 
 
-def check_fit(fit, Go, co, n, penalties, nlambda, unit=0, group=None, lambdas=None, w=None, d_tol=True):
+def check_d(d, Go, n, G_gpu=None):
+    """a7 against the oracle (R#5): d_gpu equals the oracle's own rule on the oracle's statistics
+    (up to the Gram's own 1e-12 parity), equals it on the GPU's statistics to 1e-12, and lies in
+    [lambda_1, p^(2^-12) lambda_1] (the trace bound's guarantee), lambda_1 from numpy."""
+    Gn = np.asarray(Go, dtype=float) / n
+    d_ref = orc.d_rule(Gn)[0]
+    assert abs(d - d_ref) <= 1e-11 * d_ref, (d, d_ref)
+    if G_gpu is not None:
+        d_same = orc.d_rule(np.asarray(G_gpu, dtype=float) / n)[0]
+        assert abs(d - d_same) <= 1e-12 * d_same, (d, d_same)
+    p = Gn.shape[0]
+    lam1 = np.linalg.eigvalsh(Gn)[-1]
+    assert lam1 * (1 - 1e-12) <= d <= lam1 * p ** (1 / 4096) * (1 + 1e-10) + 1e-300, (d, lam1)
+    return d_ref
+
+
+def check_fit(fit, Go, co, n, penalties, nlambda, unit=0, group=None, lambdas=None, w=None, G_gpu=None):
+    """Every output of one unit against the oracle's OWN pipeline on the oracle's statistics:
+    its d (R#5), its lambda grid (R#14-16) and its path solve (O6)."""
     d = float(fit.d[unit])
     Gn = Go / n
-    if d_tol:
-        lam1 = np.linalg.eigvalsh(Gn)[-1]
-        assert lam1 * (1 - 1e-12) <= d <= 1.01 * lam1, (d, lam1)
+    d_ref = check_d(d, Go, n, G_gpu)
     for q, (fam, gamma, alpha) in enumerate(penalties):
         if lambdas is None:
             lmax = orc.lambda_max(fam, co / n, w=w, group=group, alpha=alpha)
@@ -45,7 +61,7 @@ def check_fit(fit, Go, co, n, penalties, nlambda, unit=0, group=None, lambdas=No
             lam = np.asarray(lambdas, dtype=float)
         lg = fit.lam[unit, q].cpu().numpy()
         assert np.max(np.abs(lg - lam) / lam.clip(min=1e-300)) < 1e-13
-        B, it, cv = orc.oem_path(Gn, co / n, d, fam, lg, gamma, alpha, w=w, group=group)
+        B, it, cv = orc.oem_path(Gn, co / n, d_ref, fam, lam, gamma, alpha, w=w, group=group)
         Bg = fit.beta[unit, q].cpu().numpy()
         err = np.max(np.abs(Bg - B))
         assert err <= TOL_BETA, (fam, err)
@@ -61,7 +77,7 @@ def test_cfg1_lasso_path(ctx):
     G, c, yy, n = oem_gram(ctx, torch.from_numpy(X).cuda(), torch.from_numpy(y).cuda())
     fit = oem_fit_path(ctx, G, c, [n], cfg.penalties, nlambda=cfg.nlambda)
     Go, co, _ = orc.gram(X, y)
-    check_fit(fit, Go, co, n, cfg.penalties, cfg.nlambda)
+    check_fit(fit, Go, co, n, cfg.penalties, cfg.nlambda, G_gpu=G.cpu().numpy())
     # lambda_max nulls everything, the smallest lambda recovers the support
     assert not fit.beta[0, 0, 0].any()
     assert (fit.beta[0, 0, -1].abs() > 0.1).sum() >= 5
@@ -81,7 +97,7 @@ def test_cfg2_three_penalties(ctx, n):
         X, y = dg.rows_host(cfg.spec, bt, r, min(250_000, n - r))
         acc.add(X, y)
     Go, co, _ = acc.result()
-    check_fit(fit, Go, co, n, cfg.penalties, cfg.nlambda)
+    check_fit(fit, Go, co, n, cfg.penalties, cfg.nlambda, G_gpu=G.cpu().numpy())
     # multi-penalty independence: lasso alone == lasso inside the batch, bit for bit
     fit1 = oem_fit_path(ctx, G, c, [nn], cfg.penalties[:1], nlambda=cfg.nlambda, d_in=[float(fit.d[0])])
     assert torch.equal(fit1.beta[0, 0], fit.beta[0, 0])
@@ -171,8 +187,7 @@ def test_cfg4_full_size_paths(ctx):
     fit = oem_fit_path(ctx, G, c, [n], cfg.penalties, nlambda=cfg.nlambda, group=grp, ngroups=100)
     Gh, ch = G.cpu().numpy(), c.cpu().numpy()
     d = float(fit.d[0])
-    lam1 = np.linalg.eigvalsh(Gh / n)[-1]
-    assert lam1 * (1 - 1e-12) <= d <= 1.01 * lam1, (d, lam1)
+    check_d(d, Gh, n, Gh)
     for q, (fam, gamma, alpha) in enumerate(cfg.penalties):
         g = grp if fam.startswith("grp") else None
         lam = orc.lambda_grid(orc.lambda_max(fam, ch / n, group=g, alpha=alpha), cfg.nlambda)
@@ -199,6 +214,7 @@ def test_noncontiguous_groups_and_weights(ctx):
     pens = [("grp_lasso", 0.0, 1.0), ("grp_mcp", 3.0, 1.0), ("grp_scad", 3.7, 1.0)]
     fit = oem_fit_path(ctx, G, c, [n], pens, nlambda=25, group=grp, ngroups=17, grp_w=gw)
     d = float(fit.d[0])
+    check_d(d, Go, n)
     for q, (fam, gamma, alpha) in enumerate(pens):
         lg = fit.lam[0, q].cpu().numpy()
         B, it, cv = orc.oem_path(Go / n, co / n, d, fam, lg, gamma, alpha, group=grp, grp_w=gw)
@@ -208,6 +224,7 @@ def test_noncontiguous_groups_and_weights(ctx):
     pens = [("lasso", 0.0, 1.0), ("enet", 0.0, 0.3), ("scad", 3.7, 1.0)]
     fit = oem_fit_path(ctx, G, c, [n], pens, nlambda=30, var_w=w)
     d = float(fit.d[0])
+    check_d(d, Go, n)
     for q, (fam, gamma, alpha) in enumerate(pens):
         lg = fit.lam[0, q].cpu().numpy()
         lmax = orc.lambda_max(fam, co / n, w=w.cpu().numpy(), alpha=alpha)
@@ -289,6 +306,7 @@ def test_sparse_group_lasso(ctx, p, solver, monkeypatch):
     fit = oem_fit_path(ctx, G, c, [n], pens, nlambda=20, group=grp, ngroups=ng, grp_w=gw,
                        var_w=torch.from_numpy(w).cuda())
     d = float(fit.d[0])
+    check_d(d, Go, n)
     for q, (fam, gamma, alpha) in enumerate(pens):
         lg = fit.lam[0, q].cpu().numpy()
         lmax = orc.lambda_max(fam, co / n, w=w, group=grp, ngroups=ng, grp_w=gw, alpha=alpha)
@@ -317,6 +335,7 @@ def test_mixed_group_and_coordinate_penalties(ctx, p, solver, monkeypatch):
     pens = [("grp_lasso", 0.0, 1.0), ("enet", 0.0, 0.5), ("mcp", 3.0, 1.0), ("sgl", 0.0, 0.5)]
     fit = oem_fit_path(ctx, G, c, [n], pens, nlambda=12, group=grp, ngroups=p // 10)
     d = float(fit.d[0])
+    check_d(d, Go, n)
     for q, (fam, gamma, alpha) in enumerate(pens):
         g = grp if fam in ("grp_lasso", "sgl") else None
         lg = fit.lam[0, q].cpu().numpy()
@@ -340,6 +359,7 @@ def test_many_penalties_and_wide_p_fallbacks(ctx):
             ("enet", 0.0, 0.8), ("mcp", 5.0, 1.0)]
     fit = oem_fit_path(ctx, G, c, [n], pens, nlambda=15)
     d = float(fit.d[0])
+    check_d(d, Go, n)
     for q, (fam, gamma, alpha) in enumerate(pens):
         B, it, cv = orc.oem_path(Go / n, co / n, d, fam, fit.lam[0, q].cpu().numpy(), gamma, alpha)
         assert np.max(np.abs(fit.beta[0, q].cpu().numpy() - B)) <= TOL_BETA, fam
@@ -374,8 +394,7 @@ def test_solver_variant_boundaries(ctx, p):
     for u, (lo, hi, nn) in enumerate([(0, h, n0), (h, X.shape[0], n1)]):
         Go, co, _ = orc.gram(X[lo:hi], y[lo:hi])
         d = float(fit.d[u])
-        lam1 = np.linalg.eigvalsh(Go / nn)[-1]
-        assert lam1 * (1 - 1e-12) <= d <= 1.01 * lam1 + 1e-300
+        check_d(d, Go, nn, G[u].cpu().numpy())
         for q, (fam, gamma, alpha) in enumerate(pens):
             B, it, cv = orc.oem_path(Go / nn, co / nn, d, fam, fit.lam[u, q].cpu().numpy(), gamma, alpha)
             assert np.max(np.abs(fit.beta[u, q].cpu().numpy() - B)) <= TOL_BETA, (p, u, fam)
@@ -401,6 +420,7 @@ def test_batched_penalties_every_lean_layout(ctx, p, monkeypatch):
     for u, (lo, hi, nn) in enumerate([(0, h, n0), (h, X.shape[0], n1)]):
         Go, co, _ = orc.gram(X[lo:hi], y[lo:hi])
         d = float(fit.d[u])
+        check_d(d, Go, nn)
         for q, (fam, gamma, alpha) in enumerate(pens):
             B, it, cv = orc.oem_path(Go / nn, co / nn, d, fam, fit.lam[u, q].cpu().numpy(), gamma, alpha)
             assert np.max(np.abs(fit.beta[u, q].cpu().numpy() - B)) <= TOL_BETA, (p, u, fam)

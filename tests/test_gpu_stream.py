@@ -101,8 +101,9 @@ def test_stream_edge_cases(ctx):
 
 def test_gram_host_full_size_cfg4(ctx):
     """f4 at full size, as bench.py's e2e leg runs it: cfg4's 1e7 x 1000 design (80 GB) in pinned
-    host memory streamed through the Gram kernel in 2^20-row blocks, against the in-core pass over
-    the same rows (itself pinned to the oracle at full size in test_gpu_gram.py)."""
+    host memory streamed through the Gram kernel in 2^20-row blocks, against the oracle's sums over
+    all 1e7 rows on a 32-column sample spanning four panels (gpu_util.cfg4_oracle_sample), and
+    against the in-core pass over the same rows (every entry)."""
     from paper_1801_09661_b200 import oem_gram, oem_gram_host
     cfg = CONFIGS["cfg4"]
     bt = dg.beta(cfg.spec)
@@ -121,3 +122,8 @@ def test_gram_host_full_size_cfg4(ctx):
     d = np.sqrt(np.diag(Gh))
     assert np.max(np.abs(cs.cpu().numpy() - c.cpu().numpy()) / (d * np.sqrt(float(yy)))) <= 1e-12
     assert abs(float(yys) - float(yy)) <= 1e-12 * float(yy)
+    from gpu_util import cfg4_oracle_sample, scale_err as serr, xty_err
+    idx, Go, co, yyo, _, _ = cfg4_oracle_sample()
+    assert serr(Gs.cpu().numpy()[np.ix_(idx, idx)], Go) <= 1e-12
+    assert xty_err(cs.cpu().numpy()[idx], co, Go, yyo) <= 1e-12
+    assert abs(float(yys) - yyo) <= 1e-12 * yyo
