@@ -229,16 +229,22 @@ oem_status oem_path_loss(oem_ctx* ctx, const double* G, const double* xty, const
  * oem_gram_folds (G_folds K*p*p, xty_folds K*p, yty_folds K, counts host K) and the coefficient
  * paths of oem_fit_path in fold_mode (beta (K+1)*nP*L*p; unit k+1 = fit on the complement of
  * fold k). No pass over X: err[k][q][l] = (yty_k - 2 b^T xty_k + b^T G_k b) / n_k is the held-out
- * mean squared error of b = beta[k+1][q][l] on fold k (R#33). Summaries per penalty q (device):
- * cvm[q][l] = sum_k n_k err / n, cvsd[q][l] = sqrt(sum_k n_k (err - cvm)^2 / n / (K-1)) (R#34).
+ * mean squared error of b = beta[k+1][q][l] on fold k (R#33). A fit with an intercept (the
+ * intercept_out of a fold-mode oem_path_cfg with xsum/ysum) passes intercept ((K+1)*nP*L,
+ * device) with the fold column sums of oem_gram_moments (xsum_folds K*p, ysum_folds K); the
+ * error is then of y - b0 - X b: the above + b0 (2 b^T xsum_k - 2 ysum_k + n_k b0) / n_k.
+ * intercept = NULL: no intercept (xsum_folds / ysum_folds ignored, may be NULL).
+ * Summaries per penalty q (device): cvm[q][l] = sum_k n_k err / n,
+ * cvsd[q][l] = sqrt(sum_k n_k (err - cvm)^2 / n / (K-1)) (R#34).
  * Host outputs (may be NULL): idx_min[q] = first argmin_l cvm (the larger lambda on ties),
  * idx_1se[q] = smallest l with cvm[l] <= cvm[idx_min] + cvsd[idx_min] (the largest such lambda),
  * best = penalty with the smallest min cvm (the first on ties) (R#35). Synchronises `stream`.
- * Errors: OEM_ERR_DIM (K < 2, p/nP/L < 1), OEM_ERR_EMPTY_FOLD, OEM_ERR_UNSUPPORTED (nP > 64,
- * 8p bytes > 200 KB), OEM_ERR_CUDA. */
+ * Errors: OEM_ERR_DIM (K < 2, p/nP/L < 1), OEM_ERR_EMPTY_FOLD, OEM_ERR_INVALID_ARG (intercept
+ * without the fold sums), OEM_ERR_UNSUPPORTED (nP > 64, 8p bytes > 200 KB), OEM_ERR_CUDA. */
 oem_status oem_cv_error(oem_ctx* ctx, const double* G_folds, const double* xty_folds, const double* yty_folds,
                         const int64_t* counts /*host K*/, int32_t K, int32_t p, int32_t nP, int32_t L,
-                        const double* beta, double* err, double* cvm, double* cvsd, int32_t* idx_min /*host nP*/,
+                        const double* beta, const double* xsum_folds, const double* ysum_folds,
+                        const double* intercept, double* err, double* cvm, double* cvsd, int32_t* idx_min /*host nP*/,
                         int32_t* idx_1se /*host nP*/, int32_t* best /*host 1*/, void* stream);
 
 /* ---- instrumentation (used by bench.py; no effect on results).

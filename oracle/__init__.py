@@ -349,23 +349,24 @@ def fit_from_gram(G_raw, c_raw, n, penalties, nlambda=100, ratio=1e-3, d=None, t
 
 
 # ---------------------------------------------------------------- f2: fast-CV error and selection
-def cv_error(X, y, K, beta_units, row_offset=0):
+def cv_error(X, y, K, beta_units, row_offset=0, intercepts=None):
     """f2 held-out error by its plain definition (R#33): for fold k (rows with (row_offset + i)
-    mod K == k, R#19) and the fit b = beta_units[k+1][q][l] on the complement of fold k
-    (P:L313-327), e_k(l) = (1/n_k) sum_{i in fold k} (y_i - x_i^T b)^2. The held-out rows are
-    streamed directly (a matmul per fold as the library step); the Gram identity the product
-    uses is NOT used here. Returns err [K][nP][L]."""
+    mod K == k, R#19) and the fit (b0, b) = (intercepts[k+1][q][l], beta_units[k+1][q][l]) on the
+    complement of fold k, e_k(l) = (1/n_k) sum_{i in fold k} (y_i - b0 - x_i^T b)^2
+    (b0 = 0 without intercepts). The held-out rows are streamed directly (a matmul per fold as the
+    library step); the Gram identity the product uses is NOT used here. Returns err [K][nP][L]."""
     X = _f64(X)
     y = _f64(y)
     B = np.asarray(beta_units, dtype=np.float64)
     nU, nP, L, p = B.shape
     assert nU == K + 1 and p == X.shape[1]
+    B0 = np.zeros((nU, nP, L)) if intercepts is None else np.asarray(intercepts, dtype=np.float64)
     fold = (row_offset + np.arange(X.shape[0])) % K
     err = np.empty((K, nP, L))
     for k in range(K):
         rows = fold == k
         Xk, yk = X[rows], y[rows]
-        R = yk[:, None] - Xk @ B[k + 1].reshape(nP * L, p).T   # residuals, one column per fit
+        R = yk[:, None] - B0[k + 1].reshape(nP * L)[None, :] - Xk @ B[k + 1].reshape(nP * L, p).T
         err[k] = (np.sum(R * R, axis=0) / rows.sum()).reshape(nP, L)
     return err
 
@@ -417,7 +418,8 @@ def logit_grad(X, y01, beta):
 
 
 def logistic_path_ub(X, y01, lambdas, family="lasso", gamma=3.0, alpha=1.0, d=None, tol_in=1e-11,
-                     maxit_in=100000, tol_out=1e-10, outer_maxit=1000, squarings=SQUARINGS):
+                     maxit_in=100000, tol_out=1e-10, outer_maxit=1000, squarings=SQUARINGS,
+                     group=None, ngroups=0, grp_w=None):
     """f1: the proximal-Newton logistic path with the Hessian upper bound w_i = 1/4
     (P:L385-389, R#27), in the paper's order: per outer step the working responses
     z_i = eta_i + (y_i - mu_i)/w_i with w_i = 1/4, the weighted statistics
@@ -442,8 +444,8 @@ def logistic_path_ub(X, y01, lambdas, family="lasso", gamma=3.0, alpha=1.0, d=No
             Gw = (w * X).T @ X / n
             cw = X.T @ (w * z) / n
             dw = d if d is not None else d_rule(Gw, squarings)[0]
-            nb, it, ok = oem_path(Gw, cw, dw, family, [lam], gamma, alpha, tol=tol_in, maxit=maxit_in,
-                                  beta_init=beta)
+            nb, it, ok = oem_path(Gw, cw, dw, family, [lam], gamma, alpha, group=group, ngroups=ngroups,
+                                  grp_w=grp_w, tol=tol_in, maxit=maxit_in, beta_init=beta)
             ii[l] += it[0]
             oi[l] = o + 1
             delta = np.max(np.abs(nb[0] - beta)) if p else 0.0

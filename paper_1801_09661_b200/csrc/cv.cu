@@ -27,9 +27,11 @@ constexpr int CV_THREADS = 256;
 __global__ void __launch_bounds__(CV_THREADS) cv_err_kernel(const double* __restrict__ Gf, const double* __restrict__ cf,
                                                              const double* __restrict__ yyf, const double* __restrict__ nk,
                                                              const double* __restrict__ beta, int boff, int p, int nP, int L,
-                                                             int LB, double* __restrict__ err) {
+                                                             int LB, const double* __restrict__ xsf,
+                                                             const double* __restrict__ ysf,
+                                                             const double* __restrict__ b0u, double* __restrict__ err) {
   extern __shared__ __align__(16) double bs[];  // [LB][p]
-  __shared__ double red[CV_THREADS / 32][2 * CV_LB];
+  __shared__ double red[CV_THREADS / 32][3 * CV_LB];
   const int l0 = blockIdx.x * LB, q = blockIdx.y, k = blockIdx.z;
   const int nb = min(LB, L - l0);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = CV_THREADS / 32;
@@ -40,9 +42,11 @@ __global__ void __launch_bounds__(CV_THREADS) cv_err_kernel(const double* __rest
   __syncthreads();
   const double* G = Gf + (size_t)k * p * p;
   const double* c = cf + (size_t)k * p;
-  double quad[CV_LB], lin[CV_LB];
+  // with an intercept (b0u != null): b^T X_k^T 1 from the fold's column sums (R#33)
+  const double* xs = b0u ? xsf + (size_t)k * p : nullptr;
+  double quad[CV_LB], lin[CV_LB], lsum[CV_LB];
 #pragma unroll
-  for (int b = 0; b < CV_LB; ++b) { quad[b] = 0.0; lin[b] = 0.0; }
+  for (int b = 0; b < CV_LB; ++b) { quad[b] = 0.0; lin[b] = 0.0; lsum[b] = 0.0; }
   for (int j = warp; j < p; j += nw) {
     const double* gr = G + (size_t)j * p;
     double t[CV_LB];
@@ -63,17 +67,27 @@ __global__ void __launch_bounds__(CV_THREADS) cv_err_kernel(const double* __rest
       const double bj = bs[b * p + j];
       quad[b] = fma(bj, v, quad[b]);       // b^T G_k b, rows in this warp's order
       lin[b] = fma(bj, c[j], lin[b]);      // b^T X_k^T y_k
+      if (xs) lsum[b] = fma(bj, xs[j], lsum[b]);  // b^T X_k^T 1
     }
   }
   if (lane == 0)
 #pragma unroll
-    for (int b = 0; b < CV_LB; ++b) { red[warp][b] = quad[b]; red[warp][CV_LB + b] = lin[b]; }
+    for (int b = 0; b < CV_LB; ++b) {
+      red[warp][b] = quad[b];
+      red[warp][CV_LB + b] = lin[b];
+      red[warp][2 * CV_LB + b] = lsum[b];
+    }
   __syncthreads();
   if (threadIdx.x < nb) {
     const int b = threadIdx.x;
-    double qs = 0.0, ls = 0.0;
-    for (int w = 0; w < nw; ++w) { qs += red[w][b]; ls += red[w][CV_LB + b]; }  // fixed order
-    err[((size_t)k * nP + q) * L + l0 + b] = (yyf[k] - 2.0 * ls + qs) / nk[k];
+    double qs = 0.0, ls = 0.0, ss = 0.0;
+    for (int w = 0; w < nw; ++w) { qs += red[w][b]; ls += red[w][CV_LB + b]; ss += red[w][2 * CV_LB + b]; }  // fixed order
+    double e = yyf[k] - 2.0 * ls + qs;
+    if (b0u) {  // sum_i (y_i - b0 - x_i^T b)^2 = the above - 2 b0 1^T y_k + 2 b0 b^T X_k^T 1 + n_k b0^2
+      const double b0 = b0u[((size_t)(k + boff) * nP + q) * L + l0 + b];
+      e += b0 * (2.0 * ss - 2.0 * ysf[k] + nk[k] * b0);
+    }
+    err[((size_t)k * nP + q) * L + l0 + b] = e / nk[k];
   }
 }
 
@@ -127,12 +141,15 @@ using namespace oem;
 
 extern "C" oem_status oem_cv_error(oem_ctx* ctx, const double* G_folds, const double* xty_folds,
                                    const double* yty_folds, const int64_t* counts, int32_t K, int32_t p, int32_t nP,
-                                   int32_t L, const double* beta, double* err, double* cvm, double* cvsd,
-                                   int32_t* idx_min, int32_t* idx_1se, int32_t* best, void* stream) {
+                                   int32_t L, const double* beta, const double* xsum_folds,
+                                   const double* ysum_folds, const double* intercept, double* err, double* cvm,
+                                   double* cvsd, int32_t* idx_min, int32_t* idx_1se, int32_t* best, void* stream) {
   if (!ctx) OEM_FAIL(OEM_ERR_INVALID_ARG, "null oem_ctx");
   OEM_CUDA_TRY(cudaSetDevice(ctx->device));
   if (!G_folds || !xty_folds || !yty_folds || !counts || !beta || !err || !cvm || !cvsd)
     OEM_FAIL(OEM_ERR_INVALID_ARG, "oem_cv_error: null pointer");
+  if (intercept && (!xsum_folds || !ysum_folds))
+    OEM_FAIL(OEM_ERR_INVALID_ARG, "oem_cv_error: an intercept needs the fold column sums xsum_folds / ysum_folds");
   if (K < 2 || p < 1 || nP < 1 || L < 1) OEM_FAIL(OEM_ERR_DIM, "oem_cv_error: need K >= 2, p, nP, L >= 1");
   if (nP > 64) OEM_FAIL(OEM_ERR_UNSUPPORTED, "oem_cv_error: more than 64 penalties");
   for (int k = 0; k < K; ++k)
@@ -152,7 +169,8 @@ extern "C" oem_status oem_cv_error(oem_ctx* ctx, const double* G_folds, const do
   OEM_CUDA_TRY(cudaFuncSetAttribute(cv_err_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)std::max<size_t>(smem, 1)));
   dim3 grid((unsigned)((L + LB - 1) / LB), (unsigned)nP, (unsigned)K);
   ++ctx->launches;
-  cv_err_kernel<<<grid, CV_THREADS, smem, st>>>(G_folds, xty_folds, yty_folds, nk, beta, 1, p, nP, L, LB, err);
+  cv_err_kernel<<<grid, CV_THREADS, smem, st>>>(G_folds, xty_folds, yty_folds, nk, beta, 1, p, nP, L, LB, xsum_folds,
+                                                ysum_folds, intercept, err);
   OEM_CUDA_TRY(cudaGetLastError());
   ++ctx->launches;
   cv_summary_kernel<<<1, 256, 0, st>>>(err, nk, K, nP, L, cvm, cvsd, sel);
@@ -190,7 +208,7 @@ extern "C" oem_status oem_path_loss(oem_ctx* ctx, const double* G, const double*
   OEM_CUDA_TRY(cudaFuncSetAttribute(cv_err_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)std::max<size_t>(smem, 1)));
   dim3 grid((unsigned)((L + LB - 1) / LB), (unsigned)nP, (unsigned)nG);
   ++ctx->launches;
-  cv_err_kernel<<<grid, CV_THREADS, smem, st>>>(G, xty, yty, nk, beta, 0, p, nP, L, LB, loss);
+  cv_err_kernel<<<grid, CV_THREADS, smem, st>>>(G, xty, yty, nk, beta, 0, p, nP, L, LB, nullptr, nullptr, nullptr, loss);
   OEM_CUDA_TRY(cudaGetLastError());
   return OEM_OK;
 }

@@ -101,7 +101,7 @@ def lib():
         L.oem_logistic_cfg_default.restype = None
         L.oem_fit_logistic.argtypes = [P, P, P, i64, i32, i64, ctypes.POINTER(Penalty),
                                        ctypes.POINTER(LogisticCfg), P, P, P, P, P, P]
-        L.oem_cv_error.argtypes = [P, P, P, P, P, i32, i32, i32, i32, P, P, P, P, P, P, P, P]
+        L.oem_cv_error.argtypes = [P, P, P, P, P, i32, i32, i32, i32, P, P, P, P, P, P, P, P, P, P, P]
         L.oem_logit_grad.argtypes = [P, P, P, P, i64, i32, i64, P, P, P]
         L.oem_gram_moments.argtypes = [P, P, P, i64, i32, i64, i64, i32, P, P, P]
         L.oem_gram_host.argtypes = [P, P, P, i64, i32, i64, i64, P, P, P, ctypes.POINTER(i64), P]
@@ -131,6 +131,15 @@ def _stream(stream):
     return ctypes.c_void_p(s.cuda_stream)
 
 
+def _hold_until_done(ctx, stream, *tensors):
+    """Keep host tensors alive until `stream` has passed the enqueued work that reads them (the
+    f4 copies are asynchronous: a freed pinned block could be handed out again by PyTorch's
+    caching host allocator while DMA still reads it). Finished entries are dropped on each call."""
+    ev = torch.cuda.Event()
+    ev.record(torch.cuda.current_stream() if stream is None else stream)
+    ctx._inflight = [(e, t) for e, t in ctx._inflight if not e.query()] + [(ev, tensors)]
+
+
 class Context:
     """One per (process, device): owns workspace and (nranks > 1) the NCCL communicator."""
 
@@ -138,6 +147,7 @@ class Context:
         if not torch.cuda.is_available():
             raise RuntimeError("liboem needs a CUDA device (no CPU fallback)")
         self.device, self.nranks, self.rank = device, nranks, rank
+        self._inflight = []
         h = ctypes.c_void_p()
         buf = None if uid is None else ctypes.create_string_buffer(uid, 128)
         _check(lib().oem_ctx_create(device, nranks, rank, buf, ctypes.byref(h)))
@@ -145,8 +155,9 @@ class Context:
 
     def close(self):
         if getattr(self, "h", None):
-            lib().oem_ctx_destroy(self.h)
+            lib().oem_ctx_destroy(self.h)   # synchronises the device: in-flight copies are done
             self.h = None
+            self._inflight = []
 
     def __del__(self):
         try:
@@ -321,6 +332,7 @@ def oem_gram_host(ctx: Context, X, y, block_rows: int = 1 << 20, device=None, st
     nt = ctypes.c_int64(0)
     _check(lib().oem_gram_host(ctx.h, X.data_ptr(), y.data_ptr(), n, p, X.stride(0), int(block_rows), _ptr(G),
                                _ptr(xty), _ptr(yty), ctypes.byref(nt), _stream(stream)))
+    _hold_until_done(ctx, stream, X, y)
     return G, xty, yty, nt.value
 
 
@@ -336,6 +348,7 @@ def oem_gram_folds_host(ctx: Context, X, y, K: int, row_offset: int = 0, block_r
     counts = (ctypes.c_int64 * K)()
     _check(lib().oem_gram_folds_host(ctx.h, X.data_ptr(), y.data_ptr(), n, p, X.stride(0), row_offset, K,
                                      int(block_rows), _ptr(G), _ptr(xty), _ptr(yty), counts, _stream(stream)))
+    _hold_until_done(ctx, stream, X, y)
     return G, xty, yty, list(counts)
 
 
@@ -446,9 +459,11 @@ class CvResult:
     best: int               # penalty with the smallest min cvm
 
 
-def oem_cv_error(ctx: Context, G_folds, xty_folds, yty_folds, counts, beta, stream=None) -> CvResult:
+def oem_cv_error(ctx: Context, G_folds, xty_folds, yty_folds, counts, beta, intercept=None,
+                 xsum_folds=None, ysum_folds=None, stream=None) -> CvResult:
     """f2: fast-CV error curve and selection from the fold sums and the fold-mode paths
-    (beta: [K+1][nP][L][p] from oem_fit_path(..., fold_mode=True))."""
+    (beta: [K+1][nP][L][p] from oem_fit_path(..., fold_mode=True)); for a fit with an intercept
+    pass its intercept [K+1][nP][L] and the fold column sums of oem_gram_moments."""
     K, p, _ = G_folds.shape
     nU, nP, L, pb = beta.shape
     if nU != K + 1 or pb != p:
@@ -461,9 +476,14 @@ def oem_cv_error(ctx: Context, G_folds, xty_folds, yty_folds, counts, beta, stre
     imin = (ctypes.c_int32 * nP)()
     i1se = (ctypes.c_int32 * nP)()
     best = ctypes.c_int32()
-    _check(lib().oem_cv_error(ctx.h, _ptr(G_folds.contiguous()), _ptr(xty_folds.contiguous()),
-                              _ptr(yty_folds.contiguous()), cnt, K, p, nP, L, _ptr(beta.contiguous()),
-                              _ptr(err), _ptr(cvm), _ptr(cvsd), imin, i1se, ctypes.byref(best),
+    keep = [G_folds.contiguous(), xty_folds.contiguous(), yty_folds.contiguous(), beta.contiguous()]
+    if intercept is not None:
+        if xsum_folds is None or ysum_folds is None:
+            raise ValueError("an intercept needs xsum_folds and ysum_folds (oem_gram_moments)")
+        keep += [intercept.contiguous(), xsum_folds.reshape(K, p).contiguous(), ysum_folds.reshape(K).contiguous()]
+    ptrs = [_ptr(t) for t in keep] + [None] * (7 - len(keep))
+    _check(lib().oem_cv_error(ctx.h, ptrs[0], ptrs[1], ptrs[2], cnt, K, p, nP, L, ptrs[3], ptrs[5], ptrs[6],
+                              ptrs[4], _ptr(err), _ptr(cvm), _ptr(cvsd), imin, i1se, ctypes.byref(best),
                               _stream(stream)))
     return CvResult(err, cvm, cvsd, list(imin), list(i1se), int(best.value))
 

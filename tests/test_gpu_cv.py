@@ -93,3 +93,31 @@ def test_cv_errors(ctx):
                      torch.zeros(2, dtype=torch.float64, device="cuda"), [5, 0],
                      torch.zeros((3, 1, 2, 3), dtype=torch.float64, device="cuda"))
     assert e.value.status == "OEM_ERR_EMPTY_FOLD"
+
+
+def test_cv_error_with_intercept(ctx):
+    """fold-mode fits with an intercept are scored with it. The GPU forms the held-out
+    error of y - b0 - X b from the fold sums and the fold column sums (R#33); the oracle streams
+    the held-out rows directly (orc.cv_error with intercepts)."""
+    from paper_1801_09661_b200 import oem_cv_error, oem_fit_path, oem_gram_folds, oem_gram_moments
+    n, p, K = 9_001, 24, 5
+    spec = CONFIGS["cfg3"].spec.replace(n=n, p=p, nnz=6)
+    bt = dg.beta(spec)
+    Xd, yd = device_rows(spec, bt)
+    Xd = Xd + 0.75          # columns with nonzero means and a shifted response: the intercept matters
+    yd = yd + 3.0
+    X, y = Xd.cpu().numpy(), yd.cpu().numpy()
+    Xp = torch.zeros((n, p), dtype=torch.float64, device="cuda")
+    Xp.copy_(Xd)
+    Gk, ck, yyk, cnt = oem_gram_folds(ctx, Xp, yd, K)
+    xs, ys = oem_gram_moments(ctx, Xp, yd, K)
+    pens = [("lasso", 0.0, 1.0), ("mcp", 3.0, 1.0)]
+    fit = oem_fit_path(ctx, Gk, ck, cnt, pens, nlambda=12, fold_mode=True, xsum=xs, ysum=ys)
+    cv = oem_cv_error(ctx, Gk, ck, yyk, cnt, fit.beta, intercept=fit.intercept, xsum_folds=xs, ysum_folds=ys)
+    err_o = orc.cv_error(X, y, K, fit.beta.cpu().numpy(), intercepts=fit.intercept.cpu().numpy())
+    fold = np.arange(n) % K
+    scale = np.array([np.mean((y[fold == k] - y.mean()) ** 2) for k in range(K)])[:, None, None]
+    assert np.max(np.abs(cv.err.cpu().numpy() - err_o) / scale) <= 1e-10
+    # without the intercept the same coefficients score far worse: the correction is not a no-op
+    cv0 = oem_cv_error(ctx, Gk, ck, yyk, cnt, fit.beta)
+    assert float(cv0.cvm.min()) > 2 * float(cv.cvm.min())

@@ -48,6 +48,34 @@ def test_row_offset_and_brute_force_rational():
             assert err[k, 0, l] == float(s / len(rows))
 
 
+def test_intercept_rational_and_closed_form():
+    """With intercepts the residual is y_i - b0 - x_i^T b (a fold-mode fit with an
+    intercept must be scored with it). b = 0: e_k = mean over the fold of (y_i - b0)^2 = var_k +
+    (ybar_k - b0)^2 (closed form); integer data with rational (b0, b): exact Fraction arithmetic."""
+    rng = np.random.default_rng(9)
+    n, p, K = 41, 3, 4
+    X = rng.integers(-3, 4, size=(n, p))
+    y = rng.integers(-5, 6, size=n)
+    B = np.zeros((K + 1, 1, 2, p))
+    B0 = np.array([0.0, 1.5, -2.0, 0.25, 3.0])[:, None, None] * np.ones((K + 1, 1, 2))
+    err = orc.cv_error(X.astype(float), y.astype(float), K, B, intercepts=B0)
+    for k in range(K):
+        yk = y[np.arange(n) % K == k].astype(float)
+        expect = np.var(yk) + (yk.mean() - B0[k + 1, 0, 0]) ** 2
+        assert np.allclose(err[k], expect, rtol=1e-13, atol=0)
+    B = rng.integers(-4, 5, size=(K + 1, 1, 2, p)) / 4.0
+    B0 = rng.integers(-8, 9, size=(K + 1, 1, 2)) / 8.0
+    err = orc.cv_error(X.astype(float), y.astype(float), K, B, intercepts=B0)
+    for k in range(K):
+        rows = [i for i in range(n) if i % K == k]
+        for l in range(2):
+            b = [Fraction(v) for v in B[k + 1, 0, l]]
+            b0 = Fraction(B0[k + 1, 0, l])
+            s = sum((Fraction(int(y[i])) - b0 - sum(Fraction(int(X[i, j])) * b[j] for j in range(p))) ** 2
+                    for i in rows)
+            assert err[k, 0, l] == float(s / len(rows))
+
+
 def test_summary_two_folds_closed_form():
     """K = 2, equal folds: cvm = (e1 + e2)/2 and cvsd = |e1 - e2| / 2."""
     err = np.array([[[1.0, 4.0, 2.5]], [[3.0, 1.0, 2.5]]])
