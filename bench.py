@@ -175,6 +175,71 @@ def run_reference(args, cfg):
     return 0
 
 
+# ------------------------------------------------------------------ multi-GPU validation
+def validate_combine(cfg, ctx, Xd, yd, r0, res, rank, world, dist, torch):
+    """Untimed checks of the row-sharded combine at N > 1: (1) the SHA-256 of each rank's combined
+    statistics and coefficient paths, all-gathered: they must be identical on every rank (NCCL
+    Ring/Simple gives every rank the same reduced bits; the path solve is a deterministic replica);
+    (2) on rank 0, the combined Gram on 8 columns (the first 4 and 4 in the last 128-column
+    panel) against the oracle's compensated sums over all n rows (host generator, those columns)."""
+    import hashlib
+
+    from paper_1801_09661_b200 import oem_gram, oem_gram_folds
+    if cfg.folds:
+        Gk, ck, yyk, cnt = oem_gram_folds(ctx, Xd, yd, cfg.folds, row_offset=r0)
+        G, c, yy = Gk.sum(0), ck.sum(0), yyk.sum()
+        stats = (Gk, ck, yyk)
+    else:
+        G, c, yy, _ = oem_gram(ctx, Xd, yd)
+        stats = (G, c, yy)
+    h = hashlib.sha256()
+    for t in stats + (res.beta, res.d):
+        h.update(t.detach().cpu().numpy().tobytes())
+    mine = h.hexdigest()
+    digests = [None] * world
+    if world > 1:
+        dist.all_gather_object(digests, mine)
+    else:
+        digests = [mine]
+    out = {"digests_equal": len(set(digests)) == 1, "digest": mine[:16]}
+    if rank == 0:
+        import oracle as orc
+        p = cfg.p
+        # block-equicorrelated columns are generated independently (first 4 + last 4 columns, two
+        # panels, and y from the active groups); AR(1) columns need every earlier column and y
+        # every support column, so those designs check the first 8 columns of G only
+        block = cfg.spec.design == dg.DG_BLOCK
+        blocks = [(0, 4), (p - 4, 4)] if block and p > 8 else [(0, min(8, p))]
+        idx = np.concatenate([np.arange(a, a + m) for a, m in blocks])
+        bt = dg.beta(cfg.spec, cfg.explicit_beta)
+        acc = orc.GramAccumulator(idx.size)
+        chunk = 1_000_000
+        for r in range(0, cfg.n, chunk):
+            nr = min(chunk, cfg.n - r)
+            parts, y = [], None
+            for a, m in blocks:
+                X, yb = dg.rows_host(cfg.spec, bt, r, nr, a, m, want_y=block and y is None)
+                parts.append(X)
+                y = yb if y is None else y
+            acc.add(np.ascontiguousarray(np.hstack(parts)), y if block else np.zeros(nr))
+        Go, co, yyo = acc.result()
+        Gh = G.cpu().numpy()[np.ix_(idx, idx)]
+        dd = np.sqrt(np.outer(np.diag(Go), np.diag(Go)))
+        gerr = float(np.max(np.abs(Gh - Go) / dd))
+        out.update({"oracle_columns": idx.tolist(), "gram_scale_err": gerr})
+        out["oracle_ok"] = gerr <= 1e-12
+        if block:
+            cerr = float(np.max(np.abs(c.cpu().numpy()[idx] - co) / np.sqrt(np.diag(Go) * yyo)))
+            out.update({"xty_scale_err": cerr, "yty_rel_err": abs(float(yy) - yyo) / yyo})
+            out["oracle_ok"] = out["oracle_ok"] and cerr <= 1e-12 and out["yty_rel_err"] <= 1e-12
+    ok = torch.tensor([1.0 if out["digests_equal"] and out.get("oracle_ok", True) else 0.0],
+                      dtype=torch.float64, device="cuda")
+    if world > 1:
+        dist.all_reduce(ok, op=dist.ReduceOp.MIN)
+    out["ok"] = bool(ok.item() == 1.0)
+    return out
+
+
 # ------------------------------------------------------------------ the GPU arm
 def main():
     ap = argparse.ArgumentParser()
@@ -185,6 +250,8 @@ def main():
     ap.add_argument("--impl", default="oem", choices=["oem", "reference"])
     ap.add_argument("--e2e-steps", type=int, default=2)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--validate", action="store_true",
+                    help="run the multi-GPU validation (digests + oracle column sample) also at N = 1")
     ap.add_argument("--n", type=int, default=0, help="override n (development only; not a bench number)")
     args = ap.parse_args()
     cfg = CONFIGS[args.workload]
@@ -263,22 +330,27 @@ def main():
     clocks.start()
     barrier()
     torch.cuda.synchronize()
-    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    e0.record()
-    for _ in range(args.steps):
+    ev = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps + 1)]
+    ev[0].record()
+    for k in range(args.steps):
         res = step(Xd, yd)
-    e1.record()
+        ev[k + 1].record()
     torch.cuda.synchronize()
     barrier()
+    e0, e1 = ev[0], ev[-1]
+    step_times = [ev[k].elapsed_time(ev[k + 1]) for k in range(args.steps)]
     clk = clocks.stop()
     st = oem.stats(ctx, reset=True)
     oem.set_timing(ctx, False)
     total_ms = e0.elapsed_time(e1)
     gram_phase_ms = st["gram_ms"] + st["reduce_ms"] + st["allreduce_ms"]
     step_ms = max_over_ranks(total_ms / args.steps)
+    step_median_ms = max_over_ranks(statistics.median(step_times))
+    step_min_ms = max_over_ranks(min(step_times))
     gram_step_ms = max_over_ranks(gram_phase_ms / args.steps)
     kernel_ms = max_over_ranks(st["gram_ms"] / args.steps)
     path_step_ms = max_over_ranks((st["power_ms"] + st["path_ms"]) / args.steps)  # every rank calls (collective)
+    power_step_ms = max_over_ranks(st["power_ms"] / args.steps)                    # a7 (the d rule) alone
     passes = 1
     if cfg.logistic:
         passes = max(1, round(st["launches"] / max(1, args.steps)))  # informational only
@@ -380,20 +452,36 @@ def main():
             e2e = {"value": None, "unit": "TFLOP/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0,
                    "error": repr(ex)[:200]}
 
+    # ---- multi-GPU self-validation (untimed): every rank must hold bitwise-identical combined
+    # statistics and fits (all-gathered digests), and rank 0 checks the combined Gram against the
+    # oracle on a column sample over ALL n rows
+    validation = None
+    if (world > 1 or args.validate) and not cfg.logistic:
+        validation = validate_combine(cfg, ctx, Xd, yd, r0, res, rank, world, dist, torch)
+        if not validation["ok"]:
+            if rank == 0:
+                print(json.dumps({"error": "multi-GPU validation failed", "validation": validation}), flush=True)
+            ctx.close()
+            if world > 1:
+                dist.destroy_process_group()
+            return 1
+
+    pin = None
+    if not args.no_cpu_baseline and not cfg.logistic and not cfg.folds:
+        Gf, cf, _, nf = oem_gram(ctx, Xd, yd)   # every rank: the combine is a collective
+        iters = int(res.iters.sum())
+        est = iters * float(p) * p / 2e9  # ~2 GFLOP/s single-thread naive loops
+        pin = (Gf.cpu().numpy(), cf.cpu().numpy(), nf, float(res.d[0]),
+               [res.lam[0, q].cpu().numpy() for q in range(len(cfg.penalties))], grp, ngroups, est)
+    barrier()
     if rank == 0:
         cpu = None
-        if world == 1 and not args.no_cpu_baseline:
-            pin = None
-            if not cfg.logistic and not cfg.folds:
-                Gf, cf, _, nf = oem_gram(ctx, Xd, yd)
-                iters = int(res.iters.sum())
-                est = iters * float(p) * p / 2e9  # ~2 GFLOP/s single-thread naive loops
-                pin = (Gf.cpu().numpy(), cf.cpu().numpy(), nf, float(res.d[0]),
-                       [res.lam[0, q].cpu().numpy() for q in range(len(cfg.penalties))], grp, ngroups, est)
+        if not args.no_cpu_baseline:
             cpu = cpu_baseline(cfg, path_inputs=pin)
         line = {
             "metric": METRIC, "value": value, "unit": "TFLOP/s", "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": step_ms, "fit_seconds": step_ms / 1e3,
+            "step_ms_median": step_median_ms, "step_ms_min": step_min_ms,
             "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
             "data": "synthetic (seeded Philox4x32-10 generator, generated in place on each GPU)",
             "config": {"workload": cfg.name, "n": n, "p": p, "penalties": [f for f, _, _ in cfg.penalties],
@@ -410,6 +498,8 @@ def main():
             "nccl": {"version": ".".join(str(v) for v in torch.cuda.nccl.version()) if world > 1 else None,
                      "algo": os.environ.get("NCCL_ALGO"), "proto": os.environ.get("NCCL_PROTO")},
             "cpu_baseline": cpu,
+            "power_ms": power_step_ms,
+            "validation": validation,
         }
         print(json.dumps(line), flush=True)
     ctx.close()

@@ -20,7 +20,7 @@
  *  - Errors: the boundary never throws or aborts. Each call returns an oem_status;
  *    oem_last_error() returns a thread-local detail string for the last failing call.
  *  - Multi-GPU: one process per GPU. X is row-sharded; each rank passes its own rows. When the
- *    context was created with nranks > 1, the Gram entry points sum their raw outputs over all
+ *    context holds a communicator (nranks > 1, or a uid given), the Gram entry points sum their raw outputs over all
  *    ranks with one ncclAllReduce (sum, fp64) on `stream` before returning, so every rank holds
  *    identical reduced statistics ("computed independently ... in parallel";
  *    P:L72-76 Gram quantities computed on a cluster).
@@ -54,16 +54,18 @@ const char* oem_version(void);
 /* NCCL bootstrap: rank 0 calls oem_nccl_unique_id and broadcasts the 128 bytes to the other
  * ranks (e.g. through torch.distributed); every rank then calls oem_ctx_create with it. */
 oem_status oem_nccl_unique_id(void* uid128 /*host, 128 bytes*/);
-/* One context per (process, device). nranks == 1: uid may be NULL and no NCCL is used. */
+/* One context per (process, device). nranks == 1: uid may be NULL and no NCCL is used; with a uid
+ * (from oem_nccl_unique_id in the same process) a one-rank communicator is created and every
+ * entry point takes its multi-rank path (the allreduces run, as identities) on one GPU. */
 oem_status oem_ctx_create(int device, int nranks, int rank, const void* uid128 /*host*/, oem_ctx** out);
 oem_status oem_ctx_destroy(oem_ctx* ctx);
 
 /* ---- a2 Gram pass (P:L171-172 A = dI - X^T X, u = X^T y + A beta; "the key
  * computational step in OEM is in forming the matrix A"; P:L328-333 O(np^2 + np)).
  * One pass over [X | y]: G = X^T X (full symmetric p*p written, row-major), xty = X^T y (p),
- * yty = y^T y (1). Raw sums over this rank's rows, allreduced when nranks > 1; normalisation
+ * yty = y^T y (1). Raw sums over this rank's rows, allreduced when the context has a communicator; normalisation
  * (/n, R#1) happens in oem_fit_path. n_total (host, may be NULL) receives the global row count
- * (with nranks > 1 a small NCCL allreduce on `stream`, after which the call synchronises it).
+ * (with a communicator a small NCCL allreduce on `stream`, after which the call synchronises it).
  * n_local = 0 is allowed (zero outputs). Errors: OEM_ERR_DIM (p < 1, ldx < p, n_local < 0),
  * OEM_ERR_ALIGN, OEM_ERR_UNSUPPORTED (p > 16383), OEM_ERR_CUDA, OEM_ERR_NCCL. */
 oem_status oem_gram(oem_ctx* ctx, const double* X, const double* y, int64_t n_local, int32_t p,
@@ -75,7 +77,7 @@ oem_status oem_gram(oem_ctx* ctx, const double* X, const double* y, int64_t n_lo
  * xty_folds[k*p + j], yty_folds[k]; counts[k] (host) = global rows in fold k.
  * fold(i) = (row_offset + i) mod K for local row i (R#19); row_offset = this rank's first
  * global row. Errors: as oem_gram, plus OEM_ERR_INVALID_ARG (K < 1),
- * OEM_ERR_EMPTY_FOLD (a fold with no rows globally). Synchronises `stream` only if nranks > 1
+ * OEM_ERR_EMPTY_FOLD (a fold with no rows globally). Synchronises `stream` only with a communicator
  * (the per-rank counts are host arithmetic; their sum over ranks is one small NCCL allreduce on
  * `stream`, read back before the pass). */
 oem_status oem_gram_folds(oem_ctx* ctx, const double* X, const double* y, int64_t n_local, int32_t p,
@@ -179,7 +181,7 @@ void oem_logistic_cfg_default(oem_logistic_cfg* cfg);  /* 50, 1e-3, NULL, 1e-11,
 /* ---- f1 logistic gradient pass (P:L357-359 mu(x) = 1/(1 + exp(-x^T beta)); P:L385-389 the
  * upper-bound step needs only X^T (y - mu)). One HBM-bound pass over [X | y]: g = sum_i
  * (y_i - mu_i) x_i (p) and loglik = sum_i [y_i eta_i - log(1 + e^eta_i)] (1), raw sums over this
- * rank's rows, allreduced when nranks > 1. beta (device, p) identical on every rank. No clamp of
+ * rank's rows, allreduced when the context has a communicator. beta (device, p) identical on every rank. No clamp of
  * mu (no division by w). Errors: OEM_ERR_DIM, OEM_ERR_ALIGN (X 16-byte aligned, ldx even),
  * OEM_ERR_UNSUPPORTED (p > 512), OEM_ERR_CUDA, OEM_ERR_NCCL. */
 oem_status oem_logit_grad(oem_ctx* ctx, const double* X, const double* y01, const double* beta, int64_t n_local,
@@ -208,7 +210,7 @@ oem_status oem_gram_folds_host(oem_ctx* ctx, const double* X /*host*/, const dou
 
 /* ---- f3 column sums for the intercept / standardization (R#2-3): xsum[k*p + j] = sum of
  * x_ij over this rank's rows i of fold k (fold(i) = (row_offset + i) mod K, R#19; K = 1 for the
- * whole data), ysum[k] = sum of y_i; raw sums, allreduced when nranks > 1. One HBM-bound pass.
+ * whole data), ysum[k] = sum of y_i; raw sums, allreduced when the context has a communicator. One HBM-bound pass.
  * Errors: OEM_ERR_DIM, OEM_ERR_INVALID_ARG (K < 1), OEM_ERR_UNSUPPORTED (K > 64), OEM_ERR_CUDA. */
 oem_status oem_gram_moments(oem_ctx* ctx, const double* X, const double* y, int64_t n_local, int32_t p,
                             int64_t ldx, int64_t row_offset, int32_t K, double* xsum /*K*p*/,

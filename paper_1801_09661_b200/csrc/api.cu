@@ -23,7 +23,7 @@ bool poison_enabled() {
 }
 
 oem_status allreduce_sum(oem_ctx* ctx, double* buf, size_t count, cudaStream_t st) {
-  if (ctx->nranks <= 1 || count == 0) return OEM_OK;
+  if (!ctx->nccl_comm || count == 0) return OEM_OK;
   PhaseTimer tm(ctx, PH_ALLREDUCE, st);
   ncclResult_t r = ncclAllReduce(buf, buf, count, ncclFloat64, ncclSum, (ncclComm_t)ctx->nccl_comm, st);
   if (r != ncclSuccess) OEM_FAIL(OEM_ERR_NCCL, std::string("ncclAllReduce: ") + ncclGetErrorString(r));
@@ -54,7 +54,7 @@ oem_status host_allreduce_i64(oem_ctx* ctx, int64_t* vals, int n, cudaStream_t s
   // small integer sums (row counts) across ranks: through a context-owned device buffer and NCCL
   // int64 on the caller's stream (every collective of the communicator is issued on that stream,
   // in the same order on every rank)
-  if (ctx->nranks <= 1) return OEM_OK;
+  if (!ctx->nccl_comm) return OEM_OK;
   OEM_CUDA_TRY(ctx->counts_dev.ensure(sizeof(int64_t) * (size_t)n));
   int64_t* d = ctx->counts_dev.as<int64_t>();
   OEM_CUDA_TRY(cudaMemcpyAsync(d, vals, sizeof(int64_t) * n, cudaMemcpyHostToDevice, st));
@@ -111,7 +111,7 @@ oem_status oem_ctx_create(int device, int nranks, int rank, const void* uid128, 
   c->nranks = nranks;
   c->rank = rank;
   cudaDeviceGetAttribute(&c->num_sms, cudaDevAttrMultiProcessorCount, device);
-  if (nranks > 1) {
+  if (uid128) {  // nranks == 1 with a uid: a one-rank communicator (the collective path on one GPU)
     ncclUniqueId id;
     std::memcpy(&id, uid128, 128);
     ncclComm_t comm;

@@ -90,7 +90,7 @@ extern "C" oem_status oem_fit_logistic(oem_ctx* ctx, const double* X, const doub
   OEM_CUDA_TRY(cudaMemsetAsync(beta, 0, sizeof(double) * p, st));
   // global n
   int64_t n_total = n_local;
-  if (ctx->nranks > 1) {
+  if (ctx->nccl_comm) {
     // reuse the oem_gram row-count plumbing: sum over ranks through a tiny NCCL call
     double* tmp = delta;
     double v = (double)n_local;
