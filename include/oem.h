@@ -92,8 +92,10 @@ oem_status oem_gram_folds(oem_ctx* ctx, const double* X, const double* y, int64_
  * with scalars = NULL neither is formed (the row work is then ~5% cheaper; the logistic fit,
  * whose stopping rule is the change in beta, passes NULL).
  * beta (p, device) must be identical on every rank. y01 must hold 0.0/1.0 (not checked on the
- * device; the binding checks once per fit). Errors: as oem_gram, plus OEM_ERR_UNSUPPORTED when
- * p > 247 (this build fuses eta into the single-panel kernel only). */
+ * device; the binding checks once per fit). p <= 247: eta, w, z are formed inside the Gram kernel
+ * from the staged rows (one pass); larger p (two-panel plans, whose CTAs never hold a whole row):
+ * one HBM-bound pass forms (w_i, z_i) per row, then the contraction reads them with the rows.
+ * Errors: as oem_gram. */
 oem_status oem_gram_weighted(oem_ctx* ctx, const double* X, const double* y01, const double* beta,
                              int64_t n_local, int32_t p, int64_t ldx, double eps, double* Gw,
                              double* xtwz, double* scalars, void* stream);

@@ -140,7 +140,8 @@ __device__ __forceinline__ void consume(const GramParams& P, const Cons& cs) {
   // does this job's column range hold the augmented y column (copy it into the panel)?
   const int ycol = P.p - cs.b0;
   const bool ycopy = (MODE != MODE_WEIGHTED) && C > 0 && P.p >= 8 * cs.job.bj0 && P.p < 8 * (cs.job.bj0 + C);
-  const int yidx = lane * P.ystride + (MODE == MODE_FOLD ? cs.kprime : 0);
+  // the staged value for the augmented column: y (PLAIN), y of fold kprime (FOLD), z (WZ: ys holds (w, z) pairs)
+  const int yidx = lane * P.ystride + (MODE == MODE_FOLD ? cs.kprime : MODE == MODE_WZ ? 1 : 0);
   int st = 0;
   uint32_t ph = 0;
   for (int s = 0; s < cs.nst; ++s) {
@@ -164,8 +165,8 @@ __device__ __forceinline__ void consume(const GramParams& P, const Cons& cs) {
         for (int r = 0; r < R; ++r) a[r] = pak[8 * r];
 #pragma unroll
         for (int c = 0; c < C; ++c) b[c] = pbk[8 * c];
-        if (MODE == MODE_WEIGHTED) {  // w_k scales row k (lane & 3) of the A fragments
-          const double wk = ws[ks * 4 + (lane & 3)];
+        if (MODE == MODE_WEIGHTED || MODE == MODE_WZ) {  // w_k scales row k (lane & 3) of the A fragments
+          const double wk = MODE == MODE_WZ ? ys[2 * (ks * 4 + (lane & 3))] : ws[ks * 4 + (lane & 3)];
 #pragma unroll
           for (int r = 0; r < R; ++r) a[r] *= wk;
         }
@@ -285,6 +286,80 @@ __device__ __forceinline__ void weighted_rows(const GramParams& P, const Cons& c
   }
 }
 
+// WZ pre-pass (two-panel weighted plans, R#25): one HBM-bound pass over [X | y] that
+// forms, per row, eta = x_i^T beta, mu = sigma(eta) clamped to [eps, 1-eps], w = mu(1-mu),
+// z = eta + (y - mu)/w -> wz[i] = (w_i, z_i) (the same formulas, in the same order, as
+// weighted_rows); with want_scal, per-CTA (sum w, log-likelihood) partials in warp order.
+// Warps own interleaved rows of a contiguous per-CTA range; lanes take 16-byte column pairs,
+// two rows and four pairs per lane in flight; beta lives in shared memory (zero past p).
+constexpr int RW_THREADS = 256;
+__global__ void __launch_bounds__(RW_THREADS) row_weights_kernel(const double* __restrict__ X, const double* __restrict__ y,
+                                                                 const double* __restrict__ beta, int64_t n, int p,
+                                                                 int64_t ldx, double eps, int64_t rows_per_cta,
+                                                                 int want_scal, double2* __restrict__ wz,
+                                                                 double* __restrict__ pscal) {
+  extern __shared__ __align__(16) double bsm[];
+  __shared__ double red[RW_THREADS / 32][2];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = RW_THREADS / 32;
+  const int np2 = (p + 1) >> 1;
+  for (int j = threadIdx.x; j < 2 * np2; j += RW_THREADS) bsm[j] = j < p ? beta[j] : 0.0;
+  __syncthreads();
+  const double2* b2 = reinterpret_cast<const double2*>(bsm);
+  const int64_t r0 = (int64_t)blockIdx.x * rows_per_cta, r1 = min(n, r0 + rows_per_cta);
+  double sw = 0.0, sll = 0.0;
+  for (int64_t i0 = r0 + 2 * warp; i0 < r1; i0 += 2 * nw) {
+    double e[2];
+#pragma unroll
+    for (int rb = 0; rb < 2; ++rb) {
+      const int64_t i = min(i0 + rb, r1 - 1);
+      const double2* x2 = reinterpret_cast<const double2*>(X + i * ldx);
+      double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
+      int t = lane;
+      for (; t + 96 < np2; t += 128) {
+        double2 xa = __ldg(x2 + t), xb = __ldg(x2 + t + 32), xc = __ldg(x2 + t + 64), xd = __ldg(x2 + t + 96);
+        const double2 ba = b2[t], bb = b2[t + 32], bc = b2[t + 64], bd = b2[t + 96];
+        a0 = fma(xa.x, ba.x, fma(xa.y, ba.y, a0));
+        a1 = fma(xb.x, bb.x, fma(xb.y, bb.y, a1));
+        a2 = fma(xc.x, bc.x, fma(xc.y, bc.y, a2));
+        if (2 * (t + 96) + 1 >= p) xd.y = 0.0;  // the last pair may hold the pad element of an odd p
+        a3 = fma(xd.x, bd.x, fma(xd.y, bd.y, a3));
+      }
+      for (; t < np2; t += 32) {
+        double2 xa = __ldg(x2 + t);
+        if (2 * t + 1 >= p) xa.y = 0.0;  // the pad element of an odd p (never trusted)
+        a0 = fma(xa.x, b2[t].x, fma(xa.y, b2[t].y, a0));
+      }
+      double v = (a0 + a1) + (a2 + a3);
+#pragma unroll
+      for (int o = 16; o >= 1; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+      e[rb] = v;
+    }
+    if (lane < 2 && i0 + lane < r1) {
+      const int64_t i = i0 + lane;
+      const double ee = lane == 0 ? e[0] : e[1], yk = __ldg(y + i);
+      const double ex = exp(-ee);
+      double mu = 1.0 / (1.0 + ex);
+      mu = fmin(fmax(mu, eps), 1.0 - eps);
+      const double w = mu * (1.0 - mu);
+      wz[i] = make_double2(w, ee + (yk - mu) / w);
+      if (want_scal) {
+        sw += w;
+        sll += yk * ee - (isinf(ex) ? 0.0 : ee + log1p(ex));
+      }
+    }
+  }
+  if (!want_scal) return;
+  sw += __shfl_xor_sync(0xffffffffu, sw, 1);   // lanes 0 and 1, fixed order
+  sll += __shfl_xor_sync(0xffffffffu, sll, 1);
+  if (lane == 0) { red[warp][0] = sw; red[warp][1] = sll; }
+  __syncthreads();
+  if (threadIdx.x < 2) {
+    double a = 0.0;
+    for (int w = 0; w < nw; ++w) a += red[w][threadIdx.x];  // warp order
+    pscal[2 * blockIdx.x + threadIdx.x] = a;
+  }
+}
+
 template <int MODE, bool TWO>
 __global__ void __launch_bounds__(gram_threads(MODE, TWO), 1)
 gram_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ CUtensorMap tmY, const GramParams P) {
@@ -373,7 +448,8 @@ gram_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ CUt
           } else {
             tma_load_2d(pa, &tmX, &cs.full[st], cs.a0, rr);
             if (cs.two) tma_load_2d(pb, &tmX, &cs.full[st], cs.b0, rr);
-            if (P.ytma) tma_load_1d(ys, &tmY, &cs.full[st], rr);
+            if (MODE == MODE_WZ) tma_load_2d(ys, &tmY, &cs.full[st], 0, rr);   // (w, z) of the stage's rows
+            else if (P.ytma) tma_load_1d(ys, &tmY, &cs.full[st], rr);
           }
         }
         if (!P.ytma) {  // odd-K folds: strided y through the producer's lanes
@@ -418,7 +494,7 @@ gram_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ CUt
 __global__ void gram_reduce_kernel(const double* __restrict__ partial, int nfold, int nseg, int nblk,
                                    const int2* __restrict__ blk_coord, int p, const double* __restrict__ tail,
                                    double* __restrict__ packed, int64_t psize, const double* __restrict__ pscal,
-                                   int with_scal, int accumulate) {
+                                   int nscal, int with_scal, int accumulate) {
   const int64_t total = (int64_t)nfold * nblk * 64;
   for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < total; t += (int64_t)gridDim.x * blockDim.x) {
     const int e = (int)(t & 63);
@@ -437,7 +513,7 @@ __global__ void gram_reduce_kernel(const double* __restrict__ partial, int nfold
   }
   if (with_scal && blockIdx.x == 0 && threadIdx.x < 2) {
     double s = 0.0;
-    for (int g = 0; g < nseg; ++g) s += pscal[g * 2 + threadIdx.x];
+    for (int g = 0; g < nscal; ++g) s += pscal[g * 2 + threadIdx.x];
     packed[psize + threadIdx.x] = accumulate ? packed[psize + threadIdx.x] + s : s;
   }
 }
@@ -578,8 +654,8 @@ static oem_status build_plan(oem_ctx* ctx, int mode, int p, int64_t nrows, int K
   const int Pa = p + 1;
   const int nb_exact = (Pa + 7) / 8;
   const bool single = (8 * nb_exact + 4) <= 256;
-  if (mode == MODE_WEIGHTED && !single)
-    OEM_FAIL(OEM_ERR_UNSUPPORTED, "oem_gram_weighted: p > 247 is not supported by the fused single-panel kernel");
+  if ((mode == MODE_WEIGHTED && !single) || (mode == MODE_WZ && single))
+    OEM_FAIL(OEM_ERR_UNSUPPORTED, "gram: weighted plan kind does not match p (internal)");
   pl.two_panel = single ? 0 : 1;
   // two-panel plans pad the block count to whole 128-column panels (zero columns, TMA fill)
   pl.nb = single ? nb_exact : (nb_exact + 15) / 16 * 16;
@@ -678,6 +754,9 @@ static oem_status build_plan(oem_ctx* ctx, int mode, int p, int64_t nrows, int K
   if (mode == MODE_FOLD) {
     pl.ytma = (K % 2 == 0) && K <= 256;
     pl.ystride = pl.ytma ? K : K;  // smem row stride of ys in doubles
+  } else if (mode == MODE_WZ) {   // (w, z) pairs: 2D box [BK][2]
+    pl.ytma = 1;
+    pl.ystride = 2;
   } else {
     pl.ytma = 1;
     pl.ystride = 1;
@@ -784,18 +863,21 @@ oem_status gram_pass(oem_ctx* ctx, int mode, const double* X, const double* y, c
   const int nfold = mode == MODE_FOLD ? K : 1;
   const int64_t psize = packed_size(p);
   const int64_t nq = mode == MODE_FOLD ? n_local / K : n_local;
+  // the weighted pass of two-panel plans: row weights first (HBM-bound), then the WZ contraction
+  const bool wz = mode == MODE_WEIGHTED && (8 * ((p + 1 + 7) / 8) + 4) > 256;
+  const int kmode = wz ? (int)MODE_WZ : mode;
   if (n_local == 0 || nq == 0) {
     if (!accumulate)
       OEM_CUDA_TRY(cudaMemsetAsync(packed, 0, sizeof(double) * (nfold * psize + (mode == MODE_WEIGHTED ? 2 : 0)), st));
     if (mode != MODE_FOLD || n_local == 0) return OEM_OK;
   }
-  auto key = std::make_tuple(mode, p, nq, K);
+  auto key = std::make_tuple(kmode, p, nq, K);
   std::shared_ptr<GramPlan> plp;
   auto it = ctx->plans.find(key);
   if (it != ctx->plans.end()) plp = it->second;
   else {
     plp = std::make_shared<GramPlan>();
-    oem_status s = build_plan(ctx, mode, p, std::max<int64_t>(nq, 1), K, *plp);
+    oem_status s = build_plan(ctx, kmode, p, std::max<int64_t>(nq, 1), K, *plp);
     if (s != OEM_OK) return s;
     ctx->plans[key] = plp;
   }
@@ -808,12 +890,42 @@ oem_status gram_pass(oem_ctx* ctx, int mode, const double* X, const double* y, c
     OEM_CUDA_TRY(ctx->tail.ensure(sizeof(double) * (size_t)K * pl.nblk * 64));
     tail = ctx->tail.as<double>();
   }
+  int nscal = nq > 0 ? pl.nseg : 0;   // WEIGHTED: (sum w, loglik) partials to add in order
+  const double* yin = y;
+  if (wz && nq > 0) {
+    // per-row (w, z) and the scalar partials, one HBM-bound pass (row_weights_kernel)
+    const int64_t rows_per = std::max<int64_t>(64, (n_local + 4 * ctx->num_sms - 1) / (4 * ctx->num_sms));
+    const int nb_rw = (int)((n_local + rows_per - 1) / rows_per);
+    OEM_CUDA_TRY(ctx->wz.ensure(sizeof(double) * 2 * (size_t)n_local));
+    OEM_CUDA_TRY(ctx->partial_scal.ensure(sizeof(double) * 2 * (size_t)std::max(nb_rw, pl.nseg) + 16));
+    const size_t bsmem = sizeof(double) * (size_t)(2 * ((p + 1) / 2));
+    if (bsmem > 48 * 1024)
+      OEM_CUDA_TRY(cudaFuncSetAttribute(row_weights_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bsmem));
+    PhaseTimer tm(ctx, PH_GRAM, st);
+    ++ctx->launches;
+    row_weights_kernel<<<nb_rw, RW_THREADS, bsmem, st>>>(X, y, beta, n_local, p, ldx, eps, rows_per, want_scal,
+                                                          ctx->wz.as<double2>(), ctx->partial_scal.as<double>());
+    OEM_CUDA_TRY(cudaGetLastError());
+    nscal = want_scal ? nb_rw : 0;
+    yin = ctx->wz.as<double>();
+  }
   if (nq > 0) {
     CUtensorMap mx, my;
     std::memset(&my, 0, sizeof(my));
     const cuuint32_t boxw = (cuuint32_t)pl.ld;
     oem_status s;
-    if (mode == MODE_FOLD) {
+    if (kmode == MODE_WZ) {
+      cuuint64_t dims[2] = {(cuuint64_t)p, (cuuint64_t)n_local};
+      cuuint64_t strides[1] = {(cuuint64_t)ldx * 8};
+      cuuint32_t box[2] = {boxw, (cuuint32_t)BK};
+      s = make_map(&mx, X, 2, dims, strides, box);
+      if (s == OEM_OK) {
+        cuuint64_t yd[2] = {2, (cuuint64_t)n_local};
+        cuuint64_t ys[1] = {16};
+        cuuint32_t yb[2] = {2, (cuuint32_t)BK};
+        s = make_map(&my, yin, 2, yd, ys, yb);
+      }
+    } else if (mode == MODE_FOLD) {
       cuuint64_t dims[3] = {(cuuint64_t)p, (cuuint64_t)K, (cuuint64_t)nq};
       cuuint64_t strides[2] = {(cuuint64_t)ldx * 8, (cuuint64_t)ldx * 8 * K};
       cuuint32_t box[3] = {boxw, 1, (cuuint32_t)BK};
@@ -860,7 +972,8 @@ oem_status gram_pass(oem_ctx* ctx, int mode, const double* X, const double* y, c
       else ls = launch_t<MODE_WEIGHTED, false>(pl, mx, my, P, nfold, st);
     } else {
       if (mode == MODE_PLAIN) ls = launch_t<MODE_PLAIN, true>(pl, mx, my, P, nfold, st);
-      else ls = launch_t<MODE_FOLD, true>(pl, mx, my, P, nfold, st);
+      else if (mode == MODE_FOLD) ls = launch_t<MODE_FOLD, true>(pl, mx, my, P, nfold, st);
+      else ls = launch_t<MODE_WZ, true>(pl, mx, my, P, nfold, st);
     }
     if (ls != OEM_OK) return ls;
   }
@@ -883,18 +996,19 @@ oem_status gram_pass(oem_ctx* ctx, int mode, const double* X, const double* y, c
       const int64_t total = (int64_t)nfold * S * pl.nblk * 64;
       const int blocks = (int)std::max<int64_t>(1, std::min<int64_t>(ctx->num_sms * 16, (total + 255) / 256));
       ++ctx->launches;
+      const bool chunk_scal = mode == MODE_WEIGHTED && !wz;   // the fused pass: scalars per segment
       gram_chunk_kernel<<<blocks, 256, 0, st>>>(src, nfold, nseg, pl.nblk, S, per, out,
-                                                mode == MODE_WEIGHTED ? sscal : nullptr, oscal);
+                                                chunk_scal ? sscal : nullptr, oscal);
       OEM_CUDA_TRY(cudaGetLastError());
       src = out;
-      sscal = oscal;
+      if (chunk_scal) { sscal = oscal; nscal = S; }
       nseg = S;
     }
     const int64_t total = (int64_t)nfold * pl.nblk * 64;
     const int blocks = (int)std::max<int64_t>(1, std::min<int64_t>(ctx->num_sms * 8, (total + 255) / 256));
     ++ctx->launches;
     gram_reduce_kernel<<<blocks, 256, 0, st>>>(src, nfold, nseg, pl.nblk, pl.d_blk_coord, p, tail, packed, psize, sscal,
-                                               mode == MODE_WEIGHTED, accumulate);
+                                               nscal, mode == MODE_WEIGHTED, accumulate);
     OEM_CUDA_TRY(cudaGetLastError());
   }
   return OEM_OK;

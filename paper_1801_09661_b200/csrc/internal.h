@@ -57,7 +57,7 @@ struct oem_ctx {
   int nranks = 1, rank = 0;
   int num_sms = 148;
   void* nccl_comm = nullptr;  // ncclComm_t
-  oem::DevBuf partial, partial2, counts_dev, partial_scal, packed, tail, plan_tables, path_ws, path_small, logi, lg_part, lg_out, mom_part, mom_out, stage0, stage1, drule_ws;
+  oem::DevBuf partial, partial2, counts_dev, partial_scal, packed, tail, plan_tables, path_ws, path_small, logi, lg_part, lg_out, mom_part, mom_out, stage0, stage1, drule_ws, wz;
   cudaStream_t copy_stream = nullptr;  // f4 host streaming: H2D copies overlap the Gram kernel
   cudaEvent_t ev_copied[2] = {nullptr, nullptr}, ev_used[2] = {nullptr, nullptr};
   std::map<std::tuple<int, int, int64_t, int>, std::shared_ptr<oem::GramPlan>> plans;
@@ -96,7 +96,9 @@ struct PhaseTimer {
   }
 };
 
-enum GramMode { MODE_PLAIN = 0, MODE_FOLD = 1, MODE_WEIGHTED = 2 };
+// MODE_WZ (internal): the weighted pass of two-panel plans (p > 247), whose CTAs never see a whole
+// row: w_i and z_i come precomputed per row (row_weights_kernel) through the y staging box.
+enum GramMode { MODE_PLAIN = 0, MODE_FOLD = 1, MODE_WEIGHTED = 2, MODE_WZ = 3 };
 
 // One pass over [X | y] producing the packed upper triangle of the augmented
 // (p+1)x(p+1) Gram per fold (nfold = K for MODE_FOLD else 1), raw sums, this rank only.

@@ -130,14 +130,17 @@ extern "C" oem_status oem_fit_logistic(oem_ctx* ctx, const double* X, const doub
     OEM_CUDA_TRY(cudaStreamSynchronize(st));
     const double scale = pen->family == OEM_ENET ? pen->alpha : 1.0;
     double lmax = 0.0;
+    // c_w at beta = 0 is sum_i x_ij (y_i - 1/2), normalised exactly as the path solver does
+    // (times 1/n, prep_units_kernel), so beta = 0 is an exact fixed point at lambda_max
+    const double inv_n = 1.0 / (double)n_total;
     if (!grp) {
-      for (int j = 0; j < p; ++j)  // c_w at beta = 0 is sum_i x_ij (y_i - 1/2)
-        if (hw[j] > 0.0) lmax = std::fmax(lmax, std::fabs(hc[j] / (double)n_total) / (scale * hw[j]));
+      for (int j = 0; j < p; ++j)
+        if (hw[j] > 0.0) lmax = std::fmax(lmax, std::fabs(hc[j] * inv_n) / (scale * hw[j]));
     } else {  // max_k ||c_{g_k}|| / c_k (R#12, R#14)
       std::vector<double> ss(cfg.ngroups, 0.0);
       std::vector<int> sz(cfg.ngroups, 0);
       for (int j = 0; j < p; ++j) {
-        const double c = hc[j] / (double)n_total;
+        const double c = hc[j] * inv_n;
         ss[cfg.group[j]] += c * c;
         sz[cfg.group[j]]++;
       }

@@ -370,10 +370,40 @@ def test_weighted_extreme_eta_and_no_scalars(ctx):
     assert torch.equal(Gn, Gw) and torch.equal(cn, cw)
 
 
-def test_weighted_unsupported_large_p(ctx):
-    from paper_1801_09661_b200 import OemError, oem_gram_weighted
-    X = torch.zeros((10, 300), dtype=torch.float64, device="cuda")
-    with pytest.raises(OemError) as e:
-        oem_gram_weighted(ctx, X, torch.zeros(10, dtype=torch.float64, device="cuda"),
-                          torch.zeros(300, dtype=torch.float64, device="cuda"))
-    assert e.value.status == "OEM_ERR_UNSUPPORTED"
+@pytest.mark.parametrize("n,p", [(6001, 248), (4001, 255), (3003, 500), (2011, 1000), (1001, 1031)])
+def test_weighted_two_panel_parity(ctx, n, p):
+    """p > 247 (two-panel plans; the paper's §6.3 logistic study varies p up to 500):
+    the (w, z) pre-pass plus the WZ contraction against the oracle's weighted Gram (R#25), with
+    the scalars; ragged tails (n not a multiple of 32) and a last panel holding the augmented
+    column at every offset class."""
+    from paper_1801_09661_b200 import oem_gram_weighted
+    spec = CONFIGS["cfg5"].spec.replace(n=n, p=p, nnz=min(20, p))
+    bt = dg.beta(spec)
+    Xd, yd = device_rows(spec, bt)
+    X, y = dg.rows_host(spec, bt)
+    beta = 0.7 * bt + 0.02 * np.cos(np.arange(p))
+    Gw, cw, sc = oem_gram_weighted(ctx, Xd, yd, to_dev(beta))
+    Go, co, sco = orc.gram_weighted(X, y, beta)
+    assert scale_err(Gw.cpu().numpy(), Go) <= 1e-12
+    eta = X @ beta
+    mu = np.clip(1 / (1 + np.exp(-eta)), 1e-5, 1 - 1e-5)
+    w = mu * (1 - mu)
+    szz = np.sum(w * (eta + (y - mu) / w) ** 2)
+    assert np.max(np.abs(cw.cpu().numpy() - co) / np.sqrt(np.diag(Go) * szz)) <= 1e-12
+    assert abs(float(sc[0]) - sco[0]) <= 1e-12 * sco[0]
+    assert abs(float(sc[1]) - sco[1]) <= 1e-12 * abs(sco[1])
+    Gn, cn, sn = oem_gram_weighted(ctx, Xd, yd, to_dev(beta), scalars=False)
+    assert torch.equal(Gn, Gw) and torch.equal(cn, cw)
+
+
+def test_weighted_two_panel_zero_beta_exact(ctx):
+    """beta = 0: w = 1/4 and w z = y - 1/2 exactly, so on integer data G_w = X^T X / 4 and
+    X^T W z = X^T (y - 1/2) are exact in any summation order: bit-exact at p = 300."""
+    from paper_1801_09661_b200 import oem_gram_weighted
+    X, _ = int_design(11, 2049, 300)
+    y = (np.random.default_rng(11).random(2049) < 0.4).astype(float)
+    Gw, cw, sc = oem_gram_weighted(ctx, to_dev(X), to_dev(y), torch.zeros(300, dtype=torch.float64, device="cuda"))
+    Go, co, sco = orc.gram_weighted(X, y, np.zeros(300))
+    assert np.array_equal(Gw.cpu().numpy(), Go)
+    assert np.array_equal(cw.cpu().numpy(), co)
+    assert float(sc[0]) == sco[0]

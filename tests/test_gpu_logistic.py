@@ -21,7 +21,7 @@ def ctx():
     c.close()
 
 
-@pytest.mark.parametrize("n,p,L", [(4000, 20, 12), (20_011, 200, 8)])
+@pytest.mark.parametrize("n,p,L", [(4000, 20, 12), (20_011, 200, 8), (6_001, 500, 4)])
 def test_logistic_path_parity(ctx, n, p, L):
     from paper_1801_09661_b200 import oem_fit_logistic
     spec = CONFIGS["cfg5"].spec.replace(n=n, p=p, nnz=min(20, p // 2))
@@ -179,3 +179,21 @@ def test_logistic_full_size_cfg5(ctx):
     assert np.max(np.abs(Bg - B)) <= 1e-8, np.max(np.abs(Bg - B))
     assert np.array_equal(np.array(fit.conv), cv) and cv.all()
     assert np.max(np.abs(np.array(fit.outer_iters) - oi)) <= 1
+
+
+def test_logistic_group_lasso_p250_exact_hessian(ctx):
+    """The paper's §6.3 shape for grouped logistic regression (p up to 500, groups
+    of 25, exact-Hessian proximal Newton): p = 250 runs the two-panel weighted pass every outer
+    step; against O7 with the same groups."""
+    from paper_1801_09661_b200 import oem_fit_logistic
+    n, p, L = 5000, 250, 5
+    spec = CONFIGS["cfg5"].spec.replace(n=n, p=p, nnz=10)
+    bt = dg.beta(spec)
+    Xd, yd = device_rows(spec, bt)
+    X, y = dg.rows_host(spec, bt)
+    grp = (np.arange(p) // 25).astype(np.int32)
+    fit = oem_fit_logistic(ctx, Xd, yd, ("grp_lasso", 0.0, 1.0), nlambda=L, group=grp)
+    lam = fit.lam.cpu().numpy()
+    B, oi, ii, cv = orc.logistic_path(X, y, lam, family="grp_lasso", group=grp)
+    assert np.max(np.abs(fit.beta.cpu().numpy() - B)) <= 1e-8
+    assert np.array_equal(np.array(fit.conv), cv)

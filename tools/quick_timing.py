@@ -26,6 +26,7 @@ def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--cfg", default="cfg2")
     ap.add_argument("--n", type=int, default=0)
+    ap.add_argument("--p", type=int, default=0, help="override p (same design recipe)")
     ap.add_argument("--reps", type=int, default=3)
     ap.add_argument("--nofit", action="store_true")
     ap.add_argument("--plain", action="store_true", help="plain Gram pass even for folds / logistic workloads")
@@ -34,6 +35,8 @@ def main():
     cfg = CONFIGS[a.cfg]
     if a.n:
         cfg = cfg.with_n(a.n)
+    if a.p:
+        cfg.spec = cfg.spec.replace(p=a.p, nnz=min(cfg.spec.nnz, a.p))
     ctx = Context(0)
     bt = dg.beta(cfg.spec, cfg.explicit_beta)
     t0 = time.time()
@@ -41,7 +44,7 @@ def main():
     torch.cuda.synchronize()
     gen_s = time.time() - t0
     n, p = cfg.n, cfg.p
-    flops = n * p * (p + 3)
+    flops = n * p * (p + 6) if (cfg.logistic and not a.plain) else n * p * (p + 3)
     out = {"cfg": cfg.name, "n": n, "p": p, "gen_s": gen_s}
     grp = groups_of(cfg)
     for r in range(a.reps + 1):
