@@ -36,7 +36,7 @@ from datagen.configs import CONFIGS, groups_of  # noqa: E402
 
 METRIC = "Gram fp64 TFLOP/s (X^TX+X^Ty) and full-path fit seconds at 1/2/4/8 B200"
 FP64_PEAK_TFLOPS = 37.06   # measured DMMA peak, profiles/fp64_peak_r01.log (MEASURED_PEAKS.json has no fp64)
-HBM_PEAK_GBS = 6541.5      # MEASURED_PEAKS.json
+HBM_PEAK_GBS = 6549.8      # MEASURED_PEAKS.json (copy bandwidth, burst)
 
 
 def gram_flops(n, p):
@@ -48,6 +48,15 @@ def weighted_flops(n, p):
     """Algorithmic flops of one weighted pass: n p (p+1) (SYRK) + 2 n p (X^T W z)
     + 2 n p (eta = X beta) + n p (weight scaling) = n p (p+6)."""
     return float(n) * p * (p + 6)
+
+
+def sample_flops(cfg, X):
+    """Algorithmic flops of the Gram pass over the sample rows X: dense n p (p+3); for the sparse
+    workload (f4) the products of each row's nonzeros, m (m+1) + 4 m + 2 per row (R#38)."""
+    if cfg.spec.design == dg.DG_SPARSE:
+        m = (X != 0).sum(axis=1).astype(float)
+        return float(np.sum(m * (m + 1) + 4 * m + 2))
+    return gram_flops(X.shape[0], X.shape[1])
 
 
 # ------------------------------------------------------------------ clocks sampler
@@ -122,7 +131,7 @@ def cpu_baseline(cfg, budget_s=15.0, path_inputs=None):
     t0 = time.perf_counter()
     orc.gram(X, y, nthreads=cores)
     dt = time.perf_counter() - t0
-    out = {"value": gram_flops(rows, cfg.p) / dt / 1e12, "unit": "TFLOP/s", "cores": cores, "kind": "oracle",
+    out = {"value": sample_flops(cfg, X) / dt / 1e12, "unit": "TFLOP/s", "cores": cores, "kind": "oracle",
            "cpu_model": cpu_model(),
            "sample": f"oracle Gram (compensated fp64, {cores} threads) over rows 0..{rows} of {cfg.name} "
                      f"(n={cfg.n}, p={cfg.p}), {dt:.2f} s"}
@@ -160,7 +169,7 @@ def run_reference(args, cfg):
         dt = time.perf_counter() - t0
         if s >= args.warmup:
             times.append(dt)
-    v = gram_flops(rows, cfg.p) / (sum(times) / len(times)) / 1e12
+    v = sample_flops(cfg, X) / (sum(times) / len(times)) / 1e12
     line = {"impl": "reference", "metric": METRIC, "value": v, "unit": "TFLOP/s", "n_gpus": args.gpus,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * sum(times) / len(times),
             "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
@@ -176,7 +185,7 @@ def run_reference(args, cfg):
 
 
 # ------------------------------------------------------------------ multi-GPU validation
-def validate_combine(cfg, ctx, Xd, yd, r0, res, rank, world, dist, torch):
+def validate_combine(cfg, ctx, Xd, yd, r0, res, rank, world, dist, torch, csr=None):
     """Untimed checks of the row-sharded combine at N > 1: (1) the SHA-256 of each rank's combined
     statistics and coefficient paths, all-gathered: they must be identical on every rank (NCCL
     Ring/Simple gives every rank the same reduced bits; the path solve is a deterministic replica);
@@ -184,8 +193,11 @@ def validate_combine(cfg, ctx, Xd, yd, r0, res, rank, world, dist, torch):
     panel) against the oracle's compensated sums over all n rows (host generator, those columns)."""
     import hashlib
 
-    from paper_1801_09661_b200 import oem_gram, oem_gram_folds
-    if cfg.folds:
+    from paper_1801_09661_b200 import oem_gram, oem_gram_csr, oem_gram_folds
+    if csr is not None:
+        G, c, yy, _ = oem_gram_csr(ctx, *csr, cfg.p)
+        stats = (G, c, yy)
+    elif cfg.folds:
         Gk, ck, yyk, cnt = oem_gram_folds(ctx, Xd, yd, cfg.folds, row_offset=r0)
         G, c, yy = Gk.sum(0), ck.sum(0), yyk.sum()
         stats = (Gk, ck, yyk)
@@ -208,7 +220,7 @@ def validate_combine(cfg, ctx, Xd, yd, r0, res, rank, world, dist, torch):
         # block-equicorrelated columns are generated independently (first 4 + last 4 columns, two
         # panels, and y from the active groups); AR(1) columns need every earlier column and y
         # every support column, so those designs check the first 8 columns of G only
-        block = cfg.spec.design == dg.DG_BLOCK
+        block = cfg.spec.design in (dg.DG_BLOCK, dg.DG_SPARSE)   # independent columns
         blocks = [(0, 4), (p - 4, 4)] if block and p > 8 else [(0, min(8, p))]
         idx = np.concatenate([np.arange(a, a + m) for a, m in blocks])
         bt = dg.beta(cfg.spec, cfg.explicit_beta)
@@ -262,7 +274,7 @@ def main():
 
     import torch
     import torch.distributed as dist
-    from paper_1801_09661_b200 import Context, oem, oem_fit_path, oem_gram, oem_gram_folds
+    from paper_1801_09661_b200 import Context, oem, oem_fit_path, oem_gram, oem_gram_csr, oem_gram_folds
     from paper_1801_09661_b200.oem import oem_fit_logistic
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
@@ -286,6 +298,11 @@ def main():
         if world > 1:
             dist.barrier()
 
+    def sum_over_ranks(x):
+        t = torch.tensor([x], dtype=torch.float64, device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.SUM)
+        return float(t)
+
     def max_over_ranks(x):
         if world == 1:
             return x
@@ -299,12 +316,26 @@ def main():
     nl = r1 - r0
     bt = dg.beta(cfg.spec, cfg.explicit_beta)
     ldx = p + (p & 1)
-    Xs = torch.empty((nl, ldx), dtype=torch.float64, device="cuda")
-    Xd = Xs[:, :p]
-    yd = torch.empty(nl, dtype=torch.float64, device="cuda")
-    btd = torch.from_numpy(bt).cuda()
-    dg.rows_cuda(cfg.spec, btd.data_ptr(), r0, nl, Xs.data_ptr(), ldx, yd.data_ptr(),
-                 torch.cuda.current_stream().cuda_stream)
+    sparse = cfg.spec.design == dg.DG_SPARSE
+    csr = None
+    if sparse:
+        # f4: this rank's rows in CSR form (row offsets, ascending column indices, values)
+        csr = dg.csr_cuda(cfg.spec, bt, r0, nl)
+        Xs = Xd = None
+        yd = csr[3]
+        m = (csr[0][1:] - csr[0][:-1]).double()
+        # algorithmic work of the sparse pass: row i has m_i nonzeros and contributes
+        # m_i (m_i + 1)/2 + m_i + 1 products (2 flops each); it reads row_ptr, y and 12 B per nonzero
+        sp_flops_local = float((m * (m + 1) + 4 * m + 2).sum())
+        sp_bytes_local = float(8 * (nl + 1) + 8 * nl + 12 * int(csr[1].numel()))
+        sp_nnz = int(csr[1].numel())
+    else:
+        Xs = torch.empty((nl, ldx), dtype=torch.float64, device="cuda")
+        Xd = Xs[:, :p]
+        yd = torch.empty(nl, dtype=torch.float64, device="cuda")
+        btd = torch.from_numpy(bt).cuda()
+        dg.rows_cuda(cfg.spec, btd.data_ptr(), r0, nl, Xs.data_ptr(), ldx, yd.data_ptr(),
+                     torch.cuda.current_stream().cuda_stream)
     torch.cuda.synchronize()
     grp = groups_of(cfg)
     ngroups = p // cfg.group_size if grp is not None else 0
@@ -316,7 +347,7 @@ def main():
         if cfg.folds:
             G, c, yy, cnt = oem_gram_folds(ctx, X, y, cfg.folds, row_offset=r0)
         else:
-            G, c, yy, nn = oem_gram(ctx, X, y)
+            G, c, yy, nn = oem_gram_csr(ctx, *csr[:3], y, p) if sparse else oem_gram(ctx, X, y)
             cnt = [nn]
         return oem_fit_path(ctx, G, c, cnt, cfg.penalties, nlambda=cfg.nlambda, fold_mode=bool(cfg.folds),
                             group=grp, ngroups=ngroups)
@@ -359,6 +390,8 @@ def main():
         # every outer step is one weighted pass; count them from the fit
         outer = sum(res.outer_iters)
         flops_step = weighted_flops(n, p) * outer
+    if sparse:
+        flops_step = max_over_ranks(sp_flops_local) if world == 1 else sum_over_ranks(sp_flops_local)
     value = flops_step / (gram_step_ms * 1e-3) / 1e12
     # roofline of the dominant kernel (the tensor-core Gram kernel): algorithmic flops per
     # launch over its event-timed launch duration on this rank
@@ -371,6 +404,10 @@ def main():
             traffic = json.load(open(prof)).get(cfg.name, {}).get("dram_bytes_per_launch")
         except Exception:
             traffic = None
+    if sparse:
+        # the sparse pass is bound by reading the CSR arrays: algorithmic bytes per launch
+        # (8 (n+1) row offsets + 8 n for y + 12 per nonzero) over the event-timed launch
+        achieved = sp_bytes_local / (st["gram_ms"] / args.steps * 1e-3) / 1e9
     roofline = {"bound": "tensor", "achieved": achieved, "peak": FP64_PEAK_TFLOPS, "unit": "TFLOP/s",
                 "frac": achieved / FP64_PEAK_TFLOPS, "traffic": traffic,
                 "kernel": "oem::gram_kernel (TMA + DMMA.8x8x4)",
@@ -379,6 +416,11 @@ def main():
                 "share_of_step": st["gram_ms"] / max(total_ms, 1e-9),
                 "hbm_gbs": 8.0 * nl * (p + 1) * (sum(res.outer_iters) if cfg.logistic else 1)
                            / (st["gram_ms"] / args.steps * 1e-3) / 1e9}
+    if sparse:
+        roofline.update({"bound": "hbm", "peak": HBM_PEAK_GBS, "unit": "GB/s", "frac": achieved / HBM_PEAK_GBS,
+                         "kernel": "oem::sparse_gram_kernel (CSR, cp.async ring, warp-owned triangle rows)",
+                         "peak_source": "MEASURED_PEAKS.json hbm_gbs (copy bandwidth)",
+                         "hbm_gbs": achieved, "bytes_per_launch": sp_bytes_local, "nnz_local": sp_nnz})
     launches = int(st["launches"])
 
     # ---- e2e: the same metric through the public API with HOST buffers (pinned). Linear
@@ -390,10 +432,15 @@ def main():
     if args.e2e_steps > 0:
         try:
             from paper_1801_09661_b200 import oem_gram_folds_host, oem_gram_host
-            Xh = torch.empty((nl, ldx), dtype=torch.float64, pin_memory=True)
-            yh = torch.empty(nl, dtype=torch.float64, pin_memory=True)
-            Xh.copy_(Xs)
-            yh.copy_(yd)
+            if sparse:   # pinned host copies of the CSR arrays; copied to the device inside each step
+                hcsr = [t.cpu().pin_memory() for t in csr]
+                in_bytes = sum(t.numel() * t.element_size() for t in hcsr)
+            else:
+                Xh = torch.empty((nl, ldx), dtype=torch.float64, pin_memory=True)
+                yh = torch.empty(nl, dtype=torch.float64, pin_memory=True)
+                Xh.copy_(Xs)
+                yh.copy_(yd)
+                in_bytes = nl * ldx * 8 + nl * 8
             torch.cuda.synchronize()
             blk = 1 << 20
             out_bytes = 0
@@ -415,6 +462,12 @@ def main():
                     yd.copy_(yh, non_blocking=True)
                     r = oem_fit_logistic(ctx, Xd, yd, cfg.penalties[0], nlambda=cfg.nlambda)
                     tb.record()
+                elif sparse:
+                    for dst, src in zip(csr, hcsr):
+                        dst.copy_(src, non_blocking=True)
+                    G, c, yy, nn = oem_gram_csr(ctx, *csr[:3], csr[3], p)
+                    tb.record()
+                    r = oem_fit_path(ctx, G, c, [nn], cfg.penalties, nlambda=cfg.nlambda, group=grp, ngroups=ngroups)
                 else:
                     if cfg.folds:
                         G, c, yy, cnt = oem_gram_folds_host(ctx, Xh[:, :p], yh, cfg.folds, row_offset=r0, block_rows=blk)
@@ -437,17 +490,20 @@ def main():
                 e2e_val = flops_step / (e2e_step_ms * 1e-3) / 1e12
                 note = ("logistic: H2D of X, y (pinned) once per step + the whole proximal-Newton fit; value = "
                         "weighted-Gram flops over the whole step")
+            elif sparse:
+                e2e_val = flops_step / (e2e_gram_ms * 1e-3) / 1e12
+                note = ("sparse: H2D of the pinned CSR arrays and y + the CSR Gram pass (the Gram phase); "
+                        "fit_seconds adds the path solve and the D2H of the paths")
             else:
                 e2e_val = flops_step / (e2e_gram_ms * 1e-3) / 1e12
                 note = ("Gram phase streamed from pinned host memory in 2^20-row blocks (oem_gram_host, copies "
                         "overlapped with the kernel); fit_seconds adds the path solve and the D2H of the paths")
             e2e = {"value": e2e_val, "unit": "TFLOP/s",
-                   "h2d_bytes_per_step": int(nl * ldx * 8 + nl * 8) * world,
+                   "h2d_bytes_per_step": int(in_bytes) * world,
                    "d2h_bytes_per_step": int(out_bytes) * world,
                    "fit_seconds": e2e_step_ms / 1e3, "gram_phase_ms": e2e_gram_ms,
-                   "h2d_gbs": (nl * ldx * 8 + nl * 8) / (e2e_gram_ms * 1e-3) / 1e9 if not cfg.logistic else None,
+                   "h2d_gbs": in_bytes / (e2e_gram_ms * 1e-3) / 1e9 if not cfg.logistic else None,
                    "note": note}
-            del Xh, yh
         except Exception as ex:  # pinned memory exhausted etc.: report, do not fake
             e2e = {"value": None, "unit": "TFLOP/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0,
                    "error": repr(ex)[:200]}
@@ -457,7 +513,7 @@ def main():
     # oracle on a column sample over ALL n rows
     validation = None
     if (world > 1 or args.validate) and not cfg.logistic:
-        validation = validate_combine(cfg, ctx, Xd, yd, r0, res, rank, world, dist, torch)
+        validation = validate_combine(cfg, ctx, Xd, yd, r0, res, rank, world, dist, torch, csr)
         if not validation["ok"]:
             if rank == 0:
                 print(json.dumps({"error": "multi-GPU validation failed", "validation": validation}), flush=True)
@@ -468,7 +524,7 @@ def main():
 
     pin = None
     if not args.no_cpu_baseline and not cfg.logistic and not cfg.folds:
-        Gf, cf, _, nf = oem_gram(ctx, Xd, yd)   # every rank: the combine is a collective
+        Gf, cf, _, nf = oem_gram_csr(ctx, *csr, p) if sparse else oem_gram(ctx, Xd, yd)   # every rank: a collective
         iters = int(res.iters.sum())
         est = iters * float(p) * p / 2e9  # ~2 GFLOP/s single-thread naive loops
         pin = (Gf.cpu().numpy(), cf.cpu().numpy(), nf, float(res.d[0]),

@@ -17,7 +17,7 @@ _ROOT = os.path.dirname(_HERE)
 HOST_SO = os.path.join(_HERE, "libdatagen_host.so")
 CUDA_SO = os.path.join(_HERE, "libdatagen_cuda.so")
 
-DG_IID, DG_AR1, DG_BLOCK = 0, 1, 2
+DG_IID, DG_AR1, DG_BLOCK, DG_SPARSE = 0, 1, 2, 3
 DG_LINEAR, DG_LOGISTIC = 0, 1
 DG_BETA_EXPLICIT, DG_BETA_UNIFORM, DG_BETA_NORMAL, DG_BETA_ACTIVE_GROUPS = 0, 1, 2, 3
 
@@ -86,6 +86,11 @@ def cuda():
         _cuda.dg_rows_cuda.restype = ctypes.c_int
         _cuda.dg_rows_cuda.argtypes = [ctypes.POINTER(Spec), P, ctypes.c_int64, ctypes.c_int64, P,
                                        ctypes.c_int64, P, P]
+        _cuda.dg_csr_count_cuda.restype = ctypes.c_int
+        _cuda.dg_csr_count_cuda.argtypes = [ctypes.POINTER(Spec), ctypes.c_int64, ctypes.c_int64, P, P]
+        _cuda.dg_csr_fill_cuda.restype = ctypes.c_int
+        _cuda.dg_csr_fill_cuda.argtypes = [ctypes.POINTER(Spec), P, ctypes.c_int64, ctypes.c_int64, P, P, P,
+                                           P, P]
     return _cuda
 
 
@@ -130,3 +135,28 @@ def rows_cuda(spec: Spec, beta_dev_ptr: int, row0: int, nrows: int, X_ptr: int, 
                              stream_ptr)
     if rc != 0:
         raise RuntimeError(f"dg_rows_cuda failed rc={rc}")
+
+
+def csr_cuda(spec: Spec, beta_true, row0: int = 0, nrows: int | None = None, want_y: bool = True):
+    """SPARSE design rows [row0, row0+nrows) generated on the current CUDA device in CSR form:
+    (row_ptr int64 [nrows+1], col int32 [nnz], val float64 [nnz], y float64 [nrows] or None), torch
+    tensors. The row offsets are the exclusive prefix sum of the per-row counts (torch.cumsum:
+    input residency, not the method)."""
+    import torch
+    nrows = spec.n - row0 if nrows is None else nrows
+    st = torch.cuda.current_stream().cuda_stream
+    counts = torch.empty(max(nrows, 1), dtype=torch.int64, device="cuda")
+    if cuda().dg_csr_count_cuda(ctypes.byref(spec), row0, nrows, counts.data_ptr(), st) != 0:
+        raise RuntimeError("dg_csr_count_cuda failed")
+    row_ptr = torch.zeros(nrows + 1, dtype=torch.int64, device="cuda")
+    if nrows:
+        torch.cumsum(counts[:nrows], 0, out=row_ptr[1:])
+    nnz = int(row_ptr[-1])
+    col = torch.empty(max(nnz, 1), dtype=torch.int32, device="cuda")
+    val = torch.empty(max(nnz, 1), dtype=torch.float64, device="cuda")
+    y = torch.empty(max(nrows, 1), dtype=torch.float64, device="cuda") if want_y else None
+    b = torch.from_numpy(np.ascontiguousarray(beta_true, dtype=np.float64)).cuda()
+    if cuda().dg_csr_fill_cuda(ctypes.byref(spec), b.data_ptr(), row0, nrows, row_ptr.data_ptr(), col.data_ptr(),
+                               val.data_ptr(), None if y is None else y.data_ptr(), st) != 0:
+        raise RuntimeError("dg_csr_fill_cuda failed")
+    return row_ptr, col[:nnz], val[:nnz], (y[:nrows] if y is not None else None)

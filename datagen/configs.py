@@ -9,7 +9,7 @@ from __future__ import annotations
 from dataclasses import dataclass, field
 
 from . import (DG_AR1, DG_BETA_ACTIVE_GROUPS, DG_BETA_EXPLICIT, DG_BETA_NORMAL, DG_BETA_UNIFORM,
-               DG_BLOCK, DG_IID, DG_LINEAR, DG_LOGISTIC, Spec, make_spec)
+               DG_BLOCK, DG_IID, DG_LINEAR, DG_LOGISTIC, DG_SPARSE, Spec, make_spec)
 
 
 @dataclass
@@ -73,7 +73,18 @@ CFG5 = Config(
     notes="Logistic n=5e6, p=200, AR(1) rho=.5, 20 nonzero U(-1,1), exact-Hessian proximal Newton, "
           "lasso 50 lambda")
 
-CONFIGS = {c.name: c for c in (CFG1, CFG2, CFG3, CFG4, CFG5)}
+# f4: the paper's sparse-design example (rsparsematrix(n, 200,
+# density = 0.01), 15 nonzero coefficients U(-0.25, 0.25), noise sd 3, lasso and group lasso with
+# 40 groups of 5) at the tall size of the survey's f4 row (n = 1e7; the paper used n = 1e5).
+# Not one of BASELINE.json's configs: a widening of the hot path, benched as its own workload.
+SPARSE = Config(
+    "sparse", make_spec(6, 10_000_000, 200, DG_SPARSE, rho=0.01, sigma=3.0, beta_kind=DG_BETA_UNIFORM,
+                        nnz=15, beta_lo=-0.25, beta_hi=0.25),
+    [("lasso", 0.0, 1.0), ("grp_lasso", 0.0, 1.0)], 100, group_size=5,
+    notes="sparse CSR design n=1e7, p=200, density 0.01 (paper §5.8 example shape), 15 nonzero "
+          "U(-.25,.25), sd 3; lasso + group lasso (40 groups of 5), 100 lambda")
+
+CONFIGS = {c.name: c for c in (CFG1, CFG2, CFG3, CFG4, CFG5, SPARSE)}
 
 
 def groups_of(cfg: Config):

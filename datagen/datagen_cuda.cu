@@ -129,6 +129,14 @@ __device__ void normal_pair(const uint32_t w[4], double* z0, double* z1) {
   *z1 = MUL(r, s);
 }
 
+// SPARSE: the pattern draw u_ij of stream 5 (words 0,1 for even j, 2,3 for odd j) is < d
+__device__ __forceinline__ bool kept(const dg_spec& sp, uint64_t gi, int j) {
+  uint32_t w[4];
+  philox(sp.seed, (uint32_t)gi, (uint32_t)(gi >> 32), (uint32_t)(j >> 1), 5u, w);
+  const double u = (j & 1) ? uniform01(w[2], w[3]) : uniform01(w[0], w[1]);
+  return u < sp.rho;
+}
+
 constexpr int ROWS = 128, CH = 32;
 
 __global__ void __launch_bounds__(ROWS) rows_kernel(dg_spec sp, const double* __restrict__ beta, int64_t row0,
@@ -168,6 +176,8 @@ __global__ void __launch_bounds__(ROWS) rows_kernel(dg_spec sp, const double* __
             gpair = k >> 1;
           }
           x = ADD(MUL(sq_r, (k & 1) ? g1 : g0), MUL(sq_1r, z));
+        } else if (sp.design == DG_SPARSE) {
+          x = kept(sp, gi, j) ? z : 0.0;
         } else {
           x = z;
         }
@@ -199,12 +209,79 @@ __global__ void __launch_bounds__(ROWS) rows_kernel(dg_spec sp, const double* __
   }
 }
 
+// SPARSE in CSR form: one thread per row (the pattern of a row is a pure function of (i, j))
+__global__ void csr_count_kernel(dg_spec sp, int64_t row0, int64_t nrows, int64_t* __restrict__ counts) {
+  const int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (r >= nrows) return;
+  const uint64_t gi = (uint64_t)(row0 + r);
+  int64_t c = 0;
+  for (int j = 0; j < sp.p; ++j) c += kept(sp, gi, j) ? 1 : 0;
+  counts[r] = c;
+}
+
+__global__ void csr_fill_kernel(dg_spec sp, const double* __restrict__ beta, int64_t row0, int64_t nrows,
+                                const int64_t* __restrict__ row_ptr, int32_t* __restrict__ col,
+                                double* __restrict__ val, double* __restrict__ y) {
+  const int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (r >= nrows) return;
+  const uint64_t gi = (uint64_t)(row0 + r);
+  int64_t e = row_ptr[r];
+  double eta = 0.0, z0 = 0.0, z1 = 0.0;
+  int drawn = -1;   // column pair whose normals z0, z1 hold
+  for (int j = 0; j < sp.p; ++j) {
+    if (!kept(sp, gi, j)) continue;
+    if ((j >> 1) != drawn) {
+      uint32_t w[4];
+      philox(sp.seed, (uint32_t)gi, (uint32_t)(gi >> 32), (uint32_t)(j >> 1), 0u, w);
+      normal_pair(w, &z0, &z1);
+      drawn = j >> 1;
+    }
+    const double x = (j & 1) ? z1 : z0;
+    col[e] = j;
+    val[e] = x;
+    ++e;
+    const double b = beta ? beta[j] : 0.0;
+    if (b != 0.0) eta = ADD(eta, MUL(x, b));
+  }
+  if (y) {
+    uint32_t w[4];
+    if (sp.response == DG_LINEAR) {
+      philox(sp.seed, (uint32_t)gi, (uint32_t)(gi >> 32), 0u, 2u, w);
+      double e0, e1;
+      normal_pair(w, &e0, &e1);
+      y[r] = ADD(eta, MUL(sp.sigma, e0));
+    } else {
+      philox(sp.seed, (uint32_t)gi, (uint32_t)(gi >> 32), 0u, 4u, w);
+      const double u = uniform01(w[0], w[1]);
+      const double pr = DIV(1.0, ADD(1.0, exp_sw(-eta)));
+      y[r] = (u < pr) ? 1.0 : 0.0;
+    }
+  }
+}
+
 }  // namespace
+
+extern "C" int dg_csr_count_cuda(const dg_spec* spec, int64_t row0, int64_t nrows, int64_t* counts, void* stream) {
+  if (!spec || spec->design != DG_SPARSE || !counts || nrows < 0 || row0 < 0 || spec->p < 1) return -1;
+  if (nrows == 0) return 0;
+  csr_count_kernel<<<(unsigned)((nrows + 255) / 256), 256, 0, (cudaStream_t)stream>>>(*spec, row0, nrows, counts);
+  return cudaGetLastError() == cudaSuccess ? 0 : -2;
+}
+
+extern "C" int dg_csr_fill_cuda(const dg_spec* spec, const double* beta, int64_t row0, int64_t nrows,
+                                const int64_t* row_ptr, int32_t* col, double* val, double* y, void* stream) {
+  if (!spec || spec->design != DG_SPARSE || !row_ptr || !col || !val || nrows < 0 || row0 < 0 || spec->p < 1) return -1;
+  if (y && !beta) return -1;
+  if (nrows == 0) return 0;
+  csr_fill_kernel<<<(unsigned)((nrows + 255) / 256), 256, 0, (cudaStream_t)stream>>>(*spec, beta, row0, nrows, row_ptr,
+                                                                                      col, val, y);
+  return cudaGetLastError() == cudaSuccess ? 0 : -2;
+}
 
 extern "C" int dg_rows_cuda(const dg_spec* spec, const double* beta, int64_t row0, int64_t nrows, double* X,
                             int64_t ldx, double* y, void* stream) {
   if (!spec || !beta || !X || nrows < 0 || row0 < 0 || ldx < spec->p || spec->p < 1) return -1;
-  if (spec->design < 0 || spec->design > 2 || spec->response < 0 || spec->response > 1) return -1;
+  if (spec->design < 0 || spec->design > 3 || spec->response < 0 || spec->response > 1) return -1;
   if (spec->design == DG_BLOCK && spec->group_size < 1) return -1;
   if (nrows == 0) return 0;
   const int64_t blocks = (nrows + ROWS - 1) / ROWS;

@@ -145,7 +145,8 @@ static void normal_pair(const uint32_t w[4], double* z0, double* z1) {
 /* ---------------- beta ---------------- */
 static int spec_ok(const dg_spec* sp) {
   if (!sp || sp->n < 0 || sp->p < 1) return 0;
-  if (sp->design < 0 || sp->design > 2) return 0;
+  if (sp->design < 0 || sp->design > 3) return 0;
+  if (sp->design == DG_SPARSE && !(sp->rho >= 0.0 && sp->rho <= 1.0)) return 0;
   if (sp->design == DG_BLOCK && (sp->group_size < 1 || sp->rho < 0.0 || sp->rho > 1.0)) return 0;
   if (sp->design == DG_AR1 && !(sp->rho > -1.0 && sp->rho < 1.0)) return 0;
   if (sp->response < 0 || sp->response > 1) return 0;
@@ -228,6 +229,14 @@ static double z_of(const dg_spec* sp, uint64_t gi, int32_t j, rowcache* rc) {
   return (j & 1) ? rc->z1 : rc->z0;
 }
 
+/* SPARSE: the pattern draw u_ij of stream 5 (words 0,1 for even j, 2,3 for odd j) */
+static int kept(const dg_spec* sp, uint64_t gi, int32_t j) {
+  uint32_t w[4];
+  philox(sp->seed, (uint32_t)gi, (uint32_t)(gi >> 32), (uint32_t)(j >> 1), 5u, w);
+  double u = (j & 1) ? uniform01(w[2], w[3]) : uniform01(w[0], w[1]);
+  return u < sp->rho;
+}
+
 static double g_of(const dg_spec* sp, uint64_t gi, int32_t k, rowcache* rc) {
   int64_t m = k >> 1;
   if (rc->cached_gpair != m) {
@@ -269,6 +278,7 @@ int dg_rows_host(const dg_spec* sp, const double* beta, int64_t row0, int64_t nr
         if (!need[j]) continue;
         double z = z_of(sp, gi, j, &rc);
         if (sp->design == DG_IID) row[j] = z;
+        else if (sp->design == DG_SPARSE) row[j] = kept(sp, gi, j) ? z : 0.0;
         else row[j] = sq_r * g_of(sp, gi, j / sp->group_size, &rc) + sq_1r * z;
       }
     }

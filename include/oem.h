@@ -210,6 +210,22 @@ oem_status oem_gram_folds_host(oem_ctx* ctx, const double* X /*host*/, const dou
                                double* G_folds, double* xty_folds, double* yty_folds, int64_t* counts /*host K*/,
                                void* stream);
 
+/* ---- f4 sparse design (§5.8: oem() accepts sparse design matrices; "a substantial
+ * computational speedup and reduction in memory usage"). The a2 statistics of one pass over a
+ * design in compressed sparse row form: row_ptr (device int64, n_local + 1 offsets into col/val;
+ * row i holds entries [row_ptr[i], row_ptr[i+1])), col (device int32, column indices strictly
+ * ascending within each row, each in [0, p)), val (device fp64), y (device, n_local). Outputs,
+ * communicator and n_total exactly as oem_gram: G = X^T X (full symmetric p*p), xty, yty,
+ * raw sums over this rank's rows (the ranks' CSR blocks are their row shards), so the result
+ * feeds oem_fit_path unchanged. Work and traffic scale with the nonzeros (each row contributes
+ * the products of its nonzeros only). Deterministic (fixed partition and summation order).
+ * The CSR precondition (ascending, in-range columns) is not checked on the device.
+ * Errors: OEM_ERR_DIM, OEM_ERR_INVALID_ARG, OEM_ERR_UNSUPPORTED (p > 768), OEM_ERR_CUDA,
+ * OEM_ERR_NCCL. */
+oem_status oem_gram_csr(oem_ctx* ctx, const int64_t* row_ptr, const int32_t* col, const double* val,
+                        const double* y, int64_t n_local, int32_t p, double* G, double* xty, double* yty,
+                        int64_t* n_total /*host, may be NULL*/, void* stream);
+
 /* ---- f3 column sums for the intercept / standardization (R#2-3): xsum[k*p + j] = sum of
  * x_ij over this rank's rows i of fold k (fold(i) = (row_offset + i) mod K, R#19; K = 1 for the
  * whole data), ysum[k] = sum of y_i; raw sums, allreduced when the context has a communicator. One HBM-bound pass.

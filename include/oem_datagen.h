@@ -20,6 +20,7 @@
  *      stream 2  noise eps_i         : (i_lo, i_hi, 0, 2)
  *      stream 3  beta draws          : (t, s, 0, 3)            t = draw index, s = 0 index / 1 value
  *      stream 4  Bernoulli u_i       : (i_lo, i_hi, 0, 4)
+ *      stream 5  sparsity pattern    : (i_lo, i_hi, j>>1, 5)   columns 2m, 2m+1 share one call
  *  - uniform(w_a, w_b): k = ((w_a << 32) | w_b) >> 12 (52 bits); u = (2k + 1) * 2^-53, exact, in (0,1).
  *  - normal pair from one call (w0..w3): u1 = uniform(w0,w1), u2 = uniform(w2,w3);
  *      r = sqrt(-2 * LN(u1)); (z_even, z_odd) = (r * COS2PI(u2), r * SIN2PI(u2)).
@@ -28,7 +29,10 @@
  *    bit for bit.
  *  - designs: IID x_ij = z_ij;  AR1 x_i0 = z_i0, x_ij = rho*x_i,j-1 + sqrt(1-rho^2)*z_ij;
  *    BLOCK x_ij = sqrt(r)*g_i,k(j) + sqrt(1-r)*z_ij with k(j) = j / group_size (group factors
- *    are the stream-1 normals).  All products/sums evaluated left to right as written.
+ *    are the stream-1 normals).  SPARSE (the paper's rsparsematrix example):
+ *    x_ij = z_ij if u_ij < d else 0, with d = rho (the density) and u_ij = uniform(w0,w1) (even j)
+ *    or uniform(w2,w3) (odd j) of the stream-5 call of the pair; every cell independently (the
+ *    expected density is d).  All products/sums evaluated left to right as written.
  *  - beta: partial Fisher-Yates over [0,m) (m = p, or the number of groups for ACTIVE_GROUPS):
  *    for t < nnz: w0 of counter (t,0,0,3); j = t + ((w0 * (m - t)) >> 32); swap(perm[t], perm[j]).
  *    values: counter (t,1,0,3), uniform(w0,w1) -> lo + (hi-lo)*u (UNIFORM) or the even normal
@@ -45,7 +49,7 @@
 extern "C" {
 #endif
 
-typedef enum { DG_IID = 0, DG_AR1 = 1, DG_BLOCK = 2 } dg_design;
+typedef enum { DG_IID = 0, DG_AR1 = 1, DG_BLOCK = 2, DG_SPARSE = 3 } dg_design;
 typedef enum { DG_LINEAR = 0, DG_LOGISTIC = 1 } dg_response;
 typedef enum { DG_BETA_EXPLICIT = 0, DG_BETA_UNIFORM = 1, DG_BETA_NORMAL = 2, DG_BETA_ACTIVE_GROUPS = 3 } dg_beta_kind;
 
@@ -54,7 +58,7 @@ typedef struct {
   int64_t n;          /* global number of rows */
   int32_t p;          /* number of columns */
   int32_t design;     /* dg_design */
-  double rho;         /* AR(1) rho, or within-group correlation r for DG_BLOCK */
+  double rho;         /* AR(1) rho, within-group correlation r for DG_BLOCK, density d for DG_SPARSE */
   int32_t group_size; /* DG_BLOCK and DG_BETA_ACTIVE_GROUPS: contiguous groups of this size */
   int32_t response;   /* dg_response */
   double sigma;       /* noise sd (linear) */
@@ -86,6 +90,16 @@ int dg_rows_host(const dg_spec* spec, const double* beta, int64_t row0, int64_t 
  * `stream` (a cudaStream_t passed as void*). Returns 0, -1 invalid args, -2 CUDA launch error. */
 int dg_rows_cuda(const dg_spec* spec, const double* beta, int64_t row0, int64_t nrows,
                  double* X, int64_t ldx, double* y, void* stream);
+
+/* Device compressed-sparse-row form of the SPARSE design (rows [row0, row0+nrows), libdatagen_cuda.so):
+ * dg_csr_count_cuda writes the nonzero count of every row (int64, nrows); after the caller's
+ * exclusive prefix sum into row_ptr (nrows+1, row_ptr[0] = 0), dg_csr_fill_cuda writes the column
+ * indices (int32, ascending within each row) and values of every nonzero, and y (nrows) if
+ * non-NULL (eta over the nonzero support columns in ascending j, as above). Values equal the
+ * dense generator's bit for bit. Asynchronous on `stream`. Returns 0, -1 (invalid), -2 (CUDA). */
+int dg_csr_count_cuda(const dg_spec* spec, int64_t row0, int64_t nrows, int64_t* counts, void* stream);
+int dg_csr_fill_cuda(const dg_spec* spec, const double* beta, int64_t row0, int64_t nrows,
+                     const int64_t* row_ptr, int32_t* col, double* val, double* y, void* stream);
 
 #ifdef __cplusplus
 }

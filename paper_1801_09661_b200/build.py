@@ -14,7 +14,7 @@ NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 NVFLAGS = ARCH + ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "--expt-relaxed-constexpr"]
 
-OEM_SRCS = ["api.cu", "gram.cu", "drule.cu", "path.cu", "logistic.cu", "cv.cu", "logit_ub.cu", "moments.cu", "stream.cu"]
+OEM_SRCS = ["api.cu", "gram.cu", "drule.cu", "path.cu", "logistic.cu", "cv.cu", "logit_ub.cu", "moments.cu", "stream.cu", "sparse.cu"]
 OEM_HDRS = ["common.cuh", "internal.h"]
 LIBOEM = os.path.join(PKG, "liboem.so")
 DG_CUDA = os.path.join(ROOT, "datagen", "libdatagen_cuda.so")

@@ -144,6 +144,7 @@ oem_status oem_ctx_destroy(oem_ctx* ctx) {
   ctx->logi.release();
   ctx->drule_ws.release();
   ctx->wz.release();
+  ctx->sparse_ws.release();
   ctx->lg_part.release();
   ctx->lg_out.release();
   ctx->mom_part.release();

@@ -27,7 +27,8 @@ STATUS = ["OEM_OK", "OEM_ERR_INVALID_ARG", "OEM_ERR_DIM", "OEM_ERR_ALIGN", "OEM_
 ABI_SYMBOLS = ["oem_status_string", "oem_last_error", "oem_version", "oem_nccl_unique_id",
                "oem_ctx_create", "oem_ctx_destroy", "oem_gram", "oem_gram_folds",
                "oem_gram_weighted", "oem_fit_path", "oem_path_cfg_default", "oem_fit_logistic",
-               "oem_logistic_cfg_default", "oem_cv_error", "oem_logit_grad", "oem_gram_moments", "oem_path_loss", "oem_gram_host", "oem_gram_folds_host", "oem_ctx_set_timing", "oem_ctx_stats"]
+               "oem_logistic_cfg_default", "oem_cv_error", "oem_logit_grad", "oem_gram_moments", "oem_path_loss", "oem_gram_host", "oem_gram_folds_host", "oem_ctx_set_timing", "oem_ctx_stats",
+               "oem_gram_csr"]
 _VOID = ("oem_status_string", "oem_last_error", "oem_version", "oem_path_cfg_default",
          "oem_logistic_cfg_default")
 
@@ -107,6 +108,7 @@ def lib():
         L.oem_gram_host.argtypes = [P, P, P, i64, i32, i64, i64, P, P, P, ctypes.POINTER(i64), P]
         L.oem_gram_folds_host.argtypes = [P, P, P, i64, i32, i64, i64, i32, i64, P, P, P, P, P]
         L.oem_path_loss.argtypes = [P, P, P, P, P, i32, i32, i32, i32, P, P, P]
+        L.oem_gram_csr.argtypes = [P, P, P, P, P, i64, i32, P, P, P, ctypes.POINTER(i64), P]
         L.oem_ctx_set_timing.argtypes = [P, ctypes.c_int]
         L.oem_ctx_stats.argtypes = [P, ctypes.POINTER(Stats), ctypes.c_int]
         for name in ABI_SYMBOLS:
@@ -350,6 +352,25 @@ def oem_gram_folds_host(ctx: Context, X, y, K: int, row_offset: int = 0, block_r
                                      int(block_rows), _ptr(G), _ptr(xty), _ptr(yty), counts, _stream(stream)))
     _hold_until_done(ctx, stream, X, y)
     return G, xty, yty, list(counts)
+
+
+def oem_gram_csr(ctx: Context, row_ptr, col, val, y, p: int, stream=None):
+    """f4 sparse design: the a2 statistics (G, X^T y, y^T y, n_total) of one pass over X in CSR
+    form (row_ptr int64 [n+1], col int32 [nnz] ascending within rows, val float64 [nnz]) and y."""
+    n = row_ptr.numel() - 1
+    for t, dt in ((row_ptr, torch.int64), (col, torch.int32), (val, torch.float64), (y, torch.float64)):
+        if t.dtype != dt or not t.is_cuda or not t.is_contiguous():
+            raise ValueError("oem_gram_csr: row_ptr int64, col int32, val / y float64, contiguous CUDA tensors")
+    if y.numel() != n or col.numel() != val.numel():
+        raise ValueError("oem_gram_csr: y must have n entries and col / val the same length")
+    G = torch.empty((p, p), dtype=torch.float64, device=y.device)
+    xty = torch.empty(p, dtype=torch.float64, device=y.device)
+    yty = torch.empty(1, dtype=torch.float64, device=y.device)
+    nt = ctypes.c_int64(0)
+    _check(lib().oem_gram_csr(ctx.h, _ptr(row_ptr), _ptr(col) if col.numel() else None,
+                              _ptr(val) if val.numel() else None, _ptr(y), n, p, _ptr(G), _ptr(xty), _ptr(yty),
+                              ctypes.byref(nt), _stream(stream)))
+    return G, xty, yty, nt.value
 
 
 def oem_gram_moments(ctx: Context, X, y, K: int = 1, row_offset: int = 0, stream=None):

@@ -110,3 +110,27 @@ def test_logistic_response_model():
     # calibration: mean label matches mean probability
     assert abs(y.mean() - pr.mean()) < 0.015
     assert abs(((y - pr) * (X @ b)).mean()) < 0.05
+
+
+def test_sparse_design_pattern():
+    """SPARSE (include/oem_datagen.h): every cell is the IID design's z_ij kept with probability d
+    (stream-5 uniform < d), so the kept values equal the IID generator's bit for bit and the
+    density and the pattern's independence follow the binomial law."""
+    d = 0.05
+    spec = dg.make_spec(21, 20000, 40, dg.DG_SPARSE, rho=d, beta_kind=dg.DG_BETA_EXPLICIT)
+    iid = dg.make_spec(21, 20000, 40, dg.DG_IID, beta_kind=dg.DG_BETA_EXPLICIT)
+    X, _ = dg.rows_host(spec, np.zeros(40), want_y=False)
+    Z, _ = dg.rows_host(iid, np.zeros(40), want_y=False)
+    nz = X != 0
+    assert np.array_equal(X[nz], Z[nz])
+    m = nz.size
+    assert abs(nz.mean() - d) < 5 * np.sqrt(d * (1 - d) / m)
+    # the pattern is independent of the values: the kept values are N(0, 1)
+    assert abs(X[nz].mean()) < 0.05 and abs(X[nz].var() - 1) < 0.06
+    # column subsets and the response agree with the full rows
+    bt = np.zeros(40)
+    bt[[3, 17]] = [0.5, -1.25]
+    spec2 = spec.replace(sigma=2.0)
+    Xf, yf = dg.rows_host(spec2, bt, 100, 50)
+    Xs, ys = dg.rows_host(spec2, bt, 100, 50, 10, 7)
+    assert np.array_equal(Xs, Xf[:, 10:17]) and np.array_equal(ys, yf)
