@@ -7,17 +7,21 @@
 // nonzeros exist: row i contributes m_i (m_i + 1) / 2 + m_i + 1 terms (m_i = its nonzeros), so
 // the pass is bound by reading the CSR arrays, not by the p^2 arithmetic of the dense kernel.
 //
-// B200 design (deterministic, no atomics):
+// B200 design (deterministic: every accumulator has one owner thread and a data-fixed order):
 //  * One CTA per SM holds a SLICE of the packed upper triangle of Z^T Z in shared memory (rows
-//    [J_u, J_{u+1}) of the triangle, up to ~22k entries = 175 KB; p = 200 fits one slice) and
-//    streams a contiguous row segment of the CSR arrays: one producer warp stages chunks of up to
-//    256 rows / 768 nonzeros (row_ptr, y, col, val) into a 4-deep shared-memory ring with
-//    cp.async (completion through mbarrier arrive.noinc), eight consumer warps read them.
-//  * Every consumer warp OWNS a contiguous range of triangle rows j and scans every staged row
-//    (lane = row), emitting only its own pairs (j, k >= j), (j, p) and (p, p): no two warps ever
-//    touch the same entry. Inside a warp, lanes emit one pair per round; lanes that hit the same
-//    entry in a round are grouped with __match_any_sync and summed in lane order by the group
-//    leader -> every entry accumulates in an order fixed by the data, bitwise reproducible.
+//    [J_u, J_{u+1}) of the triangle; p = 200 fits one slice, 162 KB) and streams a contiguous row
+//    segment of the CSR arrays: one producer warp stages chunks of up to 256 rows / 768 nonzeros
+//    (row_ptr, y, col, val) into a 3-deep shared-memory ring with cp.async (completion through
+//    mbarrier arrive.noinc); a mask warp and 256 owner threads process them.
+//  * Consumer thread t OWNS triangle rows (columns) J_u + t, J_u + t + 256, ...: it alone updates
+//    G[j][k >= j] and G[j][p] for its columns. Per chunk the mask warp first marks, for every owned
+//    column j, which of the chunk's rows hold a nonzero in column j (a 256-bit row mask per column
+//    in the stage, set with shared-memory atomicOr: a bitwise OR is order-free); each owner walks its masks
+//    in ascending row order and, for every row with x_ij != 0, adds x_ij x_ik for the row's
+//    nonzeros k >= j and x_ij y_i. Work per chunk is proportional to the chunk's nonzeros and
+//    their row neighbours, with no conflicts and no redundant scanning; owner warps are coupled
+//    only through the ring (imbalance between chunks averages out). y^T y is a fixed-order warp
+//    sum per chunk (mask warp), added by the owner of the augmented column p.
 //  * Segments write their slice to a partial buffer; a second kernel adds the segments in a
 //    fixed order into the packed triangle (the NCCL allreduce and the unpack are shared with the
 //    dense path).
@@ -32,21 +36,26 @@ namespace oem {
 
 namespace {
 
-constexpr int SP_WARPS = 8;                     // consumer warps
-constexpr int SP_THREADS = (SP_WARPS + 1) * 32; // + one producer warp
-constexpr int SP_ST = 4;                        // ring depth
+constexpr int SP_WARPS = 8;                     // owner (consumer) warps: 256 threads, one per owned column
+constexpr int SP_CT = SP_WARPS * 32;
+constexpr int SP_PROD = SP_WARPS;               // warp index of the producer
+constexpr int SP_MASKW = SP_WARPS + 1;          // warp index of the mask builder
+constexpr int SP_THREADS = (SP_WARPS + 2) * 32;
+constexpr int SP_ST = 3;                        // ring depth
 constexpr int SP_ROWS = 256;                    // rows per stage (max)
+constexpr int SP_MW = SP_ROWS / 32;             // mask words per column
 constexpr int SP_ENT = 768;                     // nonzeros per stage (max): p <= SP_ENT
-constexpr int SP_STAGE_BYTES = ((SP_ROWS + 1) * 8 + SP_ROWS * 8 + SP_ENT * 4 + SP_ENT * 8 + 32 + 127) / 128 * 128;
 constexpr size_t SP_SMEM_MAX = 227 * 1024;
 
-struct SpStage {  // shared-memory layout of one ring stage (byte offsets)
+struct SpStage {  // shared-memory layout of one ring stage (byte offsets); masks follow at `mask`
   static constexpr int rp = 0;
   static constexpr int y = rp + (SP_ROWS + 1) * 8;
   static constexpr int val = y + SP_ROWS * 8;
   static constexpr int col = val + SP_ENT * 8;
-  static constexpr int hdr = col + SP_ENT * 4;  // {int R; int base_shift} then int64 e0
+  static constexpr int hdr = col + SP_ENT * 4;   // int R, pad, int64 e0, double yy (the chunk's y^T y)
+  static constexpr int mask = (hdr + 32 + 127) / 128 * 128;
 };
+__host__ __device__ constexpr int stage_bytes(int ncol) { return SpStage::mask + (ncol * SP_MW * 4 + 127) / 128 * 128; }
 
 struct SpParams {
   const int64_t* row_ptr;
@@ -57,8 +66,8 @@ struct SpParams {
   int p, U, nseg;
   int64_t seg_rows;
   const int* slice_j0;   // [U+1] first triangle row of each slice
-  const int* warp_j0;    // [U][SP_WARPS+1] first triangle row of each consumer warp
   int cap;               // entries per slice buffer (max over slices)
+  int sbytes;            // bytes per ring stage (mask columns of the widest slice)
   double* partial;       // [U][nseg][cap]
 };
 
@@ -74,36 +83,45 @@ __device__ __forceinline__ void cp_async_arrive_noinc(uint64_t* bar) {
   asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];" ::"r"(smem_u32(bar)) : "memory");
 }
 
+// Ring protocol per stage s: producer fills rows / nonzeros -> full[s] (32 cp.async arrivals +
+// the header arrive); the mask warp marks the owned columns' rows and the chunk's y^T y ->
+// ready[s]; every owner warp walks its columns, clears their mask words -> empty[s]. Owner warps
+// are coupled only through the ring, so a warp slowed by a dense column in one chunk catches up
+// on the next (up to SP_ST chunks of slack).
 __global__ void __launch_bounds__(SP_THREADS, 1) sparse_gram_kernel(const SpParams P) {
   extern __shared__ __align__(128) unsigned char sbytes[];
-  __shared__ __align__(8) uint64_t full[SP_ST], empty[SP_ST];
+  __shared__ __align__(8) uint64_t full[SP_ST], ready[SP_ST], empty[SP_ST];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int u = blockIdx.x % P.U, seg = blockIdx.x / P.U;
   const int p = P.p;
   const int64_t pa = p + 1;
   const int64_t r0 = (int64_t)seg * P.seg_rows, r1 = min(P.n, r0 + P.seg_rows);
-  const int J0 = P.slice_j0[u];
-  const int64_t base = tri_off(J0, pa);
-  double* gs = reinterpret_cast<double*>(sbytes + (size_t)SP_ST * SP_STAGE_BYTES);
-  const int64_t nent = tri_off(P.slice_j0[u + 1], pa) - base;
+  const int J0 = P.slice_j0[u], J1 = P.slice_j0[u + 1], ncol = J1 - J0;
+  const int64_t base = tri_off(J0, pa), nent = tri_off(J1, pa) - base;
+  double* gs = reinterpret_cast<double*>(sbytes + (size_t)SP_ST * P.sbytes);
   for (int64_t e = threadIdx.x; e < nent; e += SP_THREADS) gs[e] = 0.0;
+  for (int s = 0; s < SP_ST; ++s) {
+    uint32_t* m = reinterpret_cast<uint32_t*>(sbytes + (size_t)s * P.sbytes + SpStage::mask);
+    for (int e = threadIdx.x; e < ncol * SP_MW; e += SP_THREADS) m[e] = 0u;
+  }
   if (threadIdx.x == 0) {
     for (int s = 0; s < SP_ST; ++s) {
-      mbar_init(&full[s], 33);        // 32 cp.async arrivals (noinc) + the header arrive
-      mbar_init(&empty[s], SP_WARPS);
+      mbar_init(&full[s], 33);          // 32 cp.async arrivals (noinc) + the header arrive
+      mbar_init(&ready[s], 32);         // every lane of the mask warp
+      mbar_init(&empty[s], SP_WARPS);   // lane 0 of every owner warp
     }
     fence_mbar_init();
   }
   __syncthreads();
 
-  if (warp == SP_WARPS) {
+  if (warp == SP_PROD) {
     // ---------------------------------------------------------------- producer warp
     int st = 0;
     uint32_t ph = 0;
     int64_t r = r0;
     for (;;) {
       mbar_wait(&empty[st], ph ^ 1u);
-      unsigned char* sb = sbytes + (size_t)st * SP_STAGE_BYTES;
+      unsigned char* sb = sbytes + (size_t)st * P.sbytes;
       int R = 0;
       int64_t e0 = 0, e1 = 0;
       if (lane == 0 && r < r1) {
@@ -151,14 +169,47 @@ __global__ void __launch_bounds__(SP_THREADS, 1) sparse_gram_kernel(const SpPara
     return;
   }
 
-  // ------------------------------------------------------------------ consumer warps
-  const int jw0 = P.warp_j0[u * (SP_WARPS + 1) + warp], jw1 = P.warp_j0[u * (SP_WARPS + 1) + warp + 1];
-  const bool own_pp = jw0 <= p && p < jw1;   // this warp owns the (p, p) entry: y^T y
+  if (warp == SP_MASKW) {
+    // ---------------------------------------------------------------- mask warp
+    int st = 0;
+    uint32_t ph = 0;
+    for (;;) {
+      mbar_wait(&full[st], ph);
+      unsigned char* sb = sbytes + (size_t)st * P.sbytes;
+      int* h = reinterpret_cast<int*>(sb + SpStage::hdr);
+      const int R = h[0];
+      const int64_t e0 = *reinterpret_cast<const int64_t*>(h + 2);
+      const int64_t* rp_s = reinterpret_cast<const int64_t*>(sb + SpStage::rp);
+      const double* y_s = reinterpret_cast<const double*>(sb + SpStage::y);
+      const int32_t* c_s = reinterpret_cast<const int32_t*>(sb + SpStage::col);
+      uint32_t* mask = reinterpret_cast<uint32_t*>(sb + SpStage::mask);
+      double yy = 0.0;
+      for (int q = lane; q < R; q += 32) {   // lane takes rows lane, lane + 32, ...
+        const int a0 = (int)(rp_s[q] - e0), a1 = (int)(rp_s[q + 1] - e0);
+        for (int a = a0; a < a1; ++a) {
+          const int c = c_s[a] - J0;
+          if (c >= 0 && c < ncol) atomicOr(&mask[c * SP_MW + (q >> 5)], 1u << (q & 31));
+        }
+        yy = fma(y_s[q], y_s[q], yy);
+      }
+#pragma unroll
+      for (int o = 16; o >= 1; o >>= 1) yy += __shfl_xor_sync(0xffffffffu, yy, o);   // fixed order
+      if (lane == 0) *reinterpret_cast<double*>(h + 4) = yy;
+      __syncwarp();
+      mbar_arrive(&ready[st]);
+      if (++st == SP_ST) { st = 0; ph ^= 1u; }
+      if (R == 0) break;
+    }
+    return;
+  }
+
+  // ------------------------------------------------------------------ owner warps
+  const int ct = threadIdx.x;   // 0 .. SP_CT-1: owns columns J0 + ct, J0 + ct + SP_CT, ...
   int st = 0;
   uint32_t ph = 0;
   for (;;) {
-    mbar_wait(&full[st], ph);
-    const unsigned char* sb = sbytes + (size_t)st * SP_STAGE_BYTES;
+    mbar_wait(&ready[st], ph);
+    unsigned char* sb = sbytes + (size_t)st * P.sbytes;
     const int* h = reinterpret_cast<const int*>(sb + SpStage::hdr);
     const int R = h[0];
     if (R == 0) break;
@@ -167,73 +218,51 @@ __global__ void __launch_bounds__(SP_THREADS, 1) sparse_gram_kernel(const SpPara
     const double* y_s = reinterpret_cast<const double*>(sb + SpStage::y);
     const double* v_s = reinterpret_cast<const double*>(sb + SpStage::val);
     const int32_t* c_s = reinterpret_cast<const int32_t*>(sb + SpStage::col);
-    if (jw0 < jw1) {
-      for (int q0 = 0; q0 < R; q0 += 32) {
-        const int q = q0 + lane;
-        // this lane's row: entries [a, end) of the stage, the first one with column >= jw0
-        int a = 0, end = 0, b = 0, phase = 2;  // phase 0: pairs (j_a, k_b) / (j_a, p); 1: (p, p); 2: done
-        double yq = 0.0;
-        if (q < R) {
-          a = (int)(rp_s[q] - e0);
-          end = (int)(rp_s[q + 1] - e0);
-          yq = y_s[q];
-          while (a < end && c_s[a] < jw0) ++a;
-          if (a < end && c_s[a] < jw1) { phase = 0; b = a; }
-          else phase = own_pp ? 1 : 2;
-        }
-        for (;;) {
-          const bool has = phase < 2;
-          const unsigned act = __ballot_sync(0xffffffffu, has);
-          if (!act) break;
-          if (has) {
-            int64_t key;
-            double prod;
-            if (phase == 0) {
-              const int j = c_s[a];
-              const double va = v_s[a];
-              const bool isy = b == end;
-              const int k = isy ? p : c_s[b];
-              prod = va * (isy ? yq : v_s[b]);
-              key = tri_off(j, pa) + (k - j);
-            } else {
-              prod = yq * yq;
-              key = tri_off(p, pa);
-            }
-            const unsigned grp = __match_any_sync(act, (unsigned long long)key);
-            const int leader = __ffs(grp) - 1;
-            double s = prod;
-            if (grp != (1u << lane)) {   // lanes of one group sum in lane order (fixed)
-              s = 0.0;
-              unsigned m = grp;
-              while (m) {
-                const int src = __ffs(m) - 1;
-                m &= m - 1;
-                s += __shfl_sync(grp, prod, src);
-              }
-            }
-            if (lane == leader) gs[key - base] += s;
-            // advance
-            if (phase == 0) {
-              if (++b > end) {
-                ++a;
-                if (a < end && c_s[a] < jw1) b = a;
-                else phase = own_pp ? 1 : 2;
-              }
-            } else {
-              phase = 2;
-            }
+    uint32_t* mask = reinterpret_cast<uint32_t*>(sb + SpStage::mask);
+    const int nw = (R + 31) / 32;
+    for (int c = ct; c < ncol; c += SP_CT) {
+      const int j = J0 + c;
+      double* grow = gs + (tri_off(j, pa) - base) - j;   // grow[k] = G[j][k]
+      if (j == p) {   // the augmented column: y^T y of the chunk
+        grow[p] += *reinterpret_cast<const double*>(h + 4);
+        continue;
+      }
+      for (int w = 0; w < nw; ++w) {
+        uint32_t bits = mask[c * SP_MW + w];
+        if (!bits) continue;
+        mask[c * SP_MW + w] = 0u;   // ready for the stage's next use
+        do {
+          const int q = 32 * w + __ffs(bits) - 1;
+          bits &= bits - 1;
+          int a = (int)(rp_s[q] - e0);
+          const int a1 = (int)(rp_s[q + 1] - e0);
+          while (c_s[a] != j) ++a;   // the row's nonzero in column j (columns ascend)
+          const double va = v_s[a];
+          // the row's columns are distinct, so these read-modify-writes never alias: the loads
+          // of a pair are issued before either store
+          int b = a;
+          for (; b + 1 < a1; b += 2) {
+            const int k0 = c_s[b], k1 = c_s[b + 1];
+            const double g0 = grow[k0], g1 = grow[k1];
+            const double x0 = v_s[b], x1 = v_s[b + 1];
+            grow[k0] = g0 + va * x0;
+            grow[k1] = g1 + va * x1;
           }
-        }
+          if (b < a1) grow[c_s[b]] += va * v_s[b];
+          grow[p] += va * y_s[q];
+        } while (bits);
       }
     }
     __syncwarp();
     if (lane == 0) mbar_arrive(&empty[st]);
     if (++st == SP_ST) { st = 0; ph ^= 1u; }
   }
-  // epilogue: this warp's entries of the slice -> the segment's partial
-  const int64_t a0 = tri_off(jw0, pa) - base, a1 = tri_off(jw1, pa) - base;
+  // epilogue: every owner writes its columns' triangle rows to this segment's partial
   double* out = P.partial + ((size_t)u * P.nseg + seg) * P.cap;
-  for (int64_t e = a0 + lane; e < a1; e += 32) out[e] = gs[e];
+  for (int c = ct; c < ncol; c += SP_CT) {
+    const int64_t a0 = tri_off(J0 + c, pa) - base, a1 = tri_off(J0 + c + 1, pa) - base;
+    for (int64_t e = a0; e < a1; ++e) out[e] = gs[e];
+  }
 }
 
 // packed[base_u + e] = sum over segments (fixed order) of partial[u][seg][e]
@@ -271,29 +300,31 @@ extern "C" oem_status oem_gram_csr(oem_ctx* ctx, const int64_t* row_ptr, const i
   if (n_local > ((int64_t)1 << 40)) OEM_FAIL(OEM_ERR_UNSUPPORTED, "oem_gram_csr: n_local too large");
   cudaStream_t st = (cudaStream_t)stream;
   const int64_t pa = p + 1, psize = packed_size(p);
-  // slices of the packed triangle (rows of Z^T Z) that fit the shared memory beside the ring
-  const int64_t cap_max = (int64_t)(SP_SMEM_MAX - (size_t)SP_ST * SP_STAGE_BYTES - 1024) / 8;
-  std::vector<int> sj{0};
-  {
+  // slices of the packed triangle (rows of Z^T Z): a slice's entries (8 bytes each) sit in shared
+  // memory beside the ring, whose stages carry a row mask per slice column (4 * SP_MW bytes)
+  std::vector<int> sj;
+  int64_t cap = 0;
+  int sbytes = 0;
+  for (int64_t budget = (int64_t)SP_SMEM_MAX - 1024 - (int64_t)SP_ST * SpStage::mask; budget > 0; budget -= 4096) {
+    sj.assign(1, 0);
     int64_t cur = 0;
     for (int j = 0; j <= p; ++j) {
-      const int64_t len = pa - j;
-      if (cur + len > cap_max) { sj.push_back(j); cur = 0; }
-      cur += len;
+      const int64_t need = 8 * (pa - j) + (int64_t)SP_ST * 4 * SP_MW;
+      if (cur + need > budget && cur > 0) { sj.push_back(j); cur = 0; }
+      cur += need;
     }
     sj.push_back(p + 1);
+    cap = 0;
+    int ncol = 0;
+    for (size_t u = 0; u + 1 < sj.size(); ++u) {
+      const int64_t a = sj[u], b = sj[u + 1];
+      cap = std::max<int64_t>(cap, (b * pa - b * (b - 1) / 2) - (a * pa - a * (a - 1) / 2));
+      ncol = std::max(ncol, (int)(b - a));
+    }
+    sbytes = stage_bytes(ncol);
+    if ((size_t)SP_ST * sbytes + (size_t)cap * 8 <= SP_SMEM_MAX - 1024) break;
   }
   const int U = (int)sj.size() - 1;
-  int64_t cap = 0;
-  for (int u = 0; u < U; ++u) {
-    const int64_t a = sj[u], b = sj[u + 1];
-    cap = std::max<int64_t>(cap, (b * pa - b * (b - 1) / 2) - (a * pa - a * (a - 1) / 2));
-  }
-  // consumer warps of a slice split its triangle rows evenly (the work of row j is ~ the
-  // nonzeros of column j, uniform for the paper's random patterns)
-  std::vector<int> wj((size_t)U * (SP_WARPS + 1));
-  for (int u = 0; u < U; ++u)
-    for (int w = 0; w <= SP_WARPS; ++w) wj[(size_t)u * (SP_WARPS + 1) + w] = sj[u] + (int)((int64_t)(sj[u + 1] - sj[u]) * w / SP_WARPS);
   const int nseg = (int)std::max<int64_t>(1, std::min<int64_t>((n_local + 1023) / 1024, std::max(1, ctx->num_sms / U)));
   const int64_t seg_rows = n_local > 0 ? (n_local + nseg - 1) / nseg : 1;
   // workspace: partial [U][nseg][cap] | packed | tables
@@ -302,11 +333,9 @@ extern "C" oem_status oem_gram_csr(oem_ctx* ctx, const int64_t* row_ptr, const i
   const size_t o_part = take(sizeof(double) * (size_t)U * nseg * cap);
   const size_t o_pack = take(sizeof(double) * (size_t)(psize + 2));
   const size_t o_sj = take(sizeof(int) * sj.size());
-  const size_t o_wj = take(sizeof(int) * wj.size());
   OEM_CUDA_TRY(ctx->sparse_ws.ensure(off));
   char* base = ctx->sparse_ws.as<char>();
   OEM_CUDA_TRY(cudaMemcpyAsync(base + o_sj, sj.data(), sizeof(int) * sj.size(), cudaMemcpyHostToDevice, st));
-  OEM_CUDA_TRY(cudaMemcpyAsync(base + o_wj, wj.data(), sizeof(int) * wj.size(), cudaMemcpyHostToDevice, st));
   double* packed = reinterpret_cast<double*>(base + o_pack);
   if (n_local == 0) {
     OEM_CUDA_TRY(cudaMemsetAsync(packed, 0, sizeof(double) * psize, st));
@@ -315,10 +344,10 @@ extern "C" oem_status oem_gram_csr(oem_ctx* ctx, const int64_t* row_ptr, const i
     P.row_ptr = row_ptr; P.col = col; P.val = val; P.y = y; P.n = n_local; P.p = p; P.U = U; P.nseg = nseg;
     P.seg_rows = seg_rows;
     P.slice_j0 = reinterpret_cast<int*>(base + o_sj);
-    P.warp_j0 = reinterpret_cast<int*>(base + o_wj);
     P.cap = (int)cap;
+    P.sbytes = sbytes;
     P.partial = reinterpret_cast<double*>(base + o_part);
-    const size_t smem = (size_t)SP_ST * SP_STAGE_BYTES + (size_t)cap * 8;
+    const size_t smem = (size_t)SP_ST * sbytes + (size_t)cap * 8;
     OEM_CUDA_TRY(cudaFuncSetAttribute(sparse_gram_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     {
       PhaseTimer tm(ctx, PH_GRAM, st);
