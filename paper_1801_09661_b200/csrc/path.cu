@@ -1721,6 +1721,245 @@ __global__ void __launch_bounds__(PT, 1) fit_cluster_kernel(const PathParams P, 
 }
 
 // cluster layout: smallest C whose per-thread share fits registers + shared memory
+// ---------------------------------------------------------------- K5 active-set cluster solver
+// For wide units (p > 256: cfg3's 500, cfg4's 1000) on tall data the coefficient paths are sparse
+// (at lambda_min = 1e-3 lambda_max the null coordinates' |c_j| ~ 1/sqrt(n) stay below lambda), so
+// G beta needs only the columns of G whose coordinate has ever been nonzero. One cluster of C <= 16
+// CTAs per (unit, penalty); CTA c owns rows [j0, j1) (<= 64, groups never straddle CTAs) and keeps
+// G[j][k] of its rows for the ACTIVE columns k in shared memory. Per iteration (P:L171-172 E-step,
+// P:L239-297 M-steps): u_j = c_j + d b_j - sum over active k of G_jk b_k for every row (4 lanes per
+// row, active columns interleaved), the threshold on the row's first lane, the new coordinate
+// stored into every CTA's copy of the vector only where it changed (DSMEM), "needs another
+// iteration" bits and the indices of coordinates that just became nonzero OR-ed into every CTA
+// (red.shared::cluster.or), one hardware cluster barrier. After the barrier every CTA appends the
+// newly active columns in ascending index order (identical on every CTA: the summation order is a
+// deterministic function of the data) and loads their rows of G (G is symmetric: the contiguous
+// row k). Columns beyond the shared-memory capacity are read from the L2-resident Gram.
+// Skipping a column whose coordinate is exactly zero changes no sum (its terms are exact zeros);
+// the sum order over the active list differs from the dense solvers' column order (rounding only).
+struct ActArgs {
+  int C;          // CTAs per cluster
+  int amax;       // active columns cached per CTA
+  int apitch;     // shared-memory pitch of a cached row (doubles)
+  int rows;       // max rows per CTA (<= 64)
+  int pw;         // 32-bit words of a p-bit set
+};
+
+constexpr int ACT_T = 4;         // lanes per row
+
+template <int ACT_THREADS>       // 256 (64 rows per CTA) or 512 (128 rows per CTA)
+__global__ void __launch_bounds__(ACT_THREADS, 1) fit_active_kernel(const PathParams P, const ActArgs A) {
+  extern __shared__ __align__(16) double sm[];
+  __shared__ uint32_t F[3];
+  __shared__ int s_na;
+  __shared__ double s_lmax;
+  const int p = P.p, nPg = P.nP, L = P.L, C = A.C;
+  const int clu = blockIdx.x / C;
+  const int unit = clu / nPg, q = clu % nPg;   // one penalty per cluster
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31, r = tid / ACT_T, tl = tid % ACT_T;
+  constexpr int NW = ACT_THREADS / 32;
+  const uint32_t rank = cluster_rank();
+  const int j0 = P.cta_j0[blockIdx.x], j1 = P.cta_j1[blockIdx.x], nr = j1 - j0;
+  const double* Gu = P.Gn + (size_t)unit * p * p;
+  const double* cu = P.cn + (size_t)unit * p;
+  const int pv = (p + 1) & ~1;
+  // shared memory: vec [2][pv] | ga [rows][apitch] | uv [rows] | gw, ga_s, gb_s [rows] | act [amax] | abits, nbits [2][pw]
+  double* vec = sm;
+  double* ga = vec + 2 * (size_t)pv;
+  double* uv = ga + (size_t)A.rows * A.apitch;
+  double* gw_s = uv + A.rows;
+  int* ga_s = reinterpret_cast<int*>(gw_s + A.rows);
+  int* gb_s = ga_s + A.rows;
+  int* act = gb_s + A.rows;
+  uint32_t* abits = reinterpret_cast<uint32_t*>(act + p);
+  uint32_t* nbits = abits + A.pw;   // [2][pw]
+  const int fam = P.fam[q];
+  const double gq = P.gam[q], aq = P.alp[q];
+  const bool grp = P.g_of != nullptr && fam >= OEM_GRP_LASSO;
+  const int g0 = (P.g_of && nr > 0) ? P.g_of[j0] : 0;
+  const int ng_loc = (grp && nr > 0) ? P.g_of[j1 - 1] + 1 - g0 : 0;
+  for (int gg = tid; gg < ng_loc; gg += ACT_THREADS) {
+    gw_s[gg] = P.g_w[g0 + gg];
+    ga_s[gg] = P.g_start[g0 + gg] - j0;
+    gb_s[gg] = P.g_end[g0 + gg] - j0;
+  }
+  // warm or cold start (permuted order) into both buffers; the initial active set is its support
+  for (int k = tid; k < pv; k += ACT_THREADS) {
+    const double b = (P.beta_init && k < p) ? P.beta_init[((size_t)unit * nPg + q) * p + P.perm[k]] : 0.0;
+    vec[k] = b;
+    vec[pv + k] = b;
+  }
+  for (int w = tid; w < 3 * A.pw; w += ACT_THREADS) abits[w] = 0u;
+  if (tid < 3) F[tid] = 0u;
+  __syncthreads();
+  if (tid == 0) {
+    int na = 0;
+    for (int k = 0; k < p; ++k)
+      if (vec[k] != 0.0) { act[na++] = k; abits[k >> 5] |= 1u << (k & 31); }
+    s_na = na;
+  }
+  __syncthreads();
+  int na = s_na;
+  for (int e = tid; e < nr * min(na, A.amax); e += ACT_THREADS) {
+    const int rr = e / min(na, A.amax), a = e % min(na, A.amax);
+    ga[(size_t)rr * A.apitch + a] = Gu[(size_t)act[a] * p + j0 + rr];
+  }
+  const double d = P.d[unit];
+  const double c_my = r < nr ? cu[j0 + r] : 0.0;
+  const double w_my = (r < nr && P.var_w) ? P.var_w[j0 + r] : 1.0;
+  // ---- a8: lambda grid of this (unit, penalty) (R#14-16, R#22), as in the other solvers
+  if (warp == 0) {
+    double lm = 0.0;
+    const double* cc = P.shared_grid ? P.cn : cu;
+    if (P.lmax_override) {
+      lm = *P.lmax_override;
+    } else if (fam == OEM_SGL) {
+      for (int gg = lane; gg < P.ngroups; gg += 32)
+        lm = fmax(lm, sgl_lmax_group(cc, P.g_start[gg], P.g_end[gg], P.var_w, P.g_w[gg], aq));
+    } else if (fam >= OEM_GRP_LASSO) {
+      for (int gg = lane; gg < P.ngroups; gg += 32) {
+        const double cg = P.g_w[gg];
+        if (!(cg > 0.0)) continue;
+        double sq = 0.0;
+        for (int j = P.g_start[gg]; j < P.g_end[gg]; ++j) sq += cc[j] * cc[j];
+        lm = fmax(lm, sqrt(sq) / cg);
+      }
+    } else {
+      const double scl = fam == OEM_ENET ? aq : 1.0;
+      for (int j = lane; j < p; j += 32) {
+        const double wj = P.var_w ? P.var_w[j] : 1.0;
+        if (!(wj > 0.0)) continue;
+        lm = fmax(lm, fabs(cc[j]) / (scl * wj));
+      }
+    }
+#pragma unroll
+    for (int o = 16; o >= 1; o >>= 1) lm = fmax(lm, __shfl_xor_sync(0xffffffffu, lm, o));
+    if (lane == 0) {
+      s_lmax = lm;
+      bool bad = false;  // parameter validity against the d in use (R#8)
+      if (fam == OEM_MCP || fam == OEM_GRP_MCP) bad = !(gq > 1.0) || !(gq * d > 1.0);
+      if (fam == OEM_SCAD || fam == OEM_GRP_SCAD) bad = !(gq > 2.0) || !((gq - 1.0) * d > 1.0);
+      if (fam == OEM_ENET) bad = !(aq >= 0.0 && aq <= 1.0);
+      if (bad) { atomicExch(&P.flags[1], 1); s_lmax = -1.0; }
+    }
+  }
+  __syncthreads();
+  if (s_lmax < 0.0) return;   // invalid parameters: every CTA of the cluster leaves together
+  auto lam_at = [&](int l) -> double {
+    if (P.lam_explicit) return P.lam_explicit[l];
+    if (L == 1) return s_lmax;
+    return s_lmax * exp(((double)l / (double)(L - 1)) * log(P.lmin_ratio));  // R#15
+  };
+  if (rank == 0)
+    for (int l = tid; l < L; l += ACT_THREADS) P.lam_out[((size_t)unit * nPg + q) * L + l] = lam_at(l);
+  int lidx = 0, itc = 0;
+  double lam = lam_at(0);
+  cluster_sync_all();  // every CTA initialised before the first remote store
+
+  // ======================================================= a9: OEM iterations
+  for (int t = 0; lidx < L; ++t) {
+    const int cur = t & 1, par = t & 1;
+    const double* vc = vec + (size_t)cur * pv;
+    double* vn = vec + (size_t)(cur ^ 1) * pv;
+    if (tid == 0) F[(t + 1) % 3] = 0u;
+    // ---- E-step: u_j = c_j + d b_j - sum_{k active} G_jk b_k
+    double acc = 0.0;
+    if (r < nr) {
+      const double* gr = ga + (size_t)r * A.apitch;
+      const int nc = min(na, A.amax);
+      int a = tl;
+      for (; a + 3 * ACT_T < nc; a += 4 * ACT_T) {   // four independent loads in flight
+        const double b0 = vc[act[a]], b1 = vc[act[a + ACT_T]], b2 = vc[act[a + 2 * ACT_T]], b3 = vc[act[a + 3 * ACT_T]];
+        acc = fma(gr[a], b0, acc);
+        acc = fma(gr[a + ACT_T], b1, acc);
+        acc = fma(gr[a + 2 * ACT_T], b2, acc);
+        acc = fma(gr[a + 3 * ACT_T], b3, acc);
+      }
+      for (; a < nc; a += ACT_T) acc = fma(gr[a], vc[act[a]], acc);
+      for (a = A.amax + tl; a < na; a += ACT_T) acc = fma(Gu[(size_t)act[a] * p + j0 + r], vc[act[a]], acc);  // beyond capacity
+    }
+#pragma unroll
+    for (int o = ACT_T / 2; o >= 1; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+    uint32_t bits = 0;
+    const int j = j0 + r;
+    auto emit = [&](int jj, double nb) {   // new coordinate jj: vector copies, flags, activation
+      const double bj = vc[jj];
+      if (!(fabs(nb - bj) <= P.tol)) bits |= 1u;
+      if (nb != vn[jj])
+        for (int rr = 0; rr < C; ++rr) st_cl_f64(&vn[jj], rr, nb);
+      if (nb != 0.0 && !((abits[jj >> 5] >> (jj & 31)) & 1u))
+        for (int rr = 0; rr < C; ++rr) red_or_cl(&nbits[par * A.pw + (jj >> 5)], rr, 1u << (jj & 31));
+    };
+    if (tl == 0 && r < nr && lidx < L) {
+      const double u = c_my + d * vc[j] - acc;
+      if (!isfinite(u)) bits |= 0x80000000u;
+      if (!grp) emit(j, th_coord(fam, u, w_my * lam, gq, aq, d));
+      else uv[r] = u;
+    }
+    if (grp) {
+      // group M-step (eqs glasso / gmcp / gscad / sglasso); groups lie inside [j0, j1)
+      __syncthreads();
+      for (int gl = warp; gl < ng_loc; gl += NW)
+        group_mstep_warp(uv, ga_s[gl], gb_s[gl], fam, lam, gq, aq, gw_s[gl], d, P.var_w, j0, lane,
+                         [&](int rr, double nb) { emit(j0 + rr, nb); });
+    }
+    bits = __reduce_or_sync(0xffffffffu, bits);
+    if (lane == 0 && bits)
+      for (int rr = 0; rr < C; ++rr) red_or_cl(&F[t % 3], rr, bits);
+    cluster_sync_all();
+    const uint32_t f = F[t % 3];
+    if (f & 0x80000000u) {
+      if (tid == 0) atomicExch(&P.flags[0], 1);
+      break;
+    }
+    // ---- newly active columns. Every warp checks the request words in parallel (the same answer
+    // in every warp, so no block barrier when nothing changed, the common case); otherwise they
+    // are appended in ascending index order on every CTA and their rows of G loaded.
+    bool any = false;
+    for (int w = lane; w < A.pw; w += 32) any = any || (nbits[par * A.pw + w] & ~abits[w]) != 0u;
+    if (__any_sync(0xffffffffu, any)) {
+      int added = 0;
+      for (int w = 0; w < A.pw; ++w) {
+        uint32_t nw = nbits[par * A.pw + w] & ~abits[w];
+        while (nw) {
+          const int k = 32 * w + __ffs(nw) - 1;
+          nw &= nw - 1;
+          if (tid == 0) act[na + added] = k;
+          ++added;
+        }
+      }
+      __syncthreads();   // act[] complete before the loads; every thread has read nbits / abits
+      for (int e = tid; e < nr * added; e += ACT_THREADS) {
+        const int rr = e / added, a = na + e % added;
+        if (a < A.amax) ga[(size_t)rr * A.apitch + a] = Gu[(size_t)act[a] * p + j0 + rr];
+      }
+      for (int w = tid; w < A.pw; w += ACT_THREADS) {
+        abits[w] |= nbits[par * A.pw + w];
+        nbits[par * A.pw + w] = 0u;   // reused at t + 2 (after the next cluster barrier)
+      }
+      na += added;
+      __syncthreads();
+    }
+    // ---- bookkeeping (identical in every thread of every CTA of the cluster)
+    const int it = itc + 1;
+    const bool conv = !(f & 1u);   // every |dbeta_j| <= tol (R#17)
+    if (conv || it >= P.maxit) {
+      double* out = P.beta_out + (((size_t)unit * nPg + q) * L + lidx) * p;
+      for (int rr = tid; rr < nr; rr += ACT_THREADS) out[P.perm[j0 + rr]] = vn[j0 + rr];
+      if (rank == 0 && tid == 0) {
+        P.it_out[((size_t)unit * nPg + q) * L + lidx] = it;
+        P.cv_out[((size_t)unit * nPg + q) * L + lidx] = conv ? 1 : 0;
+      }
+      ++lidx;
+      itc = 0;
+      if (lidx < L) lam = lam_at(lidx);
+    } else {
+      itc = it;
+    }
+  }
+  cluster_sync_all();   // no CTA leaves while a peer may still store into its shared memory
+}
+
 struct ClusterLayout {
   int C = 0, T = 1, RG = PT, KPR = 0, NRT = 1, S = 0, pv = 0, ereg = 32, maxrows = 0;
   size_t smem = 0;
@@ -2028,6 +2267,76 @@ static oem_status launch_glob_v(const PathParams& P, const GlobArgs& A, int grid
   return coop_launch(fit_glob_kernel<NPT, 2, 16, 32>, grid, lo.smem, st, args);
 }
 
+// ---------------------------------------------------------------- active-set solver: host layout / launch
+struct ActLayout {
+  int C = 0, rows = 0, amax = 0, apitch = 0, pw = 0, nth = 256;
+  size_t smem = 0;
+  std::vector<int> cuts;
+};
+static bool make_act_layout(int p, const std::vector<int>& gstart, ActLayout& lo, int nth) {
+  const int maxrows = nth / ACT_T;   // 64 or 128
+  std::vector<int> cuts{0};
+  if (gstart.empty()) {
+    const int C = (p + maxrows - 1) / maxrows;
+    for (int c = 1; c <= C; ++c) cuts.push_back((int)((int64_t)p * c / C));
+  } else {   // cut only at group starts (greedy packing), as the lean layout
+    std::vector<int> starts(gstart);
+    std::sort(starts.begin(), starts.end());
+    starts.push_back(p);
+    int last = 0;
+    for (size_t i = 1; i < starts.size(); ++i) {
+      const int b = starts[i];
+      if (b - cuts.back() > maxrows) {
+        if (last <= cuts.back()) return false;
+        cuts.push_back(last);
+        if (b - cuts.back() > maxrows) return false;
+      }
+      last = b;
+    }
+    if (cuts.back() != p) cuts.push_back(p);
+  }
+  const int C = (int)cuts.size() - 1;
+  if (C < 1 || C > 16) return false;
+  int rows = 0;
+  for (int c = 0; c < C; ++c) rows = std::max(rows, cuts[c + 1] - cuts[c]);
+  lo.C = C;
+  lo.nth = nth;
+  lo.rows = rows;
+  lo.cuts = cuts;
+  lo.pw = (p + 31) / 32;
+  const int pv = (p + 1) & ~1;
+  const size_t fixed = (size_t)2 * pv * 8 + (size_t)rows * 8 * 2 + (size_t)rows * 4 * 2 + (size_t)p * 4 +
+                       (size_t)3 * lo.pw * 4 + 64;
+  const size_t cap = 200 * 1024;
+  if (fixed + (size_t)rows * 8 * 8 > cap) return false;
+  int apitch = (int)std::min<size_t>((cap - fixed) / ((size_t)rows * 8), (size_t)p + 2);
+  apitch -= (apitch % 2);   // keep rows 16-byte aligned
+  lo.apitch = apitch;
+  lo.amax = std::min(apitch, p);
+  lo.smem = fixed + (size_t)rows * apitch * 8;
+  return true;
+}
+template <int NTH>
+static oem_status launch_active(const PathParams& P, const ActArgs& A, int nclusters, size_t smem, cudaStream_t st) {
+  auto kern = fit_active_kernel<NTH>;
+  OEM_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  if (A.C > 8) OEM_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3((unsigned)(nclusters * A.C));
+  cfg.blockDim = dim3(NTH);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = (unsigned)A.C;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  OEM_CUDA_TRY(cudaLaunchKernelEx(&cfg, kern, P, A));
+  return OEM_OK;
+}
+
 // ---------------------------------------------------------------- host side
 struct Layout {
   std::vector<int> unit, rank, ncta, j0, j1;
@@ -2200,19 +2509,32 @@ extern "C" oem_status oem_fit_path(oem_ctx* ctx, const double* G, const double* 
   ClusterLayout cl;
   Layout lo;
   LeanLayout ll;
-  const bool use_lean = !(force && (std::string(force) == "global" || std::string(force) == "cluster")) &&
+  // active-set clusters for wide units (p > 256), whose tall-data paths are sparse; the register-
+  // resident lean clusters below that; OEM_PATH_SOLVER=active / lean / global / cluster / batched
+  // forces a variant (tests, timing studies)
+  ActLayout al;
+  const std::string fs = force ? std::string(force) : std::string();
+  // (128-row CTAs when that gives a smaller cluster: fewer CTAs meet at each barrier)
+  const bool want_act = fs == "active" || (fs.empty() && p > 256);
+  const std::vector<int> gs_act = any_grp ? gstart : std::vector<int>();
+  ActLayout al128;
+  const bool act256 = want_act && make_act_layout(p, gs_act, al, 256);
+  const bool act512 = want_act && p > 512 && make_act_layout(p, gs_act, al128, 512);
+  if (act512 && (!act256 || al128.C < al.C)) al = al128;
+  const bool use_act = act256 || act512;
+  const bool use_lean = !use_act && !(fs == "global" || fs == "cluster") &&
                         make_lean_layout(p, nP, any_grp ? gstart : std::vector<int>(), ll);
   GlobLayout gl;
-  const bool glob_ok = !use_lean && !(force && (std::string(force) == "global" || std::string(force) == "cluster"));
+  const bool glob_ok = !use_act && !use_lean && !(force && (std::string(force) == "global" || std::string(force) == "cluster"));
   const bool use_glob =
       glob_ok && ((nP > 1 && !(force && std::string(force) == "batched") &&
                    make_glob_layout(nU, p, nP, any_grp ? gstart : std::vector<int>(), ctx->num_sms, gl, true)) ||
                   make_glob_layout(nU, p, nP, any_grp ? gstart : std::vector<int>(), ctx->num_sms, gl, false));
-  bool use_cluster = !use_lean && !use_glob && !(force && std::string(force) == "global") &&
+  bool use_cluster = !use_act && !use_lean && !use_glob && !(force && std::string(force) == "global") &&
                      make_cluster_layout(nU, p, NPT, any_grp ? gstart : std::vector<int>(), ctx->num_sms,
                                          ereg_for(NPT), cl);
   std::string why;
-  if (!use_lean && !use_glob && !use_cluster &&
+  if (!use_act && !use_lean && !use_glob && !use_cluster &&
       !make_layout(nU, p, NPT, any_grp ? gstart : std::vector<int>(), ctx->num_sms, 200 * 1024, lo, why))
     OEM_FAIL(OEM_ERR_UNSUPPORTED, "oem_fit_path: persistent solver layout: " + why);
   // penalty split: with SMs to spare, each (unit, penalty) gets its own cluster (NPT = 1: no
@@ -2223,7 +2545,14 @@ extern "C" oem_status oem_fit_path(oem_ctx* ctx, const double* G, const double* 
                       (int64_t)nU * nP * ll1.C <= ctx->num_sms;
   if (qsplit) ll = ll1;
   std::vector<int> t_unit, t_rank, t_ncta, t_j0, t_j1;
-  if (use_lean) {
+  if (use_act) {
+    for (int u = 0; u < nU; ++u)
+      for (int q = 0; q < nP; ++q)
+        for (int c = 0; c < al.C; ++c) {
+          t_unit.push_back(u); t_rank.push_back(c); t_j0.push_back(al.cuts[c]); t_j1.push_back(al.cuts[c + 1]);
+        }
+    t_ncta.assign(nU, al.C);
+  } else if (use_lean) {
     for (int u = 0; u < nU; ++u)
       for (int q = 0; q < (qsplit ? nP : 1); ++q)
         for (int c = 0; c < ll.C; ++c) {
@@ -2252,7 +2581,7 @@ extern "C" oem_status oem_fit_path(oem_ctx* ctx, const double* G, const double* 
         if (gstart[g] < t_j0[i] && gend[g] > t_j0[i])
           OEM_FAIL(OEM_ERR_UNSUPPORTED, "oem_fit_path: a group is larger than one solver CTA's rows");
   }
-  const int Cmax = use_lean ? ll.C : use_glob ? gl.C : use_cluster ? cl.C : lo.Cmax;
+  const int Cmax = use_act ? al.C : use_lean ? ll.C : use_glob ? gl.C : use_cluster ? cl.C : lo.Cmax;
   // ---- workspace (device)
   const size_t pp = (size_t)p * p;
   size_t off = 0;
@@ -2413,6 +2742,16 @@ extern "C" oem_status oem_fit_path(oem_ctx* ctx, const double* G, const double* 
     else if (nP == 2) s = launch_glob_v<2>(P, A, grid, gl, st);
     else if (nP == 3) s = launch_glob_v<3>(P, A, grid, gl, st);
     else s = launch_glob_v<4>(P, A, grid, gl, st);
+    if (s != OEM_OK) return s;
+  } else if (use_act) {
+    // ---- a8-a10 in one launch: an active-set cluster per (unit, penalty)
+    P.ps = 0; P.T = 0; P.smem_rows = 0;
+    ActArgs A;
+    A.C = al.C; A.amax = al.amax; A.apitch = al.apitch; A.rows = al.rows; A.pw = al.pw;
+    PhaseTimer tm(ctx, PH_PATH, st);
+    ++ctx->launches;
+    oem_status s = al.nth == 512 ? launch_active<512>(P, A, nU * nP, al.smem, st)
+                                 : launch_active<256>(P, A, nU * nP, al.smem, st);
     if (s != OEM_OK) return s;
   } else if (use_lean) {
     // ---- a7-a10 fused in one launch: register-resident G, one cluster per unit

@@ -424,3 +424,46 @@ def test_batched_penalties_every_lean_layout(ctx, p, monkeypatch):
         for q, (fam, gamma, alpha) in enumerate(pens):
             B, it, cv = orc.oem_path(Go / nn, co / nn, d, fam, fit.lam[u, q].cpu().numpy(), gamma, alpha)
             assert np.max(np.abs(fit.beta[u, q].cpu().numpy() - B)) <= TOL_BETA, (p, u, fam)
+
+
+@pytest.mark.parametrize("p,solver", [(60, "active"), (260, None), (300, "global"), (700, "lean"), (1000, None)])
+def test_active_set_solver(ctx, p, solver, monkeypatch):
+    """The active-set cluster solver (default for p > 256; forced at p = 60) and the solvers it
+    replaced there (grid-wide at p = 300, forced; lean has no layout at p = 700, so that case
+    runs the grid-wide solver too), four penalties including a group one, two units, warm starts
+    from a previous path and an explicit grid, all against the oracle's own pipeline."""
+    from paper_1801_09661_b200 import oem_fit_path, oem_gram
+    if solver:
+        monkeypatch.setenv("OEM_PATH_SOLVER", solver)
+    spec = CONFIGS["cfg4"].spec.replace(n=3000 + 2 * p, p=p - p % 10, nnz=3)
+    pp = spec.p
+    bt = dg.beta(spec)
+    X, y = dg.rows_host(spec, bt)
+    Xd, yd = torch.from_numpy(X).cuda(), torch.from_numpy(y).cuda()
+    h = (X.shape[0] // 2) & ~1
+    G0, c0, _, n0 = oem_gram(ctx, Xd[:h], yd[:h])
+    G1, c1, _, n1 = oem_gram(ctx, Xd[h:], yd[h:])
+    grp = (np.arange(pp) // 10).astype(np.int32)
+    pens = [("lasso", 0.0, 1.0), ("grp_lasso", 0.0, 1.0), ("mcp", 3.0, 1.0), ("enet", 0.0, 0.5)]
+    G = torch.stack([G0, G1]); c = torch.stack([c0, c1])
+    fit = oem_fit_path(ctx, G, c, [n0, n1], pens, nlambda=10, group=grp, ngroups=pp // 10)
+    for u, (lo, hi, nn) in enumerate([(0, h, n0), (h, X.shape[0], n1)]):
+        Go, co, _ = orc.gram(X[lo:hi], y[lo:hi])
+        d_ref = check_d(float(fit.d[u]), Go, nn, G[u].cpu().numpy())
+        for q, (fam, gamma, alpha) in enumerate(pens):
+            g = grp if fam.startswith("grp") else None
+            lam = orc.lambda_grid(orc.lambda_max(fam, co / nn, group=g, alpha=alpha), 10)
+            assert np.max(np.abs(fit.lam[u, q].cpu().numpy() - lam) / lam) < 1e-13
+            B, it, cv = orc.oem_path(Go / nn, co / nn, d_ref, fam, lam, gamma, alpha, group=g)
+            assert np.max(np.abs(fit.beta[u, q].cpu().numpy() - B)) <= TOL_BETA, (p, u, fam)
+            assert np.array_equal(fit.conv[u, q].cpu().numpy().astype(bool), cv)
+    # warm start from the last solutions, explicit two-point grid below the path's end
+    init = fit.beta[:, :, -1, :].contiguous()
+    lam2 = [float(fit.lam[0, 0, -1]) * 0.7, float(fit.lam[0, 0, -1]) * 0.5]
+    fit2 = oem_fit_path(ctx, G, c, [n0, n1], pens[:1], lambdas=lam2, beta_init=init[:, :1].contiguous(),
+                        d_in=[float(v) for v in fit.d.cpu()])
+    for u, (lo, hi, nn) in enumerate([(0, h, n0), (h, X.shape[0], n1)]):
+        Go, co, _ = orc.gram(X[lo:hi], y[lo:hi])
+        B, it, cv = orc.oem_path(Go / nn, co / nn, float(fit.d[u]), "lasso", lam2,
+                                 beta_init=init[u, 0].cpu().numpy())
+        assert np.max(np.abs(fit2.beta[u, 0].cpu().numpy() - B)) <= TOL_BETA
