@@ -182,7 +182,8 @@ void oem_logistic_cfg_default(oem_logistic_cfg* cfg);  /* 50, 1e-3, NULL, 1e-11,
 
 /* ---- f1 logistic gradient pass (P:L357-359 mu(x) = 1/(1 + exp(-x^T beta)); P:L385-389 the
  * upper-bound step needs only X^T (y - mu)). One HBM-bound pass over [X | y]: g = sum_i
- * (y_i - mu_i) x_i (p) and loglik = sum_i [y_i eta_i - log(1 + e^eta_i)] (1), raw sums over this
+ * (y_i - mu_i) x_i (p) and loglik = sum_i [y_i eta_i - log(1 + e^eta_i)] (1, device, or NULL: not
+ * formed, which drops a third of the per-row fp64 work), raw sums over this
  * rank's rows, allreduced when the context has a communicator. beta (device, p) identical on every rank. No clamp of
  * mu (no division by w). Errors: OEM_ERR_DIM, OEM_ERR_ALIGN (X 16-byte aligned, ldx even),
  * OEM_ERR_UNSUPPORTED (p > 512), OEM_ERR_CUDA, OEM_ERR_NCCL. */

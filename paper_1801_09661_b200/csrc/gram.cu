@@ -290,8 +290,8 @@ __device__ __forceinline__ void weighted_rows(const GramParams& P, const Cons& c
 // forms, per row, eta = x_i^T beta, mu = sigma(eta) clamped to [eps, 1-eps], w = mu(1-mu),
 // z = eta + (y - mu)/w -> wz[i] = (w_i, z_i) (the same formulas, in the same order, as
 // weighted_rows); with want_scal, per-CTA (sum w, log-likelihood) partials in warp order.
-// Warps own interleaved rows of a contiguous per-CTA range; lanes take 16-byte column pairs,
-// two rows and four pairs per lane in flight; beta lives in shared memory (zero past p).
+// Warps own blocks of 32 rows of a contiguous per-CTA range; lanes take 16-byte column pairs
+// (four in flight); beta lives in shared memory (zero past p).
 constexpr int RW_THREADS = 256;
 __global__ void __launch_bounds__(RW_THREADS) row_weights_kernel(const double* __restrict__ X, const double* __restrict__ y,
                                                                  const double* __restrict__ beta, int64_t n, int p,
@@ -307,12 +307,14 @@ __global__ void __launch_bounds__(RW_THREADS) row_weights_kernel(const double* _
   const double2* b2 = reinterpret_cast<const double2*>(bsm);
   const int64_t r0 = (int64_t)blockIdx.x * rows_per_cta, r1 = min(n, r0 + rows_per_cta);
   double sw = 0.0, sll = 0.0;
-  for (int64_t i0 = r0 + 2 * warp; i0 < r1; i0 += 2 * nw) {
-    double e[2];
-#pragma unroll
-    for (int rb = 0; rb < 2; ++rb) {
-      const int64_t i = min(i0 + rb, r1 - 1);
-      const double2* x2 = reinterpret_cast<const double2*>(X + i * ldx);
+  // a warp takes 32 rows per step: their dot products one by one (lanes over column pairs, four
+  // pairs in flight, butterfly sum), lane k keeping eta of row k; then the per-row scalar work
+  // (exp, clamp, two divisions) runs once per lane instead of once per row on a whole warp
+  for (int64_t i0 = r0 + 32 * warp; i0 < r1; i0 += 32 * nw) {
+    double eta = 0.0;
+    const int nrow = r1 - i0 < 32 ? (int)(r1 - i0) : 32;
+    for (int k = 0; k < nrow; ++k) {
+      const double2* x2 = reinterpret_cast<const double2*>(X + (i0 + k) * ldx);
       double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
       int t = lane;
       for (; t + 96 < np2; t += 128) {
@@ -332,11 +334,11 @@ __global__ void __launch_bounds__(RW_THREADS) row_weights_kernel(const double* _
       double v = (a0 + a1) + (a2 + a3);
 #pragma unroll
       for (int o = 16; o >= 1; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
-      e[rb] = v;
+      if (lane == k) eta = v;
     }
-    if (lane < 2 && i0 + lane < r1) {
+    if (lane < nrow) {
       const int64_t i = i0 + lane;
-      const double ee = lane == 0 ? e[0] : e[1], yk = __ldg(y + i);
+      const double ee = eta, yk = __ldg(y + i);
       const double ex = exp(-ee);
       double mu = 1.0 / (1.0 + ex);
       mu = fmin(fmax(mu, eps), 1.0 - eps);
@@ -349,8 +351,11 @@ __global__ void __launch_bounds__(RW_THREADS) row_weights_kernel(const double* _
     }
   }
   if (!want_scal) return;
-  sw += __shfl_xor_sync(0xffffffffu, sw, 1);   // lanes 0 and 1, fixed order
-  sll += __shfl_xor_sync(0xffffffffu, sll, 1);
+#pragma unroll
+  for (int o = 16; o >= 1; o >>= 1) {   // butterfly over the lanes, fixed order
+    sw += __shfl_xor_sync(0xffffffffu, sw, o);
+    sll += __shfl_xor_sync(0xffffffffu, sll, o);
+  }
   if (lane == 0) { red[warp][0] = sw; red[warp][1] = sll; }
   __syncthreads();
   if (threadIdx.x < 2) {

@@ -116,7 +116,7 @@ oem_status host_allreduce_i64(oem_ctx* ctx, int64_t* vals, int n, cudaStream_t s
 
 // f1 (logit_ub.cu): out[0..p) = X^T (y - sigma(X beta)), out[p] = loglik, raw sums allreduced
 oem_status logit_grad_pass(oem_ctx* ctx, const double* X, const double* y01, const double* beta, int64_t n_local,
-                           int p, int64_t ldx, double* out, cudaStream_t st);
+                           int p, int64_t ldx, double* out, cudaStream_t st, int want_ll = 1);
 // a7 (drule.cu): d[u] = min(Gershgorin, trace(G_u^(2^S))^(1/2^S) (1 + 2Spu)) for the nU normalised
 // p x p unit Grams Gn (R#5); d_out device [nU]
 oem_status d_rule(oem_ctx* ctx, const double* Gn, int nU, int p, int S, double* d_out, cudaStream_t st);

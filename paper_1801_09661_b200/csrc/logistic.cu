@@ -113,7 +113,7 @@ extern "C" oem_status oem_fit_logistic(oem_ctx* ctx, const double* X, const doub
     int64_t nt = 0;
     s = oem_gram(ctx, X, y01, n_local, p, ldx, Gw, cw, sc, &nt, stream);
     if (s != OEM_OK) return s;
-    s = logit_grad_pass(ctx, X, y01, beta, n_local, p, ldx, gb, st);
+    s = logit_grad_pass(ctx, X, y01, beta, n_local, p, ldx, gb, st, 0);
     if (s != OEM_OK) return s;
   } else {
     // a4 at beta = 0: gives lambda_max (R#14) and the first outer step's weighted Gram
@@ -177,7 +177,7 @@ extern "C" oem_status oem_fit_logistic(oem_ctx* ctx, const double* X, const doub
     while (o < cfg.outer_maxit) {
       if (ub) {
         if (!have_gram) {
-          s = logit_grad_pass(ctx, X, y01, beta, n_local, p, ldx, gb, st);
+          s = logit_grad_pass(ctx, X, y01, beta, n_local, p, ldx, gb, st, 0);
           if (s != OEM_OK) return s;
         }
         s = ub_rhs(ctx, Gw, beta, gb, p, cw, st);  // c = X^T X beta + 4 X^T (y - mu)

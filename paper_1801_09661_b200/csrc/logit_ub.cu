@@ -25,7 +25,7 @@ constexpr int LG_WARPS = LG_THREADS / 32;
 
 __device__ __forceinline__ double softplus_dev(double e) { return e > 0.0 ? e + log1p(exp(-e)) : log1p(exp(e)); }
 
-template <int PS>  // double2 slots per lane: p <= 64 * PS
+template <int PS, bool LL>  // double2 slots per lane: p <= 64 * PS; LL: also the log-likelihood
 __global__ void __launch_bounds__(LG_THREADS, PS >= 8 ? 1 : 2) logit_grad_kernel(const double* __restrict__ X, const double* __restrict__ y,
                                                                 const double* __restrict__ beta, int64_t n, int p,
                                                                 int64_t ldx, int64_t rows_per_cta,
@@ -77,7 +77,7 @@ __global__ void __launch_bounds__(LG_THREADS, PS >= 8 ? 1 : 2) logit_grad_kernel
           g[s].x = fma(r, x[rb][s].x, g[s].x);
           g[s].y = fma(r, x[rb][s].y, g[s].y);
         }
-        if (lane == 0) ll += yv[rb] * e - softplus_dev(e);
+        if (LL && lane == 0) ll += yv[rb] * e - softplus_dev(e);
       }
     }
   }
@@ -130,15 +130,18 @@ oem_status ub_rhs(oem_ctx* ctx, const double* G, const double* beta, const doubl
 
 template <int PS>
 static oem_status launch_lg(int grid, const double* X, const double* y, const double* beta, int64_t n, int p,
-                            int64_t ldx, int64_t rpc, double* part, cudaStream_t st) {
-  logit_grad_kernel<PS><<<grid, LG_THREADS, 0, st>>>(X, y, beta, n, p, ldx, rpc, part);
+                            int64_t ldx, int64_t rpc, double* part, bool ll, cudaStream_t st) {
+  if (ll) logit_grad_kernel<PS, true><<<grid, LG_THREADS, 0, st>>>(X, y, beta, n, p, ldx, rpc, part);
+  else logit_grad_kernel<PS, false><<<grid, LG_THREADS, 0, st>>>(X, y, beta, n, p, ldx, rpc, part);
   OEM_CUDA_TRY(cudaGetLastError());
   return OEM_OK;
 }
 
-// g (p) and loglik (1) as raw sums over this rank's rows into out[0..p]; allreduced over ranks
+// g (p) and loglik (1) as raw sums over this rank's rows into out[0..p]; allreduced over ranks.
+// want_ll = 0: out[p] = 0 (the upper-bound fit stops on the change in beta and needs no
+// log-likelihood; dropping its log1p / exp per row takes a third of the per-row fp64 work)
 oem_status logit_grad_pass(oem_ctx* ctx, const double* X, const double* y01, const double* beta, int64_t n_local,
-                           int p, int64_t ldx, double* out, cudaStream_t st) {
+                           int p, int64_t ldx, double* out, cudaStream_t st, int want_ll) {
   if (p > 512) OEM_FAIL(OEM_ERR_UNSUPPORTED, "oem_logit_grad: p > 512 (register-resident beta and gradient)");
   const int grid = std::max(1, std::min<int>(ctx->num_sms * 4, (int)((n_local + 255) / 256)));
   const int64_t rpc = n_local > 0 ? (n_local + grid - 1) / grid : 0;
@@ -150,10 +153,10 @@ oem_status logit_grad_pass(oem_ctx* ctx, const double* X, const double* y01, con
     PhaseTimer tm(ctx, PH_GRAM, st);
     ++ctx->launches;
     oem_status s;
-    if (p <= 64) s = launch_lg<1>(grid, X, y01, beta, n_local, p, ldx, rpc, part, st);
-    else if (p <= 128) s = launch_lg<2>(grid, X, y01, beta, n_local, p, ldx, rpc, part, st);
-    else if (p <= 256) s = launch_lg<4>(grid, X, y01, beta, n_local, p, ldx, rpc, part, st);
-    else s = launch_lg<8>(grid, X, y01, beta, n_local, p, ldx, rpc, part, st);
+    if (p <= 64) s = launch_lg<1>(grid, X, y01, beta, n_local, p, ldx, rpc, part, want_ll != 0, st);
+    else if (p <= 128) s = launch_lg<2>(grid, X, y01, beta, n_local, p, ldx, rpc, part, want_ll != 0, st);
+    else if (p <= 256) s = launch_lg<4>(grid, X, y01, beta, n_local, p, ldx, rpc, part, want_ll != 0, st);
+    else s = launch_lg<8>(grid, X, y01, beta, n_local, p, ldx, rpc, part, want_ll != 0, st);
     if (s != OEM_OK) return s;
     PhaseTimer tm2(ctx, PH_REDUCE, st);
     ++ctx->launches;
@@ -178,7 +181,7 @@ extern "C" oem_status oem_logit_grad(oem_ctx* ctx, const double* X, const double
   cudaStream_t st = (cudaStream_t)stream;
   OEM_CUDA_TRY(ctx->lg_out.ensure(sizeof(double) * (p + 1)));
   double* out = ctx->lg_out.as<double>();
-  oem_status s = logit_grad_pass(ctx, X, y01, beta, n_local, p, ldx, out, st);
+  oem_status s = logit_grad_pass(ctx, X, y01, beta, n_local, p, ldx, out, st, loglik != nullptr);
   if (s != OEM_OK) return s;
   OEM_CUDA_TRY(cudaMemcpyAsync(g, out, sizeof(double) * p, cudaMemcpyDeviceToDevice, st));
   if (loglik) OEM_CUDA_TRY(cudaMemcpyAsync(loglik, out + p, sizeof(double), cudaMemcpyDeviceToDevice, st));

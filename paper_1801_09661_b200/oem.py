@@ -457,14 +457,15 @@ def oem_fit_logistic(ctx: Context, X, y01, penalty=("lasso", 0.0, 1.0), nlambda=
     return LogisticResult(beta, lam, list(oi), list(ii), [bool(v) for v in cv])
 
 
-def oem_logit_grad(ctx: Context, X, y01, beta, stream=None):
-    """f1: (X^T (y - sigma(X beta)), loglik) as raw sums in one pass over [X | y]."""
+def oem_logit_grad(ctx: Context, X, y01, beta, stream=None, loglik=True):
+    """f1: (X^T (y - sigma(X beta)), loglik) as raw sums in one pass over [X | y];
+    loglik=False skips the log-likelihood (second result None)."""
     _check_x(X, y01)
     n, p = X.shape
     if beta.dtype != torch.float64 or not beta.is_cuda or beta.numel() != p:
         raise ValueError("beta must be a float64 CUDA tensor of length p")
     g = torch.empty(p, dtype=torch.float64, device=X.device)
-    ll = torch.empty(1, dtype=torch.float64, device=X.device)
+    ll = torch.empty(1, dtype=torch.float64, device=X.device) if loglik else None
     _check(lib().oem_logit_grad(ctx.h, _ptr(X), _ptr(y01), _ptr(beta.contiguous()), n, p, X.stride(0),
                                 _ptr(g), _ptr(ll), _stream(stream)))
     return g, ll

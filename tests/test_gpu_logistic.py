@@ -199,3 +199,15 @@ def test_logistic_group_lasso_p250_exact_hessian(ctx):
     B, oi, ii, cv = orc.logistic_path(X, y, lam, family="grp_lasso", group=grp)
     assert np.max(np.abs(fit.beta.cpu().numpy() - B)) <= 1e-8
     assert np.array_equal(np.array(fit.conv), cv)
+
+
+def test_logit_grad_without_loglik(ctx):
+    """loglik=False (the upper-bound fit's call) gives the same gradient bit for bit."""
+    from paper_1801_09661_b200 import oem_logit_grad
+    spec = CONFIGS["cfg5"].spec.replace(n=7_001, p=90, nnz=9)
+    bt = dg.beta(spec)
+    Xd, yd = device_rows(spec, bt)
+    beta = torch.from_numpy(0.5 * bt).cuda()
+    g1, ll = oem_logit_grad(ctx, Xd, yd, beta)
+    g2, none = oem_logit_grad(ctx, Xd, yd, beta, loglik=False)
+    assert none is None and ll is not None and torch.equal(g1, g2)
