@@ -43,7 +43,7 @@ __global__ void __launch_bounds__(LG_THREADS, PS >= 8 ? 1 : 2) logit_grad_kernel
     g[s] = make_double2(0.0, 0.0);
   }
   double ll = 0.0;
-  constexpr int RB = PS <= 2 ? 4 : 2;  // rows in flight per warp
+  constexpr int RB = PS <= 2 ? 4 : 2;  // rows per warp step
   for (int64_t i0 = r0 + warp * RB; i0 < r1; i0 += LG_WARPS * RB) {
     double2 x[RB][PS];
     double yv[RB];
@@ -62,25 +62,39 @@ __global__ void __launch_bounds__(LG_THREADS, PS >= 8 ? 1 : 2) logit_grad_kernel
       }
       yv[rb] = ok ? __ldg(y + i) : 0.0;
     }
+    // eta of every row of the step (butterfly sums: every lane holds all of them); lane rb does
+    // row rb's scalar work (exp, division, log-likelihood) once, not the whole warp per row
+    double e[RB];
 #pragma unroll
     for (int rb = 0; rb < RB; ++rb) {
-      double e = 0.0;
+      double v = 0.0;
 #pragma unroll
-      for (int s = 0; s < PS; ++s) e = fma(b[s].x, x[rb][s].x, fma(b[s].y, x[rb][s].y, e));
+      for (int s = 0; s < PS; ++s) v = fma(b[s].x, x[rb][s].x, fma(b[s].y, x[rb][s].y, v));
 #pragma unroll
-      for (int o = 16; o >= 1; o >>= 1) e += __shfl_xor_sync(0xffffffffu, e, o);
-      if (i0 + rb < r1) {
-        const double mu = 1.0 / (1.0 + exp(-e));   // sigma(eta)
-        const double r = yv[rb] - mu;
+      for (int o = 16; o >= 1; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+      e[rb] = v;
+    }
+    double rmine = 0.0;
 #pragma unroll
-        for (int s = 0; s < PS; ++s) {
-          g[s].x = fma(r, x[rb][s].x, g[s].x);
-          g[s].y = fma(r, x[rb][s].y, g[s].y);
-        }
-        if (LL && lane == 0) ll += yv[rb] * e - softplus_dev(e);
+    for (int rb = 0; rb < RB; ++rb)
+      if (lane == rb && i0 + rb < r1) {
+        const double mu = 1.0 / (1.0 + exp(-e[rb]));   // sigma(eta)
+        rmine = yv[rb] - mu;
+        if (LL) ll += yv[rb] * e[rb] - softplus_dev(e[rb]);
+      }
+#pragma unroll
+    for (int rb = 0; rb < RB; ++rb) {
+      const double r = __shfl_sync(0xffffffffu, rmine, rb);   // 0 for rows past the segment
+#pragma unroll
+      for (int s = 0; s < PS; ++s) {
+        g[s].x = fma(r, x[rb][s].x, g[s].x);
+        g[s].y = fma(r, x[rb][s].y, g[s].y);
       }
     }
   }
+  // the log-likelihood terms sit on lanes 0 .. RB-1: fixed-order butterfly to every lane
+#pragma unroll
+  for (int o = 16; o >= 1; o >>= 1) ll += __shfl_xor_sync(0xffffffffu, ll, o);
   // per-CTA sum in warp order (deterministic), one warp at a time into shared memory
   for (int w = 0; w < LG_WARPS; ++w) {
     if (warp == w) {
