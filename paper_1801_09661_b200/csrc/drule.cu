@@ -12,9 +12,10 @@
 // (mma.sync m8n8k4 -> DMMA; tcgen05 has no f64 kind). B_t is symmetric, so only the tiles of the
 // upper block triangle are computed (the mirror tile is written transposed: the same products in
 // the same order, so the result stays bitwise symmetric), and both operands of a tile are row
-// panels of B_t (B_t[k][j] = B_t[j][k]) -> every global load is a contiguous 256-byte row segment.
-// The whole p x p working set (8 MB at p = 1000) stays in L2 between squarings; reads use
-// ld.global.cg because another SM wrote the data since this SM last looked. Traces are
+// panels of B_t (B_t[k][j] = B_t[j][k]) -> every global load is a contiguous 256-byte row segment,
+// staged through a 4-deep cp.async ring of 32-column chunks (three chunks in flight hide the L2
+// latency). The whole p x p working set (8 MB at p = 1000) stays in L2 between squarings; B_t
+// (t >= 1) is read with cp.async.cg (L2 only) because another SM wrote it since this SM last looked. Traces are
 // per-diagonal-tile partial sums added in tile order (deterministic); one grid barrier
 // (wrap-safe counter) separates the squarings.
 #include <algorithm>
@@ -35,12 +36,12 @@ constexpr int DTHR = 256;       // 8 warps: 2 (rows of 32) x 4 (columns of 16)
 
 struct DRuleArgs {
   const double* G;   // [nU][p][p] normalised unit Grams (read only)
-  double* buf;       // [2][nU][p][p] B_1, B_2, ... ping-pong
+  double* buf;       // [2][nU][p][pb] B_1, B_2, ... ping-pong (pb = p rounded up to even)
   double* tr;        // [S+1][nU][nb] partial traces of B_t per diagonal block
   double* gsl;       // [nU][nb] Gershgorin: max row abs-sum per row block
   unsigned* bar;     // grid barrier counter (zero at launch)
   double* d_out;     // [nU]
-  int p, nU, nb, ntile, S;
+  int p, pb, nU, nb, ntile, S;   // pb: even row pitch of buf
 };
 
 __device__ __forceinline__ unsigned ld_acquire_u32(const unsigned* a) {
@@ -69,15 +70,25 @@ __device__ __forceinline__ void tile_ij(int t, int nb, int& bi, int& bj) {
   bj = i + t;
 }
 
-__device__ __forceinline__ double ldcg(const double* a, bool cg) { return cg ? __ldcg(a) : __ldg(a); }
+__device__ __forceinline__ void cp_async_ca8(double* dst, const double* src) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"(smem_u32(dst)), "l"(src) : "memory");
+}
+__device__ __forceinline__ void cp_async_cg16(double* dst, const double* src) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_u32(dst)), "l"(src) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
+
+constexpr int DNS = 4;                       // k-chunks in flight (cp.async ring)
+constexpr int DSTAGE = 2 * DT * DPITCH;      // doubles per ring stage (A and B panels)
 
 __global__ void __launch_bounds__(DTHR, 1) drule_kernel(const DRuleArgs A) {
-  __shared__ __align__(16) double As[DT * DPITCH];
-  __shared__ __align__(16) double Bs[DT * DPITCH];
+  extern __shared__ __align__(16) double dsm[];   // [DNS][2][DT][DPITCH]
   __shared__ double red[DTHR / 32];
   __shared__ double diag[DT];
-  const int p = A.p, nb = A.nb, tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-  const size_t pp = (size_t)p * p;
+  const int p = A.p, nb = A.nb, pb = A.pb, tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const size_t pp = (size_t)p * p, ppb = (size_t)p * pb;
   unsigned phase = 0;
 
   // ---- phase 0: Gershgorin row sums and the trace of B_0 = G, per (unit, row block)
@@ -86,8 +97,16 @@ __global__ void __launch_bounds__(DTHR, 1) drule_kernel(const DRuleArgs A) {
     const double* Gu = A.G + (size_t)u * pp;
     double gm = 0.0, tr = 0.0;
     for (int r = bi * DT + warp; r < min(p, (bi + 1) * DT); r += DTHR / 32) {
-      double s = 0.0;
-      for (int k = lane; k < p; k += 32) s += fabs(Gu[(size_t)r * p + k]);
+      double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;   // four loads in flight
+      int k = lane;
+      for (; k + 96 < p; k += 128) {
+        s0 += fabs(Gu[(size_t)r * p + k]);
+        s1 += fabs(Gu[(size_t)r * p + k + 32]);
+        s2 += fabs(Gu[(size_t)r * p + k + 64]);
+        s3 += fabs(Gu[(size_t)r * p + k + 96]);
+      }
+      for (; k < p; k += 32) s0 += fabs(Gu[(size_t)r * p + k]);
+      double s = (s0 + s1) + (s2 + s3);
 #pragma unroll
       for (int o = 16; o >= 1; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
       gm = fmax(gm, s);
@@ -107,10 +126,14 @@ __global__ void __launch_bounds__(DTHR, 1) drule_kernel(const DRuleArgs A) {
 
   // ---- phases 1..S: B_{t+1} = (B_t / s_t)^2 on the upper block triangle
   const int wr = warp >> 2, wc = warp & 3;
+  const int nch = (p + DK - 1) / DK;
   for (int t = 0; t < A.S; ++t) {
-    const bool cg = t > 0;  // B_0 = G was never written by this launch
-    const double* Bin = t == 0 ? A.G : A.buf + (size_t)((t - 1) & 1) * A.nU * pp;
-    double* Bout = A.buf + (size_t)(t & 1) * A.nU * pp;
+    // B_0 = G (pitch p, never written by this launch: 8-byte cp.async through L1); B_t, t >= 1,
+    // another SM wrote it since this SM last looked: 16-byte cp.async.cg (L2 only), even pitch pb
+    const bool first = t == 0;
+    const double* Bin = first ? A.G : A.buf + (size_t)((t - 1) & 1) * A.nU * ppb;
+    const int ldin = first ? p : pb;
+    double* Bout = A.buf + (size_t)(t & 1) * A.nU * ppb;
     for (int w = blockIdx.x; w < A.nU * A.ntile; w += gridDim.x) {
       const int u = w / A.ntile;
       int bi, bj;
@@ -118,34 +141,51 @@ __global__ void __launch_bounds__(DTHR, 1) drule_kernel(const DRuleArgs A) {
       double s = 0.0;
       for (int b = 0; b < nb; ++b) s += __ldcg(A.tr + ((size_t)t * A.nU + u) * nb + b);  // fixed order
       const double sc = s > 0.0 ? 1.0 / (s * s) : 0.0;
-      const double* Bu = Bin + (size_t)u * pp;
+      const double* Bu = Bin + (size_t)u * (first ? pp : ppb);
       const int r0 = bi * DT, c0 = bj * DT;
+      // stage chunk c (columns [c DK, c DK + DK)) of the row panels r0.. and c0.. into ring slot c % DNS
+      auto issue = [&](int c) {
+        if (c < nch) {
+          double* As = dsm + (size_t)(c % DNS) * DSTAGE;
+          double* Bs = As + DT * DPITCH;
+          const int k0 = c * DK;
+          if (first) {
+#pragma unroll
+            for (int i = 0; i < (DT * DK) / DTHR; ++i) {
+              const int e = tid + i * DTHR, r = e / DK, kk = k0 + e % DK;
+              double* da = As + r * DPITCH + e % DK;
+              double* db = Bs + r * DPITCH + e % DK;
+              if (r0 + r < p && kk < p) cp_async_ca8(da, Bu + (size_t)(r0 + r) * ldin + kk); else *da = 0.0;
+              if (c0 + r < p && kk < p) cp_async_ca8(db, Bu + (size_t)(c0 + r) * ldin + kk); else *db = 0.0;
+            }
+          } else {
+#pragma unroll
+            for (int i = 0; i < (DT * DK) / (2 * DTHR); ++i) {
+              const int e = 2 * (tid + i * DTHR), r = e / DK, kk = k0 + e % DK;   // column pairs
+              double* da = As + r * DPITCH + e % DK;
+              double* db = Bs + r * DPITCH + e % DK;
+              // kk even, pitch even: a pair never straddles the row; its second element may be the
+              // zero pad column p of an odd p (written by the epilogue)
+              if (r0 + r < p && kk < p) cp_async_cg16(da, Bu + (size_t)(r0 + r) * ldin + kk); else { da[0] = 0.0; da[1] = 0.0; }
+              if (c0 + r < p && kk < p) cp_async_cg16(db, Bu + (size_t)(c0 + r) * ldin + kk); else { db[0] = 0.0; db[1] = 0.0; }
+            }
+          }
+        }
+        cp_async_commit();   // one group per chunk index (empty past the end: uniform counting)
+      };
       double acc[4][2][2];
 #pragma unroll
       for (int i = 0; i < 4; ++i)
 #pragma unroll
         for (int j = 0; j < 2; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
-      // register-staged prefetch of the next k-chunk (8 + 8 doubles per thread)
-      double ra[8], rb[8];
-      auto fetch = [&](int k0) {
 #pragma unroll
-        for (int i = 0; i < 8; ++i) {
-          const int e = tid + i * DTHR, r = e / DK, kk = k0 + e % DK;
-          ra[i] = (r0 + r < p && kk < p) ? ldcg(Bu + (size_t)(r0 + r) * p + kk, cg) : 0.0;
-          rb[i] = (c0 + r < p && kk < p) ? ldcg(Bu + (size_t)(c0 + r) * p + kk, cg) : 0.0;
-        }
-      };
-      fetch(0);
-      for (int k0 = 0; k0 < p; k0 += DK) {
-        __syncthreads();  // previous chunk's fragments consumed
-#pragma unroll
-        for (int i = 0; i < 8; ++i) {
-          const int e = tid + i * DTHR;
-          As[(e / DK) * DPITCH + e % DK] = ra[i];
-          Bs[(e / DK) * DPITCH + e % DK] = rb[i];
-        }
-        __syncthreads();
-        if (k0 + DK < p) fetch(k0 + DK);
+      for (int c = 0; c < DNS - 1; ++c) issue(c);
+      for (int c = 0; c < nch; ++c) {
+        issue(c + DNS - 1);
+        cp_async_wait<DNS - 1>();   // this thread's copies of chunk c have landed
+        __syncthreads();            // ... and every thread's
+        const double* As = dsm + (size_t)(c % DNS) * DSTAGE;
+        const double* Bs = As + DT * DPITCH;
 #pragma unroll
         for (int k4 = 0; k4 < DK; k4 += 4) {
           double a[4], b[2];
@@ -158,9 +198,12 @@ __global__ void __launch_bounds__(DTHR, 1) drule_kernel(const DRuleArgs A) {
 #pragma unroll
             for (int j = 0; j < 2; ++j) dmma_8x8x4(acc[i][j][0], acc[i][j][1], a[i], b[j]);
         }
+        __syncthreads();            // slot c % DNS is refilled by the next iteration's issue
       }
-      // epilogue: scale by 1/s_t^2, write the tile and (off the diagonal) its transpose
-      double* Ou = Bout + (size_t)u * pp;
+      cp_async_wait<0>();
+      // epilogue: scale by 1/s_t^2, write the tile and (off the diagonal) its transpose; the pad
+      // column p of an odd p is written as zero (the next squaring's 16-byte copies read it)
+      double* Ou = Bout + (size_t)u * ppb;
 #pragma unroll
       for (int i = 0; i < 4; ++i)
 #pragma unroll
@@ -170,8 +213,10 @@ __global__ void __launch_bounds__(DTHR, 1) drule_kernel(const DRuleArgs A) {
             const int r = wr * 32 + i * 8 + (lane >> 2), c = wc * 16 + j * 8 + 2 * (lane & 3) + e;
             const double v = acc[i][j][e] * sc;
             if (r0 + r < p && c0 + c < p) {
-              Ou[(size_t)(r0 + r) * p + c0 + c] = v;
-              if (bi != bj) Ou[(size_t)(c0 + c) * p + r0 + r] = v;
+              Ou[(size_t)(r0 + r) * pb + c0 + c] = v;
+              if (bi != bj) Ou[(size_t)(c0 + c) * pb + r0 + r] = v;
+            } else if (r0 + r < p && c0 + c == p && pb > p) {
+              Ou[(size_t)(r0 + r) * pb + p] = 0.0;
             }
             if (bi == bj && r == c) diag[r] = r0 + r < p ? v : 0.0;
           }
@@ -213,7 +258,8 @@ oem_status d_rule(oem_ctx* ctx, const double* Gn, int nU, int p, int S, double* 
   const size_t pp = (size_t)p * p;
   size_t off = 0;
   auto take = [&](size_t bytes) { size_t o = off; off += (bytes + 255) / 256 * 256; return o; };
-  const size_t o_buf = take(S > 0 ? sizeof(double) * 2 * (size_t)nU * pp : 8);
+  const int pb = p + (p & 1);
+  const size_t o_buf = take(S > 0 ? sizeof(double) * 2 * (size_t)nU * p * pb : 8);
   const size_t o_tr = take(sizeof(double) * (size_t)(S + 1) * nU * nb);
   const size_t o_gsl = take(sizeof(double) * (size_t)nU * nb);
   const size_t o_bar = take(sizeof(unsigned));
@@ -227,15 +273,17 @@ oem_status d_rule(oem_ctx* ctx, const double* Gn, int nU, int p, int S, double* 
   A.gsl = reinterpret_cast<double*>(base + o_gsl);
   A.bar = reinterpret_cast<unsigned*>(base + o_bar);
   A.d_out = d_out;
-  A.p = p; A.nU = nU; A.nb = nb; A.ntile = ntile; A.S = S;
+  A.p = p; A.pb = pb; A.nU = nU; A.nb = nb; A.ntile = ntile; A.S = S;
+  const size_t smem = sizeof(double) * (size_t)DNS * DSTAGE;
+  OEM_CUDA_TRY(cudaFuncSetAttribute(drule_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   int per_sm = 0;
-  OEM_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, drule_kernel, DTHR, 0));
+  OEM_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, drule_kernel, DTHR, smem));
   const int work = std::max(nU * ntile, nU * nb);
   const int grid = std::max(1, std::min(work, ctx->num_sms * std::max(1, per_sm)));
   void* args[] = {&A};
   PhaseTimer tm(ctx, PH_POWER, st);
   ++ctx->launches;
-  OEM_CUDA_TRY(cudaLaunchCooperativeKernel((const void*)drule_kernel, dim3(grid), dim3(DTHR), args, 0, st));
+  OEM_CUDA_TRY(cudaLaunchCooperativeKernel((const void*)drule_kernel, dim3(grid), dim3(DTHR), args, smem, st));
   return OEM_OK;
 }
 
