@@ -145,6 +145,7 @@ oem_status oem_ctx_destroy(oem_ctx* ctx) {
   ctx->drule_ws.release();
   ctx->wz.release();
   ctx->sparse_ws.release();
+  ctx->gram_acc.release();
   ctx->lg_part.release();
   ctx->lg_out.release();
   ctx->mom_part.release();

@@ -42,6 +42,7 @@ constexpr int BK = 32;      // rows per pipeline stage
 constexpr int MAXST = 6;    // max pipeline stages
 constexpr int NWC_MAX = 16; // consumer (MMA) warps per CTA: 16 for single-panel plans, 8 for two-panel ones
 __host__ __device__ constexpr int nwc_of(bool two) { return two ? 8 : 16; }
+constexpr int ORD_W = 2;    // ordered epilogue: interleaved accumulation chains per (fold, tile type)
 constexpr int NRW = 2;      // WEIGHTED: row warps (eta, mu, w, z per row, one stage ahead of the MMA warps)
 __host__ __device__ constexpr int gram_threads(int mode, bool two) { return (nwc_of(two) + (mode == 2 ? NRW : 0) + 1) * 32; }
 
@@ -102,6 +103,9 @@ struct GramParams {
   double eps;
   int want_scal;          // WEIGHTED: accumulate sum w and the log-likelihood (else zeros)
   double* partial;        // [nfold][nseg][nblk][64]
+  int ordered;            // 1: segments add into accum in segment order (no partial buffer)
+  unsigned* ticket;       // [ORD_W][U] next link of each chain allowed to add (zero at launch)
+  double* accum;          // [ORD_W][nblk][64]
   double* partial_scal;   // WEIGHTED: [nseg][2]
   const CtaDesc* ctas;
   const int32_t* blk_of;  // [nb*nb] -> packed upper block index
@@ -123,7 +127,18 @@ struct Cons {
   Job job;
   const double* beta_s;
   double* scal_s;     // WEIGHTED: [NRW][2] per-row-warp (sum w, loglik)
+  int njob;           // consumer warps with a job in this CTA
+  unsigned* done_s;   // ordered epilogue: warps of this CTA that have added their blocks
 };
+
+__device__ __forceinline__ unsigned ld_acquire_gpu(const unsigned* a) {
+  unsigned v;
+  asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(a) : "memory");
+  return v;
+}
+__device__ __forceinline__ void st_release_gpu(unsigned* a, unsigned v) {
+  asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(a), "r"(v) : "memory");
+}
 
 template <int MODE, int KIND>
 __device__ __forceinline__ void consume(const GramParams& P, const Cons& cs) {
@@ -183,6 +198,40 @@ __device__ __forceinline__ void consume(const GramParams& P, const Cons& cs) {
     __syncwarp();
     if (cs.lane == 0) mbar_arrive(&cs.empty[st]);
     if (++st == P.ST) { st = 0; ph ^= 1u; }
+  }
+  // epilogue, ordered plans: add this segment's blocks into the (fold, tile type)'s running sums
+  // after the previous segment's CTA of the same tile type has added its own (a ticket per
+  // (fold, tile type), released once every job warp of the CTA is done), so every entry is
+  // ((seg 0 + seg 1) + seg 2) + ... in segment order: deterministic, the same order as the
+  // partial-buffer reduction, without the partial buffer (L2 read-modify-writes, never HBM)
+  if (KIND != J_NONE && P.ordered) {
+    // ORD_W interleaved chains (segment s joins chain s % ORD_W as its (s / ORD_W)-th link): the
+    // CTAs of one tile type that run in the same wave are never neighbours in a chain
+    const int chain = cs.seg % ORD_W, link = cs.seg / ORD_W;
+    unsigned* tk = P.ticket + (size_t)chain * P.U + cs.u;   // ordered plans have one fold
+    if (lane == 0)
+      while (ld_acquire_gpu(tk) != (unsigned)link) __nanosleep(32);
+    __syncwarp();
+    double* out = P.accum + (size_t)chain * P.nblk * 64;
+#pragma unroll
+    for (int r = 0; r < R; ++r)
+#pragma unroll
+      for (int c = 0; c < C; ++c)
+        if (kind_active(KIND, r, c)) {
+          const int idx = P.blk_of[(cs.job.bi0 + r) * P.nb + cs.job.bj0 + c];
+          double2* o = reinterpret_cast<double2*>(out + (size_t)idx * 64 + (lane >> 2) * 8 + 2 * (lane & 3));
+          double2 v = make_double2(acc[r][c][0], acc[r][c][1]);
+          if (link > 0) {   // L2 only: the previous link was added by another SM
+            const double2 prev = __ldcg(o);
+            v.x = prev.x + v.x;
+            v.y = prev.y + v.y;
+          }
+          __stcg(o, v);
+        }
+    __threadfence();
+    __syncwarp();
+    if (lane == 0 && atomicAdd(cs.done_s, 1u) == (unsigned)cs.njob - 1u) st_release_gpu(tk, (unsigned)link + 1u);
+    return;
   }
   // epilogue: this (fold, segment)'s partial blocks
   if (KIND != J_NONE) {
@@ -386,7 +435,9 @@ gram_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ CUt
   }
   __shared__ double scal_s[2 * NRW];
   __shared__ __align__(8) uint64_t ready_s[MAXST];
+  __shared__ unsigned done_s;
   Cons cs;
+  cs.done_s = &done_s;
   cs.scal_s = scal_s;
   cs.u = u;
   cs.seg = rest % P.nseg;
@@ -406,10 +457,12 @@ gram_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ CUt
   cs.b0 = cd->b0;
   cs.two = TWO && !cd->same;
   const int njob = cd->njob;
+  cs.njob = njob;
   const int nconsumers = njob + (MODE == MODE_WEIGHTED ? NRW : 0);  // arrivals per stage release
   const int full_count = P.ytma ? 1 : 32;
 
   if (threadIdx.x == 0) {
+    done_s = 0u;
     for (int s = 0; s < P.ST; ++s) {
       mbar_init(&cs.full[s], full_count);
       mbar_init(&cs.empty[s], nconsumers);
@@ -599,7 +652,7 @@ __global__ void gram_unpack_kernel(const double* __restrict__ packed, int nfold,
 
 // ------------------------------------------------------------------ host side: plans
 struct GramPlan {
-  int mode = 0, p = 0, nb = 0, ld = 0, two_panel = 0, U = 0, U_off = 0, nseg = 0, ST = 0, nblk = 0;
+  int mode = 0, p = 0, nb = 0, ld = 0, two_panel = 0, U = 0, U_off = 0, nseg = 0, ST = 0, nblk = 0, ordered = 0;
   int64_t seg_rows = 0;
   size_t smem = 0;
   int stage_doubles = 0, ys_off = 0, ystride = 1, ytma = 1;
@@ -745,14 +798,21 @@ static oem_status build_plan(oem_ctx* ctx, int mode, int p, int64_t nrows, int K
     }
   }
   pl.U = (int)pl.ctas.size();
-  // Two-panel plans dispatch the costlier off-diagonal tiles first (U_off). The L2-friendly
-  // alternative - many short segments, segment-major, every tile of a segment dispatched together
-  // (OEM_GRAM_LPT=0 OEM_GRAM_WAVES=384) - cuts cfg4's DRAM reads from 350-404 GB to 98 GB
-  // (algorithmic 80 GB; L2 hit rate 44% -> 77%) at the same kernel time (288.3 ms) but adds 1 ms
-  // to the split-n reduction (6.4 GB of partial blocks): the kernel is DMMA-bound with HBM at
-  // ~19% of its peak, so the re-reads cost no time.
+  // Two-panel plans dispatch the costlier off-diagonal tiles first (U_off), in up to 48 waves of
+  // long segments whose partial blocks a fixed-order kernel sums. DRAM traffic studies at cfg4
+  // (profiles/cfg4_l2_schedule_r02.md; the kernel is DMMA-bound with HBM at ~20% of its peak, so
+  // re-reads cost no time): this default reads X 4.6x from DRAM (372 GB) at 288.3 ms; 384 waves of
+  // short segments, segment-major, every tile type of a segment together (OEM_GRAM_LPT=0
+  // OEM_GRAM_WAVES=384) read 97.6 GB (1.22x) at the same kernel time but add 1.4 ms of reduction
+  // (6.4 GB of partial blocks); the same schedule with the segments added in order into running
+  // sums inside the kernel (OEM_GRAM_ORDERED=1: no partial blocks) reads 102.7 GB but runs
+  // 294.9 ms. The default keeps the fastest Gram phase.
+  const char* ordv = std::getenv("OEM_GRAM_ORDERED");
+  // (plain and WZ passes only: a fold pass splits every segment into K items whose same-tile
+  // neighbours run in the same wave; cfg3 went 74.5 -> 124.5 ms ordered)
+  pl.ordered = (pl.two_panel && mode != MODE_FOLD && ordv && ordv[0] == '1') ? 1 : 0;
   const char* lpt = std::getenv("OEM_GRAM_LPT");  // developer override (timing studies): 0 / 1
-  const bool use_lpt = lpt ? lpt[0] == '1' : true;
+  const bool use_lpt = lpt ? lpt[0] == '1' : !pl.ordered;
   if (!pl.two_panel || pl.U_off == 0 || !use_lpt) pl.U_off = pl.U;
   // y staging: 1D TMA box (PLAIN/WEIGHTED); FOLD: 2D box [BK][Kpad] over y viewed as [nq][K]
   // (needs K*8 % 16 == 0, i.e. even K), else the producer's lanes load it
@@ -788,7 +848,7 @@ static oem_status build_plan(oem_ctx* ctx, int mode, int p, int64_t nrows, int K
   // smaller split-n reduction, fewer pipeline fills. Measured (whole call): cfg2 4 waves 0.396 ms,
   // 2 waves 0.390, 1 wave 0.382; cfg5 weighted pass 33 waves 8.42 ms, 8 waves 8.19, 2 waves 8.16;
   // two-panel plans need many waves to balance their unequal tiles (cfg4: 8 waves 301 ms, 48: 288)
-  const double w_fit = std::min(pl.two_panel ? 48.0 : 2.0, (double)units / 64.0 / per_wave);
+  const double w_fit = std::min(pl.ordered ? 384.0 : pl.two_panel ? 48.0 : 2.0, (double)units / 64.0 / per_wave);
   const int waves = wv ? std::max(1, std::atoi(wv)) : std::max(1, (int)std::ceil(w_fit));
   int64_t want = std::max<int64_t>(1, (int64_t)std::llround(waves * per_wave));
   want = std::min<int64_t>(want, std::max<int64_t>(1, units / 8));
@@ -887,8 +947,18 @@ oem_status gram_pass(oem_ctx* ctx, int mode, const double* X, const double* y, c
     ctx->plans[key] = plp;
   }
   const GramPlan& pl = *plp;
-  const size_t part_bytes = sizeof(double) * (size_t)nfold * pl.nseg * pl.nblk * 64;
-  OEM_CUDA_TRY(ctx->partial.ensure(part_bytes));
+  double* accum = nullptr;
+  unsigned* ticket = nullptr;
+  if (pl.ordered) {   // running sums [ORD_W][nblk][64] + tickets [ORD_W][U] (one fold)
+    const size_t acc_bytes = sizeof(double) * (size_t)ORD_W * pl.nblk * 64;
+    OEM_CUDA_TRY(ctx->gram_acc.ensure(acc_bytes + sizeof(unsigned) * (size_t)ORD_W * pl.U + 256));
+    accum = ctx->gram_acc.as<double>();
+    ticket = reinterpret_cast<unsigned*>(ctx->gram_acc.as<char>() + (acc_bytes + 255) / 256 * 256);
+    OEM_CUDA_TRY(cudaMemsetAsync(ticket, 0, sizeof(unsigned) * (size_t)ORD_W * pl.U, st));
+  } else {
+    const size_t part_bytes = sizeof(double) * (size_t)nfold * pl.nseg * pl.nblk * 64;
+    OEM_CUDA_TRY(ctx->partial.ensure(part_bytes));
+  }
   OEM_CUDA_TRY(ctx->partial_scal.ensure(sizeof(double) * 2 * (size_t)pl.nseg + 16));
   double* tail = nullptr;
   if (mode == MODE_FOLD && n_local % K != 0) {
@@ -962,6 +1032,9 @@ oem_status gram_pass(oem_ctx* ctx, int mode, const double* X, const double* y, c
     P.ytma = pl.ytma; P.ystride = pl.ystride;
     P.y = y; P.beta = beta; P.eps = eps; P.want_scal = want_scal;
     P.partial = ctx->partial.as<double>();
+    P.ordered = pl.ordered;
+    P.ticket = ticket;
+    P.accum = accum;
     P.partial_scal = ctx->partial_scal.as<double>();
     P.ctas = pl.d_ctas; P.blk_of = pl.d_blk_of;
     P.xbox_bytes = (uint32_t)(BK * pl.ld * 8);
@@ -990,9 +1063,10 @@ oem_status gram_pass(oem_ctx* ctx, int mode, const double* X, const double* y, c
     OEM_CUDA_TRY(cudaGetLastError());
   }
   {
-    const double* src = ctx->partial.as<double>();
+    const double* src = pl.ordered ? accum : ctx->partial.as<double>();
     const double* sscal = ctx->partial_scal.as<double>();
-    int nseg = nq > 0 ? pl.nseg : 0;
+    // ordered plans: the segments are already summed into min(ORD_W, nseg) chains
+    int nseg = nq > 0 ? (pl.ordered ? std::min(ORD_W, pl.nseg) : pl.nseg) : 0;
     if (nseg > 64) {  // two-level: chunks of `per` segments in parallel, then the final sum
       const int per = 16, S = (nseg + per - 1) / per;
       OEM_CUDA_TRY(ctx->partial2.ensure(sizeof(double) * (size_t)nfold * S * pl.nblk * 64 + sizeof(double) * (2 * S + 16)));

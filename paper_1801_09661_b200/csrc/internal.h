@@ -57,7 +57,7 @@ struct oem_ctx {
   int nranks = 1, rank = 0;
   int num_sms = 148;
   void* nccl_comm = nullptr;  // ncclComm_t
-  oem::DevBuf partial, partial2, counts_dev, partial_scal, packed, tail, plan_tables, path_ws, path_small, logi, lg_part, lg_out, mom_part, mom_out, stage0, stage1, drule_ws, wz, sparse_ws;
+  oem::DevBuf partial, partial2, counts_dev, partial_scal, packed, tail, plan_tables, path_ws, path_small, logi, lg_part, lg_out, mom_part, mom_out, stage0, stage1, drule_ws, wz, sparse_ws, gram_acc;
   cudaStream_t copy_stream = nullptr;  // f4 host streaming: H2D copies overlap the Gram kernel
   cudaEvent_t ev_copied[2] = {nullptr, nullptr}, ev_used[2] = {nullptr, nullptr};
   std::map<std::tuple<int, int, int64_t, int>, std::shared_ptr<oem::GramPlan>> plans;
