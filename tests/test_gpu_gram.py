@@ -407,3 +407,31 @@ def test_weighted_two_panel_zero_beta_exact(ctx):
     assert np.array_equal(Gw.cpu().numpy(), Go)
     assert np.array_equal(cw.cpu().numpy(), co)
     assert float(sc[0]) == sco[0]
+
+
+@pytest.mark.parametrize("sched", ["OEM_GRAM_ORDERED=1", "OEM_GRAM_LPT=0 OEM_GRAM_WAVES=384"])
+def test_alternative_two_panel_schedules(sched, monkeypatch):
+    """The DRAM-traffic schedules of profiles/cfg4_l2_schedule_r02.md (ordered in-kernel running
+    sums; short segment-major segments): integer data stays bit-exact against the oracle in the
+    plain pass, and the weighted (WZ) pass matches the oracle at 1e-12, with many segments."""
+    from paper_1801_09661_b200 import Context, oem_gram, oem_gram_weighted
+    for kv in sched.split():
+        k, v = kv.split("=")
+        monkeypatch.setenv(k, v)
+    c = Context(0)   # fresh context: plans are built (and the schedule read) per context
+    try:
+        X, y = int_design(21, 70_001, 300)
+        G, xty, yy, nt = oem_gram(c, to_dev(X), to_dev(y))
+        Go, co, yyo = orc.gram(X, y)
+        assert np.array_equal(G.cpu().numpy(), Go) and np.array_equal(xty.cpu().numpy(), co) and float(yy) == yyo
+        spec = CONFIGS["cfg5"].spec.replace(n=30_011, p=260, nnz=10)
+        bt = dg.beta(spec)
+        Xd, yd = device_rows(spec, bt)
+        Xh, yh = dg.rows_host(spec, bt)
+        beta = 0.6 * bt
+        Gw, cw, sc = oem_gram_weighted(c, Xd, yd, to_dev(beta))
+        Gwo, cwo, sco = orc.gram_weighted(Xh, yh, beta)
+        assert scale_err(Gw.cpu().numpy(), Gwo) <= 1e-12
+        assert abs(float(sc[0]) - sco[0]) <= 1e-12 * sco[0]
+    finally:
+        c.close()

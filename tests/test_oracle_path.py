@@ -337,6 +337,52 @@ def test_logistic_kkt_and_null_fixed_point():
         assert np.all(mu * (1 - mu) <= 0.25)
 
 
+def test_logistic_group_lasso_kkt():
+    """O7 with the group lasso (P:L1146-1148 fits group penalties to logistic models): at every
+    lambda the logistic group-lasso subgradient conditions hold, ||(1/n) X_g^T (y - mu)|| <=
+    lambda c_g on zero groups and (1/n) X_g^T (y - mu) = lambda c_g b_g / ||b_g|| on the others,
+    with c_g = sqrt(|g|) (R#12); beta = 0 at lambda_max = max_g ||c_g|| / c_g (R#14)."""
+    X, y = logistic_data(24, 3000, 12)
+    n, p = X.shape
+    grp = (np.arange(p) // 3).astype(np.int32)
+    _, cw0, _ = orc.gram_weighted(X, y, np.zeros(p))
+    lmax = orc.lambda_max("grp_lasso", cw0 / n, group=grp)
+    lams = orc.lambda_grid(lmax, 10, 1e-2)
+    B, oi, ii, cv = orc.logistic_path(X, y, lams, family="grp_lasso", group=grp)
+    assert cv.all() and not B[0].any()
+    for b, l in zip(B, lams):
+        gr = X.T @ (y - 1 / (1 + np.exp(-(X @ b)))) / n
+        for g in range(p // 3):
+            idx = grp == g
+            nb = np.linalg.norm(b[idx])
+            if nb == 0:
+                assert np.linalg.norm(gr[idx]) <= l * np.sqrt(3) * (1 + 1e-6) + 1e-9
+            else:
+                assert np.max(np.abs(gr[idx] - l * np.sqrt(3) * b[idx] / nb)) <= 1e-7
+
+
+def test_logistic_enet_kkt_and_mcp_scad_limits():
+    """O7 with the elastic net: (1/n) X^T (y - mu) - lambda (1 - alpha) b = lambda alpha sign(b) on
+    the support, |.| <= lambda alpha off it. MCP and SCAD: below their flat zone (|b_j| > gamma
+    lambda, resp. > gamma lambda for SCAD) the penalty's derivative vanishes, so at a tiny lambda
+    every coefficient is unpenalised and the path point is the Newton-Raphson MLE."""
+    X, y = logistic_data(25, 2500, 5)
+    n = X.shape[0]
+    lams = [0.02, 0.005]
+    B, oi, ii, cv = orc.logistic_path(X, y, lams, family="enet", alpha=0.5)
+    assert cv.all()
+    for b, l in zip(B, lams):
+        gr = X.T @ (y - 1 / (1 + np.exp(-(X @ b)))) / n
+        nz = b != 0
+        assert np.all(np.abs(gr[~nz]) <= 0.5 * l + 1e-7)
+        assert np.all(np.abs(gr[nz] - 0.5 * l * b[nz] - 0.5 * l * np.sign(b[nz])) <= 1e-7)
+    mle = newton_mle(X, y)
+    for fam, gam in (("mcp", 3.0), ("scad", 3.7)):
+        lam = 0.1 * np.min(np.abs(mle)) / gam
+        B, oi, ii, cv = orc.logistic_path(X, y, [lam], family=fam, gamma=gam, tol_out=1e-12)
+        assert cv.all() and np.max(np.abs(B[0] - mle)) <= 1e-8, fam
+
+
 # ---------------------------------------------------------------- f1 upper-bound logistic oracle
 def test_logit_grad_zero_beta_exact():
     """beta = 0: mu = 1/2, g = X^T (y - 1/2) exactly on integer X (all partial sums are exact)."""
