@@ -29,7 +29,8 @@ namespace oem {
 
 namespace {
 
-constexpr int DT = 64;          // output tile (rows and columns)
+// output tiles of DT x DT (64, or 32 for small problems: more CTAs share a squaring, since one
+// SM's FP64 rate, ~250 GFLOP/s, bounds a tile's time)
 constexpr int DK = 32;          // k-chunk staged in shared memory
 constexpr int DPITCH = DK + 4;  // smem row pitch (doubles): 2 wavefronts per 8-byte fragment load
 constexpr int DTHR = 256;       // 8 warps: 2 (rows of 32) x 4 (columns of 16)
@@ -50,14 +51,15 @@ __device__ __forceinline__ unsigned ld_acquire_u32(const unsigned* a) {
   return v;
 }
 
-// all CTAs of the (co-resident) grid; `target` = phase * gridDim.x, compared wrap-safe
+// all CTAs of the (co-resident) grid; `target` = phase * gridDim.x, compared wrap-safe. The
+// CTA barrier orders the CTA's writes before thread 0's release add (cumulative), the acquire
+// poll orders the other CTAs' writes before the closing CTA barrier: no sequentially consistent
+// fences (a fence.sc per CTA per squaring cost ~10 us at p = 200)
 __device__ __forceinline__ void grid_sync(unsigned* bar, unsigned target) {
   __syncthreads();
   if (threadIdx.x == 0) {
-    __threadfence();
     asm volatile("red.release.gpu.global.add.u32 [%0], %1;" ::"l"(bar), "r"(1u) : "memory");
-    while ((int)(ld_acquire_u32(bar) - target) < 0) __nanosleep(32);
-    __threadfence();
+    while ((int)(ld_acquire_u32(bar) - target) < 0) {}
   }
   __syncthreads();
 }
@@ -81,9 +83,10 @@ template <int N>
 __device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
 
 constexpr int DNS = 4;                       // k-chunks in flight (cp.async ring)
-constexpr int DSTAGE = 2 * DT * DPITCH;      // doubles per ring stage (A and B panels)
-
+template <int DT>
 __global__ void __launch_bounds__(DTHR, 1) drule_kernel(const DRuleArgs A) {
+  constexpr int DSTAGE = 2 * DT * DPITCH;      // doubles per ring stage (A and B panels)
+  constexpr int MT = DT / 16, NT = DT / 32;    // 8x8 output blocks per warp: MT rows x NT columns
   extern __shared__ __align__(16) double dsm[];   // [DNS][2][DT][DPITCH]
   __shared__ double red[DTHR / 32];
   __shared__ double diag[DT];
@@ -125,7 +128,7 @@ __global__ void __launch_bounds__(DTHR, 1) drule_kernel(const DRuleArgs A) {
   grid_sync(A.bar, ++phase * gridDim.x);
 
   // ---- phases 1..S: B_{t+1} = (B_t / s_t)^2 on the upper block triangle
-  const int wr = warp >> 2, wc = warp & 3;
+  const int wr = warp >> 2, wc = warp & 3;   // warp tile: rows wr DT/2 + [0, DT/2), columns wc DT/4 + [0, DT/4)
   const int nch = (p + DK - 1) / DK;
   for (int t = 0; t < A.S; ++t) {
     // B_0 = G (pitch p, never written by this launch: 8-byte cp.async through L1); B_t, t >= 1,
@@ -173,11 +176,11 @@ __global__ void __launch_bounds__(DTHR, 1) drule_kernel(const DRuleArgs A) {
         }
         cp_async_commit();   // one group per chunk index (empty past the end: uniform counting)
       };
-      double acc[4][2][2];
+      double acc[MT][NT][2];
 #pragma unroll
-      for (int i = 0; i < 4; ++i)
+      for (int i = 0; i < MT; ++i)
 #pragma unroll
-        for (int j = 0; j < 2; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
+        for (int j = 0; j < NT; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
 #pragma unroll
       for (int c = 0; c < DNS - 1; ++c) issue(c);
       for (int c = 0; c < nch; ++c) {
@@ -188,15 +191,15 @@ __global__ void __launch_bounds__(DTHR, 1) drule_kernel(const DRuleArgs A) {
         const double* Bs = As + DT * DPITCH;
 #pragma unroll
         for (int k4 = 0; k4 < DK; k4 += 4) {
-          double a[4], b[2];
+          double a[MT], b[NT];
 #pragma unroll
-          for (int i = 0; i < 4; ++i) a[i] = As[(wr * 32 + i * 8 + (lane >> 2)) * DPITCH + k4 + (lane & 3)];
+          for (int i = 0; i < MT; ++i) a[i] = As[(wr * (DT / 2) + i * 8 + (lane >> 2)) * DPITCH + k4 + (lane & 3)];
 #pragma unroll
-          for (int j = 0; j < 2; ++j) b[j] = Bs[(wc * 16 + j * 8 + (lane >> 2)) * DPITCH + k4 + (lane & 3)];
+          for (int j = 0; j < NT; ++j) b[j] = Bs[(wc * (DT / 4) + j * 8 + (lane >> 2)) * DPITCH + k4 + (lane & 3)];
 #pragma unroll
-          for (int i = 0; i < 4; ++i)
+          for (int i = 0; i < MT; ++i)
 #pragma unroll
-            for (int j = 0; j < 2; ++j) dmma_8x8x4(acc[i][j][0], acc[i][j][1], a[i], b[j]);
+            for (int j = 0; j < NT; ++j) dmma_8x8x4(acc[i][j][0], acc[i][j][1], a[i], b[j]);
         }
         __syncthreads();            // slot c % DNS is refilled by the next iteration's issue
       }
@@ -205,12 +208,12 @@ __global__ void __launch_bounds__(DTHR, 1) drule_kernel(const DRuleArgs A) {
       // column p of an odd p is written as zero (the next squaring's 16-byte copies read it)
       double* Ou = Bout + (size_t)u * ppb;
 #pragma unroll
-      for (int i = 0; i < 4; ++i)
+      for (int i = 0; i < MT; ++i)
 #pragma unroll
-        for (int j = 0; j < 2; ++j)
+        for (int j = 0; j < NT; ++j)
 #pragma unroll
           for (int e = 0; e < 2; ++e) {
-            const int r = wr * 32 + i * 8 + (lane >> 2), c = wc * 16 + j * 8 + 2 * (lane & 3) + e;
+            const int r = wr * (DT / 2) + i * 8 + (lane >> 2), c = wc * (DT / 4) + j * 8 + 2 * (lane & 3) + e;
             const double v = acc[i][j][e] * sc;
             if (r0 + r < p && c0 + c < p) {
               Ou[(size_t)(r0 + r) * pb + c0 + c] = v;
@@ -253,6 +256,9 @@ __global__ void __launch_bounds__(DTHR, 1) drule_kernel(const DRuleArgs A) {
 
 oem_status d_rule(oem_ctx* ctx, const double* Gn, int nU, int p, int S, double* d_out, cudaStream_t st) {
   if (S < 0 || S > 60) OEM_FAIL(OEM_ERR_INVALID_ARG, "d rule: need 0 <= squarings <= 60");
+  // 64-wide tiles unless they leave most SMs idle (one unit at p <= ~300: cfg5's inner solves)
+  const int nb64 = (p + 63) / 64;
+  const int DT = (int64_t)nU * nb64 * (nb64 + 1) / 2 * 4 <= ctx->num_sms ? 32 : 64;
   const int nb = (p + DT - 1) / DT;
   const int ntile = nb * (nb + 1) / 2;
   const size_t pp = (size_t)p * p;
@@ -274,16 +280,17 @@ oem_status d_rule(oem_ctx* ctx, const double* Gn, int nU, int p, int S, double* 
   A.bar = reinterpret_cast<unsigned*>(base + o_bar);
   A.d_out = d_out;
   A.p = p; A.pb = pb; A.nU = nU; A.nb = nb; A.ntile = ntile; A.S = S;
-  const size_t smem = sizeof(double) * (size_t)DNS * DSTAGE;
-  OEM_CUDA_TRY(cudaFuncSetAttribute(drule_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  const size_t smem = sizeof(double) * (size_t)DNS * 2 * DT * DPITCH;
+  const void* kern = DT == 32 ? (const void*)drule_kernel<32> : (const void*)drule_kernel<64>;
+  OEM_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   int per_sm = 0;
-  OEM_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, drule_kernel, DTHR, smem));
+  OEM_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, DTHR, smem));
   const int work = std::max(nU * ntile, nU * nb);
   const int grid = std::max(1, std::min(work, ctx->num_sms * std::max(1, per_sm)));
   void* args[] = {&A};
   PhaseTimer tm(ctx, PH_POWER, st);
   ++ctx->launches;
-  OEM_CUDA_TRY(cudaLaunchCooperativeKernel((const void*)drule_kernel, dim3(grid), dim3(DTHR), args, smem, st));
+  OEM_CUDA_TRY(cudaLaunchCooperativeKernel(kern, dim3(grid), dim3(DTHR), args, smem, st));
   return OEM_OK;
 }
 
