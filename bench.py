@@ -398,10 +398,11 @@ def main():
     per_launch_flops = (weighted_flops(nl, p) * sum(res.outer_iters)) if cfg.logistic else gram_flops(nl, p)
     achieved = per_launch_flops / (st["gram_ms"] / args.steps * 1e-3) / 1e12
     traffic = None
-    prof = os.path.join(ROOT, "profiles", "ncu_summary_r01.json")
+    prof = os.path.join(ROOT, "profiles", "ncu_summary_r02.json")   # one `ncu --set full` capture per kernel
     if os.path.exists(prof):
         try:
-            traffic = json.load(open(prof)).get(cfg.name, {}).get("dram_bytes_per_launch")
+            key = "sparse" if sparse else f"gram_{cfg.name}"
+            traffic = json.load(open(prof)).get(key, {}).get("dram_bytes_per_launch")
         except Exception:
             traffic = None
     if sparse:
