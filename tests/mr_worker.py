@@ -63,7 +63,13 @@ def main():
     Gw, cw, sw = oem_gram_weighted(ctx, Xd, y01, beta)
     fit = oem_fit_path(ctx, G, c, [n], [("lasso", 0, 1), ("mcp", 3, 1)], nlambda=12)
     cvf = oem_fit_path(ctx, Gk, ck, cnt, [("lasso", 0, 1)], nlambda=8, fold_mode=True)
-    mine = digest(G, c, yy, Gk, ck, yyk, Gw, cw, sw, fit.beta, fit.d, cvf.beta, cvf.d)
+    # the sparse pass over this rank's rows in CSR form (f4)
+    from paper_1801_09661_b200 import oem_gram_csr
+    sspec = CONFIGS["sparse"].spec.replace(n=40_007, p=96, nnz=8)
+    sbt = dg.beta(sspec)
+    rp, scol, sval, sy = dg.csr_cuda(sspec, sbt, r0, nl)
+    Gs, cs, yys, ns = oem_gram_csr(ctx, rp, scol, sval, sy, sspec.p)
+    mine = digest(G, c, yy, Gk, ck, yyk, Gw, cw, sw, fit.beta, fit.d, cvf.beta, cvf.d, Gs, cs, yys)
     digests = [None] * world
     if world > 1:
         dist.all_gather_object(digests, mine)
@@ -92,6 +98,10 @@ def main():
             lam = orc.lambda_grid(orc.lambda_max(fam, co / n), 12)
             B, it, cv = orc.oem_path(Go / n, co / n, d_ref, fam, lam, gamma, alpha)
             assert np.max(np.abs(fit.beta[0, q].cpu().numpy() - B)) <= 1e-8
+        Xs, yh = dg.rows_host(sspec, sbt)
+        Gso, cso, yyso = orc.gram(Xs, yh)
+        assert ns == sspec.n and scale_err(Gs.cpu().numpy(), Gso) <= 1e-12
+        assert xty_err(cs.cpu().numpy(), cso, Gso, yyso) <= 1e-12
         print(f"MR_WORKER_OK world={world} digest={mine[:16]}", flush=True)
     ctx.close()
     if world > 1:

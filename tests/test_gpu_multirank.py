@@ -69,6 +69,14 @@ def test_one_rank_communicator_is_bitwise_identity(ctxs):
     la = oem_fit_logistic(plain, Xd, y01, nlambda=4)
     lb = oem_fit_logistic(nccl, Xd, y01, nlambda=4)
     assert torch.equal(la.beta, lb.beta) and la.outer_iters == lb.outer_iters
+    from paper_1801_09661_b200 import oem_gram_csr
+    sspec = CONFIGS["sparse"].spec.replace(n=30_011)
+    rp, col, val, ys = dg.csr_cuda(sspec, dg.beta(sspec))
+    a = oem_gram_csr(plain, rp, col, val, ys, sspec.p)
+    b = oem_gram_csr(nccl, rp, col, val, ys, sspec.p)
+    assert a[3] == b[3] == sspec.n
+    for u, v in zip(a[:3], b[:3]):
+        assert torch.equal(u, v)
 
 
 def _free_port():
