@@ -670,7 +670,10 @@ struct GramPlan {
 
 // Spread jobs over CTA types (longest-processing-time first), then order each CTA's jobs so
 // the 4 SM sub-partitions (warp w -> SMSP w % 4) carry similar DMMA counts.
-static void pack_jobs(std::vector<Job>& jobs, int a0, int b0, int same, std::vector<CtaDesc>& out, int NWC) {
+// rw_bias: DMMA-block equivalents of row-warp work on SMSPs 0 and 1 (the weighted pass's two row
+// warps are warps 16 and 17 of the CTA), so the packer gives those sub-partitions less DMMA work
+static void pack_jobs(std::vector<Job>& jobs, int a0, int b0, int same, std::vector<CtaDesc>& out, int NWC,
+                      int rw_bias = 0) {
   std::sort(jobs.begin(), jobs.end(),
             [](const Job& x, const Job& y) { return kind_cost(x.kind) > kind_cost(y.kind); });
   const int U = std::max<int>(1, ((int)jobs.size() + NWC - 1) / NWC);
@@ -688,7 +691,7 @@ static void pack_jobs(std::vector<Job>& jobs, int a0, int b0, int same, std::vec
     std::memset(&cd, 0, sizeof(cd));
     cd.a0 = a0; cd.b0 = b0; cd.same = same;
     std::vector<std::vector<Job>> sub(4);
-    std::vector<int> sl(4, 0);
+    std::vector<int> sl{rw_bias, rw_bias, 0, 0};
     for (auto& j : bin) {  // already sorted by cost
       int best = -1;
       for (int q = 0; q < 4; ++q)
@@ -758,8 +761,17 @@ static oem_status build_plan(oem_ctx* ctx, int mode, int p, int64_t nrows, int K
     };
     std::vector<CtaDesc> c0, c1;
     auto j0 = tile(false), j1 = tile(true);
-    pack_jobs(j0, 0, 0, 1, c0, nwc_of(false));
-    pack_jobs(j1, 0, 0, 1, c1, nwc_of(false));
+    // the weighted pass's row warps (eta: p FMAs per row, exp, divisions) share sub-partitions 0
+    // and 1 with DMMA warps; counting them as ~0.07 p blocks of DMMA work when packing measured
+    // best (tools/rw_bias_sweep.sh, n = 5e6: p = 64 1.40 -> 1.37 ms, 100 2.52 -> 2.22, 150
+    // 4.42 -> 4.19, 200 8.21 -> 7.76, 247 18.4 -> 13.9; OEM_GRAM_RW_BIAS overrides)
+    int rw_bias = 0;
+    if (mode == MODE_WEIGHTED) {
+      const char* b = std::getenv("OEM_GRAM_RW_BIAS");
+      rw_bias = b ? std::atoi(b) : (int)std::lround(0.07 * p);
+    }
+    pack_jobs(j0, 0, 0, 1, c0, nwc_of(false), rw_bias);
+    pack_jobs(j1, 0, 0, 1, c1, nwc_of(false), rw_bias);
     pl.ctas = score(c1) < score(c0) ? c1 : c0;
   } else {
     pl.ld = 132;  // 128-column panel + 4 (mod 16 = 4)
