@@ -180,10 +180,17 @@ __device__ __forceinline__ void consume(const GramParams& P, const Cons& cs) {
         for (int r = 0; r < R; ++r) a[r] = pak[8 * r];
 #pragma unroll
         for (int c = 0; c < C; ++c) b[c] = pbk[8 * c];
-        if (MODE == MODE_WEIGHTED || MODE == MODE_WZ) {  // w_k scales row k (lane & 3) of the A fragments
+        if (MODE == MODE_WEIGHTED || MODE == MODE_WZ) {  // w_k scales row k (lane & 3) of one operand:
+          // the A fragments, or the B fragments when the job has fewer block columns than rows
+          // (both hold row k = lane & 3 of the stage; fewer DMULs on the DMMA warps)
           const double wk = MODE == MODE_WZ ? ys[2 * (ks * 4 + (lane & 3))] : ws[ks * 4 + (lane & 3)];
+          if (C < R) {
 #pragma unroll
-          for (int r = 0; r < R; ++r) a[r] *= wk;
+            for (int c = 0; c < C; ++c) b[c] *= wk;
+          } else {
+#pragma unroll
+            for (int r = 0; r < R; ++r) a[r] *= wk;
+          }
         }
 #pragma unroll
         for (int r = 0; r < R; ++r)
