@@ -772,11 +772,8 @@ static oem_status build_plan(oem_ctx* ctx, int mode, int p, int64_t nrows, int K
     // and 1 with DMMA warps; counting them as ~0.07 p blocks of DMMA work when packing measured
     // best (tools/rw_bias_sweep.sh, n = 5e6: p = 64 1.40 -> 1.37 ms, 100 2.52 -> 2.22, 150
     // 4.42 -> 4.19, 200 8.21 -> 7.76, 247 18.4 -> 13.9; OEM_GRAM_RW_BIAS overrides)
-    int rw_bias = 0;
-    if (mode == MODE_WEIGHTED) {
-      const char* b = std::getenv("OEM_GRAM_RW_BIAS");
-      rw_bias = b ? std::atoi(b) : (int)std::lround(0.07 * p);
-    }
+    const char* rwb = std::getenv("OEM_GRAM_RW_BIAS");
+    const int rw_bias = rwb ? std::atoi(rwb) : mode == MODE_WEIGHTED ? (int)std::lround(0.07 * p) : 0;
     pack_jobs(j0, 0, 0, 1, c0, nwc_of(false), rw_bias);
     pack_jobs(j1, 0, 0, 1, c1, nwc_of(false), rw_bias);
     pl.ctas = score(c1) < score(c0) ? c1 : c0;
