@@ -119,6 +119,13 @@ __global__ void __launch_bounds__(SP_THREADS, 1) sparse_gram_kernel(const SpPara
     int st = 0;
     uint32_t ph = 0;
     int64_t r = r0;
+    // row offsets of the next chunk's first row and of its full-size end, loaded one chunk ahead
+    // (their global-load latency overlaps the wait for a free stage)
+    int64_t pf_lo = 0, pf_hi = 0;
+    if (lane == 0 && r < r1) {
+      pf_lo = P.row_ptr[r];
+      pf_hi = P.row_ptr[r + (r1 - r < (int64_t)SP_ROWS ? r1 - r : (int64_t)SP_ROWS)];
+    }
     for (;;) {
       mbar_wait(&empty[st], ph ^ 1u);
       unsigned char* sb = sbytes + (size_t)st * P.sbytes;
@@ -126,9 +133,10 @@ __global__ void __launch_bounds__(SP_THREADS, 1) sparse_gram_kernel(const SpPara
       int64_t e0 = 0, e1 = 0;
       if (lane == 0 && r < r1) {
         // the largest R <= SP_ROWS whose nonzeros fit the stage (binary search on row_ptr)
-        int hi = (int)(r1 - r < (int64_t)SP_ROWS ? r1 - r : (int64_t)SP_ROWS);
-        e0 = P.row_ptr[r];
-        if (P.row_ptr[r + hi] - e0 <= SP_ENT) {
+        const int full_r = (int)(r1 - r < (int64_t)SP_ROWS ? r1 - r : (int64_t)SP_ROWS);
+        int hi = full_r;
+        e0 = pf_lo;
+        if (pf_hi - e0 <= SP_ENT) {
           R = hi;
         } else {
           int lo = 1;  // a single row always fits (p <= SP_ENT)
@@ -139,7 +147,13 @@ __global__ void __launch_bounds__(SP_THREADS, 1) sparse_gram_kernel(const SpPara
           }
           R = lo;
         }
-        e1 = P.row_ptr[r + R];
+        e1 = R == full_r ? pf_hi : P.row_ptr[r + R];
+        // prefetch the next chunk's bounds (it starts at r + R)
+        const int64_t rn = r + R;
+        if (rn < r1) {
+          pf_lo = e1;
+          pf_hi = P.row_ptr[rn + (r1 - rn < (int64_t)SP_ROWS ? r1 - rn : (int64_t)SP_ROWS)];
+        }
       }
       R = __shfl_sync(0xffffffffu, R, 0);
       e0 = __shfl_sync(0xffffffffu, e0, 0);
