@@ -13,6 +13,8 @@ ROOT = os.path.dirname(PKG)
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 NVFLAGS = ARCH + ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "--expt-relaxed-constexpr"]
+# developer hook (instrumented builds, e.g. -DSP_PROFILE); rebuild with force=True after changing it
+NVFLAGS += os.environ.get("OEM_NVCC_EXTRA", "").split()
 
 OEM_SRCS = ["api.cu", "gram.cu", "drule.cu", "path.cu", "logistic.cu", "cv.cu", "logit_ub.cu", "moments.cu", "stream.cu", "sparse.cu"]
 OEM_HDRS = ["common.cuh", "internal.h"]

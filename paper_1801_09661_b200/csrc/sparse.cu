@@ -55,7 +55,13 @@ struct SpStage {  // shared-memory layout of one ring stage (byte offsets); mask
   static constexpr int hdr = col + SP_ENT * 4;   // int R, pad, int64 e0, double yy (the chunk's y^T y)
   static constexpr int mask = (hdr + 32 + 127) / 128 * 128;
 };
-__host__ __device__ constexpr int stage_bytes(int ncol) { return SpStage::mask + (ncol * SP_MW * 4 + 127) / 128 * 128; }
+// The masks are stored word-major and, within a word, in OWNER order: column c is owned by
+// thread slot(c) = (c & ~255) | (c & 7) << 5 | (c & 255) >> 3 (warp c & 7, lane (c & 255) >> 3),
+// so the slice's columns spread over all 8 owner warps and an owner warp's 32 mask loads hit 32
+// banks; word w of column c sits at mask[w * mask_ld(ncol) + slot(c)].
+__host__ __device__ constexpr int mask_ld(int ncol) { return (ncol + SP_CT - 1) / SP_CT * SP_CT; }
+__device__ __forceinline__ int mask_slot(int c) { return (c & ~255) | ((c & 7) << 5) | ((c & 255) >> 3); }
+__host__ __device__ constexpr int stage_bytes(int ncol) { return SpStage::mask + (mask_ld(ncol) * SP_MW * 4 + 127) / 128 * 128; }
 
 struct SpParams {
   const int64_t* row_ptr;
@@ -70,6 +76,23 @@ struct SpParams {
   int sbytes;            // bytes per ring stage (mask columns of the widest slice)
   double* partial;       // [U][nseg][cap]
 };
+
+#ifdef SP_PROFILE
+// developer instrumentation: cycles each role spends waiting on its ring barrier vs in total (CTA 0)
+#define SP_WAIT(bar, par)                               \
+  do {                                                  \
+    const long long t_ = clock64();                     \
+    mbar_wait(bar, par);                                \
+    prof_wait += clock64() - t_;                        \
+  } while (0)
+#define SP_REPORT(role)                                                                              \
+  if (blockIdx.x == 0 && lane == 0)                                                                  \
+    printf("SP_PROFILE %s warp %d wait %lld total %lld chunks %d\n", role, warp, prof_wait,          \
+           clock64() - prof_t0, prof_chunks)
+#else
+#define SP_WAIT(bar, par) mbar_wait(bar, par)
+#define SP_REPORT(role)
+#endif
 
 __device__ __forceinline__ int64_t tri_off(int64_t j, int64_t pa) { return j * pa - j * (j - 1) / 2; }  // packed index of (j, j)
 
@@ -92,17 +115,21 @@ __global__ void __launch_bounds__(SP_THREADS, 1) sparse_gram_kernel(const SpPara
   extern __shared__ __align__(128) unsigned char sbytes[];
   __shared__ __align__(8) uint64_t full[SP_ST], ready[SP_ST], empty[SP_ST];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+#ifdef SP_PROFILE
+  long long prof_wait = 0, prof_t0 = clock64();
+  int prof_chunks = 0;
+#endif
   const int u = blockIdx.x % P.U, seg = blockIdx.x / P.U;
   const int p = P.p;
   const int64_t pa = p + 1;
   const int64_t r0 = (int64_t)seg * P.seg_rows, r1 = min(P.n, r0 + P.seg_rows);
-  const int J0 = P.slice_j0[u], J1 = P.slice_j0[u + 1], ncol = J1 - J0;
+  const int J0 = P.slice_j0[u], J1 = P.slice_j0[u + 1], ncol = J1 - J0, mld = mask_ld(ncol);
   const int64_t base = tri_off(J0, pa), nent = tri_off(J1, pa) - base;
   double* gs = reinterpret_cast<double*>(sbytes + (size_t)SP_ST * P.sbytes);
   for (int64_t e = threadIdx.x; e < nent; e += SP_THREADS) gs[e] = 0.0;
   for (int s = 0; s < SP_ST; ++s) {
     uint32_t* m = reinterpret_cast<uint32_t*>(sbytes + (size_t)s * P.sbytes + SpStage::mask);
-    for (int e = threadIdx.x; e < ncol * SP_MW; e += SP_THREADS) m[e] = 0u;
+    for (int e = threadIdx.x; e < mask_ld(ncol) * SP_MW; e += SP_THREADS) m[e] = 0u;
   }
   if (threadIdx.x == 0) {
     for (int s = 0; s < SP_ST; ++s) {
@@ -127,7 +154,7 @@ __global__ void __launch_bounds__(SP_THREADS, 1) sparse_gram_kernel(const SpPara
       pf_hi = P.row_ptr[r + (r1 - r < (int64_t)SP_ROWS ? r1 - r : (int64_t)SP_ROWS)];
     }
     for (;;) {
-      mbar_wait(&empty[st], ph ^ 1u);
+      SP_WAIT(&empty[st], ph ^ 1u);
       unsigned char* sb = sbytes + (size_t)st * P.sbytes;
       int R = 0;
       int64_t e0 = 0, e1 = 0;
@@ -179,7 +206,11 @@ __global__ void __launch_bounds__(SP_THREADS, 1) sparse_gram_kernel(const SpPara
       if (++st == SP_ST) { st = 0; ph ^= 1u; }
       if (R == 0) break;  // the terminating (empty) stage has been published
       r += R;
+#ifdef SP_PROFILE
+      ++prof_chunks;
+#endif
     }
+    SP_REPORT("producer");
     return;
   }
 
@@ -188,7 +219,7 @@ __global__ void __launch_bounds__(SP_THREADS, 1) sparse_gram_kernel(const SpPara
     int st = 0;
     uint32_t ph = 0;
     for (;;) {
-      mbar_wait(&full[st], ph);
+      SP_WAIT(&full[st], ph);
       unsigned char* sb = sbytes + (size_t)st * P.sbytes;
       int* h = reinterpret_cast<int*>(sb + SpStage::hdr);
       const int R = h[0];
@@ -202,7 +233,7 @@ __global__ void __launch_bounds__(SP_THREADS, 1) sparse_gram_kernel(const SpPara
         const int a0 = (int)(rp_s[q] - e0), a1 = (int)(rp_s[q + 1] - e0);
         for (int a = a0; a < a1; ++a) {
           const int c = c_s[a] - J0;
-          if (c >= 0 && c < ncol) atomicOr(&mask[c * SP_MW + (q >> 5)], 1u << (q & 31));
+          if (c >= 0 && c < ncol) atomicOr(&mask[(q >> 5) * mld + mask_slot(c)], 1u << (q & 31));
         }
         yy = fma(y_s[q], y_s[q], yy);
       }
@@ -213,16 +244,20 @@ __global__ void __launch_bounds__(SP_THREADS, 1) sparse_gram_kernel(const SpPara
       mbar_arrive(&ready[st]);
       if (++st == SP_ST) { st = 0; ph ^= 1u; }
       if (R == 0) break;
+#ifdef SP_PROFILE
+      ++prof_chunks;
+#endif
     }
+    SP_REPORT("mask");
     return;
   }
 
   // ------------------------------------------------------------------ owner warps
-  const int ct = threadIdx.x;   // 0 .. SP_CT-1: owns columns J0 + ct, J0 + ct + SP_CT, ...
+  const int ct = threadIdx.x;   // 0 .. SP_CT-1: mask slot; owns columns lane * 8 + warp (+ SP_CT, ...)
   int st = 0;
   uint32_t ph = 0;
   for (;;) {
-    mbar_wait(&ready[st], ph);
+    SP_WAIT(&ready[st], ph);
     unsigned char* sb = sbytes + (size_t)st * P.sbytes;
     const int* h = reinterpret_cast<const int*>(sb + SpStage::hdr);
     const int R = h[0];
@@ -234,46 +269,64 @@ __global__ void __launch_bounds__(SP_THREADS, 1) sparse_gram_kernel(const SpPara
     const int32_t* c_s = reinterpret_cast<const int32_t*>(sb + SpStage::col);
     uint32_t* mask = reinterpret_cast<uint32_t*>(sb + SpStage::mask);
     const int nw = (R + 31) / 32;
-    for (int c = ct; c < ncol; c += SP_CT) {
+    for (int i = 0;; i += SP_CT) {
+      const int c = i + lane * 8 + warp;   // the column of mask slot i + ct
+      if (c >= ncol) break;
       const int j = J0 + c;
       double* grow = gs + (tri_off(j, pa) - base) - j;   // grow[k] = G[j][k]
       if (j == p) {   // the augmented column: y^T y of the chunk
         grow[p] += *reinterpret_cast<const double*>(h + 4);
         continue;
       }
-      for (int w = 0; w < nw; ++w) {
-        uint32_t bits = mask[c * SP_MW + w];
-        if (!bits) continue;
-        mask[c * SP_MW + w] = 0u;   // ready for the stage's next use
-        do {
-          const int q = 32 * w + __ffs(bits) - 1;
-          bits &= bits - 1;
-          int a = (int)(rp_s[q] - e0);
-          const int a1 = (int)(rp_s[q + 1] - e0);
-          while (c_s[a] != j) ++a;   // the row's nonzero in column j (columns ascend)
-          const double va = v_s[a];
-          // the row's columns are distinct, so these read-modify-writes never alias: the loads
-          // of a pair are issued before either store
-          int b = a;
-          for (; b + 1 < a1; b += 2) {
-            const int k0 = c_s[b], k1 = c_s[b + 1];
-            const double g0 = grow[k0], g1 = grow[k1];
-            const double x0 = v_s[b], x1 = v_s[b + 1];
-            grow[k0] = g0 + va * x0;
-            grow[k1] = g1 + va * x1;
-          }
-          if (b < a1) grow[c_s[b]] += va * v_s[b];
-          grow[p] += va * y_s[q];
-        } while (bits);
+      // the column's row mask, loaded whole (independent, conflict-free loads) and cleared for
+      // the stage's next use; then its set bits in ascending row order, each lane at its own pace
+      uint32_t mw[SP_MW];
+#pragma unroll
+      for (int w = 0; w < SP_MW; ++w) {
+        mw[w] = w < nw ? mask[w * mld + i + ct] : 0u;
+        if (mw[w]) mask[w * mld + i + ct] = 0u;
+      }
+      int w = 0;
+      uint32_t bits = mw[0];
+      for (;;) {
+        while (!bits) {
+          if (++w == SP_MW) break;
+#pragma unroll
+          for (int t = 1; t < SP_MW; ++t)
+            if (t == w) bits = mw[t];
+        }
+        if (!bits) break;
+        const int q = 32 * w + __ffs(bits) - 1;
+        bits &= bits - 1;
+        int a = (int)(rp_s[q] - e0);
+        const int a1 = (int)(rp_s[q + 1] - e0);
+        while (c_s[a] != j) ++a;   // the row's nonzero in column j (columns ascend)
+        const double va = v_s[a];
+        // the row's columns are distinct, so these read-modify-writes never alias: the loads
+        // of a pair are issued before either store
+        int b = a;
+        for (; b + 1 < a1; b += 2) {
+          const int k0 = c_s[b], k1 = c_s[b + 1];
+          const double g0 = grow[k0], g1 = grow[k1];
+          const double x0 = v_s[b], x1 = v_s[b + 1];
+          grow[k0] = g0 + va * x0;
+          grow[k1] = g1 + va * x1;
+        }
+        if (b < a1) grow[c_s[b]] += va * v_s[b];
+        grow[p] += va * y_s[q];
       }
     }
     __syncwarp();
     if (lane == 0) mbar_arrive(&empty[st]);
     if (++st == SP_ST) { st = 0; ph ^= 1u; }
+#ifdef SP_PROFILE
+    ++prof_chunks;
+#endif
   }
+  SP_REPORT("owner");
   // epilogue: every owner writes its columns' triangle rows to this segment's partial
   double* out = P.partial + ((size_t)u * P.nseg + seg) * P.cap;
-  for (int c = ct; c < ncol; c += SP_CT) {
+  for (int c = lane * 8 + warp; c < ncol; c += SP_CT) {   // the same columns as above (no CTA barrier needed)
     const int64_t a0 = tri_off(J0 + c, pa) - base, a1 = tri_off(J0 + c + 1, pa) - base;
     for (int64_t e = a0; e < a1; ++e) out[e] = gs[e];
   }
