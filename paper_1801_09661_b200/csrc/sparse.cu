@@ -39,8 +39,9 @@ namespace {
 constexpr int SP_WARPS = 8;                     // owner (consumer) warps: 256 threads, one per owned column
 constexpr int SP_CT = SP_WARPS * 32;
 constexpr int SP_PROD = SP_WARPS;               // warp index of the producer
-constexpr int SP_MASKW = SP_WARPS + 1;          // warp index of the mask builder
-constexpr int SP_THREADS = (SP_WARPS + 2) * 32;
+constexpr int SP_MASKW = SP_WARPS + 1;          // warp index of the first mask builder
+constexpr int SP_NMASK = 4;                     // mask-builder warps (rows 32 m + lane + 128 t)
+constexpr int SP_THREADS = (SP_WARPS + 1 + SP_NMASK) * 32;
 constexpr int SP_ST = 3;                        // ring depth
 constexpr int SP_ROWS = 256;                    // rows per stage (max)
 constexpr int SP_MW = SP_ROWS / 32;             // mask words per column
@@ -52,8 +53,8 @@ struct SpStage {  // shared-memory layout of one ring stage (byte offsets); mask
   static constexpr int y = rp + (SP_ROWS + 1) * 8;
   static constexpr int val = y + SP_ROWS * 8;
   static constexpr int col = val + SP_ENT * 8;
-  static constexpr int hdr = col + SP_ENT * 4;   // int R, pad, int64 e0, double yy (the chunk's y^T y)
-  static constexpr int mask = (hdr + 32 + 127) / 128 * 128;
+  static constexpr int hdr = col + SP_ENT * 4;   // int R, pad, int64 e0, double yy[SP_NMASK] (the chunk's y^T y)
+  static constexpr int mask = (hdr + 16 + 8 * SP_NMASK + 127) / 128 * 128;
 };
 // The masks are stored word-major and, within a word, in OWNER order: column c is owned by
 // thread slot(c) = (c & ~255) | (c & 7) << 5 | (c & 255) >> 3 (warp c & 7, lane (c & 255) >> 3),
@@ -134,7 +135,7 @@ __global__ void __launch_bounds__(SP_THREADS, 1) sparse_gram_kernel(const SpPara
   if (threadIdx.x == 0) {
     for (int s = 0; s < SP_ST; ++s) {
       mbar_init(&full[s], 33);          // 32 cp.async arrivals (noinc) + the header arrive
-      mbar_init(&ready[s], 32);         // every lane of the mask warp
+      mbar_init(&ready[s], 32 * SP_NMASK);   // every lane of the mask warps
       mbar_init(&empty[s], SP_WARPS);   // lane 0 of every owner warp
     }
     fence_mbar_init();
@@ -214,7 +215,8 @@ __global__ void __launch_bounds__(SP_THREADS, 1) sparse_gram_kernel(const SpPara
     return;
   }
 
-  if (warp == SP_MASKW) {
+  if (warp >= SP_MASKW) {
+    const int m = warp - SP_MASKW;
     // ---------------------------------------------------------------- mask warp
     int st = 0;
     uint32_t ph = 0;
@@ -229,7 +231,7 @@ __global__ void __launch_bounds__(SP_THREADS, 1) sparse_gram_kernel(const SpPara
       const int32_t* c_s = reinterpret_cast<const int32_t*>(sb + SpStage::col);
       uint32_t* mask = reinterpret_cast<uint32_t*>(sb + SpStage::mask);
       double yy = 0.0;
-      for (int q = lane; q < R; q += 32) {   // lane takes rows lane, lane + 32, ...
+      for (int q = 32 * m + lane; q < R; q += 32 * SP_NMASK) {   // warp m, lane: rows 32 m + lane + 128 t
         const int a0 = (int)(rp_s[q] - e0), a1 = (int)(rp_s[q + 1] - e0);
         for (int a = a0; a < a1; ++a) {
           const int c = c_s[a] - J0;
@@ -239,7 +241,7 @@ __global__ void __launch_bounds__(SP_THREADS, 1) sparse_gram_kernel(const SpPara
       }
 #pragma unroll
       for (int o = 16; o >= 1; o >>= 1) yy += __shfl_xor_sync(0xffffffffu, yy, o);   // fixed order
-      if (lane == 0) *reinterpret_cast<double*>(h + 4) = yy;
+      if (lane == 0) reinterpret_cast<double*>(h + 4)[m] = yy;
       __syncwarp();
       mbar_arrive(&ready[st]);
       if (++st == SP_ST) { st = 0; ph ^= 1u; }
@@ -275,32 +277,49 @@ __global__ void __launch_bounds__(SP_THREADS, 1) sparse_gram_kernel(const SpPara
       const int j = J0 + c;
       double* grow = gs + (tri_off(j, pa) - base) - j;   // grow[k] = G[j][k]
       if (j == p) {   // the augmented column: y^T y of the chunk
-        grow[p] += *reinterpret_cast<const double*>(h + 4);
+        const double* yyc = reinterpret_cast<const double*>(h + 4);
+        double yy = yyc[0];
+#pragma unroll
+        for (int mm = 1; mm < SP_NMASK; ++mm) yy += yyc[mm];   // fixed order
+        grow[p] += yy;
         continue;
       }
       // the column's row mask, loaded whole (independent, conflict-free loads) and cleared for
       // the stage's next use; then its set bits in ascending row order, each lane at its own pace
-      uint32_t mw[SP_MW];
+      uint32_t mw[SP_MW], nzw = 0u;   // nzw: the non-empty words
 #pragma unroll
       for (int w = 0; w < SP_MW; ++w) {
         mw[w] = w < nw ? mask[w * mld + i + ct] : 0u;
-        if (mw[w]) mask[w * mld + i + ct] = 0u;
+        if (mw[w]) {
+          mask[w * mld + i + ct] = 0u;
+          nzw |= 1u << w;
+        }
       }
       int w = 0;
-      uint32_t bits = mw[0];
-      for (;;) {
-        while (!bits) {
-          if (++w == SP_MW) break;
+      uint32_t bits = 0u;
+      for (;;) {   // one set bit per trip: a lane's trip count is its column's nonzeros in the chunk
+        if (!bits) {
+          if (!nzw) break;
+          w = __ffs(nzw) - 1;
+          nzw &= nzw - 1;
+          bits = mw[0];
 #pragma unroll
-          for (int t = 1; t < SP_MW; ++t)
-            if (t == w) bits = mw[t];
+          for (int t = 1; t < SP_MW; ++t) bits = w == t ? mw[t] : bits;
         }
-        if (!bits) break;
         const int q = 32 * w + __ffs(bits) - 1;
         bits &= bits - 1;
-        int a = (int)(rp_s[q] - e0);
+        const int a0 = (int)(rp_s[q] - e0);
         const int a1 = (int)(rp_s[q + 1] - e0);
-        while (c_s[a] != j) ++a;   // the row's nonzero in column j (columns ascend)
+        // the row's nonzero in column j, four columns per probe: the row's columns ascend and
+        // are distinct, so the first match is it (slots past the row end come after it)
+        int a = a0;
+        for (;; a += 4) {
+          const int k0 = c_s[a], k1 = c_s[a + 1], k2 = c_s[a + 2], k3 = c_s[a + 3];
+          if (k0 == j) break;
+          if (k1 == j) { a += 1; break; }
+          if (k2 == j) { a += 2; break; }
+          if (k3 == j) { a += 3; break; }
+        }
         const double va = v_s[a];
         // the row's columns are distinct, so these read-modify-writes never alias: the loads
         // of a pair are issued before either store
