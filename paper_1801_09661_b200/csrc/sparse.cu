@@ -36,8 +36,8 @@ namespace oem {
 
 namespace {
 
-constexpr int SP_WARPS = 8;                     // owner (consumer) warps: 256 threads, one per owned column
-constexpr int SP_CT = SP_WARPS * 32;
+constexpr int SP_WARPS = 16;                    // owner (consumer) warps; a lane owns columns
+constexpr int SP_LGW = 4;                       // log2(SP_WARPS)
 constexpr int SP_PROD = SP_WARPS;               // warp index of the producer
 constexpr int SP_MASKW = SP_WARPS + 1;          // warp index of the first mask builder
 constexpr int SP_NMASK = 4;                     // mask-builder warps (rows 32 m + lane + 128 t)
@@ -56,12 +56,24 @@ struct SpStage {  // shared-memory layout of one ring stage (byte offsets); mask
   static constexpr int hdr = col + SP_ENT * 4;   // int R, pad, int64 e0, double yy[SP_NMASK] (the chunk's y^T y)
   static constexpr int mask = (hdr + 16 + 8 * SP_NMASK + 127) / 128 * 128;
 };
-// The masks are stored word-major and, within a word, in OWNER order: column c is owned by
-// thread slot(c) = (c & ~255) | (c & 7) << 5 | (c & 255) >> 3 (warp c & 7, lane (c & 255) >> 3),
-// so the slice's columns spread over all 8 owner warps and an owner warp's 32 mask loads hit 32
-// banks; word w of column c sits at mask[w * mask_ld(ncol) + slot(c)].
-__host__ __device__ constexpr int mask_ld(int ncol) { return (ncol + SP_CT - 1) / SP_CT * SP_CT; }
-__device__ __forceinline__ int mask_slot(int c) { return (c & ~255) | ((c & 7) << 5) | ((c & 255) >> 3); }
+// The masks are stored word-major and, within a word, in OWNER order: with L = 2^lgl lanes per
+// owner warp per round (the least power of two with SP_WARPS L >= ncol, at most 32), column c is
+// owned by warp c % SP_WARPS, lane (c / SP_WARPS) % L, so the slice's columns spread over all
+// owner warps (4 per SM sub-partition, hiding each other's shared-memory latency), and its mask
+// slot is round * SP_WARPS L + warp L + lane: an owner warp's mask loads hit distinct banks.
+// Word w of column c sits at mask[w * mask_ld(ncol) + slot(c)].
+__host__ __device__ constexpr int lg_lanes(int ncol) {   // log2 of the lanes per owner warp per round
+  int l = 0;
+  while ((SP_WARPS << l) < ncol && l < 5) ++l;
+  return l;
+}
+__host__ __device__ constexpr int mask_ld(int ncol) {
+  const int nl = SP_WARPS << lg_lanes(ncol);
+  return (ncol + nl - 1) / nl * nl;
+}
+__device__ __forceinline__ int mask_slot(int c, int lgl) {
+  return (c & ~((SP_WARPS << lgl) - 1)) | ((c & (SP_WARPS - 1)) << lgl) | ((c >> SP_LGW) & ((1 << lgl) - 1));
+}
 __host__ __device__ constexpr int stage_bytes(int ncol) { return SpStage::mask + (mask_ld(ncol) * SP_MW * 4 + 127) / 128 * 128; }
 
 struct SpParams {
@@ -124,7 +136,7 @@ __global__ void __launch_bounds__(SP_THREADS, 1) sparse_gram_kernel(const SpPara
   const int p = P.p;
   const int64_t pa = p + 1;
   const int64_t r0 = (int64_t)seg * P.seg_rows, r1 = min(P.n, r0 + P.seg_rows);
-  const int J0 = P.slice_j0[u], J1 = P.slice_j0[u + 1], ncol = J1 - J0, mld = mask_ld(ncol);
+  const int J0 = P.slice_j0[u], J1 = P.slice_j0[u + 1], ncol = J1 - J0, mld = mask_ld(ncol), lgl = lg_lanes(ncol);
   const int64_t base = tri_off(J0, pa), nent = tri_off(J1, pa) - base;
   double* gs = reinterpret_cast<double*>(sbytes + (size_t)SP_ST * P.sbytes);
   for (int64_t e = threadIdx.x; e < nent; e += SP_THREADS) gs[e] = 0.0;
@@ -235,7 +247,7 @@ __global__ void __launch_bounds__(SP_THREADS, 1) sparse_gram_kernel(const SpPara
         const int a0 = (int)(rp_s[q] - e0), a1 = (int)(rp_s[q + 1] - e0);
         for (int a = a0; a < a1; ++a) {
           const int c = c_s[a] - J0;
-          if (c >= 0 && c < ncol) atomicOr(&mask[(q >> 5) * mld + mask_slot(c)], 1u << (q & 31));
+          if (c >= 0 && c < ncol) atomicOr(&mask[(q >> 5) * mld + mask_slot(c, lgl)], 1u << (q & 31));
         }
         yy = fma(y_s[q], y_s[q], yy);
       }
@@ -255,7 +267,9 @@ __global__ void __launch_bounds__(SP_THREADS, 1) sparse_gram_kernel(const SpPara
   }
 
   // ------------------------------------------------------------------ owner warps
-  const int ct = threadIdx.x;   // 0 .. SP_CT-1: mask slot; owns columns lane * 8 + warp (+ SP_CT, ...)
+  // owner (warp, lane < 2^lgl) holds mask slot ct (+ one round of SP_WARPS << lgl slots per trip)
+  // and owns columns (lane << SP_LGW) + warp (+ the same per trip)
+  const int ct = (warp << lgl) | lane;
   int st = 0;
   uint32_t ph = 0;
   for (;;) {
@@ -271,9 +285,9 @@ __global__ void __launch_bounds__(SP_THREADS, 1) sparse_gram_kernel(const SpPara
     const int32_t* c_s = reinterpret_cast<const int32_t*>(sb + SpStage::col);
     uint32_t* mask = reinterpret_cast<uint32_t*>(sb + SpStage::mask);
     const int nw = (R + 31) / 32;
-    for (int i = 0;; i += SP_CT) {
-      const int c = i + lane * 8 + warp;   // the column of mask slot i + ct
-      if (c >= ncol) break;
+    for (int i = 0;; i += SP_WARPS << lgl) {
+      const int c = i + (lane << SP_LGW) + warp;   // the column of mask slot i + ct
+      if (lane >> lgl || c >= ncol) break;
       const int j = J0 + c;
       double* grow = gs + (tri_off(j, pa) - base) - j;   // grow[k] = G[j][k]
       if (j == p) {   // the augmented column: y^T y of the chunk
@@ -345,7 +359,7 @@ __global__ void __launch_bounds__(SP_THREADS, 1) sparse_gram_kernel(const SpPara
   SP_REPORT("owner");
   // epilogue: every owner writes its columns' triangle rows to this segment's partial
   double* out = P.partial + ((size_t)u * P.nseg + seg) * P.cap;
-  for (int c = lane * 8 + warp; c < ncol; c += SP_CT) {   // the same columns as above (no CTA barrier needed)
+  for (int c = (lane << SP_LGW) + warp; !(lane >> lgl) && c < ncol; c += SP_WARPS << lgl) {   // the same columns as above (no CTA barrier needed)
     const int64_t a0 = tri_off(J0 + c, pa) - base, a1 = tri_off(J0 + c + 1, pa) - base;
     for (int64_t e = a0; e < a1; ++e) out[e] = gs[e];
   }
