@@ -84,6 +84,24 @@ oem_status oem_gram_folds(oem_ctx* ctx, const double* X, const double* y, int64_
                           int64_t ldx, int64_t row_offset, int32_t K, double* G_folds,
                           double* xty_folds, double* yty_folds, int64_t* counts /*host K*/, void* stream);
 
+/* ---- a2/a3 with a ones column (f3 intercept / standardization, R#2-3): the
+ * same single pass over Z = [X | y | 1] (the ones column is formed in shared memory, no extra
+ * HBM bytes), which also yields the column sums the intercept needs: xsum[j] = sum_i x_ij (p),
+ * ysum = sum_i y_i (1), raw over this rank's rows and allreduced with G (one allreduce).
+ * G, xty, yty, n_total exactly as oem_gram (the sums of the shared entries may differ from
+ * oem_gram's in the last bits when the extra column changes the tiling). Replaces the second,
+ * HBM-bound pass of oem_gram_moments for in-core data. Errors: as oem_gram. */
+oem_status oem_gram_sums(oem_ctx* ctx, const double* X, const double* y, int64_t n_local, int32_t p,
+                         int64_t ldx, double* G, double* xty, double* yty, double* xsum /*p*/,
+                         double* ysum /*1*/, int64_t* n_total /*host, may be NULL*/, void* stream);
+/* The fold-segmented form (a3 + f3): oem_gram_folds plus, per fold k, xsum_folds[k*p + j] and
+ * ysum_folds[k] (the fold column sums oem_cv_error and an intercept fit take), one pass.
+ * Errors: as oem_gram_folds. */
+oem_status oem_gram_folds_sums(oem_ctx* ctx, const double* X, const double* y, int64_t n_local, int32_t p,
+                               int64_t ldx, int64_t row_offset, int32_t K, double* G_folds,
+                               double* xty_folds, double* yty_folds, double* xsum_folds /*K*p*/,
+                               double* ysum_folds /*K*/, int64_t* counts /*host K*/, void* stream);
+
 /* ---- a4 weighted Gram for the proximal-Newton logistic step (§4; working
  * responses z_i and weights w_i at P:L376-380; R#23-25). Per row: eta = x_i^T beta,
  * mu = 1/(1+exp(-eta)) clamped to [eps, 1-eps], w = mu(1-mu), z = eta + (y - mu)/w.

@@ -215,16 +215,26 @@ oem_status oem_gram(oem_ctx* ctx, const double* X, const double* y, int64_t n_lo
   return OEM_OK;
 }
 
-oem_status oem_gram_folds(oem_ctx* ctx, const double* X, const double* y, int64_t n_local, int32_t p, int64_t ldx,
-                          int64_t row_offset, int32_t K, double* G_folds, double* xty_folds, double* yty_folds,
-                          int64_t* counts, void* stream) {
+}  // extern "C"
+
+// xsum[f*p + j] = sums[f*(p+2) + j] (j < p), ysum[f] = sums[f*(p+2) + p]
+static oem_status unpack_sums(const double* sums, int nfold, int p, double* xsum, double* ysum, cudaStream_t st) {
+  OEM_CUDA_TRY(cudaMemcpy2DAsync(xsum, sizeof(double) * p, sums, sizeof(double) * (p + 2), sizeof(double) * p, nfold,
+                                 cudaMemcpyDeviceToDevice, st));
+  OEM_CUDA_TRY(cudaMemcpy2DAsync(ysum, sizeof(double), sums + p, sizeof(double) * (p + 2), sizeof(double), nfold,
+                                 cudaMemcpyDeviceToDevice, st));
+  return OEM_OK;
+}
+
+// a3 (and its ones-column variant): K raw per-fold sums in one pass
+static oem_status gram_folds_impl(oem_ctx* ctx, const double* X, const double* y, int64_t n_local, int32_t p,
+                                  int64_t ldx, int64_t row_offset, int32_t K, double* G_folds, double* xty_folds,
+                                  double* yty_folds, double* xsum_folds, double* ysum_folds, int64_t* counts,
+                                  cudaStream_t st) {
   oem_status s;
-  if ((s = check_ctx(ctx)) != OEM_OK) return s;
-  if ((s = check_x(X, y, n_local, p, ldx, "oem_gram_folds")) != OEM_OK) return s;
   if (K < 1 || K > 65535) OEM_FAIL(OEM_ERR_INVALID_ARG, "oem_gram_folds: need 1 <= K <= 65535");
   if (row_offset < 0) OEM_FAIL(OEM_ERR_INVALID_ARG, "oem_gram_folds: row_offset < 0");
   if (!G_folds || !xty_folds || !yty_folds || !counts) OEM_FAIL(OEM_ERR_INVALID_ARG, "oem_gram_folds: null output");
-  cudaStream_t st = (cudaStream_t)stream;
   // fold sizes are arithmetic on the row indices (host): rows i with (off + i) mod K == k
   for (int k = 0; k < K; ++k) {
     const int64_t first = ((k - row_offset) % K + K) % K;  // first local row in fold k
@@ -234,12 +244,67 @@ oem_status oem_gram_folds(oem_ctx* ctx, const double* X, const double* y, int64_
   for (int k = 0; k < K; ++k)
     if (counts[k] == 0) OEM_FAIL(OEM_ERR_EMPTY_FOLD, "oem_gram_folds: fold " + std::to_string(k) + " has no rows");
   const int64_t psize = packed_size(p);
-  OEM_CUDA_TRY(ctx->packed.ensure(sizeof(double) * (psize * K + 2)));
+  const bool ones = xsum_folds != nullptr;
+  const int64_t total = psize * K + (ones ? (int64_t)K * (p + 2) : 0);   // triangles | sums: one allreduce
+  OEM_CUDA_TRY(ctx->packed.ensure(sizeof(double) * (total + 2)));
   double* packed = ctx->packed.as<double>();
-  if ((s = gram_pass(ctx, MODE_FOLD, X, y, nullptr, 0.0, n_local, p, ldx, row_offset, K, packed, st)) != OEM_OK)
+  double* sums = ones ? packed + psize * K : nullptr;
+  if ((s = gram_pass(ctx, MODE_FOLD, X, y, nullptr, 0.0, n_local, p, ldx, row_offset, K, packed, st, 0, 1, sums)) !=
+      OEM_OK)
     return s;
-  if ((s = allreduce_sum(ctx, packed, (size_t)psize * K, st)) != OEM_OK) return s;
-  return gram_unpack(ctx, packed, K, p, G_folds, xty_folds, yty_folds, st);
+  if ((s = allreduce_sum(ctx, packed, (size_t)total, st)) != OEM_OK) return s;
+  if ((s = gram_unpack(ctx, packed, K, p, G_folds, xty_folds, yty_folds, st)) != OEM_OK) return s;
+  return ones ? unpack_sums(sums, K, p, xsum_folds, ysum_folds, st) : OEM_OK;
+}
+
+extern "C" {
+
+oem_status oem_gram_folds(oem_ctx* ctx, const double* X, const double* y, int64_t n_local, int32_t p, int64_t ldx,
+                          int64_t row_offset, int32_t K, double* G_folds, double* xty_folds, double* yty_folds,
+                          int64_t* counts, void* stream) {
+  oem_status s;
+  if ((s = check_ctx(ctx)) != OEM_OK) return s;
+  if ((s = check_x(X, y, n_local, p, ldx, "oem_gram_folds")) != OEM_OK) return s;
+  return gram_folds_impl(ctx, X, y, n_local, p, ldx, row_offset, K, G_folds, xty_folds, yty_folds, nullptr, nullptr,
+                         counts, (cudaStream_t)stream);
+}
+
+oem_status oem_gram_sums(oem_ctx* ctx, const double* X, const double* y, int64_t n_local, int32_t p, int64_t ldx,
+                         double* G, double* xty, double* yty, double* xsum, double* ysum, int64_t* n_total,
+                         void* stream) {
+  oem_status s;
+  if ((s = check_ctx(ctx)) != OEM_OK) return s;
+  if ((s = check_x(X, y, n_local, p, ldx, "oem_gram_sums")) != OEM_OK) return s;
+  if (!G || !xty || !yty || !xsum || !ysum) OEM_FAIL(OEM_ERR_INVALID_ARG, "oem_gram_sums: null output");
+  cudaStream_t st = (cudaStream_t)stream;
+  const int64_t psize = packed_size(p);
+  // packed triangle | sums [p + 2]: one allreduce for both
+  OEM_CUDA_TRY(ctx->packed.ensure(sizeof(double) * (psize + p + 2)));
+  double* packed = ctx->packed.as<double>();
+  double* sums = packed + psize;
+  if ((s = gram_pass(ctx, MODE_PLAIN, X, y, nullptr, 0.0, n_local, p, ldx, 0, 1, packed, st, 0, 1, sums)) != OEM_OK)
+    return s;
+  if ((s = allreduce_sum(ctx, packed, psize + p + 2, st)) != OEM_OK) return s;
+  if ((s = gram_unpack(ctx, packed, 1, p, G, xty, yty, st)) != OEM_OK) return s;
+  if ((s = unpack_sums(sums, 1, p, xsum, ysum, st)) != OEM_OK) return s;
+  if (n_total) {
+    int64_t n = n_local;
+    if ((s = host_allreduce_i64(ctx, &n, 1, st)) != OEM_OK) return s;
+    *n_total = n;
+  }
+  return OEM_OK;
+}
+
+oem_status oem_gram_folds_sums(oem_ctx* ctx, const double* X, const double* y, int64_t n_local, int32_t p,
+                               int64_t ldx, int64_t row_offset, int32_t K, double* G_folds, double* xty_folds,
+                               double* yty_folds, double* xsum_folds, double* ysum_folds, int64_t* counts,
+                               void* stream) {
+  oem_status s;
+  if ((s = check_ctx(ctx)) != OEM_OK) return s;
+  if ((s = check_x(X, y, n_local, p, ldx, "oem_gram_folds_sums")) != OEM_OK) return s;
+  if (!xsum_folds || !ysum_folds) OEM_FAIL(OEM_ERR_INVALID_ARG, "oem_gram_folds_sums: null output");
+  return gram_folds_impl(ctx, X, y, n_local, p, ldx, row_offset, K, G_folds, xty_folds, yty_folds, xsum_folds,
+                         ysum_folds, counts, (cudaStream_t)stream);
 }
 
 oem_status oem_gram_weighted(oem_ctx* ctx, const double* X, const double* y01, const double* beta, int64_t n_local,

@@ -102,6 +102,7 @@ struct GramParams {
   const double* beta;
   double eps;
   int want_scal;          // WEIGHTED: accumulate sum w and the log-likelihood (else zeros)
+  int ones;               // PLAIN / FOLD: a ones column at p + 1 (Z = [X | y | 1])
   double* partial;        // [nfold][nseg][nblk][64]
   int ordered;            // 1: segments add into accum in segment order (no partial buffer)
   unsigned* ticket;       // [ORD_W][U] next link of each chain allowed to add (zero at launch)
@@ -155,6 +156,14 @@ __device__ __forceinline__ void consume(const GramParams& P, const Cons& cs) {
   // does this job's column range hold the augmented y column (copy it into the panel)?
   const int ycol = P.p - cs.b0;
   const bool ycopy = (MODE != MODE_WEIGHTED) && C > 0 && P.p >= 8 * cs.job.bj0 && P.p < 8 * (cs.job.bj0 + C);
+  // ... and the ones column (1 for the segment's rows, 0 for the zero-filled rows past its end).
+  // With the ones column the y column can also sit in the job's ROW range only (block rows ending
+  // at p, columns in the next block, where the ones column opened a block): then y goes into the A
+  // panel (for a shared panel, the same location any B-side writer fills with the same value)
+  const bool onecopy = (MODE == MODE_PLAIN || MODE == MODE_FOLD) && C > 0 && P.ones && P.p + 1 >= 8 * cs.job.bj0 &&
+                       P.p + 1 < 8 * (cs.job.bj0 + C);
+  const bool ycopyA = (MODE == MODE_PLAIN || MODE == MODE_FOLD) && R > 0 && P.ones && !ycopy &&
+                      P.p >= 8 * cs.job.bi0 && P.p < 8 * (cs.job.bi0 + R);
   // the staged value for the augmented column: y (PLAIN), y of fold kprime (FOLD), z (WZ: ys holds (w, z) pairs)
   const int yidx = lane * P.ystride + (MODE == MODE_FOLD ? cs.kprime : MODE == MODE_WZ ? 1 : 0);
   int st = 0;
@@ -166,10 +175,10 @@ __device__ __forceinline__ void consume(const GramParams& P, const Cons& cs) {
     double* pb = cs.two ? pa + (size_t)BK * ld : pa;
     double* ys = pa + P.ys_off;
     double* ws = ys + BK * P.ystride;
-    if (MODE != MODE_WEIGHTED && ycopy) {
-      pb[lane * ld + ycol] = ys[yidx];
-      __syncwarp();
-    }
+    if (MODE != MODE_WEIGHTED && ycopy) pb[lane * ld + ycol] = ys[yidx];
+    if (ycopyA) pa[lane * ld + P.p - cs.a0] = ys[yidx];
+    if (onecopy) pb[lane * ld + ycol + 1] = cs.r0 + (int64_t)s * BK + lane < cs.r1 ? 1.0 : 0.0;
+    if (ycopy || ycopyA || onecopy) __syncwarp();
     if (KIND != J_NONE) {
       const double* pak = pa + aoff;
       const double* pbk = pb + boff;
@@ -201,7 +210,7 @@ __device__ __forceinline__ void consume(const GramParams& P, const Cons& cs) {
         pbk += 4 * ld;
       }
     }
-    if (ycopy) fence_proxy_async_smem();  // generic smem writes precede the next TMA refill
+    if (ycopy || ycopyA || onecopy) fence_proxy_async_smem();  // generic smem writes precede the next TMA refill
     __syncwarp();
     if (cs.lane == 0) mbar_arrive(&cs.empty[st]);
     if (++st == P.ST) { st = 0; ph ^= 1u; }
@@ -559,7 +568,7 @@ gram_kernel(const __grid_constant__ CUtensorMap tmX, const __grid_constant__ CUt
 __global__ void gram_reduce_kernel(const double* __restrict__ partial, int nfold, int nseg, int nblk,
                                    const int2* __restrict__ blk_coord, int p, const double* __restrict__ tail,
                                    double* __restrict__ packed, int64_t psize, const double* __restrict__ pscal,
-                                   int nscal, int with_scal, int accumulate) {
+                                   int nscal, int with_scal, int accumulate, double* __restrict__ sums) {
   const int64_t total = (int64_t)nfold * nblk * 64;
   for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < total; t += (int64_t)gridDim.x * blockDim.x) {
     const int e = (int)(t & 63);
@@ -568,11 +577,15 @@ __global__ void gram_reduce_kernel(const double* __restrict__ partial, int nfold
     const int f = (int)(fb / nblk);
     const int2 bc = blk_coord[idx];
     const int j = 8 * bc.x + (e >> 3), l = 8 * bc.y + (e & 7);
-    if (j > l || l > p) continue;
+    if (j > l || l > p + (sums ? 1 : 0)) continue;
     double s = 0.0;
     const double* src = partial + ((size_t)f * nseg * nblk + idx) * 64 + e;
     for (int g = 0; g < nseg; ++g) s += src[(size_t)g * nblk * 64];
     if (tail) s += tail[((size_t)f * nblk + idx) * 64 + e];
+    if (l == p + 1) {   // the ones column: X^T 1, 1^T y, the row count
+      sums[(size_t)f * (p + 2) + j] = s;
+      continue;
+    }
     double* dst = packed + (size_t)f * psize + (int64_t)j * (p + 1) - (int64_t)j * (j - 1) / 2 + (l - j);
     *dst = accumulate ? *dst + s : s;   // streamed row blocks add in block order (f4)
   }
@@ -612,7 +625,7 @@ __global__ void gram_chunk_kernel(const double* __restrict__ partial, int nfold,
 // FOLD tail: rows i in [nq*K, n_local) (fewer than K, so at most one per fold) as outer products.
 __global__ void gram_fold_tail_kernel(const double* __restrict__ X, const double* __restrict__ y, int64_t ldx,
                                       int64_t n_local, int64_t nq, int K, int off_mod, int p, int nblk,
-                                      const int2* __restrict__ blk_coord, double* __restrict__ tail) {
+                                      const int2* __restrict__ blk_coord, double* __restrict__ tail, int ones) {
   const int64_t total = (int64_t)K * nblk * 64;
   for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < total; t += (int64_t)gridDim.x * blockDim.x) {
     const int e = (int)(t & 63);
@@ -625,9 +638,9 @@ __global__ void gram_fold_tail_kernel(const double* __restrict__ X, const double
     if (i < n_local) {
       const int2 bc = blk_coord[idx];
       const int j = 8 * bc.x + (e >> 3), l = 8 * bc.y + (e & 7);
-      if (j <= p && l <= p) {
-        const double zj = j < p ? X[i * ldx + j] : y[i];
-        const double zl = l < p ? X[i * ldx + l] : y[i];
+      if (j <= p + ones && l <= p + ones) {   // z = [x_i | y_i | 1]
+        const double zj = j < p ? X[i * ldx + j] : j == p ? y[i] : 1.0;
+        const double zl = l < p ? X[i * ldx + l] : l == p ? y[i] : 1.0;
         v = zj * zl;
       }
     }
@@ -716,10 +729,10 @@ static void pack_jobs(std::vector<Job>& jobs, int a0, int b0, int same, std::vec
   }
 }
 
-static oem_status build_plan(oem_ctx* ctx, int mode, int p, int64_t nrows, int K, GramPlan& pl) {
+static oem_status build_plan(oem_ctx* ctx, int mode, int p, int64_t nrows, int K, int ones, GramPlan& pl) {
   pl.mode = mode;
   pl.p = p;
-  const int Pa = p + 1;
+  const int Pa = p + 1 + ones;   // augmented columns: [X | y] or [X | y | 1]
   const int nb_exact = (Pa + 7) / 8;
   const bool single = (8 * nb_exact + 4) <= 256;
   if ((mode == MODE_WEIGHTED && !single) || (mode == MODE_WZ && single))
@@ -940,7 +953,10 @@ static oem_status launch_t(const GramPlan& pl, const CUtensorMap& mx, const CUte
 
 oem_status gram_pass(oem_ctx* ctx, int mode, const double* X, const double* y, const double* beta, double eps,
                      int64_t n_local, int p, int64_t ldx, int64_t row_offset, int K, double* packed, cudaStream_t st,
-                     int accumulate, int want_scal) {
+                     int accumulate, int want_scal, double* sums) {
+  const int ones = sums ? 1 : 0;
+  if (ones && (mode == MODE_WEIGHTED || accumulate))
+    OEM_FAIL(OEM_ERR_UNSUPPORTED, "gram: the ones column is for single plain / fold passes (internal)");
   const int nfold = mode == MODE_FOLD ? K : 1;
   const int64_t psize = packed_size(p);
   const int64_t nq = mode == MODE_FOLD ? n_local / K : n_local;
@@ -950,15 +966,16 @@ oem_status gram_pass(oem_ctx* ctx, int mode, const double* X, const double* y, c
   if (n_local == 0 || nq == 0) {
     if (!accumulate)
       OEM_CUDA_TRY(cudaMemsetAsync(packed, 0, sizeof(double) * (nfold * psize + (mode == MODE_WEIGHTED ? 2 : 0)), st));
+    if (sums) OEM_CUDA_TRY(cudaMemsetAsync(sums, 0, sizeof(double) * nfold * (p + 2), st));
     if (mode != MODE_FOLD || n_local == 0) return OEM_OK;
   }
-  auto key = std::make_tuple(kmode, p, nq, K);
+  auto key = std::make_tuple(kmode, p, nq, K, ones);
   std::shared_ptr<GramPlan> plp;
   auto it = ctx->plans.find(key);
   if (it != ctx->plans.end()) plp = it->second;
   else {
     plp = std::make_shared<GramPlan>();
-    oem_status s = build_plan(ctx, kmode, p, std::max<int64_t>(nq, 1), K, *plp);
+    oem_status s = build_plan(ctx, kmode, p, std::max<int64_t>(nq, 1), K, ones, *plp);
     if (s != OEM_OK) return s;
     ctx->plans[key] = plp;
   }
@@ -1046,7 +1063,7 @@ oem_status gram_pass(oem_ctx* ctx, int mode, const double* X, const double* y, c
     P.nblk = pl.nblk; P.nrows = nq; P.seg_rows = pl.seg_rows; P.K = K;
     P.off_mod = mode == MODE_FOLD ? (int)(((row_offset % K) + K) % K) : 0;
     P.ytma = pl.ytma; P.ystride = pl.ystride;
-    P.y = y; P.beta = beta; P.eps = eps; P.want_scal = want_scal;
+    P.y = y; P.beta = beta; P.eps = eps; P.want_scal = want_scal; P.ones = ones;
     P.partial = ctx->partial.as<double>();
     P.ordered = pl.ordered;
     P.ticket = ticket;
@@ -1075,7 +1092,7 @@ oem_status gram_pass(oem_ctx* ctx, int mode, const double* X, const double* y, c
   if (tail) {
     ++ctx->launches;
     gram_fold_tail_kernel<<<std::max(1, std::min(1024, (int)((K * (int64_t)pl.nblk * 64 + 255) / 256))), 256, 0, st>>>(
-        X, y, ldx, n_local, nq, K, (int)(((row_offset % K) + K) % K), p, pl.nblk, pl.d_blk_coord, tail);
+        X, y, ldx, n_local, nq, K, (int)(((row_offset % K) + K) % K), p, pl.nblk, pl.d_blk_coord, tail, ones);
     OEM_CUDA_TRY(cudaGetLastError());
   }
   {
@@ -1103,7 +1120,7 @@ oem_status gram_pass(oem_ctx* ctx, int mode, const double* X, const double* y, c
     const int blocks = (int)std::max<int64_t>(1, std::min<int64_t>(ctx->num_sms * 8, (total + 255) / 256));
     ++ctx->launches;
     gram_reduce_kernel<<<blocks, 256, 0, st>>>(src, nfold, nseg, pl.nblk, pl.d_blk_coord, p, tail, packed, psize, sscal,
-                                               nscal, mode == MODE_WEIGHTED, accumulate);
+                                               nscal, mode == MODE_WEIGHTED, accumulate, sums);
     OEM_CUDA_TRY(cudaGetLastError());
   }
   return OEM_OK;

@@ -60,7 +60,7 @@ struct oem_ctx {
   oem::DevBuf partial, partial2, counts_dev, partial_scal, packed, tail, plan_tables, path_ws, path_small, logi, lg_part, lg_out, mom_part, mom_out, stage0, stage1, drule_ws, wz, sparse_ws, gram_acc;
   cudaStream_t copy_stream = nullptr;  // f4 host streaming: H2D copies overlap the Gram kernel
   cudaEvent_t ev_copied[2] = {nullptr, nullptr}, ev_used[2] = {nullptr, nullptr};
-  std::map<std::tuple<int, int, int64_t, int>, std::shared_ptr<oem::GramPlan>> plans;
+  std::map<std::tuple<int, int, int64_t, int, int>, std::shared_ptr<oem::GramPlan>> plans;
   // instrumentation (oem_ctx_set_timing / oem_ctx_stats)
   bool timing = false;
   int64_t launches = 0;
@@ -103,9 +103,12 @@ enum GramMode { MODE_PLAIN = 0, MODE_FOLD = 1, MODE_WEIGHTED = 2, MODE_WZ = 3 };
 // One pass over [X | y] producing the packed upper triangle of the augmented
 // (p+1)x(p+1) Gram per fold (nfold = K for MODE_FOLD else 1), raw sums, this rank only.
 // packed: nfold * psize (+2 scalars for MODE_WEIGHTED), psize = (p+1)(p+2)/2.
+// ones = 1 (MODE_PLAIN / MODE_FOLD, not streamed): the pass is over [X | y | 1] and also writes
+// sums[f][j] = column j of the ones column per fold (X^T 1 for j < p, 1^T y at p, the row count
+// at p + 1; nfold * (p + 2) doubles), in the same pass.
 oem_status gram_pass(oem_ctx* ctx, int mode, const double* X, const double* y, const double* beta, double eps,
                      int64_t n_local, int p, int64_t ldx, int64_t row_offset, int K, double* packed,
-                     cudaStream_t st, int accumulate = 0, int want_scal = 1);
+                     cudaStream_t st, int accumulate = 0, int want_scal = 1, double* sums = nullptr);
 // packed (nfold blocks) -> full symmetric G (nfold*p*p), xty (nfold*p), yty (nfold)
 oem_status gram_unpack(oem_ctx* ctx, const double* packed, int nfold, int p, double* G, double* xty, double* yty, cudaStream_t st);
 inline int64_t packed_size(int p) { return (int64_t)(p + 1) * (p + 2) / 2; }

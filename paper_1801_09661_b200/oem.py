@@ -28,7 +28,7 @@ ABI_SYMBOLS = ["oem_status_string", "oem_last_error", "oem_version", "oem_nccl_u
                "oem_ctx_create", "oem_ctx_destroy", "oem_gram", "oem_gram_folds",
                "oem_gram_weighted", "oem_fit_path", "oem_path_cfg_default", "oem_fit_logistic",
                "oem_logistic_cfg_default", "oem_cv_error", "oem_logit_grad", "oem_gram_moments", "oem_path_loss", "oem_gram_host", "oem_gram_folds_host", "oem_ctx_set_timing", "oem_ctx_stats",
-               "oem_gram_csr"]
+               "oem_gram_csr", "oem_gram_sums", "oem_gram_folds_sums"]
 _VOID = ("oem_status_string", "oem_last_error", "oem_version", "oem_path_cfg_default",
          "oem_logistic_cfg_default")
 
@@ -109,6 +109,8 @@ def lib():
         L.oem_gram_folds_host.argtypes = [P, P, P, i64, i32, i64, i64, i32, i64, P, P, P, P, P]
         L.oem_path_loss.argtypes = [P, P, P, P, P, i32, i32, i32, i32, P, P, P]
         L.oem_gram_csr.argtypes = [P, P, P, P, P, i64, i32, P, P, P, ctypes.POINTER(i64), P]
+        L.oem_gram_sums.argtypes = [P, P, P, i64, i32, i64, P, P, P, P, P, ctypes.POINTER(i64), P]
+        L.oem_gram_folds_sums.argtypes = [P, P, P, i64, i32, i64, i64, i32, P, P, P, P, P, P, P]
         L.oem_ctx_set_timing.argtypes = [P, ctypes.c_int]
         L.oem_ctx_stats.argtypes = [P, ctypes.POINTER(Stats), ctypes.c_int]
         for name in ABI_SYMBOLS:
@@ -209,6 +211,38 @@ def oem_gram_folds(ctx: Context, X, y, K: int, row_offset: int = 0, stream=None)
     _check(lib().oem_gram_folds(ctx.h, _ptr(X), _ptr(y), n, p, X.stride(0), row_offset, K, _ptr(G),
                                 _ptr(xty), _ptr(yty), counts, _stream(stream)))
     return G, xty, yty, list(counts)
+
+
+def oem_gram_sums(ctx: Context, X: torch.Tensor, y: torch.Tensor, stream=None):
+    """a2 + f3 in one pass over [X | y | 1]: (G, xty, yty, xsum = X^T 1, ysum = 1^T y [1], n_total)."""
+    _check_x(X, y)
+    n, p = X.shape
+    dev = X.device
+    G = torch.empty((p, p), dtype=torch.float64, device=dev)
+    xty = torch.empty(p, dtype=torch.float64, device=dev)
+    yty = torch.empty(1, dtype=torch.float64, device=dev)
+    xs = torch.empty(p, dtype=torch.float64, device=dev)
+    ys = torch.empty(1, dtype=torch.float64, device=dev)
+    nt = ctypes.c_int64()
+    _check(lib().oem_gram_sums(ctx.h, _ptr(X), _ptr(y), n, p, X.stride(0), _ptr(G), _ptr(xty), _ptr(yty),
+                               _ptr(xs), _ptr(ys), ctypes.byref(nt), _stream(stream)))
+    return G, xty, yty, xs, ys, nt.value
+
+
+def oem_gram_folds_sums(ctx: Context, X, y, K: int, row_offset: int = 0, stream=None):
+    """a3 + f3 in one pass: (G_k, xty_k, yty_k, xsum_k [K][p], ysum_k [K], counts)."""
+    _check_x(X, y)
+    n, p = X.shape
+    dev = X.device
+    G = torch.empty((K, p, p), dtype=torch.float64, device=dev)
+    xty = torch.empty((K, p), dtype=torch.float64, device=dev)
+    yty = torch.empty(K, dtype=torch.float64, device=dev)
+    xs = torch.empty((K, p), dtype=torch.float64, device=dev)
+    ys = torch.empty(K, dtype=torch.float64, device=dev)
+    counts = (ctypes.c_int64 * K)()
+    _check(lib().oem_gram_folds_sums(ctx.h, _ptr(X), _ptr(y), n, p, X.stride(0), row_offset, K, _ptr(G),
+                                     _ptr(xty), _ptr(yty), _ptr(xs), _ptr(ys), counts, _stream(stream)))
+    return G, xty, yty, xs, ys, list(counts)
 
 
 def oem_gram_weighted(ctx: Context, X, y01, beta, eps=1e-5, stream=None, scalars=True):

@@ -69,7 +69,12 @@ def main():
     sbt = dg.beta(sspec)
     rp, scol, sval, sy = dg.csr_cuda(sspec, sbt, r0, nl)
     Gs, cs, yys, ns = oem_gram_csr(ctx, rp, scol, sval, sy, sspec.p)
-    mine = digest(G, c, yy, Gk, ck, yyk, Gw, cw, sw, fit.beta, fit.d, cvf.beta, cvf.d, Gs, cs, yys)
+    # the one-pass column sums (ones column), whole data and per fold
+    from paper_1801_09661_b200 import oem_gram_folds_sums, oem_gram_sums
+    G1, c1, yy1, xs1, ys1, n1 = oem_gram_sums(ctx, Xd, yd)
+    _, _, _, xsk, ysk, _ = oem_gram_folds_sums(ctx, Xd, yd, K, row_offset=r0)
+    mine = digest(G, c, yy, Gk, ck, yyk, Gw, cw, sw, fit.beta, fit.d, cvf.beta, cvf.d, Gs, cs, yys, G1, xs1, ys1,
+                  xsk, ysk)
     digests = [None] * world
     if world > 1:
         dist.all_gather_object(digests, mine)
@@ -98,6 +103,13 @@ def main():
             lam = orc.lambda_grid(orc.lambda_max(fam, co / n), 12)
             B, it, cv = orc.oem_path(Go / n, co / n, d_ref, fam, lam, gamma, alpha)
             assert np.max(np.abs(fit.beta[0, q].cpu().numpy() - B)) <= 1e-8
+        assert n1 == spec.n and scale_err(G1.cpu().numpy(), Go) <= 1e-12
+        xabs = np.abs(X).sum(axis=0)
+        assert np.max(np.abs(xs1.cpu().numpy() - X.sum(axis=0)) / xabs) <= 1e-12
+        assert abs(float(ys1) - y.sum()) <= 1e-12 * np.abs(y).sum()
+        fold = (np.arange(spec.n)) % K
+        for k in range(K):
+            assert np.max(np.abs(xsk[k].cpu().numpy() - X[fold == k].sum(axis=0)) / xabs) <= 1e-12
         Xs, yh = dg.rows_host(sspec, sbt)
         Gso, cso, yyso = orc.gram(Xs, yh)
         assert ns == sspec.n and scale_err(Gs.cpu().numpy(), Gso) <= 1e-12

@@ -123,16 +123,22 @@ def test_gram_full_n_column_subset_cfg4(ctx):
     sub-Gram over four column blocks in four different 128-column panels (diagonal and
     off-diagonal panel pairs, 528 distinct entries), X^T y and the f3 column sums on those columns,
     against the oracle's sums over all 1e7 rows (gpu_util.cfg4_oracle_sample)."""
-    from paper_1801_09661_b200 import oem_gram, oem_gram_moments
+    from paper_1801_09661_b200 import oem_gram, oem_gram_moments, oem_gram_sums
     cfg = CONFIGS["cfg4"]
     bt = dg.beta(cfg.spec)
     Xd, yd = device_rows(cfg.spec, bt)
     G, c, yy, nt = oem_gram(ctx, Xd, yd)
     xs, ysum = oem_gram_moments(ctx, Xd, yd, 1, 0)   # f3 column sums at full size, same launch shape
+    G1, c1, yy1, xs1, ys1, nt1 = oem_gram_sums(ctx, Xd, yd)   # the same in one pass over [X | y | 1]
     del Xd
     torch.cuda.empty_cache()
     idx, Go, co, yyo, xso, xabs = cfg4_oracle_sample()
     assert np.max(np.abs(xs[0].cpu().numpy()[idx] - xso) / xabs) <= 1e-12
+    assert nt1 == nt and np.max(np.abs(xs1.cpu().numpy()[idx] - xso) / xabs) <= 1e-12
+    G1h = G1.cpu().numpy()
+    assert scale_err(G1h[np.ix_(idx, idx)], Go) <= 1e-12
+    assert xty_err(c1.cpu().numpy()[idx], co, Go, yyo) <= 1e-12 and abs(float(yy1) - yyo) <= 1e-12 * yyo
+    del G1h
     Gh = G.cpu().numpy()
     assert scale_err(Gh[np.ix_(idx, idx)], Go) <= 1e-12
     assert xty_err(c.cpu().numpy()[idx], co, Go, yyo) <= 1e-12

@@ -69,6 +69,11 @@ def test_one_rank_communicator_is_bitwise_identity(ctxs):
     la = oem_fit_logistic(plain, Xd, y01, nlambda=4)
     lb = oem_fit_logistic(nccl, Xd, y01, nlambda=4)
     assert torch.equal(la.beta, lb.beta) and la.outer_iters == lb.outer_iters
+    from paper_1801_09661_b200 import oem_gram_folds_sums, oem_gram_sums
+    for u, v in zip(oem_gram_sums(plain, Xd, yd), oem_gram_sums(nccl, Xd, yd)):
+        assert torch.equal(u, v) if torch.is_tensor(u) else u == v
+    for u, v in zip(oem_gram_folds_sums(plain, Xd, yd, 7, 3), oem_gram_folds_sums(nccl, Xd, yd, 7, 3)):
+        assert torch.equal(u, v) if torch.is_tensor(u) else u == v
     from paper_1801_09661_b200 import oem_gram_csr
     sspec = CONFIGS["sparse"].spec.replace(n=30_011)
     rp, col, val, ys = dg.csr_cuda(sspec, dg.beta(sspec))
