@@ -12,16 +12,17 @@
 //    [J_u, J_{u+1}) of the triangle; p = 200 fits one slice, 162 KB) and streams a contiguous row
 //    segment of the CSR arrays: one producer warp stages chunks of up to 256 rows / 768 nonzeros
 //    (row_ptr, y, col, val) into a 3-deep shared-memory ring with cp.async (completion through
-//    mbarrier arrive.noinc); a mask warp and 256 owner threads process them.
-//  * Consumer thread t OWNS triangle rows (columns) J_u + t, J_u + t + 256, ...: it alone updates
-//    G[j][k >= j] and G[j][p] for its columns. Per chunk the mask warp first marks, for every owned
-//    column j, which of the chunk's rows hold a nonzero in column j (a 256-bit row mask per column
-//    in the stage, set with shared-memory atomicOr: a bitwise OR is order-free); each owner walks its masks
-//    in ascending row order and, for every row with x_ij != 0, adds x_ij x_ik for the row's
-//    nonzeros k >= j and x_ij y_i. Work per chunk is proportional to the chunk's nonzeros and
-//    their row neighbours, with no conflicts and no redundant scanning; owner warps are coupled
-//    only through the ring (imbalance between chunks averages out). y^T y is a fixed-order warp
-//    sum per chunk (mask warp), added by the owner of the augmented column p.
+//    mbarrier arrive.noinc); four mask warps and 16 owner warps process them.
+//  * Owner lanes OWN triangle rows (columns): column c belongs to warp c % 16 (4 owner warps per
+//    SM sub-partition), lane (c / 16) % L; it alone updates G[j][k >= j] and G[j][p] for its
+//    columns. Per chunk the mask warps first mark, for every owned column j, which of the chunk's
+//    rows hold a nonzero in column j (a 256-bit row mask per column in the stage, set with
+//    shared-memory atomicOr: a bitwise OR is order-free); each owner walks its masks in ascending
+//    row order and, for every row with x_ij != 0, adds x_ij x_ik for the row's nonzeros k >= j and
+//    x_ij y_i. Work per chunk is proportional to the chunk's nonzeros and their row neighbours, with
+//    no conflicts and no redundant scanning; owner warps are coupled only through the ring
+//    (imbalance between chunks averages out). y^T y is a fixed-order warp sum per mask warp and
+//    chunk, added in warp order by the owner of the augmented column p.
 //  * Segments write their slice to a partial buffer; a second kernel adds the segments in a
 //    fixed order into the packed triangle (the NCCL allreduce and the unpack are shared with the
 //    dense path).
@@ -120,7 +121,7 @@ __device__ __forceinline__ void cp_async_arrive_noinc(uint64_t* bar) {
 }
 
 // Ring protocol per stage s: producer fills rows / nonzeros -> full[s] (32 cp.async arrivals +
-// the header arrive); the mask warp marks the owned columns' rows and the chunk's y^T y ->
+// the header arrive); the mask warps mark the owned columns' rows and the chunk's y^T y ->
 // ready[s]; every owner warp walks its columns, clears their mask words -> empty[s]. Owner warps
 // are coupled only through the ring, so a warp slowed by a dense column in one chunk catches up
 // on the next (up to SP_ST chunks of slack).
