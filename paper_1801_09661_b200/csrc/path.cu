@@ -106,11 +106,15 @@ __device__ __forceinline__ void group_barrier(unsigned* bar, int C) {
 // exact transcriptions of PAPER.md §2.2; lam is the weighted level (w_j lambda or c_k lambda)
 __device__ __forceinline__ double sgn(double u) { return u > 0.0 ? 1.0 : (u < 0.0 ? -1.0 : 0.0); }
 __device__ __forceinline__ double pos(double a) { return a > 0.0 ? a : 0.0; }
+// (a non-positive numerator gives pos(.) = 0 without dividing: the fp64 division routine is long,
+// and the thresholded coordinates of a sparse path are mostly zero)
 __device__ __forceinline__ double th_soft(double u, double lam, double d) {     // eq (lasso)
-  return sgn(u) * pos((fabs(u) - lam) / d);
+  const double t = fabs(u) - lam;
+  return t > 0.0 ? sgn(u) * (t / d) : 0.0;
 }
 __device__ __forceinline__ double th_enet(double u, double lam, double a, double d) {  // eq (net)
-  return sgn(u) * pos((fabs(u) - lam * a) / (d + lam * (1.0 - a)));
+  const double t = fabs(u) - lam * a;
+  return t > 0.0 ? sgn(u) * (t / (d + lam * (1.0 - a))) : 0.0;
 }
 // (a zero numerator is returned without dividing: 0/x takes the slow path of the fp64 division
 // routine on the GPU, and the thresholded coordinates of a sparse path are mostly zero)
@@ -136,6 +140,42 @@ __device__ __forceinline__ double th_coord(int fam, double u, double lam, double
     case OEM_ENET: return th_enet(u, lam, a, d);
     case OEM_MCP: return th_mcp(u, lam, g, d);
     default: return th_scad(u, lam, g, d);
+  }
+}
+
+// The same operators with the constant divisors' reciprocals precomputed (rd = 1/d; rg = 1/(g d - 1)
+// for MCP, 1/((g - 1) d - 1) for SCAD): each division becomes x r refined by one fused
+// multiply-add on the exact remainder (q = x r, q += (x - q den) r), the correctly rounded
+// quotient to within one ulp (~40 cycles of dependent FMAs instead of the ~130-cycle fp64
+// division routine, measured by tools/lat_probe.cu). Used by the lean solver, whose iteration
+// is one short dependent chain; the elastic net (a divisor that moves with lambda) divides.
+__device__ __forceinline__ double div_r(double x, double den, double r) {
+  const double q = x * r;
+  return fma(fma(-q, den, x), r, q);
+}
+__device__ __forceinline__ double th_coord_r(int fam, double u, double lam, double g, double a, double d, double rd,
+                                             double rg) {
+  switch (fam) {
+    case OEM_LASSO: {
+      const double t = fabs(u) - lam;
+      return t > 0.0 ? sgn(u) * div_r(t, d, rd) : 0.0;
+    }
+    case OEM_ENET: return th_enet(u, lam, a, d);
+    case OEM_MCP:
+      if (fabs(u) <= lam * g * d) {
+        const double t = pos(fabs(u) - lam);
+        return t > 0.0 ? div_r(sgn(u) * g * t, g * d - 1.0, rg) : 0.0;
+      }
+      return div_r(u, d, rd);
+    default: {
+      const double aa = fabs(u);
+      if (aa <= (d + 1.0) * lam) {
+        const double t = pos(aa - lam);
+        return t > 0.0 ? div_r(sgn(u) * t, d, rd) : 0.0;
+      }
+      if (aa <= lam * g * d) return div_r(sgn(u) * ((g - 1.0) * aa - lam * g), (g - 1.0) * d - 1.0, rg);
+      return div_r(u, d, rd);
+    }
   }
 }
 
@@ -755,6 +795,57 @@ __device__ __forceinline__ int vix(int q, int k, int pvl) {
 template <int NPT, int RT, int KC, int T, int NV, int VP, class GEL>
 __device__ __forceinline__ void lean_matvec(double (&a)[VP], const double* vc, int pvl, int kcu, int tl, GEL gel) {
   constexpr int MC = KC < 4 ? KC : 4;
+  if constexpr (NV <= 2) {
+    // one or two penalties per vector entry: software pipelined, the next chunk's loads issued
+    // before this chunk's FMAs (the vector buffers hold KC * T entries, so loading a chunk past
+    // kcu stays in bounds; it is never used). Same FMAs in the same order.
+    constexpr bool SPLIT = VP <= 4;
+    double a2[VP];
+#pragma unroll
+    for (int v = 0; v < VP; ++v) a2[v] = 0.0;
+    double bn[MC][NV];
+#pragma unroll
+    for (int mm = 0; mm < MC; ++mm)
+#pragma unroll
+      for (int h = 0; h < NV; ++h) bn[mm][h] = vc[NV * (tl + mm * T) + h];   // layout [k][NV] (vix)
+#pragma unroll
+    for (int m0 = 0; m0 < KC; m0 += MC) {
+      if (m0 >= kcu) break;
+      double b[MC][NV];
+#pragma unroll
+      for (int mm = 0; mm < MC; ++mm)
+#pragma unroll
+        for (int q = 0; q < NV; ++q) b[mm][q] = bn[mm][q];
+      if (m0 + MC < KC) {
+#pragma unroll
+        for (int mm = 0; mm < MC; ++mm) {
+          const int k = tl + (m0 + MC + mm) * T;
+          if (NV == 1) {
+            bn[mm][0] = vc[k];
+          } else {
+            const double2 t2 = *reinterpret_cast<const double2*>(vc + 2 * k);
+            bn[mm][0] = t2.x;
+            bn[mm][1] = t2.y;
+          }
+        }
+      }
+      // two interleaved chains per sum (even / odd chunks) halve the dependent-FMA depth when a
+      // thread has few sums; added at the end (a fixed order: deterministic)
+      double* acc = (SPLIT && ((m0 / MC) & 1)) ? a2 : a;
+#pragma unroll
+      for (int mm = 0; mm < MC; ++mm)
+#pragma unroll
+        for (int i = 0; i < RT; ++i) {
+          const double gv = gel(i, m0 + mm);
+#pragma unroll
+          for (int q = 0; q < NPT; ++q) acc[i * NPT + q] = fma(gv, b[mm][q], acc[i * NPT + q]);
+        }
+    }
+    if (SPLIT)
+#pragma unroll
+      for (int v = 0; v < VP; ++v) a[v] += a2[v];
+    return;
+  }
 #pragma unroll
   for (int m0 = 0; m0 < KC; m0 += MC) {
     if (m0 >= kcu) break;
@@ -950,16 +1041,20 @@ __global__ void __launch_bounds__(NTH, 1) fit_lean_kernel(const PathParams P, co
   bool grpm = false;
   for (int q = 0; q < nP; ++q) grpm = grpm || (grp && s_fam[q] >= OEM_GRP_LASSO);
   int fam_my[CNT];
-  double gam_my[CNT], alp_my[CNT];
+  double gam_my[CNT], alp_my[CNT], rg_my[CNT];
+  const double rd = 1.0 / d;
 #pragma unroll
   for (int s2 = 0; s2 < CNT; ++s2) {
     fam_my[s2] = s_fam[mq[s2]];
     gam_my[s2] = s_gam[mq[s2]];
     alp_my[s2] = s_alp[mq[s2]];
+    rg_my[s2] = fam_my[s2] == OEM_MCP ? 1.0 / (gam_my[s2] * d - 1.0)
+              : fam_my[s2] == OEM_SCAD ? 1.0 / ((gam_my[s2] - 1.0) * d - 1.0) : 0.0;
   }
   cluster_sync_all();  // every CTA's buffers are initialised before the first remote store
 
   // ======================================================= a9: OEM iterations
+  uint32_t nan_seen = 0;
   for (int t = 0;; ++t) {
     uint32_t qmask = 0;
 #pragma unroll
@@ -989,7 +1084,7 @@ __global__ void __launch_bounds__(NTH, 1) fit_lean_kernel(const PathParams P, co
 #pragma unroll
         for (int q = 0; q < NPT; ++q)
           if (q == mq[s2]) lq = lam[q];
-        const double nb = th_coord(fam_my[s2], u, w_my[s2] * lq, gam_my[s2], alp_my[s2], d);
+        const double nb = th_coord_r(fam_my[s2], u, w_my[s2] * lq, gam_my[s2], alp_my[s2], d, rd, rg_my[s2]);
         if (!(fabs(nb - bj) <= P.tol)) bits |= 1u << mq[s2];
         if (C == 1) vn[vi] = nb;
         else for (int rr = 0; rr < C; ++rr) st_cl_f64(&vn[vi], rr, nb);
@@ -1016,13 +1111,23 @@ __global__ void __launch_bounds__(NTH, 1) fit_lean_kernel(const PathParams P, co
                          });
       }
     }
-    bits = __reduce_or_sync(0xffffffffu, bits);
-    if (lane == 0 && bits) {
-      if (C == 1) atomicOr(&F[t % 3], bits);
-      else for (int rr = 0; rr < C; ++rr) red_or_cl(&F[t % 3], rr, bits);
+    uint32_t f;
+    if (NPT == 1 && C == 1) {
+      // one CTA, one penalty: the barrier itself ORs the "not converged" predicate (bar.red.or),
+      // no shared flag word on the iteration's critical path. A non-finite u also leaves its
+      // coordinate "not converged"; that is reduced every 64 iterations (sticky per thread)
+      nan_seen |= bits >> 31;
+      f = __syncthreads_or((int)(bits & 1u)) ? 1u : 0u;
+      if ((t & 63) == 63 && __syncthreads_or((int)nan_seen)) f |= 0x80000000u;
+    } else {
+      bits = __reduce_or_sync(0xffffffffu, bits);
+      if (lane == 0 && bits) {
+        if (C == 1) atomicOr(&F[t % 3], bits);
+        else for (int rr = 0; rr < C; ++rr) red_or_cl(&F[t % 3], rr, bits);
+      }
+      sync_all();
+      f = F[t % 3];
     }
-    sync_all();
-    const uint32_t f = F[t % 3];
     if (f & 0x80000000u) {
       if (tid == 0) atomicExch(&P.flags[0], 1);
       break;
@@ -1049,6 +1154,8 @@ __global__ void __launch_bounds__(NTH, 1) fit_lean_kernel(const PathParams P, co
       }
     }
   }
+  // the periodic non-finite check of the one-CTA form, once more for the last iterations
+  if (NPT == 1 && C == 1 && __syncthreads_or((int)nan_seen) && tid == 0) atomicExch(&P.flags[0], 1);
 }
 
 // ---------------------------------------------------------------- K4+K5 lean, grid-wide variant
