@@ -1,6 +1,6 @@
 """Summarise `ncu --set full` reports (gpurun_out/*.ncu-rep) into profiles/ncu_summary_<round>.json.
 
-    python tools/ncu_summary.py r01 cfg4=gpurun_out/ncu_gram_cfg4.ncu-rep cfg5=...
+    python tools/ncu_summary.py r01 cfg4=gpurun_out/ncu_gram_cfg4.ncu-rep cfg5=... (or a --page raw --csv export)
 
 Per report: kernel name, duration, DRAM bytes read+write (the `traffic` of bench.py's roofline
 object), DMMA pipe utilisation, issue/stall ratios. Existing entries of the same file are kept.
@@ -34,7 +34,9 @@ SCALE = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "Tbyte": 1e12,
 
 
 def summarise(path):
-    out = subprocess.run(["ncu", "-i", path, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
+    # a report, or its `ncu -i <rep> --page raw --csv` export (summarised on the GPU box)
+    out = open(path).read() if path.endswith(".csv") else \
+        subprocess.run(["ncu", "-i", path, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
     rows = list(csv.reader(io.StringIO(out)))
     h, u, v = rows[0], rows[1], rows[2]
     res = {"kernel": v[h.index("Kernel Name")], "report": os.path.basename(path)}
