@@ -164,6 +164,7 @@ __device__ __forceinline__ void consume(const GramParams& P, const Cons& cs) {
                        P.p + 1 < 8 * (cs.job.bj0 + C);
   const bool ycopyA = (MODE == MODE_PLAIN || MODE == MODE_FOLD) && R > 0 && P.ones && !ycopy &&
                       P.p >= 8 * cs.job.bi0 && P.p < 8 * (cs.job.bi0 + R);
+  const bool anycopy = ycopy || ycopyA || onecopy;   // warp-uniform: one branch per stage
   // the staged value for the augmented column: y (PLAIN), y of fold kprime (FOLD), z (WZ: ys holds (w, z) pairs)
   const int yidx = lane * P.ystride + (MODE == MODE_FOLD ? cs.kprime : MODE == MODE_WZ ? 1 : 0);
   int st = 0;
@@ -175,10 +176,12 @@ __device__ __forceinline__ void consume(const GramParams& P, const Cons& cs) {
     double* pb = cs.two ? pa + (size_t)BK * ld : pa;
     double* ys = pa + P.ys_off;
     double* ws = ys + BK * P.ystride;
-    if (MODE != MODE_WEIGHTED && ycopy) pb[lane * ld + ycol] = ys[yidx];
-    if (ycopyA) pa[lane * ld + P.p - cs.a0] = ys[yidx];
-    if (onecopy) pb[lane * ld + ycol + 1] = cs.r0 + (int64_t)s * BK + lane < cs.r1 ? 1.0 : 0.0;
-    if (ycopy || ycopyA || onecopy) __syncwarp();
+    if (MODE != MODE_WEIGHTED && anycopy) {
+      if (ycopy) pb[lane * ld + ycol] = ys[yidx];
+      if (ycopyA) pa[lane * ld + P.p - cs.a0] = ys[yidx];
+      if (onecopy) pb[lane * ld + ycol + 1] = cs.r0 + (int64_t)s * BK + lane < cs.r1 ? 1.0 : 0.0;
+      __syncwarp();
+    }
     if (KIND != J_NONE) {
       const double* pak = pa + aoff;
       const double* pbk = pb + boff;
@@ -210,7 +213,7 @@ __device__ __forceinline__ void consume(const GramParams& P, const Cons& cs) {
         pbk += 4 * ld;
       }
     }
-    if (ycopy || ycopyA || onecopy) fence_proxy_async_smem();  // generic smem writes precede the next TMA refill
+    if (MODE != MODE_WEIGHTED && anycopy) fence_proxy_async_smem();  // generic smem writes precede the next TMA refill
     __syncwarp();
     if (cs.lane == 0) mbar_arrive(&cs.empty[st]);
     if (++st == P.ST) { st = 0; ph ^= 1u; }
@@ -827,21 +830,28 @@ static oem_status build_plan(oem_ctx* ctx, int mode, int p, int64_t nrows, int K
     }
   }
   pl.U = (int)pl.ctas.size();
-  // Two-panel plans dispatch the costlier off-diagonal tiles first (U_off), in up to 48 waves of
-  // long segments whose partial blocks a fixed-order kernel sums. DRAM traffic studies at cfg4
-  // (profiles/cfg4_l2_schedule_r02.md; the kernel is DMMA-bound with HBM at ~20% of its peak, so
-  // re-reads cost no time): this default reads X 4.6x from DRAM (372 GB) at 288.3 ms; 384 waves of
-  // short segments, segment-major, every tile type of a segment together (OEM_GRAM_LPT=0
-  // OEM_GRAM_WAVES=384) read 97.6 GB (1.22x) at the same kernel time but add 1.4 ms of reduction
+  // Two-panel fold / WZ plans dispatch the costlier off-diagonal tiles first (U_off), in up to 48
+  // waves of long segments whose partial blocks a fixed-order kernel sums. DRAM traffic studies at
+  // cfg4 (profiles/cfg4_l2_schedule_r02.md; the kernel is DMMA-bound with HBM at ~20% of its
+  // peak, so re-reads cost no kernel time): that schedule reads X 4.6-4.9x from DRAM (372-389 GB)
+  // at 288.3 ms; 384 waves of short segments, segment-major, every tile type of a segment
+  // together (the plain two-panel default since round 2; OEM_GRAM_LPT=1 OEM_GRAM_WAVES=48 restores
+  // the other) read 97.0-97.6 GB (1.21x) at the same kernel time but add 1.4 ms of reduction
   // (6.4 GB of partial blocks); the same schedule with the segments added in order into running
   // sums inside the kernel (OEM_GRAM_ORDERED=1: no partial blocks) reads 102.7 GB but runs
-  // 294.9 ms. The default keeps the fastest Gram phase.
+  // 294.9 ms.
   const char* ordv = std::getenv("OEM_GRAM_ORDERED");
   // (plain and WZ passes only: a fold pass splits every segment into K items whose same-tile
   // neighbours run in the same wave; cfg3 went 74.5 -> 124.5 ms ordered)
   pl.ordered = (pl.two_panel && mode != MODE_FOLD && ordv && ordv[0] == '1') ? 1 : 0;
+  // plain two-panel passes default to the segment-major schedule of short segments (below): the
+  // same kernel time with ~4x less DRAM traffic (cfg4: 388.6 -> 97.0 GB read, 1.21x the
+  // algorithmic bytes; the whole call +1.4 ms = 0.5% for the larger split-n reduction). Fold
+  // passes keep the costliest-first order: there the short segments cost kernel time (cfg3 384
+  // waves: 44.3 GB = 1.10x but +1.2% kernel, +2.6% call; profiles/cfg4_l2_schedule_r02.md)
+  const bool seg_major = pl.two_panel && mode == MODE_PLAIN && !pl.ordered;
   const char* lpt = std::getenv("OEM_GRAM_LPT");  // developer override (timing studies): 0 / 1
-  const bool use_lpt = lpt ? lpt[0] == '1' : !pl.ordered;
+  const bool use_lpt = lpt ? lpt[0] == '1' : !pl.ordered && !seg_major;
   if (!pl.two_panel || pl.U_off == 0 || !use_lpt) pl.U_off = pl.U;
   // y staging: 1D TMA box (PLAIN/WEIGHTED); FOLD: 2D box [BK][Kpad] over y viewed as [nq][K]
   // (needs K*8 % 16 == 0, i.e. even K), else the producer's lanes load it
@@ -877,7 +887,7 @@ static oem_status build_plan(oem_ctx* ctx, int mode, int p, int64_t nrows, int K
   // smaller split-n reduction, fewer pipeline fills. Measured (whole call): cfg2 4 waves 0.396 ms,
   // 2 waves 0.390, 1 wave 0.382; cfg5 weighted pass 33 waves 8.42 ms, 8 waves 8.19, 2 waves 8.16;
   // two-panel plans need many waves to balance their unequal tiles (cfg4: 8 waves 301 ms, 48: 288)
-  const double w_fit = std::min(pl.ordered ? 384.0 : pl.two_panel ? 48.0 : 2.0, (double)units / 64.0 / per_wave);
+  const double w_fit = std::min(pl.ordered || seg_major ? 384.0 : pl.two_panel ? 48.0 : 2.0, (double)units / 64.0 / per_wave);
   const int waves = wv ? std::max(1, std::atoi(wv)) : std::max(1, (int)std::ceil(w_fit));
   int64_t want = std::max<int64_t>(1, (int64_t)std::llround(waves * per_wave));
   want = std::min<int64_t>(want, std::max<int64_t>(1, units / 8));
