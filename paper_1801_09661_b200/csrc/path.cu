@@ -2145,6 +2145,9 @@ struct LeanLayout {
   std::vector<int> cuts;  // C + 1 row cuts (group aligned)
 };
 
+static bool lean_layout_try(int p, int NPT, const std::vector<int>& gstart, int v, int R, int KC, int T, int RS,
+                            int NTH, LeanLayout& lo);
+
 static bool make_lean_layout(int p, int NPT, const std::vector<int>& gstart, LeanLayout& lo) {
   // variants: rows per CTA = R * 512 / T, columns = KC * T
   // variant 5: 32 register rows + 32 shared-memory rows per CTA (p <= 512, clusters of <= 8)
@@ -2152,20 +2155,35 @@ static bool make_lean_layout(int p, int NPT, const std::vector<int>& gstart, Lea
   // variants 7, 8: four lanes per row (short reduce-scatter, 32-column FMA chains), 256 / 512 threads
   // variant 9: 256 threads, 4 rows x 16 columns per thread (the 256-thread form of variant 2)
   // variant 10: 256 threads, 4 register + 4 shared-memory rows per thread (the 256-thread form of 5)
-  static const int R_[11] = {1, 2, 2, 1, 1, 2, 4, 2, 1, 4, 4},
-                   KC_[11] = {8, 16, 16, 8, 16, 16, 16, 32, 32, 16, 16},
-                   T_[11] = {8, 8, 16, 16, 16, 32, 8, 4, 4, 16, 32}, RS_[11] = {0, 0, 0, 0, 0, 2, 0, 0, 0, 0, 4},
-                   NTH_[11] = {PT, PT, PT, PT, PT, PT, 256, 256, PT, 256, 256};
+  // variant 11: 256 threads, 4 register + 4 shared-memory rows x 16 columns per thread, 16 lanes
+  // per row (128 rows per CTA: p <= 256 in clusters of 2)
+  // variant 12: 256 threads, 2 rows x 16 columns per thread, 16 lanes per row (32 rows per CTA:
+  // p <= 256 in clusters of up to 8)
+  static const int R_[13] = {1, 2, 2, 1, 1, 2, 4, 2, 1, 4, 4, 4, 2},
+                   KC_[13] = {8, 16, 16, 8, 16, 16, 16, 32, 32, 16, 16, 16, 16},
+                   T_[13] = {8, 8, 16, 16, 16, 32, 8, 4, 4, 16, 32, 16, 16},
+                   RS_[13] = {0, 0, 0, 0, 0, 2, 0, 0, 0, 0, 4, 4, 0},
+                   NTH_[13] = {PT, PT, PT, PT, PT, PT, 256, 256, PT, 256, 256, 256, 256};
   // measured (path phase, one B200): p = 20 variant 0 0.83 -> 7 0.76 us/iteration; p = 100
   // (cfg2) 1 1.01 -> 7 0.88; p = 200 (cfg5 inner solves) 2 96.7 ms -> 9 83.2 ms; p = 500 (cfg3)
   // 5 2.49 -> 10 2.18 us/iteration
-  int v = p <= 128 ? 7 : p <= 256 ? 9 : p <= 512 ? 10 : -1;
+  // p = 200 (sparse workload paths, 2 penalties): variant 9 (C = 4) 2.96 -> 12 (C = 7) 2.16
+  // us/iteration, 11 (C = 2) 4.79; variant 12 needs groups of <= 32 columns, else 9
+  std::vector<int> cand = p <= 128 ? std::vector<int>{7} : p <= 256 ? std::vector<int>{12, 9}
+                        : p <= 512 ? std::vector<int>{10} : std::vector<int>{};
   if (const char* ev = std::getenv("OEM_LEAN_VARIANT")) {  // developer override (timing studies)
     const int f = std::atoi(ev);
-    if (f >= 0 && f < 11 && KC_[f] * T_[f] >= p) v = f;
+    if (f >= 0 && f < 13 && KC_[f] * T_[f] >= p) cand = {f};
   }
-  if (v < 0 || NPT > 4) return false;
-  const int rows = (R_[v] + RS_[v]) * (NTH_[v] / T_[v]);
+  if (NPT > 4) return false;
+  for (int v : cand)
+    if (lean_layout_try(p, NPT, gstart, v, R_[v], KC_[v], T_[v], RS_[v], NTH_[v], lo)) return true;
+  return false;
+}
+
+static bool lean_layout_try(int p, int NPT, const std::vector<int>& gstart, int v, int R, int KC, int T, int RS,
+                            int NTH, LeanLayout& lo) {
+  const int rows = (R + RS) * (NTH / T);
   // contiguous row blocks of <= rows rows, cut only at group starts (greedy packing)
   std::vector<int> cuts{0};
   if (gstart.empty()) {
@@ -2192,10 +2210,10 @@ static bool make_lean_layout(int p, int NPT, const std::vector<int>& gstart, Lea
   lo.variant = v;
   lo.C = C;
   lo.rows = rows;
-  lo.pvl = KC_[v] * T_[v];
+  lo.pvl = KC * T;
   lo.cuts = cuts;
   const int NV = NPT == 1 ? 1 : 2 * ((NPT + 1) / 2);
-  lo.smem = ((size_t)2 * NV * lo.pvl + (size_t)RS_[v] * (NTH_[v] / T_[v]) * lo.pvl + (size_t)2 * C * (NTH_[v] / 32) +
+  lo.smem = ((size_t)2 * NV * lo.pvl + (size_t)RS * (NTH / T) * lo.pvl + (size_t)2 * C * (NTH / 32) +
              (size_t)NPT * rows + rows) * 8 +
             (size_t)2 * rows * 4 + 16;
   return true;
@@ -2273,6 +2291,8 @@ static oem_status launch_lean_v(const PathParams& P, const LeanArgs& A, int nU, 
   if (lo.variant == 8) return launch_lean_nth<NPT, 1, 32, 4, PT>(P, A, nU, lo.smem, st);
   if (lo.variant == 9) return launch_lean_nth<NPT, 4, 16, 16, 256>(P, A, nU, lo.smem, st);
   if (lo.variant == 10) return launch_lean_nth<NPT, 4, 16, 32, 256, 4>(P, A, nU, lo.smem, st);
+  if (lo.variant == 11) return launch_lean_nth<NPT, 4, 16, 16, 256, 4>(P, A, nU, lo.smem, st);
+  if (lo.variant == 12) return launch_lean_nth<NPT, 2, 16, 16, 256>(P, A, nU, lo.smem, st);
   return launch_lean_t<NPT, 2, 16, 16>(P, A, nU, lo.smem, st);
 }
 
