@@ -2645,8 +2645,10 @@ extern "C" oem_status oem_fit_path(oem_ctx* ctx, const double* G, const double* 
   const bool want_act = fs == "active" || (fs.empty() && p > 256);
   const std::vector<int> gs_act = any_grp ? gstart : std::vector<int>();
   ActLayout al128;
-  const bool act256 = want_act && make_act_layout(p, gs_act, al, 256);
-  const bool act512 = want_act && p > 512 && make_act_layout(p, gs_act, al128, 512);
+  const char* ath = std::getenv("OEM_ACT_THREADS");   // developer override (timing studies): 256 / 512
+  const int force_th = ath ? std::atoi(ath) : 0;
+  const bool act256 = want_act && force_th != 512 && make_act_layout(p, gs_act, al, 256);
+  const bool act512 = want_act && (p > 512 || force_th == 512) && force_th != 256 && make_act_layout(p, gs_act, al128, 512);
   if (act512 && (!act256 || al128.C < al.C)) al = al128;
   const bool use_act = act256 || act512;
   const bool use_lean = !use_act && !(fs == "global" || fs == "cluster") &&
