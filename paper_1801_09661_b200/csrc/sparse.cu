@@ -55,7 +55,8 @@ struct SpStage {  // shared-memory layout of one ring stage (byte offsets); mask
   static constexpr int val = y + SP_ROWS * 8;
   static constexpr int col = val + SP_ENT * 8;
   static constexpr int hdr = col + SP_ENT * 4;   // int R, pad, int64 e0, double yy[SP_NMASK] (the chunk's y^T y)
-  static constexpr int mask = (hdr + 16 + 8 * SP_NMASK + 127) / 128 * 128;
+  static constexpr int rs = hdr + 16 + 8 * SP_NMASK;   // int16 [SP_ROWS + 1]: row offsets relative to e0 (mask warps)
+  static constexpr int summ = (rs + 2 * (SP_ROWS + 1) + 15) / 16 * 16;   // one byte per mask slot: its non-empty words
 };
 // The masks are stored word-major and, within a word, in OWNER order: with L = 2^lgl lanes per
 // owner warp per round (the least power of two with SP_WARPS L >= ncol, at most 32), column c is
@@ -75,7 +76,9 @@ __host__ __device__ constexpr int mask_ld(int ncol) {
 __device__ __forceinline__ int mask_slot(int c, int lgl) {
   return (c & ~((SP_WARPS << lgl) - 1)) | ((c & (SP_WARPS - 1)) << lgl) | ((c >> SP_LGW) & ((1 << lgl) - 1));
 }
-__host__ __device__ constexpr int stage_bytes(int ncol) { return SpStage::mask + (mask_ld(ncol) * SP_MW * 4 + 127) / 128 * 128; }
+// the masks follow the per-slot summary bytes (mask_ld(ncol) of them)
+__host__ __device__ constexpr int mask_off(int ncol) { return (SpStage::summ + mask_ld(ncol) + 127) / 128 * 128; }
+__host__ __device__ constexpr int stage_bytes(int ncol) { return mask_off(ncol) + (mask_ld(ncol) * SP_MW * 4 + 127) / 128 * 128; }
 
 struct SpParams {
   const int64_t* row_ptr;
@@ -142,8 +145,10 @@ __global__ void __launch_bounds__(SP_THREADS, 1) sparse_gram_kernel(const SpPara
   double* gs = reinterpret_cast<double*>(sbytes + (size_t)SP_ST * P.sbytes);
   for (int64_t e = threadIdx.x; e < nent; e += SP_THREADS) gs[e] = 0.0;
   for (int s = 0; s < SP_ST; ++s) {
-    uint32_t* m = reinterpret_cast<uint32_t*>(sbytes + (size_t)s * P.sbytes + SpStage::mask);
+    uint32_t* m = reinterpret_cast<uint32_t*>(sbytes + (size_t)s * P.sbytes + mask_off(ncol));
     for (int e = threadIdx.x; e < mask_ld(ncol) * SP_MW; e += SP_THREADS) m[e] = 0u;
+    uint32_t* sm4 = reinterpret_cast<uint32_t*>(sbytes + (size_t)s * P.sbytes + SpStage::summ);
+    for (int e = threadIdx.x; e < mld / 4; e += SP_THREADS) sm4[e] = 0u;
   }
   if (threadIdx.x == 0) {
     for (int s = 0; s < SP_ST; ++s) {
@@ -242,13 +247,27 @@ __global__ void __launch_bounds__(SP_THREADS, 1) sparse_gram_kernel(const SpPara
       const int64_t* rp_s = reinterpret_cast<const int64_t*>(sb + SpStage::rp);
       const double* y_s = reinterpret_cast<const double*>(sb + SpStage::y);
       const int32_t* c_s = reinterpret_cast<const int32_t*>(sb + SpStage::col);
-      uint32_t* mask = reinterpret_cast<uint32_t*>(sb + SpStage::mask);
+      int16_t* rs = reinterpret_cast<int16_t*>(sb + SpStage::rs);
+      uint32_t* summ = reinterpret_cast<uint32_t*>(sb + SpStage::summ);
+      uint32_t* mask = reinterpret_cast<uint32_t*>(sb + mask_off(ncol));
+      // the stage's masks and summaries start from zero (the owners only read them): the mask
+      // warps clear them, then meet at a named barrier before marking
+      const int tm = 32 * m + lane;
+      for (int e = tm; e < mld * SP_MW / 4; e += 32 * SP_NMASK) reinterpret_cast<uint4*>(mask)[e] = make_uint4(0u, 0u, 0u, 0u);
+      for (int e = tm; e < mld / 4; e += 32 * SP_NMASK) summ[e] = 0u;
+      named_bar_sync(1, 32 * SP_NMASK);
       double yy = 0.0;
-      for (int q = 32 * m + lane; q < R; q += 32 * SP_NMASK) {   // warp m, lane: rows 32 m + lane + 128 t
+      if (tm == 0) rs[R] = (int16_t)(rp_s[R] - e0);
+      for (int q = tm; q < R; q += 32 * SP_NMASK) {   // warp m, lane: rows 32 m + lane + 128 t
         const int a0 = (int)(rp_s[q] - e0), a1 = (int)(rp_s[q + 1] - e0);
+        rs[q] = (int16_t)a0;
         for (int a = a0; a < a1; ++a) {
           const int c = c_s[a] - J0;
-          if (c >= 0 && c < ncol) atomicOr(&mask[(q >> 5) * mld + mask_slot(c, lgl)], 1u << (q & 31));
+          if (c >= 0 && c < ncol) {
+            const int sl = mask_slot(c, lgl);
+            atomicOr(&mask[(q >> 5) * mld + sl], 1u << (q & 31));
+            atomicOr(&summ[sl >> 2], 1u << ((q >> 5) + 8 * (sl & 3)));   // word q/32 of slot sl is non-empty
+          }
         }
         yy = fma(y_s[q], y_s[q], yy);
       }
@@ -279,13 +298,12 @@ __global__ void __launch_bounds__(SP_THREADS, 1) sparse_gram_kernel(const SpPara
     const int* h = reinterpret_cast<const int*>(sb + SpStage::hdr);
     const int R = h[0];
     if (R == 0) break;
-    const int64_t e0 = *reinterpret_cast<const int64_t*>(h + 2);
-    const int64_t* rp_s = reinterpret_cast<const int64_t*>(sb + SpStage::rp);
+    const int16_t* rs = reinterpret_cast<const int16_t*>(sb + SpStage::rs);
     const double* y_s = reinterpret_cast<const double*>(sb + SpStage::y);
     const double* v_s = reinterpret_cast<const double*>(sb + SpStage::val);
     const int32_t* c_s = reinterpret_cast<const int32_t*>(sb + SpStage::col);
-    uint32_t* mask = reinterpret_cast<uint32_t*>(sb + SpStage::mask);
-    const int nw = (R + 31) / 32;
+    const uint32_t* summ = reinterpret_cast<const uint32_t*>(sb + SpStage::summ);
+    const uint32_t* mask = reinterpret_cast<const uint32_t*>(sb + mask_off(ncol));
     for (int i = 0;; i += SP_WARPS << lgl) {
       const int c = i + (lane << SP_LGW) + warp;   // the column of mask slot i + ct
       if (lane >> lgl || c >= ncol) break;
@@ -299,17 +317,10 @@ __global__ void __launch_bounds__(SP_THREADS, 1) sparse_gram_kernel(const SpPara
         grow[p] += yy;
         continue;
       }
-      // the column's row mask, loaded whole (independent, conflict-free loads) and cleared for
-      // the stage's next use; then its set bits in ascending row order, each lane at its own pace
-      uint32_t mw[SP_MW], nzw = 0u;   // nzw: the non-empty words
-#pragma unroll
-      for (int w = 0; w < SP_MW; ++w) {
-        mw[w] = w < nw ? mask[w * mld + i + ct] : 0u;
-        if (mw[w]) {
-          mask[w * mld + i + ct] = 0u;
-          nzw |= 1u << w;
-        }
-      }
+      // the column's non-empty mask words (its summary byte), then their set bits in ascending
+      // row order, each lane at its own pace (a word is loaded when the walk reaches it)
+      const int sl = i + ct;
+      uint32_t nzw = (summ[sl >> 2] >> (8 * (sl & 3))) & 0xffu;
       int w = 0;
       uint32_t bits = 0u;
       for (;;) {   // one set bit per trip: a lane's trip count is its column's nonzeros in the chunk
@@ -317,14 +328,12 @@ __global__ void __launch_bounds__(SP_THREADS, 1) sparse_gram_kernel(const SpPara
           if (!nzw) break;
           w = __ffs(nzw) - 1;
           nzw &= nzw - 1;
-          bits = mw[0];
-#pragma unroll
-          for (int t = 1; t < SP_MW; ++t) bits = w == t ? mw[t] : bits;
+          bits = mask[w * mld + sl];
         }
         const int q = 32 * w + __ffs(bits) - 1;
         bits &= bits - 1;
-        const int a0 = (int)(rp_s[q] - e0);
-        const int a1 = (int)(rp_s[q + 1] - e0);
+        const int a0 = rs[q];
+        const int a1 = rs[q + 1];
         // the row's nonzero in column j, four columns per probe: the row's columns ascend and
         // are distinct, so the first match is it (slots past the row end come after it)
         int a = a0;
@@ -406,11 +415,11 @@ extern "C" oem_status oem_gram_csr(oem_ctx* ctx, const int64_t* row_ptr, const i
   std::vector<int> sj;
   int64_t cap = 0;
   int sbytes = 0;
-  for (int64_t budget = (int64_t)SP_SMEM_MAX - 1024 - (int64_t)SP_ST * SpStage::mask; budget > 0; budget -= 4096) {
+  for (int64_t budget = (int64_t)SP_SMEM_MAX - 1024 - (int64_t)SP_ST * SpStage::summ; budget > 0; budget -= 4096) {
     sj.assign(1, 0);
     int64_t cur = 0;
     for (int j = 0; j <= p; ++j) {
-      const int64_t need = 8 * (pa - j) + (int64_t)SP_ST * 4 * SP_MW;
+      const int64_t need = 8 * (pa - j) + (int64_t)SP_ST * (4 * SP_MW + 1);
       if (cur + need > budget && cur > 0) { sj.push_back(j); cur = 0; }
       cur += need;
     }
