@@ -20,6 +20,7 @@
 #include <cmath>
 #include <cstring>
 #include <numeric>
+#include <type_traits>
 #include <vector>
 
 #include <cstdlib>
@@ -672,7 +673,11 @@ struct ClusterArgs {
   int maxrows;    // max rows per CTA (shared-memory row tables)
 };
 
+// (.aligned: every thread of the warp executes it convergently, so the warp is reconverged first;
+// a warp arriving while one lane still runs a divergent tail of remote stores could complete the
+// barrier before those stores are issued)
 __device__ __forceinline__ void cluster_sync_all() {
+  __syncwarp();
   asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
 }
 __device__ __forceinline__ uint32_t cluster_rank() {
@@ -1844,22 +1849,50 @@ __global__ void __launch_bounds__(PT, 1) fit_cluster_kernel(const PathParams P, 
 // row k). Columns beyond the shared-memory capacity are read from the L2-resident Gram.
 // Skipping a column whose coordinate is exactly zero changes no sum (its terms are exact zeros);
 // the sum order over the active list differs from the dense solvers' column order (rounding only).
+//
+// Screened compact iterations (the iterates are the paper's, up to rounding). Between full
+// iterations the coordinates outside the active set A are provably still zero. At a full
+// iteration t0 every inactive coordinate j (or inactive group g) has a zero-test slack
+// tau - z(u(t0)) (z = |u_j|, or the group M-step's norm, tau its threshold; z is 1-Lipschitz in u),
+// and for a later iteration s, u_j(s) - u_j(t0) = -sum_{k in A} G_jk (b_k(s-1) - b_k(t0-1)), so
+// |du_j| <= ||G_{j,A}||_2 D with D = ||b(s-1) - b(t0-1)||_2 (a group: ||G_{g,A}||_F D). The full
+// iteration measures those norms over A and every CTA forms the same minimum s_min of
+// (tau - z - rounding) / ||G_{j,A}||; while D (+ a rounding term) <= s_min, the iteration restricted
+// to the rows and columns of A equals the full iteration (every inactive threshold returns 0), so
+// CTA 0 runs those iterations alone, in one warp (one or two rows per lane) with G_AA in shared
+// memory: no cluster barrier, no exchange. D is bounded by per-coordinate running maxima, checked
+// every CW iterations and at the exit; a failed check rolls back to the last certified iterate and
+// the cluster resumes full iterations (every lambda starts with one, which re-derives the slacks).
+// For group families A holds whole groups.
 struct ActArgs {
   int C;          // CTAs per cluster
   int amax;       // active columns cached per CTA
   int apitch;     // shared-memory pitch of a cached row (doubles)
   int rows;       // max rows per CTA (<= 64)
   int pw;         // 32-bit words of a p-bit set
+  int screen;     // 1: screened compact iterations between full ones
+  int ncmax;      // compact capacity (32, 64 or, 256-thread CTAs, 128 active coordinates; 0: no screening)
 };
 
 constexpr int ACT_T = 4;         // lanes per row
+constexpr int CW = 8;            // compact iterations per screening check
+
+__device__ __forceinline__ void st_cl_s32(int* local, uint32_t rank, int v) {
+  uint32_t a = smem_u32(local), ra;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(ra) : "r"(a), "r"(rank));
+  asm volatile("st.shared::cluster.s32 [%0], %1;" ::"r"(ra), "r"(v) : "memory");
+}
 
 template <int ACT_THREADS>       // 256 (64 rows per CTA) or 512 (128 rows per CTA)
 __global__ void __launch_bounds__(ACT_THREADS, 1) fit_active_kernel(const PathParams P, const ActArgs A) {
   extern __shared__ __align__(16) double sm[];
   __shared__ uint32_t F[3];
+  // per (CTA, warp) of a full iteration (parity t & 1): minimum screening slack, sum of (db_j)^2,
+  // sum of b_j(t0-1)^2
+  __shared__ double SLs[2][3][256];
   __shared__ int s_na;
   __shared__ double s_lmax;
+  __shared__ int s_oc[2];                // compact phase: outcome, iterations
   const int p = P.p, nPg = P.nP, L = P.L, C = A.C;
   const int clu = blockIdx.x / C;
   const int unit = clu / nPg, q = clu % nPg;   // one penalty per cluster
@@ -1870,11 +1903,18 @@ __global__ void __launch_bounds__(ACT_THREADS, 1) fit_active_kernel(const PathPa
   const double* Gu = P.Gn + (size_t)unit * p * p;
   const double* cu = P.cn + (size_t)unit * p;
   const int pv = (p + 1) & ~1;
-  // shared memory: vec [2][pv] | ga [rows][apitch] | uv [rows] | gw, ga_s, gb_s [rows] | act [amax] | abits, nbits [2][pw]
+  const int NCM = A.ncmax;
+  // shared memory: vec [2][pv] | gc [NCM][NCM] | bcv [2][NCM] | res, ucv, cwv [NCM] | ga [rows][apitch] |
+  //                uv [2][rows] | gw, ga_s, gb_s [rows] | act [p] | abits, nbits [2][pw]
   double* vec = sm;
-  double* ga = vec + 2 * (size_t)pv;
-  double* uv = ga + (size_t)A.rows * A.apitch;
-  double* gw_s = uv + A.rows;
+  double* gc = vec + 2 * (size_t)pv;
+  double* bcv = gc + (size_t)NCM * NCM;
+  double* res = bcv + 2 * (size_t)NCM;
+  double* ucv = res + NCM;
+  double* cwv = ucv + NCM;
+  double* ga = cwv + NCM;
+  double* uv = ga + (size_t)A.rows * A.apitch;   // [2][rows]: u, then ||G_{j,A}||^2 (screening)
+  double* gw_s = uv + 2 * A.rows;
   int* ga_s = reinterpret_cast<int*>(gw_s + A.rows);
   int* gb_s = ga_s + A.rows;
   int* act = gb_s + A.rows;
@@ -1891,6 +1931,7 @@ __global__ void __launch_bounds__(ACT_THREADS, 1) fit_active_kernel(const PathPa
     gb_s[gg] = P.g_end[g0 + gg] - j0;
   }
   // warm or cold start (permuted order) into both buffers; the initial active set is its support
+  // (whole groups for a group family)
   for (int k = tid; k < pv; k += ACT_THREADS) {
     const double b = (P.beta_init && k < p) ? P.beta_init[((size_t)unit * nPg + q) * p + P.perm[k]] : 0.0;
     vec[k] = b;
@@ -1901,8 +1942,19 @@ __global__ void __launch_bounds__(ACT_THREADS, 1) fit_active_kernel(const PathPa
   __syncthreads();
   if (tid == 0) {
     int na = 0;
-    for (int k = 0; k < p; ++k)
-      if (vec[k] != 0.0) { act[na++] = k; abits[k >> 5] |= 1u << (k & 31); }
+    if (P.beta_init) {
+      for (int k = 0; k < p; ++k)
+        if (vec[k] != 0.0) abits[k >> 5] |= 1u << (k & 31);
+      if (grp)
+        for (int gg = 0; gg < P.ngroups; ++gg) {
+          bool on = false;
+          for (int k = P.g_start[gg]; k < P.g_end[gg]; ++k) on = on || ((abits[k >> 5] >> (k & 31)) & 1u);
+          if (on)
+            for (int k = P.g_start[gg]; k < P.g_end[gg]; ++k) abits[k >> 5] |= 1u << (k & 31);
+        }
+      for (int k = 0; k < p; ++k)
+        if ((abits[k >> 5] >> (k & 31)) & 1u) act[na++] = k;
+    }
     s_na = na;
   }
   __syncthreads();
@@ -1914,6 +1966,8 @@ __global__ void __launch_bounds__(ACT_THREADS, 1) fit_active_kernel(const PathPa
   const double d = P.d[unit];
   const double c_my = r < nr ? cu[j0 + r] : 0.0;
   const double w_my = (r < nr && P.var_w) ? P.var_w[j0 + r] : 1.0;
+  // rounding scale of a computed u_j (gamma_{p+4}, times a safety factor of 4)
+  const double gam_u = 4.0 * (p + 4) * 1.1102230246251565e-16;
   // ---- a8: lambda grid of this (unit, penalty) (R#14-16, R#22), as in the other solvers
   if (warp == 0) {
     double lm = 0.0;
@@ -1961,7 +2015,14 @@ __global__ void __launch_bounds__(ACT_THREADS, 1) fit_active_kernel(const PathPa
     for (int l = tid; l < L; l += ACT_THREADS) P.lam_out[((size_t)unit * nPg + q) * L + l] = lam_at(l);
   int lidx = 0, itc = 0;
   double lam = lam_at(0);
+  const double rd = 1.0 / d;
+  // (the group families' norm thresholds are the coordinate MCP / SCAD ones)
+  const double rgq = (fam == OEM_MCP || fam == OEM_GRP_MCP) ? 1.0 / (gq * d - 1.0)
+                   : (fam == OEM_SCAD || fam == OEM_GRP_SCAD) ? 1.0 / ((gq - 1.0) * d - 1.0) : 0.0;
+  int cfail = 0, cwait = 0;      // failed compact phases at this lambda; full iterations before the next
+  int built_na = -1;             // CTA 0: size of the active set whose G_AA is in gc
   cluster_sync_all();  // every CTA initialised before the first remote store
+  auto inA = [&](int k) -> bool { return (abits[k >> 5] >> (k & 31)) & 1u; };
 
   // ======================================================= a9: OEM iterations
   for (int t = 0; lidx < L; ++t) {
@@ -1970,45 +2031,136 @@ __global__ void __launch_bounds__(ACT_THREADS, 1) fit_active_kernel(const PathPa
     double* vn = vec + (size_t)(cur ^ 1) * pv;
     if (tid == 0) F[(t + 1) % 3] = 0u;
     // ---- E-step: u_j = c_j + d b_j - sum_{k active} G_jk b_k
-    double acc = 0.0;
+    // (screening: r2 = ||G_{j,A}||^2 over the same active columns)
+    double acc = 0.0, r2 = 0.0;
     if (r < nr) {
       const double* gr = ga + (size_t)r * A.apitch;
       const int nc = min(na, A.amax);
       int a = tl;
       for (; a + 3 * ACT_T < nc; a += 4 * ACT_T) {   // four independent loads in flight
         const double b0 = vc[act[a]], b1 = vc[act[a + ACT_T]], b2 = vc[act[a + 2 * ACT_T]], b3 = vc[act[a + 3 * ACT_T]];
-        acc = fma(gr[a], b0, acc);
-        acc = fma(gr[a + ACT_T], b1, acc);
-        acc = fma(gr[a + 2 * ACT_T], b2, acc);
-        acc = fma(gr[a + 3 * ACT_T], b3, acc);
+        const double g0 = gr[a], g1 = gr[a + ACT_T], g2 = gr[a + 2 * ACT_T], g3 = gr[a + 3 * ACT_T];
+        acc = fma(g0, b0, acc);
+        acc = fma(g1, b1, acc);
+        acc = fma(g2, b2, acc);
+        acc = fma(g3, b3, acc);
+        if (A.screen) r2 = fma(g3, g3, fma(g2, g2, fma(g1, g1, fma(g0, g0, r2))));
       }
-      for (; a < nc; a += ACT_T) acc = fma(gr[a], vc[act[a]], acc);
-      for (a = A.amax + tl; a < na; a += ACT_T) acc = fma(Gu[(size_t)act[a] * p + j0 + r], vc[act[a]], acc);  // beyond capacity
+      for (; a < nc; a += ACT_T) {
+        const double g0 = gr[a];
+        acc = fma(g0, vc[act[a]], acc);
+        r2 = fma(g0, g0, r2);
+      }
+      for (a = A.amax + tl; a < na; a += ACT_T) {  // beyond capacity
+        const double g0 = Gu[(size_t)act[a] * p + j0 + r];
+        acc = fma(g0, vc[act[a]], acc);
+        r2 = fma(g0, g0, r2);
+      }
     }
 #pragma unroll
-    for (int o = ACT_T / 2; o >= 1; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+    for (int o = ACT_T / 2; o >= 1; o >>= 1) {
+      acc += __shfl_xor_sync(0xffffffffu, acc, o);
+      r2 += __shfl_xor_sync(0xffffffffu, r2, o);
+    }
     uint32_t bits = 0;
+    double slk = INFINITY;   // this lane's screening slack (inactive coordinates / groups)
     const int j = j0 + r;
-    auto emit = [&](int jj, double nb) {   // new coordinate jj: vector copies, flags, activation
+    double dsq = 0.0, bsq = 0.0;   // screening: this lane's sum of (db_j)^2 and of b_j^2
+    auto emit = [&](int jj, double nb, bool req) {   // new coordinate jj: vector copies, flags, activation
       const double bj = vc[jj];
+      dsq = fma(nb - bj, nb - bj, dsq);
+      bsq = fma(bj, bj, bsq);
       if (!(fabs(nb - bj) <= P.tol)) bits |= 1u;
       if (nb != vn[jj])
         for (int rr = 0; rr < C; ++rr) st_cl_f64(&vn[jj], rr, nb);
-      if (nb != 0.0 && !((abits[jj >> 5] >> (jj & 31)) & 1u))
+      if (req && !inA(jj))
         for (int rr = 0; rr < C; ++rr) red_or_cl(&nbits[par * A.pw + (jj >> 5)], rr, 1u << (jj & 31));
     };
     if (tl == 0 && r < nr && lidx < L) {
       const double u = c_my + d * vc[j] - acc;
       if (!isfinite(u)) bits |= 0x80000000u;
-      if (!grp) emit(j, th_coord(fam, u, w_my * lam, gq, aq, d));
-      else uv[r] = u;
+      if (!grp) {
+        const double nb = th_coord(fam, u, w_my * lam, gq, aq, d);
+        emit(j, nb, nb != 0.0);
+        // zero iff |u| <= tau (lasso, MCP, SCAD: w lam; elastic net: w lam alpha); u_j moves by at
+        // most ||G_{j,A}|| ||db_A||, and its rounding by gam_u (|c_j| + ||G_{j,A}|| ||b||)
+        if (A.screen && nb == 0.0 && !inA(j) && r2 > 0.0) {
+          const double tau = w_my * lam * (fam == OEM_ENET ? aq : 1.0);
+          slk = fmax((tau - fabs(u) - 2.0 * gam_u * fabs(c_my) - 1e-13 * tau) / (sqrt(r2) * (1.0 + 1e-12)), 0.0);
+        }
+      } else {
+        uv[r] = u;
+        uv[A.rows + r] = r2;
+      }
     }
     if (grp) {
-      // group M-step (eqs glasso / gmcp / gscad / sglasso); groups lie inside [j0, j1)
+      // group M-step (eqs glasso / gmcp / gscad / sglasso; the arithmetic of
+      // group_mstep_warp); groups lie inside [j0, j1). A group enters the active set whole.
       __syncthreads();
-      for (int gl = warp; gl < ng_loc; gl += NW)
-        group_mstep_warp(uv, ga_s[gl], gb_s[gl], fam, lam, gq, aq, gw_s[gl], d, P.var_w, j0, lane,
-                         [&](int rr, double nb) { emit(j0 + rr, nb); });
+      const bool sgl = fam == OEM_SGL;
+      for (int gl = warp; gl < ng_loc; gl += NW) {
+        const int ra = ga_s[gl], rb = gb_s[gl];
+        double ss = 0.0;
+        for (int rr = ra + lane; rr < rb; rr += 32) {
+          const double v = sgl ? th_soft(uv[rr], (P.var_w ? P.var_w[j0 + rr] : 1.0) * lam * aq, d) : uv[rr];
+          ss += v * v;
+        }
+#pragma unroll
+        for (int o = 16; o >= 1; o >>= 1) ss += __shfl_xor_sync(0xffffffffu, ss, o);
+        const double nu = sqrt(ss);
+        const double cg = gw_s[gl], lw = cg * lam;
+        double f;
+        if (sgl) f = nu > 0.0 ? pos(1.0 - cg * lam * (1.0 - aq) / (d * nu)) : 0.0;   // R#11 (nu = ||v||)
+        else if (fam == OEM_GRP_LASSO) f = nu > 0.0 ? pos(1.0 - lw / nu) : 0.0;
+        else f = nu > 0.0 ? (fam == OEM_GRP_MCP ? th_mcp(nu, lw, gq, d) : th_scad(nu, lw, gq, d)) / nu : 0.0;
+        for (int rr = ra + lane; rr < rb; rr += 32) {
+          const double nb = sgl ? f * th_soft(uv[rr], (P.var_w ? P.var_w[j0 + rr] : 1.0) * lam * aq, d)
+                          : fam == OEM_GRP_LASSO ? uv[rr] / d * f : f * uv[rr];
+          emit(j0 + rr, nb, f > 0.0);
+        }
+        // zero iff z <= tau: z = ||u_g|| against c_g lam, or (sparse group lasso) d ||v|| =
+        // ||S(u_g, w lam tau)|| against c_g lam (1 - tau); both 1-Lipschitz in u_g, which moves by
+        // at most ||G_{g,A}||_F ||db_A|| (rounding: gam_u (||c_g|| + ||G_{g,A}||_F ||b||))
+        if (A.screen) {
+          double f2 = 0.0, c2 = 0.0;
+          for (int rr = ra + lane; rr < rb; rr += 32) {
+            f2 += uv[A.rows + rr];
+            c2 = fma(cu[j0 + rr], cu[j0 + rr], c2);
+          }
+#pragma unroll
+          for (int o = 16; o >= 1; o >>= 1) {
+            f2 += __shfl_xor_sync(0xffffffffu, f2, o);
+            c2 += __shfl_xor_sync(0xffffffffu, c2, o);
+          }
+          if (f == 0.0 && !inA(j0 + ra) && f2 > 0.0) {
+            const double tau = sgl ? cg * lam * (1.0 - aq) : lw;
+            const double z = sgl ? d * nu : nu;
+            slk = fmin(slk, fmax((tau - z - 2.0 * gam_u * sqrt(c2) - 1e-13 * tau) / (sqrt(f2) * (1.0 + 1e-12)), 0.0));
+          }
+        }
+      }
+    }
+    if (A.screen) {
+#pragma unroll
+      for (int o = 16; o >= 1; o >>= 1) {
+        slk = fmin(slk, __shfl_xor_sync(0xffffffffu, slk, o));
+        dsq += __shfl_xor_sync(0xffffffffu, dsq, o);
+        bsq += __shfl_xor_sync(0xffffffffu, bsq, o);
+      }
+      // every warp's minimum into its slot in every CTA (plain stores, read after the barrier;
+      // parity t & 1: the slot is rewritten at t + 2, after the next barrier)
+      if (lane == 0) {
+        const int sl = rank * NW + warp;
+        if (C == 1) {
+          SLs[t & 1][0][sl] = slk; SLs[t & 1][1][sl] = dsq; SLs[t & 1][2][sl] = bsq;
+        } else {
+          for (int rr = 0; rr < C; ++rr) {
+            st_cl_f64(&SLs[t & 1][0][sl], rr, slk);
+            st_cl_f64(&SLs[t & 1][1][sl], rr, dsq);
+            st_cl_f64(&SLs[t & 1][2][sl], rr, bsq);
+          }
+        }
+      }
     }
     bits = __reduce_or_sync(0xffffffffu, bits);
     if (lane == 0 && bits)
@@ -2024,7 +2176,8 @@ __global__ void __launch_bounds__(ACT_THREADS, 1) fit_active_kernel(const PathPa
     // are appended in ascending index order on every CTA and their rows of G loaded.
     bool any = false;
     for (int w = lane; w < A.pw; w += 32) any = any || (nbits[par * A.pw + w] & ~abits[w]) != 0u;
-    if (__any_sync(0xffffffffu, any)) {
+    const bool grew = __any_sync(0xffffffffu, any);
+    if (grew) {
       int added = 0;
       for (int w = 0; w < A.pw; ++w) {
         uint32_t nw = nbits[par * A.pw + w] & ~abits[w];
@@ -2048,9 +2201,7 @@ __global__ void __launch_bounds__(ACT_THREADS, 1) fit_active_kernel(const PathPa
       __syncthreads();
     }
     // ---- bookkeeping (identical in every thread of every CTA of the cluster)
-    const int it = itc + 1;
-    const bool conv = !(f & 1u);   // every |dbeta_j| <= tol (R#17)
-    if (conv || it >= P.maxit) {
+    auto finish_lambda = [&](int it, bool conv) {
       double* out = P.beta_out + (((size_t)unit * nPg + q) * L + lidx) * p;
       for (int rr = tid; rr < nr; rr += ACT_THREADS) out[P.perm[j0 + rr]] = vn[j0 + rr];
       if (rank == 0 && tid == 0) {
@@ -2059,9 +2210,243 @@ __global__ void __launch_bounds__(ACT_THREADS, 1) fit_active_kernel(const PathPa
       }
       ++lidx;
       itc = 0;
+      cfail = 0;
+      cwait = 0;
       if (lidx < L) lam = lam_at(lidx);
-    } else {
+    };
+    {
+      const int it = itc + 1;
+      const bool conv = !(f & 1u);   // every |dbeta_j| <= tol (R#17)
+      if (conv || it >= P.maxit) {
+        finish_lambda(it, conv);
+        continue;
+      }
       itc = it;
+    }
+    if (cwait > 0) --cwait;
+    // (after an activation the next full iteration first measures ||G_{j,A}|| over the new A)
+    if (!A.screen || cwait > 0 || grew || na == 0 || na > NCM) continue;
+    // the cluster's minimum slack and the entry certificate, ||b(t0) - b(t0-1)||_2 against it (same
+    // values, summed in the same order, on every CTA: a uniform decision)
+    double smin = INFINITY, dsum = 0.0, bsum = 0.0;
+    for (int k = lane; k < C * NW; k += 32) {
+      smin = fmin(smin, SLs[t & 1][0][k]);
+      dsum += SLs[t & 1][1][k];
+      bsum += SLs[t & 1][2][k];
+    }
+#pragma unroll
+    for (int o = 16; o >= 1; o >>= 1) {
+      smin = fmin(smin, __shfl_xor_sync(0xffffffffu, smin, o));
+      dsum += __shfl_xor_sync(0xffffffffu, dsum, o);
+      bsum += __shfl_xor_sync(0xffffffffu, bsum, o);
+    }
+    if (!(sqrt(dsum) * (1.0 + 2.0 * gam_u) + 2.0 * gam_u * sqrt(bsum) <= smin * (1.0 - 1e-12))) continue;
+
+    // ======================================================= screened compact phase (CTA 0)
+    // A = act[0..na) (whole groups for group families, contiguous); b(t0) in vn, b(t0-1) in vc.
+    if (rank == 0) {
+      const int nc = na, ncp = (nc + 3) & ~3;
+      // G_AA column-major (gc[k][i] = G[act[i]][act[k]]), zero-padded (kept while A is unchanged);
+      // current b into bcv[0]
+      // Only the entries of new rows / columns are loaded (A only grows), four L2 loads in flight
+      // per thread; padding columns [nc, ncp) are zero (rows >= nc are never used).
+      if (nc != built_na) {
+        const int b0 = built_na < 0 ? 0 : built_na, tot = ncp * nc;
+        for (int e0 = tid; e0 < tot; e0 += 4 * ACT_THREADS) {
+          double v[4];
+          int at[4];
+#pragma unroll
+          for (int u4 = 0; u4 < 4; ++u4) {
+            const int e = e0 + u4 * ACT_THREADS, k = e / nc, i = e - k * nc;
+            at[u4] = (e < tot && (k >= b0 || i >= b0)) ? k * NCM + i : -1;
+            v[u4] = (at[u4] >= 0 && k < nc) ? Gu[(size_t)act[k] * p + act[i]] : 0.0;
+          }
+#pragma unroll
+          for (int u4 = 0; u4 < 4; ++u4)
+            if (at[u4] >= 0) gc[at[u4]] = v[u4];
+        }
+        built_na = nc;
+      }
+      for (int i = tid; i < NCM; i += ACT_THREADS) {
+        bcv[i] = i < nc ? vn[act[i]] : 0.0;
+        bcv[NCM + i] = 0.0;
+        cwv[i] = (i < nc && P.var_w) ? P.var_w[act[i]] : 1.0;
+      }
+      __syncthreads();
+      if (warp == 0) {
+        // one warp, R = 1 or 2 rows per lane (rows lane, lane + 32): no block barrier in the loop.
+        // Divisions by d use the refined reciprocal (within one ulp), the group norms rsqrt: the
+        // compact iterate equals the full one up to rounding.
+        auto run = [&](auto RC) {
+          constexpr int R = decltype(RC)::value;
+          int ii[R], ci[R], cga[R], cgb[R];
+          bool valid[R];
+          double c_i[R], w_i[R], cg_i[R], b[R], bref[R], e[R], bsnap[R];
+          double s_b2 = 0.0, s_e2 = 0.0;
+#pragma unroll
+          for (int h = 0; h < R; ++h) {
+            ii[h] = lane + 32 * h;
+            valid[h] = ii[h] < nc;
+            ci[h] = valid[h] ? act[ii[h]] : 0;
+            c_i[h] = valid[h] ? cu[ci[h]] : 0.0;
+            w_i[h] = cwv[ii[h]];
+            cga[h] = ii[h];
+            cgb[h] = ii[h] + 1;
+            cg_i[h] = 0.0;
+            if (grp && valid[h]) {
+              const int g = P.g_of[ci[h]];
+              cga[h] = ii[h] - (ci[h] - P.g_start[g]);
+              cgb[h] = cga[h] + (P.g_end[g] - P.g_start[g]);
+              cg_i[h] = P.g_w[g];
+            }
+            b[h] = bcv[ii[h]];
+            bref[h] = valid[h] ? vc[ci[h]] : 0.0;
+            e[h] = valid[h] ? fabs(b[h] - bref[h]) : 0.0;
+            bsnap[h] = b[h];
+            s_b2 = fma(bref[h], bref[h], s_b2);
+            s_e2 = fma(e[h], e[h], s_e2);
+          }
+          auto wsum = [&](double v) -> double {
+#pragma unroll
+            for (int o = 16; o >= 1; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+            return v;
+          };
+          // ||b(t0-1)||_2 over A (every other coordinate is 0): the rounding term's scale;
+          // se = sum_i e_i^2 >= ||b(s-1) - b(t0-1)||_2^2 over the iterations so far
+          const double nbref = sqrt(wsum(s_b2));
+          auto certified = [&](double se) -> bool {
+            return sqrt(se) * (1.0 + 2.0 * gam_u) + 2.0 * gam_u * nbref <= smin;
+          };
+          const double se0 = wsum(s_e2);
+          int it = 0, itsnap = 0, oc = 2;
+          const bool sgl = fam == OEM_SGL;
+          const int cfam = fam == OEM_GRP_MCP ? OEM_MCP : fam == OEM_GRP_SCAD ? OEM_SCAD : fam;
+          if (certified(se0)) {
+            for (;;) {
+              const double* bcur = bcv + (it & 1) * NCM;
+              double* bnx = bcv + ((it & 1) ^ 1) * NCM;
+              double a[R][4];
+#pragma unroll
+              for (int h = 0; h < R; ++h) a[h][0] = a[h][1] = a[h][2] = a[h][3] = 0.0;
+              const double* gk = gc + lane;
+#pragma unroll 2
+              for (int k = 0; k < ncp; k += 4, gk += 4 * NCM) {
+                const double2 x0 = *reinterpret_cast<const double2*>(bcur + k);
+                const double2 x1 = *reinterpret_cast<const double2*>(bcur + k + 2);
+#pragma unroll
+                for (int h = 0; h < R; ++h) {
+                  a[h][0] = fma(gk[32 * h], x0.x, a[h][0]);
+                  a[h][1] = fma(gk[NCM + 32 * h], x0.y, a[h][1]);
+                  a[h][2] = fma(gk[2 * NCM + 32 * h], x1.x, a[h][2]);
+                  a[h][3] = fma(gk[3 * NCM + 32 * h], x1.y, a[h][3]);
+                }
+              }
+              double u[R], nb[R];
+#pragma unroll
+              for (int h = 0; h < R; ++h) u[h] = c_i[h] + d * b[h] - ((a[h][0] + a[h][1]) + (a[h][2] + a[h][3]));
+              if (!grp) {
+#pragma unroll
+                for (int h = 0; h < R; ++h) nb[h] = th_coord_r(fam, u[h], w_i[h] * lam, gq, aq, d, rd, rgq);
+              } else {
+#pragma unroll
+                for (int h = 0; h < R; ++h) ucv[ii[h]] = u[h];
+                __syncwarp();
+#pragma unroll
+                for (int h = 0; h < R; ++h) {
+                  double s0 = 0.0, s1 = 0.0;
+                  int rr = cga[h];
+                  for (; rr + 1 < cgb[h]; rr += 2) {
+                    double v0 = ucv[rr], v1 = ucv[rr + 1];
+                    if (sgl) {
+                      v0 = th_coord_r(OEM_LASSO, v0, cwv[rr] * lam * aq, 0.0, 0.0, d, rd, 0.0);
+                      v1 = th_coord_r(OEM_LASSO, v1, cwv[rr + 1] * lam * aq, 0.0, 0.0, d, rd, 0.0);
+                    }
+                    s0 = fma(v0, v0, s0);
+                    s1 = fma(v1, v1, s1);
+                  }
+                  if (rr < cgb[h]) {
+                    double v0 = ucv[rr];
+                    if (sgl) v0 = th_coord_r(OEM_LASSO, v0, cwv[rr] * lam * aq, 0.0, 0.0, d, rd, 0.0);
+                    s0 = fma(v0, v0, s0);
+                  }
+                  const double ss = s0 + s1;
+                  const double rnu = ss > 0.0 ? rsqrt(ss) : 0.0, nu = ss * rnu;
+                  const double lw = cg_i[h] * lam;
+                  double fg;
+                  if (sgl) fg = pos(1.0 - cg_i[h] * lam * (1.0 - aq) * rd * rnu);
+                  else if (fam == OEM_GRP_LASSO) fg = pos(1.0 - lw * rnu);
+                  else fg = th_coord_r(cfam, nu, lw, gq, 0.0, d, rd, rgq) * rnu;
+                  nb[h] = sgl ? fg * th_coord_r(OEM_LASSO, u[h], w_i[h] * lam * aq, 0.0, 0.0, d, rd, 0.0)
+                        : fam == OEM_GRP_LASSO ? u[h] * rd * fg : fg * u[h];
+                }
+              }
+              int fl = 0;
+              double le2 = 0.0;
+#pragma unroll
+              for (int h = 0; h < R; ++h) {
+                if (valid[h]) {
+                  fl |= (!(fabs(nb[h] - b[h]) <= P.tol) ? 1 : 0) | (!isfinite(u[h]) ? 2 : 0);
+                  bnx[ii[h]] = nb[h];
+                  e[h] = fmax(e[h], fabs(nb[h] - bref[h]));
+                  b[h] = nb[h];
+                }
+                le2 = fma(e[h], e[h], le2);
+              }
+              ++it;
+              fl = __reduce_or_sync(0xffffffffu, fl);
+              __syncwarp();
+              if (fl & 2) { oc = 4; break; }
+              const bool conv = !(fl & 1);
+              const bool capped = itc + it >= P.maxit;
+              if (conv || capped || (it % CW) == 0) {
+                const double sek = wsum(le2);
+                if (!certified(sek)) {
+                  oc = 2;
+#pragma unroll
+                  for (int h = 0; h < R; ++h) b[h] = bsnap[h];
+                  it = itsnap;
+                  break;
+                }
+#pragma unroll
+                for (int h = 0; h < R; ++h) bsnap[h] = b[h];
+                itsnap = it;
+                if (conv) { oc = 1; break; }
+                if (capped) { oc = 3; break; }
+              }
+            }
+          }
+#pragma unroll
+          for (int h = 0; h < R; ++h)
+            if (valid[h]) res[ii[h]] = b[h];
+          if (tid == 0) { s_oc[0] = oc; s_oc[1] = it; }
+        };
+        if (nc <= 32) run(std::integral_constant<int, 1>{});
+        else if (nc <= 64) run(std::integral_constant<int, 2>{});
+        else if constexpr (ACT_THREADS == 256) run(std::integral_constant<int, 4>{});   // (register budget)
+      }
+      __syncthreads();
+      const int oc = s_oc[0], its = s_oc[1];
+      // the result into both vector buffers of every CTA, the outcome into every CTA
+      for (int e = tid; e < nc * C; e += ACT_THREADS) {
+        const int i = e % nc, rr = e / nc, k = act[i];
+        st_cl_f64(&vec[k], rr, res[i]);
+        st_cl_f64(&vec[pv + k], rr, res[i]);
+      }
+      if (tid == 0)
+        for (int rr = 1; rr < C; ++rr) { st_cl_s32(&s_oc[0], rr, oc); st_cl_s32(&s_oc[1], rr, its); }
+    }
+    cluster_sync_all();
+    const int oc = s_oc[0], its = s_oc[1];
+    if (oc == 4) {
+      if (tid == 0) atomicExch(&P.flags[0], 1);
+      break;
+    }
+    itc += its;
+    if (oc == 1 || oc == 3) {
+      finish_lambda(itc, oc == 1);
+    } else {
+      ++cfail;
+      cwait = 1 << min(cfail, 3);
     }
   }
   cluster_sync_all();   // no CTA leaves while a peer may still store into its shared memory
@@ -2396,11 +2781,13 @@ static oem_status launch_glob_v(const PathParams& P, const GlobArgs& A, int grid
 
 // ---------------------------------------------------------------- active-set solver: host layout / launch
 struct ActLayout {
-  int C = 0, rows = 0, amax = 0, apitch = 0, pw = 0, nth = 256;
+  int C = 0, rows = 0, amax = 0, apitch = 0, pw = 0, nth = 256, ncmax = 0;
   size_t smem = 0;
   std::vector<int> cuts;
 };
-static bool make_act_layout(int p, const std::vector<int>& gstart, ActLayout& lo, int nth) {
+// ncmax: capacity of the screened compact iterations (G_AA of up to ncmax active coordinates in
+// CTA 0's shared memory), 0 without screening
+static bool make_act_layout(int p, const std::vector<int>& gstart, ActLayout& lo, int nth, int ncmax = 0) {
   const int maxrows = nth / ACT_T;   // 64 or 128
   std::vector<int> cuts{0};
   if (gstart.empty()) {
@@ -2432,8 +2819,9 @@ static bool make_act_layout(int p, const std::vector<int>& gstart, ActLayout& lo
   lo.cuts = cuts;
   lo.pw = (p + 31) / 32;
   const int pv = (p + 1) & ~1;
-  const size_t fixed = (size_t)2 * pv * 8 + (size_t)rows * 8 * 2 + (size_t)rows * 4 * 2 + (size_t)p * 4 +
-                       (size_t)3 * lo.pw * 4 + 64;
+  lo.ncmax = ncmax;
+  const size_t fixed = (size_t)2 * pv * 8 + (size_t)ncmax * ncmax * 8 + (size_t)5 * ncmax * 8 +
+                       (size_t)rows * 8 * 3 + (size_t)rows * 4 * 2 + (size_t)p * 4 + (size_t)3 * lo.pw * 4 + 64;
   const size_t cap = 200 * 1024;
   if (fixed + (size_t)rows * 8 * 8 > cap) return false;
   int apitch = (int)std::min<size_t>((cap - fixed) / ((size_t)rows * 8), (size_t)p + 2);
@@ -2636,19 +3024,29 @@ extern "C" oem_status oem_fit_path(oem_ctx* ctx, const double* G, const double* 
   ClusterLayout cl;
   Layout lo;
   LeanLayout ll;
-  // active-set clusters for wide units (p > 256), whose tall-data paths are sparse; the register-
-  // resident lean clusters below that; OEM_PATH_SOLVER=active / lean / global / cluster / batched
-  // forces a variant (tests, timing studies)
+  // active-set clusters with screened compact iterations (tall-data paths are sparse) for p > 256
+  // and p <= 128; the register-resident lean clusters for 128 < p <= 256, whose 32-row CTAs make
+  // a full iteration cheap (measured, B200: the sparse workload's p = 200 paths, ~6 iterations per
+  // lambda, 1.41 ms lean vs 3.64 ms screened; cfg5's inner solves 39.8 vs 37.6 ms; cfg2, p = 100,
+  // 6.65 ms lean vs 4.70 ms screened). Without screening (OEM_SCREEN=0, timing studies) the
+  // active-set clusters for p > 256 and the lean clusters below. OEM_PATH_SOLVER=active / lean /
+  // global / cluster / batched forces a variant (tests, timing studies)
+  const char* scr = std::getenv("OEM_SCREEN");
+  const int ncmax = (scr && std::string(scr) == "0") ? 0 : (scr && std::string(scr) == "32") ? 32 : 64;
   ActLayout al;
   const std::string fs = force ? std::string(force) : std::string();
   // (128-row CTAs when that gives a smaller cluster: fewer CTAs meet at each barrier)
-  const bool want_act = fs == "active" || (fs.empty() && p > 256);
+  const bool want_act = fs == "active" || (fs.empty() && (p > 256 || (ncmax > 0 && p <= 128)));
   const std::vector<int> gs_act = any_grp ? gstart : std::vector<int>();
   ActLayout al128;
   const char* ath = std::getenv("OEM_ACT_THREADS");   // developer override (timing studies): 256 / 512
   const int force_th = ath ? std::atoi(ath) : 0;
-  const bool act256 = want_act && force_th != 512 && make_act_layout(p, gs_act, al, 256);
-  const bool act512 = want_act && (p > 512 || force_th == 512) && force_th != 256 && make_act_layout(p, gs_act, al128, 512);
+  // (256-thread CTAs hold up to 128 compact rows, 4 per lane, when p <= 256)
+  const int ncmax256 = (ncmax == 64 && p <= 256 && p > 64) ? 128 : ncmax;
+  const bool act256 = want_act && force_th != 512 &&
+                      (make_act_layout(p, gs_act, al, 256, ncmax256) || make_act_layout(p, gs_act, al, 256, ncmax));
+  const bool act512 =
+      want_act && (p > 512 || force_th == 512) && force_th != 256 && make_act_layout(p, gs_act, al128, 512, ncmax);
   if (act512 && (!act256 || al128.C < al.C)) al = al128;
   const bool use_act = act256 || act512;
   const bool use_lean = !use_act && !(fs == "global" || fs == "cluster") &&
@@ -2877,6 +3275,7 @@ extern "C" oem_status oem_fit_path(oem_ctx* ctx, const double* G, const double* 
     P.ps = 0; P.T = 0; P.smem_rows = 0;
     ActArgs A;
     A.C = al.C; A.amax = al.amax; A.apitch = al.apitch; A.rows = al.rows; A.pw = al.pw;
+    A.screen = al.ncmax > 0 ? 1 : 0; A.ncmax = al.ncmax;
     PhaseTimer tm(ctx, PH_PATH, st);
     ++ctx->launches;
     oem_status s = al.nth == 512 ? launch_active<512>(P, A, nU * nP, al.smem, st)

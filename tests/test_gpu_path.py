@@ -467,3 +467,31 @@ def test_active_set_solver(ctx, p, solver, monkeypatch):
         B, it, cv = orc.oem_path(Go / nn, co / nn, float(fit.d[u]), "lasso", lam2,
                                  beta_init=init[u, 0].cpu().numpy())
         assert np.max(np.abs(fit2.beta[u, 0].cpu().numpy() - B)) <= TOL_BETA
+
+
+@pytest.mark.parametrize("screen", ["0", "1", "32"])  # off, default capacity, 32 compact rows
+def test_screened_active_cfg2_full_size(ctx, screen, monkeypatch):
+    """The active-set solver on cfg2 at full size (n = 1e6, p = 100; lasso, MCP, SCAD paths of 100
+    lambda), with and without the screened compact iterations (OEM_SCREEN): every unit against the
+    oracle's path solve on the same Gram at the GPU's d."""
+    from paper_1801_09661_b200 import oem_fit_path, oem_gram
+    monkeypatch.setenv("OEM_PATH_SOLVER", "active")
+    monkeypatch.setenv("OEM_SCREEN", screen)
+    cfg = CONFIGS["cfg2"]
+    bt = dg.beta(cfg.spec)
+    Xd, yd = device_rows(cfg.spec, bt)
+    G, c, yy, n = oem_gram(ctx, Xd, yd)
+    del Xd, yd
+    fit = oem_fit_path(ctx, G, c, [n], cfg.penalties, nlambda=cfg.nlambda)
+    Gh, ch = G.cpu().numpy(), c.cpu().numpy()
+    d = float(fit.d[0])
+    errs = []
+    for q, (fam, gamma, alpha) in enumerate(cfg.penalties):
+        lg = fit.lam[0, q].cpu().numpy()
+        B, it, cv = orc.oem_path(Gh / n, ch / n, d, fam, lg, gamma, alpha)
+        Bg = fit.beta[0, q].cpu().numpy()
+        e = np.max(np.abs(Bg - B), axis=1)
+        errs.append((fam, float(e.max()), int(np.argmax(e)), int(fit.iters[0, q].sum()), int(it.sum())))
+    for fam, e, l, itg, ito in errs:
+        assert e <= TOL_BETA, errs
+        assert abs(itg - ito) <= max(2, 0.02 * ito), errs
