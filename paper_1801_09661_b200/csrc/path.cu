@@ -1859,8 +1859,9 @@ __global__ void __launch_bounds__(PT, 1) fit_cluster_kernel(const PathParams P, 
 // iteration measures those norms over A and every CTA forms the same minimum s_min of
 // (tau - z - rounding) / ||G_{j,A}||; while D (+ a rounding term) <= s_min, the iteration restricted
 // to the rows and columns of A equals the full iteration (every inactive threshold returns 0), so
-// CTA 0 runs those iterations alone, in one warp (one or two rows per lane) with G_AA in shared
-// memory: no cluster barrier, no exchange. D is bounded by per-coordinate running maxima, checked
+// CTA 0 runs those iterations alone, in four warps (the matvec split by columns, one named barrier
+// per iteration, two for group families) with G_AA in shared memory: no cluster barrier, no
+// exchange. D is bounded by per-coordinate running maxima, checked
 // every CW iterations and at the exit; a failed check rolls back to the last certified iterate and
 // the cluster resumes full iterations (every lambda starts with one, which re-derives the slacks).
 // For group families A holds whole groups.
@@ -1893,6 +1894,8 @@ __global__ void __launch_bounds__(ACT_THREADS, 1) fit_active_kernel(const PathPa
   __shared__ int s_na;
   __shared__ double s_lmax;
   __shared__ int s_oc[2];                // compact phase: outcome, iterations
+  __shared__ int cfl4[2][4];             // compact warps' flag words (iteration parity, warp)
+  __shared__ double csum4[2][4];         // compact warps' partial sums (slot, warp)
   const int p = P.p, nPg = P.nP, L = P.L, C = A.C;
   const int clu = blockIdx.x / C;
   const int unit = clu / nPg, q = clu % nPg;   // one penalty per cluster
@@ -1904,7 +1907,7 @@ __global__ void __launch_bounds__(ACT_THREADS, 1) fit_active_kernel(const PathPa
   const double* cu = P.cn + (size_t)unit * p;
   const int pv = (p + 1) & ~1;
   const int NCM = A.ncmax;
-  // shared memory: vec [2][pv] | gc [NCM][NCM] | bcv [2][NCM] | res, ucv, cwv [NCM] | ga [rows][apitch] |
+  // shared memory: vec [2][pv] | gc [NCM][NCM] | bcv [2][NCM] | res, ucv, cwv [NCM] | part [4][NCM] | ga [rows][apitch] |
   //                uv [2][rows] | gw, ga_s, gb_s [rows] | act [p] | abits, nbits [2][pw]
   double* vec = sm;
   double* gc = vec + 2 * (size_t)pv;
@@ -1912,7 +1915,8 @@ __global__ void __launch_bounds__(ACT_THREADS, 1) fit_active_kernel(const PathPa
   double* res = bcv + 2 * (size_t)NCM;
   double* ucv = res + NCM;
   double* cwv = ucv + NCM;
-  double* ga = cwv + NCM;
+  double* part = cwv + NCM;   // [4][NCM] compact matvec partial sums
+  double* ga = part + 4 * (size_t)NCM;
   double* uv = ga + (size_t)A.rows * A.apitch;   // [2][rows]: u, then ||G_{j,A}||^2 (screening)
   double* gw_s = uv + 2 * A.rows;
   int* ga_s = reinterpret_cast<int*>(gw_s + A.rows);
@@ -2020,7 +2024,7 @@ __global__ void __launch_bounds__(ACT_THREADS, 1) fit_active_kernel(const PathPa
   const double rgq = (fam == OEM_MCP || fam == OEM_GRP_MCP) ? 1.0 / (gq * d - 1.0)
                    : (fam == OEM_SCAD || fam == OEM_GRP_SCAD) ? 1.0 / ((gq - 1.0) * d - 1.0) : 0.0;
   int cfail = 0, cwait = 0;      // failed compact phases at this lambda; full iterations before the next
-  int built_na = -1;             // CTA 0: size of the active set whose G_AA is in gc
+  int built_na = -1, built_pitch = 0;   // CTA 0: size of the active set whose G_AA is in gc, its pitch
   cluster_sync_all();  // every CTA initialised before the first remote store
   auto inA = [&](int k) -> bool { return (abits[k >> 5] >> (k & 31)) & 1u; };
 
@@ -2245,11 +2249,13 @@ __global__ void __launch_bounds__(ACT_THREADS, 1) fit_active_kernel(const PathPa
     // ======================================================= screened compact phase (CTA 0)
     // A = act[0..na) (whole groups for group families, contiguous); b(t0) in vn, b(t0-1) in vc.
     if (rank == 0) {
-      const int nc = na, ncp = (nc + 3) & ~3;
-      // G_AA column-major (gc[k][i] = G[act[i]][act[k]]), zero-padded (kept while A is unchanged);
-      // current b into bcv[0]
+      const int nc = na, ncp = (nc + 7) & ~7;
+      // G_AA column-major with pitch 32 R (R = rows per lane of the compact warp: a compile-time
+      // pitch in the loop), gc[k][i] = G[act[i]][act[k]], zero-padded, kept while A is unchanged.
       // Only the entries of new rows / columns are loaded (A only grows), four L2 loads in flight
       // per thread; padding columns [nc, ncp) are zero (rows >= nc are never used).
+      const int pitch = nc <= 32 ? 32 : nc <= 64 ? 64 : 128;
+      if (pitch != built_pitch) { built_na = -1; built_pitch = pitch; }
       if (nc != built_na) {
         const int b0 = built_na < 0 ? 0 : built_na, tot = ncp * nc;
         for (int e0 = tid; e0 < tot; e0 += 4 * ACT_THREADS) {
@@ -2258,7 +2264,7 @@ __global__ void __launch_bounds__(ACT_THREADS, 1) fit_active_kernel(const PathPa
 #pragma unroll
           for (int u4 = 0; u4 < 4; ++u4) {
             const int e = e0 + u4 * ACT_THREADS, k = e / nc, i = e - k * nc;
-            at[u4] = (e < tot && (k >= b0 || i >= b0)) ? k * NCM + i : -1;
+            at[u4] = (e < tot && (k >= b0 || i >= b0)) ? k * pitch + i : -1;
             v[u4] = (at[u4] >= 0 && k < nc) ? Gu[(size_t)act[k] * p + act[i]] : 0.0;
           }
 #pragma unroll
@@ -2273,151 +2279,141 @@ __global__ void __launch_bounds__(ACT_THREADS, 1) fit_active_kernel(const PathPa
         cwv[i] = (i < nc && P.var_w) ? P.var_w[act[i]] : 1.0;
       }
       __syncthreads();
-      if (warp == 0) {
-        // one warp, R = 1 or 2 rows per lane (rows lane, lane + 32): no block barrier in the loop.
-        // Divisions by d use the refined reciprocal (within one ulp), the group norms rsqrt: the
-        // compact iterate equals the full one up to rounding.
+      if (warp < 4) {
+        // Four warps (one per SM sub-partition, named barrier 1): in the matvec warp w sums the
+        // columns [w ncp/4, (w+1) ncp/4) for every row (R rows per lane: lane + 32 h); the partial
+        // sums meet in shared memory and are added in a fixed order; warp w then thresholds row
+        // lane + 32 w. Divisions by constants use the refined reciprocal (within one ulp), group
+        // norms rsqrt: the compact iterate equals the full one up to rounding.
         auto run = [&](auto RC) {
-          constexpr int R = decltype(RC)::value;
-          int ii[R], ci[R], cga[R], cgb[R];
-          bool valid[R];
-          double c_i[R], w_i[R], cg_i[R], b[R], bref[R], e[R], bsnap[R];
-          double s_b2 = 0.0, s_e2 = 0.0;
-#pragma unroll
-          for (int h = 0; h < R; ++h) {
-            ii[h] = lane + 32 * h;
-            valid[h] = ii[h] < nc;
-            ci[h] = valid[h] ? act[ii[h]] : 0;
-            c_i[h] = valid[h] ? cu[ci[h]] : 0.0;
-            w_i[h] = cwv[ii[h]];
-            cga[h] = ii[h];
-            cgb[h] = ii[h] + 1;
-            cg_i[h] = 0.0;
-            if (grp && valid[h]) {
-              const int g = P.g_of[ci[h]];
-              cga[h] = ii[h] - (ci[h] - P.g_start[g]);
-              cgb[h] = cga[h] + (P.g_end[g] - P.g_start[g]);
-              cg_i[h] = P.g_w[g];
-            }
-            b[h] = bcv[ii[h]];
-            bref[h] = valid[h] ? vc[ci[h]] : 0.0;
-            e[h] = valid[h] ? fabs(b[h] - bref[h]) : 0.0;
-            bsnap[h] = b[h];
-            s_b2 = fma(bref[h], bref[h], s_b2);
-            s_e2 = fma(e[h], e[h], s_e2);
+          constexpr int R = decltype(RC)::value;   // 32-row blocks of the matvec (nc <= 32 R)
+          constexpr int PR = 32 * R;               // gc pitch
+          auto csync = []() { asm volatile("bar.sync 1, 128;" ::: "memory"); };
+          const int i = lane + 32 * warp;          // this lane's row in the threshold step
+          const bool valid = i < nc;
+          const int ci = valid ? act[i] : 0;
+          const double c_i = valid ? cu[ci] : 0.0, w_i = valid ? cwv[i] : 1.0;
+          const double enden = d + w_i * lam * (1.0 - aq), rden = 1.0 / enden;
+          int cga = i, cgb = i + 1;
+          double cg_i = 0.0;
+          if (grp && valid) {
+            const int g = P.g_of[ci];
+            cga = i - (ci - P.g_start[g]);
+            cgb = cga + (P.g_end[g] - P.g_start[g]);
+            cg_i = P.g_w[g];
           }
-          auto wsum = [&](double v) -> double {
+          double b = valid ? bcv[i] : 0.0;
+          const double bref = valid ? vc[ci] : 0.0;
+          double e = valid ? fabs(b - bref) : 0.0, bsnap = b;
+          // sum over the four warps (warp sums, then a fixed order); slot alternates
+          auto xsum = [&](double v, int slot) -> double {
 #pragma unroll
             for (int o = 16; o >= 1; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
-            return v;
+            if (lane == 0) csum4[slot][warp] = v;
+            csync();
+            return (csum4[slot][0] + csum4[slot][1]) + (csum4[slot][2] + csum4[slot][3]);
           };
           // ||b(t0-1)||_2 over A (every other coordinate is 0): the rounding term's scale;
           // se = sum_i e_i^2 >= ||b(s-1) - b(t0-1)||_2^2 over the iterations so far
-          const double nbref = sqrt(wsum(s_b2));
+          const double nbref = sqrt(xsum(bref * bref, 0));
           auto certified = [&](double se) -> bool {
             return sqrt(se) * (1.0 + 2.0 * gam_u) + 2.0 * gam_u * nbref <= smin;
           };
-          const double se0 = wsum(s_e2);
-          int it = 0, itsnap = 0, oc = 2;
+          const double se0 = xsum(e * e, 1);
+          int it = 0, itsnap = 0, oc = 2, slot = 0;
           const bool sgl = fam == OEM_SGL;
           const int cfam = fam == OEM_GRP_MCP ? OEM_MCP : fam == OEM_GRP_SCAD ? OEM_SCAD : fam;
+          const int ncq = ncp >> 2, k0 = warp * ncq;
           if (certified(se0)) {
             for (;;) {
               const double* bcur = bcv + (it & 1) * NCM;
               double* bnx = bcv + ((it & 1) ^ 1) * NCM;
-              double a[R][4];
+              // ---- matvec partials over this warp's columns
+              double a[R][2];
 #pragma unroll
-              for (int h = 0; h < R; ++h) a[h][0] = a[h][1] = a[h][2] = a[h][3] = 0.0;
-              const double* gk = gc + lane;
-#pragma unroll 2
-              for (int k = 0; k < ncp; k += 4, gk += 4 * NCM) {
-                const double2 x0 = *reinterpret_cast<const double2*>(bcur + k);
-                const double2 x1 = *reinterpret_cast<const double2*>(bcur + k + 2);
+              for (int h = 0; h < R; ++h) a[h][0] = a[h][1] = 0.0;
+              const double* gk = gc + (size_t)k0 * PR + lane;
+              const double* xk = bcur + k0;
+#pragma unroll 4
+              for (int k = 0; k < ncq; k += 2, gk += 2 * PR, xk += 2) {
+                const double2 x0 = *reinterpret_cast<const double2*>(xk);
 #pragma unroll
                 for (int h = 0; h < R; ++h) {
                   a[h][0] = fma(gk[32 * h], x0.x, a[h][0]);
-                  a[h][1] = fma(gk[NCM + 32 * h], x0.y, a[h][1]);
-                  a[h][2] = fma(gk[2 * NCM + 32 * h], x1.x, a[h][2]);
-                  a[h][3] = fma(gk[3 * NCM + 32 * h], x1.y, a[h][3]);
+                  a[h][1] = fma(gk[PR + 32 * h], x0.y, a[h][1]);
                 }
               }
-              double u[R], nb[R];
 #pragma unroll
-              for (int h = 0; h < R; ++h) u[h] = c_i[h] + d * b[h] - ((a[h][0] + a[h][1]) + (a[h][2] + a[h][3]));
+              for (int h = 0; h < R; ++h) part[warp * NCM + lane + 32 * h] = a[h][0] + a[h][1];
+              csync();
+              // ---- E-step and M-step of row i
+              const int iu = valid ? i : 0;
+              const double u = c_i + d * b - ((part[iu] + part[NCM + iu]) + (part[2 * NCM + iu] + part[3 * NCM + iu]));
+              double nb = 0.0;
               if (!grp) {
-#pragma unroll
-                for (int h = 0; h < R; ++h) nb[h] = th_coord_r(fam, u[h], w_i[h] * lam, gq, aq, d, rd, rgq);
-              } else {
-#pragma unroll
-                for (int h = 0; h < R; ++h) ucv[ii[h]] = u[h];
-                __syncwarp();
-#pragma unroll
-                for (int h = 0; h < R; ++h) {
-                  double s0 = 0.0, s1 = 0.0;
-                  int rr = cga[h];
-                  for (; rr + 1 < cgb[h]; rr += 2) {
-                    double v0 = ucv[rr], v1 = ucv[rr + 1];
-                    if (sgl) {
-                      v0 = th_coord_r(OEM_LASSO, v0, cwv[rr] * lam * aq, 0.0, 0.0, d, rd, 0.0);
-                      v1 = th_coord_r(OEM_LASSO, v1, cwv[rr + 1] * lam * aq, 0.0, 0.0, d, rd, 0.0);
-                    }
-                    s0 = fma(v0, v0, s0);
-                    s1 = fma(v1, v1, s1);
-                  }
-                  if (rr < cgb[h]) {
-                    double v0 = ucv[rr];
-                    if (sgl) v0 = th_coord_r(OEM_LASSO, v0, cwv[rr] * lam * aq, 0.0, 0.0, d, rd, 0.0);
-                    s0 = fma(v0, v0, s0);
-                  }
-                  const double ss = s0 + s1;
-                  const double rnu = ss > 0.0 ? rsqrt(ss) : 0.0, nu = ss * rnu;
-                  const double lw = cg_i[h] * lam;
-                  double fg;
-                  if (sgl) fg = pos(1.0 - cg_i[h] * lam * (1.0 - aq) * rd * rnu);
-                  else if (fam == OEM_GRP_LASSO) fg = pos(1.0 - lw * rnu);
-                  else fg = th_coord_r(cfam, nu, lw, gq, 0.0, d, rd, rgq) * rnu;
-                  nb[h] = sgl ? fg * th_coord_r(OEM_LASSO, u[h], w_i[h] * lam * aq, 0.0, 0.0, d, rd, 0.0)
-                        : fam == OEM_GRP_LASSO ? u[h] * rd * fg : fg * u[h];
+                if (fam == OEM_ENET) {   // eq (net): the divisor d + w lam (1 - alpha) is fixed in the phase
+                  const double t = fabs(u) - w_i * lam * aq;
+                  nb = t > 0.0 ? sgn(u) * div_r(t, enden, rden) : 0.0;
+                } else {
+                  nb = th_coord_r(fam, u, w_i * lam, gq, aq, d, rd, rgq);
                 }
+              } else {
+                // the row's square (of u, or of its soft-threshold for the sparse group lasso),
+                // then every row sums its group's squares
+                const double vs = sgl ? th_coord_r(OEM_LASSO, u, w_i * lam * aq, 0.0, 0.0, d, rd, 0.0) : u;
+                if (valid) ucv[i] = vs * vs;
+                csync();
+                double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;
+                int rr = cga;
+                if (valid) {
+                  for (; rr + 3 < cgb; rr += 4) {
+                    s0 += ucv[rr];
+                    s1 += ucv[rr + 1];
+                    s2 += ucv[rr + 2];
+                    s3 += ucv[rr + 3];
+                  }
+                  for (; rr < cgb; ++rr) s0 += ucv[rr];
+                }
+                const double ss = (s0 + s1) + (s2 + s3);
+                const double rnu = ss > 0.0 ? rsqrt(ss) : 0.0, nu = ss * rnu;
+                const double lw = cg_i * lam;
+                double fg;
+                if (sgl) fg = pos(1.0 - cg_i * lam * (1.0 - aq) * rd * rnu);
+                else if (fam == OEM_GRP_LASSO) fg = pos(1.0 - lw * rnu);
+                else fg = th_coord_r(cfam, nu, lw, gq, 0.0, d, rd, rgq) * rnu;
+                nb = sgl ? fg * vs : fam == OEM_GRP_LASSO ? u * rd * fg : fg * u;
               }
               int fl = 0;
-              double le2 = 0.0;
-#pragma unroll
-              for (int h = 0; h < R; ++h) {
-                if (valid[h]) {
-                  fl |= (!(fabs(nb[h] - b[h]) <= P.tol) ? 1 : 0) | (!isfinite(u[h]) ? 2 : 0);
-                  bnx[ii[h]] = nb[h];
-                  e[h] = fmax(e[h], fabs(nb[h] - bref[h]));
-                  b[h] = nb[h];
-                }
-                le2 = fma(e[h], e[h], le2);
+              if (valid) {
+                fl = (!(fabs(nb - b) <= P.tol) ? 1 : 0) | (!isfinite(u) ? 2 : 0);
+                bnx[i] = nb;
+                e = fmax(e, fabs(nb - bref));
+                b = nb;
               }
               ++it;
               fl = __reduce_or_sync(0xffffffffu, fl);
-              __syncwarp();
+              if (lane == 0) cfl4[it & 1][warp] = fl;
+              csync();
+              fl = (cfl4[it & 1][0] | cfl4[it & 1][1]) | (cfl4[it & 1][2] | cfl4[it & 1][3]);
               if (fl & 2) { oc = 4; break; }
               const bool conv = !(fl & 1);
               const bool capped = itc + it >= P.maxit;
               if (conv || capped || (it % CW) == 0) {
-                const double sek = wsum(le2);
-                if (!certified(sek)) {
+                if (!certified(xsum(e * e, slot))) {
                   oc = 2;
-#pragma unroll
-                  for (int h = 0; h < R; ++h) b[h] = bsnap[h];
+                  b = bsnap;
                   it = itsnap;
                   break;
                 }
-#pragma unroll
-                for (int h = 0; h < R; ++h) bsnap[h] = b[h];
+                slot ^= 1;
+                bsnap = b;
                 itsnap = it;
                 if (conv) { oc = 1; break; }
                 if (capped) { oc = 3; break; }
               }
             }
           }
-#pragma unroll
-          for (int h = 0; h < R; ++h)
-            if (valid[h]) res[ii[h]] = b[h];
+          if (valid) res[i] = b;
           if (tid == 0) { s_oc[0] = oc; s_oc[1] = it; }
         };
         if (nc <= 32) run(std::integral_constant<int, 1>{});
@@ -2820,7 +2816,7 @@ static bool make_act_layout(int p, const std::vector<int>& gstart, ActLayout& lo
   lo.pw = (p + 31) / 32;
   const int pv = (p + 1) & ~1;
   lo.ncmax = ncmax;
-  const size_t fixed = (size_t)2 * pv * 8 + (size_t)ncmax * ncmax * 8 + (size_t)5 * ncmax * 8 +
+  const size_t fixed = (size_t)2 * pv * 8 + (size_t)ncmax * ncmax * 8 + (size_t)9 * ncmax * 8 +
                        (size_t)rows * 8 * 3 + (size_t)rows * 4 * 2 + (size_t)p * 4 + (size_t)3 * lo.pw * 4 + 64;
   const size_t cap = 200 * 1024;
   if (fixed + (size_t)rows * 8 * 8 > cap) return false;
