@@ -30,6 +30,7 @@ def main():
     ap.add_argument("--solver", default="", help="OEM_PATH_SOLVER for both modes")
     ap.add_argument("--reps", type=int, default=3)
     ap.add_argument("--modes", default="0,1", help="OEM_SCREEN values to compare")
+    ap.add_argument("--pen", type=int, default=-1, help="fit only penalty #pen of the workload")
     a = ap.parse_args()
     cfg = CONFIGS[a.cfg]
     if a.n:
@@ -57,7 +58,8 @@ def main():
         ms = []
         for _ in range(a.reps + 1):
             stats(ctx, reset=True)
-            fit = oem_fit_path(ctx, G, c, cnt, cfg.penalties, **kw)
+            pens = cfg.penalties if a.pen < 0 else [cfg.penalties[a.pen]]
+            fit = oem_fit_path(ctx, G, c, cnt, pens, **kw)
             torch.cuda.synchronize()
             ms.append(stats(ctx)["path_ms"])
         it = int(fit.iters.sum(-1).max())
