@@ -2139,7 +2139,9 @@ __global__ void __launch_bounds__(ACT_THREADS, 1) fit_active_kernel(const PathPa
           if (f == 0.0 && !inA(j0 + ra) && f2 > 0.0) {
             const double tau = sgl ? cg * lam * (1.0 - aq) : lw;
             const double z = sgl ? d * nu : nu;
-            slk = fmin(slk, fmax((tau - z - 2.0 * gam_u * sqrt(c2) - 1e-13 * tau) / (sqrt(f2) * (1.0 + 1e-12)), 0.0));
+            // (the norm's own rounding: (n_g + 8) ulps relative, and 1e-13 for the M-step's test)
+            const double rel = 1e-13 + 4.0 * 1.1102230246251565e-16 * (rb - ra + 8);
+            slk = fmin(slk, fmax((tau - z - 2.0 * gam_u * sqrt(c2) - rel * tau) / (sqrt(f2) * (1.0 + 1e-12)), 0.0));
           }
         }
       }
