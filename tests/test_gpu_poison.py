@@ -1,7 +1,8 @@
 """Scratch-poisoning run (OEM_POISON=1: every workspace the library hands a kernel is first filled
-with a NaN pattern): the cfg1 fit, a fold-mode CV fit, the logistic paths, the active-set solver,
-the d rule, the two-panel weighted pass and the sparse pass must still match the oracle, i.e. no
-kernel reads scratch it did not write in the same call."""
+with a NaN pattern): the cfg1 fit, a fold-mode CV fit, the logistic paths, the active-set solver
+(its screened compact iterations for every family), the d rule, the two-panel weighted pass and
+the sparse pass must still match the oracle, i.e. no kernel reads scratch it did not write in the
+same call."""
 import os
 import subprocess
 import sys
@@ -21,6 +22,7 @@ def test_poisoned_workspace_subprocess():
            os.path.join(ROOT, "tests", "test_gpu_cv.py"),
            os.path.join(ROOT, "tests", "test_gpu_logistic.py"),
            os.path.join(ROOT, "tests", "test_gpu_path.py") + "::test_active_set_solver",
+           os.path.join(ROOT, "tests", "test_gpu_path.py") + "::test_screened_every_family",
            os.path.join(ROOT, "tests", "test_gpu_gram.py") + "::test_weighted_two_panel_parity",
            os.path.join(ROOT, "tests", "test_gpu_sparse.py") + "::test_sparse_gram_parity",
            "-k", "not full_size"]
