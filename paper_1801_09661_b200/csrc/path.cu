@@ -2287,8 +2287,11 @@ __global__ void __launch_bounds__(ACT_THREADS, 1) fit_active_kernel(const PathPa
         // sums meet in shared memory and are added in a fixed order; warp w then thresholds row
         // lane + 32 w. Divisions by constants use the refined reciprocal (within one ulp), group
         // norms rsqrt: the compact iterate equals the full one up to rounding.
-        auto run = [&](auto RC) {
+        // FC: the coordinate family as a compile-time constant (no per-iteration dispatch), or 4 for
+        // the group families (dispatched on `fam` inside)
+        auto run = [&](auto RC, auto FC) {
           constexpr int R = decltype(RC)::value;   // 32-row blocks of the matvec (nc <= 32 R)
+          constexpr int FAMC = decltype(FC)::value;
           constexpr int PR = 32 * R;               // gc pitch
           auto csync = []() { asm volatile("bar.sync 1, 128;" ::: "memory"); };
           const int i = lane + 32 * warp;          // this lane's row in the threshold step
@@ -2352,13 +2355,11 @@ __global__ void __launch_bounds__(ACT_THREADS, 1) fit_active_kernel(const PathPa
               const int iu = valid ? i : 0;
               const double u = c_i + d * b - ((part[iu] + part[NCM + iu]) + (part[2 * NCM + iu] + part[3 * NCM + iu]));
               double nb = 0.0;
-              if (!grp) {
-                if (fam == OEM_ENET) {   // eq (net): the divisor d + w lam (1 - alpha) is fixed in the phase
-                  const double t = fabs(u) - w_i * lam * aq;
-                  nb = t > 0.0 ? sgn(u) * div_r(t, enden, rden) : 0.0;
-                } else {
-                  nb = th_coord_r(fam, u, w_i * lam, gq, aq, d, rd, rgq);
-                }
+              if constexpr (FAMC == OEM_ENET) {   // eq (net): the divisor d + w lam (1 - alpha) is fixed in the phase
+                const double t = fabs(u) - w_i * lam * aq;
+                nb = t > 0.0 ? sgn(u) * div_r(t, enden, rden) : 0.0;
+              } else if constexpr (FAMC < 4) {
+                nb = th_coord_r(FAMC, u, w_i * lam, gq, aq, d, rd, rgq);
               } else {
                 // the row's square (of u, or of its soft-threshold for the sparse group lasso),
                 // then every row sums its group's squares
@@ -2418,9 +2419,16 @@ __global__ void __launch_bounds__(ACT_THREADS, 1) fit_active_kernel(const PathPa
           if (valid) res[i] = b;
           if (tid == 0) { s_oc[0] = oc; s_oc[1] = it; }
         };
-        if (nc <= 32) run(std::integral_constant<int, 1>{});
-        else if (nc <= 64) run(std::integral_constant<int, 2>{});
-        else if constexpr (ACT_THREADS == 256) run(std::integral_constant<int, 4>{});   // (register budget)
+        auto go = [&](auto RC) {
+          if (grp) run(RC, std::integral_constant<int, 4>{});
+          else if (fam == OEM_LASSO) run(RC, std::integral_constant<int, OEM_LASSO>{});
+          else if (fam == OEM_ENET) run(RC, std::integral_constant<int, OEM_ENET>{});
+          else if (fam == OEM_MCP) run(RC, std::integral_constant<int, OEM_MCP>{});
+          else run(RC, std::integral_constant<int, OEM_SCAD>{});
+        };
+        if (nc <= 32) go(std::integral_constant<int, 1>{});
+        else if (nc <= 64) go(std::integral_constant<int, 2>{});
+        else if constexpr (ACT_THREADS == 256) go(std::integral_constant<int, 4>{});   // (register budget)
       }
       __syncthreads();
       const int oc = s_oc[0], its = s_oc[1];
