@@ -162,6 +162,10 @@ typedef struct {
  * lambda_out[nG'][nP][L], iters_out[nG'][nP][L] (int64), converged_out[nG'][nP][L] (uint8),
  * d_out[nG'] (double). Units run independently; a unit's lambda advances only when that unit
  * converges or hits maxit. Synchronises `stream` (reads the non-finite flag).
+ * The iterates are the paper's; for p > 256 and p <= 128 the solver
+ * iterates only the active block while a certificate proves every other coordinate's threshold
+ * returns zero (developer overrides, read per call: OEM_SCREEN=0 turns that off,
+ * OEM_PATH_SOLVER=active|lean|global|cluster|batched forces a solver layout).
  * Errors: OEM_ERR_INVALID_ARG (MCP gamma*d <= 1, SCAD (gamma-1)*d <= 1, alpha outside [0,1],
  * groups missing for group families, L < 1, bad ratio), OEM_ERR_EMPTY_FOLD (count 0),
  * OEM_ERR_NONFINITE, OEM_ERR_UNSUPPORTED (p > 16383), OEM_ERR_CUDA. */
